@@ -1,0 +1,169 @@
+"""Host-side conjugation tables: 1q axis maps, composed U_k blocks, CX tables.
+
+Stays on the host by design: the tables are O(K*n*9)
+doubles, and building them with the *same* arithmetic as the reference
+(``math.cos/sin`` of the full angle, numpy 3x3 ``@`` in gate order,
+``lut.py:41-52,67-74``) keeps every weight the device multiplies bit-identical
+to the reference's, so that only the merge's summation order can differ.
+
+The second half packs those tables into what the kernels consume:
+  * ``perm_word``   -- a 1q signed axis permutation as a 9-bit field,
+  * ``branch_table`` -- per (qubit, input axis): how many output axes, which,
+    and their weights, zero entries removed exactly like the reference does
+    (``stabilizer.py:210``, ``engine.py:197-202``).
+"""
+
+from __future__ import annotations
+
+import math
+
+import numpy as np
+
+# new_w = M @ w on (X, Y, Z) weight vectors (reference lut.py:29-38).
+_H = ((0.0, 0.0, 1.0), (0.0, -1.0, 0.0), (1.0, 0.0, 0.0))      # X<->Z, Y->-Y
+_S = ((0.0, -1.0, 0.0), (1.0, 0.0, 0.0), (0.0, 0.0, 1.0))      # X->Y, Y->-X
+_X = ((1.0, 0.0, 0.0), (0.0, -1.0, 0.0), (0.0, 0.0, -1.0))     # Y->-Y, Z->-Z
+_SX = ((1.0, 0.0, 0.0), (0.0, 0.0, -1.0), (0.0, 1.0, 0.0))     # Y->Z, Z->-Y
+_FIXED = {"H": _H, "S": _S, "X": _X, "SX": _SX}
+
+
+def axis_map(gate: str, theta: float = 0.0) -> np.ndarray:
+    """3x3 action of one gate on (X, Y, Z) weights; R_a(theta) = exp(-i theta a / 2)."""
+    fixed = _FIXED.get(gate)
+    if fixed is not None:
+        return np.array(fixed)
+    c, s = math.cos(theta), math.sin(theta)
+    if gate == "RX":
+        rows = ((1.0, 0.0, 0.0), (0.0, c, -s), (0.0, s, c))
+    elif gate == "RY":
+        rows = ((c, 0.0, s), (0.0, 1.0, 0.0), (-s, 0.0, c))
+    elif gate == "RZ":
+        rows = ((c, -s, 0.0), (s, c, 0.0), (0.0, 0.0, 1.0))
+    else:
+        raise ValueError(f"no single-qubit conjugation rule for gate {gate!r}")
+    return np.array(rows)
+
+
+def compose_block(gates) -> np.ndarray:
+    """One U_{k,j} block: row p = image of axis p after all gates in circuit order.
+
+    Same left-multiplication and final transpose as reference ``lut.py:67-74``;
+    numpy's ``@`` is used on purpose so rounding matches the reference's.
+    """
+    acc = np.eye(3)
+    for inst in gates:
+        acc = axis_map(inst.gate, inst.theta) @ acc
+    return np.ascontiguousarray(acc.T)
+
+
+def create_lut_1q(partition, workers=None) -> np.ndarray:
+    """(K, n, 3, 3) tensor of composed blocks (reference lut.py:77-103).
+
+    Only cells that hold gates are composed; the rest are the exact identity,
+    which is what composing an empty list yields.  ``workers`` is accepted for
+    signature compatibility; cells are independent so the result is the same.
+    """
+    lut = np.empty((partition.k, partition.n, 3, 3))
+    lut[:] = np.eye(3)
+    for ki, bucket in enumerate(partition.u_groups):
+        for wire, gates in bucket.items():
+            lut[ki, wire] = compose_block(gates)
+    return lut
+
+
+# CX tables indexed [control axis, target axis] (reference lut.py:108-134).
+# Derived here from the x/z rule instead of typed in: with code bits (hi, lo),
+# z = hi and x = hi ^ lo;  CX: x_t ^= x_c, z_c ^= z_t, sign = -1 iff
+# x_c & z_t & ~(x_t ^ z_c) on the inputs.
+def _cx_tables():
+    tc = np.zeros((4, 4), dtype=np.int64)
+    tt = np.zeros((4, 4), dtype=np.int64)
+    ts = np.ones((4, 4), dtype=np.int64)
+    for dc in range(4):
+        for dt in range(4):
+            zc, xc = dc >> 1, (dc >> 1) ^ (dc & 1)
+            zt, xt = dt >> 1, (dt >> 1) ^ (dt & 1)
+            if xc & zt & (1 ^ xt ^ zc):
+                ts[dc, dt] = -1
+            xt2, zc2 = xt ^ xc, zc ^ zt
+            tc[dc, dt] = (zc2 << 1) | (zc2 ^ xc)
+            tt[dc, dt] = (zt << 1) | (zt ^ xt2)
+    return tc, tt, ts
+
+
+LUT_C, LUT_T, LUT_SIGN = _cx_tables()
+
+
+def cx_lookup(c: int, t: int) -> tuple:
+    """(c', t', sign) of CX conjugation on one (control, target) axis pair."""
+    return int(LUT_C[c, t]), int(LUT_T[c, t]), int(LUT_SIGN[c, t])
+
+
+def cx_device_words(sign_table=None) -> tuple:
+    """The three CX tables packed for the kernel: 2 bits (axes) / 1 bit (sign) per entry.
+
+    ``sign_table`` lets the tests inject a corrupted table (the reference's
+    mutation check, tests/test_cli.py:198-203) and see parity fail.
+    """
+    sign = LUT_SIGN if sign_table is None else sign_table
+    wc = wt = ws = 0
+    for dc in range(4):
+        for dt in range(4):
+            e = dc * 4 + dt
+            wc |= int(LUT_C[dc, dt]) << (2 * e)
+            wt |= int(LUT_T[dc, dt]) << (2 * e)
+            ws |= (1 if sign[dc, dt] < 0 else 0) << e
+    return wc, wt, ws
+
+
+def perm_word(block: np.ndarray):
+    """Pack a 3x3 block as a signed axis permutation, or None if it is not one.
+
+    A block qualifies only if every row has exactly one nonzero and that entry
+    is exactly +1.0 or -1.0 -- then conjugation neither branches nor rescales,
+    so no merge is needed after it.  Layout: bits 2(p-1)..2(p-1)+1 = image axis
+    of input axis p (1..3), bit 6+(p-1) = 1 for a minus sign.
+    """
+    word = 0
+    for p in range(3):
+        row = block[p]
+        hot = np.flatnonzero(row)
+        if len(hot) != 1:
+            return None
+        v = row[hot[0]]
+        if v != 1.0 and v != -1.0:
+            return None
+        word |= (int(hot[0]) + 1) << (2 * p)
+        if v < 0.0:
+            word |= 1 << (6 + p)
+    return word
+
+
+IDENTITY_PERM = perm_word(np.eye(3))
+
+
+def branch_table(block3: np.ndarray) -> tuple:
+    """(counts[3], axes[3][3], weights[3][3]) of one qubit's block.
+
+    Row p-1 describes input axis p: its nonzero output weights in ascending
+    axis order (the reference's ragged cell, stabilizer.py:209-214).  Unused
+    slots hold axis 0 / weight 0.0.
+    """
+    counts = np.zeros(3, dtype=np.int32)
+    axes = np.zeros((3, 3), dtype=np.int32)
+    weights = np.zeros((3, 3), dtype=np.float64)
+    for p in range(3):
+        hot = np.flatnonzero(block3[p])
+        counts[p] = len(hot)
+        axes[p, : len(hot)] = hot + 1
+        weights[p, : len(hot)] = block3[p, hot]
+    return counts, axes, weights
+
+
+def gate_branch_block(gate: str, theta: float) -> np.ndarray:
+    """The block a lone gate contributes: row p = column p of its axis map.
+
+    This is what v1's per-digit tables (reference engine.py:190-202) read:
+    for input digit d the candidates are the nonzeros of column d-1.
+    """
+    return np.ascontiguousarray(axis_map(gate, theta).T)
