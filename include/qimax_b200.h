@@ -1,0 +1,186 @@
+/*
+ * qimax_b200.h -- C ABI of the B200 extended-stabilizer hot path (libqimax_b200.so).
+ *
+ * The reference (stabsim, pure Python/numpy) has no FFI; its boundary is the
+ * public Python API.  Each entry point below names the reference function it
+ * replaces (paths under /root/reference/pkg/src/stabsim/).  INTEGRATION.md shows
+ * the ctypes binding a reference maintainer would add.
+ *
+ * Conventions
+ *   - plain pointers and sizes only; every pointer is HOST memory unless the
+ *     parameter name starts with d_ (then it is a device pointer on the store's device);
+ *   - every call returns a qx_status; on failure qx_last_error() (thread-local)
+ *     holds a message.  Python maps INVALID -> ValueError, RESOURCE ->
+ *     ResourceLimitError, CONSISTENCY -> ConsistencyError, CUDA/UNSUPPORTED -> NativeError;
+ *   - the caller owns handles; no pointer passed in is retained after return;
+ *   - a handle is not thread-safe; distinct handles may be used from distinct threads.
+ *
+ * Term layout (both host side and in HBM): structure of arrays.
+ *   key    uint64  base-4 Pauli word, 2 bits per qubit, qubit 0 most significant,
+ *                  axis codes I=0 X=1 Y=2 Z=3 (reference pauli.py:24-30,67-86).  With
+ *                  code bits (hi,lo): z = hi, x = hi ^ lo, so this *is* the packed
+ *                  2-bit x/z form, ordered so that unsigned integer order equals the
+ *                  reference's canonical order.  n_qubits <= 32 (one word).
+ *   lambda float64 real coefficient (reference stabilizer.py:92).
+ * A store holds n_segments generators back to back; offsets[s]..offsets[s+1] is
+ * generator s.  16 bytes per term.
+ */
+#ifndef QIMAX_B200_H
+#define QIMAX_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define QX_ABI_VERSION 1
+
+typedef enum {
+  QX_OK = 0,
+  QX_ERR_INVALID = 1,      /* bad argument (reference raises ValueError) */
+  QX_ERR_RESOURCE = 2,     /* a cap / budget / HBM limit would be exceeded (ResourceLimitError) */
+  QX_ERR_CUDA = 3,         /* CUDA runtime failure or no usable device */
+  QX_ERR_UNSUPPORTED = 4,  /* e.g. n_qubits > 32 */
+  QX_ERR_CONSISTENCY = 5   /* internal invariant failed (ConsistencyError) */
+} qx_status;
+
+typedef struct qx_store qx_store;          /* term store: a1 */
+typedef struct qx_expansion qx_expansion;  /* density-expansion accumulator: a9 */
+
+/* ---- library ------------------------------------------------------------ */
+int qx_abi_version(void);
+const char* qx_last_error(void);
+int qx_device_count(int* count);
+int qx_device_info(int device, char* name, int name_cap, int* sm_count, int* cc_major,
+                   int* cc_minor, int64_t* total_bytes, int64_t* free_bytes);
+
+/* Page-locked host buffers so uploads/downloads run at full PCIe rate (optional). */
+int qx_host_alloc(int64_t bytes, void** out);
+int qx_host_free(void* ptr);
+
+/* ---- a1: term store (stabilizer.py:83-109 SimpleGenerator, :157-174 GeneratorSet/init_z) */
+int qx_store_create(int device, int n_qubits, int n_segments, int64_t capacity_terms,
+                    qx_store** out);
+int qx_store_destroy(qx_store* s);
+/* Launch on this CUDA stream (a cudaStream_t) instead of the legacy default stream. */
+int qx_store_set_stream(qx_store* s, void* cuda_stream);
+/* Segment i := 1.0 * Z on qubit qubits[i] (init_z, stabilizer.py:169-174); NULL = qubit i. */
+int qx_store_init_z(qx_store* s, const int32_t* qubits);
+/* Replace the whole content: offsets has n_segments+1 entries, offsets[0] == 0. */
+int qx_store_upload(qx_store* s, const int64_t* offsets, const uint64_t* keys,
+                    const double* lambdas);
+/* Current term count per segment (synchronises). */
+int qx_store_ranks(qx_store* s, int64_t* ranks);
+/* Copy everything out: offsets (n_segments+1), then up to cap_terms keys/lambdas. */
+int qx_store_download(qx_store* s, int64_t* offsets, uint64_t* keys, double* lambdas,
+                      int64_t cap_terms);
+/* Device views for zero-copy consumers (valid until the next mutating call). */
+int qx_store_device_view(qx_store* s, const uint64_t** d_keys, const double** d_lambdas,
+                         const int64_t** d_offsets);
+int qx_store_capacity(qx_store* s, int64_t* capacity_terms, int64_t* hbm_bytes);
+int qx_store_synchronize(qx_store* s);
+
+/* ---- a2 + Clifford part of a3: fused run of sign-permutation gates ----------
+ * Replaces apply_cx (stabilizer.py:340-363) and _apply_1q_terms (engine.py:183-218)
+ * for H/S/X/SX and any composed U_k block that is a signed axis permutation.
+ * One launch pushes every term through the whole program in registers; conjugation
+ * by a Clifford is a bijection on words, so no merge is needed afterwards.
+ * op word: bits 0-1 kind (0 = 1q permutation, 1 = CX); bits 2-7 shift of the
+ * (control) digit = 2*(n-1-q); bits 8-13 shift of the CX target digit; for kind 0
+ * bits 16-23 = image axis of input axis a at bits 16+2a, bits 24-27 = sign bit of axis a.
+ * cx_c/cx_t: 2 bits per [control*4+target] entry; cx_s: 1 bit per entry
+ * (LUT_C/LUT_T/LUT_SIGN, lut.py:108-134). */
+int qx_apply_clifford(qx_store* s, const uint32_t* program, int32_t n_ops, uint32_t cx_c,
+                      uint32_t cx_t, uint32_t cx_s);
+
+/* ---- non-Clifford part of a3: split each term on one qubit (engine.py:190-217).
+ * For input digit d: first branch (a1[d], w1[d]) always, second branch (a2[d], w2[d])
+ * iff w2[d] != 0.  Output per segment is term-major: each term's first branch, then its
+ * second branch if it has one (slots from a warp-ballot prefix sum + tile look-back).
+ * A key only ever receives first branches or only second branches, so duplicates keep
+ * the relative order of the reference's [firsts..., seconds...] list and the merge sums
+ * them in the same order.  Unmerged; call qx_merge next. */
+int qx_apply_split(qx_store* s, int32_t qubit, const int32_t a1[4], const double w1[4],
+                   const int32_t a2[4], const double w2[4]);
+
+/* ---- a4 + a5: substitute-and-flatten of one U_k (stabilizer.py:189-206, 289-322).
+ * counts[j*3+p-1] = number of nonzero weights of input axis p on qubit j (1..3),
+ * axes/weights[(j*3+p-1)*3+b] = b-th (axis, weight), ascending axis.  Every term
+ * expands into the Cartesian product over its non-identity digits, branches in C
+ * order with qubit 0 slowest, lambda * w_q0 * w_q1 * ... left to right.
+ * Unmerged; raw_total receives the raw term count.  term_limit > 0 refuses
+ * (QX_ERR_RESOURCE) a raw count above it before anything is written. */
+int qx_apply_operator(qx_store* s, const int32_t* counts, const int32_t* axes,
+                      const double* weights, int64_t term_limit, int64_t* raw_total);
+/* Number of raw branches the same call would produce per segment, nothing written
+ * (branch_counts, stabilizer.py:232-237). */
+int qx_count_operator(qx_store* s, const int32_t* counts, int64_t* raw_per_segment);
+
+/* ---- a6: duplicate-term merge (canonicalize, stabilizer.py:325-337).
+ * Per segment: stable sort by key, in-order segmented sum, keep |sum| >= eps,
+ * ascending.  ranks (may be NULL) receives the new per-segment counts. */
+int qx_merge(qx_store* s, double eps, int64_t* ranks);
+
+/* ---- north-star kernel (4): per segment, sum of lambda over Z/I-only words. */
+int qx_store_zi_sums(qx_store* s, double* sums);
+/* Per segment sum of lambda^2 (the P^2 = I self-check). */
+int qx_store_norms(qx_store* s, double* sum_sq);
+
+/* ---- a9/a10: density expansion 2^-n prod_j (I + P_j) (measure.py:40-91) ---- */
+int qx_expansion_create(int device, int n_qubits, int64_t capacity_terms, qx_expansion** out);
+int qx_expansion_destroy(qx_expansion* e);
+int qx_expansion_reset(qx_expansion* e); /* acc := { I^n : 1 } */
+/* acc := merge(acc U acc*g) for one generator given as host arrays; refuses with
+ * QX_ERR_RESOURCE when |acc| * (1 + count) > term_budget (measure.py:59-62). */
+int qx_expansion_multiply(qx_expansion* e, const uint64_t* keys, const double* lambdas,
+                          int64_t count, int64_t term_budget);
+/* Same with the generator read from a store segment already in HBM. */
+int qx_expansion_multiply_segment(qx_expansion* e, qx_store* s, int32_t segment,
+                                  int64_t term_budget);
+int qx_expansion_size(qx_expansion* e, int64_t* terms);
+int qx_expansion_max_abs_imag(qx_expansion* e, double* worst);
+int qx_expansion_download(qx_expansion* e, uint64_t* keys, double* re, double* im,
+                          int64_t cap_terms);
+/* Unscaled real coefficient of each word (0 if absent): coeffs.get (measure.py:35-37). */
+int qx_expansion_lookup(qx_expansion* e, const uint64_t* words, int64_t n_words, double* re);
+
+/* ---- term hash-partition for multi-GPU rebalancing ----------
+ * Reorders every segment so that terms owned by rank r = mix(key) % world are
+ * contiguous, rank-major; send_counts[r * n_segments + s] = terms of segment s owned by r.
+ * After the call the store is laid out [rank0: seg0..segS-1][rank1: ...]. */
+int qx_store_partition_by_owner(qx_store* s, int32_t world, int64_t* send_counts);
+/* Inverse side of the exchange: d_keys/d_lambdas (DEVICE pointers) hold what this rank
+ * received, laid out [source 0: seg0..segS-1][source 1: ...] with
+ * recv_counts[q * n_segments + s] terms each; the store becomes segment-major
+ * (sources in rank order inside a segment), ready for qx_merge. */
+int qx_store_assemble(qx_store* s, const uint64_t* d_keys, const double* d_lambdas, int32_t world,
+                      const int64_t* recv_counts);
+
+/* ---- instrumentation: per kernel-class CUDA-event timing -------------------- */
+typedef enum {
+  QX_K_CLIFFORD = 0,
+  QX_K_SPLIT = 1,
+  QX_K_EXPAND_COUNT = 2,
+  QX_K_EXPAND_EMIT = 3,
+  QX_K_SORT_HIST = 4,
+  QX_K_SORT_PASS = 5,
+  QX_K_REDUCE = 6,
+  QX_K_SMALL_MERGE = 7,
+  QX_K_READOUT_PRODUCT = 8,
+  QX_K_READOUT_REDUCE = 9,
+  QX_K_PARTITION = 10,
+  QX_K_CLASSES = 11
+} qx_kernel_class;
+int qx_profile_enable(int on);
+int qx_profile_reset(void);
+/* launches, summed device milliseconds and summed algorithmic bytes of one class
+ * since the last reset (synchronises the device). */
+int qx_profile_read(int kernel_class, int64_t* launches, double* total_ms, double* alg_bytes);
+/* Total kernel launches issued by this library since load (never reset). */
+int qx_launch_count(int64_t* launches);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* QIMAX_B200_H */

@@ -1,0 +1,415 @@
+// Non-Clifford gate-apply: the kernels that make terms branch.
+//
+//   qx_apply_split    -- v1, one rotation on one qubit: each term keeps its first
+//                        branch and, where the gate mixes axes, emits a second one
+//                        (reference engine.py:183-218).  Single pass: warp ballot
+//                        prefix sums + one decoupled look-back per tile give every
+//                        term its compacted output slot.
+//   qx_apply_operator -- v2/v3, a whole U_k: substitute the per-qubit 3x3 blocks and
+//                        flatten the Cartesian product (reference stabilizer.py:189-206
+//                        sub, :289-322 _flatten_ragged).  The (S, n, 4) weight tensor
+//                        is never materialised: a count pass gives each term its raw
+//                        offset, then one thread per OUTPUT term decodes its branch
+//                        id as a mixed-radix number over the term's non-identity
+//                        digits (qubit 0 slowest) and multiplies the weights left to
+//                        right in qubit order, like the reference does.
+//
+// Both leave the store unmerged (raw); qx_merge follows.  Output order inside a
+// segment is "term-major, branches ascending", which keeps duplicates of one key in
+// the same relative order as the reference's raw lists, so the merge sums them in
+// the same order.
+#include <algorithm>
+
+#include "qx_device.cuh"
+
+namespace {
+
+constexpr int kThreads = QX_SCAN_THREADS;
+constexpr int kItems = QX_SCAN_ITEMS;
+constexpr int kTile = QX_SCAN_TILE;
+constexpr int kWarps = kThreads / 32;
+constexpr int kSegSmem = 1024;          // offsets cached in shared memory up to this many segments
+
+// ---------------------------------------------------------------------------------
+// v1 split
+// ---------------------------------------------------------------------------------
+struct SplitTable {
+  double w1[4], w2[4];
+  u32 a1[4], a2[4];
+  u32 shift;
+};
+
+__global__ void __launch_bounds__(kThreads)
+k_split(const u64* __restrict__ keys_in, const double* __restrict__ lam_in,
+        const int64_t* __restrict__ seg_in, int n_seg, u64* __restrict__ keys_out,
+        double* __restrict__ lam_out, int64_t* __restrict__ seg_out, u64* status, u32* ticket,
+        const SplitTable tb) {
+  __shared__ int s_tile;
+  __shared__ u64 s_scan[kWarps + 1];
+  __shared__ u64 s_base;
+  const int tile = take_ticket(ticket, &s_tile);
+  const int64_t total = seg_in[n_seg];
+  const int64_t ntiles = total > 0 ? (total + kTile - 1) / kTile : 1;
+  if (tile >= ntiles) return;
+  const int warp = threadIdx.x >> 5, lane = lane_id();
+  const int64_t wbase = (int64_t)tile * kTile + (int64_t)warp * (32 * kItems);
+
+  u64 key[kItems];
+  double lam[kItems];
+  u32 dig[kItems];
+  u32 pre[kItems];                         // second-branch count before this item, inside the warp
+  u32 running = 0;
+#pragma unroll
+  for (int k = 0; k < kItems; ++k) {
+    const int64_t i = wbase + k * 32 + lane;
+    const bool live = i < total;
+    key[k] = live ? ld_stream(keys_in + i) : 0ull;
+    lam[k] = live ? ld_stream(lam_in + i) : 0.0;
+    dig[k] = (u32)(key[k] >> tb.shift) & 3u;
+    const bool second = live && tb.w2[dig[k]] != 0.0;
+    const u32 votes = __ballot_sync(QX_FULL_MASK, second);
+    pre[k] = running + __popc(votes & lanemask_lt());
+    running += __popc(votes);
+  }
+  // exclusive prefix of the warp totals, then of the tile
+  u64 tile_total;
+  const u64 mine = (lane == 0) ? (u64)running : 0ull;
+  u64 warp_excl = block_exclusive_sum<u64>(mine, s_scan, tile_total);
+  warp_excl = __shfl_sync(QX_FULL_MASK, warp_excl, 0);
+  if (warp == 0) {
+    const u64 excl = lookback_exclusive(status, tile, tile_total);
+    if (lane == 0) s_base = excl;
+  }
+  __syncthreads();
+  const u64 base = s_base + warp_excl;
+
+#pragma unroll
+  for (int k = 0; k < kItems; ++k) {
+    const int64_t i = wbase + k * 32 + lane;
+    if (i >= total) continue;
+    const int64_t pos = i + (int64_t)(base + pre[k]);
+    const u32 d = dig[k];
+    const u64 cleared = key[k] & ~(3ull << tb.shift);
+    st_stream(keys_out + pos, cleared | ((u64)tb.a1[d] << tb.shift));
+    st_stream(lam_out + pos, lam[k] * tb.w1[d]);
+    if (tb.w2[d] != 0.0) {
+      st_stream(keys_out + pos + 1, cleared | ((u64)tb.a2[d] << tb.shift));
+      st_stream(lam_out + pos + 1, lam[k] * tb.w2[d]);
+    }
+    const int g = segment_of(seg_in, n_seg, i);
+    if (seg_in[g] == i) open_offsets(seg_in, seg_out, g, i, pos);
+  }
+  if (tile == ntiles - 1 && threadIdx.x == 0)
+    close_offsets(seg_in, seg_out, n_seg, total, total + (int64_t)(s_base + tile_total));
+}
+
+// ---------------------------------------------------------------------------------
+// v2/v3 operator
+// ---------------------------------------------------------------------------------
+// Indexed by digit position p = n-1-qubit (p = 0 is the least significant digit).
+struct OperatorTable {
+  double w[QX_MAX_QUBITS][3][3];
+  unsigned char axis[QX_MAX_QUBITS][3][3];
+  unsigned char cnt[QX_MAX_QUBITS][3];
+};
+
+__device__ __forceinline__ u64 branch_count(u64 key, const unsigned char (*cnt)[3]) {
+  u64 m = support_mask(key), c = 1;
+  while (m) {
+    const int b = __ffsll((long long)m) - 1;
+    m &= m - 1;
+    c *= cnt[b >> 1][((key >> b) & 3ull) - 1];
+  }
+  return c;
+}
+
+// roff[i] = raw terms produced by input terms before i (roff[total] = raw total).
+__global__ void __launch_bounds__(kThreads)
+k_expand_count(const u64* __restrict__ keys_in, const int64_t* __restrict__ seg_in, int n_seg,
+               u64* __restrict__ roff, u64* status, u32* ticket,
+               const __grid_constant__ OperatorTable tb) {
+  __shared__ int s_tile;
+  __shared__ u64 s_scan[kWarps + 1];
+  __shared__ u64 s_base;
+  __shared__ unsigned char s_cnt[QX_MAX_QUBITS][3];
+  for (int i = threadIdx.x; i < QX_MAX_QUBITS * 3; i += kThreads) s_cnt[i / 3][i % 3] = tb.cnt[i / 3][i % 3];
+  const int tile = take_ticket(ticket, &s_tile);     // has the __syncthreads that publishes s_cnt
+  const int64_t total = seg_in[n_seg];
+  const int64_t ntiles = total > 0 ? (total + kTile - 1) / kTile : 1;
+  if (tile >= ntiles) return;
+  const int warp = threadIdx.x >> 5, lane = lane_id();
+  const int64_t wbase = (int64_t)tile * kTile + (int64_t)warp * (32 * kItems);
+  u64 pre[kItems];
+  u64 running = 0;
+#pragma unroll
+  for (int k = 0; k < kItems; ++k) {
+    const int64_t i = wbase + k * 32 + lane;
+    const u64 c = (i < total) ? branch_count(ld_stream(keys_in + i), s_cnt) : 0ull;
+    const u64 inc = warp_inclusive_sum(c);
+    pre[k] = running + inc - c;
+    running += __shfl_sync(QX_FULL_MASK, inc, 31);
+  }
+  u64 tile_total;
+  const u64 mine = (lane == 0) ? running : 0ull;
+  u64 warp_excl = block_exclusive_sum<u64>(mine, s_scan, tile_total);
+  warp_excl = __shfl_sync(QX_FULL_MASK, warp_excl, 0);
+  if (warp == 0) {
+    const u64 excl = lookback_exclusive(status, tile, tile_total);
+    if (lane == 0) s_base = excl;
+  }
+  __syncthreads();
+  const u64 base = s_base + warp_excl;
+#pragma unroll
+  for (int k = 0; k < kItems; ++k) {
+    const int64_t i = wbase + k * 32 + lane;
+    if (i < total) roff[i] = base + pre[k];
+  }
+  if (tile == ntiles - 1 && threadIdx.x == 0) roff[total] = s_base + tile_total;
+}
+
+__global__ void k_gather_offsets(const int64_t* __restrict__ seg_in, int n_seg,
+                                 const u64* __restrict__ roff, int64_t* __restrict__ seg_out) {
+  const int g = blockIdx.x * blockDim.x + threadIdx.x;
+  if (g <= n_seg) seg_out[g] = (int64_t)roff[seg_in[g]];
+}
+
+constexpr int kEmitItems = 8;
+constexpr int kEmitTile = kThreads * kEmitItems;
+
+// index of the last entry <= r in a strictly increasing array a[0..n)
+__device__ __forceinline__ int64_t last_le(const u64* a, int64_t n, u64 r) {
+  int64_t lo = 0, hi = n;                  // a[lo] <= r < a[hi] (a[n] = +inf)
+  while (hi - lo > 1) {
+    const int64_t mid = (lo + hi) >> 1;
+    if (a[mid] <= r) lo = mid; else hi = mid;
+  }
+  return lo;
+}
+
+__global__ void __launch_bounds__(kThreads)
+k_expand_emit(const u64* __restrict__ keys_in, const double* __restrict__ lam_in,
+              const u64* __restrict__ roff, int64_t total_in, u64* __restrict__ keys_out,
+              double* __restrict__ lam_out, const __grid_constant__ OperatorTable tb) {
+  __shared__ OperatorTable s_tb;
+  __shared__ u64 s_win[kEmitTile + 1];
+  __shared__ int64_t s_lohi[2];
+  {
+    const u32* src = reinterpret_cast<const u32*>(&tb);
+    u32* dst = reinterpret_cast<u32*>(&s_tb);
+    for (int i = threadIdx.x; i < (int)(sizeof(OperatorTable) / 4); i += kThreads) dst[i] = src[i];
+  }
+  const u64 raw_total = roff[total_in];
+  const int64_t ntiles = (int64_t)((raw_total + kEmitTile - 1) / kEmitTile);
+  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const u64 r0 = (u64)tile * kEmitTile;
+    const u64 r1 = min(r0 + (u64)kEmitTile, raw_total);          // exclusive
+    __syncthreads();                                             // previous window fully consumed
+    if (threadIdx.x == 0) s_lohi[0] = last_le(roff, total_in, r0);
+    if (threadIdx.x == 32) s_lohi[1] = last_le(roff, total_in, r1 - 1);
+    __syncthreads();
+    const int64_t lo = s_lohi[0], hi = s_lohi[1];
+    const int span = (int)(hi - lo) + 1;                          // source terms feeding this tile
+    for (int i = threadIdx.x; i < span; i += kThreads) s_win[i] = roff[lo + i];
+    __syncthreads();
+#pragma unroll 2
+    for (int k = 0; k < kEmitItems; ++k) {
+      const u64 r = r0 + (u64)k * kThreads + threadIdx.x;
+      if (r >= r1) break;
+      const int rel = (int)last_le(s_win, span, r);
+      const int64_t src = lo + rel;
+      const u64 key = keys_in[src];
+      u64 b = r - s_win[rel];
+      // pass 1, least significant digit first: peel one mixed-radix digit per non-identity qubit
+      u64 m = support_mask(key);
+      u64 choice = 0;                                            // 2 bits per digit position
+      for (u64 mm = m; mm;) {
+        const int bit = __ffsll((long long)mm) - 1;
+        mm &= mm - 1;
+        const u32 c = s_tb.cnt[bit >> 1][((key >> bit) & 3ull) - 1];
+        u32 pick = 0;
+        if (c == 2) { pick = (u32)(b & 1ull); b >>= 1; }
+        else if (c == 3) { const u64 q = b / 3ull; pick = (u32)(b - 3ull * q); b = q; }
+        choice |= (u64)pick << bit;
+      }
+      // pass 2, qubit 0 first: multiply weights in the reference's order, assemble the word
+      double v = lam_in[src];
+      u64 out = 0;
+      while (m) {
+        const int bit = 63 - __clzll((long long)m);
+        m ^= 1ull << bit;
+        const u32 d = (u32)((key >> bit) & 3ull) - 1u;
+        const u32 pick = (u32)(choice >> bit) & 3u;
+        v *= s_tb.w[bit >> 1][d][pick];
+        out |= (u64)s_tb.axis[bit >> 1][d][pick] << bit;
+      }
+      st_stream(keys_out + r, out);
+      st_stream(lam_out + r, v);
+    }
+  }
+}
+
+int fill_table(const qx_store* s, const int32_t* counts, const int32_t* axes, const double* weights,
+               OperatorTable* tb) {
+  for (int p = 0; p < QX_MAX_QUBITS; ++p)
+    for (int a = 0; a < 3; ++a) {
+      tb->cnt[p][a] = 1;
+      for (int b = 0; b < 3; ++b) {
+        tb->axis[p][a][b] = (unsigned char)(a + 1);
+        tb->w[p][a][b] = (b == 0) ? 1.0 : 0.0;
+      }
+    }
+  for (int j = 0; j < s->n_qubits; ++j) {
+    const int p = s->n_qubits - 1 - j;
+    for (int a = 0; a < 3; ++a) {
+      const int c = counts[j * 3 + a];
+      QX_REQUIRE(c >= 1 && c <= 3, "qubit %d axis %d: %d nonzero weights (need 1..3)", j, a + 1, c);
+      tb->cnt[p][a] = (unsigned char)c;
+      if (!axes || !weights) continue;
+      int prev = 0;
+      for (int b = 0; b < c; ++b) {
+        const int ax = axes[(j * 3 + a) * 3 + b];
+        QX_REQUIRE(ax > prev && ax <= 3, "qubit %d axis %d: output axes must ascend within 1..3", j, a + 1);
+        prev = ax;
+        tb->axis[p][a][b] = (unsigned char)ax;
+        tb->w[p][a][b] = weights[(j * 3 + a) * 3 + b];
+      }
+    }
+  }
+  return QX_OK;
+}
+
+int prepare_lookback(qx_store* s, int64_t tiles, u64** status, u32** ticket) {
+  // layout in scratch: [ticket (8 bytes)] [status u64 * tiles]
+  const int64_t bytes = 8 + 8 * (tiles + 1);
+  QX_TRY(qx_store_scratch(s, bytes));
+  QX_CUDA(cudaMemsetAsync(s->scratch, 0, (size_t)bytes, s->stream));
+  *ticket = reinterpret_cast<u32*>(s->scratch);
+  *status = reinterpret_cast<u64*>(reinterpret_cast<char*>(s->scratch) + 8);
+  return QX_OK;
+}
+
+}  // namespace
+
+extern "C" int qx_apply_split(qx_store* s, int32_t qubit, const int32_t a1[4], const double w1[4],
+                              const int32_t a2[4], const double w2[4]) {
+  QX_REQUIRE(s && a1 && w1 && a2 && w2, "NULL argument");
+  QX_REQUIRE(qubit >= 0 && qubit < s->n_qubits, "qubit %d out of range for n=%d", qubit, s->n_qubits);
+  SplitTable tb;
+  tb.shift = 2u * (u32)(s->n_qubits - 1 - qubit);
+  for (int d = 0; d < 4; ++d) {
+    QX_REQUIRE(a1[d] >= 0 && a1[d] <= 3 && a2[d] >= 0 && a2[d] <= 3, "axis code out of range");
+    tb.a1[d] = (u32)a1[d];
+    tb.a2[d] = (u32)a2[d];
+    tb.w1[d] = w1[d];
+    tb.w2[d] = w2[d];
+  }
+  QX_CUDA(cudaSetDevice(s->device));
+  const int64_t ub_in = s->ub_total;
+  QX_TRY(qx_store_reserve(s, 2 * ub_in + 2, true));
+  const int64_t tiles = std::max<int64_t>(1, (s->ub_total + kTile - 1) / kTile);
+  u64* status;
+  u32* ticket;
+  QX_TRY(prepare_lookback(s, tiles, &status, &ticket));
+  const int in = s->cur, out = s->cur ^ 1;
+  {
+    QxProfileScope prof(QX_K_SPLIT, s->stream, 16.0 * 3.0 * (double)s->ub_total);
+    k_split<<<(unsigned)tiles, kThreads, 0, s->stream>>>(s->keys[in], s->lam[in], s->seg[in], s->n_seg,
+                                                         s->keys[out], s->lam[out], s->seg[out], status,
+                                                         ticket, tb);
+    QX_CUDA(cudaGetLastError());
+  }
+  qx_store_flip(s);
+  s->exact = false;
+  s->ub_total = 2 * ub_in;
+  s->ub_seg = 2 * s->ub_seg;
+  return QX_OK;
+}
+
+static int count_pass(qx_store* s, const OperatorTable& tb, u64** roff_out) {
+  // needs exact input size: the count array is indexed by input term
+  if (!s->exact) QX_TRY(qx_store_refresh(s));
+  const int64_t total = s->h_seg[s->n_seg];
+  const int64_t tiles = std::max<int64_t>(1, (total + kTile - 1) / kTile);
+  const int64_t lb_bytes = 8 + 8 * (tiles + 1);
+  const int64_t roff_at = (lb_bytes + 255) / 256 * 256;
+  QX_TRY(qx_store_scratch(s, roff_at + 8 * (total + 1)));
+  QX_CUDA(cudaMemsetAsync(s->scratch, 0, (size_t)lb_bytes, s->stream));
+  u32* ticket = reinterpret_cast<u32*>(s->scratch);
+  u64* status = reinterpret_cast<u64*>(reinterpret_cast<char*>(s->scratch) + 8);
+  u64* roff = reinterpret_cast<u64*>(reinterpret_cast<char*>(s->scratch) + roff_at);
+  {
+    QxProfileScope prof(QX_K_EXPAND_COUNT, s->stream, 16.0 * (double)total);
+    k_expand_count<<<(unsigned)tiles, kThreads, 0, s->stream>>>(s->keys[s->cur], s->seg[s->cur],
+                                                                s->n_seg, roff, status, ticket, tb);
+    QX_CUDA(cudaGetLastError());
+  }
+  *roff_out = roff;
+  return QX_OK;
+}
+
+extern "C" int qx_count_operator(qx_store* s, const int32_t* counts, int64_t* raw_per_segment) {
+  QX_REQUIRE(s && counts && raw_per_segment, "NULL argument");
+  OperatorTable tb;
+  QX_TRY(fill_table(s, counts, nullptr, nullptr, &tb));
+  QX_CUDA(cudaSetDevice(s->device));
+  u64* roff;
+  QX_TRY(count_pass(s, tb, &roff));
+  // borrow the dead offsets array for the gathered raw offsets
+  int64_t* tmp = s->seg[s->cur ^ 1];
+  k_gather_offsets<<<(s->n_seg + 256) / 256, 256, 0, s->stream>>>(s->seg[s->cur], s->n_seg, roff, tmp);
+  qx_count_launches(1);
+  QX_CUDA(cudaGetLastError());
+  QX_CUDA(cudaMemcpyAsync(s->h_pinned, tmp, sizeof(int64_t) * (size_t)(s->n_seg + 1),
+                          cudaMemcpyDeviceToHost, s->stream));
+  QX_CUDA(cudaStreamSynchronize(s->stream));
+  for (int g = 0; g < s->n_seg; ++g) raw_per_segment[g] = s->h_pinned[g + 1] - s->h_pinned[g];
+  return QX_OK;
+}
+
+extern "C" int qx_apply_operator(qx_store* s, const int32_t* counts, const int32_t* axes,
+                                 const double* weights, int64_t term_limit, int64_t* raw_total) {
+  QX_REQUIRE(s && counts && axes && weights, "NULL argument");
+  OperatorTable tb;
+  QX_TRY(fill_table(s, counts, axes, weights, &tb));
+  QX_CUDA(cudaSetDevice(s->device));
+  u64* roff;
+  QX_TRY(count_pass(s, tb, &roff));
+  const int64_t total_in = s->h_seg[s->n_seg];
+  const int in = s->cur, out = s->cur ^ 1;
+  k_gather_offsets<<<(s->n_seg + 256) / 256, 256, 0, s->stream>>>(s->seg[in], s->n_seg, roff, s->seg[out]);
+  qx_count_launches(1);
+  QX_CUDA(cudaGetLastError());
+  QX_CUDA(cudaMemcpyAsync(s->h_pinned, s->seg[out], sizeof(int64_t) * (size_t)(s->n_seg + 1),
+                          cudaMemcpyDeviceToHost, s->stream));
+  QX_CUDA(cudaStreamSynchronize(s->stream));
+  const int64_t raw = s->h_pinned[s->n_seg];
+  if (raw_total) *raw_total = raw;
+  if (term_limit > 0 && raw > term_limit)
+    return qx_fail(QX_ERR_RESOURCE, "operator would expand %lld terms into %lld raw terms (limit %lld)",
+                   (long long)total_in, (long long)raw, (long long)term_limit);
+  if (raw > s->cap) {
+    // growing moves the live terms; the count array (scratch) and the gathered offsets stay valid
+    std::vector<int64_t> raw_off(s->h_pinned, s->h_pinned + s->n_seg + 1);
+    QX_TRY(qx_store_reserve(s, raw, true));
+    QX_CUDA(cudaMemcpyAsync(s->seg[s->cur ^ 1], raw_off.data(), sizeof(int64_t) * (size_t)(s->n_seg + 1),
+                            cudaMemcpyHostToDevice, s->stream));
+    QX_CUDA(cudaStreamSynchronize(s->stream));
+  }
+  const int in2 = s->cur, out2 = s->cur ^ 1;
+  if (raw > 0) {
+    const int64_t tiles = (raw + kEmitTile - 1) / kEmitTile;
+    const int grid = (int)std::min<int64_t>(tiles, (int64_t)s->sm_count * 8);
+    QxProfileScope prof(QX_K_EXPAND_EMIT, s->stream, 16.0 * ((double)total_in + (double)raw));
+    k_expand_emit<<<grid, kThreads, 0, s->stream>>>(s->keys[in2], s->lam[in2], roff, total_in,
+                                                    s->keys[out2], s->lam[out2], tb);
+    QX_CUDA(cudaGetLastError());
+  }
+  (void)in; (void)out;
+  qx_store_flip(s);
+  for (int g = 0; g <= s->n_seg; ++g) s->h_seg[g] = s->h_pinned[g];
+  s->exact = true;
+  s->ub_total = raw;
+  s->ub_seg = 0;
+  for (int g = 0; g < s->n_seg; ++g) s->ub_seg = std::max(s->ub_seg, s->h_seg[g + 1] - s->h_seg[g]);
+  return QX_OK;
+}

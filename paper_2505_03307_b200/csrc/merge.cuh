@@ -1,0 +1,579 @@
+// a6: the duplicate-term merge (reference stabilizer.py:325-337 canonicalize;
+// measure.py:76-91 _merge for the complex read-out accumulator).
+//
+//   unique-sort by key  ->  in-order sum of each run of equal keys  ->  drop  ->  ascending
+//
+// Two device paths, same semantics, both deterministic (no floating-point atomics:
+// the sort is stable and every run is summed sequentially in input order, which is
+// the order np.add.at uses):
+//
+//   small  every segment <= QX_SMALL_MAX raw terms: ONE launch, one CTA per segment;
+//          bitonic sort on (key, input position) in shared memory, run sums, and a
+//          look-back across segments so the output is written compacted.  This is the
+//          latency path (configs 1, 2, 3, 5: a few thousand terms, hundreds of merges).
+//   large  segmented onesweep LSD radix sort, 8 bits per pass over the 2n significant
+//          key bits only (n = 16 -> 4 passes, not 8): one histogram pass, then per digit
+//          one pass that ranks a 4608-term tile in shared memory (warp match + per-warp
+//          counters), resolves its global offsets by decoupled look-back, and scatters
+//          through shared memory so runs of equal digit leave as coalesced stores.
+//          Tiles are segment-aligned, so generators never mix and no generator-id pass
+//          is needed.  A final reduce-by-key pass sums runs, applies the drop rule and
+//          compacts with a second look-back.  HBM-bound: 32 B per term per sort pass.
+//
+// Templated on the coefficient type: double (evolution, keep |sum| >= eps) and
+// double2 (read-out, complex, keep sum != 0).
+#pragma once
+
+#include <algorithm>
+
+#include "qx_device.cuh"
+
+namespace qxm {
+
+// ---------------------------------------------------------------------------------
+// coefficient traits
+// ---------------------------------------------------------------------------------
+__device__ __forceinline__ void acc(double& a, double b) { a += b; }
+__device__ __forceinline__ void acc(double2& a, double2 b) { a.x += b.x; a.y += b.y; }
+__device__ __forceinline__ bool keep(double v, double eps) { return fabs(v) >= eps; }
+__device__ __forceinline__ bool keep(double2 v, double) { return v.x != 0.0 || v.y != 0.0; }
+
+constexpr int kSortThreads = QX_SORT_THREADS;
+constexpr int kSortItems = QX_SORT_ITEMS;
+constexpr int kSortTile = QX_SORT_TILE;
+constexpr int kSortWarps = kSortThreads / 32;
+constexpr u32 kFlagAgg = 1u << 30;
+constexpr u32 kFlagInc = 2u << 30;
+constexpr u32 kFlagVal = (1u << 30) - 1;
+
+// ---------------------------------------------------------------------------------
+// plan: segment-aligned tile table
+// ---------------------------------------------------------------------------------
+// tile_prefix[g] = sort tiles owned by segments before g; [n_seg] = total tiles.
+static __global__ void k_sort_plan(const int64_t* __restrict__ seg, int n_seg,
+                            int64_t* __restrict__ tile_prefix, u32* ticket) {
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    int64_t run = 0;
+    for (int g = 0; g < n_seg; ++g) {
+      tile_prefix[g] = run;
+      run += (seg[g + 1] - seg[g] + kSortTile - 1) / kSortTile;
+    }
+    tile_prefix[n_seg] = run;
+    *ticket = 0u;
+  }
+}
+
+// largest g with tile_prefix[g] <= tile < tile_prefix[g+1]
+__device__ __forceinline__ int tile_segment(const int64_t* tile_prefix, int n_seg, int64_t tile) {
+  int lo = 0, hi = n_seg;
+  while (hi - lo > 1) {
+    const int mid = (lo + hi) >> 1;
+    if (tile_prefix[mid] <= tile) lo = mid; else hi = mid;
+  }
+  return lo;
+}
+
+// ---------------------------------------------------------------------------------
+// histogram: hist[g][pass][digit], all passes in one read of the keys
+// ---------------------------------------------------------------------------------
+constexpr int kMaxPasses = 8;
+
+static __global__ void __launch_bounds__(kSortThreads)
+k_sort_hist(const u64* __restrict__ keys, const int64_t* __restrict__ seg, int n_seg,
+            const int64_t* __restrict__ tile_prefix, u32* __restrict__ hist, int passes) {
+  __shared__ u32 sh[kMaxPasses][QX_RADIX];
+  for (int i = threadIdx.x; i < kMaxPasses * QX_RADIX; i += kSortThreads) (&sh[0][0])[i] = 0u;
+  __syncthreads();
+  const int64_t total_tiles = tile_prefix[n_seg];
+  int cur_g = -1;
+  for (int64_t tile = blockIdx.x; tile < total_tiles; tile += gridDim.x) {
+    const int g = tile_segment(tile_prefix, n_seg, tile);
+    if (g != cur_g) {
+      if (cur_g >= 0) {
+        __syncthreads();
+        for (int i = threadIdx.x; i < passes * QX_RADIX; i += kSortThreads) {
+          const u32 c = (&sh[0][0])[i];
+          if (c) atomicAdd(hist + (size_t)cur_g * passes * QX_RADIX + i, c);
+          (&sh[0][0])[i] = 0u;
+        }
+        __syncthreads();
+      }
+      cur_g = g;
+    }
+    const int64_t start = seg[g] + (tile - tile_prefix[g]) * kSortTile;
+    const int count = (int)min((int64_t)kSortTile, seg[g + 1] - start);
+#pragma unroll 4
+    for (int k = 0; k < kSortItems; ++k) {
+      const int idx = k * kSortThreads + threadIdx.x;
+      const bool live = idx < count;
+      const u64 key = live ? ld_stream(keys + start + idx) : 0ull;
+      const u32 alive = __ballot_sync(QX_FULL_MASK, live);
+      for (int p = 0; p < passes; ++p) {
+        const u32 d = (u32)(key >> (QX_RADIX_BITS * p)) & (QX_RADIX - 1);
+        // Pauli words are sparse: whole warps often share a digit; count those once.
+        const u32 d0 = __shfl_sync(QX_FULL_MASK, d, __ffs(alive | 0x80000000u) - 1);
+        const bool same = __all_sync(QX_FULL_MASK, !live || d == d0);
+        if (same) {
+          if (live && lane_id() == (u32)(__ffs(alive) - 1)) atomicAdd(&sh[p][d], (u32)__popc(alive));
+        } else if (live) {
+          atomicAdd(&sh[p][d], 1u);
+        }
+      }
+    }
+  }
+  if (cur_g >= 0) {
+    __syncthreads();
+    for (int i = threadIdx.x; i < passes * QX_RADIX; i += kSortThreads) {
+      const u32 c = (&sh[0][0])[i];
+      if (c) atomicAdd(hist + (size_t)cur_g * passes * QX_RADIX + i, c);
+    }
+  }
+}
+
+// counts -> exclusive digit offsets inside the segment, in place; one block per (g, pass)
+static __global__ void __launch_bounds__(QX_RADIX) k_sort_scan_hist(u32* __restrict__ hist) {
+  __shared__ u32 s_scan[QX_RADIX / 32 + 1];
+  u32* row = hist + (size_t)blockIdx.x * QX_RADIX;
+  const u32 c = row[threadIdx.x];
+  u32 total;
+  const u32 excl = block_exclusive_sum<u32>(c, s_scan, total);
+  row[threadIdx.x] = excl;
+}
+
+// ---------------------------------------------------------------------------------
+// one onesweep pass
+// ---------------------------------------------------------------------------------
+template <typename V>
+struct SortSmem {
+  u32 whist[kSortWarps][QX_RADIX];   // per-warp digit counters -> exclusive warp offsets
+  u32 tile_start[QX_RADIX];          // first slot of each digit in the tile-sorted order
+  int64_t gbase[QX_RADIX];           // global index of slot 0 of each digit, minus tile_start
+  u32 scan[kSortWarps + 1];
+  int tile;
+  u64 keys[kSortTile];
+  V vals[kSortTile];
+};
+
+template <typename V>
+__global__ void __launch_bounds__(kSortThreads)
+k_onesweep(const u64* __restrict__ keys_in, const V* __restrict__ vals_in,
+           u64* __restrict__ keys_out, V* __restrict__ vals_out,
+           const int64_t* __restrict__ seg, int n_seg, const int64_t* __restrict__ tile_prefix,
+           const u32* __restrict__ digit_base, int base_stride, u32* status, u32* ticket, int shift) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  SortSmem<V>& sm = *reinterpret_cast<SortSmem<V>*>(smem_raw);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = lane_id();
+
+  if (tid == 0) sm.tile = (int)atomicAdd(ticket, 1u);
+  for (int i = tid; i < kSortWarps * QX_RADIX; i += kSortThreads) (&sm.whist[0][0])[i] = 0u;
+  __syncthreads();
+  const int64_t tile = sm.tile;
+  if (tile >= tile_prefix[n_seg]) return;
+  const int g = tile_segment(tile_prefix, n_seg, tile);
+  const bool first = tile == tile_prefix[g];
+  const int64_t start = seg[g] + (tile - tile_prefix[g]) * kSortTile;
+  const int count = (int)min((int64_t)kSortTile, seg[g + 1] - start);
+
+  // ---- load, warp-striped: warp w owns tile slots [w*32*ITEMS, (w+1)*32*ITEMS)
+  u64 key[kSortItems];
+  u32 rank[kSortItems];
+  const int wslot = warp * (32 * kSortItems) + lane;
+#pragma unroll
+  for (int k = 0; k < kSortItems; ++k) {
+    const int idx = wslot + k * 32;
+    key[k] = idx < count ? ld_stream(keys_in + start + idx) : ~0ull;   // padding sorts last
+  }
+  // ---- rank inside the warp: lanes with equal digits form a group, the lowest lane
+  // bumps the warp's counter by the group size, everyone takes old + position in group
+#pragma unroll
+  for (int k = 0; k < kSortItems; ++k) {
+    const u32 d = (u32)(key[k] >> shift) & (QX_RADIX - 1);
+    const u32 peers = __match_any_sync(QX_FULL_MASK, d);
+    const u32 below = __popc(peers & lanemask_lt());
+    u32 old = 0;
+    if (below == 0) {
+      old = sm.whist[warp][d];
+      sm.whist[warp][d] = old + __popc(peers);
+    }
+    old = __shfl_sync(QX_FULL_MASK, old, __ffs(peers) - 1);
+    rank[k] = old + below;
+    __syncwarp();
+  }
+  __syncthreads();
+
+  // ---- per digit: exclusive offsets over warps, tile totals, exclusive scan over digits
+  u32 digit_total = 0;
+  if (tid < QX_RADIX) {
+#pragma unroll
+    for (int w = 0; w < kSortWarps; ++w) {
+      const u32 c = sm.whist[w][tid];
+      sm.whist[w][tid] = digit_total;
+      digit_total += c;
+    }
+  }
+  u32 tile_sum;
+  const u32 dstart = block_exclusive_sum<u32>(digit_total, sm.scan, tile_sum);
+  if (tid < QX_RADIX) {
+    sm.tile_start[tid] = dstart;
+    // padding keys all carry digit 255 and sit behind the live ones
+    const u32 live_total = digit_total - ((tid == QX_RADIX - 1) ? (u32)(kSortTile - count) : 0u);
+    // ---- decoupled look-back, one chain per digit, confined to this segment's tiles
+    u32* mine = status + (size_t)tile * QX_RADIX + tid;
+    u32 excl = 0;
+    if (first) {
+      st_volatile_u32(mine, kFlagInc | live_total);
+    } else {
+      st_volatile_u32(mine, kFlagAgg | live_total);
+      const u32* prev = mine - QX_RADIX;
+      while (true) {
+        u32 w;
+        do { w = ld_volatile_u32(prev); } while ((w >> 30) == 0u);
+        excl += w & kFlagVal;
+        if ((w >> 30) == 2u) break;
+        prev -= QX_RADIX;
+      }
+      st_volatile_u32(mine, kFlagInc | (excl + live_total));
+    }
+    sm.gbase[tid] = seg[g] + (int64_t)digit_base[(size_t)g * base_stride + tid] + (int64_t)excl -
+                    (int64_t)dstart;
+  }
+  __syncthreads();
+
+  // ---- scatter into tile-sorted order in shared memory
+#pragma unroll
+  for (int k = 0; k < kSortItems; ++k) {
+    const u32 d = (u32)(key[k] >> shift) & (QX_RADIX - 1);
+    rank[k] += sm.tile_start[d] + sm.whist[warp][d];
+    sm.keys[rank[k]] = key[k];
+  }
+#pragma unroll
+  for (int k = 0; k < kSortItems; ++k) {
+    const int idx = wslot + k * 32;
+    if (idx < count) sm.vals[rank[k]] = ld_stream(vals_in + start + idx);
+  }
+  __syncthreads();
+
+  // ---- coalesced write-out: consecutive slots of one digit are consecutive in HBM
+#pragma unroll
+  for (int k = 0; k < kSortItems; ++k) {
+    const int slot = k * kSortThreads + tid;
+    if (slot < count) {
+      const u64 kk = sm.keys[slot];
+      const int64_t dst = sm.gbase[(u32)(kk >> shift) & (QX_RADIX - 1)] + slot;
+      st_stream(keys_out + dst, kk);
+      st_stream(vals_out + dst, sm.vals[slot]);
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------------
+// reduce-by-key + drop + compaction over the sorted segments
+// ---------------------------------------------------------------------------------
+constexpr int kRedThreads = QX_SCAN_THREADS;
+constexpr int kRedItems = QX_SCAN_ITEMS;
+constexpr int kRedTile = QX_SCAN_TILE;
+constexpr int kRedWarps = kRedThreads / 32;
+
+template <typename V>
+__global__ void __launch_bounds__(kRedThreads)
+k_reduce(const u64* __restrict__ keys_in, const V* __restrict__ vals_in,
+         const int64_t* __restrict__ seg_in, int n_seg, u64* __restrict__ keys_out,
+         V* __restrict__ vals_out, int64_t* __restrict__ seg_out, u64* status, u32* ticket,
+         double eps) {
+  __shared__ int s_tile;
+  __shared__ u64 s_scan[kRedWarps + 1];
+  __shared__ u64 s_base;
+  if (threadIdx.x == 0) s_tile = (int)atomicAdd(ticket, 1u);
+  __syncthreads();
+  const int tile = s_tile;
+  const int64_t total = seg_in[n_seg];
+  const int64_t ntiles = total > 0 ? (total + kRedTile - 1) / kRedTile : 1;
+  if (tile >= ntiles) return;
+  const int warp = threadIdx.x >> 5, lane = lane_id();
+  const int64_t wbase = (int64_t)tile * kRedTile + (int64_t)warp * (32 * kRedItems);
+
+  u64 key[kRedItems];
+  V sum[kRedItems];
+  u32 pre[kRedItems];          // kept heads before this item inside the warp
+  u32 flags = 0;               // bit k: item k is a kept head; bit 16+k: item k opens a segment
+  int segid[kRedItems];
+  u32 running = 0;
+#pragma unroll
+  for (int k = 0; k < kRedItems; ++k) {
+    const int64_t i = wbase + k * 32 + lane;
+    bool kept = false;
+    segid[k] = 0;
+    if (i < total) {
+      key[k] = keys_in[i];
+      const int g = segment_of(seg_in, n_seg, i);
+      segid[k] = g;
+      const bool opens = seg_in[g] == i;
+      const bool head = opens || keys_in[i - 1] != key[k];
+      if (opens) flags |= 1u << (16 + k);
+      if (head) {
+        V s = vals_in[i];
+        const int64_t end = seg_in[g + 1];
+        for (int64_t j = i + 1; j < end && keys_in[j] == key[k]; ++j) acc(s, vals_in[j]);
+        sum[k] = s;
+        kept = keep(s, eps);
+      }
+    }
+    if (kept) flags |= 1u << k;
+    const u32 votes = __ballot_sync(QX_FULL_MASK, kept);
+    pre[k] = running + __popc(votes & lanemask_lt());
+    running += __popc(votes);
+  }
+  u64 tile_total;
+  const u64 mine = (lane == 0) ? (u64)running : 0ull;
+  u64 warp_excl = block_exclusive_sum<u64>(mine, s_scan, tile_total);
+  warp_excl = __shfl_sync(QX_FULL_MASK, warp_excl, 0);
+  if (warp == 0) {
+    const u64 excl = lookback_exclusive(status, tile, tile_total);
+    if (lane == 0) s_base = excl;
+  }
+  __syncthreads();
+  const int64_t base = (int64_t)(s_base + warp_excl);
+#pragma unroll
+  for (int k = 0; k < kRedItems; ++k) {
+    const int64_t i = wbase + k * 32 + lane;
+    const int64_t pos = base + pre[k];
+    if (flags & (1u << k)) {
+      keys_out[pos] = key[k];
+      vals_out[pos] = sum[k];
+    }
+    if (flags & (1u << (16 + k))) {
+      seg_out[segid[k]] = pos;
+      for (int h = segid[k] - 1; h >= 0 && seg_in[h] == i; --h) seg_out[h] = pos;
+    }
+  }
+  if (tile == ntiles - 1 && threadIdx.x == 0) {
+    const int64_t total_out = (int64_t)(s_base + tile_total);
+    for (int g = n_seg; g >= 0 && seg_in[g] == total; --g) seg_out[g] = total_out;
+  }
+}
+
+// ---------------------------------------------------------------------------------
+// small path: one CTA per segment, everything in shared memory
+// ---------------------------------------------------------------------------------
+constexpr int kSmallThreads = 512;
+constexpr int kSmallWarps = kSmallThreads / 32;
+
+template <typename V>
+__global__ void __launch_bounds__(kSmallThreads)
+k_small_merge(const u64* __restrict__ keys_in, const V* __restrict__ vals_in,
+              const int64_t* __restrict__ seg_in, int n_seg, u64* __restrict__ keys_out,
+              V* __restrict__ vals_out, int64_t* __restrict__ seg_out, u64* status, u32* ticket,
+              int* error, int cap, double eps) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  u64* skey = reinterpret_cast<u64*>(smem_raw);                       // cap
+  unsigned short* sidx = reinterpret_cast<unsigned short*>(skey + cap);   // cap
+  __shared__ int s_g;
+  __shared__ u64 s_scan[kSmallWarps + 1];
+  __shared__ u64 s_base;
+  if (threadIdx.x == 0) s_g = (int)atomicAdd(ticket, 1u);
+  __syncthreads();
+  const int g = s_g;
+  if (g >= n_seg) return;
+  const int64_t start = seg_in[g];
+  int len = (int)min((int64_t)0x7fffffff, seg_in[g + 1] - start);
+  if (len > cap) {                       // host bound was wrong: flag it, keep the chain alive
+    if (threadIdx.x == 0) atomicExch(error, 1);
+    len = 0;
+  }
+  int m = 32;
+  while (m < len) m <<= 1;
+  for (int e = threadIdx.x; e < m; e += kSmallThreads) {
+    skey[e] = e < len ? keys_in[start + e] : ~0ull;
+    sidx[e] = (unsigned short)e;
+  }
+  __syncthreads();
+  // bitonic network on (key, input position): position breaks ties, so equal keys
+  // stay in input order and padding (key = max, position >= len) ends up last
+  for (int k = 2; k <= m; k <<= 1) {
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      for (int t = threadIdx.x; t < (m >> 1); t += kSmallThreads) {
+        const int lo = ((t & ~(j - 1)) << 1) | (t & (j - 1));
+        const int hi = lo | j;
+        const u64 ka = skey[lo], kb = skey[hi];
+        const unsigned short ia = sidx[lo], ib = sidx[hi];
+        const bool greater = ka > kb || (ka == kb && ia > ib);
+        const bool ascending = (lo & k) == 0;
+        if (greater == ascending) {
+          skey[lo] = kb; skey[hi] = ka;
+          sidx[lo] = ib; sidx[hi] = ia;
+        }
+      }
+      __syncthreads();
+    }
+  }
+  // run sums (sequential, input order), drop rule, ordered compaction row by row
+  const int rows = (len + kSmallThreads - 1) / kSmallThreads;
+  u64 kept_before = 0;                   // kept heads in earlier rows
+  // first sweep: count, so that the segment's output base is known before writing
+  u64 my_count = 0;
+  for (int r = 0; r < rows; ++r) {
+    const int e = r * kSmallThreads + threadIdx.x;
+    if (e < len) {
+      const u64 key = skey[e];
+      if (e == 0 || skey[e - 1] != key) {
+        V s = vals_in[start + sidx[e]];
+        for (int j = e + 1; j < len && skey[j] == key; ++j) acc(s, vals_in[start + sidx[j]]);
+        if (keep(s, eps)) ++my_count;
+      }
+    }
+  }
+  u64 seg_total;
+  block_exclusive_sum<u64>(my_count, s_scan, seg_total);
+  if ((threadIdx.x >> 5) == 0) {
+    const u64 excl = lookback_exclusive(status, g, seg_total);
+    if (lane_id() == 0) s_base = excl;
+  }
+  __syncthreads();
+  const int64_t base = (int64_t)s_base;
+  for (int r = 0; r < rows; ++r) {
+    const int e = r * kSmallThreads + threadIdx.x;
+    bool kept = false;
+    u64 key = 0;
+    V s;
+    if (e < len) {
+      key = skey[e];
+      if (e == 0 || skey[e - 1] != key) {
+        s = vals_in[start + sidx[e]];
+        for (int j = e + 1; j < len && skey[j] == key; ++j) acc(s, vals_in[start + sidx[j]]);
+        kept = keep(s, eps);
+      }
+    }
+    u64 row_total;
+    const u64 excl = block_exclusive_sum<u64>(kept ? 1ull : 0ull, s_scan, row_total);
+    if (kept) {
+      const int64_t pos = base + (int64_t)(kept_before + excl);
+      keys_out[pos] = key;
+      vals_out[pos] = s;
+    }
+    kept_before += row_total;
+  }
+  if (threadIdx.x == 0) {
+    seg_out[g] = base;
+    if (g == n_seg - 1) seg_out[n_seg] = base + (int64_t)seg_total;
+  }
+}
+
+// ---------------------------------------------------------------------------------
+// host driver
+// ---------------------------------------------------------------------------------
+template <typename V>
+struct MergeBuffers {
+  u64* keys[2];
+  V* vals[2];
+  int64_t* seg[2];
+  int cur;            // live buffer on entry; updated to the live buffer on exit
+  int n_seg;
+  int64_t ub_total;   // host upper bounds on the raw sizes
+  int64_t ub_seg;
+};
+
+inline int64_t align_up(int64_t v, int64_t a) { return (v + a - 1) / a * a; }
+
+template <typename V>
+int merge_small(QxArena* ar, MergeBuffers<V>& mb, double eps, int cls) {
+  int cap = 32;
+  while (cap < mb.ub_seg) cap <<= 1;
+  const size_t smem = (size_t)cap * (sizeof(u64) + sizeof(unsigned short));
+  const int64_t bytes = 16 + 8 * ((int64_t)mb.n_seg + 1);
+  QX_TRY(qx_arena_scratch(ar, bytes));
+  QX_CUDA(cudaMemsetAsync(ar->scratch, 0, (size_t)bytes, ar->stream));
+  u32* ticket = reinterpret_cast<u32*>(ar->scratch);
+  int* error = reinterpret_cast<int*>(reinterpret_cast<char*>(ar->scratch) + 8);
+  u64* status = reinterpret_cast<u64*>(reinterpret_cast<char*>(ar->scratch) + 16);
+  static bool attr_set[2] = {false, false};
+  const int which = sizeof(V) == 8 ? 0 : 1;
+  if (!attr_set[which]) {
+    QX_CUDA(cudaFuncSetAttribute(k_small_merge<V>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 QX_SMALL_MAX * (int)(sizeof(u64) + sizeof(unsigned short))));
+    attr_set[which] = true;
+  }
+  const int in = mb.cur, out = mb.cur ^ 1;
+  {
+    QxProfileScope prof(cls, ar->stream, (16.0 + sizeof(V)) * (double)mb.ub_total);
+    k_small_merge<V><<<mb.n_seg, kSmallThreads, smem, ar->stream>>>(
+        mb.keys[in], mb.vals[in], mb.seg[in], mb.n_seg, mb.keys[out], mb.vals[out], mb.seg[out],
+        status, ticket, error, cap, eps);
+    QX_CUDA(cudaGetLastError());
+  }
+  QX_CUDA(cudaMemcpyAsync(ar->h_pinned, error, sizeof(int), cudaMemcpyDeviceToHost, ar->stream));
+  mb.cur = out;
+  return QX_OK;     // caller synchronises and checks *(int*)h_pinned
+}
+
+template <typename V>
+int merge_large(QxArena* ar, MergeBuffers<V>& mb, double eps, int cls_reduce) {
+  const int n_seg = mb.n_seg;
+  const int passes = std::min(kMaxPasses, (2 * ar->n_qubits + QX_RADIX_BITS - 1) / QX_RADIX_BITS);
+  if (mb.ub_seg >= (int64_t)kFlagVal)
+    return qx_fail(QX_ERR_RESOURCE, "a generator with %lld raw terms exceeds the sort's 2^30 limit",
+                   (long long)mb.ub_seg);
+  const int64_t tiles_ub = (mb.ub_total + kSortTile - 1) / kSortTile + n_seg;
+  const int64_t red_tiles = std::max<int64_t>(1, (mb.ub_total + kRedTile - 1) / kRedTile);
+  // scratch layout: ticket | tile_prefix | hist | reduce look-back
+  const int64_t off_prefix = 256;
+  const int64_t off_hist = align_up(off_prefix + 8 * ((int64_t)n_seg + 1), 256);
+  const int64_t hist_bytes = 4ll * n_seg * passes * QX_RADIX;
+  const int64_t off_red = align_up(off_hist + hist_bytes, 256);
+  const int64_t total_bytes = off_red + 8 * (red_tiles + 1);
+  QX_TRY(qx_arena_scratch(ar, total_bytes));
+  QX_TRY(qx_arena_status(ar, tiles_ub * QX_RADIX));
+  char* base = reinterpret_cast<char*>(ar->scratch);
+  u32* ticket = reinterpret_cast<u32*>(base);
+  int64_t* tile_prefix = reinterpret_cast<int64_t*>(base + off_prefix);
+  u32* hist = reinterpret_cast<u32*>(base + off_hist);
+  u64* red_status = reinterpret_cast<u64*>(base + off_red);
+  QX_CUDA(cudaMemsetAsync(base, 0, (size_t)total_bytes, ar->stream));
+
+  static bool attr_set[2] = {false, false};
+  const int which = sizeof(V) == 8 ? 0 : 1;
+  if (!attr_set[which]) {
+    QX_CUDA(cudaFuncSetAttribute(k_onesweep<V>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)sizeof(SortSmem<V>)));
+    attr_set[which] = true;
+  }
+  int cur = mb.cur;
+  k_sort_plan<<<1, 32, 0, ar->stream>>>(mb.seg[cur], n_seg, tile_prefix, ticket);
+  qx_count_launches(1);
+  QX_CUDA(cudaGetLastError());
+  {
+    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(tiles_ub, (int64_t)ar->sm_count * 4));
+    QxProfileScope prof(QX_K_SORT_HIST, ar->stream, 8.0 * (double)mb.ub_total);
+    k_sort_hist<<<grid, kSortThreads, 0, ar->stream>>>(mb.keys[cur], mb.seg[cur], n_seg, tile_prefix,
+                                                       hist, passes);
+    QX_CUDA(cudaGetLastError());
+  }
+  k_sort_scan_hist<<<n_seg * passes, QX_RADIX, 0, ar->stream>>>(hist);
+  qx_count_launches(1);
+  QX_CUDA(cudaGetLastError());
+  // the offsets do not change under a sort; both buffers need them for the ping-pong
+  QX_CUDA(cudaMemcpyAsync(mb.seg[cur ^ 1], mb.seg[cur], sizeof(int64_t) * (size_t)(n_seg + 1),
+                          cudaMemcpyDeviceToDevice, ar->stream));
+  for (int p = 0; p < passes; ++p) {
+    QX_CUDA(cudaMemsetAsync(ar->status, 0, sizeof(u32) * (size_t)(tiles_ub * QX_RADIX), ar->stream));
+    QX_CUDA(cudaMemsetAsync(ticket, 0, sizeof(u32), ar->stream));
+    QxProfileScope prof(QX_K_SORT_PASS, ar->stream, 2.0 * (8.0 + sizeof(V)) * (double)mb.ub_total);
+    k_onesweep<V><<<(unsigned)tiles_ub, kSortThreads, sizeof(SortSmem<V>), ar->stream>>>(
+        mb.keys[cur], mb.vals[cur], mb.keys[cur ^ 1], mb.vals[cur ^ 1], mb.seg[cur], n_seg,
+        tile_prefix, hist + (size_t)p * QX_RADIX, passes * QX_RADIX, ar->status, ticket,
+        p * QX_RADIX_BITS);
+    QX_CUDA(cudaGetLastError());
+    cur ^= 1;
+  }
+  QX_CUDA(cudaMemsetAsync(ticket, 0, sizeof(u32), ar->stream));
+  {
+    QxProfileScope prof(cls_reduce, ar->stream, (8.0 + sizeof(V)) * 2.0 * (double)mb.ub_total);
+    k_reduce<V><<<(unsigned)red_tiles, kRedThreads, 0, ar->stream>>>(
+        mb.keys[cur], mb.vals[cur], mb.seg[cur], n_seg, mb.keys[cur ^ 1], mb.vals[cur ^ 1],
+        mb.seg[cur ^ 1], red_status, ticket, eps);
+    QX_CUDA(cudaGetLastError());
+  }
+  mb.cur = cur ^ 1;
+  return QX_OK;
+}
+
+}  // namespace qxm

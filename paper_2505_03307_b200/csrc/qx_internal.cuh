@@ -1,0 +1,106 @@
+// Internal declarations shared by the translation units of libqimax_b200.so.
+// sm_100a only; no CPU fallback anywhere in this library.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+#include <vector>
+
+#include "../../include/qimax_b200.h"
+
+typedef unsigned long long u64;
+typedef unsigned int u32;
+
+// ----------------------------------------------------------------------------
+// error plumbing
+// ----------------------------------------------------------------------------
+int qx_fail(int status, const char* fmt, ...);
+
+#define QX_CUDA(expr)                                                              \
+  do {                                                                             \
+    cudaError_t _e = (expr);                                                       \
+    if (_e != cudaSuccess)                                                         \
+      return qx_fail(QX_ERR_CUDA, "%s failed: %s (%s:%d)", #expr,                  \
+                     cudaGetErrorString(_e), __FILE__, __LINE__);                  \
+  } while (0)
+
+#define QX_TRY(expr)                 \
+  do {                               \
+    int _s = (expr);                 \
+    if (_s != QX_OK) return _s;      \
+  } while (0)
+
+#define QX_REQUIRE(cond, ...)                              \
+  do {                                                     \
+    if (!(cond)) return qx_fail(QX_ERR_INVALID, __VA_ARGS__); \
+  } while (0)
+
+// ----------------------------------------------------------------------------
+// instrumentation (profile.cu)
+// ----------------------------------------------------------------------------
+struct QxProfileScope {
+  int cls;
+  cudaStream_t stream;
+  cudaEvent_t start, stop;
+  bool active;
+  QxProfileScope(int kernel_class, cudaStream_t st, double alg_bytes, int launches = 1);
+  ~QxProfileScope();
+};
+void qx_count_launches(int n);
+
+// ----------------------------------------------------------------------------
+// geometry of the device-wide passes
+// ----------------------------------------------------------------------------
+constexpr int QX_MAX_QUBITS = 32;
+constexpr int QX_RADIX_BITS = 8;
+constexpr int QX_RADIX = 1 << QX_RADIX_BITS;
+constexpr int QX_SORT_THREADS = 384;     // 12 warps
+constexpr int QX_SORT_ITEMS = 12;        // keys per thread, warp-striped
+constexpr int QX_SORT_TILE = QX_SORT_THREADS * QX_SORT_ITEMS;   // 4608 terms
+constexpr int QX_SMALL_MAX = 8192;       // largest segment the one-CTA merge takes
+constexpr int QX_SCAN_THREADS = 256;
+constexpr int QX_SCAN_ITEMS = 8;
+constexpr int QX_SCAN_TILE = QX_SCAN_THREADS * QX_SCAN_ITEMS;   // 2048 terms
+
+// ----------------------------------------------------------------------------
+// per-handle device context + scratch, shared by the store and the expansion
+// ----------------------------------------------------------------------------
+struct QxArena {
+  int device = 0;
+  int n_qubits = 0;
+  int sm_count = 148;
+  cudaStream_t stream = 0;
+  void* scratch = nullptr;      // generic byte scratch (tables, histograms, offsets)
+  int64_t scratch_bytes = 0;
+  u32* status = nullptr;        // look-back words of the sort passes
+  int64_t status_words = 0;
+  int64_t* h_pinned = nullptr;  // small pinned staging
+  int64_t h_pinned_words = 0;
+};
+int qx_arena_init(QxArena* a, int device, int n_qubits, int64_t pinned_words);
+void qx_arena_release(QxArena* a);
+int qx_arena_scratch(QxArena* a, int64_t bytes);
+int qx_arena_status(QxArena* a, int64_t words);
+
+// ----------------------------------------------------------------------------
+// the term store (a1)
+// ----------------------------------------------------------------------------
+struct qx_store : QxArena {
+  int n_seg = 0;
+  int64_t cap = 0;              // terms per buffer
+  u64* keys[2] = {nullptr, nullptr};
+  double* lam[2] = {nullptr, nullptr};
+  int64_t* seg[2] = {nullptr, nullptr};   // device offsets, n_seg+1 each
+  int cur = 0;                  // which of the two buffers is live
+  int64_t* h_seg = nullptr;     // pinned host mirror of the live offsets
+  bool exact = false;           // h_seg matches the device
+  int64_t ub_total = 0;         // host upper bound on the live term count
+  int64_t ub_seg = 0;           // host upper bound on the largest live segment
+};
+
+int qx_store_reserve(qx_store* s, int64_t terms, bool keep_live);
+int qx_store_refresh(qx_store* s);          // D2H of the live offsets, sets exact
+inline void qx_store_flip(qx_store* s) { s->cur ^= 1; }
+inline int qx_store_scratch(qx_store* s, int64_t bytes) { return qx_arena_scratch(s, bytes); }

@@ -1,0 +1,315 @@
+"""Simulation engine: the reference's ``engine.run`` on the B200 term store.
+
+Same entry points and report as the reference (``engine.py:45-243``): ``run``,
+``run_all_modes``, ``compare_reports``, ``Mode``, ``RunReport``.  Semantics per mode
+are the reference's -- where terms branch, where they are merged, which
+coefficients are dropped -- but the schedule is built for the GPU:
+
+* every gate/operator that is an exact signed axis permutation (H, S, X, SX, CX,
+  and any composed U_k block with entries 0/+-1) is a bijection on Pauli words and
+  keeps |lambda|, so the merge the reference runs after it can only re-sort.  Those
+  are queued and executed as ONE fused launch per run of such gates
+  (``qx_apply_clifford``), and the sort is deferred to the next real merge;
+* a gate/operator that branches (any rotation whose matrix is not a signed
+  permutation -- including angles like pi/2 whose cosine is 6e-17, exactly as the
+  reference treats them) flushes the queue, runs the branching kernel
+  (``qx_apply_split`` in v1, ``qx_apply_operator`` in v2/v3) and merges with the
+  reference's drop rule, at the same point of the circuit as the reference;
+* terms stay in HBM from ``init_z`` to the final download.
+
+The host walks the circuit; it never touches a term.
+"""
+
+from __future__ import annotations
+
+import time
+from dataclasses import dataclass, field
+from enum import Enum
+from typing import Sequence
+
+import numpy as np
+
+from . import lut as _lut
+from .circuit import Instruction, divide_instruction
+from .errors import NumericalCollapseError, ResourceLimitError
+from .stabilizer import (
+    DEFAULT_EPS,
+    DENSE_FLATTEN_BUDGET,
+    GeneratorSet,
+    SimpleGenerator,
+    keys_to_indices,
+    rank_stats,
+    split_tables,
+)
+from .store import DeviceStore
+
+
+class Mode(Enum):
+    V1 = "v1"
+    V2 = "v2"
+    V3 = "v3"
+
+    @classmethod
+    def coerce(cls, value) -> "Mode":
+        if isinstance(value, Mode):
+            return value
+        return cls(str(value).lower())
+
+
+@dataclass
+class RunReport:
+    """Final state, rank trace, timings and counters (reference engine.py:57-78)."""
+
+    mode: Mode
+    n: int
+    final: GeneratorSet
+    rank_trace: list
+    timings: dict
+    counters: dict
+    k: int
+    k_prime: int
+    order: list = field(default_factory=list)
+    # additions (not in the reference): what the device did
+    device: dict = field(default_factory=dict)
+
+    @property
+    def mean_rank(self) -> float:
+        return rank_stats(self.final)[1]
+
+    @property
+    def max_rank(self) -> int:
+        return max(max(step) for step in self.rank_trace)
+
+
+@dataclass
+class AgreementReport:
+    index_sets_equal: bool
+    max_lambda_deviation: float
+
+
+class _Walker:
+    """Queues sign-permutation ops and flushes them as one fused launch."""
+
+    def __init__(self, store: DeviceStore, n: int, ids, eps: float, timings: dict):
+        self.store, self.n, self.ids, self.eps = store, n, list(ids), eps
+        self.timings = timings
+        self.queue: list = []
+        self.queue_has_cx = False
+        self.unsorted = False          # a permutation ran since the last merge
+        self.ranks = [1] * len(self.ids)
+        self.launch_log = {"clifford_runs": 0, "branch_ops": 0, "merges": 0}
+
+    def push_perm(self, qubit: int, table: int):
+        if table != _lut.IDENTITY_PERM:
+            self.queue.append(_lut.perm_op(self.n, qubit, table))
+
+    def push_cx(self, control: int, target: int):
+        self.queue.append(_lut.cx_op(self.n, control, target))
+        self.queue_has_cx = True
+
+    def flush(self):
+        if not self.queue:
+            return
+        t0 = time.perf_counter()
+        self.store.apply_clifford(np.array(self.queue, dtype=np.uint32))
+        self.timings["cx" if self.queue_has_cx else "sub_flatten"] += time.perf_counter() - t0
+        self.queue, self.queue_has_cx = [], False
+        self.unsorted = True
+        self.launch_log["clifford_runs"] += 1
+
+    def merge(self, step: int, phase: str):
+        t0 = time.perf_counter()
+        self.ranks = self.store.merge(self.eps)
+        self.timings[phase] += time.perf_counter() - t0
+        self.unsorted = False
+        self.launch_log["merges"] += 1
+        for local, r in enumerate(self.ranks):
+            if r == 0:
+                raise NumericalCollapseError(
+                    f"all terms of generator {self.ids[local]} dropped at operator step {step}"
+                )
+
+
+def run(instructions: Sequence[Instruction], n: int, mode, eps: float = DEFAULT_EPS, *,
+        device=None, generators=None, capacity: int = 0, pinned: bool = False,
+        download: bool = True, initial=None) -> RunReport:
+    """Simulate a circuit; returns the canonical final generator set.
+
+    Positional arguments and result are the reference's (engine.py:89).  Keyword
+    extras: ``device`` (CUDA ordinal; default QX_DEVICE / LOCAL_RANK / 0),
+    ``generators`` (evolve only these generator ids -- they are independent, this is
+    the multi-GPU shard), ``capacity`` (initial terms of HBM to reserve), ``pinned``
+    (download into page-locked memory), ``download=False`` (leave the result in HBM;
+    ``report.final`` is then None and ``report.device['store']`` holds the live
+    store), ``initial`` (list of (lambdas, keys) replacing init_z, for read-out
+    back-propagation).
+    """
+    mode = Mode.coerce(mode)
+    timings = {"partition": 0.0, "lut": 0.0, "sub_flatten": 0.0, "cx": 0.0}
+    counters = {"gates": len(instructions), "sub_flatten_ops": 0, "cx_applications": 0}
+
+    t0 = time.perf_counter()
+    partition = divide_instruction(instructions, n)
+    timings["partition"] = time.perf_counter() - t0
+
+    if initial is not None:
+        ids = list(range(len(initial)))
+    else:
+        ids = list(range(n)) if generators is None else [int(g) for g in generators]
+        if any(g < 0 or g >= n for g in ids):
+            raise ValueError(f"generator ids {ids} out of range for n={n}")
+    if n < 1:
+        raise ValueError(f"qubit count must be positive, got {n}")
+
+    store = DeviceStore(n, max(len(ids), 1), capacity, device)
+    try:
+        if initial is not None:
+            store.upload(initial)
+            walker_ranks = [len(l) for l, _ in initial]
+            min_abs = min((float(np.min(np.abs(l))) for l, _ in initial if len(l)), default=1.0)
+        else:
+            store.init_z(ids)
+            walker_ranks = [1] * len(ids)
+            min_abs = 1.0
+        w = _Walker(store, n, ids, eps, timings)
+        w.ranks = walker_ranks
+        # If eps could already drop an initial term, merge after every step like the
+        # reference does; otherwise deferring the re-sort of permutation steps is exact.
+        eager = eps > min_abs
+        trace = [list(w.ranks)]
+
+        if mode is Mode.V1:
+            _walk_v1(instructions, partition, w, trace, counters, eager)
+        else:
+            t0 = time.perf_counter()
+            lut = _lut.create_lut_1q(partition)
+            is_perm, tables = _lut.classify_lut(lut) if partition.k else (None, None)
+            timings["lut"] = time.perf_counter() - t0
+            _walk_operators(partition, lut, is_perm, tables, w, trace, counters, mode, eager)
+
+        # final canonical order
+        w.flush()
+        if w.unsorted:
+            w.merge(max(len(trace) - 2, 0), "cx")
+        counters["operators"] = partition.k + partition.k_prime
+
+        info = {"device": store.device, **w.launch_log}
+        final = None
+        if download:
+            segs = store.segments(pinned)
+            final_gens = [SimpleGenerator(n, lam, keys_to_indices(keys, n)) for lam, keys in segs]
+            final = GeneratorSet(n, final_gens) if len(final_gens) == n else _Shard(n, ids, final_gens)
+        else:
+            info["store"] = store
+        return RunReport(mode=mode, n=n, final=final, rank_trace=trace, timings=timings,
+                         counters=counters, k=partition.k, k_prime=partition.k_prime,
+                         order=list(partition.order), device=info)
+    finally:
+        if download:
+            store.close()
+
+
+@dataclass
+class _Shard:
+    """A subset of the generators (multi-GPU shard or read-out words): same fields as
+    GeneratorSet without the exactly-n check, plus the global ids."""
+
+    n: int
+    ids: list
+    generators: list
+
+
+def _walk_v1(instructions, partition, w: _Walker, trace, counters, eager):
+    """Gate by gate (reference engine.py:155-180): rank snapshots at operator boundaries."""
+    n = w.n
+    boundaries = set(np.cumsum(partition.operator_sizes()).tolist())
+    for pos, inst in enumerate(instructions, start=1):
+        if inst.is_two_qubit:
+            w.push_cx(*inst.wires)
+            counters["cx_applications"] += 1
+            if eager:
+                w.flush()
+                w.merge(pos - 1, "cx")
+        else:
+            q = inst.wires[0]
+            table = _lut.FIXED_PERMS.get(inst.gate)
+            block = None
+            if table is None:
+                block = _lut.gate_branch_block(inst.gate, inst.theta)
+                table = _lut.perm_word(block)
+            if table is not None:
+                w.push_perm(q, table)
+                if eager:
+                    w.flush()
+                    w.merge(pos - 1, "sub_flatten")
+            else:
+                w.flush()
+                t0 = time.perf_counter()
+                w.store.apply_split(q, *split_tables(block))
+                w.timings["sub_flatten"] += time.perf_counter() - t0
+                w.launch_log["branch_ops"] += 1
+                w.merge(pos - 1, "sub_flatten")
+            counters["v1_gate_applications"] = counters.get("v1_gate_applications", 0) + 1
+        if pos in boundaries:
+            trace.append(list(w.ranks))
+
+
+def _walk_operators(partition, lut, is_perm, tables, w: _Walker, trace, counters, mode, eager):
+    """Operator chain (reference engine.py:110-132): U_k = substitute + flatten, V_k = CX run."""
+    n = w.n
+    ui = vi = 0
+    for step, bit in enumerate(partition.order):
+        if bit == 0:
+            if bool(is_perm[ui].all()):
+                for j in np.flatnonzero(tables[ui] != _lut.IDENTITY_PERM):
+                    w.push_perm(int(j), int(tables[ui][j]))
+                if eager:
+                    w.flush()
+                    w.merge(step, "sub_flatten")
+            else:
+                w.flush()
+                counts, axes, weights = _lut.operator_tables(lut[ui])
+                t0 = time.perf_counter()
+                if mode is Mode.V2 and 4 ** n > DENSE_FLATTEN_BUDGET:
+                    # dense layout: a branching substitution needs a 4**n scatter buffer
+                    # (reference stabilizer.py:264-276); one-hot rows take the fast path
+                    raw = w.store.count_operator(counts)
+                    if any(r > have for r, have in zip(raw, w.ranks)):
+                        raise ResourceLimitError(
+                            f"dense flatten needs a 4**{n}-element buffer (> {DENSE_FLATTEN_BUDGET}); "
+                            "use the ragged layout for circuits of this size"
+                        )
+                w.store.apply_operator(counts, axes, weights)
+                w.timings["sub_flatten"] += time.perf_counter() - t0
+                w.launch_log["branch_ops"] += 1
+                w.merge(step, "sub_flatten")
+            counters["sub_flatten_ops"] += 1
+            ui += 1
+        else:
+            for inst in partition.v_groups[vi]:
+                w.push_cx(*inst.wires)
+                counters["cx_applications"] += 1
+            if eager:
+                w.flush()
+                w.merge(step, "cx")
+            vi += 1
+        trace.append(list(w.ranks))
+
+
+def run_all_modes(instructions: Sequence[Instruction], n: int, eps: float = DEFAULT_EPS, **kw):
+    """Every mode on the same circuit + pairwise comparison (reference engine.py:221-226)."""
+    reports = {mode: run(instructions, n, mode, eps, **kw) for mode in Mode}
+    return reports, compare_reports(list(reports.values()))
+
+
+def compare_reports(reports: Sequence[RunReport]) -> AgreementReport:
+    """Index-set equality and max coefficient deviation (reference engine.py:229-243)."""
+    equal, worst = True, 0.0
+    for i, a in enumerate(reports):
+        for b in reports[i + 1:]:
+            for ga, gb in zip(a.final.generators, b.final.generators):
+                if ga.rank != gb.rank or list(ga.indices) != list(gb.indices):
+                    equal = False
+                elif ga.rank:
+                    worst = max(worst, float(np.max(np.abs(ga.lambdas - gb.lambdas))))
+    return AgreementReport(equal, worst if equal else float("inf"))

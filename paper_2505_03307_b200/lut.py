@@ -121,12 +121,13 @@ def perm_word(block: np.ndarray):
 
     A block qualifies only if every row has exactly one nonzero and that entry
     is exactly +1.0 or -1.0 -- then conjugation neither branches nor rescales,
-    so no merge is needed after it.  Layout: bits 2(p-1)..2(p-1)+1 = image axis
-    of input axis p (1..3), bit 6+(p-1) = 1 for a minus sign.
+    so no merge is needed after it.  Layout (12 bits, the table field of a
+    ``qx_apply_clifford`` op): bits 2a..2a+1 = image axis of input axis a
+    (a = 0 is the identity and maps to 0), bit 8+a = 1 for a minus sign.
     """
     word = 0
-    for p in range(3):
-        row = block[p]
+    for p in (1, 2, 3):
+        row = block[p - 1]
         hot = np.flatnonzero(row)
         if len(hot) != 1:
             return None
@@ -135,8 +136,18 @@ def perm_word(block: np.ndarray):
             return None
         word |= (int(hot[0]) + 1) << (2 * p)
         if v < 0.0:
-            word |= 1 << (6 + p)
+            word |= 1 << (8 + p)
     return word
+
+
+def perm_op(n: int, qubit: int, table: int) -> int:
+    """32-bit op word of a 1q signed permutation on ``qubit`` (include/qimax_b200.h)."""
+    return 0 | ((2 * (n - 1 - qubit)) << 2) | (table << 16)
+
+
+def cx_op(n: int, control: int, target: int) -> int:
+    """32-bit op word of CX(control, target)."""
+    return 1 | ((2 * (n - 1 - control)) << 2) | ((2 * (n - 1 - target)) << 8)
 
 
 IDENTITY_PERM = perm_word(np.eye(3))
@@ -167,3 +178,42 @@ def gate_branch_block(gate: str, theta: float) -> np.ndarray:
     for input digit d the candidates are the nonzeros of column d-1.
     """
     return np.ascontiguousarray(axis_map(gate, theta).T)
+
+
+def classify_lut(lut: np.ndarray) -> tuple:
+    """Vectorised ``perm_word`` over a whole (K, n, 3, 3) tensor.
+
+    Returns (is_perm bool[K, n], table uint32[K, n]); ``table`` is only
+    meaningful where ``is_perm``.
+    """
+    nz = lut != 0.0
+    one_hot = nz.sum(axis=-1) == 1                                   # (K, n, 3)
+    unit = np.where(nz, np.abs(lut) == 1.0, True).all(axis=-1)       # nonzeros are exactly +-1
+    is_perm = (one_hot & unit).all(axis=-1)
+    image = nz.argmax(axis=-1).astype(np.uint32) + 1                  # (K, n, 3)
+    minus = (lut.sum(axis=-1) < 0.0).astype(np.uint32)
+    table = np.zeros(lut.shape[:2], dtype=np.uint32)
+    for p in (1, 2, 3):
+        table |= image[..., p - 1] << np.uint32(2 * p)
+        table |= minus[..., p - 1] << np.uint32(8 + p)
+    return is_perm, table
+
+
+FIXED_PERMS = {name: perm_word(axis_map(name).T) for name in ("H", "S", "X", "SX")}
+
+
+def operator_tables(block: np.ndarray) -> tuple:
+    """Branch tables of a whole U_k: (counts[n,3], axes[n,3,3], weights[n,3,3])."""
+    n = block.shape[0]
+    nz = block != 0.0
+    counts = nz.sum(axis=-1).astype(np.int32)
+    # stable argsort of "is zero" lists the nonzero axes first, ascending
+    order = np.argsort(~nz, axis=-1, kind="stable")
+    weights = np.take_along_axis(block, order, axis=-1)
+    axes = (order + 1).astype(np.int32)
+    slot = np.arange(3)[None, None, :]
+    dead = slot >= counts[..., None]
+    axes[dead] = 0
+    weights = np.where(dead, 0.0, weights)
+    assert counts.shape == (n, 3)
+    return counts, axes, np.ascontiguousarray(weights)

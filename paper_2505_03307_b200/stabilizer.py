@@ -1,0 +1,258 @@
+"""Generator containers and the kernel-level operations, GPU-backed.
+
+Host-side mirror of the reference's ``stabilizer.py`` interface for the hot
+path: the same names, argument meaning and error behaviour
+(``SimpleGenerator`` :83-109, ``GeneratorSet`` :157-166, ``init_z`` :169-174,
+``sub`` :189-206, ``flatten`` :240-256, ``canonicalize`` :325-337,
+``apply_cx`` :340-363, ``rank_stats`` :366-369), so the reference's unit
+tests can be pointed at this module.  All arithmetic happens in
+``libqimax_b200.so`` on the GPU; these functions upload one generator, run the
+kernel(s), and download the result.  They are pure (inputs never mutated).
+
+For whole circuits use ``engine.run`` -- it keeps the terms in HBM between
+gates instead of round-tripping per call.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import lut as _lut
+from .errors import ResourceLimitError
+from .store import DeviceStore
+
+DEFAULT_EPS = 1e-12                 # reference stabilizer.py:38
+DENSE_FLATTEN_BUDGET = 4 ** 10      # reference stabilizer.py:45
+_INT64_MAX_QUBITS = 31              # 4**31 - 1 < 2**63
+MAX_QUBITS = 32                     # one uint64 key per term on the device
+
+
+def index_dtype(n: int):
+    """int64 up to 31 qubits, Python ints (object) beyond (reference stabilizer.py:48-49)."""
+    return np.int64 if n <= _INT64_MAX_QUBITS else object
+
+
+def make_index_array(values, n: int) -> np.ndarray:
+    if index_dtype(n) is object:
+        out = np.empty(len(values), dtype=object)
+        out[:] = [int(v) for v in values]
+        return out
+    return np.asarray(values, dtype=np.int64)
+
+
+def keys_to_indices(keys: np.ndarray, n: int) -> np.ndarray:
+    """Device keys (uint64) -> the reference's index array dtype."""
+    if index_dtype(n) is object:
+        return make_index_array(keys.tolist(), n)
+    return keys.view(np.int64) if keys.dtype == np.uint64 else keys.astype(np.int64)
+
+
+def indices_to_keys(indices, n: int) -> np.ndarray:
+    """Reference index array (int64 or object) -> uint64 keys, range-checked."""
+    if isinstance(indices, np.ndarray) and indices.dtype == np.int64:
+        if len(indices) and int(indices.min()) < 0:
+            raise ValueError("negative word index")
+        return indices.astype(np.uint64)
+    vals = [int(v) for v in indices]
+    if any(v < 0 or v >= 4 ** n for v in vals):
+        raise ValueError(f"word index out of range [0, 4**{n})")
+    return np.array(vals, dtype=np.uint64)
+
+
+@dataclass(eq=False)
+class SimpleGenerator:
+    """A generator as a weighted sum of Pauli words (reference stabilizer.py:83-109)."""
+
+    n: int
+    lambdas: np.ndarray
+    indices: np.ndarray
+
+    def __post_init__(self):
+        self.lambdas = np.asarray(self.lambdas, dtype=np.float64)
+        want = index_dtype(self.n)
+        if not isinstance(self.indices, np.ndarray) or self.indices.dtype != want:
+            self.indices = make_index_array(self.indices, self.n)
+        if len(self.lambdas) != len(self.indices):
+            raise ValueError("lambdas and indices must have equal length")
+
+    @property
+    def rank(self) -> int:
+        return len(self.lambdas)
+
+    @property
+    def is_degenerate(self) -> bool:
+        return self.rank == 0
+
+    def copy(self) -> "SimpleGenerator":
+        return SimpleGenerator(self.n, self.lambdas.copy(), self.indices.copy())
+
+    def keys(self) -> np.ndarray:
+        return indices_to_keys(self.indices, self.n)
+
+
+@dataclass
+class GeneratorSet:
+    """The n generators of an n-qubit state (reference stabilizer.py:157-166)."""
+
+    n: int
+    generators: list
+
+    def __post_init__(self):
+        if len(self.generators) != self.n:
+            raise ValueError(f"expected exactly {self.n} generators, got {len(self.generators)}")
+
+
+def init_z(n: int) -> GeneratorSet:
+    """Generators of |0...0>: Z_j with coefficient 1 (reference stabilizer.py:169-174)."""
+    if n < 1:
+        raise ValueError(f"qubit count must be positive, got {n}")
+    return GeneratorSet(n, [SimpleGenerator(n, [1.0], [3 * 4 ** (n - 1 - j)]) for j in range(n)])
+
+
+def rank_stats(gs: GeneratorSet) -> tuple:
+    counts = [g.rank for g in gs.generators]
+    return counts, sum(counts) / len(counts)
+
+
+def generator_set_to_dict(gs: GeneratorSet) -> dict:
+    """JSON-ready dump (reference stabilizer.py:372-383)."""
+    return {
+        "n": gs.n,
+        "generators": [
+            {"lambda": [float(v) for v in g.lambdas], "index": [int(v) for v in g.indices]}
+            for g in gs.generators
+        ],
+    }
+
+
+# ------------------------------------------------------------------------------
+# kernel-level operations on one generator
+# ------------------------------------------------------------------------------
+def _one_segment(g: SimpleGenerator, capacity: int = 0) -> DeviceStore:
+    st = DeviceStore(g.n, 1, max(capacity, 2 * g.rank + 2))
+    st.upload([(g.lambdas, g.keys())])
+    return st
+
+
+def _fetch(st: DeviceStore, n: int) -> SimpleGenerator:
+    (lam, keys), = st.segments()
+    return SimpleGenerator(n, lam.copy(), keys_to_indices(keys.copy(), n))
+
+
+def apply_cx(g: SimpleGenerator, c: int, t: int) -> SimpleGenerator:
+    """Conjugate every word by CX(c, t); term count unchanged, output unsorted
+    (reference stabilizer.py:340-363)."""
+    n = g.n
+    if c == t:
+        raise ValueError(f"control and target must differ, got {c}")
+    if not (0 <= c < n and 0 <= t < n):
+        raise ValueError(f"wires ({c}, {t}) out of range for n={n}")
+    with _one_segment(g) as st:
+        st.apply_clifford([_lut.cx_op(n, c, t)])
+        return _fetch(st, n)
+
+
+def canonicalize(g: SimpleGenerator, eps: float = DEFAULT_EPS) -> SimpleGenerator:
+    """Merge duplicate words, drop |coefficient| < eps, sort ascending
+    (reference stabilizer.py:325-337)."""
+    if g.rank == 0:
+        return g.copy()
+    with _one_segment(g) as st:
+        st.merge(eps)
+        return _fetch(st, g.n)
+
+
+def apply_1q(g: SimpleGenerator, gate: str, q: int, theta: float = 0.0,
+             eps: float = DEFAULT_EPS) -> SimpleGenerator:
+    """One single-qubit gate on one generator, merged: the reference's
+    ``engine._apply_1q_terms`` (engine.py:183-218)."""
+    n = g.n
+    if not 0 <= q < n:
+        raise ValueError(f"wire {q} out of range for n={n}")
+    block = _lut.gate_branch_block(gate, theta)
+    with _one_segment(g) as st:
+        table = _lut.perm_word(block)
+        if table is not None:
+            st.apply_clifford([_lut.perm_op(n, q, table)])
+        else:
+            st.apply_split(q, *split_tables(block))
+        st.merge(eps)
+        return _fetch(st, n)
+
+
+def split_tables(block: np.ndarray) -> tuple:
+    """Per-digit (a1, w1, a2, w2) of a lone gate (reference engine.py:190-202)."""
+    counts, axes, weights = _lut.branch_table(block)
+    if int(counts.max()) > 2:
+        raise ValueError("a single gate maps an axis to at most two axes")
+    a1 = np.zeros(4, dtype=np.int32)
+    a2 = np.zeros(4, dtype=np.int32)
+    w1 = np.zeros(4)
+    w2 = np.zeros(4)
+    w1[0] = 1.0
+    a1[1:], w1[1:] = axes[:, 0], weights[:, 0]
+    a2[1:], w2[1:] = axes[:, 1], weights[:, 1]
+    return a1, w1, a2, w2
+
+
+@dataclass(eq=False)
+class ComplexForm:
+    """A generator with one U_k block substituted but not yet flattened.
+
+    Stands in for the reference's Dense/RaggedComplexGenerator
+    (stabilizer.py:112-154): on the device the (S, n, 4) weight tensor is never
+    materialised, so this only records the operands; ``flatten`` runs the
+    expansion kernel.
+    """
+
+    n: int
+    lambdas: np.ndarray
+    keys: np.ndarray
+    block: np.ndarray
+    layout: str = "ragged"
+
+
+def sub(g: SimpleGenerator, block: np.ndarray, layout: str = "ragged") -> ComplexForm:
+    """Substitute an (n, 3, 3) operator block (reference stabilizer.py:189-206)."""
+    block = np.asarray(block, dtype=np.float64)
+    if block.shape != (g.n, 3, 3):
+        raise ValueError(f"expected block shape ({g.n}, 3, 3), got {block.shape}")
+    if layout not in ("dense", "ragged"):
+        raise ValueError(f"unknown layout {layout!r}")
+    return ComplexForm(g.n, g.lambdas.copy(), g.keys(), block.copy(), layout)
+
+
+def branch_counts(cg: ComplexForm) -> np.ndarray:
+    """Raw branches the whole generator would expand into (sum of the reference's
+    per-string ``branch_counts``, stabilizer.py:232-237)."""
+    counts, _, _ = _lut.operator_tables(cg.block)
+    with DeviceStore(cg.n, 1, len(cg.lambdas) + 2) as st:
+        st.upload([(cg.lambdas, cg.keys)])
+        return np.array(st.count_operator(counts), dtype=np.int64)
+
+
+def flatten(cg: ComplexForm, eps: float = DEFAULT_EPS, canonical: bool = True) -> SimpleGenerator:
+    """Expand a complex form back into a simple form (reference stabilizer.py:240-256).
+
+    ``canonical=False`` returns the raw branch list (term-major, C order).  The
+    dense layout keeps the reference's budget guard (stabilizer.py:272-276): it
+    refuses a branching expansion when 4**n exceeds DENSE_FLATTEN_BUDGET.
+    """
+    if not isinstance(cg, ComplexForm):
+        raise TypeError(f"cannot flatten {type(cg).__name__}")
+    n = cg.n
+    counts, axes, weights = _lut.operator_tables(cg.block)
+    with DeviceStore(n, 1, 2 * len(cg.lambdas) + 2) as st:
+        st.upload([(cg.lambdas, cg.keys)])
+        if cg.layout == "dense" and canonical and 4 ** n > DENSE_FLATTEN_BUDGET:
+            if st.count_operator(counts)[0] > len(cg.lambdas):
+                raise ResourceLimitError(
+                    f"dense flatten needs a 4**{n}-element buffer (> {DENSE_FLATTEN_BUDGET}); "
+                    "use the ragged layout for circuits of this size"
+                )
+        st.apply_operator(counts, axes, weights)
+        if canonical:
+            st.merge(eps)
+        return _fetch(st, n)

@@ -1,0 +1,175 @@
+"""Python handle on the HBM term store (``qx_store`` in include/qimax_b200.h).
+
+Thin by design: every method is one C-ABI call.  Host <-> device copies happen
+only in ``upload`` / ``download``; everything else leaves the terms in HBM.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+
+import numpy as np
+
+from . import _native as nat
+from . import lut
+
+
+class DeviceStore:
+    """n_segments generators of an n-qubit system, structure-of-arrays in HBM."""
+
+    def __init__(self, n: int, n_segments: int, capacity: int = 0, device=None):
+        self.n = int(n)
+        self.n_segments = int(n_segments)
+        self.device = nat.default_device() if device is None else int(device)
+        self._h = C.c_void_p()
+        nat.check(nat.lib().qx_store_create(self.device, self.n, self.n_segments, int(capacity),
+                                            C.byref(self._h)))
+        self._cx = lut.cx_device_words()
+
+    # -- lifetime ---------------------------------------------------------------
+    def close(self):
+        h, self._h = self._h, None
+        if h is not None and h.value:
+            nat.check(nat.lib().qx_store_destroy(h))
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+    @property
+    def handle(self):
+        return self._h
+
+    def set_stream(self, cuda_stream: int):
+        nat.check(nat.lib().qx_store_set_stream(self._h, C.c_void_p(int(cuda_stream))))
+
+    def set_cx_tables(self, sign_table):
+        """Test hook: run with a (possibly corrupted) CX sign table."""
+        self._cx = lut.cx_device_words(sign_table)
+
+    # -- content ----------------------------------------------------------------
+    def init_z(self, qubits=None):
+        arr = None if qubits is None else np.ascontiguousarray(qubits, dtype=np.int32)
+        if arr is not None and len(arr) != self.n_segments:
+            raise ValueError(f"expected {self.n_segments} qubits, got {len(arr)}")
+        nat.check(nat.lib().qx_store_init_z(self._h, nat.ptr(arr)))
+
+    def upload(self, gens):
+        """gens: sequence of (lambdas, keys) per segment."""
+        if len(gens) != self.n_segments:
+            raise ValueError(f"expected {self.n_segments} segments, got {len(gens)}")
+        off = np.zeros(self.n_segments + 1, dtype=np.int64)
+        for i, (lam, keys) in enumerate(gens):
+            if len(lam) != len(keys):
+                raise ValueError("lambdas and indices must have equal length")
+            off[i + 1] = off[i] + len(lam)
+        keys = np.empty(int(off[-1]), dtype=np.uint64)
+        lam = np.empty(int(off[-1]), dtype=np.float64)
+        for i, (l, k) in enumerate(gens):
+            keys[off[i]:off[i + 1]] = np.asarray(k, dtype=np.uint64) if not _is_object(k) else [int(v) for v in k]
+            lam[off[i]:off[i + 1]] = l
+        nat.check(nat.lib().qx_store_upload(self._h, nat.ptr(off), nat.ptr(keys), nat.ptr(lam)))
+
+    def ranks(self) -> list:
+        out = np.zeros(self.n_segments, dtype=np.int64)
+        nat.check(nat.lib().qx_store_ranks(self._h, nat.ptr(out)))
+        return out.tolist()
+
+    def download(self, pinned: bool = False):
+        """(offsets int64[n_seg+1], keys uint64[total], lambdas float64[total]) on the host."""
+        off = np.zeros(self.n_segments + 1, dtype=np.int64)
+        nat.check(nat.lib().qx_store_download(self._h, nat.ptr(off), None, None, 0))
+        total = int(off[-1])
+        if pinned and total > 0:
+            buf = nat.PinnedBuffer(16 * total)
+            keys = buf.view(np.uint64, 0, total)
+            lam = buf.view(np.float64, 8 * total, total)
+        else:
+            keys = np.empty(total, dtype=np.uint64)
+            lam = np.empty(total, dtype=np.float64)
+        nat.check(nat.lib().qx_store_download(self._h, nat.ptr(off), nat.ptr(keys), nat.ptr(lam), total))
+        return off, keys, lam
+
+    def segments(self, pinned: bool = False) -> list:
+        """[(lambdas, keys)] per segment (views into one download)."""
+        off, keys, lam = self.download(pinned)
+        return [(lam[off[i]:off[i + 1]], keys[off[i]:off[i + 1]]) for i in range(self.n_segments)]
+
+    def device_view(self) -> tuple:
+        k, l, o = C.c_void_p(), C.c_void_p(), C.c_void_p()
+        nat.check(nat.lib().qx_store_device_view(self._h, C.byref(k), C.byref(l), C.byref(o)))
+        return k.value, l.value, o.value
+
+    def capacity(self) -> tuple:
+        cap, hbm = C.c_int64(), C.c_int64()
+        nat.check(nat.lib().qx_store_capacity(self._h, C.byref(cap), C.byref(hbm)))
+        return cap.value, hbm.value
+
+    def synchronize(self):
+        nat.check(nat.lib().qx_store_synchronize(self._h))
+
+    # -- kernels ----------------------------------------------------------------
+    def apply_clifford(self, program):
+        prog = np.ascontiguousarray(program, dtype=np.uint32)
+        if len(prog):
+            c, t, s = self._cx
+            nat.check(nat.lib().qx_apply_clifford(self._h, nat.ptr(prog), len(prog), c, t, s))
+
+    def apply_split(self, qubit: int, a1, w1, a2, w2):
+        a1 = np.ascontiguousarray(a1, dtype=np.int32)
+        a2 = np.ascontiguousarray(a2, dtype=np.int32)
+        w1 = np.ascontiguousarray(w1, dtype=np.float64)
+        w2 = np.ascontiguousarray(w2, dtype=np.float64)
+        nat.check(nat.lib().qx_apply_split(self._h, int(qubit), nat.ptr(a1), nat.ptr(w1), nat.ptr(a2), nat.ptr(w2)))
+
+    def apply_operator(self, counts, axes, weights, term_limit: int = 0) -> int:
+        counts = np.ascontiguousarray(counts, dtype=np.int32).reshape(-1)
+        axes = np.ascontiguousarray(axes, dtype=np.int32).reshape(-1)
+        weights = np.ascontiguousarray(weights, dtype=np.float64).reshape(-1)
+        raw = C.c_int64()
+        nat.check(nat.lib().qx_apply_operator(self._h, nat.ptr(counts), nat.ptr(axes), nat.ptr(weights),
+                                              int(term_limit), C.byref(raw)))
+        return raw.value
+
+    def count_operator(self, counts) -> list:
+        counts = np.ascontiguousarray(counts, dtype=np.int32).reshape(-1)
+        out = np.zeros(self.n_segments, dtype=np.int64)
+        nat.check(nat.lib().qx_count_operator(self._h, nat.ptr(counts), nat.ptr(out)))
+        return out.tolist()
+
+    def merge(self, eps: float) -> list:
+        out = np.zeros(self.n_segments, dtype=np.int64)
+        nat.check(nat.lib().qx_merge(self._h, float(eps), nat.ptr(out)))
+        return out.tolist()
+
+    def zi_sums(self) -> np.ndarray:
+        out = np.zeros(self.n_segments, dtype=np.float64)
+        nat.check(nat.lib().qx_store_zi_sums(self._h, nat.ptr(out)))
+        return out
+
+    def norms(self) -> np.ndarray:
+        out = np.zeros(self.n_segments, dtype=np.float64)
+        nat.check(nat.lib().qx_store_norms(self._h, nat.ptr(out)))
+        return out
+
+    def partition_by_owner(self, world: int) -> np.ndarray:
+        out = np.zeros((int(world), self.n_segments), dtype=np.int64)
+        nat.check(nat.lib().qx_store_partition_by_owner(self._h, int(world), nat.ptr(out)))
+        return out
+
+    def assemble(self, d_keys: int, d_lambdas: int, recv_counts):
+        rc = np.ascontiguousarray(recv_counts, dtype=np.int64)
+        nat.check(nat.lib().qx_store_assemble(self._h, C.c_void_p(int(d_keys)), C.c_void_p(int(d_lambdas)),
+                                              rc.shape[0], nat.ptr(rc.reshape(-1))))
+
+
+def _is_object(arr) -> bool:
+    return isinstance(arr, np.ndarray) and arr.dtype == object

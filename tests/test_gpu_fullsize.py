@@ -1,0 +1,44 @@
+"""BASELINE.json's largest-rank config at full size: xyz_chain(16, 2) (1.25e8 final terms).
+
+The reference needs ~3 minutes and the oracle cannot finish in seconds, so parity here is through
+size-independent properties: every generator is U Z_j U^dagger so sum(lambda^2) = 1;
+the final ranks are the ones the reference reported (125 430 039 terms, max 55 284 529);
+keys are strictly ascending inside every generator; two runs are bitwise identical; and the same
+circuit at (14, 2) matches the reference digests term for term (test_gpu_engine.py)."""
+
+import hashlib
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+from gpu_util import qx  # noqa: E402
+
+from paper_2505_03307_b200 import workloads  # noqa: E402
+
+
+def test_config4_16_2_properties():
+    n, gates = workloads.build("c4_xyz_16_2")
+    rep = qx.run(gates, n, "v3", download=False)
+    store = rep.device["store"]
+    try:
+        ranks = rep.rank_trace[-1]
+        assert sum(ranks) == 125_430_039 and max(ranks) == 55_284_529
+        assert np.max(np.abs(store.norms() - 1.0)) < 1e-9                   # P^2 = I
+        off, keys, lam = store.download(pinned=True)
+        for g in range(n):
+            seg = keys[off[g]:off[g + 1]]
+            assert np.all(seg[1:] > seg[:-1]), f"generator {g} not strictly ascending"
+        assert float(np.min(np.abs(lam))) >= 1e-12                          # drop rule applied
+        first = hashlib.sha256(keys.tobytes()).hexdigest(), hashlib.sha256(lam.tobytes()).hexdigest()
+    finally:
+        store.close()
+    rep2 = qx.run(gates, n, "v3", download=False)
+    store = rep2.device["store"]
+    try:
+        off2, keys2, lam2 = store.download(pinned=True)
+        second = hashlib.sha256(keys2.tobytes()).hexdigest(), hashlib.sha256(lam2.tobytes()).hexdigest()
+    finally:
+        store.close()
+    assert first == second                                                  # bitwise run-to-run determinism

@@ -1,0 +1,208 @@
+"""Kernel-level parity on the GPU: each C-ABI entry point against the reference's unit vectors
+(tests/golden/units.json, produced by the reference itself) and against the CPU oracle on seeded
+random inputs.  Keys must match bit-exactly; coefficients within 1e-10 (float64)."""
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+from gpu_util import DeviceStore, merge_on_device, oracle, qx, random_terms  # noqa: E402
+
+from paper_2505_03307_b200 import lut  # noqa: E402
+from paper_2505_03307_b200.stabilizer import SimpleGenerator, keys_to_indices  # noqa: E402
+
+TOL = 1e-10
+
+
+def _sg(n, lam, keys):
+    return SimpleGenerator(n, lam, keys_to_indices(np.asarray(keys, dtype=np.uint64), n))
+
+
+def test_units_apply_cx(golden):
+    for u in golden.load_json("units.json")["apply_cx"]:
+        lam, idx = golden.gen(u["in"])
+        out = qx.apply_cx(_sg(u["n"], lam, idx), u["c"], u["t"])
+        golden.assert_gens_equal([(out.lambdas, out.keys())], [golden.gen(u["out"])], exact=True)
+
+
+def test_units_apply_1q(golden):
+    for u in golden.load_json("units.json")["apply_1q"]:
+        lam, idx = golden.gen(u["in"])
+        out = qx.apply_1q(_sg(u["n"], lam, idx), u["gate"], u["q"], float.fromhex(u["theta"]))
+        golden.assert_gens_equal([(out.lambdas, out.keys())], [golden.gen(u["out"])], tol=TOL)
+
+
+def test_units_canonicalize(golden):
+    for u in golden.load_json("units.json")["canonicalize"]:
+        lam, idx = golden.gen(u["in"])
+        out = qx.canonicalize(_sg(u["n"], lam, idx), 1e-12)
+        golden.assert_gens_equal([(out.lambdas, out.keys())], [golden.gen(u["out"])], tol=TOL)
+
+
+def test_units_operator(golden):
+    for u in golden.load_json("units.json")["operator"]:
+        n = u["n"]
+        block = golden.unhex(u["block"]).reshape(n, 3, 3)
+        lam, idx = golden.gen(u["in"])
+        g = _sg(n, lam, idx)
+        raw = qx.flatten(qx.sub(g, block), canonical=False)
+        # raw lists: same multiset of (key, coefficient); order is term-major on the device
+        wl, wk = golden.gen(u["raw"])
+        assert sorted(zip(raw.keys().tolist(), raw.lambdas.tolist())) == sorted(zip(wk.tolist(), wl.tolist()))
+        for layout in ("ragged", "dense"):
+            out = qx.flatten(qx.sub(g, block, layout), 1e-12)
+            golden.assert_gens_equal([(out.lambdas, out.keys())], [golden.gen(u["out"])], tol=TOL)
+
+
+def test_kats_from_reference_tests():
+    # tests/test_stabilizer.py:219-229 (CX), :271-292 (merge), :140-155 (golden flatten)
+    out = qx.apply_cx(SimpleGenerator(3, [1.0], [16]), 0, 1)
+    assert list(out.indices) == [20] and list(out.lambdas) == [1.0]
+    out = qx.canonicalize(SimpleGenerator(1, [1.0, 1.0], [3, 3]))
+    assert list(out.lambdas) == [2.0] and list(out.indices) == [3]
+    out = qx.canonicalize(SimpleGenerator(1, [1e-15], [2]), eps=1e-12)
+    assert out.is_degenerate
+    out = qx.canonicalize(SimpleGenerator(2, [1.0, 2.0, 3.0], [9, 2, 5]))
+    assert list(out.indices) == [2, 5, 9]
+    block = np.zeros((2, 3, 3))
+    block[:] = np.eye(3)
+    block[0, 1] = [0.0, 3.0, 4.0]
+    block[1, 0] = [1.0, 0.0, 1.0]
+    out = qx.flatten(qx.sub(SimpleGenerator(2, [2.0, 1.0], [11, 1]), block))
+    assert list(out.indices) == [1, 3, 11, 15] and list(out.lambdas) == [1.0, 1.0, 6.0, 8.0]
+    with pytest.raises(ValueError):
+        qx.apply_cx(SimpleGenerator(2, [1.0], [5]), 1, 1)
+    with pytest.raises(ValueError):
+        qx.sub(SimpleGenerator(2, [1.0], [5]), np.zeros((3, 3, 3)))
+    big = qx.apply_cx(qx.init_z(32).generators[0], 1, 0)
+    assert int(big.indices[0]) == 3 * 4 ** 31 + 3 * 4 ** 30        # n > 31: Python-int indices
+
+
+@pytest.mark.parametrize("n,count,distinct", [
+    (1, 5, 3), (2, 33, 9), (4, 1000, 200), (8, 4096, 4096), (16, 8192, 3000), (32, 8192, 8000),   # small path
+    (5, 8193, 700), (16, 100_000, 40_000), (32, 300_000, 299_000), (10, 1_000_000, 600_000),          # large path
+    (16, 3_000_000, 1_000_000),
+])
+def test_merge_matches_oracle(n, count, distinct):
+    rng = np.random.default_rng(count * 31 + n)
+    lam, keys = random_terms(rng, n, count, distinct)
+    lam[rng.integers(0, count, size=max(1, count // 7))] *= 1e-13
+    (gl, gk), = merge_on_device(n, [(lam, keys)])
+    wl, wk = oracle.merge(lam, keys)
+    assert np.array_equal(gk, wk)
+    assert np.array_equal(gl, wl)          # same summation order as np.add.at -> bitwise
+
+
+def test_merge_many_segments_with_empties():
+    rng = np.random.default_rng(5)
+    n = 12
+    sizes = [0, 7, 0, 20_000, 1, 0, 9000, 4608, 4609, 0]
+    gens = [random_terms(rng, n, s, max(1, s // 2)) if s else (np.zeros(0), np.zeros(0, dtype=np.uint64)) for s in sizes]
+    got = merge_on_device(n, gens)
+    for (gl, gk), (lam, keys) in zip(got, gens):
+        wl, wk = oracle.merge(lam, keys)
+        assert np.array_equal(gk, wk) and np.array_equal(gl, wl)
+    small = [g if len(g[0]) <= 8192 else (g[0][:100], g[1][:100]) for g in gens]
+    got = merge_on_device(n, small)
+    for (gl, gk), (lam, keys) in zip(got, small):
+        wl, wk = oracle.merge(lam, keys)
+        assert np.array_equal(gk, wk) and np.array_equal(gl, wl)
+
+
+def test_merge_adversarial_keys():
+    n = 16
+    # all equal, already sorted, reverse sorted, two values alternating; sums that cancel exactly
+    same = (np.full(20_000, 0.25), np.full(20_000, 12345, dtype=np.uint64))
+    asc = (np.ones(30_000), np.arange(30_000, dtype=np.uint64) * np.uint64(65537) % np.uint64(4 ** n))
+    desc = (np.ones(30_000), asc[1][::-1].copy())
+    alt = (np.tile([1.0, -1.0], 10_000), np.tile(np.array([7, 7], dtype=np.uint64), 10_000))
+    got = merge_on_device(n, [same, asc, desc, alt])
+    for (gl, gk), (lam, keys) in zip(got, [same, asc, desc, alt]):
+        wl, wk = oracle.merge(lam, keys)
+        assert np.array_equal(gk, wk) and np.array_equal(gl, wl)
+    assert len(got[3][0]) == 0             # exact cancellation -> dropped -> empty generator
+
+
+def test_clifford_run_matches_oracle():
+    rng = np.random.default_rng(11)
+    for n in (2, 7, 16, 31, 32):
+        gates = qx.gen_random(n, 300, rng, gates=("H", "S", "X", "SX", "CX"))
+        lam, keys = random_terms(rng, n, 5001, 5001)
+        prog = []
+        wl, wk = lam.copy(), keys.copy()
+        for g in gates:
+            if g.gate == "CX":
+                prog.append(lut.cx_op(n, *g.wires))
+                wl, wk = oracle.conj_cx(wl, wk, n, *g.wires)
+            else:
+                prog.append(lut.perm_op(n, g.wires[0], lut.FIXED_PERMS[g.gate]))
+                m = oracle.axis_map(g.gate)
+                # oracle single-gate conjugation without merge: permutation => first branch only
+                a1 = {d: int(np.nonzero(m[:, d - 1])[0][0]) + 1 for d in (1, 2, 3)}
+                sg = {d: m[a1[d] - 1, d - 1] for d in (1, 2, 3)}
+                sh = np.uint64(2 * (n - 1 - g.wires[0]))
+                d = ((wk >> sh) & np.uint64(3)).astype(np.int64)
+                newd = np.array([0, a1[1], a1[2], a1[3]], dtype=np.uint64)[d]
+                wk = (wk & ~(np.uint64(3) << sh)) | (newd << sh)
+                wl = wl * np.array([1.0, sg[1], sg[2], sg[3]])[d]
+        with DeviceStore(n, 1, 0) as st:
+            st.upload([(lam, keys)])
+            st.apply_clifford(prog)
+            (gl, gk), = st.segments()
+            assert np.array_equal(gk, wk) and np.array_equal(gl, wl)
+
+
+def test_split_and_operator_raw_match_oracle():
+    rng = np.random.default_rng(21)
+    for n in (3, 9, 16, 32):
+        lam, keys = random_terms(rng, n, 6000, 6000)
+        # v1 split on a random qubit for each rotation family
+        for gate in ("RX", "RY", "RZ"):
+            q, theta = int(rng.integers(n)), float(rng.uniform(0, 6.28))
+            out = qx.apply_1q(SimpleGenerator(n, lam, keys_to_indices(keys, n)), gate, q, theta)
+            wl0, wk0 = oracle.conj_1q_v1(lam, keys, n, q, oracle.axis_map(gate, theta))
+            assert np.array_equal(out.keys(), wk0) and np.max(np.abs(out.lambdas - wl0)) < TOL
+        # v3 operator with rotations on every qubit, few input terms (big fan-out)
+        gates = [qx.Instruction(str(rng.choice(["RX", "RY", "RZ"])), (j,), float(rng.uniform(0, 6.28))) for j in range(min(n, 10))]
+        block = oracle.lut_blocks(oracle.partition(gates, n), n)[0]
+        few = SimpleGenerator(n, lam[:5], keys_to_indices(keys[:5], n))
+        out = qx.flatten(qx.sub(few, block))
+        wl, wk = oracle.operator_v3(lam[:5], keys[:5], n, block)
+        assert np.array_equal(out.keys(), wk) and np.max(np.abs(out.lambdas - wl)) < TOL
+        counts = qx.stabilizer.branch_counts(qx.sub(few, block))
+        assert int(counts[0]) == len(oracle.expand_operator(lam[:5], keys[:5], n, block)[0])
+
+
+def test_partition_by_owner_roundtrip(golden):
+    rng = np.random.default_rng(3)
+    n, world = 14, 4
+    gens = [random_terms(rng, n, s, s) for s in (5000, 1, 70_000)] + [(np.zeros(0), np.zeros(0, dtype=np.uint64))]
+    with DeviceStore(n, len(gens), 0) as st:
+        st.upload(gens)
+        counts = st.partition_by_owner(world)
+        # owner = splitmix64(key) % world, computed independently on the host
+        for s, (lam, keys) in enumerate(gens):
+            z = keys + np.uint64(0x9E3779B97F4A7C15)
+            z = (z ^ (z >> np.uint64(30))) * np.uint64(0xBF58476D1CE4E5B9)
+            z = (z ^ (z >> np.uint64(27))) * np.uint64(0x94D049BB133111EB)
+            z = z ^ (z >> np.uint64(31))
+            owner = (z % np.uint64(world)).astype(np.int64)
+            assert [int((owner == r).sum()) for r in range(world)] == counts[:, s].tolist()
+        d_keys, d_lam, _ = st.device_view()
+        st.assemble(d_keys, d_lam, counts)          # loop-back: receive what was sent
+        back = st.segments()
+        for (bl, bk), (lam, keys) in zip(back, gens):
+            assert sorted(zip(bk.tolist(), bl.tolist())) == sorted(zip(keys.tolist(), lam.tolist()))
+
+
+def test_zi_sums_and_norms():
+    rng = np.random.default_rng(8)
+    n = 9
+    gens = [random_terms(rng, n, s, s) for s in (1, 300, 70_000)]
+    with DeviceStore(n, 3, 0) as st:
+        st.upload(gens)
+        zi, nr = st.zi_sums(), st.norms()
+    for (lam, keys), a, b in zip(gens, zi, nr):
+        mask = (((keys >> np.uint64(1)) ^ keys) & np.uint64(0x5555555555555555)) == 0
+        assert abs(a - lam[mask].sum()) < 1e-9 and abs(b - np.dot(lam, lam)) < 1e-9
