@@ -1,0 +1,357 @@
+"""bench.py -- the driver's measurement contract for the extended-stabilizer hot path.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--workload c4_xyz_16_2] [--mode v3]
+
+One "step" = one whole circuit: init_z -> every gate/operator -> final canonical generators
+(the paper's timing window).  The metric is BASELINE.json's: term-gate updates/s,
+where the update count of a circuit is sum over gates of the ranks before the gate in the
+reference's v1 semantics -- a property of the circuit, the same numerator for
+every mode and for the CPU arm.  Default workload: BASELINE's largest-rank config, the
+xyz_chain(16, 2) point of config 4 (1.25e8 final terms; the n=20, L=4 point is infeasible for
+any exact method).
+
+  value     updates/s, K steps bracketed by barrier + synchronize, CUDA events on the launch
+            stream, max over ranks; terms never leave HBM inside the timed region
+  e2e       the same through the public API run(instructions, n, mode) with host buffers: gate
+            tables go host->device and the final generators come back into pinned host memory
+  roofline  the dominant kernel (one onesweep radix pass, 32 B of algorithmic traffic per term)
+            timed per launch with CUDA events in a second, instrumented set of steps
+  cpu_baseline  the numpy oracle port on the host cores over a bounded sample (a subset of the
+            same circuit's generators -- they evolve independently), same unit
+
+N > 1 (torchrun): generators are sharded over ranks (LPT on rank), no data-path collective; the
+only NCCL traffic is the barrier and the max/sum of scalars.  --impl reference runs the CPU arm.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+from paper_2505_03307_b200 import workloads  # noqa: E402
+
+DEFAULT_WORKLOAD = "c4_xyz_16_2"
+# generator subset used as the bounded CPU sample of each workload (None = whole circuit)
+CPU_SAMPLE = {"c4_xyz_16_2": list(range(4, 16)), "c4_xyz_18_2": list(range(7, 18)),
+              "c4_xyz_14_2": list(range(2, 14))}
+
+
+def peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(path):
+        with open(path) as fh:
+            return float(json.load(fh)["hbm_gbs"]), "measured (MEASURED_PEAKS.json)"
+    return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device):
+        self.device, self.rows, self.proc = device, [], None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._pump, daemon=True)
+            self.thread.start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def _pump(self):
+        for line in self.proc.stdout:
+            self.rows.append([c.strip() for c in line.split(",")])
+
+    def __exit__(self, *exc):
+        if self.proc:
+            time.sleep(0.15)
+            self.proc.terminate()
+            self.thread.join(timeout=2)
+
+    def summary(self):
+        sm, mx, reasons = [], 0.0, set()
+        names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+        for r in self.rows:
+            try:
+                sm.append(float(r[0]))
+                mx = max(mx, float(r[1]))
+            except (ValueError, IndexError):
+                continue
+            for name, flag in zip(names, r[3:7]):
+                if flag.lower().startswith("active"):
+                    reasons.add(name)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx or None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def lpt_shards(weights, world):
+    """Longest-processing-time assignment of generators to ranks."""
+    loads, shards = [0.0] * world, [[] for _ in range(world)]
+    for g in sorted(range(len(weights)), key=lambda i: -weights[i]):
+        r = loads.index(min(loads))
+        shards[r].append(g)
+        loads[r] += weights[g]
+    return [sorted(s) for s in shards]
+
+
+# ------------------------------------------------------------------------------------------
+# CPU arm (numpy oracle port): also the cpu_baseline leg of the GPU arm
+# ------------------------------------------------------------------------------------------
+def _cpu_worker(args):
+    name, mode, gens = args
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import stabsim_port as port
+
+    n, gates = workloads.build(name)
+    t0 = time.perf_counter()
+    res = port.run(gates, n, mode, generators=gens)
+    return time.perf_counter() - t0, [len(l) for l, _ in res["final"]]
+
+
+def cpu_step(name, mode, gens, procs):
+    """One pass of the oracle over `gens`, split over `procs` processes; returns wall seconds."""
+    import multiprocessing as mp
+
+    if procs <= 1:
+        return _cpu_worker((name, mode, gens))[0]
+    # rank grows towards low generator ids on the ladder: deal them round-robin from the heavy end
+    parts = [gens[i::procs] for i in range(procs)]
+    parts = [p for p in parts if p]
+    t0 = time.perf_counter()
+    with mp.get_context("fork").Pool(len(parts)) as pool:
+        pool.map(_cpu_worker, [(name, mode, p) for p in parts])
+    return time.perf_counter() - t0
+
+
+def run_reference(args, updates_per_gen):
+    """--impl reference: the reference algorithm (oracle port) on the host cores."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    n, gates = workloads.build(args.workload)
+    gens = CPU_SAMPLE.get(args.workload) or list(range(n))
+    cores = os.cpu_count() or 1
+    procs = max(1, min(cores, len(gens)))
+    upd = float(sum(updates_per_gen[g] for g in gens))
+    for _ in range(args.warmup):
+        cpu_step(args.workload, args.mode, gens[-2:], 1)          # warm imports/pages, tiny
+    t = [cpu_step(args.workload, args.mode, gens, procs) for _ in range(args.steps)]
+    sec = sum(t) / len(t)
+    value = upd / sec
+    sample = (f"generators {gens[0]}..{gens[-1]} of {args.workload} ({len(gens)} of {n}; generators evolve "
+              f"independently), {args.mode}, numpy port of the reference (oracle/stabsim_port.py), "
+              f"{procs} processes")
+    line = {
+        "impl": "reference", "metric": "term_gate_updates_per_s", "value": value, "unit": "updates/s",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": sec * 1e3,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic", "config": {"workload": args.workload, "mode": args.mode, "sample": sample},
+        "cpu_baseline": {"value": value, "unit": "updates/s", "cores": procs, "kind": "port", "sample": sample},
+        "e2e": {"value": value, "unit": "updates/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "gpu_launches": 0,
+    }
+    print(json.dumps(line))
+
+
+# ------------------------------------------------------------------------------------------
+# GPU arm
+# ------------------------------------------------------------------------------------------
+def count_updates_gpu(name, device):
+    """v1-defined update count per generator, measured with the GPU's own v1 mode (untimed)."""
+    import paper_2505_03307_b200 as qx
+
+    n, gates = workloads.build(name)
+    rep = qx.run(gates, n, "v1", device=device, download=False)
+    rep.device["store"].close()
+    return rep.device["updates_per_generator"], rep.rank_trace[-1]
+
+
+def table_bytes(n, gates):
+    """Host->device bytes of one run: packed gate words + per-operator branch tables."""
+    from paper_2505_03307_b200 import circuit as ir
+
+    part = ir.divide_instruction(gates, n)
+    return 4 * len(gates) + part.k * n * 3 * (4 + 3 * 4 + 3 * 8)
+
+
+def run_ours(args):
+    import torch
+
+    import paper_2505_03307_b200 as qx
+    from paper_2505_03307_b200 import _native as nat
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    device = local
+    torch.cuda.set_device(device)
+    n, gates = workloads.build(args.workload)
+
+    # untimed: update counts (v1 semantics) and final ranks for LPT sharding
+    updates_per_gen, final_ranks = count_updates_gpu(args.workload, device)
+    total_updates = float(sum(updates_per_gen))
+    shards = lpt_shards(final_ranks, world)
+    mine = shards[rank]
+    my_cap = int(sum(final_ranks[g] for g in mine) * 2.6) + 1024
+
+    def barrier():
+        if dist is not None:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    def step_resident():
+        rep = qx.run(gates, n, args.mode, device=device, generators=mine, capacity=my_cap, download=False)
+        rep.device["store"].close()
+        return rep
+
+    def step_e2e():
+        return qx.run(gates, n, args.mode, device=device, generators=mine, capacity=my_cap, pinned=True)
+
+    for _ in range(max(args.warmup, 3)):
+        step_resident()
+
+    # ---- value: K steps, device-timed on the launch stream, max over ranks
+    barrier()
+    l0 = nat.launch_count()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(device) as clocks:
+        ev0.record()
+        for _ in range(args.steps):
+            step_resident()
+        ev1.record()
+        barrier()
+    ms = ev0.elapsed_time(ev1)
+    launches = nat.launch_count() - l0
+    t = torch.tensor([ms], device="cuda", dtype=torch.float64)
+    if dist is not None:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_per_step = float(t.item()) / args.steps
+    value = total_updates / (ms_per_step * 1e-3)
+
+    # ---- e2e: public API with host buffers (tables H2D, final generators D2H into pinned memory)
+    step_e2e()
+    barrier()
+    t0 = time.perf_counter()
+    reports = [step_e2e() for _ in range(args.steps)]
+    barrier()
+    e2e_s = (time.perf_counter() - t0) / args.steps
+    t = torch.tensor([e2e_s], device="cuda", dtype=torch.float64)
+    if dist is not None:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    e2e_s = float(t.item())
+    final_terms = sum(g.rank for g in reports[-1].final.generators)
+    d2h = 16 * final_terms + 8 * (len(mine) + 1)
+    del reports
+
+    # ---- roofline of the dominant kernel: instrumented steps (CUDA events around every launch)
+    nat.profile_enable(True)
+    nat.profile_reset()
+    for _ in range(max(1, min(args.steps, 3))):
+        step_resident()
+    prof = nat.profile_read()
+    nat.profile_enable(False)
+    peak, peak_src = peaks()
+    busy = {k: v for k, v in prof.items() if v["launches"]}
+    dom = max(busy, key=lambda k: busy[k]["ms"]) if busy else None
+    roof = None
+    if dom:
+        d = busy[dom]
+        achieved = d["alg_bytes"] / (d["ms"] * 1e-3) / 1e9
+        roof = {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "GB/s",
+                "frac": achieved / peak, "traffic": None, "peak_source": peak_src,
+                "launches_per_step": d["launches"] / max(1, min(args.steps, 3)),
+                "avg_launch_ms": d["ms"] / d["launches"],
+                "alg_bytes_per_launch": d["alg_bytes"] / d["launches"],
+                "classes": {k: {"ms": round(v["ms"], 4), "launches": v["launches"],
+                                "gbs": round(v["alg_bytes"] / max(v["ms"], 1e-9) / 1e6, 1)}
+                            for k, v in busy.items()}}
+        traffic_file = os.path.join(ROOT, "profiles", "traffic.json")
+        if os.path.exists(traffic_file):
+            with open(traffic_file) as fh:
+                roof["traffic"] = json.load(fh).get(dom)
+
+    if rank != 0:
+        if dist is not None:
+            dist.destroy_process_group()
+        return
+
+    # ---- cpu_baseline (rank 0, N = 1 only): oracle port on a bounded sample, one core
+    cpu = None
+    if world == 1 and not args.no_cpu:
+        gens = CPU_SAMPLE.get(args.workload) or list(range(n))
+        sec = cpu_step(args.workload, args.mode, gens, 1)
+        cpu = {"value": float(sum(updates_per_gen[g] for g in gens)) / sec, "unit": "updates/s", "cores": 1,
+               "kind": "port",
+               "sample": f"generators {gens[0]}..{gens[-1]} of {args.workload} ({len(gens)} of {n}), {args.mode}, "
+                         f"numpy port of the reference (oracle/stabsim_port.py), {sec:.1f} s on 1 core"}
+
+    line = {
+        "metric": "term_gate_updates_per_s", "value": value, "unit": "updates/s", "n_gpus": world,
+        "steps": args.steps, "warmup": max(args.warmup, 3), "ms_per_step": ms_per_step,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": args.workload, "mode": args.mode, "qubits": n, "gates": len(gates),
+                   "term_gate_updates": total_updates, "final_terms": int(sum(final_ranks)),
+                   "parallelism": f"generator shards x{world} (LPT on rank)",
+                   "l2": "inputs larger than L2: every pass streams 2-5 GB per GPU, L2 is 126 MB"},
+        "e2e": {"value": total_updates / e2e_s, "unit": "updates/s", "ms_per_step": e2e_s * 1e3,
+                "h2d_bytes_per_step": table_bytes(n, gates), "d2h_bytes_per_step": d2h},
+        "gpu_launches": launches,
+        "clocks": clocks.summary(),
+        "roofline": roof,
+        "cpu_baseline": cpu,
+    }
+    print(json.dumps(line))
+    if dist is not None:
+        dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=("ours", "reference"))
+    ap.add_argument("--workload", default=DEFAULT_WORKLOAD)
+    ap.add_argument("--mode", default="v3")
+    ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        # update counts of the sample come from the fixture table (no GPU on this arm)
+        with open(os.path.join(ROOT, "tests", "golden", "updates.json")) as fh:
+            table = json.load(fh)["data"]
+        if args.workload not in table:
+            print(json.dumps({"impl": "reference", "unavailable": f"no update table for {args.workload}"}))
+            return
+        run_reference(args, table[args.workload])
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -164,10 +164,12 @@ class PinnedBuffer:
         check(lib().qx_host_alloc(self.nbytes, C.byref(raw)))
         self._raw = raw
         self._ctype = (C.c_uint8 * max(self.nbytes, 8)).from_address(raw.value)
+        # numpy views keep the ctypes array alive; the array keeps this object alive, so the
+        # pinned block is only released once the last view is gone
+        self._ctype._qx_owner = self
 
     def view(self, dtype, offset: int, count: int) -> np.ndarray:
-        arr = np.frombuffer(self._ctype, dtype=dtype, count=count, offset=offset)
-        return arr
+        return np.frombuffer(self._ctype, dtype=dtype, count=count, offset=offset)
 
     def __del__(self):
         raw, self._raw = getattr(self, "_raw", None), None

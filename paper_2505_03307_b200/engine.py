@@ -90,14 +90,17 @@ class AgreementReport:
 class _Walker:
     """Queues sign-permutation ops and flushes them as one fused launch."""
 
-    def __init__(self, store: DeviceStore, n: int, ids, eps: float, timings: dict):
+    def __init__(self, store: DeviceStore, n: int, ids, eps: float, timings: dict,
+                 before_merge=None, reduce_ranks=None):
         self.store, self.n, self.ids, self.eps = store, n, list(ids), eps
         self.timings = timings
+        self.before_merge, self.reduce_ranks = before_merge, reduce_ranks
         self.queue: list = []
         self.queue_has_cx = False
         self.unsorted = False          # a permutation ran since the last merge
         self.ranks = [1] * len(self.ids)
         self.launch_log = {"clifford_runs": 0, "branch_ops": 0, "merges": 0}
+        self.updates = None            # v1 only: term-gate updates per generator (SURVEY.md 8d)
 
     def push_perm(self, qubit: int, table: int):
         if table != _lut.IDENTITY_PERM:
@@ -117,9 +120,13 @@ class _Walker:
         self.unsorted = True
         self.launch_log["clifford_runs"] += 1
 
-    def merge(self, step: int, phase: str):
+    def merge(self, step: int, phase: str, after_branch: bool = False):
         t0 = time.perf_counter()
+        if after_branch and self.before_merge is not None:
+            self.before_merge(self.store)      # term-partitioned runs: equal keys must meet first
         self.ranks = self.store.merge(self.eps)
+        if self.reduce_ranks is not None:
+            self.ranks = self.reduce_ranks(self.ranks)
         self.timings[phase] += time.perf_counter() - t0
         self.unsorted = False
         self.launch_log["merges"] += 1
@@ -132,7 +139,7 @@ class _Walker:
 
 def run(instructions: Sequence[Instruction], n: int, mode, eps: float = DEFAULT_EPS, *,
         device=None, generators=None, capacity: int = 0, pinned: bool = False,
-        download: bool = True, initial=None) -> RunReport:
+        download: bool = True, initial=None, before_merge=None, reduce_ranks=None) -> RunReport:
     """Simulate a circuit; returns the canonical final generator set.
 
     Positional arguments and result are the reference's (engine.py:89).  Keyword
@@ -142,7 +149,9 @@ def run(instructions: Sequence[Instruction], n: int, mode, eps: float = DEFAULT_
     (download into page-locked memory), ``download=False`` (leave the result in HBM;
     ``report.final`` is then None and ``report.device['store']`` holds the live
     store), ``initial`` (list of (lambdas, keys) replacing init_z, for read-out
-    back-propagation).
+    back-propagation), ``before_merge(store)`` / ``reduce_ranks(ranks)`` (hooks of the
+    term-partitioned multi-GPU mode, see dist.py: re-home terms before a merge that
+    follows a branching step, and turn local ranks into global ones).
     """
     mode = Mode.coerce(mode)
     timings = {"partition": 0.0, "lut": 0.0, "sub_flatten": 0.0, "cx": 0.0}
@@ -171,8 +180,8 @@ def run(instructions: Sequence[Instruction], n: int, mode, eps: float = DEFAULT_
             store.init_z(ids)
             walker_ranks = [1] * len(ids)
             min_abs = 1.0
-        w = _Walker(store, n, ids, eps, timings)
-        w.ranks = walker_ranks
+        w = _Walker(store, n, ids, eps, timings, before_merge, reduce_ranks)
+        w.ranks = reduce_ranks(walker_ranks) if reduce_ranks is not None else walker_ranks
         # If eps could already drop an initial term, merge after every step like the
         # reference does; otherwise deferring the re-sort of permutation steps is exact.
         eager = eps > min_abs
@@ -194,6 +203,8 @@ def run(instructions: Sequence[Instruction], n: int, mode, eps: float = DEFAULT_
         counters["operators"] = partition.k + partition.k_prime
 
         info = {"device": store.device, **w.launch_log}
+        if w.updates is not None:
+            info["updates_per_generator"] = w.updates.tolist()
         final = None
         if download:
             segs = store.segments(pinned)
@@ -223,7 +234,9 @@ def _walk_v1(instructions, partition, w: _Walker, trace, counters, eager):
     """Gate by gate (reference engine.py:155-180): rank snapshots at operator boundaries."""
     n = w.n
     boundaries = set(np.cumsum(partition.operator_sizes()).tolist())
+    w.updates = np.zeros(len(w.ids), dtype=np.int64)
     for pos, inst in enumerate(instructions, start=1):
+        w.updates += np.asarray(w.ranks, dtype=np.int64)      # terms present before this gate
         if inst.is_two_qubit:
             w.push_cx(*inst.wires)
             counters["cx_applications"] += 1
@@ -248,7 +261,7 @@ def _walk_v1(instructions, partition, w: _Walker, trace, counters, eager):
                 w.store.apply_split(q, *split_tables(block))
                 w.timings["sub_flatten"] += time.perf_counter() - t0
                 w.launch_log["branch_ops"] += 1
-                w.merge(pos - 1, "sub_flatten")
+                w.merge(pos - 1, "sub_flatten", after_branch=True)
             counters["v1_gate_applications"] = counters.get("v1_gate_applications", 0) + 1
         if pos in boundaries:
             trace.append(list(w.ranks))
@@ -282,7 +295,7 @@ def _walk_operators(partition, lut, is_perm, tables, w: _Walker, trace, counters
                 w.store.apply_operator(counts, axes, weights)
                 w.timings["sub_flatten"] += time.perf_counter() - t0
                 w.launch_log["branch_ops"] += 1
-                w.merge(step, "sub_flatten")
+                w.merge(step, "sub_flatten", after_branch=True)
             counters["sub_flatten_ops"] += 1
             ui += 1
         else:

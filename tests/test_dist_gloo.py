@@ -1,0 +1,117 @@
+"""Host-side multi-GPU logic on CPU: world_size 2, gloo backend.
+
+The compute kernels need a GPU, so the per-rank ``runner`` is replaced by a fake that answers
+from the CPU oracle (test infrastructure); what is under test is the plumbing that has no GPU
+in it: LPT sharding, gathering rank traces and ragged generators, and the all-to-all-v of
+hash-partitioned terms with its [source][segment] layout contract."""
+
+import os
+import socket
+import sys
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, os.path.join(HERE, "..", "oracle"))
+sys.path.insert(0, os.path.join(HERE, ".."))
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _fake_runner(instructions, n, mode, eps=1e-12, *, generators=None, **kw):
+    """engine.run look-alike backed by the oracle (only for exercising dist.py on CPU)."""
+    import stabsim_port as port
+
+    from paper_2505_03307_b200.engine import Mode, RunReport, _Shard
+    from paper_2505_03307_b200.stabilizer import SimpleGenerator, keys_to_indices
+
+    res = port.run(instructions, n, mode, eps, generators=generators)
+    gens = [SimpleGenerator(n, lam, keys_to_indices(idx, n)) for lam, idx in res["final"]]
+    return RunReport(Mode.coerce(mode), n, _Shard(n, list(generators), gens), res["rank_trace"], {},
+                     res["counters"], res["k"], res["k_prime"], res["order"])
+
+
+def _worker(rank, world, port, out_dir):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import stabsim_port as oracle
+
+        from paper_2505_03307_b200 import dist as qd
+        from paper_2505_03307_b200 import workloads
+
+        # ---- generator-sharded run, LPT on skewed weights
+        n, gates = 8, workloads.gen_xyz_chain(8, 2, 1, 4)
+        weights = [4 ** (n - g) for g in range(n)]
+        report, shards = qd.run_sharded(gates, n, "v3", weights=weights, runner=_fake_runner)
+        assert sorted(g for s in shards for g in s) == list(range(n))
+        want = oracle.run(gates, n, "v3")
+        assert report.rank_trace == want["rank_trace"]
+        for g, (lam, idx) in zip(report.final.generators, want["final"]):
+            assert np.array_equal(g.keys(), idx) and np.array_equal(g.lambdas, lam)
+
+        # ---- more ranks than generators with work: an empty shard must not deadlock
+        report, shards = qd.run_sharded(workloads.gen_ghz(1) if False else [], 1, "v1", runner=_fake_runner)
+        assert report.rank_trace == [[1]] and int(report.final.generators[0].indices[0]) == 3
+
+        # ---- all-to-all-v of hash-partitioned terms
+        rng = np.random.default_rng(100 + rank)
+        n_seg = 3
+        segs = [rng.integers(0, 4 ** 10, size=s, dtype=np.uint64) for s in (50 + 7 * rank, 0, 400)]
+        lams = [rng.uniform(-1, 1, size=len(k)) for k in segs]
+        counts = np.zeros((world, n_seg), dtype=np.int64)
+        send_k, send_l = [], []
+        for r in range(world):                      # what the device partition kernel produces
+            for s in range(n_seg):
+                sel = qd.owner_of(segs[s], world) == r
+                counts[r, s] = int(sel.sum())
+                send_k.append(segs[s][sel])
+                send_l.append(lams[s][sel])
+        keys = torch.from_numpy(np.concatenate(send_k).view(np.int64))
+        lam = torch.from_numpy(np.concatenate(send_l))
+        rk, rl, rc = qd.exchange_partitioned(keys, lam, counts)
+        assert rc.shape == (world, n_seg) and int(rc.sum()) == len(rk) == len(rl)
+        got = rk.numpy().view(np.uint64)
+        assert np.all(qd.owner_of(got, world) == rank)          # I only hold what I own
+        np.save(os.path.join(out_dir, f"sent_{rank}.npy"), np.concatenate(segs))
+        np.save(os.path.join(out_dir, f"recv_{rank}.npy"), got)
+        np.save(os.path.join(out_dir, f"rc_{rank}.npy"), rc)
+        np.save(os.path.join(out_dir, f"sc_{rank}.npy"), counts)
+    finally:
+        dist.destroy_process_group()
+
+
+def test_world2_gloo(tmp_path):
+    world = 2
+    mp.spawn(_worker, args=(world, _free_port(), str(tmp_path)), nprocs=world, join=True)
+    sent = np.concatenate([np.load(tmp_path / f"sent_{r}.npy") for r in range(world)])
+    recv = np.concatenate([np.load(tmp_path / f"recv_{r}.npy") for r in range(world)])
+    assert sorted(sent.tolist()) == sorted(recv.tolist())        # nothing lost, nothing duplicated
+    for r in range(world):                                        # recv_counts[q] on r == send_counts[r] on q
+        rc = np.load(tmp_path / f"rc_{r}.npy")
+        for q in range(world):
+            assert np.array_equal(rc[q], np.load(tmp_path / f"sc_{q}.npy")[r])
+
+
+def test_lpt_shards_balance():
+    from paper_2505_03307_b200.dist import lpt_shards, owner_of
+
+    ranks = [41737064, 55284529, 18866855, 6353359, 2125649, 708223, 236205, 78732, 26253, 8757, 2925, 981,
+             333, 117, 45, 12]                                    # xyz_chain(16, 2) final ranks
+    for world in (1, 2, 4, 8):
+        shards = lpt_shards(ranks, world)
+        assert sorted(g for s in shards for g in s) == list(range(16))
+        loads = [sum(ranks[g] for g in s) for s in shards]
+        assert max(loads) <= max(max(ranks), sum(ranks) / world * 1.34)
+    assert lpt_shards([1, 1, 1], 5)[3:] == [[], []]
+    keys = np.arange(100000, dtype=np.uint64) * np.uint64(2654435761)
+    share = np.bincount(owner_of(keys, 8), minlength=8) / len(keys)
+    assert np.all(np.abs(share - 0.125) < 0.01)

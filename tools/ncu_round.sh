@@ -1,0 +1,15 @@
+#!/bin/bash
+# ncu evidence for one round: launch list at full size + full captures of the hot kernels at (14,2)
+R=${1:-r01}
+mkdir -p gpurun_out
+ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/${R}_launches_c4_16_2.csv \
+    python tools/profile_step.py --workload c4_xyz_16_2 --mode v3 --warmup 1 --steps 1 > gpurun_out/${R}_launches.log 2>&1
+for k in k_onesweep k_expand_emit k_reduce k_clifford_run k_sort_hist; do
+  skip=8; cnt=2
+  [ $k != k_onesweep ] && skip=2 && cnt=1
+  timeout 900 ncu --set full --clock-control none --import-source on -k regex:$k -s $skip -c $cnt -f \
+      -o gpurun_out/${R}_${k} python tools/profile_step.py --workload c4_xyz_14_2 --mode v3 --warmup 1 --steps 1 \
+      > gpurun_out/${R}_${k}.log 2>&1
+  echo "$k rc=$?"
+done
+ls -la gpurun_out | tail -20
