@@ -58,6 +58,8 @@ int qx_device_info(int device, char* name, int name_cap, int* sm_count, int* cc_
 /* Page-locked host buffers so uploads/downloads run at full PCIe rate (optional). */
 int qx_host_alloc(int64_t bytes, void** out);
 int qx_host_free(void* ptr);
+/* Return the library's cached (freed but retained) device blocks to the driver. */
+int qx_trim(void);
 
 /* ---- a1: term store (stabilizer.py:83-109 SimpleGenerator, :157-174 GeneratorSet/init_z) */
 int qx_store_create(int device, int n_qubits, int n_segments, int64_t capacity_terms,
@@ -121,6 +123,11 @@ int qx_count_operator(qx_store* s, const int32_t* counts, int64_t* raw_per_segme
  * Per segment: stable sort by key, in-order segmented sum, keep |sum| >= eps,
  * ascending.  ranks (may be NULL) receives the new per-segment counts. */
 int qx_merge(qx_store* s, double eps, int64_t* ranks);
+/* Canonical order only: stable sort of every segment by key, nothing summed or dropped.
+ * What canonicalize amounts to after Clifford gates (a bijection on words that keeps
+ * |lambda|): term counts are unchanged, so nothing is read back.  Precondition: keys are
+ * unique inside each segment (with duplicates, use qx_merge). */
+int qx_sort(qx_store* s);
 
 /* ---- north-star kernel (4): per segment, sum of lambda over Z/I-only words. */
 int qx_store_zi_sums(qx_store* s, double* sums);

@@ -39,6 +39,7 @@ SIGNATURES = {
                                  _P(_i64), _P(_i64)]),
     "qx_host_alloc": (C.c_int, [_i64, _P(_p)]),
     "qx_host_free": (C.c_int, [_p]),
+    "qx_trim": (C.c_int, []),
     "qx_store_create": (C.c_int, [C.c_int, C.c_int, C.c_int, _i64, _P(_p)]),
     "qx_store_destroy": (C.c_int, [_p]),
     "qx_store_set_stream": (C.c_int, [_p, _p]),
@@ -54,6 +55,7 @@ SIGNATURES = {
     "qx_apply_operator": (C.c_int, [_p, _p, _p, _p, _i64, _P(_i64)]),
     "qx_count_operator": (C.c_int, [_p, _p, _p]),
     "qx_merge": (C.c_int, [_p, _f64, _p]),
+    "qx_sort": (C.c_int, [_p]),
     "qx_store_zi_sums": (C.c_int, [_p, _p]),
     "qx_store_norms": (C.c_int, [_p, _p]),
     "qx_expansion_create": (C.c_int, [C.c_int, C.c_int, _i64, _P(_p)]),
@@ -180,6 +182,32 @@ class PinnedBuffer:
                 pass
 
 
+class PinnedPool:
+    """Reuses page-locked blocks across downloads: pinning gigabytes costs far more than the
+    copy itself.  A block is handed out again only when no numpy view of it is alive."""
+
+    def __init__(self, keep: int = 4):
+        self.keep, self.blocks = keep, []
+
+    def take(self, nbytes: int) -> PinnedBuffer:
+        import sys
+
+        best = None
+        for blk in self.blocks:
+            idle = sys.getrefcount(blk._ctype) <= 2          # blk._ctype + getrefcount's argument
+            if idle and blk.nbytes >= nbytes and (best is None or blk.nbytes < best.nbytes):
+                best = blk
+        if best is None:
+            best = PinnedBuffer(nbytes + nbytes // 16)
+            self.blocks.append(best)
+            if len(self.blocks) > self.keep:                 # forget the oldest; it frees itself
+                self.blocks.pop(0)                           # once its last view is gone
+        return best
+
+
+PINNED = PinnedPool()
+
+
 def profile_enable(on: bool = True) -> None:
     check(lib().qx_profile_enable(1 if on else 0))
 
@@ -196,6 +224,11 @@ def profile_read() -> dict:
         check(lib().qx_profile_read(i, C.byref(n), C.byref(ms), C.byref(by)))
         out[name] = {"launches": n.value, "ms": ms.value, "alg_bytes": by.value}
     return out
+
+
+def trim() -> None:
+    """Give cached device blocks back to the driver."""
+    check(lib().qx_trim())
 
 
 def launch_count() -> int:

@@ -173,9 +173,6 @@ __global__ void k_gather_offsets(const int64_t* __restrict__ seg_in, int n_seg,
   if (g <= n_seg) seg_out[g] = (int64_t)roff[seg_in[g]];
 }
 
-constexpr int kEmitItems = 8;
-constexpr int kEmitTile = kThreads * kEmitItems;
-
 // index of the last entry <= r in a strictly increasing array a[0..n)
 __device__ __forceinline__ int64_t last_le(const u64* a, int64_t n, u64 r) {
   int64_t lo = 0, hi = n;                  // a[lo] <= r < a[hi] (a[n] = +inf)
@@ -186,12 +183,121 @@ __device__ __forceinline__ int64_t last_le(const u64* a, int64_t n, u64 r) {
   return lo;
 }
 
+// One source term being enumerated: a mixed-radix counter over its non-identity digits.
+// The two least significant digits are advanced in registers; everything above them is
+// folded once into (p_hi, k_hi) and only recomputed when a carry leaves the low pair, i.e.
+// every c0*c1 outputs.  The product order stays the reference's: ((lambda * w_top ...) * w1) * w0.
+struct Branch {
+  u64 key;        // source word
+  u64 hi_mask;    // support bits above the low pair
+  u64 choice;     // current pick of every digit, 2 bits at the digit's position
+  u64 k_hi;       // output word assembled from the high digits
+  double lam;     // source coefficient
+  double p_hi;    // lam * product of the high digits' weights, qubit 0 first
+  int bit0, bit1; // positions of the two lowest support digits (-1 if absent)
+  u32 c0, c1;     // their radices
+};
+
+__device__ __forceinline__ void fold_high(Branch& br, const OperatorTable& tb) {
+  double v = br.lam;
+  u64 out = 0;
+  for (u64 m = br.hi_mask; m;) {
+    const int bit = 63 - __clzll((long long)m);
+    m ^= 1ull << bit;
+    const u32 d = (u32)((br.key >> bit) & 3ull) - 1u;
+    const u32 pick = (u32)(br.choice >> bit) & 3u;
+    v *= tb.w[bit >> 1][d][pick];
+    out |= (u64)tb.axis[bit >> 1][d][pick] << bit;
+  }
+  br.p_hi = v;
+  br.k_hi = out;
+}
+
+// position the counter of source (key, lam) at branch id b
+__device__ __forceinline__ void seek(Branch& br, u64 key, double lam, u64 b, const OperatorTable& tb) {
+  br.key = key;
+  br.lam = lam;
+  u64 m = support_mask(key);
+  br.bit0 = br.bit1 = -1;
+  br.c0 = br.c1 = 1;
+  if (m) {
+    br.bit0 = __ffsll((long long)m) - 1;
+    br.c0 = tb.cnt[br.bit0 >> 1][((key >> br.bit0) & 3ull) - 1];
+    m &= m - 1;
+  }
+  if (m) {
+    br.bit1 = __ffsll((long long)m) - 1;
+    br.c1 = tb.cnt[br.bit1 >> 1][((key >> br.bit1) & 3ull) - 1];
+    m &= m - 1;
+  }
+  br.hi_mask = m;
+  u64 choice = 0;
+  for (u64 mm = support_mask(key); mm;) {          // least significant digit first
+    const int bit = __ffsll((long long)mm) - 1;
+    mm &= mm - 1;
+    const u32 c = tb.cnt[bit >> 1][((key >> bit) & 3ull) - 1];
+    u32 pick = 0;
+    if (c == 2) { pick = (u32)(b & 1ull); b >>= 1; }
+    else if (c == 3) { const u64 q = b / 3ull; pick = (u32)(b - 3ull * q); b = q; }
+    choice |= (u64)pick << bit;
+  }
+  br.choice = choice;
+  fold_high(br, tb);
+}
+
+__device__ __forceinline__ void emit_one(const Branch& br, const OperatorTable& tb, u64& out_key,
+                                         double& out_lam) {
+  double v = br.p_hi;
+  u64 k = br.k_hi;
+  if (br.bit1 >= 0) {
+    const u32 d = (u32)((br.key >> br.bit1) & 3ull) - 1u, pick = (u32)(br.choice >> br.bit1) & 3u;
+    v *= tb.w[br.bit1 >> 1][d][pick];
+    k |= (u64)tb.axis[br.bit1 >> 1][d][pick] << br.bit1;
+  }
+  if (br.bit0 >= 0) {
+    const u32 d = (u32)((br.key >> br.bit0) & 3ull) - 1u, pick = (u32)(br.choice >> br.bit0) & 3u;
+    v *= tb.w[br.bit0 >> 1][d][pick];
+    k |= (u64)tb.axis[br.bit0 >> 1][d][pick] << br.bit0;
+  }
+  out_key = k;
+  out_lam = v;
+}
+
+// next branch of the same source (caller guarantees there is one)
+__device__ __forceinline__ void advance(Branch& br, const OperatorTable& tb) {
+  if (br.bit0 >= 0) {
+    const u32 p0 = (u32)(br.choice >> br.bit0) & 3u;
+    if (p0 + 1 < br.c0) { br.choice += 1ull << br.bit0; return; }
+    br.choice &= ~(3ull << br.bit0);
+  }
+  if (br.bit1 >= 0) {
+    const u32 p1 = (u32)(br.choice >> br.bit1) & 3u;
+    if (p1 + 1 < br.c1) { br.choice += 1ull << br.bit1; return; }
+    br.choice &= ~(3ull << br.bit1);
+  }
+  for (u64 m = br.hi_mask; m;) {                   // carry into the high digits
+    const int bit = __ffsll((long long)m) - 1;
+    m &= m - 1;
+    const u32 c = tb.cnt[bit >> 1][((br.key >> bit) & 3ull) - 1];
+    const u32 p = (u32)(br.choice >> bit) & 3u;
+    if (p + 1 < c) { br.choice += 1ull << bit; break; }
+    br.choice &= ~(3ull << bit);
+  }
+  fold_high(br, tb);
+}
+
+constexpr int kEmitPer = 8;                         // consecutive outputs per thread
+constexpr int kEmitTile = kThreads * kEmitPer;
+
+// One thread produces kEmitPer CONSECUTIVE raw terms (64 B of keys + 64 B of coefficients,
+// written with 128-bit stores): consecutive branch ids differ only in their low digits, so
+// the per-term work is two table look-ups and two multiplies instead of a full decode.
 __global__ void __launch_bounds__(kThreads)
 k_expand_emit(const u64* __restrict__ keys_in, const double* __restrict__ lam_in,
               const u64* __restrict__ roff, int64_t total_in, u64* __restrict__ keys_out,
               double* __restrict__ lam_out, const __grid_constant__ OperatorTable tb) {
   __shared__ OperatorTable s_tb;
-  __shared__ u64 s_win[kEmitTile + 1];
+  __shared__ u64 s_win[kEmitTile + 2];
   __shared__ int64_t s_lohi[2];
   {
     const u32* src = reinterpret_cast<const u32*>(&tb);
@@ -209,41 +315,47 @@ k_expand_emit(const u64* __restrict__ keys_in, const double* __restrict__ lam_in
     __syncthreads();
     const int64_t lo = s_lohi[0], hi = s_lohi[1];
     const int span = (int)(hi - lo) + 1;                          // source terms feeding this tile
-    for (int i = threadIdx.x; i < span; i += kThreads) s_win[i] = roff[lo + i];
+    for (int i = threadIdx.x; i <= span; i += kThreads) s_win[i] = roff[lo + i];   // + end sentinel
     __syncthreads();
-#pragma unroll 2
-    for (int k = 0; k < kEmitItems; ++k) {
-      const u64 r = r0 + (u64)k * kThreads + threadIdx.x;
-      if (r >= r1) break;
-      const int rel = (int)last_le(s_win, span, r);
-      const int64_t src = lo + rel;
-      const u64 key = keys_in[src];
-      u64 b = r - s_win[rel];
-      // pass 1, least significant digit first: peel one mixed-radix digit per non-identity qubit
-      u64 m = support_mask(key);
-      u64 choice = 0;                                            // 2 bits per digit position
-      for (u64 mm = m; mm;) {
-        const int bit = __ffsll((long long)mm) - 1;
-        mm &= mm - 1;
-        const u32 c = s_tb.cnt[bit >> 1][((key >> bit) & 3ull) - 1];
-        u32 pick = 0;
-        if (c == 2) { pick = (u32)(b & 1ull); b >>= 1; }
-        else if (c == 3) { const u64 q = b / 3ull; pick = (u32)(b - 3ull * q); b = q; }
-        choice |= (u64)pick << bit;
+    const u64 rbeg = r0 + (u64)threadIdx.x * kEmitPer;
+    if (rbeg >= r1) continue;
+    const int todo = (int)min((u64)kEmitPer, r1 - rbeg);
+    int rel = (int)last_le(s_win, span, rbeg);
+    Branch br;
+    seek(br, keys_in[lo + rel], lam_in[lo + rel], rbeg - s_win[rel], s_tb);
+    u64 left = s_win[rel + 1] - rbeg;                             // branches left in this source
+    u64 ok[kEmitPer];
+    double ov[kEmitPer];
+#pragma unroll
+    for (int k = 0; k < kEmitPer; ++k) {
+      if (k < todo) {
+        emit_one(br, s_tb, ok[k], ov[k]);
+        if (k + 1 < todo) {
+          if (--left == 0) {
+            ++rel;
+            seek(br, keys_in[lo + rel], lam_in[lo + rel], 0ull, s_tb);
+            left = s_win[rel + 1] - s_win[rel];
+          } else {
+            advance(br, s_tb);
+          }
+        }
       }
-      // pass 2, qubit 0 first: multiply weights in the reference's order, assemble the word
-      double v = lam_in[src];
-      u64 out = 0;
-      while (m) {
-        const int bit = 63 - __clzll((long long)m);
-        m ^= 1ull << bit;
-        const u32 d = (u32)((key >> bit) & 3ull) - 1u;
-        const u32 pick = (u32)(choice >> bit) & 3u;
-        v *= s_tb.w[bit >> 1][d][pick];
-        out |= (u64)s_tb.axis[bit >> 1][d][pick] << bit;
+    }
+    if (todo == kEmitPer) {
+      ulonglong2* kp = reinterpret_cast<ulonglong2*>(keys_out + rbeg);
+      double2* vp = reinterpret_cast<double2*>(lam_out + rbeg);
+#pragma unroll
+      for (int k = 0; k < kEmitPer; k += 2) {
+        __stcs(kp + (k >> 1), make_ulonglong2(ok[k], ok[k + 1]));
+        __stcs(vp + (k >> 1), make_double2(ov[k], ov[k + 1]));
       }
-      st_stream(keys_out + r, out);
-      st_stream(lam_out + r, v);
+    } else {
+#pragma unroll
+      for (int k = 0; k < kEmitPer; ++k)
+        if (k < todo) {
+          keys_out[rbeg + k] = ok[k];
+          lam_out[rbeg + k] = ov[k];
+        }
     }
   }
 }

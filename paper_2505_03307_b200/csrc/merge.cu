@@ -5,7 +5,7 @@
 
 namespace {
 
-int run_merge(qx_store* s, double eps) {
+int run_merge(qx_store* s, double eps, bool sort_only) {
   if (s->ub_seg > QX_SMALL_MAX && !s->exact) QX_TRY(qx_store_refresh(s));
   // both paths write into the other buffer; make sure it can hold the raw terms
   qxm::MergeBuffers<double> mb;
@@ -22,7 +22,11 @@ int run_merge(qx_store* s, double eps) {
   if (small) {
     QX_TRY(qxm::merge_small<double>(s, mb, eps, QX_K_SMALL_MERGE));
   } else {
-    QX_TRY(qxm::merge_large<double>(s, mb, eps, QX_K_REDUCE));
+    QX_TRY(qxm::merge_large<double>(s, mb, eps, QX_K_REDUCE, !sort_only));
+    if (sort_only) {            // a permutation inside each segment: sizes are what they were
+      s->cur = mb.cur;
+      return QX_OK;
+    }
   }
   s->cur = mb.cur;
   s->exact = false;
@@ -102,10 +106,16 @@ extern "C" int qx_merge(qx_store* s, double eps, int64_t* ranks) {
   QX_REQUIRE(s != nullptr, "store is NULL");
   QX_REQUIRE(eps >= 0.0, "eps must be non-negative");
   QX_CUDA(cudaSetDevice(s->device));
-  QX_TRY(run_merge(s, eps));
+  QX_TRY(run_merge(s, eps, false));
   if (ranks)
     for (int g = 0; g < s->n_seg; ++g) ranks[g] = s->h_seg[g + 1] - s->h_seg[g];
   return QX_OK;
+}
+
+extern "C" int qx_sort(qx_store* s) {
+  QX_REQUIRE(s != nullptr, "store is NULL");
+  QX_CUDA(cudaSetDevice(s->device));
+  return run_merge(s, 0.0, true);
 }
 
 extern "C" int qx_store_zi_sums(qx_store* s, double* sums) { return segment_reduce<0>(s, sums); }

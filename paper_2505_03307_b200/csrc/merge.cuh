@@ -51,12 +51,12 @@ constexpr u32 kFlagVal = (1u << 30) - 1;
 // ---------------------------------------------------------------------------------
 // tile_prefix[g] = sort tiles owned by segments before g; [n_seg] = total tiles.
 static __global__ void k_sort_plan(const int64_t* __restrict__ seg, int n_seg,
-                            int64_t* __restrict__ tile_prefix, u32* ticket) {
+                                   int64_t* __restrict__ tile_prefix, u32* ticket, int tile_terms) {
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     int64_t run = 0;
     for (int g = 0; g < n_seg; ++g) {
       tile_prefix[g] = run;
-      run += (seg[g + 1] - seg[g] + kSortTile - 1) / kSortTile;
+      run += (seg[g + 1] - seg[g] + tile_terms - 1) / tile_terms;
     }
     tile_prefix[n_seg] = run;
     *ticket = 0u;
@@ -80,7 +80,8 @@ constexpr int kMaxPasses = 8;
 
 static __global__ void __launch_bounds__(kSortThreads)
 k_sort_hist(const u64* __restrict__ keys, const int64_t* __restrict__ seg, int n_seg,
-            const int64_t* __restrict__ tile_prefix, u32* __restrict__ hist, int passes) {
+            const int64_t* __restrict__ tile_prefix, u32* __restrict__ hist, int passes,
+            int tile_terms) {
   __shared__ u32 sh[kMaxPasses][QX_RADIX];
   for (int i = threadIdx.x; i < kMaxPasses * QX_RADIX; i += kSortThreads) (&sh[0][0])[i] = 0u;
   __syncthreads();
@@ -100,10 +101,11 @@ k_sort_hist(const u64* __restrict__ keys, const int64_t* __restrict__ seg, int n
       }
       cur_g = g;
     }
-    const int64_t start = seg[g] + (tile - tile_prefix[g]) * kSortTile;
-    const int count = (int)min((int64_t)kSortTile, seg[g + 1] - start);
+    const int64_t start = seg[g] + (tile - tile_prefix[g]) * tile_terms;
+    const int count = (int)min((int64_t)tile_terms, seg[g + 1] - start);
+    const int rounds = (count + kSortThreads - 1) / kSortThreads;
 #pragma unroll 4
-    for (int k = 0; k < kSortItems; ++k) {
+    for (int k = 0; k < rounds; ++k) {
       const int idx = k * kSortThreads + threadIdx.x;
       const bool live = idx < count;
       const u64 key = live ? ld_stream(keys + start + idx) : 0ull;
@@ -143,69 +145,95 @@ static __global__ void __launch_bounds__(QX_RADIX) k_sort_scan_hist(u32* __restr
 // ---------------------------------------------------------------------------------
 // one onesweep pass
 // ---------------------------------------------------------------------------------
-template <typename V>
+template <typename V, int THREADS, int ITEMS>
 struct SortSmem {
-  u32 whist[kSortWarps][QX_RADIX];   // per-warp digit counters -> exclusive warp offsets
-  u32 tile_start[QX_RADIX];          // first slot of each digit in the tile-sorted order
-  int64_t gbase[QX_RADIX];           // global index of slot 0 of each digit, minus tile_start
-  u32 scan[kSortWarps + 1];
+  u32 whist[THREADS / 32][QX_RADIX];  // per-warp digit counters -> exclusive warp offsets
+  u32 tile_start[QX_RADIX];           // first slot of each digit in the tile-sorted order
+  int64_t gbase[QX_RADIX];            // global index of slot 0 of each digit, minus tile_start
+  u32 scan[THREADS / 32 + 1];
   int tile;
-  u64 keys[kSortTile];
-  V vals[kSortTile];
+  u64 keys[THREADS * ITEMS];
+  V vals[THREADS * ITEMS];
 };
 
-template <typename V>
-__global__ void __launch_bounds__(kSortThreads)
+// THREADS x ITEMS terms per tile, warp-striped.  EARLY: issue the coefficient loads right
+// after ranking so their HBM latency hides behind the digit scan and the look-back instead
+// of being exposed before the shared-memory scatter (costs ITEMS * sizeof(V) / 4 registers).
+template <typename V, int THREADS, int ITEMS, bool EARLY>
+__global__ void __launch_bounds__(THREADS)
 k_onesweep(const u64* __restrict__ keys_in, const V* __restrict__ vals_in,
            u64* __restrict__ keys_out, V* __restrict__ vals_out,
            const int64_t* __restrict__ seg, int n_seg, const int64_t* __restrict__ tile_prefix,
            const u32* __restrict__ digit_base, int base_stride, u32* status, u32* ticket, int shift) {
+  constexpr int WARPS = THREADS / 32;
+  constexpr int TILE = THREADS * ITEMS;
+  static_assert(THREADS >= QX_RADIX, "one thread per digit in the scan");
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  SortSmem<V>& sm = *reinterpret_cast<SortSmem<V>*>(smem_raw);
+  SortSmem<V, THREADS, ITEMS>& sm = *reinterpret_cast<SortSmem<V, THREADS, ITEMS>*>(smem_raw);
   const int tid = threadIdx.x, warp = tid >> 5, lane = lane_id();
 
   if (tid == 0) sm.tile = (int)atomicAdd(ticket, 1u);
-  for (int i = tid; i < kSortWarps * QX_RADIX; i += kSortThreads) (&sm.whist[0][0])[i] = 0u;
+  for (int i = tid; i < WARPS * QX_RADIX; i += THREADS) (&sm.whist[0][0])[i] = 0u;
   __syncthreads();
   const int64_t tile = sm.tile;
   if (tile >= tile_prefix[n_seg]) return;
   const int g = tile_segment(tile_prefix, n_seg, tile);
   const bool first = tile == tile_prefix[g];
-  const int64_t start = seg[g] + (tile - tile_prefix[g]) * kSortTile;
-  const int count = (int)min((int64_t)kSortTile, seg[g + 1] - start);
+  const int64_t start = seg[g] + (tile - tile_prefix[g]) * TILE;
+  const int count = (int)min((int64_t)TILE, seg[g + 1] - start);
 
   // ---- load, warp-striped: warp w owns tile slots [w*32*ITEMS, (w+1)*32*ITEMS)
-  u64 key[kSortItems];
-  u32 rank[kSortItems];
-  const int wslot = warp * (32 * kSortItems) + lane;
+  u64 key[ITEMS];
+  u32 rank[ITEMS];
+  const int wslot = warp * (32 * ITEMS) + lane;
 #pragma unroll
-  for (int k = 0; k < kSortItems; ++k) {
+  for (int k = 0; k < ITEMS; ++k) {
     const int idx = wslot + k * 32;
     key[k] = idx < count ? ld_stream(keys_in + start + idx) : ~0ull;   // padding sorts last
   }
-  // ---- rank inside the warp: lanes with equal digits form a group, the lowest lane
-  // bumps the warp's counter by the group size, everyone takes old + position in group
+  // ---- rank inside the warp.  Lanes with equal digits form a group; the group mask comes
+  // from 8 ballots (one per digit bit) -- the MATCH instruction costs one trip through the
+  // ADU pipe per distinct value and made this kernel latency-bound (profiles/r01).  The
+  // lowest lane of each group bumps the warp's digit counter with ONE shared-memory atomic
+  // and everyone takes old + position in group.  __syncwarp orders item k's update before
+  // item k+1's (different lanes may lead), which is what makes the ranking stable; the
+  // broadcast of `old` is deferred so the ballot groups pipeline.
+  u32 meta[ITEMS];                           // leader lane | lanes below me << 5
 #pragma unroll
-  for (int k = 0; k < kSortItems; ++k) {
+  for (int k = 0; k < ITEMS; ++k) {
     const u32 d = (u32)(key[k] >> shift) & (QX_RADIX - 1);
-    const u32 peers = __match_any_sync(QX_FULL_MASK, d);
+    u32 peers = QX_FULL_MASK;
+#pragma unroll
+    for (int b = 0; b < QX_RADIX_BITS; ++b) {
+      const bool bit = (d >> b) & 1u;
+      const u32 votes = __ballot_sync(QX_FULL_MASK, bit);
+      peers &= bit ? votes : ~votes;
+    }
     const u32 below = __popc(peers & lanemask_lt());
     u32 old = 0;
-    if (below == 0) {
-      old = sm.whist[warp][d];
-      sm.whist[warp][d] = old + __popc(peers);
-    }
-    old = __shfl_sync(QX_FULL_MASK, old, __ffs(peers) - 1);
-    rank[k] = old + below;
+    if (below == 0) old = atomicAdd(&sm.whist[warp][d], (u32)__popc(peers));
+    rank[k] = old;
+    meta[k] = (u32)(__ffs(peers) - 1) | (below << 5);
     __syncwarp();
   }
+  V val[EARLY ? ITEMS : 1];
+  if (EARLY) {
+#pragma unroll
+    for (int k = 0; k < ITEMS; ++k) {
+      const int idx = wslot + k * 32;
+      if (idx < count) val[EARLY ? k : 0] = ld_stream(vals_in + start + idx);
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < ITEMS; ++k)
+    rank[k] = __shfl_sync(QX_FULL_MASK, rank[k], meta[k] & 31u) + (meta[k] >> 5);
   __syncthreads();
 
   // ---- per digit: exclusive offsets over warps, tile totals, exclusive scan over digits
   u32 digit_total = 0;
   if (tid < QX_RADIX) {
 #pragma unroll
-    for (int w = 0; w < kSortWarps; ++w) {
+    for (int w = 0; w < WARPS; ++w) {
       const u32 c = sm.whist[w][tid];
       sm.whist[w][tid] = digit_total;
       digit_total += c;
@@ -216,7 +244,7 @@ k_onesweep(const u64* __restrict__ keys_in, const V* __restrict__ vals_in,
   if (tid < QX_RADIX) {
     sm.tile_start[tid] = dstart;
     // padding keys all carry digit 255 and sit behind the live ones
-    const u32 live_total = digit_total - ((tid == QX_RADIX - 1) ? (u32)(kSortTile - count) : 0u);
+    const u32 live_total = digit_total - ((tid == QX_RADIX - 1) ? (u32)(TILE - count) : 0u);
     // ---- decoupled look-back, one chain per digit, confined to this segment's tiles
     u32* mine = status + (size_t)tile * QX_RADIX + tid;
     u32 excl = 0;
@@ -241,22 +269,22 @@ k_onesweep(const u64* __restrict__ keys_in, const V* __restrict__ vals_in,
 
   // ---- scatter into tile-sorted order in shared memory
 #pragma unroll
-  for (int k = 0; k < kSortItems; ++k) {
+  for (int k = 0; k < ITEMS; ++k) {
     const u32 d = (u32)(key[k] >> shift) & (QX_RADIX - 1);
     rank[k] += sm.tile_start[d] + sm.whist[warp][d];
     sm.keys[rank[k]] = key[k];
   }
 #pragma unroll
-  for (int k = 0; k < kSortItems; ++k) {
+  for (int k = 0; k < ITEMS; ++k) {
     const int idx = wslot + k * 32;
-    if (idx < count) sm.vals[rank[k]] = ld_stream(vals_in + start + idx);
+    if (idx < count) sm.vals[rank[k]] = EARLY ? val[EARLY ? k : 0] : ld_stream(vals_in + start + idx);
   }
   __syncthreads();
 
   // ---- coalesced write-out: consecutive slots of one digit are consecutive in HBM
 #pragma unroll
-  for (int k = 0; k < kSortItems; ++k) {
-    const int slot = k * kSortThreads + tid;
+  for (int k = 0; k < ITEMS; ++k) {
+    const int slot = k * THREADS + tid;
     if (slot < count) {
       const u64 kk = sm.keys[slot];
       const int64_t dst = sm.gbase[(u32)(kk >> shift) & (QX_RADIX - 1)] + slot;
@@ -275,45 +303,84 @@ constexpr int kRedTile = QX_SCAN_TILE;
 constexpr int kRedWarps = kRedThreads / 32;
 
 template <typename V>
+struct ReduceSmem {
+  u64 key[kRedTile + 2];       // [0] = key before the tile, [1..cnt] = tile
+  V val[kRedTile];
+  u32 opens[kRedTile / 32];    // bit j: tile slot j is the first term of a non-empty segment
+  u64 scan[kRedWarps + 1];
+  u64 base;
+  int tile;
+};
+
+// One pass over the sorted segments: a term is a head if it opens a segment or its key differs
+// from its predecessor's; the head sums its run sequentially (input order = np.add.at order),
+// applies the drop rule, and kept heads are compacted with a ballot prefix + tile look-back.
+// The tile (keys, coefficients, one halo key) is staged in shared memory with coalesced
+// streaming loads, so every term is read from HBM exactly once and no thread searches the
+// offset table; only runs that cross the tile end touch global memory again.
+template <typename V>
 __global__ void __launch_bounds__(kRedThreads)
 k_reduce(const u64* __restrict__ keys_in, const V* __restrict__ vals_in,
          const int64_t* __restrict__ seg_in, int n_seg, u64* __restrict__ keys_out,
          V* __restrict__ vals_out, int64_t* __restrict__ seg_out, u64* status, u32* ticket,
          double eps) {
-  __shared__ int s_tile;
-  __shared__ u64 s_scan[kRedWarps + 1];
-  __shared__ u64 s_base;
-  if (threadIdx.x == 0) s_tile = (int)atomicAdd(ticket, 1u);
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  ReduceSmem<V>& sm = *reinterpret_cast<ReduceSmem<V>*>(smem_raw);
+  if (threadIdx.x == 0) sm.tile = (int)atomicAdd(ticket, 1u);
+  if (threadIdx.x < kRedTile / 32) sm.opens[threadIdx.x] = 0u;
   __syncthreads();
-  const int tile = s_tile;
+  const int tile = sm.tile;
   const int64_t total = seg_in[n_seg];
   const int64_t ntiles = total > 0 ? (total + kRedTile - 1) / kRedTile : 1;
   if (tile >= ntiles) return;
   const int warp = threadIdx.x >> 5, lane = lane_id();
-  const int64_t wbase = (int64_t)tile * kRedTile + (int64_t)warp * (32 * kRedItems);
+  const int64_t t0 = (int64_t)tile * kRedTile;
+  const int cnt = (int)min((int64_t)kRedTile, total - t0);
+
+  for (int j = threadIdx.x; j < cnt; j += kRedThreads) {
+    sm.key[1 + j] = ld_stream(keys_in + t0 + j);
+    sm.val[j] = ld_stream(vals_in + t0 + j);
+  }
+  if (threadIdx.x == 0) sm.key[0] = t0 > 0 ? keys_in[t0 - 1] : 0ull;
+  {   // segments that start inside this tile
+    int lo = 0, hi = n_seg;                         // first g with seg_in[g] >= t0
+    while (lo < hi) {
+      const int mid = (lo + hi) >> 1;
+      if (seg_in[mid] < t0) lo = mid + 1; else hi = mid;
+    }
+    for (int g = lo + threadIdx.x; g < n_seg; g += kRedThreads) {
+      const int64_t at = seg_in[g];
+      if (at >= t0 + cnt) break;
+      if (seg_in[g + 1] > at) atomicOr(&sm.opens[(at - t0) >> 5], 1u << ((at - t0) & 31));
+    }
+  }
+  __syncthreads();
 
   u64 key[kRedItems];
   V sum[kRedItems];
   u32 pre[kRedItems];          // kept heads before this item inside the warp
   u32 flags = 0;               // bit k: item k is a kept head; bit 16+k: item k opens a segment
-  int segid[kRedItems];
   u32 running = 0;
 #pragma unroll
   for (int k = 0; k < kRedItems; ++k) {
-    const int64_t i = wbase + k * 32 + lane;
+    const int j = warp * (32 * kRedItems) + k * 32 + lane;
     bool kept = false;
-    segid[k] = 0;
-    if (i < total) {
-      key[k] = keys_in[i];
-      const int g = segment_of(seg_in, n_seg, i);
-      segid[k] = g;
-      const bool opens = seg_in[g] == i;
-      const bool head = opens || keys_in[i - 1] != key[k];
+    if (j < cnt) {
+      key[k] = sm.key[1 + j];
+      const bool opens = (sm.opens[j >> 5] >> (j & 31)) & 1u;
       if (opens) flags |= 1u << (16 + k);
-      if (head) {
-        V s = vals_in[i];
-        const int64_t end = seg_in[g + 1];
-        for (int64_t j = i + 1; j < end && keys_in[j] == key[k]; ++j) acc(s, vals_in[j]);
+      if (opens || sm.key[j] != key[k]) {
+        V s = sm.val[j];
+        int e = j + 1;
+        while (e < cnt && sm.key[1 + e] == key[k] && !((sm.opens[e >> 5] >> (e & 31)) & 1u)) {
+          acc(s, sm.val[e]);
+          ++e;
+        }
+        if (e == cnt && t0 + cnt < total) {          // the run may continue past the tile
+          const int g = segment_of(seg_in, n_seg, t0 + j);
+          const int64_t end = seg_in[g + 1];
+          for (int64_t i = t0 + cnt; i < end && keys_in[i] == key[k]; ++i) acc(s, vals_in[i]);
+        }
         sum[k] = s;
         kept = keep(s, eps);
       }
@@ -325,31 +392,28 @@ k_reduce(const u64* __restrict__ keys_in, const V* __restrict__ vals_in,
   }
   u64 tile_total;
   const u64 mine = (lane == 0) ? (u64)running : 0ull;
-  u64 warp_excl = block_exclusive_sum<u64>(mine, s_scan, tile_total);
+  u64 warp_excl = block_exclusive_sum<u64>(mine, sm.scan, tile_total);
   warp_excl = __shfl_sync(QX_FULL_MASK, warp_excl, 0);
   if (warp == 0) {
     const u64 excl = lookback_exclusive(status, tile, tile_total);
-    if (lane == 0) s_base = excl;
+    if (lane == 0) sm.base = excl;
   }
   __syncthreads();
-  const int64_t base = (int64_t)(s_base + warp_excl);
+  const int64_t base = (int64_t)(sm.base + warp_excl);
 #pragma unroll
   for (int k = 0; k < kRedItems; ++k) {
-    const int64_t i = wbase + k * 32 + lane;
     const int64_t pos = base + pre[k];
     if (flags & (1u << k)) {
-      keys_out[pos] = key[k];
-      vals_out[pos] = sum[k];
+      st_stream(keys_out + pos, key[k]);
+      st_stream(vals_out + pos, sum[k]);
     }
     if (flags & (1u << (16 + k))) {
-      seg_out[segid[k]] = pos;
-      for (int h = segid[k] - 1; h >= 0 && seg_in[h] == i; --h) seg_out[h] = pos;
+      const int64_t i = t0 + warp * (32 * kRedItems) + k * 32 + lane;
+      open_offsets(seg_in, seg_out, segment_of(seg_in, n_seg, i), i, pos);
     }
   }
-  if (tile == ntiles - 1 && threadIdx.x == 0) {
-    const int64_t total_out = (int64_t)(s_base + tile_total);
-    for (int g = n_seg; g >= 0 && seg_in[g] == total; --g) seg_out[g] = total_out;
-  }
+  if (tile == ntiles - 1 && threadIdx.x == 0)
+    close_offsets(seg_in, seg_out, n_seg, total, (int64_t)(sm.base + tile_total));
 }
 
 // ---------------------------------------------------------------------------------
@@ -505,14 +569,79 @@ int merge_small(QxArena* ar, MergeBuffers<V>& mb, double eps, int cls) {
   return QX_OK;     // caller synchronises and checks *(int*)h_pinned
 }
 
+struct SortVariant {
+  int tile_terms;
+  const char* name;
+};
+
+template <typename V, int THREADS, int ITEMS, bool EARLY>
+int launch_pass(QxArena* ar, MergeBuffers<V>& mb, int cur, int64_t tiles_ub, const int64_t* tile_prefix,
+                const u32* digit_base, int base_stride, u32* ticket, int shift) {
+  using Smem = SortSmem<V, THREADS, ITEMS>;
+  static bool attr_set = false;
+  if (!attr_set) {
+    QX_CUDA(cudaFuncSetAttribute(k_onesweep<V, THREADS, ITEMS, EARLY>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(Smem)));
+    attr_set = true;
+  }
+  k_onesweep<V, THREADS, ITEMS, EARLY><<<(unsigned)tiles_ub, THREADS, sizeof(Smem), ar->stream>>>(
+      mb.keys[cur], mb.vals[cur], mb.keys[cur ^ 1], mb.vals[cur ^ 1], mb.seg[cur], mb.n_seg, tile_prefix,
+      digit_base, base_stride, ar->status, ticket, shift);
+  QX_CUDA(cudaGetLastError());
+  return QX_OK;
+}
+
+// Tile geometry of the sort pass; QX_SORT_VARIANT picks one for A/B runs on the GPU.
+inline int sort_variant() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("QX_SORT_VARIANT");
+    v = e ? atoi(e) : 0;
+    if (v < 0 || v > 5) v = 0;
+  }
+  return v;
+}
+
+inline int sort_tile_terms(int variant, size_t value_bytes) {
+  if (value_bytes > 8) return 256 * 12;            // complex coefficients: one geometry
+  switch (variant) {
+    case 1: return 384 * 12;
+    case 2: return 256 * 12;
+    case 3: return 256 * 16;
+    case 4: return 512 * 8;
+    case 5: return 256 * 12;
+    default: return 384 * 12;
+  }
+}
+
 template <typename V>
-int merge_large(QxArena* ar, MergeBuffers<V>& mb, double eps, int cls_reduce) {
+int dispatch_pass(int variant, QxArena* ar, MergeBuffers<V>& mb, int cur, int64_t tiles_ub,
+                  const int64_t* tile_prefix, const u32* digit_base, int base_stride, u32* ticket,
+                  int shift) {
+  if (sizeof(V) > 8)
+    return launch_pass<V, 256, 12, false>(ar, mb, cur, tiles_ub, tile_prefix, digit_base, base_stride, ticket, shift);
+  switch (variant) {
+    case 1: return launch_pass<V, 384, 12, true>(ar, mb, cur, tiles_ub, tile_prefix, digit_base, base_stride, ticket, shift);
+    case 2: return launch_pass<V, 256, 12, false>(ar, mb, cur, tiles_ub, tile_prefix, digit_base, base_stride, ticket, shift);
+    case 3: return launch_pass<V, 256, 16, false>(ar, mb, cur, tiles_ub, tile_prefix, digit_base, base_stride, ticket, shift);
+    case 4: return launch_pass<V, 512, 8, false>(ar, mb, cur, tiles_ub, tile_prefix, digit_base, base_stride, ticket, shift);
+    case 5: return launch_pass<V, 256, 12, true>(ar, mb, cur, tiles_ub, tile_prefix, digit_base, base_stride, ticket, shift);
+    default: return launch_pass<V, 384, 12, false>(ar, mb, cur, tiles_ub, tile_prefix, digit_base, base_stride, ticket, shift);
+  }
+}
+
+// do_reduce = false: sort only (keys known unique and nothing to drop, e.g. after a run of
+// Clifford gates) -- the segment offsets do not change and no rank read-back is needed.
+template <typename V>
+int merge_large(QxArena* ar, MergeBuffers<V>& mb, double eps, int cls_reduce, bool do_reduce = true) {
   const int n_seg = mb.n_seg;
   const int passes = std::min(kMaxPasses, (2 * ar->n_qubits + QX_RADIX_BITS - 1) / QX_RADIX_BITS);
   if (mb.ub_seg >= (int64_t)kFlagVal)
     return qx_fail(QX_ERR_RESOURCE, "a generator with %lld raw terms exceeds the sort's 2^30 limit",
                    (long long)mb.ub_seg);
-  const int64_t tiles_ub = (mb.ub_total + kSortTile - 1) / kSortTile + n_seg;
+  const int variant = sort_variant();
+  const int tile_terms = sort_tile_terms(variant, sizeof(V));
+  const int64_t tiles_ub = (mb.ub_total + tile_terms - 1) / tile_terms + n_seg;
   const int64_t red_tiles = std::max<int64_t>(1, (mb.ub_total + kRedTile - 1) / kRedTile);
   // scratch layout: ticket | tile_prefix | hist | reduce look-back
   const int64_t off_prefix = 256;
@@ -532,19 +661,19 @@ int merge_large(QxArena* ar, MergeBuffers<V>& mb, double eps, int cls_reduce) {
   static bool attr_set[2] = {false, false};
   const int which = sizeof(V) == 8 ? 0 : 1;
   if (!attr_set[which]) {
-    QX_CUDA(cudaFuncSetAttribute(k_onesweep<V>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)sizeof(SortSmem<V>)));
+    QX_CUDA(cudaFuncSetAttribute(k_reduce<V>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)sizeof(ReduceSmem<V>)));
     attr_set[which] = true;
   }
   int cur = mb.cur;
-  k_sort_plan<<<1, 32, 0, ar->stream>>>(mb.seg[cur], n_seg, tile_prefix, ticket);
+  k_sort_plan<<<1, 32, 0, ar->stream>>>(mb.seg[cur], n_seg, tile_prefix, ticket, tile_terms);
   qx_count_launches(1);
   QX_CUDA(cudaGetLastError());
   {
     const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(tiles_ub, (int64_t)ar->sm_count * 4));
     QxProfileScope prof(QX_K_SORT_HIST, ar->stream, 8.0 * (double)mb.ub_total);
     k_sort_hist<<<grid, kSortThreads, 0, ar->stream>>>(mb.keys[cur], mb.seg[cur], n_seg, tile_prefix,
-                                                       hist, passes);
+                                                       hist, passes, tile_terms);
     QX_CUDA(cudaGetLastError());
   }
   k_sort_scan_hist<<<n_seg * passes, QX_RADIX, 0, ar->stream>>>(hist);
@@ -557,17 +686,18 @@ int merge_large(QxArena* ar, MergeBuffers<V>& mb, double eps, int cls_reduce) {
     QX_CUDA(cudaMemsetAsync(ar->status, 0, sizeof(u32) * (size_t)(tiles_ub * QX_RADIX), ar->stream));
     QX_CUDA(cudaMemsetAsync(ticket, 0, sizeof(u32), ar->stream));
     QxProfileScope prof(QX_K_SORT_PASS, ar->stream, 2.0 * (8.0 + sizeof(V)) * (double)mb.ub_total);
-    k_onesweep<V><<<(unsigned)tiles_ub, kSortThreads, sizeof(SortSmem<V>), ar->stream>>>(
-        mb.keys[cur], mb.vals[cur], mb.keys[cur ^ 1], mb.vals[cur ^ 1], mb.seg[cur], n_seg,
-        tile_prefix, hist + (size_t)p * QX_RADIX, passes * QX_RADIX, ar->status, ticket,
-        p * QX_RADIX_BITS);
-    QX_CUDA(cudaGetLastError());
+    QX_TRY(dispatch_pass<V>(variant, ar, mb, cur, tiles_ub, tile_prefix, hist + (size_t)p * QX_RADIX,
+                            passes * QX_RADIX, ticket, p * QX_RADIX_BITS));
     cur ^= 1;
+  }
+  if (!do_reduce) {
+    mb.cur = cur;
+    return QX_OK;
   }
   QX_CUDA(cudaMemsetAsync(ticket, 0, sizeof(u32), ar->stream));
   {
     QxProfileScope prof(cls_reduce, ar->stream, (8.0 + sizeof(V)) * 2.0 * (double)mb.ub_total);
-    k_reduce<V><<<(unsigned)red_tiles, kRedThreads, 0, ar->stream>>>(
+    k_reduce<V><<<(unsigned)red_tiles, kRedThreads, sizeof(ReduceSmem<V>), ar->stream>>>(
         mb.keys[cur], mb.vals[cur], mb.seg[cur], n_seg, mb.keys[cur ^ 1], mb.vals[cur ^ 1],
         mb.seg[cur ^ 1], red_status, ticket, eps);
     QX_CUDA(cudaGetLastError());

@@ -79,6 +79,18 @@ struct QxArena {
   int64_t* h_pinned = nullptr;  // small pinned staging
   int64_t h_pinned_words = 0;
 };
+// Device allocations through the library's caching allocator (store.cu): a store created
+// per circuit run gets its multi-GB buffers back in microseconds instead of paying
+// cudaMalloc/cudaFree (tens of ms) every run.
+int qx_dev_alloc(void** out, int64_t bytes, cudaStream_t stream, int device);
+void qx_dev_free(void* ptr, cudaStream_t stream);
+int qx_pinned_alloc(void** out, int64_t bytes);
+void qx_pinned_free(void* ptr);
+template <typename T>
+inline int qx_dev_alloc_t(T** out, int64_t count, cudaStream_t stream, int device) {
+  return qx_dev_alloc(reinterpret_cast<void**>(out), (int64_t)sizeof(T) * count, stream, device);
+}
+
 int qx_arena_init(QxArena* a, int device, int n_qubits, int64_t pinned_words);
 void qx_arena_release(QxArena* a);
 int qx_arena_scratch(QxArena* a, int64_t bytes);

@@ -111,32 +111,28 @@ __global__ void k_lookup(const u64* __restrict__ keys, const double2* __restrict
 
 int reserve(qx_expansion* e, int64_t terms) {
   if (terms <= e->cap) return QX_OK;
-  QX_CUDA(cudaStreamSynchronize(e->stream));
   const int64_t want = std::max<int64_t>(terms + terms / 8, 2 * e->cap);
-  size_t free_b = 0, total_b = 0;
-  QX_CUDA(cudaMemGetInfo(&free_b, &total_b));
-  if (48.0 * (double)want > 0.9 * ((double)free_b + 48.0 * (double)e->cap))
-    return qx_fail(QX_ERR_RESOURCE, "density expansion of %lld terms needs %.1f GB of HBM",
-                   (long long)want, 48.0 * (double)want / 1e9);
-  const int dead = e->cur ^ 1;
-  QX_CUDA(cudaFree(e->keys[dead]));
-  QX_CUDA(cudaFree(e->vals[dead]));
-  QX_CUDA(cudaMalloc(&e->keys[dead], sizeof(u64) * (size_t)want));
-  QX_CUDA(cudaMalloc(&e->vals[dead], sizeof(double2) * (size_t)want));
+  const int dead = e->cur ^ 1, old = e->cur;
+  qx_dev_free(e->keys[dead], e->stream);
+  qx_dev_free(e->vals[dead], e->stream);
+  e->keys[dead] = nullptr;
+  e->vals[dead] = nullptr;
+  QX_TRY(qx_dev_alloc_t(&e->keys[dead], want, e->stream, e->device));
+  QX_TRY(qx_dev_alloc_t(&e->vals[dead], want, e->stream, e->device));
   if (e->count > 0) {
-    QX_CUDA(cudaMemcpyAsync(e->keys[dead], e->keys[e->cur], sizeof(u64) * (size_t)e->count,
+    QX_CUDA(cudaMemcpyAsync(e->keys[dead], e->keys[old], sizeof(u64) * (size_t)e->count,
                             cudaMemcpyDeviceToDevice, e->stream));
-    QX_CUDA(cudaMemcpyAsync(e->vals[dead], e->vals[e->cur], sizeof(double2) * (size_t)e->count,
+    QX_CUDA(cudaMemcpyAsync(e->vals[dead], e->vals[old], sizeof(double2) * (size_t)e->count,
                             cudaMemcpyDeviceToDevice, e->stream));
   }
-  QX_CUDA(cudaMemcpyAsync(e->seg[dead], e->seg[e->cur], sizeof(int64_t) * 2, cudaMemcpyDeviceToDevice,
+  QX_CUDA(cudaMemcpyAsync(e->seg[dead], e->seg[old], sizeof(int64_t) * 2, cudaMemcpyDeviceToDevice,
                           e->stream));
-  QX_CUDA(cudaStreamSynchronize(e->stream));
-  const int old = e->cur;
-  QX_CUDA(cudaFree(e->keys[old]));
-  QX_CUDA(cudaFree(e->vals[old]));
-  QX_CUDA(cudaMalloc(&e->keys[old], sizeof(u64) * (size_t)want));
-  QX_CUDA(cudaMalloc(&e->vals[old], sizeof(double2) * (size_t)want));
+  qx_dev_free(e->keys[old], e->stream);
+  qx_dev_free(e->vals[old], e->stream);
+  e->keys[old] = nullptr;
+  e->vals[old] = nullptr;
+  QX_TRY(qx_dev_alloc_t(&e->keys[old], want, e->stream, e->device));
+  QX_TRY(qx_dev_alloc_t(&e->vals[old], want, e->stream, e->device));
   e->cur = dead;
   e->cap = want;
   return QX_OK;
@@ -201,14 +197,12 @@ extern "C" int qx_expansion_create(int device, int n_qubits, int64_t capacity_te
     return st;
   }
   e->cap = std::max<int64_t>(capacity_terms, 4096);
-  cudaError_t err = cudaSuccess;
-  for (int b = 0; b < 2 && err == cudaSuccess; ++b) {
-    err = cudaMalloc(&e->keys[b], sizeof(u64) * (size_t)e->cap);
-    if (err == cudaSuccess) err = cudaMalloc(&e->vals[b], sizeof(double2) * (size_t)e->cap);
-    if (err == cudaSuccess) err = cudaMalloc(&e->seg[b], sizeof(int64_t) * 2);
+  for (int b = 0; b < 2 && st == QX_OK; ++b) {
+    st = qx_dev_alloc_t(&e->keys[b], e->cap, e->stream, e->device);
+    if (st == QX_OK) st = qx_dev_alloc_t(&e->vals[b], e->cap, e->stream, e->device);
+    if (st == QX_OK) st = qx_dev_alloc_t(&e->seg[b], 2, e->stream, e->device);
   }
-  if (err != cudaSuccess) {
-    st = qx_fail(QX_ERR_RESOURCE, "expansion allocation failed: %s", cudaGetErrorString(err));
+  if (st != QX_OK) {
     qx_expansion_destroy(e);
     return st;
   }
@@ -226,12 +220,12 @@ extern "C" int qx_expansion_destroy(qx_expansion* e) {
   cudaSetDevice(e->device);
   cudaStreamSynchronize(e->stream);
   for (int b = 0; b < 2; ++b) {
-    cudaFree(e->keys[b]);
-    cudaFree(e->vals[b]);
-    cudaFree(e->seg[b]);
+    qx_dev_free(e->keys[b], e->stream);
+    qx_dev_free(e->vals[b], e->stream);
+    qx_dev_free(e->seg[b], e->stream);
   }
-  cudaFree(e->g_keys);
-  cudaFree(e->g_lam);
+  qx_dev_free(e->g_keys, e->stream);
+  qx_dev_free(e->g_lam, e->stream);
   qx_arena_release(e);
   delete e;
   return QX_OK;
@@ -253,15 +247,14 @@ extern "C" int qx_expansion_multiply(qx_expansion* e, const uint64_t* keys, cons
   QX_REQUIRE(count == 0 || (keys && lambdas), "keys/lambdas are NULL");
   QX_CUDA(cudaSetDevice(e->device));
   if (count > e->g_cap) {
-    QX_CUDA(cudaStreamSynchronize(e->stream));
-    cudaFree(e->g_keys);
-    cudaFree(e->g_lam);
+    qx_dev_free(e->g_keys, e->stream);
+    qx_dev_free(e->g_lam, e->stream);
     e->g_keys = nullptr;
     e->g_lam = nullptr;
     e->g_cap = 0;
     const int64_t want = std::max<int64_t>(count, 1024);
-    QX_CUDA(cudaMalloc(&e->g_keys, sizeof(u64) * (size_t)want));
-    QX_CUDA(cudaMalloc(&e->g_lam, sizeof(double) * (size_t)want));
+    QX_TRY(qx_dev_alloc_t(&e->g_keys, want, e->stream, e->device));
+    QX_TRY(qx_dev_alloc_t(&e->g_lam, want, e->stream, e->device));
     e->g_cap = want;
   }
   if (count > 0) {

@@ -7,7 +7,9 @@
 
 #include <algorithm>
 #include <atomic>
+#include <map>
 #include <mutex>
+#include <unordered_map>
 
 #include "qx_internal.cuh"
 
@@ -171,19 +173,137 @@ extern "C" int qx_launch_count(int64_t* launches) {
 }
 
 // ----------------------------------------------------------------------------
+// device memory: caching allocator
+// ----------------------------------------------------------------------------
+// A store is created per circuit run and owns multi-GB buffers; cudaMalloc/cudaFree (and
+// the driver's pool when block sizes vary from run to run) cost tens to hundreds of
+// milliseconds per run, more than the kernels.  Freed blocks are therefore kept in a
+// per-device free list and handed out again for any request they fit within 2x.  Reuse is
+// stream-ordered: a block freed on stream S may still be in use by kernels queued on S, so
+// it is only handed to the same stream without a wait; any other stream synchronises S first.
+namespace {
+struct DevBlock {
+  void* ptr;
+  size_t bytes;
+  int device;
+  cudaStream_t stream;   // stream of the last user
+};
+std::mutex g_alloc_mu;
+std::unordered_map<void*, DevBlock> g_live;
+std::multimap<size_t, DevBlock> g_free[64];
+
+size_t round_block(size_t bytes) {
+  const size_t unit = bytes >= (1u << 20) ? (2u << 20) : 512;   // 2 MiB granules for big blocks
+  return (bytes + unit - 1) / unit * unit;
+}
+
+void release_cached(int device) {
+  for (auto& kv : g_free[device]) {
+    cudaStreamSynchronize(kv.second.stream);
+    cudaFree(kv.second.ptr);
+  }
+  g_free[device].clear();
+}
+}  // namespace
+
+int qx_dev_alloc(void** out, int64_t bytes, cudaStream_t stream, int device) {
+  *out = nullptr;
+  if (device < 0 || device >= 64) return qx_fail(QX_ERR_INVALID, "bad device %d", device);
+  const size_t want = round_block((size_t)std::max<int64_t>(bytes, 256));
+  std::lock_guard<std::mutex> lock(g_alloc_mu);
+  auto it = g_free[device].lower_bound(want);
+  if (it != g_free[device].end() && it->first <= 2 * want + (64u << 20)) {
+    DevBlock blk = it->second;
+    g_free[device].erase(it);
+    if (blk.stream != stream) cudaStreamSynchronize(blk.stream);
+    blk.stream = stream;
+    g_live[blk.ptr] = blk;
+    *out = blk.ptr;
+    return QX_OK;
+  }
+  void* p = nullptr;
+  cudaError_t e = cudaMalloc(&p, want);
+  if (e != cudaSuccess) {            // give the cache back to the driver and retry once
+    cudaGetLastError();
+    release_cached(device);
+    e = cudaMalloc(&p, want);
+  }
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    size_t free_b = 0, total_b = 0;
+    cudaMemGetInfo(&free_b, &total_b);
+    return qx_fail(QX_ERR_RESOURCE, "cannot allocate %.2f GB of HBM on device %d (%.1f GB free): %s",
+                   want / 1e9, device, free_b / 1e9, cudaGetErrorString(e));
+  }
+  g_live[p] = DevBlock{p, want, device, stream};
+  *out = p;
+  return QX_OK;
+}
+
+void qx_dev_free(void* ptr, cudaStream_t stream) {
+  if (!ptr) return;
+  std::lock_guard<std::mutex> lock(g_alloc_mu);
+  auto it = g_live.find(ptr);
+  if (it == g_live.end()) {
+    cudaFree(ptr);
+    return;
+  }
+  DevBlock blk = it->second;
+  g_live.erase(it);
+  blk.stream = stream;
+  g_free[blk.device].emplace(blk.bytes, blk);
+}
+
+// small page-locked staging blocks (offset mirrors): same idea, cudaMallocHost is ~0.3 ms a call
+namespace {
+std::multimap<size_t, void*> g_pinned_free;
+std::unordered_map<void*, size_t> g_pinned_live;
+}  // namespace
+
+int qx_pinned_alloc(void** out, int64_t bytes) {
+  const size_t want = ((size_t)std::max<int64_t>(bytes, 64) + 4095) / 4096 * 4096;
+  std::lock_guard<std::mutex> lock(g_alloc_mu);
+  auto it = g_pinned_free.lower_bound(want);
+  if (it != g_pinned_free.end() && it->first <= 4 * want) {
+    *out = it->second;
+    g_pinned_live[*out] = it->first;
+    g_pinned_free.erase(it);
+    return QX_OK;
+  }
+  QX_CUDA(cudaMallocHost(out, want));
+  g_pinned_live[*out] = want;
+  return QX_OK;
+}
+
+void qx_pinned_free(void* ptr) {
+  if (!ptr) return;
+  std::lock_guard<std::mutex> lock(g_alloc_mu);
+  auto it = g_pinned_live.find(ptr);
+  if (it == g_pinned_live.end()) {
+    cudaFreeHost(ptr);
+    return;
+  }
+  g_pinned_free.emplace(it->second, ptr);
+  g_pinned_live.erase(it);
+}
+
+extern "C" int qx_trim(void) {
+  std::lock_guard<std::mutex> lock(g_alloc_mu);
+  for (int d = 0; d < 64; ++d)
+    if (!g_free[d].empty()) {
+      cudaSetDevice(d);
+      release_cached(d);
+    }
+  return QX_OK;
+}
+
+// ----------------------------------------------------------------------------
 // store lifetime and capacity
 // ----------------------------------------------------------------------------
 static int alloc_buffers(qx_store* s, int64_t cap, u64** keys, double** lam) {
-  size_t free_b = 0, total_b = 0;
-  QX_CUDA(cudaMemGetInfo(&free_b, &total_b));
-  const double need = 2.0 * 16.0 * (double)cap;
-  if (need > 0.92 * (double)free_b)
-    return qx_fail(QX_ERR_RESOURCE,
-                   "term store of %lld terms needs %.1f GB of HBM, %.1f GB free on device %d",
-                   (long long)cap, need / 1e9, free_b / 1e9, s->device);
   for (int b = 0; b < 2; ++b) {
-    QX_CUDA(cudaMalloc(&keys[b], sizeof(u64) * (size_t)cap));
-    QX_CUDA(cudaMalloc(&lam[b], sizeof(double) * (size_t)cap));
+    QX_TRY(qx_dev_alloc_t(&keys[b], cap, s->stream, s->device));
+    QX_TRY(qx_dev_alloc_t(&lam[b], cap, s->stream, s->device));
   }
   return QX_OK;
 }
@@ -210,11 +330,13 @@ extern "C" int qx_store_create(int device, int n_qubits, int n_segments, int64_t
   int st = alloc_buffers(s, s->cap, s->keys, s->lam);
   if (st == QX_OK) {
     cudaError_t e = cudaSuccess;
-    for (int b = 0; b < 2 && e == cudaSuccess; ++b)
-      e = cudaMalloc(&s->seg[b], sizeof(int64_t) * (size_t)(n_segments + 1));
-    if (e == cudaSuccess) e = cudaMallocHost(&s->h_seg, sizeof(int64_t) * (size_t)(n_segments + 1));
-    if (e == cudaSuccess) e = cudaMemset(s->seg[0], 0, sizeof(int64_t) * (size_t)(n_segments + 1));
-    if (e != cudaSuccess) st = qx_fail(QX_ERR_CUDA, "store allocation failed: %s", cudaGetErrorString(e));
+    for (int b = 0; b < 2 && st == QX_OK; ++b)
+      st = qx_dev_alloc_t(&s->seg[b], (int64_t)n_segments + 1, s->stream, s->device);
+    if (st == QX_OK)
+      st = qx_pinned_alloc(reinterpret_cast<void**>(&s->h_seg), 8 * ((int64_t)n_segments + 1));
+    if (st == QX_OK && e == cudaSuccess)
+      e = cudaMemsetAsync(s->seg[0], 0, sizeof(int64_t) * (size_t)(n_segments + 1), s->stream);
+    if (st == QX_OK && e != cudaSuccess) st = qx_fail(QX_ERR_CUDA, "store allocation failed: %s", cudaGetErrorString(e));
   }
   if (st != QX_OK) {
     qx_store_destroy(s);
@@ -231,11 +353,11 @@ extern "C" int qx_store_destroy(qx_store* s) {
   cudaSetDevice(s->device);
   cudaStreamSynchronize(s->stream);
   for (int b = 0; b < 2; ++b) {
-    cudaFree(s->keys[b]);
-    cudaFree(s->lam[b]);
-    cudaFree(s->seg[b]);
+    qx_dev_free(s->keys[b], s->stream);
+    qx_dev_free(s->lam[b], s->stream);
+    qx_dev_free(s->seg[b], s->stream);
   }
-  cudaFreeHost(s->h_seg);
+  qx_pinned_free(s->h_seg);
   qx_arena_release(s);
   delete s;
   return QX_OK;
@@ -254,45 +376,50 @@ int qx_store_reserve(qx_store* s, int64_t terms, bool keep_live) {
   QX_CUDA(cudaSetDevice(s->device));
   if (keep_live && !s->exact) QX_TRY(qx_store_refresh(s));
   const int64_t live = keep_live ? s->h_seg[s->n_seg] : 0;
-  QX_CUDA(cudaStreamSynchronize(s->stream));
-  // Growth is done one buffer pair at a time so the peak is old + new, not 2x new.
+  // One buffer pair at a time so the peak is old + new, not 2x new.  Try generous growth
+  // first, fall back to the exact need when HBM is tight.
+  const int dead = s->cur ^ 1, old = s->cur;
   int64_t want = std::max<int64_t>(terms + terms / 8, s->cap * 2);
-  size_t free_b = 0, total_b = 0;
-  QX_CUDA(cudaMemGetInfo(&free_b, &total_b));
-  const double avail = 0.94 * ((double)free_b + 32.0 * (double)s->cap);
-  if (32.0 * (double)want > avail) want = terms;
-  if (32.0 * (double)want > avail)
-    return qx_fail(QX_ERR_RESOURCE,
-                   "term store would need %.1f GB of HBM for %lld terms (%.1f GB usable on device %d)",
-                   32.0 * (double)want / 1e9, (long long)want, avail / 1e9, s->device);
-  const int dead = s->cur ^ 1;
-  QX_CUDA(cudaFree(s->keys[dead]));
-  QX_CUDA(cudaFree(s->lam[dead]));
+  qx_dev_free(s->keys[dead], s->stream);
+  qx_dev_free(s->lam[dead], s->stream);
   s->keys[dead] = nullptr;
   s->lam[dead] = nullptr;
-  QX_CUDA(cudaMalloc(&s->keys[dead], sizeof(u64) * (size_t)want));
-  QX_CUDA(cudaMalloc(&s->lam[dead], sizeof(double) * (size_t)want));
-  if (live > 0) {
-    QX_CUDA(cudaMemcpyAsync(s->keys[dead], s->keys[s->cur], sizeof(u64) * (size_t)live,
-                            cudaMemcpyDeviceToDevice, s->stream));
-    QX_CUDA(cudaMemcpyAsync(s->lam[dead], s->lam[s->cur], sizeof(double) * (size_t)live,
-                            cudaMemcpyDeviceToDevice, s->stream));
-    QX_CUDA(cudaStreamSynchronize(s->stream));
+  int st = qx_dev_alloc_t(&s->keys[dead], want, s->stream, s->device);
+  if (st == QX_OK) st = qx_dev_alloc_t(&s->lam[dead], want, s->stream, s->device);
+  if (st != QX_OK && want > terms) {
+    qx_dev_free(s->keys[dead], s->stream);
+    qx_dev_free(s->lam[dead], s->stream);
+    s->keys[dead] = nullptr;
+    s->lam[dead] = nullptr;
+    want = terms;
+    st = qx_dev_alloc_t(&s->keys[dead], want, s->stream, s->device);
+    if (st == QX_OK) st = qx_dev_alloc_t(&s->lam[dead], want, s->stream, s->device);
   }
-  const int old = s->cur;
-  QX_CUDA(cudaFree(s->keys[old]));
-  QX_CUDA(cudaFree(s->lam[old]));
+  if (st != QX_OK) {
+    s->cap = 0;      // the store is unusable now; the caller surfaces ResourceLimitError
+    return qx_fail(QX_ERR_RESOURCE, "term store would need %.1f GB of HBM for %lld terms on device %d",
+                   32.0 * (double)terms / 1e9, (long long)terms, s->device);
+  }
+  if (live > 0) {
+    QX_CUDA(cudaMemcpyAsync(s->keys[dead], s->keys[old], sizeof(u64) * (size_t)live,
+                            cudaMemcpyDeviceToDevice, s->stream));
+    QX_CUDA(cudaMemcpyAsync(s->lam[dead], s->lam[old], sizeof(double) * (size_t)live,
+                            cudaMemcpyDeviceToDevice, s->stream));
+  }
+  QX_CUDA(cudaMemcpyAsync(s->seg[dead], s->seg[old], sizeof(int64_t) * (size_t)(s->n_seg + 1),
+                          cudaMemcpyDeviceToDevice, s->stream));
+  qx_dev_free(s->keys[old], s->stream);
+  qx_dev_free(s->lam[old], s->stream);
   s->keys[old] = nullptr;
   s->lam[old] = nullptr;
-  QX_CUDA(cudaMalloc(&s->keys[old], sizeof(u64) * (size_t)want));
-  QX_CUDA(cudaMalloc(&s->lam[old], sizeof(double) * (size_t)want));
-  // live data now sits in `dead`; the offsets follow the live index
-  if (s->cur != dead) {
-    QX_CUDA(cudaMemcpyAsync(s->seg[dead], s->seg[s->cur], sizeof(int64_t) * (size_t)(s->n_seg + 1),
-                            cudaMemcpyDeviceToDevice, s->stream));
-    QX_CUDA(cudaStreamSynchronize(s->stream));
-    s->cur = dead;
+  st = qx_dev_alloc_t(&s->keys[old], want, s->stream, s->device);
+  if (st == QX_OK) st = qx_dev_alloc_t(&s->lam[old], want, s->stream, s->device);
+  if (st != QX_OK) {
+    s->cap = 0;
+    return qx_fail(QX_ERR_RESOURCE, "term store would need %.1f GB of HBM for %lld terms on device %d",
+                   32.0 * (double)want / 1e9, (long long)want, s->device);
   }
+  s->cur = dead;
   s->cap = want;
   return QX_OK;
 }
@@ -303,23 +430,29 @@ int qx_arena_init(QxArena* a, int device, int n_qubits, int64_t pinned_words) {
   if (device < 0 || device >= count)
     return qx_fail(QX_ERR_CUDA, "CUDA device %d not available (%d visible)", device, count);
   QX_CUDA(cudaSetDevice(device));
-  cudaDeviceProp prop;
-  QX_CUDA(cudaGetDeviceProperties(&prop, device));
-  if (prop.major < 10)
-    return qx_fail(QX_ERR_CUDA, "device %d is sm_%d%d; this library is built for sm_100a only",
-                   device, prop.major, prop.minor);
+  static int cached_sm[64] = {0}, cached_major[64] = {0};
+  if (device < 64 && cached_sm[device] == 0) {      // cudaGetDeviceProperties costs ~1 ms
+    int sm = 0, major = 0;
+    QX_CUDA(cudaDeviceGetAttribute(&sm, cudaDevAttrMultiProcessorCount, device));
+    QX_CUDA(cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, device));
+    cached_sm[device] = sm;
+    cached_major[device] = major;
+  }
+  if (cached_major[device] < 10)
+    return qx_fail(QX_ERR_CUDA, "device %d is sm_%dx; this library is built for sm_100a only",
+                   device, cached_major[device]);
   a->device = device;
   a->n_qubits = n_qubits;
-  a->sm_count = prop.multiProcessorCount;
+  a->sm_count = cached_sm[device];
   a->h_pinned_words = pinned_words;
-  QX_CUDA(cudaMallocHost(&a->h_pinned, sizeof(int64_t) * (size_t)pinned_words));
+  QX_TRY(qx_pinned_alloc(reinterpret_cast<void**>(&a->h_pinned), 8 * pinned_words));
   return QX_OK;
 }
 
 void qx_arena_release(QxArena* a) {
-  cudaFree(a->scratch);
-  cudaFree(a->status);
-  cudaFreeHost(a->h_pinned);
+  qx_dev_free(a->scratch, a->stream);
+  qx_dev_free(a->status, a->stream);
+  qx_pinned_free(a->h_pinned);
   a->scratch = nullptr;
   a->status = nullptr;
   a->h_pinned = nullptr;
@@ -327,30 +460,22 @@ void qx_arena_release(QxArena* a) {
 
 int qx_arena_scratch(QxArena* s, int64_t bytes) {
   if (bytes <= s->scratch_bytes) return QX_OK;
-  QX_CUDA(cudaStreamSynchronize(s->stream));
-  if (s->scratch) QX_CUDA(cudaFree(s->scratch));
+  qx_dev_free(s->scratch, s->stream);     // stream-ordered: earlier kernels still see it
   s->scratch = nullptr;
   s->scratch_bytes = 0;
   const int64_t want = bytes + bytes / 4 + 4096;
-  cudaError_t e = cudaMalloc(&s->scratch, (size_t)want);
-  if (e != cudaSuccess)
-    return qx_fail(QX_ERR_RESOURCE, "scratch of %.2f GB not available: %s", want / 1e9,
-                   cudaGetErrorString(e));
+  QX_TRY(qx_dev_alloc(&s->scratch, want, s->stream, s->device));
   s->scratch_bytes = want;
   return QX_OK;
 }
 
 int qx_arena_status(QxArena* s, int64_t words) {
   if (words <= s->status_words) return QX_OK;
-  QX_CUDA(cudaStreamSynchronize(s->stream));
-  if (s->status) QX_CUDA(cudaFree(s->status));
+  qx_dev_free(s->status, s->stream);
   s->status = nullptr;
   s->status_words = 0;
   const int64_t want = words + words / 4 + 1024;
-  cudaError_t e = cudaMalloc(&s->status, sizeof(u32) * (size_t)want);
-  if (e != cudaSuccess)
-    return qx_fail(QX_ERR_RESOURCE, "look-back table of %.2f GB not available: %s",
-                   4.0 * want / 1e9, cudaGetErrorString(e));
+  QX_TRY(qx_dev_alloc_t(&s->status, want, s->stream, s->device));
   s->status_words = want;
   return QX_OK;
 }

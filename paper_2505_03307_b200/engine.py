@@ -88,20 +88,34 @@ class AgreementReport:
 
 
 class _Walker:
-    """Queues sign-permutation ops and flushes them as one fused launch."""
+    """Schedules the device work of one run.
+
+    Sign-permutation ops are queued and flushed as one fused launch.  The merge of a
+    branching op is *deferred* past the permutation ops that follow it: they are bijections
+    on words that keep |lambda|, so merging before or after them sums the same duplicates in
+    the same order and drops the same terms -- but afterwards the result is already in the
+    final order, which saves the reference's second sort (its canonicalize after every V_k).
+    The deferred merge runs before the next branching op or at the end; rank-trace entries
+    and v1 update counts that fall in between are filled in then.
+    """
 
     def __init__(self, store: DeviceStore, n: int, ids, eps: float, timings: dict,
                  before_merge=None, reduce_ranks=None):
         self.store, self.n, self.ids, self.eps = store, n, list(ids), eps
         self.timings = timings
         self.before_merge, self.reduce_ranks = before_merge, reduce_ranks
+        self.eager = False             # merge after every step (eps could drop an input term)
         self.queue: list = []
         self.queue_has_cx = False
         self.unsorted = False          # a permutation ran since the last merge
+        self.pending = None            # (step, phase) of a branching op whose merge is deferred
+        self.open_slots: list = []     # trace rows waiting for the deferred merge
+        self.pending_gates = 0         # v1 gates applied since the deferred branch
         self.ranks = [1] * len(self.ids)
-        self.launch_log = {"clifford_runs": 0, "branch_ops": 0, "merges": 0}
+        self.launch_log = {"clifford_runs": 0, "branch_ops": 0, "merges": 0, "sorts": 0}
         self.updates = None            # v1 only: term-gate updates per generator (SURVEY.md 8d)
 
+    # -- queue ---------------------------------------------------------------------
     def push_perm(self, qubit: int, table: int):
         if table != _lut.IDENTITY_PERM:
             self.queue.append(_lut.perm_op(self.n, qubit, table))
@@ -120,7 +134,8 @@ class _Walker:
         self.unsorted = True
         self.launch_log["clifford_runs"] += 1
 
-    def merge(self, step: int, phase: str, after_branch: bool = False):
+    # -- merges ----------------------------------------------------------------------
+    def _merge_now(self, step: int, phase: str, after_branch: bool):
         t0 = time.perf_counter()
         if after_branch and self.before_merge is not None:
             self.before_merge(self.store)      # term-partitioned runs: equal keys must meet first
@@ -135,6 +150,59 @@ class _Walker:
                 raise NumericalCollapseError(
                     f"all terms of generator {self.ids[local]} dropped at operator step {step}"
                 )
+
+    def resolve(self, trace):
+        """Run the deferred merge (after the permutation ops queued behind it)."""
+        if self.pending is None:
+            return
+        step, phase = self.pending
+        self.flush()
+        self._merge_now(step, phase, after_branch=True)
+        self.pending = None
+        for slot in self.open_slots:
+            trace[slot] = list(self.ranks)
+        self.open_slots = []
+        if self.updates is not None and self.pending_gates:
+            self.updates += np.asarray(self.ranks, dtype=np.int64) * self.pending_gates
+        self.pending_gates = 0
+
+    def branched(self, step: int, phase: str, trace):
+        """A branching kernel just ran: its merge is now owed."""
+        self.launch_log["branch_ops"] += 1
+        self.pending = (step, phase)
+        if self.eager:
+            self.resolve(trace)
+
+    def step_done(self, step: int, phase: str, trace):
+        """End of a permutation-only step."""
+        if self.eager:
+            self.flush()
+            self._merge_now(step, phase, after_branch=False)
+
+    def snapshot(self, trace):
+        if self.pending is None:
+            trace.append(list(self.ranks))
+        else:
+            self.open_slots.append(len(trace))
+            trace.append(None)
+
+    def count_gate(self):
+        """v1: one more gate sees the current terms."""
+        if self.pending is None:
+            self.updates += np.asarray(self.ranks, dtype=np.int64)
+        else:
+            self.pending_gates += 1
+
+    def finish(self, trace):
+        self.resolve(trace)
+        self.flush()
+        if self.unsorted:
+            # only permutations since the last merge: canonicalize can only re-sort
+            t0 = time.perf_counter()
+            self.store.sort()
+            self.timings["cx"] += time.perf_counter() - t0
+            self.unsorted = False
+            self.launch_log["sorts"] += 1
 
 
 def run(instructions: Sequence[Instruction], n: int, mode, eps: float = DEFAULT_EPS, *,
@@ -185,6 +253,10 @@ def run(instructions: Sequence[Instruction], n: int, mode, eps: float = DEFAULT_
         # If eps could already drop an initial term, merge after every step like the
         # reference does; otherwise deferring the re-sort of permutation steps is exact.
         eager = eps > min_abs
+        if initial is not None:
+            # caller-supplied generators may hold duplicate or sub-eps terms: canonicalize first
+            eager = eager or any(len(np.unique(k)) != len(k) for _, k in initial)
+        w.eager = eager
         trace = [list(w.ranks)]
 
         if mode is Mode.V1:
@@ -196,10 +268,7 @@ def run(instructions: Sequence[Instruction], n: int, mode, eps: float = DEFAULT_
             timings["lut"] = time.perf_counter() - t0
             _walk_operators(partition, lut, is_perm, tables, w, trace, counters, mode, eager)
 
-        # final canonical order
-        w.flush()
-        if w.unsorted:
-            w.merge(max(len(trace) - 2, 0), "cx")
+        w.finish(trace)                  # deferred merge, queued permutations, canonical order
         counters["operators"] = partition.k + partition.k_prime
 
         info = {"device": store.device, **w.launch_log}
@@ -232,17 +301,14 @@ class _Shard:
 
 def _walk_v1(instructions, partition, w: _Walker, trace, counters, eager):
     """Gate by gate (reference engine.py:155-180): rank snapshots at operator boundaries."""
-    n = w.n
     boundaries = set(np.cumsum(partition.operator_sizes()).tolist())
     w.updates = np.zeros(len(w.ids), dtype=np.int64)
     for pos, inst in enumerate(instructions, start=1):
-        w.updates += np.asarray(w.ranks, dtype=np.int64)      # terms present before this gate
         if inst.is_two_qubit:
+            w.count_gate()
             w.push_cx(*inst.wires)
             counters["cx_applications"] += 1
-            if eager:
-                w.flush()
-                w.merge(pos - 1, "cx")
+            w.step_done(pos - 1, "cx", trace)
         else:
             q = inst.wires[0]
             table = _lut.FIXED_PERMS.get(inst.gate)
@@ -251,20 +317,20 @@ def _walk_v1(instructions, partition, w: _Walker, trace, counters, eager):
                 block = _lut.gate_branch_block(inst.gate, inst.theta)
                 table = _lut.perm_word(block)
             if table is not None:
+                w.count_gate()
                 w.push_perm(q, table)
-                if eager:
-                    w.flush()
-                    w.merge(pos - 1, "sub_flatten")
+                w.step_done(pos - 1, "sub_flatten", trace)
             else:
+                w.resolve(trace)               # this gate must see merged terms
+                w.count_gate()
                 w.flush()
                 t0 = time.perf_counter()
                 w.store.apply_split(q, *split_tables(block))
                 w.timings["sub_flatten"] += time.perf_counter() - t0
-                w.launch_log["branch_ops"] += 1
-                w.merge(pos - 1, "sub_flatten", after_branch=True)
+                w.branched(pos - 1, "sub_flatten", trace)
             counters["v1_gate_applications"] = counters.get("v1_gate_applications", 0) + 1
         if pos in boundaries:
-            trace.append(list(w.ranks))
+            w.snapshot(trace)
 
 
 def _walk_operators(partition, lut, is_perm, tables, w: _Walker, trace, counters, mode, eager):
@@ -276,10 +342,9 @@ def _walk_operators(partition, lut, is_perm, tables, w: _Walker, trace, counters
             if bool(is_perm[ui].all()):
                 for j in np.flatnonzero(tables[ui] != _lut.IDENTITY_PERM):
                     w.push_perm(int(j), int(tables[ui][j]))
-                if eager:
-                    w.flush()
-                    w.merge(step, "sub_flatten")
+                w.step_done(step, "sub_flatten", trace)
             else:
+                w.resolve(trace)               # expand merged terms only
                 w.flush()
                 counts, axes, weights = _lut.operator_tables(lut[ui])
                 t0 = time.perf_counter()
@@ -287,26 +352,23 @@ def _walk_operators(partition, lut, is_perm, tables, w: _Walker, trace, counters
                     # dense layout: a branching substitution needs a 4**n scatter buffer
                     # (reference stabilizer.py:264-276); one-hot rows take the fast path
                     raw = w.store.count_operator(counts)
-                    if any(r > have for r, have in zip(raw, w.ranks)):
+                    if any(r > have for r, have in zip(raw, w.store.ranks())):
                         raise ResourceLimitError(
                             f"dense flatten needs a 4**{n}-element buffer (> {DENSE_FLATTEN_BUDGET}); "
                             "use the ragged layout for circuits of this size"
                         )
                 w.store.apply_operator(counts, axes, weights)
                 w.timings["sub_flatten"] += time.perf_counter() - t0
-                w.launch_log["branch_ops"] += 1
-                w.merge(step, "sub_flatten", after_branch=True)
+                w.branched(step, "sub_flatten", trace)
             counters["sub_flatten_ops"] += 1
             ui += 1
         else:
             for inst in partition.v_groups[vi]:
                 w.push_cx(*inst.wires)
                 counters["cx_applications"] += 1
-            if eager:
-                w.flush()
-                w.merge(step, "cx")
+            w.step_done(step, "cx", trace)
             vi += 1
-        trace.append(list(w.ranks))
+        w.snapshot(trace)
 
 
 def run_all_modes(instructions: Sequence[Instruction], n: int, eps: float = DEFAULT_EPS, **kw):

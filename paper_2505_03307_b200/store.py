@@ -89,7 +89,7 @@ class DeviceStore:
         nat.check(nat.lib().qx_store_download(self._h, nat.ptr(off), None, None, 0))
         total = int(off[-1])
         if pinned and total > 0:
-            buf = nat.PinnedBuffer(16 * total)
+            buf = nat.PINNED.take(16 * total)
             keys = buf.view(np.uint64, 0, total)
             lam = buf.view(np.float64, 8 * total, total)
         else:
@@ -149,6 +149,9 @@ class DeviceStore:
         out = np.zeros(self.n_segments, dtype=np.int64)
         nat.check(nat.lib().qx_merge(self._h, float(eps), nat.ptr(out)))
         return out.tolist()
+
+    def sort(self):
+        nat.check(nat.lib().qx_sort(self._h))
 
     def zi_sums(self) -> np.ndarray:
         out = np.zeros(self.n_segments, dtype=np.float64)

@@ -5,8 +5,12 @@ mkdir -p gpurun_out
 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/${R}_launches_c4_16_2.csv \
     python tools/profile_step.py --workload c4_xyz_16_2 --mode v3 --warmup 1 --steps 1 > gpurun_out/${R}_launches.log 2>&1
 for k in k_onesweep k_expand_emit k_reduce k_clifford_run k_sort_hist; do
-  skip=8; cnt=2
-  [ $k != k_onesweep ] && skip=2 && cnt=1
+  case $k in
+    k_onesweep) skip=8; cnt=2;;        # 8 passes per step: skip the warm-up step
+    k_expand_emit|k_clifford_run) skip=3; cnt=1;;   # 2 per step, the second one is the big one
+    k_reduce) skip=1; cnt=1;;
+    *) skip=2; cnt=1;;
+  esac
   timeout 900 ncu --set full --clock-control none --import-source on -k regex:$k -s $skip -c $cnt -f \
       -o gpurun_out/${R}_${k} python tools/profile_step.py --workload c4_xyz_14_2 --mode v3 --warmup 1 --steps 1 \
       > gpurun_out/${R}_${k}.log 2>&1
