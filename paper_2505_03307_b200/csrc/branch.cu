@@ -183,125 +183,98 @@ __device__ __forceinline__ int64_t last_le(const u64* a, int64_t n, u64 r) {
   return lo;
 }
 
-// One source term being enumerated: a mixed-radix counter over its non-identity digits.
-// The two least significant digits are advanced in registers; everything above them is
-// folded once into (p_hi, k_hi) and only recomputed when a carry leaves the low pair, i.e.
-// every c0*c1 outputs.  The product order stays the reference's: ((lambda * w_top ...) * w1) * w0.
-struct Branch {
-  u64 key;        // source word
-  u64 hi_mask;    // support bits above the low pair
-  u64 choice;     // current pick of every digit, 2 bits at the digit's position
-  u64 k_hi;       // output word assembled from the high digits
-  double lam;     // source coefficient
-  double p_hi;    // lam * product of the high digits' weights, qubit 0 first
-  int bit0, bit1; // positions of the two lowest support digits (-1 if absent)
-  u32 c0, c1;     // their radices
+// ---- working-key width ------------------------------------------------------------------
+// For n <= 16 a word fits 32 bits and a term has at most 3^16 < 2^32 branches, so the whole
+// enumeration runs on 32-bit registers (these kernels are ALU-bound: half the instructions).
+template <typename K> struct KeyOps;
+template <> struct KeyOps<u32> {
+  static __device__ __forceinline__ int lowest(u32 m) { return __ffs((int)m) - 1; }
+  static __device__ __forceinline__ int highest(u32 m) { return 31 - __clz((int)m); }
+  static __device__ __forceinline__ u32 support(u32 k) { return (k | (k >> 1)) & 0x55555555u; }
+};
+template <> struct KeyOps<u64> {
+  static __device__ __forceinline__ int lowest(u64 m) { return __ffsll((long long)m) - 1; }
+  static __device__ __forceinline__ int highest(u64 m) { return 63 - __clzll((long long)m); }
+  static __device__ __forceinline__ u64 support(u64 k) { return support_mask(k); }
 };
 
-__device__ __forceinline__ void fold_high(Branch& br, const OperatorTable& tb) {
-  double v = br.lam;
-  u64 out = 0;
-  for (u64 m = br.hi_mask; m;) {
-    const int bit = 63 - __clzll((long long)m);
-    m ^= 1ull << bit;
-    const u32 d = (u32)((br.key >> bit) & 3ull) - 1u;
-    const u32 pick = (u32)(br.choice >> bit) & 3u;
-    v *= tb.w[bit >> 1][d][pick];
-    out |= (u64)tb.axis[bit >> 1][d][pick] << bit;
+// ---- two-level branch decode --------------------------------------------------------------
+// A source term with non-identity digits d_0 < d_1 < ... (least significant first) and radices
+// c_i expands into prod c_i raw terms, branch id b = mixed-radix number with d_0 fastest.
+// Split the digits into a LOW group (d_0, d_1, d_2: L = c0*c1*c2 <= 27 branches) and the HIGH
+// rest.  All L branches of one "block" h = b / L share the high digits, i.e. the partial
+// product p_hi = lambda * w(top) * ... * w(d_3) and the partial word k_hi.  Per output tile:
+//   1. every source that feeds the tile counts the blocks it touches (prefix sum in smem);
+//   2. one thread per BLOCK decodes h and folds the high digits once into (p_hi, k_hi) in smem
+//      -- the only loops over digits, amortised over up to 27 outputs;
+//   3. one thread per OUTPUT (consecutive lanes = consecutive raw terms, so stores are fully
+//      coalesced) splits b into (h, three low picks), reads its block's (p_hi, k_hi) and does
+//      three multiplies, in the reference's order: ((p_hi * w2) * w1) * w0 with qubit 0 first.
+// Control flow in step 3 is uniform across the warp: no loops, no data-dependent branches.
+template <typename K>
+struct LowGroup {
+  int bit[3];      // digit positions (bit offsets), -1 if absent
+  u32 rad[3];      // radices (1 if absent)
+  u32 dig[3];      // input axis - 1 at those positions
+  K hi_mask;       // support bits above the group
+  u32 L;           // rad[0] * rad[1] * rad[2]
+};
+
+template <typename K>
+__device__ __forceinline__ LowGroup<K> low_group(K key, const OperatorTable& tb) {
+  LowGroup<K> g;
+  K m = KeyOps<K>::support(key);
+#pragma unroll
+  for (int j = 0; j < 3; ++j) {
+    g.bit[j] = -1;
+    g.rad[j] = 1;
+    g.dig[j] = 0;
+    if (m) {
+      const int bit = KeyOps<K>::lowest(m);
+      m &= m - 1;
+      g.bit[j] = bit;
+      g.dig[j] = (u32)((key >> bit) & 3u) - 1u;
+      g.rad[j] = tb.cnt[bit >> 1][g.dig[j]];
+    }
   }
-  br.p_hi = v;
-  br.k_hi = out;
+  g.hi_mask = m;
+  g.L = g.rad[0] * g.rad[1] * g.rad[2];
+  return g;
 }
 
-// position the counter of source (key, lam) at branch id b
-__device__ __forceinline__ void seek(Branch& br, u64 key, double lam, u64 b, const OperatorTable& tb) {
-  br.key = key;
-  br.lam = lam;
-  u64 m = support_mask(key);
-  br.bit0 = br.bit1 = -1;
-  br.c0 = br.c1 = 1;
-  if (m) {
-    br.bit0 = __ffsll((long long)m) - 1;
-    br.c0 = tb.cnt[br.bit0 >> 1][((key >> br.bit0) & 3ull) - 1];
-    m &= m - 1;
-  }
-  if (m) {
-    br.bit1 = __ffsll((long long)m) - 1;
-    br.c1 = tb.cnt[br.bit1 >> 1][((key >> br.bit1) & 3ull) - 1];
-    m &= m - 1;
-  }
-  br.hi_mask = m;
-  u64 choice = 0;
-  for (u64 mm = support_mask(key); mm;) {          // least significant digit first
-    const int bit = __ffsll((long long)mm) - 1;
-    mm &= mm - 1;
-    const u32 c = tb.cnt[bit >> 1][((key >> bit) & 3ull) - 1];
-    u32 pick = 0;
-    if (c == 2) { pick = (u32)(b & 1ull); b >>= 1; }
-    else if (c == 3) { const u64 q = b / 3ull; pick = (u32)(b - 3ull * q); b = q; }
-    choice |= (u64)pick << bit;
-  }
-  br.choice = choice;
-  fold_high(br, tb);
+// q = b / c, r = b % c for c in {1, 2, 3} without a divide
+template <typename K>
+__device__ __forceinline__ void divmod_small(K b, u32 c, K& q, u32& r) {
+  if (c == 1) { q = b; r = 0; }
+  else if (c == 2) { q = b >> 1; r = (u32)(b & 1u); }
+  else { q = b / 3u; r = (u32)(b - 3u * q); }
 }
 
-__device__ __forceinline__ void emit_one(const Branch& br, const OperatorTable& tb, u64& out_key,
-                                         double& out_lam) {
-  double v = br.p_hi;
-  u64 k = br.k_hi;
-  if (br.bit1 >= 0) {
-    const u32 d = (u32)((br.key >> br.bit1) & 3ull) - 1u, pick = (u32)(br.choice >> br.bit1) & 3u;
-    v *= tb.w[br.bit1 >> 1][d][pick];
-    k |= (u64)tb.axis[br.bit1 >> 1][d][pick] << br.bit1;
-  }
-  if (br.bit0 >= 0) {
-    const u32 d = (u32)((br.key >> br.bit0) & 3ull) - 1u, pick = (u32)(br.choice >> br.bit0) & 3u;
-    v *= tb.w[br.bit0 >> 1][d][pick];
-    k |= (u64)tb.axis[br.bit0 >> 1][d][pick] << br.bit0;
-  }
-  out_key = k;
-  out_lam = v;
-}
+constexpr int kEmitPer = 8;                          // outputs per thread, striped
+constexpr int kEmitTile = kThreads * kEmitPer;       // 2048 raw terms per tile
 
-// next branch of the same source (caller guarantees there is one)
-__device__ __forceinline__ void advance(Branch& br, const OperatorTable& tb) {
-  if (br.bit0 >= 0) {
-    const u32 p0 = (u32)(br.choice >> br.bit0) & 3u;
-    if (p0 + 1 < br.c0) { br.choice += 1ull << br.bit0; return; }
-    br.choice &= ~(3ull << br.bit0);
-  }
-  if (br.bit1 >= 0) {
-    const u32 p1 = (u32)(br.choice >> br.bit1) & 3u;
-    if (p1 + 1 < br.c1) { br.choice += 1ull << br.bit1; return; }
-    br.choice &= ~(3ull << br.bit1);
-  }
-  for (u64 m = br.hi_mask; m;) {                   // carry into the high digits
-    const int bit = __ffsll((long long)m) - 1;
-    m &= m - 1;
-    const u32 c = tb.cnt[bit >> 1][((br.key >> bit) & 3ull) - 1];
-    const u32 p = (u32)(br.choice >> bit) & 3u;
-    if (p + 1 < c) { br.choice += 1ull << bit; break; }
-    br.choice &= ~(3ull << bit);
-  }
-  fold_high(br, tb);
-}
+template <typename K>
+struct EmitSmem {
+  OperatorTable tb;
+  u64 win[kEmitTile + 2];      // raw offsets of the sources feeding the tile (+ end sentinel)
+  u32 blk[kEmitTile + 2];      // exclusive prefix of blocks per source
+  double p_hi[kEmitTile + 1];
+  K k_hi[kEmitTile + 1];
+  u32 scan[kThreads / 32 + 1];
+  int64_t lohi[2];
+  u64 hfirst0;                 // first block id of the first source (it may start mid-way)
+};
 
-constexpr int kEmitPer = 8;                         // consecutive outputs per thread
-constexpr int kEmitTile = kThreads * kEmitPer;
-
-// One thread produces kEmitPer CONSECUTIVE raw terms (64 B of keys + 64 B of coefficients,
-// written with 128-bit stores): consecutive branch ids differ only in their low digits, so
-// the per-term work is two table look-ups and two multiplies instead of a full decode.
+template <typename K>
 __global__ void __launch_bounds__(kThreads)
 k_expand_emit(const u64* __restrict__ keys_in, const double* __restrict__ lam_in,
               const u64* __restrict__ roff, int64_t total_in, u64* __restrict__ keys_out,
               double* __restrict__ lam_out, const __grid_constant__ OperatorTable tb) {
-  __shared__ OperatorTable s_tb;
-  __shared__ u64 s_win[kEmitTile + 2];
-  __shared__ int64_t s_lohi[2];
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  EmitSmem<K>& sm = *reinterpret_cast<EmitSmem<K>*>(smem_raw);
   {
     const u32* src = reinterpret_cast<const u32*>(&tb);
-    u32* dst = reinterpret_cast<u32*>(&s_tb);
+    u32* dst = reinterpret_cast<u32*>(&sm.tb);
     for (int i = threadIdx.x; i < (int)(sizeof(OperatorTable) / 4); i += kThreads) dst[i] = src[i];
   }
   const u64 raw_total = roff[total_in];
@@ -309,53 +282,95 @@ k_expand_emit(const u64* __restrict__ keys_in, const double* __restrict__ lam_in
   for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
     const u64 r0 = (u64)tile * kEmitTile;
     const u64 r1 = min(r0 + (u64)kEmitTile, raw_total);          // exclusive
-    __syncthreads();                                             // previous window fully consumed
-    if (threadIdx.x == 0) s_lohi[0] = last_le(roff, total_in, r0);
-    if (threadIdx.x == 32) s_lohi[1] = last_le(roff, total_in, r1 - 1);
+    __syncthreads();                                             // previous tile fully consumed
+    if (threadIdx.x == 0) sm.lohi[0] = last_le(roff, total_in, r0);
+    if (threadIdx.x == 32) sm.lohi[1] = last_le(roff, total_in, r1 - 1);
     __syncthreads();
-    const int64_t lo = s_lohi[0], hi = s_lohi[1];
-    const int span = (int)(hi - lo) + 1;                          // source terms feeding this tile
-    for (int i = threadIdx.x; i <= span; i += kThreads) s_win[i] = roff[lo + i];   // + end sentinel
+    const int64_t lo = sm.lohi[0], hi = sm.lohi[1];
+    const int span = (int)(hi - lo) + 1;                          // sources feeding this tile
+    for (int i = threadIdx.x; i <= span; i += kThreads) sm.win[i] = roff[lo + i];
     __syncthreads();
-    const u64 rbeg = r0 + (u64)threadIdx.x * kEmitPer;
-    if (rbeg >= r1) continue;
-    const int todo = (int)min((u64)kEmitPer, r1 - rbeg);
-    int rel = (int)last_le(s_win, span, rbeg);
-    Branch br;
-    seek(br, keys_in[lo + rel], lam_in[lo + rel], rbeg - s_win[rel], s_tb);
-    u64 left = s_win[rel + 1] - rbeg;                             // branches left in this source
-    u64 ok[kEmitPer];
-    double ov[kEmitPer];
-#pragma unroll
-    for (int k = 0; k < kEmitPer; ++k) {
-      if (k < todo) {
-        emit_one(br, s_tb, ok[k], ov[k]);
-        if (k + 1 < todo) {
-          if (--left == 0) {
-            ++rel;
-            seek(br, keys_in[lo + rel], lam_in[lo + rel], 0ull, s_tb);
-            left = s_win[rel + 1] - s_win[rel];
-          } else {
-            advance(br, s_tb);
-          }
-        }
+
+    // ---- 1. blocks per source, exclusive prefix (chunks of kThreads sources)
+    u32 carried = 0;
+    for (int base = 0; base < span; base += kThreads) {
+      const int rel = base + threadIdx.x;
+      u32 nb = 0;
+      if (rel < span) {
+        const LowGroup<K> g = low_group<K>((K)keys_in[lo + rel], sm.tb);
+        const u64 bb = (rel == 0 ? r0 : sm.win[rel]) - sm.win[rel];
+        const u64 be = min(sm.win[rel + 1], r1) - sm.win[rel];     // exclusive, > bb
+        const u64 hf = bb / g.L;
+        nb = (u32)((be - 1) / g.L - hf) + 1u;
+        if (rel == 0) sm.hfirst0 = hf;
       }
+      u32 total;
+      const u32 excl = block_exclusive_sum<u32>(nb, sm.scan, total);
+      if (rel < span) sm.blk[rel] = carried + excl;
+      carried += total;
     }
-    if (todo == kEmitPer) {
-      ulonglong2* kp = reinterpret_cast<ulonglong2*>(keys_out + rbeg);
-      double2* vp = reinterpret_cast<double2*>(lam_out + rbeg);
-#pragma unroll
-      for (int k = 0; k < kEmitPer; k += 2) {
-        __stcs(kp + (k >> 1), make_ulonglong2(ok[k], ok[k + 1]));
-        __stcs(vp + (k >> 1), make_double2(ov[k], ov[k + 1]));
+    if (threadIdx.x == 0) sm.blk[span] = carried;
+    __syncthreads();
+
+    // ---- 2. fold the high digits of every block once
+    const int n_blocks = (int)sm.blk[span];
+    for (int e = threadIdx.x; e < n_blocks; e += kThreads) {
+      int a = 0, z = span;                                        // last rel with blk[rel] <= e
+      while (z - a > 1) {
+        const int mid = (a + z) >> 1;
+        if (sm.blk[mid] <= (u32)e) a = mid; else z = mid;
       }
-    } else {
+      const K key = (K)keys_in[lo + a];
+      const LowGroup<K> g = low_group<K>(key, sm.tb);
+      K h = (K)(a == 0 ? sm.hfirst0 : 0ull) + (K)((u32)e - sm.blk[a]);
+      // decode h over the high digits (least significant first), remember the picks
+      K choice = 0;
+      for (K m = g.hi_mask; m;) {
+        const int bit = KeyOps<K>::lowest(m);
+        m &= m - 1;
+        u32 pick;
+        divmod_small<K>(h, sm.tb.cnt[bit >> 1][(u32)((key >> bit) & 3u) - 1u], h, pick);
+        choice |= (K)pick << bit;
+      }
+      // fold: qubit 0 (most significant digit) first, like stabilizer.py:311-319
+      double v = lam_in[lo + a];
+      K out = 0;
+      for (K m = g.hi_mask; m;) {
+        const int bit = KeyOps<K>::highest(m);
+        m ^= (K)1 << bit;
+        const u32 d = (u32)((key >> bit) & 3u) - 1u, pick = (u32)(choice >> bit) & 3u;
+        v *= sm.tb.w[bit >> 1][d][pick];
+        out |= (K)sm.tb.axis[bit >> 1][d][pick] << bit;
+      }
+      sm.p_hi[e] = v;
+      sm.k_hi[e] = out;
+    }
+    __syncthreads();
+
+    // ---- 3. one raw term per thread per round, consecutive lanes = consecutive terms
+#pragma unroll 2
+    for (int k = 0; k < kEmitPer; ++k) {
+      const u64 r = r0 + (u64)k * kThreads + threadIdx.x;
+      if (r >= r1) break;
+      const int rel = span == 1 ? 0 : (int)last_le(sm.win, span, r);
+      const K key = (K)keys_in[lo + rel];
+      const LowGroup<K> g = low_group<K>(key, sm.tb);
+      K q = (K)(r - sm.win[rel]);
+      u32 pick[3];
 #pragma unroll
-      for (int k = 0; k < kEmitPer; ++k)
-        if (k < todo) {
-          keys_out[rbeg + k] = ok[k];
-          lam_out[rbeg + k] = ov[k];
+      for (int j = 0; j < 3; ++j) divmod_small<K>(q, g.rad[j], q, pick[j]);
+      const u32 e = sm.blk[rel] + (u32)(q - (K)(rel == 0 ? sm.hfirst0 : 0ull));
+      double v = sm.p_hi[e];
+      K out = sm.k_hi[e];
+#pragma unroll
+      for (int j = 2; j >= 0; --j) {
+        if (g.bit[j] >= 0) {
+          v *= sm.tb.w[g.bit[j] >> 1][g.dig[j]][pick[j]];
+          out |= (K)sm.tb.axis[g.bit[j] >> 1][g.dig[j]][pick[j]] << g.bit[j];
         }
+      }
+      st_stream(keys_out + r, (u64)out);
+      st_stream(lam_out + r, v);
     }
   }
 }
@@ -512,8 +527,20 @@ extern "C" int qx_apply_operator(qx_store* s, const int32_t* counts, const int32
     const int64_t tiles = (raw + kEmitTile - 1) / kEmitTile;
     const int grid = (int)std::min<int64_t>(tiles, (int64_t)s->sm_count * 8);
     QxProfileScope prof(QX_K_EXPAND_EMIT, s->stream, 16.0 * ((double)total_in + (double)raw));
-    k_expand_emit<<<grid, kThreads, 0, s->stream>>>(s->keys[in2], s->lam[in2], roff, total_in,
-                                                    s->keys[out2], s->lam[out2], tb);
+    static bool attr_set = false;
+    if (!attr_set) {
+      QX_CUDA(cudaFuncSetAttribute(k_expand_emit<u32>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)sizeof(EmitSmem<u32>)));
+      QX_CUDA(cudaFuncSetAttribute(k_expand_emit<u64>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)sizeof(EmitSmem<u64>)));
+      attr_set = true;
+    }
+    if (s->n_qubits <= 16)
+      k_expand_emit<u32><<<grid, kThreads, sizeof(EmitSmem<u32>), s->stream>>>(
+          s->keys[in2], s->lam[in2], roff, total_in, s->keys[out2], s->lam[out2], tb);
+    else
+      k_expand_emit<u64><<<grid, kThreads, sizeof(EmitSmem<u64>), s->stream>>>(
+          s->keys[in2], s->lam[in2], roff, total_in, s->keys[out2], s->lam[out2], tb);
     QX_CUDA(cudaGetLastError());
   }
   (void)in; (void)out;

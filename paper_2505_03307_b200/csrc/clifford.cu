@@ -24,13 +24,16 @@ struct CxTables {
   u32 c, t, s;
 };
 
-__device__ __forceinline__ void apply_op(u32 op, u64& key, u32& neg, const CxTables cx) {
+// K = u32 when the word fits 32 bits (n <= 16): the kernel is ALU-bound and 64-bit variable
+// shifts cost two to three instructions each.
+template <typename K>
+__device__ __forceinline__ void apply_op(u32 op, K& key, u32& neg, const CxTables cx) {
   const u32 s0 = (op >> 2) & 63u;
   const u32 d0 = (u32)(key >> s0) & 3u;
   if ((op & 3u) == 0u) {
     const u32 nd = (op >> (16u + 2u * d0)) & 3u;
     neg ^= (op >> (24u + d0)) & 1u;
-    key ^= (u64)(d0 ^ nd) << s0;
+    key ^= (K)(d0 ^ nd) << s0;
   } else {
     const u32 s1 = (op >> 8) & 63u;
     const u32 d1 = (u32)(key >> s1) & 3u;
@@ -38,10 +41,11 @@ __device__ __forceinline__ void apply_op(u32 op, u64& key, u32& neg, const CxTab
     const u32 n0 = (cx.c >> (2u * e)) & 3u;
     const u32 n1 = (cx.t >> (2u * e)) & 3u;
     neg ^= (cx.s >> e) & 1u;
-    key ^= ((u64)(d0 ^ n0) << s0) | ((u64)(d1 ^ n1) << s1);
+    key ^= ((K)(d0 ^ n0) << s0) | ((K)(d1 ^ n1) << s1);
   }
 }
 
+template <typename K>
 __global__ void __launch_bounds__(kThreads)
 k_clifford_run(u64* __restrict__ keys, double* __restrict__ lam,
                const int64_t* __restrict__ seg_off, int n_seg,
@@ -56,14 +60,14 @@ k_clifford_run(u64* __restrict__ keys, double* __restrict__ lam,
   double2* lam2 = reinterpret_cast<double2*>(lam);
   for (int64_t p = (int64_t)blockIdx.x * kThreads + threadIdx.x; p < pairs; p += stride) {
     ulonglong2 k = __ldcs(keys2 + p);
-    u64 ka = k.x, kb = k.y;
+    K ka = (K)k.x, kb = (K)k.y;
     u32 na = 0, nb = 0;
     for (int i = 0; i < n_ops; ++i) {
       const u32 op = prog[i];
-      apply_op(op, ka, na, cx);
-      apply_op(op, kb, nb, cx);
+      apply_op<K>(op, ka, na, cx);
+      apply_op<K>(op, kb, nb, cx);
     }
-    __stcs(keys2 + p, make_ulonglong2(ka, kb));
+    __stcs(keys2 + p, make_ulonglong2((u64)ka, (u64)kb));
     if (na | nb) {                       // sign flips are exact: only touch lambda when needed
       double2 l = lam2[p];
       if (na) l.x = -l.x;
@@ -73,10 +77,10 @@ k_clifford_run(u64* __restrict__ keys, double* __restrict__ lam,
   }
   if ((total & 1) && blockIdx.x == 0 && threadIdx.x == 0) {
     const int64_t i = total - 1;
-    u64 k = keys[i];
+    K k = (K)keys[i];
     u32 neg = 0;
-    for (int j = 0; j < n_ops; ++j) apply_op(prog[j], k, neg, cx);
-    keys[i] = k;
+    for (int j = 0; j < n_ops; ++j) apply_op<K>(prog[j], k, neg, cx);
+    keys[i] = (u64)k;
     if (neg) lam[i] = -lam[i];
   }
 }
@@ -111,9 +115,12 @@ extern "C" int qx_apply_clifford(qx_store* s, const uint32_t* program, int32_t n
     QX_CUDA(cudaMemcpyAsync(s->scratch, program + done, sizeof(u32) * (size_t)chunk,
                             cudaMemcpyHostToDevice, s->stream));
     QxProfileScope prof(QX_K_CLIFFORD, s->stream, 32.0 * (double)s->ub_total);
-    k_clifford_run<<<grid, kThreads, 0, s->stream>>>(s->keys[s->cur], s->lam[s->cur],
-                                                     s->seg[s->cur], s->n_seg,
-                                                     (const u32*)s->scratch, chunk, cx);
+    if (s->n_qubits <= 16)
+      k_clifford_run<u32><<<grid, kThreads, 0, s->stream>>>(s->keys[s->cur], s->lam[s->cur], s->seg[s->cur],
+                                                            s->n_seg, (const u32*)s->scratch, chunk, cx);
+    else
+      k_clifford_run<u64><<<grid, kThreads, 0, s->stream>>>(s->keys[s->cur], s->lam[s->cur], s->seg[s->cur],
+                                                            s->n_seg, (const u32*)s->scratch, chunk, cx);
     QX_CUDA(cudaGetLastError());
   }
   return QX_OK;
