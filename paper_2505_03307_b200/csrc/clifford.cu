@@ -11,6 +11,8 @@
 //
 // HBM-bound elementwise kernel: 128-bit loads/stores (two terms per thread per
 // step), gate program broadcast from shared memory, grid = SMs * resident CTAs.
+#include <string.h>
+
 #include <algorithm>
 
 #include "qx_device.cuh"
@@ -18,7 +20,15 @@
 namespace {
 
 constexpr int kThreads = 256;
-constexpr int kProgChunk = 2048;    // ops staged in shared memory per launch
+constexpr int kProgChunk = 960;     // ops per launch: the program travels as a kernel parameter
+
+// The gate program sits in the parameter (constant) bank: every thread reads the same word,
+// so the field decode (kind, shifts, table) runs once per warp on the uniform datapath
+// instead of once per thread.
+struct Program {
+  u32 n_ops;
+  u32 ops[kProgChunk];
+};
 
 struct CxTables {
   u32 c, t, s;
@@ -49,10 +59,9 @@ template <typename K>
 __global__ void __launch_bounds__(kThreads)
 k_clifford_run(u64* __restrict__ keys, double* __restrict__ lam,
                const int64_t* __restrict__ seg_off, int n_seg,
-               const u32* __restrict__ program, int n_ops, CxTables cx) {
-  __shared__ u32 prog[kProgChunk];
-  for (int i = threadIdx.x; i < n_ops; i += kThreads) prog[i] = program[i];
-  __syncthreads();
+               const __grid_constant__ Program pg, const CxTables cx) {
+  const int n_ops = (int)pg.n_ops;
+  const u32* prog = pg.ops;
   const int64_t total = seg_off[n_seg];
   const int64_t pairs = total >> 1;
   const int64_t stride = (int64_t)gridDim.x * kThreads;
@@ -104,23 +113,22 @@ extern "C" int qx_apply_clifford(qx_store* s, const uint32_t* program, int32_t n
     }
   }
   QX_CUDA(cudaSetDevice(s->device));
-  QX_TRY(qx_store_scratch(s, sizeof(u32) * (size_t)kProgChunk));
   const int64_t ub = std::max<int64_t>(s->ub_total, 1);
   const int64_t want = (ub / 2 + kThreads - 1) / kThreads;
   const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)s->sm_count * 8));
   const CxTables cx = {cx_c, cx_t, cx_s};
+  static Program pg;       // host staging; the launch copies it into the parameter buffer
   for (int done = 0; done < n_ops; done += kProgChunk) {
     const int chunk = std::min(kProgChunk, n_ops - done);
-    // pageable source: the copy is staged before the call returns, so `program` may be reused
-    QX_CUDA(cudaMemcpyAsync(s->scratch, program + done, sizeof(u32) * (size_t)chunk,
-                            cudaMemcpyHostToDevice, s->stream));
+    pg.n_ops = (u32)chunk;
+    memcpy(pg.ops, program + done, sizeof(u32) * (size_t)chunk);
     QxProfileScope prof(QX_K_CLIFFORD, s->stream, 32.0 * (double)s->ub_total);
     if (s->n_qubits <= 16)
       k_clifford_run<u32><<<grid, kThreads, 0, s->stream>>>(s->keys[s->cur], s->lam[s->cur], s->seg[s->cur],
-                                                            s->n_seg, (const u32*)s->scratch, chunk, cx);
+                                                            s->n_seg, pg, cx);
     else
       k_clifford_run<u64><<<grid, kThreads, 0, s->stream>>>(s->keys[s->cur], s->lam[s->cur], s->seg[s->cur],
-                                                            s->n_seg, (const u32*)s->scratch, chunk, cx);
+                                                            s->n_seg, pg, cx);
     QX_CUDA(cudaGetLastError());
   }
   return QX_OK;

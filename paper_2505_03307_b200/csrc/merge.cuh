@@ -159,12 +159,44 @@ struct SortSmem {
 // THREADS x ITEMS terms per tile, warp-striped.  EARLY: issue the coefficient loads right
 // after ranking so their HBM latency hides behind the digit scan and the look-back instead
 // of being exposed before the shared-memory scatter (costs ITEMS * sizeof(V) / 4 registers).
+// Lanes of the warp whose 8-bit digit equals mine.  Hand-scheduled: one R2P moves the digit's
+// bits into predicates, then per bit one VOTE and two logic ops (the compiler's version of the
+// same loop spends six instructions per bit; this kernel is issue-bound, profiles/r01b).
+__device__ __forceinline__ u32 match_digit8(u32 d) {
+  u32 peers;
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      ".reg .b32 v, t;\n"
+      "mov.b32 %0, 0xffffffff;\n"
+#define QX_MATCH_BIT(m)                                  \
+      "and.b32 t, %1, " #m ";\n"                         \
+      "setp.ne.b32 p, t, 0;\n"                           \
+      "vote.sync.ballot.b32 v, p, 0xffffffff;\n"         \
+      "@!p not.b32 v, v;\n"                              \
+      "and.b32 %0, %0, v;\n"
+      QX_MATCH_BIT(1) QX_MATCH_BIT(2) QX_MATCH_BIT(4) QX_MATCH_BIT(8)
+      QX_MATCH_BIT(16) QX_MATCH_BIT(32) QX_MATCH_BIT(64) QX_MATCH_BIT(128)
+#undef QX_MATCH_BIT
+      "}\n"
+      : "=r"(peers)
+      : "r"(d));
+  return peers;
+}
+
+// digit = byte `which` of the key: one PRMT on the right half instead of a 64-bit shift + mask
+__device__ __forceinline__ u32 key_byte(u64 key, int which) {
+  const u32 half = which < 4 ? (u32)key : (u32)(key >> 32);
+  return __byte_perm(half, 0u, 0x4440u | (u32)(which & 3));
+}
+
 template <typename V, int THREADS, int ITEMS, bool EARLY>
-__global__ void __launch_bounds__(THREADS)
+__global__ void __launch_bounds__(THREADS, (THREADS <= 256 ? 3 : 2))
 k_onesweep(const u64* __restrict__ keys_in, const V* __restrict__ vals_in,
            u64* __restrict__ keys_out, V* __restrict__ vals_out,
            const int64_t* __restrict__ seg, int n_seg, const int64_t* __restrict__ tile_prefix,
-           const u32* __restrict__ digit_base, int base_stride, u32* status, u32* ticket, int shift) {
+           const u32* __restrict__ digit_base, int base_stride, u32* status, u32* ticket, int which,
+           int ahead, int debug) {
   constexpr int WARPS = THREADS / 32;
   constexpr int TILE = THREADS * ITEMS;
   static_assert(THREADS >= QX_RADIX, "one thread per digit in the scan");
@@ -181,52 +213,46 @@ k_onesweep(const u64* __restrict__ keys_in, const V* __restrict__ vals_in,
   const bool first = tile == tile_prefix[g];
   const int64_t start = seg[g] + (tile - tile_prefix[g]) * TILE;
   const int count = (int)min((int64_t)TILE, seg[g + 1] - start);
+  const bool full = count == TILE;
+  const u64* kin = keys_in + start;
+  const V* vin = vals_in + start;
+
+  // ---- L2 prefetch of the tile that a CTA will own `ahead` tickets from now.  Tickets are
+  // handed out in order, so every tile is prefetched exactly once, by the CTA `ahead` tiles
+  // before it; with ahead ~ number of resident CTAs the lines arrive in L2 just before use and
+  // the loads below pay L2 latency instead of HBM latency.
+  if (ahead > 0 && tile + ahead < tile_prefix[n_seg]) {
+    const int64_t tp = tile + ahead;
+    const int gp = tile_segment(tile_prefix, n_seg, tp);
+    const int64_t sp = seg[gp] + (tp - tile_prefix[gp]) * TILE;
+    const int cp = (int)min((int64_t)TILE, seg[gp + 1] - sp);
+    for (int i = tid * 16; i < cp; i += THREADS * 16) {
+      asm volatile("prefetch.global.L2 [%0];" ::"l"(keys_in + sp + i));
+      asm volatile("prefetch.global.L2 [%0];" ::"l"(vals_in + sp + i));
+      if (sizeof(V) > 8) asm volatile("prefetch.global.L2 [%0];" ::"l"(vals_in + sp + i + 8));
+    }
+  }
 
   // ---- load, warp-striped: warp w owns tile slots [w*32*ITEMS, (w+1)*32*ITEMS)
   u64 key[ITEMS];
-  u32 rank[ITEMS];
   const int wslot = warp * (32 * ITEMS) + lane;
+  if (full) {
 #pragma unroll
-  for (int k = 0; k < ITEMS; ++k) {
-    const int idx = wslot + k * 32;
-    key[k] = idx < count ? ld_stream(keys_in + start + idx) : ~0ull;   // padding sorts last
-  }
-  // ---- rank inside the warp.  Lanes with equal digits form a group; the group mask comes
-  // from 8 ballots (one per digit bit) -- the MATCH instruction costs one trip through the
-  // ADU pipe per distinct value and made this kernel latency-bound (profiles/r01).  The
-  // lowest lane of each group bumps the warp's digit counter with ONE shared-memory atomic
-  // and everyone takes old + position in group.  __syncwarp orders item k's update before
-  // item k+1's (different lanes may lead), which is what makes the ranking stable; the
-  // broadcast of `old` is deferred so the ballot groups pipeline.
-  u32 meta[ITEMS];                           // leader lane | lanes below me << 5
-#pragma unroll
-  for (int k = 0; k < ITEMS; ++k) {
-    const u32 d = (u32)(key[k] >> shift) & (QX_RADIX - 1);
-    u32 peers = QX_FULL_MASK;
-#pragma unroll
-    for (int b = 0; b < QX_RADIX_BITS; ++b) {
-      const bool bit = (d >> b) & 1u;
-      const u32 votes = __ballot_sync(QX_FULL_MASK, bit);
-      peers &= bit ? votes : ~votes;
-    }
-    const u32 below = __popc(peers & lanemask_lt());
-    u32 old = 0;
-    if (below == 0) old = atomicAdd(&sm.whist[warp][d], (u32)__popc(peers));
-    rank[k] = old;
-    meta[k] = (u32)(__ffs(peers) - 1) | (below << 5);
-    __syncwarp();
-  }
-  V val[EARLY ? ITEMS : 1];
-  if (EARLY) {
+    for (int k = 0; k < ITEMS; ++k) key[k] = ld_stream(kin + wslot + k * 32);
+  } else {
 #pragma unroll
     for (int k = 0; k < ITEMS; ++k) {
       const int idx = wslot + k * 32;
-      if (idx < count) val[EARLY ? k : 0] = ld_stream(vals_in + start + idx);
+      key[k] = idx < count ? ld_stream(kin + idx) : ~0ull;          // padding sorts last
     }
   }
+
+  // ---- early counts: per-warp digit histogram with fire-and-forget shared atomics.  Order
+  // does not matter for counts, so the tile's aggregate can be published for the tiles behind
+  // us BEFORE the (much longer) stable ranking -- their look-back then overlaps our ranking
+  // instead of waiting for it (look-back stalls were 26 % of the pass, profiles/r01d).
 #pragma unroll
-  for (int k = 0; k < ITEMS; ++k)
-    rank[k] = __shfl_sync(QX_FULL_MASK, rank[k], meta[k] & 31u) + (meta[k] >> 5);
+  for (int k = 0; k < ITEMS; ++k) atomicAdd(&sm.whist[warp][key_byte(key[k], which)], 1u);
   __syncthreads();
 
   // ---- per digit: exclusive offsets over warps, tile totals, exclusive scan over digits
@@ -241,24 +267,69 @@ k_onesweep(const u64* __restrict__ keys_in, const V* __restrict__ vals_in,
   }
   u32 tile_sum;
   const u32 dstart = block_exclusive_sum<u32>(digit_total, sm.scan, tile_sum);
+  // padding keys all carry digit 255 and sit behind the live ones
+  const u32 live_total = digit_total - ((tid == QX_RADIX - 1) ? (u32)(TILE - count) : 0u);
+  u32* mine = status + (size_t)tile * QX_RADIX + tid;
+  const bool solo = first || (debug & 1);
   if (tid < QX_RADIX) {
     sm.tile_start[tid] = dstart;
-    // padding keys all carry digit 255 and sit behind the live ones
-    const u32 live_total = digit_total - ((tid == QX_RADIX - 1) ? (u32)(TILE - count) : 0u);
-    // ---- decoupled look-back, one chain per digit, confined to this segment's tiles
-    u32* mine = status + (size_t)tile * QX_RADIX + tid;
+    st_volatile_u32(mine, (solo ? kFlagInc : kFlagAgg) | live_total);
+  }
+  __syncthreads();
+
+  // ---- stable rank inside the warp, straight into the tile-sorted slot.  Lanes with equal
+  // digits form a group (match_digit8); the lowest lane advances the warp's running offset
+  // for that digit with one shared atomic and everyone takes old + position in group.  The
+  // shuffle that broadcasts `old` also orders item k's update before item k+1's (different
+  // lanes may lead), which is what makes the ranking stable.
+  u32 slot[ITEMS];
+#pragma unroll
+  for (int k = 0; k < ITEMS; ++k) {
+    const u32 d = key_byte(key[k], which);
+    const u32 peers = match_digit8(d);
+    const u32 below = __popc(peers & lanemask_lt());
+    u32 old = 0;
+    if (below == 0) old = atomicAdd(&sm.whist[warp][d], (u32)__popc(peers));
+    slot[k] = sm.tile_start[d] + __shfl_sync(QX_FULL_MASK, old, __ffs(peers) - 1) + below;
+    sm.keys[slot[k]] = key[k];
+  }
+  // coefficients: twelve independent loads in flight, landing while the look-back below runs
+  if (full) {
+#pragma unroll
+    for (int k = 0; k < ITEMS; ++k) sm.vals[slot[k]] = ld_stream(vin + wslot + k * 32);
+  } else {
+#pragma unroll
+    for (int k = 0; k < ITEMS; ++k) {
+      const int idx = wslot + k * 32;
+      if (idx < count) sm.vals[slot[k]] = ld_stream(vin + idx);
+    }
+  }
+
+  // ---- decoupled look-back, one chain per digit, confined to this segment's tiles.  Eight
+  // predecessors are read per round trip: with ~300 tiles in flight the nearest inclusive
+  // prefix is typically a dozen tiles back, and walking there one dependent L2 load at a
+  // time was the critical path of the kernel.
+  if (tid < QX_RADIX) {
     u32 excl = 0;
-    if (first) {
-      st_volatile_u32(mine, kFlagInc | live_total);
-    } else {
-      st_volatile_u32(mine, kFlagAgg | live_total);
-      const u32* prev = mine - QX_RADIX;
-      while (true) {
-        u32 w;
-        do { w = ld_volatile_u32(prev); } while ((w >> 30) == 0u);
-        excl += w & kFlagVal;
-        if ((w >> 30) == 2u) break;
-        prev -= QX_RADIX;
+    if (!solo) {
+      constexpr int W = 8;
+      const int64_t first_tile = tile_prefix[g];
+      int64_t t = tile - 1;
+      bool done = false;
+      while (!done) {
+        u32 w[W];
+#pragma unroll
+        for (int j = 0; j < W; ++j)
+          w[j] = (t - j >= first_tile) ? ld_volatile_u32(status + (size_t)(t - j) * QX_RADIX + tid) : kFlagInc;
+#pragma unroll
+        for (int j = 0; j < W; ++j) {
+          if (!done) {
+            while ((w[j] >> 30) == 0u) w[j] = ld_volatile_u32(status + (size_t)(t - j) * QX_RADIX + tid);
+            excl += w[j] & kFlagVal;
+            done = (w[j] >> 30) == 2u;
+          }
+        }
+        t -= W;
       }
       st_volatile_u32(mine, kFlagInc | (excl + live_total));
     }
@@ -267,27 +338,13 @@ k_onesweep(const u64* __restrict__ keys_in, const V* __restrict__ vals_in,
   }
   __syncthreads();
 
-  // ---- scatter into tile-sorted order in shared memory
-#pragma unroll
-  for (int k = 0; k < ITEMS; ++k) {
-    const u32 d = (u32)(key[k] >> shift) & (QX_RADIX - 1);
-    rank[k] += sm.tile_start[d] + sm.whist[warp][d];
-    sm.keys[rank[k]] = key[k];
-  }
-#pragma unroll
-  for (int k = 0; k < ITEMS; ++k) {
-    const int idx = wslot + k * 32;
-    if (idx < count) sm.vals[rank[k]] = EARLY ? val[EARLY ? k : 0] : ld_stream(vals_in + start + idx);
-  }
-  __syncthreads();
-
   // ---- coalesced write-out: consecutive slots of one digit are consecutive in HBM
 #pragma unroll
   for (int k = 0; k < ITEMS; ++k) {
     const int slot = k * THREADS + tid;
-    if (slot < count) {
+    if (full || slot < count) {
       const u64 kk = sm.keys[slot];
-      const int64_t dst = sm.gbase[(u32)(kk >> shift) & (QX_RADIX - 1)] + slot;
+      const int64_t dst = sm.gbase[key_byte(kk, which)] + slot;
       st_stream(keys_out + dst, kk);
       st_stream(vals_out + dst, sm.vals[slot]);
     }
@@ -574,9 +631,18 @@ struct SortVariant {
   const char* name;
 };
 
+inline int sort_prefetch_distance(int sm_count) {
+  static int v = -2;
+  if (v == -2) {
+    const char* e = getenv("QX_SORT_PREFETCH");
+    v = e ? atoi(e) : -1;
+  }
+  return v >= 0 ? v : 2 * sm_count;     // ~ resident CTAs (two per SM)
+}
+
 template <typename V, int THREADS, int ITEMS, bool EARLY>
 int launch_pass(QxArena* ar, MergeBuffers<V>& mb, int cur, int64_t tiles_ub, const int64_t* tile_prefix,
-                const u32* digit_base, int base_stride, u32* ticket, int shift) {
+                const u32* digit_base, int base_stride, u32* ticket, int which) {
   using Smem = SortSmem<V, THREADS, ITEMS>;
   static bool attr_set = false;
   if (!attr_set) {
@@ -586,7 +652,8 @@ int launch_pass(QxArena* ar, MergeBuffers<V>& mb, int cur, int64_t tiles_ub, con
   }
   k_onesweep<V, THREADS, ITEMS, EARLY><<<(unsigned)tiles_ub, THREADS, sizeof(Smem), ar->stream>>>(
       mb.keys[cur], mb.vals[cur], mb.keys[cur ^ 1], mb.vals[cur ^ 1], mb.seg[cur], mb.n_seg, tile_prefix,
-      digit_base, base_stride, ar->status, ticket, shift);
+      digit_base, base_stride, ar->status, ticket, which, sort_prefetch_distance(ar->sm_count),
+      getenv("QX_SORT_DEBUG") ? atoi(getenv("QX_SORT_DEBUG")) : 0);
   QX_CUDA(cudaGetLastError());
   return QX_OK;
 }
@@ -597,7 +664,7 @@ inline int sort_variant() {
   if (v < 0) {
     const char* e = getenv("QX_SORT_VARIANT");
     v = e ? atoi(e) : 0;
-    if (v < 0 || v > 5) v = 0;
+    if (v < 0 || v > 8) v = 0;
   }
   return v;
 }
@@ -610,6 +677,9 @@ inline int sort_tile_terms(int variant, size_t value_bytes) {
     case 3: return 256 * 16;
     case 4: return 512 * 8;
     case 5: return 256 * 12;
+    case 6: return 768 * 6;
+    case 7: return 1024 * 4;
+    case 8: return 512 * 6;
     default: return 384 * 12;
   }
 }
@@ -617,16 +687,19 @@ inline int sort_tile_terms(int variant, size_t value_bytes) {
 template <typename V>
 int dispatch_pass(int variant, QxArena* ar, MergeBuffers<V>& mb, int cur, int64_t tiles_ub,
                   const int64_t* tile_prefix, const u32* digit_base, int base_stride, u32* ticket,
-                  int shift) {
+                  int which) {
   if (sizeof(V) > 8)
-    return launch_pass<V, 256, 12, false>(ar, mb, cur, tiles_ub, tile_prefix, digit_base, base_stride, ticket, shift);
+    return launch_pass<V, 256, 12, false>(ar, mb, cur, tiles_ub, tile_prefix, digit_base, base_stride, ticket, which);
   switch (variant) {
-    case 1: return launch_pass<V, 384, 12, true>(ar, mb, cur, tiles_ub, tile_prefix, digit_base, base_stride, ticket, shift);
-    case 2: return launch_pass<V, 256, 12, false>(ar, mb, cur, tiles_ub, tile_prefix, digit_base, base_stride, ticket, shift);
-    case 3: return launch_pass<V, 256, 16, false>(ar, mb, cur, tiles_ub, tile_prefix, digit_base, base_stride, ticket, shift);
-    case 4: return launch_pass<V, 512, 8, false>(ar, mb, cur, tiles_ub, tile_prefix, digit_base, base_stride, ticket, shift);
-    case 5: return launch_pass<V, 256, 12, true>(ar, mb, cur, tiles_ub, tile_prefix, digit_base, base_stride, ticket, shift);
-    default: return launch_pass<V, 384, 12, false>(ar, mb, cur, tiles_ub, tile_prefix, digit_base, base_stride, ticket, shift);
+    case 1: return launch_pass<V, 384, 12, true>(ar, mb, cur, tiles_ub, tile_prefix, digit_base, base_stride, ticket, which);
+    case 2: return launch_pass<V, 256, 12, false>(ar, mb, cur, tiles_ub, tile_prefix, digit_base, base_stride, ticket, which);
+    case 3: return launch_pass<V, 256, 16, false>(ar, mb, cur, tiles_ub, tile_prefix, digit_base, base_stride, ticket, which);
+    case 4: return launch_pass<V, 512, 8, false>(ar, mb, cur, tiles_ub, tile_prefix, digit_base, base_stride, ticket, which);
+    case 5: return launch_pass<V, 256, 12, true>(ar, mb, cur, tiles_ub, tile_prefix, digit_base, base_stride, ticket, which);
+    case 6: return launch_pass<V, 768, 6, false>(ar, mb, cur, tiles_ub, tile_prefix, digit_base, base_stride, ticket, which);
+    case 7: return launch_pass<V, 1024, 4, false>(ar, mb, cur, tiles_ub, tile_prefix, digit_base, base_stride, ticket, which);
+    case 8: return launch_pass<V, 512, 6, false>(ar, mb, cur, tiles_ub, tile_prefix, digit_base, base_stride, ticket, which);
+    default: return launch_pass<V, 384, 12, false>(ar, mb, cur, tiles_ub, tile_prefix, digit_base, base_stride, ticket, which);
   }
 }
 
@@ -687,7 +760,7 @@ int merge_large(QxArena* ar, MergeBuffers<V>& mb, double eps, int cls_reduce, bo
     QX_CUDA(cudaMemsetAsync(ticket, 0, sizeof(u32), ar->stream));
     QxProfileScope prof(QX_K_SORT_PASS, ar->stream, 2.0 * (8.0 + sizeof(V)) * (double)mb.ub_total);
     QX_TRY(dispatch_pass<V>(variant, ar, mb, cur, tiles_ub, tile_prefix, hist + (size_t)p * QX_RADIX,
-                            passes * QX_RADIX, ticket, p * QX_RADIX_BITS));
+                            passes * QX_RADIX, ticket, p));
     cur ^= 1;
   }
   if (!do_reduce) {
