@@ -44,8 +44,8 @@ from paper_2505_03307_b200 import workloads  # noqa: E402
 
 DEFAULT_WORKLOAD = "c4_xyz_16_2"
 # generator subset used as the bounded CPU sample of each workload (None = whole circuit)
-CPU_SAMPLE = {"c4_xyz_16_2": list(range(4, 16)), "c4_xyz_18_2": list(range(7, 18)),
-              "c4_xyz_14_2": list(range(2, 14))}
+CPU_SAMPLE = {"c4_xyz_16_2": list(range(2, 16)), "c4_xyz_18_2": list(range(4, 18)),
+              "c4_xyz_14_2": list(range(0, 14))}
 
 
 def peaks():

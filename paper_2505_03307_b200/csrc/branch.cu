@@ -348,13 +348,16 @@ k_expand_emit(const u64* __restrict__ keys_in, const double* __restrict__ lam_in
     __syncthreads();
 
     // ---- 3. one raw term per thread per round, consecutive lanes = consecutive terms
+    const bool one_source = span == 1;                 // the common heavy case: hoist its digits
+    const K key0 = (K)keys_in[lo];
+    const LowGroup<K> g0 = low_group<K>(key0, sm.tb);
 #pragma unroll 2
     for (int k = 0; k < kEmitPer; ++k) {
       const u64 r = r0 + (u64)k * kThreads + threadIdx.x;
       if (r >= r1) break;
-      const int rel = span == 1 ? 0 : (int)last_le(sm.win, span, r);
-      const K key = (K)keys_in[lo + rel];
-      const LowGroup<K> g = low_group<K>(key, sm.tb);
+      const int rel = one_source ? 0 : (int)last_le(sm.win, span, r);
+      const K key = one_source ? key0 : (K)keys_in[lo + rel];
+      const LowGroup<K> g = one_source ? g0 : low_group<K>(key, sm.tb);
       K q = (K)(r - sm.win[rel]);
       u32 pick[3];
 #pragma unroll
