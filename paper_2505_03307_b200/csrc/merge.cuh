@@ -156,9 +156,7 @@ struct SortSmem {
   V vals[THREADS * ITEMS];
 };
 
-// THREADS x ITEMS terms per tile, warp-striped.  EARLY: issue the coefficient loads right
-// after ranking so their HBM latency hides behind the digit scan and the look-back instead
-// of being exposed before the shared-memory scatter (costs ITEMS * sizeof(V) / 4 registers).
+// THREADS x ITEMS terms per tile, warp-striped; LB = predecessors read per look-back round trip.
 // Lanes of the warp whose 8-bit digit equals mine.  Hand-scheduled: one R2P moves the digit's
 // bits into predicates, then per bit one VOTE and two logic ops (the compiler's version of the
 // same loop spends six instructions per bit; this kernel is issue-bound, profiles/r01b).
@@ -190,7 +188,7 @@ __device__ __forceinline__ u32 key_byte(u64 key, int which) {
   return __byte_perm(half, 0u, 0x4440u | (u32)(which & 3));
 }
 
-template <typename V, int THREADS, int ITEMS, bool EARLY>
+template <typename V, int THREADS, int ITEMS, int LB>
 __global__ void __launch_bounds__(THREADS, (THREADS <= 256 ? 3 : 2))
 k_onesweep(const u64* __restrict__ keys_in, const V* __restrict__ vals_in,
            u64* __restrict__ keys_out, V* __restrict__ vals_out,
@@ -312,7 +310,7 @@ k_onesweep(const u64* __restrict__ keys_in, const V* __restrict__ vals_in,
   if (tid < QX_RADIX) {
     u32 excl = 0;
     if (!solo) {
-      constexpr int W = 8;
+      constexpr int W = LB;
       const int64_t first_tile = tile_prefix[g];
       int64_t t = tile - 1;
       bool done = false;
@@ -354,13 +352,10 @@ k_onesweep(const u64* __restrict__ keys_in, const V* __restrict__ vals_in,
 // ---------------------------------------------------------------------------------
 // reduce-by-key + drop + compaction over the sorted segments
 // ---------------------------------------------------------------------------------
-constexpr int kRedThreads = QX_SCAN_THREADS;
-constexpr int kRedItems = QX_SCAN_ITEMS;
-constexpr int kRedTile = QX_SCAN_TILE;
-constexpr int kRedWarps = kRedThreads / 32;
-
-template <typename V>
+template <typename V, int kRedThreads, int kRedItems>
 struct ReduceSmem {
+  static constexpr int kRedTile = kRedThreads * kRedItems;
+  static constexpr int kRedWarps = kRedThreads / 32;
   u64 key[kRedTile + 2];       // [0] = key before the tile, [1..cnt] = tile
   V val[kRedTile];
   u32 opens[kRedTile / 32];    // bit j: tile slot j is the first term of a non-empty segment
@@ -375,14 +370,15 @@ struct ReduceSmem {
 // The tile (keys, coefficients, one halo key) is staged in shared memory with coalesced
 // streaming loads, so every term is read from HBM exactly once and no thread searches the
 // offset table; only runs that cross the tile end touch global memory again.
-template <typename V>
+template <typename V, int kRedThreads, int kRedItems>
 __global__ void __launch_bounds__(kRedThreads)
 k_reduce(const u64* __restrict__ keys_in, const V* __restrict__ vals_in,
          const int64_t* __restrict__ seg_in, int n_seg, u64* __restrict__ keys_out,
          V* __restrict__ vals_out, int64_t* __restrict__ seg_out, u64* status, u32* ticket,
-         double eps) {
+         double eps, int debug) {
+  constexpr int kRedTile = kRedThreads * kRedItems;
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  ReduceSmem<V>& sm = *reinterpret_cast<ReduceSmem<V>*>(smem_raw);
+  ReduceSmem<V, kRedThreads, kRedItems>& sm = *reinterpret_cast<ReduceSmem<V, kRedThreads, kRedItems>*>(smem_raw);
   if (threadIdx.x == 0) sm.tile = (int)atomicAdd(ticket, 1u);
   if (threadIdx.x < kRedTile / 32) sm.opens[threadIdx.x] = 0u;
   __syncthreads();
@@ -452,7 +448,7 @@ k_reduce(const u64* __restrict__ keys_in, const V* __restrict__ vals_in,
   u64 warp_excl = block_exclusive_sum<u64>(mine, sm.scan, tile_total);
   warp_excl = __shfl_sync(QX_FULL_MASK, warp_excl, 0);
   if (warp == 0) {
-    const u64 excl = lookback_exclusive(status, tile, tile_total);
+    const u64 excl = (debug & 2) ? (u64)tile * kRedTile : lookback_exclusive(status, tile, tile_total);
     if (lane == 0) sm.base = excl;
   }
   __syncthreads();
@@ -640,17 +636,17 @@ inline int sort_prefetch_distance(int sm_count) {
   return v >= 0 ? v : 2 * sm_count;     // ~ resident CTAs (two per SM)
 }
 
-template <typename V, int THREADS, int ITEMS, bool EARLY>
+template <typename V, int THREADS, int ITEMS, int LB>
 int launch_pass(QxArena* ar, MergeBuffers<V>& mb, int cur, int64_t tiles_ub, const int64_t* tile_prefix,
                 const u32* digit_base, int base_stride, u32* ticket, int which) {
   using Smem = SortSmem<V, THREADS, ITEMS>;
   static bool attr_set = false;
   if (!attr_set) {
-    QX_CUDA(cudaFuncSetAttribute(k_onesweep<V, THREADS, ITEMS, EARLY>,
+    QX_CUDA(cudaFuncSetAttribute(k_onesweep<V, THREADS, ITEMS, LB>,
                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(Smem)));
     attr_set = true;
   }
-  k_onesweep<V, THREADS, ITEMS, EARLY><<<(unsigned)tiles_ub, THREADS, sizeof(Smem), ar->stream>>>(
+  k_onesweep<V, THREADS, ITEMS, LB><<<(unsigned)tiles_ub, THREADS, sizeof(Smem), ar->stream>>>(
       mb.keys[cur], mb.vals[cur], mb.keys[cur ^ 1], mb.vals[cur ^ 1], mb.seg[cur], mb.n_seg, tile_prefix,
       digit_base, base_stride, ar->status, ticket, which, sort_prefetch_distance(ar->sm_count),
       getenv("QX_SORT_DEBUG") ? atoi(getenv("QX_SORT_DEBUG")) : 0);
@@ -676,10 +672,10 @@ inline int sort_tile_terms(int variant, size_t value_bytes) {
     case 2: return 256 * 12;
     case 3: return 256 * 16;
     case 4: return 512 * 8;
-    case 5: return 256 * 12;
+    case 5: return 384 * 12;
     case 6: return 768 * 6;
     case 7: return 1024 * 4;
-    case 8: return 512 * 6;
+    case 8: return 384 * 12;
     default: return 384 * 12;
   }
 }
@@ -689,17 +685,17 @@ int dispatch_pass(int variant, QxArena* ar, MergeBuffers<V>& mb, int cur, int64_
                   const int64_t* tile_prefix, const u32* digit_base, int base_stride, u32* ticket,
                   int which) {
   if (sizeof(V) > 8)
-    return launch_pass<V, 256, 12, false>(ar, mb, cur, tiles_ub, tile_prefix, digit_base, base_stride, ticket, which);
+    return launch_pass<V, 256, 12, 8>(ar, mb, cur, tiles_ub, tile_prefix, digit_base, base_stride, ticket, which);
   switch (variant) {
-    case 1: return launch_pass<V, 384, 12, true>(ar, mb, cur, tiles_ub, tile_prefix, digit_base, base_stride, ticket, which);
-    case 2: return launch_pass<V, 256, 12, false>(ar, mb, cur, tiles_ub, tile_prefix, digit_base, base_stride, ticket, which);
-    case 3: return launch_pass<V, 256, 16, false>(ar, mb, cur, tiles_ub, tile_prefix, digit_base, base_stride, ticket, which);
-    case 4: return launch_pass<V, 512, 8, false>(ar, mb, cur, tiles_ub, tile_prefix, digit_base, base_stride, ticket, which);
-    case 5: return launch_pass<V, 256, 12, true>(ar, mb, cur, tiles_ub, tile_prefix, digit_base, base_stride, ticket, which);
-    case 6: return launch_pass<V, 768, 6, false>(ar, mb, cur, tiles_ub, tile_prefix, digit_base, base_stride, ticket, which);
-    case 7: return launch_pass<V, 1024, 4, false>(ar, mb, cur, tiles_ub, tile_prefix, digit_base, base_stride, ticket, which);
-    case 8: return launch_pass<V, 512, 6, false>(ar, mb, cur, tiles_ub, tile_prefix, digit_base, base_stride, ticket, which);
-    default: return launch_pass<V, 384, 12, false>(ar, mb, cur, tiles_ub, tile_prefix, digit_base, base_stride, ticket, which);
+    case 1: return launch_pass<V, 384, 12, 16>(ar, mb, cur, tiles_ub, tile_prefix, digit_base, base_stride, ticket, which);
+    case 2: return launch_pass<V, 256, 12, 8>(ar, mb, cur, tiles_ub, tile_prefix, digit_base, base_stride, ticket, which);
+    case 3: return launch_pass<V, 256, 16, 8>(ar, mb, cur, tiles_ub, tile_prefix, digit_base, base_stride, ticket, which);
+    case 4: return launch_pass<V, 512, 8, 8>(ar, mb, cur, tiles_ub, tile_prefix, digit_base, base_stride, ticket, which);
+    case 5: return launch_pass<V, 384, 12, 32>(ar, mb, cur, tiles_ub, tile_prefix, digit_base, base_stride, ticket, which);
+    case 6: return launch_pass<V, 768, 6, 8>(ar, mb, cur, tiles_ub, tile_prefix, digit_base, base_stride, ticket, which);
+    case 7: return launch_pass<V, 1024, 4, 8>(ar, mb, cur, tiles_ub, tile_prefix, digit_base, base_stride, ticket, which);
+    case 8: return launch_pass<V, 384, 12, 4>(ar, mb, cur, tiles_ub, tile_prefix, digit_base, base_stride, ticket, which);
+    default: return launch_pass<V, 384, 12, 8>(ar, mb, cur, tiles_ub, tile_prefix, digit_base, base_stride, ticket, which);
   }
 }
 
@@ -715,7 +711,9 @@ int merge_large(QxArena* ar, MergeBuffers<V>& mb, double eps, int cls_reduce, bo
   const int variant = sort_variant();
   const int tile_terms = sort_tile_terms(variant, sizeof(V));
   const int64_t tiles_ub = (mb.ub_total + tile_terms - 1) / tile_terms + n_seg;
-  const int64_t red_tiles = std::max<int64_t>(1, (mb.ub_total + kRedTile - 1) / kRedTile);
+  static const int red_variant = getenv("QX_REDUCE_VARIANT") ? atoi(getenv("QX_REDUCE_VARIANT")) : 0;
+  const int red_tile = sizeof(V) > 8 ? 2048 : (red_variant == 1 ? 1024 : red_variant == 2 ? 2048 : red_variant == 3 ? 4096 : 2048);
+  const int64_t red_tiles = std::max<int64_t>(1, (mb.ub_total + red_tile - 1) / red_tile);
   // scratch layout: ticket | tile_prefix | hist | reduce look-back
   const int64_t off_prefix = 256;
   const int64_t off_hist = align_up(off_prefix + 8 * ((int64_t)n_seg + 1), 256);
@@ -731,13 +729,6 @@ int merge_large(QxArena* ar, MergeBuffers<V>& mb, double eps, int cls_reduce, bo
   u64* red_status = reinterpret_cast<u64*>(base + off_red);
   QX_CUDA(cudaMemsetAsync(base, 0, (size_t)total_bytes, ar->stream));
 
-  static bool attr_set[2] = {false, false};
-  const int which = sizeof(V) == 8 ? 0 : 1;
-  if (!attr_set[which]) {
-    QX_CUDA(cudaFuncSetAttribute(k_reduce<V>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)sizeof(ReduceSmem<V>)));
-    attr_set[which] = true;
-  }
   int cur = mb.cur;
   k_sort_plan<<<1, 32, 0, ar->stream>>>(mb.seg[cur], n_seg, tile_prefix, ticket, tile_terms);
   qx_count_launches(1);
@@ -770,9 +761,24 @@ int merge_large(QxArena* ar, MergeBuffers<V>& mb, double eps, int cls_reduce, bo
   QX_CUDA(cudaMemsetAsync(ticket, 0, sizeof(u32), ar->stream));
   {
     QxProfileScope prof(cls_reduce, ar->stream, (8.0 + sizeof(V)) * 2.0 * (double)mb.ub_total);
-    k_reduce<V><<<(unsigned)red_tiles, kRedThreads, sizeof(ReduceSmem<V>), ar->stream>>>(
-        mb.keys[cur], mb.vals[cur], mb.seg[cur], n_seg, mb.keys[cur ^ 1], mb.vals[cur ^ 1],
-        mb.seg[cur ^ 1], red_status, ticket, eps);
+#define QX_LAUNCH_REDUCE(T, I)                                                                        \
+  do {                                                                                                \
+    static bool attr = false;                                                                         \
+    if (!attr) {                                                                                      \
+      QX_CUDA(cudaFuncSetAttribute(k_reduce<V, T, I>, cudaFuncAttributeMaxDynamicSharedMemorySize,    \
+                                   (int)sizeof(ReduceSmem<V, T, I>)));                                \
+      attr = true;                                                                                    \
+    }                                                                                                 \
+    k_reduce<V, T, I><<<(unsigned)red_tiles, T, sizeof(ReduceSmem<V, T, I>), ar->stream>>>(           \
+        mb.keys[cur], mb.vals[cur], mb.seg[cur], n_seg, mb.keys[cur ^ 1], mb.vals[cur ^ 1],           \
+        mb.seg[cur ^ 1], red_status, ticket, eps,                                                     \
+        getenv("QX_SORT_DEBUG") ? atoi(getenv("QX_SORT_DEBUG")) : 0);                                 \
+  } while (0)
+    if (sizeof(V) > 8 || red_variant == 0) QX_LAUNCH_REDUCE(256, 8);
+    else if (red_variant == 1) QX_LAUNCH_REDUCE(128, 8);
+    else if (red_variant == 2) QX_LAUNCH_REDUCE(128, 16);
+    else QX_LAUNCH_REDUCE(512, 8);
+#undef QX_LAUNCH_REDUCE
     QX_CUDA(cudaGetLastError());
   }
   mb.cur = cur ^ 1;

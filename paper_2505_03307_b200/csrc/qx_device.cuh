@@ -86,6 +86,10 @@ constexpr u64 QX_LB_INC = 2ull << 62;
 constexpr u64 QX_LB_VAL = (1ull << 62) - 1;
 
 // Called by all 32 lanes of ONE warp; returns the exclusive prefix of `aggregate`.
+// R status words per lane per round trip (32 * R predecessors): with hundreds of tiles in
+// flight a new tile starts every ~10-25 ns, so a walker that consumes only 32 predecessors
+// per L2 round trip (~0.4 us) cannot catch up with the frontier of resolved tiles.
+template <int R = 1>
 __device__ __forceinline__ u64 lookback_exclusive(u64* status, int tile, u64 aggregate) {
   if (tile == 0) {
     if (lane_id() == 0) st_volatile_u64(status, QX_LB_INC | aggregate);
@@ -94,22 +98,30 @@ __device__ __forceinline__ u64 lookback_exclusive(u64* status, int tile, u64 agg
   if (lane_id() == 0) st_volatile_u64(status + tile, QX_LB_AGG | aggregate);
   u64 excl = 0;
   int base = tile - 1;
-  while (true) {
-    const int t = base - (int)lane_id();
-    u64 w = QX_LB_INC;                      // virtual tiles before tile 0: inclusive 0
-    if (t >= 0) {
-      do { w = ld_volatile_u64(status + t); } while ((w >> 62) == 0);
+  bool done = false;
+  while (!done) {
+    u64 w[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      const int t = base - r * 32 - (int)lane_id();
+      w[r] = t >= 0 ? ld_volatile_u64(status + t) : QX_LB_INC;   // before tile 0: inclusive 0
     }
-    const u32 inc = __ballot_sync(QX_FULL_MASK, (w >> 62) == 2);
-    u64 v = w & QX_LB_VAL;
-    if (inc) {
-      const int first = __ffs(inc) - 1;     // nearest tile holding an inclusive prefix
-      if ((int)lane_id() > first) v = 0;
-      excl += warp_sum(v);
-      break;
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      if (!done) {
+        const int t = base - r * 32 - (int)lane_id();
+        while ((w[r] >> 62) == 0) w[r] = ld_volatile_u64(status + t);
+        const u32 inc = __ballot_sync(QX_FULL_MASK, (w[r] >> 62) == 2);
+        u64 v = w[r] & QX_LB_VAL;
+        if (inc) {
+          const int first = __ffs(inc) - 1;     // nearest tile holding an inclusive prefix
+          if ((int)lane_id() > first) v = 0;
+          done = true;
+        }
+        excl += warp_sum(v);
+      }
     }
-    excl += warp_sum(v);
-    base -= 32;
+    base -= 32 * R;
   }
   if (lane_id() == 0) st_volatile_u64(status + tile, QX_LB_INC | (excl + aggregate));
   return excl;
