@@ -115,6 +115,18 @@ int qx_apply_split(qx_store* s, int32_t qubit, const int32_t a1[4], const double
  * (QX_ERR_RESOURCE) a raw count above it before anything is written. */
 int qx_apply_operator(qx_store* s, const int32_t* counts, const int32_t* axes,
                       const double* weights, int64_t term_limit, int64_t* raw_total);
+/* ---- a4 + a5 + a2 + a6 in one call: U_k, the run of sign-permutation ops that follows it
+ * (the CX group V_k and any Clifford blocks up to the next branching operator), then the merge
+ * (engine.py:110-132: sub, flatten, apply_cx..., canonicalize).  Same result as
+ * qx_apply_operator + qx_apply_clifford + qx_merge, but conjugation by the run is folded into the
+ * expansion kernel (a Clifford run is a homomorphism: the image of a raw term is the product of
+ * the images of its single-digit factors), so raw terms are written once, already conjugated,
+ * and for 2n <= 32 as 32-bit keys that only the sort passes see.  program/n_ops/cx_*: as in
+ * qx_apply_clifford (n_ops may be 0).  ranks (may be NULL): per-segment counts after the merge. */
+int qx_apply_operator_run(qx_store* s, const int32_t* counts, const int32_t* axes,
+                          const double* weights, const uint32_t* program, int32_t n_ops,
+                          uint32_t cx_c, uint32_t cx_t, uint32_t cx_s, double eps,
+                          int64_t term_limit, int64_t* raw_total, int64_t* ranks);
 /* Number of raw branches the same call would produce per segment, nothing written
  * (branch_counts, stabilizer.py:232-237). */
 int qx_count_operator(qx_store* s, const int32_t* counts, int64_t* raw_per_segment);

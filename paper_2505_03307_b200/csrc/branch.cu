@@ -18,6 +18,9 @@
 // segment is "term-major, branches ascending", which keeps duplicates of one key in
 // the same relative order as the reference's raw lists, so the merge sums them in
 // the same order.
+#include <stdlib.h>
+#include <string.h>
+
 #include <algorithm>
 
 #include "qx_device.cuh"
@@ -198,6 +201,47 @@ template <> struct KeyOps<u64> {
   static __device__ __forceinline__ u64 support(u64 k) { return support_mask(k); }
 };
 
+// ---- Clifford run folded into the expansion ---------------------------------------------------
+// In v2/v3 every U_k is followed by a run of sign-permutation ops (the CX group V_k, Clifford
+// blocks of later U's).  Conjugation by the run is a group homomorphism on Pauli operators, so the
+// image of a raw term is the ordered product of the images of its single-digit factors: the host
+// pushes the 3n single-digit words through the run once (ImageTable) and the expansion kernel
+// composes images instead of OR-ing digits -- the raw terms leave the kernel already conjugated
+// and the separate read+write pass of the Clifford kernel disappears.
+// Bookkeeping in "XZ form": a Hermitian word with sign s is i^e X^x Z^z with e = #Y + 2s, and
+//   (i^ea X^xa Z^za)(i^eb X^xb Z^zb) = i^(ea + eb + 2|za & xb|) X^(xa^xb) Z^(za^zb);
+// on the packed base-4 code (hi = z, lo = x ^ z) the word part is one XOR, the exponent one
+// popcount.  Factors of one term act on different qubits, so they commute and the final
+// exponent minus #Y of the final word is 0 or 2: the sign, applied to lambda exactly.
+template <typename K>
+struct ImageTable {
+  K img[QX_MAX_QUBITS][3];             // image word of axis a+1 at digit position p
+  K imx[QX_MAX_QUBITS][3];             // its x plane ((w ^ w >> 1) & 0x55..), precomputed
+  unsigned char e[QX_MAX_QUBITS][3];   // (#Y of the image + 2 * sign) mod 4
+};
+
+template <typename K> struct Plane;
+template <> struct Plane<u32> {
+  static constexpr u32 lo = 0x55555555u;
+  static __device__ __forceinline__ u32 popc(u32 v) { return (u32)__popc(v); }
+};
+template <> struct Plane<u64> {
+  static constexpr u64 lo = 0x5555555555555555ull;
+  static __device__ __forceinline__ u32 popc(u64 v) { return (u32)__popcll(v); }
+};
+
+template <typename K>
+__device__ __forceinline__ void compose(K& word, u32& e, K img, K imx, u32 ie) {
+  e += ie + 2u * Plane<K>::popc((word >> 1) & imx);
+  word ^= img;
+}
+// 1 iff the composed operator is MINUS the Hermitian word
+template <typename K>
+__device__ __forceinline__ u32 composed_sign(K word, u32 e) {
+  const u32 ny = Plane<K>::popc((word >> 1) & ~word & Plane<K>::lo);
+  return ((e - ny) >> 1) & 1u;
+}
+
 // ---- two-level branch decode --------------------------------------------------------------
 // A source term with non-identity digits d_0 < d_1 < ... (least significant first) and radices
 // c_i expands into prod c_i raw terms, branch id b = mixed-radix number with d_0 fastest.
@@ -256,6 +300,8 @@ constexpr int kEmitTile = kThreads * kEmitPer;       // 2048 raw terms per tile
 template <typename K>
 struct EmitSmem {
   OperatorTable tb;
+  ImageTable<K> im;
+  unsigned char e_hi[kEmitTile + 1];
   u64 win[kEmitTile + 2];      // raw offsets of the sources feeding the tile (+ end sentinel)
   u32 blk[kEmitTile + 2];      // exclusive prefix of blocks per source
   double p_hi[kEmitTile + 1];
@@ -265,17 +311,25 @@ struct EmitSmem {
   u64 hfirst0;                 // first block id of the first source (it may start mid-way)
 };
 
-template <typename K>
+// K = working key type, KO = type of the keys written (u32 = narrow raw terms for the sort),
+// FUSED = compose Clifford images (im) instead of placing digits.
+template <typename K, typename KO, bool FUSED>
 __global__ void __launch_bounds__(kThreads)
 k_expand_emit(const u64* __restrict__ keys_in, const double* __restrict__ lam_in,
-              const u64* __restrict__ roff, int64_t total_in, u64* __restrict__ keys_out,
-              double* __restrict__ lam_out, const __grid_constant__ OperatorTable tb) {
+              const u64* __restrict__ roff, int64_t total_in, KO* __restrict__ keys_out,
+              double* __restrict__ lam_out, const __grid_constant__ OperatorTable tb,
+              const __grid_constant__ ImageTable<K> im) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   EmitSmem<K>& sm = *reinterpret_cast<EmitSmem<K>*>(smem_raw);
   {
     const u32* src = reinterpret_cast<const u32*>(&tb);
     u32* dst = reinterpret_cast<u32*>(&sm.tb);
     for (int i = threadIdx.x; i < (int)(sizeof(OperatorTable) / 4); i += kThreads) dst[i] = src[i];
+    if (FUSED) {
+      const u32* isrc = reinterpret_cast<const u32*>(&im);
+      u32* idst = reinterpret_cast<u32*>(&sm.im);
+      for (int i = threadIdx.x; i < (int)(sizeof(ImageTable<K>) / 4); i += kThreads) idst[i] = isrc[i];
+    }
   }
   const u64 raw_total = roff[total_in];
   const int64_t ntiles = (int64_t)((raw_total + kEmitTile - 1) / kEmitTile);
@@ -335,15 +389,19 @@ k_expand_emit(const u64* __restrict__ keys_in, const double* __restrict__ lam_in
       // fold: qubit 0 (most significant digit) first, like stabilizer.py:311-319
       double v = lam_in[lo + a];
       K out = 0;
+      u32 ex = 0;
       for (K m = g.hi_mask; m;) {
         const int bit = KeyOps<K>::highest(m);
         m ^= (K)1 << bit;
         const u32 d = (u32)((key >> bit) & 3u) - 1u, pick = (u32)(choice >> bit) & 3u;
         v *= sm.tb.w[bit >> 1][d][pick];
-        out |= (K)sm.tb.axis[bit >> 1][d][pick] << bit;
+        const u32 ax = sm.tb.axis[bit >> 1][d][pick];
+        if (FUSED) compose<K>(out, ex, sm.im.img[bit >> 1][ax - 1], sm.im.imx[bit >> 1][ax - 1], sm.im.e[bit >> 1][ax - 1]);
+        else out |= (K)ax << bit;
       }
       sm.p_hi[e] = v;
       sm.k_hi[e] = out;
+      if (FUSED) sm.e_hi[e] = (unsigned char)(ex & 3u);
     }
     __syncthreads();
 
@@ -365,14 +423,19 @@ k_expand_emit(const u64* __restrict__ keys_in, const double* __restrict__ lam_in
       const u32 e = sm.blk[rel] + (u32)(q - (K)(rel == 0 ? sm.hfirst0 : 0ull));
       double v = sm.p_hi[e];
       K out = sm.k_hi[e];
+      u32 ex = FUSED ? (u32)sm.e_hi[e] : 0u;
 #pragma unroll
       for (int j = 2; j >= 0; --j) {
         if (g.bit[j] >= 0) {
-          v *= sm.tb.w[g.bit[j] >> 1][g.dig[j]][pick[j]];
-          out |= (K)sm.tb.axis[g.bit[j] >> 1][g.dig[j]][pick[j]] << g.bit[j];
+          const int p = g.bit[j] >> 1;
+          v *= sm.tb.w[p][g.dig[j]][pick[j]];
+          const u32 ax = sm.tb.axis[p][g.dig[j]][pick[j]];
+          if (FUSED) compose<K>(out, ex, sm.im.img[p][ax - 1], sm.im.imx[p][ax - 1], sm.im.e[p][ax - 1]);
+          else out |= (K)ax << g.bit[j];
         }
       }
-      st_stream(keys_out + r, (u64)out);
+      if (FUSED && composed_sign<K>(out, ex)) v = -v;     // sign flips are exact
+      st_stream(keys_out + r, (KO)out);
       st_stream(lam_out + r, v);
     }
   }
@@ -496,20 +559,75 @@ extern "C" int qx_count_operator(qx_store* s, const int32_t* counts, int64_t* ra
   return QX_OK;
 }
 
-extern "C" int qx_apply_operator(qx_store* s, const int32_t* counts, const int32_t* axes,
-                                 const double* weights, int64_t term_limit, int64_t* raw_total) {
-  QX_REQUIRE(s && counts && axes && weights, "NULL argument");
-  OperatorTable tb;
-  QX_TRY(fill_table(s, counts, axes, weights, &tb));
+// ---- host side of the fused path -----------------------------------------------------------
+namespace {
+
+// one op of a sign-permutation program on one word (same encoding as clifford.cu apply_op)
+void host_apply_op(u32 op, u64& key, u32& neg, u32 cx_c, u32 cx_t, u32 cx_s) {
+  const u32 s0 = (op >> 2) & 63u;
+  const u32 d0 = (u32)(key >> s0) & 3u;
+  if ((op & 3u) == 0u) {
+    const u32 nd = (op >> (16u + 2u * d0)) & 3u;
+    neg ^= (op >> (24u + d0)) & 1u;
+    key ^= (u64)(d0 ^ nd) << s0;
+  } else {
+    const u32 s1 = (op >> 8) & 63u;
+    const u32 d1 = (u32)(key >> s1) & 3u;
+    const u32 e = d0 * 4u + d1;
+    const u32 n0 = (cx_c >> (2u * e)) & 3u, n1 = (cx_t >> (2u * e)) & 3u;
+    neg ^= (cx_s >> e) & 1u;
+    key ^= ((u64)(d0 ^ n0) << s0) | ((u64)(d1 ^ n1) << s1);
+  }
+}
+
+template <typename K>
+void fill_images(int n_qubits, const uint32_t* program, int n_ops, u32 cx_c, u32 cx_t, u32 cx_s,
+                 ImageTable<K>* im) {
+  memset(im, 0, sizeof(*im));
+  const u64 lo = 0x5555555555555555ull;
+  for (int p = 0; p < n_qubits; ++p)
+    for (u32 a = 1; a <= 3; ++a) {
+      u64 w = (u64)a << (2 * p);
+      u32 neg = 0;
+      for (int i = 0; i < n_ops; ++i) host_apply_op(program[i], w, neg, cx_c, cx_t, cx_s);
+      const u32 ny = (u32)__builtin_popcountll((w >> 1) & ~w & lo);
+      im->img[p][a - 1] = (K)w;
+      im->imx[p][a - 1] = (K)((w ^ (w >> 1)) & lo);
+      im->e[p][a - 1] = (unsigned char)((ny + 2u * neg) & 3u);
+    }
+}
+
+template <typename K, typename KO, bool FUSED>
+int launch_emit(qx_store* s, const OperatorTable& tb, const ImageTable<K>& im, const u64* roff,
+                int64_t total_in, int64_t raw, int in, int out) {
+  const int64_t tiles = (raw + kEmitTile - 1) / kEmitTile;
+  const int grid = (int)std::min<int64_t>(tiles, (int64_t)s->sm_count * 8);
+  static bool attr_set = false;
+  if (!attr_set) {
+    QX_CUDA(cudaFuncSetAttribute(k_expand_emit<K, KO, FUSED>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)sizeof(EmitSmem<K>)));
+    attr_set = true;
+  }
+  k_expand_emit<K, KO, FUSED><<<grid, kThreads, sizeof(EmitSmem<K>), s->stream>>>(
+      s->keys[in], s->lam[in], roff, total_in, reinterpret_cast<KO*>(s->keys[out]), s->lam[out], tb, im);
+  QX_CUDA(cudaGetLastError());
+  return QX_OK;
+}
+
+// U_k (+ an optional Clifford run folded in).  narrow_ok: the caller merges right away with the
+// large path, so for 2n <= 32 the raw keys may be written as 32-bit words; *narrow says whether
+// they were.
+int expand(qx_store* s, const OperatorTable& tb, const uint32_t* program, int n_ops, u32 cx_c,
+           u32 cx_t, u32 cx_s, bool narrow_ok, int64_t term_limit, int64_t* raw_total, bool* narrow) {
   QX_CUDA(cudaSetDevice(s->device));
   u64* roff;
   QX_TRY(count_pass(s, tb, &roff));
   const int64_t total_in = s->h_seg[s->n_seg];
-  const int in = s->cur, out = s->cur ^ 1;
-  k_gather_offsets<<<(s->n_seg + 256) / 256, 256, 0, s->stream>>>(s->seg[in], s->n_seg, roff, s->seg[out]);
+  k_gather_offsets<<<(s->n_seg + 256) / 256, 256, 0, s->stream>>>(s->seg[s->cur], s->n_seg, roff,
+                                                                  s->seg[s->cur ^ 1]);
   qx_count_launches(1);
   QX_CUDA(cudaGetLastError());
-  QX_CUDA(cudaMemcpyAsync(s->h_pinned, s->seg[out], sizeof(int64_t) * (size_t)(s->n_seg + 1),
+  QX_CUDA(cudaMemcpyAsync(s->h_pinned, s->seg[s->cur ^ 1], sizeof(int64_t) * (size_t)(s->n_seg + 1),
                           cudaMemcpyDeviceToHost, s->stream));
   QX_CUDA(cudaStreamSynchronize(s->stream));
   const int64_t raw = s->h_pinned[s->n_seg];
@@ -525,33 +643,75 @@ extern "C" int qx_apply_operator(qx_store* s, const int32_t* counts, const int32
                             cudaMemcpyHostToDevice, s->stream));
     QX_CUDA(cudaStreamSynchronize(s->stream));
   }
-  const int in2 = s->cur, out2 = s->cur ^ 1;
+  int64_t ub_seg = 0;
+  for (int g = 0; g < s->n_seg; ++g) ub_seg = std::max(ub_seg, s->h_pinned[g + 1] - s->h_pinned[g]);
+  const bool small_keys = s->n_qubits <= 16;
+  const bool go_narrow = narrow_ok && small_keys && ub_seg > QX_SMALL_MAX;
+  if (narrow) *narrow = go_narrow;
+  const int in = s->cur, out = s->cur ^ 1;
   if (raw > 0) {
-    const int64_t tiles = (raw + kEmitTile - 1) / kEmitTile;
-    const int grid = (int)std::min<int64_t>(tiles, (int64_t)s->sm_count * 8);
-    QxProfileScope prof(QX_K_EXPAND_EMIT, s->stream, 16.0 * ((double)total_in + (double)raw));
-    static bool attr_set = false;
-    if (!attr_set) {
-      QX_CUDA(cudaFuncSetAttribute(k_expand_emit<u32>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   (int)sizeof(EmitSmem<u32>)));
-      QX_CUDA(cudaFuncSetAttribute(k_expand_emit<u64>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   (int)sizeof(EmitSmem<u64>)));
-      attr_set = true;
+    const double key_bytes = go_narrow ? 4.0 : 8.0;
+    QxProfileScope prof(QX_K_EXPAND_EMIT, s->stream, 16.0 * (double)total_in + (8.0 + key_bytes) * (double)raw);
+    if (small_keys) {
+      ImageTable<u32> im;
+      if (n_ops > 0) fill_images<u32>(s->n_qubits, program, n_ops, cx_c, cx_t, cx_s, &im);
+      if (n_ops > 0 && go_narrow) QX_TRY((launch_emit<u32, u32, true>(s, tb, im, roff, total_in, raw, in, out)));
+      else if (n_ops > 0) QX_TRY((launch_emit<u32, u64, true>(s, tb, im, roff, total_in, raw, in, out)));
+      else if (go_narrow) QX_TRY((launch_emit<u32, u32, false>(s, tb, im, roff, total_in, raw, in, out)));
+      else QX_TRY((launch_emit<u32, u64, false>(s, tb, im, roff, total_in, raw, in, out)));
+    } else {
+      ImageTable<u64> im;
+      if (n_ops > 0) {
+        fill_images<u64>(s->n_qubits, program, n_ops, cx_c, cx_t, cx_s, &im);
+        QX_TRY((launch_emit<u64, u64, true>(s, tb, im, roff, total_in, raw, in, out)));
+      } else {
+        QX_TRY((launch_emit<u64, u64, false>(s, tb, im, roff, total_in, raw, in, out)));
+      }
     }
-    if (s->n_qubits <= 16)
-      k_expand_emit<u32><<<grid, kThreads, sizeof(EmitSmem<u32>), s->stream>>>(
-          s->keys[in2], s->lam[in2], roff, total_in, s->keys[out2], s->lam[out2], tb);
-    else
-      k_expand_emit<u64><<<grid, kThreads, sizeof(EmitSmem<u64>), s->stream>>>(
-          s->keys[in2], s->lam[in2], roff, total_in, s->keys[out2], s->lam[out2], tb);
-    QX_CUDA(cudaGetLastError());
   }
-  (void)in; (void)out;
   qx_store_flip(s);
   for (int g = 0; g <= s->n_seg; ++g) s->h_seg[g] = s->h_pinned[g];
   s->exact = true;
   s->ub_total = raw;
-  s->ub_seg = 0;
-  for (int g = 0; g < s->n_seg; ++g) s->ub_seg = std::max(s->ub_seg, s->h_seg[g + 1] - s->h_seg[g]);
+  s->ub_seg = ub_seg;
+  return QX_OK;
+}
+
+}  // namespace
+
+extern "C" int qx_apply_operator(qx_store* s, const int32_t* counts, const int32_t* axes,
+                                 const double* weights, int64_t term_limit, int64_t* raw_total) {
+  QX_REQUIRE(s && counts && axes && weights, "NULL argument");
+  OperatorTable tb;
+  QX_TRY(fill_table(s, counts, axes, weights, &tb));
+  return expand(s, tb, nullptr, 0, 0, 0, 0, false, term_limit, raw_total, nullptr);
+}
+
+extern "C" int qx_apply_operator_run(qx_store* s, const int32_t* counts, const int32_t* axes,
+                                     const double* weights, const uint32_t* program, int32_t n_ops,
+                                     uint32_t cx_c, uint32_t cx_t, uint32_t cx_s, double eps,
+                                     int64_t term_limit, int64_t* raw_total, int64_t* ranks) {
+  QX_REQUIRE(s && counts && axes && weights, "NULL argument");
+  QX_REQUIRE(n_ops >= 0 && (n_ops == 0 || program), "bad program");
+  QX_REQUIRE(eps >= 0.0, "eps must be non-negative");
+  OperatorTable tb;
+  QX_TRY(fill_table(s, counts, axes, weights, &tb));
+  QX_TRY(qx_check_program(s, program, n_ops));
+  u32 std_c, std_t, std_s;
+  qx_standard_cx(&std_c, &std_t, &std_s);
+  static const bool no_fuse = getenv("QX_NO_FUSE") != nullptr;
+  if (no_fuse || cx_c != std_c || cx_t != std_t || cx_s != std_s) {
+    // tables that are not the CX conjugation (mutation tests) are not a homomorphism: run the
+    // three steps one after the other, table-driven
+    QX_TRY(expand(s, tb, nullptr, 0, 0, 0, 0, false, term_limit, raw_total, nullptr));
+    QX_TRY(qx_apply_clifford(s, program, n_ops, cx_c, cx_t, cx_s));
+    return qx_merge(s, eps, ranks);
+  }
+  static const bool no_narrow = getenv("QX_NO_NARROW") != nullptr;
+  bool narrow = false;
+  QX_TRY(expand(s, tb, program, n_ops, cx_c, cx_t, cx_s, !no_narrow, term_limit, raw_total, &narrow));
+  QX_TRY(qx_run_merge(s, eps, false, narrow));
+  if (ranks)
+    for (int g = 0; g < s->n_seg; ++g) ranks[g] = s->h_seg[g + 1] - s->h_seg[g];
   return QX_OK;
 }

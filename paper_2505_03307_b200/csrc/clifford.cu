@@ -199,8 +199,21 @@ k_clifford_sliced(u64* __restrict__ keys, double* __restrict__ lam,
 
 }  // namespace
 
-extern "C" int qx_apply_clifford(qx_store* s, const uint32_t* program, int32_t n_ops, uint32_t cx_c,
-                                 uint32_t cx_t, uint32_t cx_s) {
+void qx_standard_cx(u32* cx_c, u32* cx_t, u32* cx_s) {
+  u32 std_c = 0, std_t = 0, std_s = 0;
+  for (u32 dc = 0; dc < 4; ++dc)
+    for (u32 dt = 0; dt < 4; ++dt) {
+      const u32 hc = dc >> 1, lc = dc & 1, ht = dt >> 1, lt = dt & 1, e = dc * 4 + dt;
+      std_c |= ((((hc ^ ht) << 1) | (lc ^ ht)) << (2 * e));
+      std_t |= (((ht << 1) | (lt ^ hc ^ lc)) << (2 * e));
+      std_s |= (((hc ^ lc) & ht & (1u ^ ht ^ lt ^ hc)) << e);
+    }
+  *cx_c = std_c;
+  *cx_t = std_t;
+  *cx_s = std_s;
+}
+
+int qx_check_program(const qx_store* s, const uint32_t* program, int32_t n_ops) {
   QX_REQUIRE(s != nullptr, "store is NULL");
   QX_REQUIRE(n_ops >= 0, "negative op count");
   if (n_ops == 0) return QX_OK;
@@ -215,6 +228,13 @@ extern "C" int qx_apply_clifford(qx_store* s, const uint32_t* program, int32_t n
       QX_REQUIRE(s0 != s1, "op %d: control and target must differ", i);
     }
   }
+  return QX_OK;
+}
+
+extern "C" int qx_apply_clifford(qx_store* s, const uint32_t* program, int32_t n_ops, uint32_t cx_c,
+                                 uint32_t cx_t, uint32_t cx_s) {
+  QX_TRY(qx_check_program(s, program, n_ops));
+  if (n_ops == 0) return QX_OK;
   QX_CUDA(cudaSetDevice(s->device));
   const int64_t ub = std::max<int64_t>(s->ub_total, 1);
   const int64_t want = (ub / 2 + kThreads - 1) / kThreads;
@@ -223,14 +243,8 @@ extern "C" int qx_apply_clifford(qx_store* s, const uint32_t* program, int32_t n
   static Program pg;       // host staging; the launch copies it into the parameter buffer
   // the sliced kernel evaluates CX from the x/z rule, which equals the reference's tables
   // (lut.py:108-134); a caller passing other tables (mutation tests) gets the table-driven kernel
-  u32 std_c = 0, std_t = 0, std_s = 0;
-  for (u32 dc = 0; dc < 4; ++dc)
-    for (u32 dt = 0; dt < 4; ++dt) {
-      const u32 hc = dc >> 1, lc = dc & 1, ht = dt >> 1, lt = dt & 1, e = dc * 4 + dt;
-      std_c |= ((((hc ^ ht) << 1) | (lc ^ ht)) << (2 * e));
-      std_t |= (((ht << 1) | (lt ^ hc ^ lc)) << (2 * e));
-      std_s |= (((hc ^ lc) & ht & (1u ^ ht ^ lt ^ hc)) << e);
-    }
+  u32 std_c, std_t, std_s;
+  qx_standard_cx(&std_c, &std_t, &std_s);
   static const bool per_term_only = getenv("QX_CLIFFORD_PER_TERM") != nullptr;
   const bool no_slice = per_term_only || cx_c != std_c || cx_t != std_t || cx_s != std_s;
   for (int done = 0; done < n_ops; done += kProgChunk) {

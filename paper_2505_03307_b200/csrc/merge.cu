@@ -3,9 +3,7 @@
 // kernel 4) and sum of squares (the P^2 = I self-check).
 #include "merge.cuh"
 
-namespace {
-
-int run_merge(qx_store* s, double eps, bool sort_only) {
+int qx_run_merge(qx_store* s, double eps, bool sort_only, bool narrow) {
   if (s->ub_seg > QX_SMALL_MAX && !s->exact) QX_TRY(qx_store_refresh(s));
   // both paths write into the other buffer; make sure it can hold the raw terms
   qxm::MergeBuffers<double> mb;
@@ -19,7 +17,10 @@ int run_merge(qx_store* s, double eps, bool sort_only) {
   mb.ub_total = s->ub_total;
   mb.ub_seg = s->ub_seg;
   bool small = s->ub_seg <= QX_SMALL_MAX;
-  if (small) {
+  if (narrow) {
+    if (small || sort_only) return qx_fail(QX_ERR_CONSISTENCY, "narrow keys outside the large merge (internal error)");
+    QX_TRY((qxm::merge_large<double, u32>(s, mb, eps, QX_K_REDUCE, true)));
+  } else if (small) {
     QX_TRY(qxm::merge_small<double>(s, mb, eps, QX_K_SMALL_MERGE));
   } else {
     QX_TRY(qxm::merge_large<double>(s, mb, eps, QX_K_REDUCE, !sort_only));
@@ -35,6 +36,8 @@ int run_merge(qx_store* s, double eps, bool sort_only) {
     return qx_fail(QX_ERR_CONSISTENCY, "small-merge segment bound violated (internal error)");
   return QX_OK;
 }
+
+namespace {
 
 // ---- per-segment deterministic reductions -------------------------------------------
 constexpr int kRedThreads = 256;
@@ -106,7 +109,7 @@ extern "C" int qx_merge(qx_store* s, double eps, int64_t* ranks) {
   QX_REQUIRE(s != nullptr, "store is NULL");
   QX_REQUIRE(eps >= 0.0, "eps must be non-negative");
   QX_CUDA(cudaSetDevice(s->device));
-  QX_TRY(run_merge(s, eps, false));
+  QX_TRY(qx_run_merge(s, eps, false, false));
   if (ranks)
     for (int g = 0; g < s->n_seg; ++g) ranks[g] = s->h_seg[g + 1] - s->h_seg[g];
   return QX_OK;
@@ -115,7 +118,7 @@ extern "C" int qx_merge(qx_store* s, double eps, int64_t* ranks) {
 extern "C" int qx_sort(qx_store* s) {
   QX_REQUIRE(s != nullptr, "store is NULL");
   QX_CUDA(cudaSetDevice(s->device));
-  return run_merge(s, 0.0, true);
+  return qx_run_merge(s, 0.0, true, false);
 }
 
 extern "C" int qx_store_zi_sums(qx_store* s, double* sums) { return segment_reduce<0>(s, sums); }

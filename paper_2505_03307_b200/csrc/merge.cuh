@@ -78,8 +78,9 @@ __device__ __forceinline__ int tile_segment(const int64_t* tile_prefix, int n_se
 // ---------------------------------------------------------------------------------
 constexpr int kMaxPasses = 8;
 
+template <typename K>
 static __global__ void __launch_bounds__(kSortThreads)
-k_sort_hist(const u64* __restrict__ keys, const int64_t* __restrict__ seg, int n_seg,
+k_sort_hist(const K* __restrict__ keys, const int64_t* __restrict__ seg, int n_seg,
             const int64_t* __restrict__ tile_prefix, u32* __restrict__ hist, int passes,
             int tile_terms) {
   __shared__ u32 sh[kMaxPasses][QX_RADIX];
@@ -108,7 +109,7 @@ k_sort_hist(const u64* __restrict__ keys, const int64_t* __restrict__ seg, int n
     for (int k = 0; k < rounds; ++k) {
       const int idx = k * kSortThreads + threadIdx.x;
       const bool live = idx < count;
-      const u64 key = live ? ld_stream(keys + start + idx) : 0ull;
+      const K key = live ? ld_stream(keys + start + idx) : (K)0;
       const u32 alive = __ballot_sync(QX_FULL_MASK, live);
       for (int p = 0; p < passes; ++p) {
         const u32 d = (u32)(key >> (QX_RADIX_BITS * p)) & (QX_RADIX - 1);
@@ -145,15 +146,15 @@ static __global__ void __launch_bounds__(QX_RADIX) k_sort_scan_hist(u32* __restr
 // ---------------------------------------------------------------------------------
 // one onesweep pass
 // ---------------------------------------------------------------------------------
-template <typename V, int THREADS, int ITEMS>
+template <typename K, typename V, int THREADS, int ITEMS>
 struct SortSmem {
   u32 whist[THREADS / 32][QX_RADIX];  // per-warp digit counters -> exclusive warp offsets
   u32 tile_start[QX_RADIX];           // first slot of each digit in the tile-sorted order
   int64_t gbase[QX_RADIX];            // global index of slot 0 of each digit, minus tile_start
   u32 scan[THREADS / 32 + 1];
   int tile;
-  u64 keys[THREADS * ITEMS];
   V vals[THREADS * ITEMS];
+  K keys[THREADS * ITEMS];
 };
 
 // THREADS x ITEMS terms per tile, warp-striped; LB = predecessors read per look-back round trip.
@@ -187,11 +188,15 @@ __device__ __forceinline__ u32 key_byte(u64 key, int which) {
   const u32 half = which < 4 ? (u32)key : (u32)(key >> 32);
   return __byte_perm(half, 0u, 0x4440u | (u32)(which & 3));
 }
+// narrow keys (2n <= 32 bits): the whole word is one register
+__device__ __forceinline__ u32 key_byte(u32 key, int which) {
+  return __byte_perm(key, 0u, 0x4440u | (u32)(which & 3));
+}
 
-template <typename V, int THREADS, int ITEMS, int LB>
-__global__ void __launch_bounds__(THREADS, (THREADS <= 256 ? 3 : 2))
-k_onesweep(const u64* __restrict__ keys_in, const V* __restrict__ vals_in,
-           u64* __restrict__ keys_out, V* __restrict__ vals_out,
+template <typename K, typename V, int THREADS, int ITEMS, int LB, int MINB = (THREADS <= 256 ? 3 : 2)>
+__global__ void __launch_bounds__(THREADS, MINB)
+k_onesweep(const K* __restrict__ keys_in, const V* __restrict__ vals_in,
+           K* __restrict__ keys_out, V* __restrict__ vals_out,
            const int64_t* __restrict__ seg, int n_seg, const int64_t* __restrict__ tile_prefix,
            const u32* __restrict__ digit_base, int base_stride, u32* status, u32* ticket, int which,
            int ahead, int debug) {
@@ -199,7 +204,7 @@ k_onesweep(const u64* __restrict__ keys_in, const V* __restrict__ vals_in,
   constexpr int TILE = THREADS * ITEMS;
   static_assert(THREADS >= QX_RADIX, "one thread per digit in the scan");
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  SortSmem<V, THREADS, ITEMS>& sm = *reinterpret_cast<SortSmem<V, THREADS, ITEMS>*>(smem_raw);
+  SortSmem<K, V, THREADS, ITEMS>& sm = *reinterpret_cast<SortSmem<K, V, THREADS, ITEMS>*>(smem_raw);
   const int tid = threadIdx.x, warp = tid >> 5, lane = lane_id();
 
   if (tid == 0) sm.tile = (int)atomicAdd(ticket, 1u);
@@ -212,7 +217,7 @@ k_onesweep(const u64* __restrict__ keys_in, const V* __restrict__ vals_in,
   const int64_t start = seg[g] + (tile - tile_prefix[g]) * TILE;
   const int count = (int)min((int64_t)TILE, seg[g + 1] - start);
   const bool full = count == TILE;
-  const u64* kin = keys_in + start;
+  const K* kin = keys_in + start;
   const V* vin = vals_in + start;
 
   // ---- L2 prefetch of the tile that a CTA will own `ahead` tickets from now.  Tickets are
@@ -224,15 +229,15 @@ k_onesweep(const u64* __restrict__ keys_in, const V* __restrict__ vals_in,
     const int gp = tile_segment(tile_prefix, n_seg, tp);
     const int64_t sp = seg[gp] + (tp - tile_prefix[gp]) * TILE;
     const int cp = (int)min((int64_t)TILE, seg[gp + 1] - sp);
-    for (int i = tid * 16; i < cp; i += THREADS * 16) {
-      asm volatile("prefetch.global.L2 [%0];" ::"l"(keys_in + sp + i));
+    for (int i = tid * 16; i < cp; i += THREADS * 16) {      // one 128-byte line of doubles per step
+      if (sizeof(K) == 8 || (i & 16) == 0) asm volatile("prefetch.global.L2 [%0];" ::"l"(keys_in + sp + i));
       asm volatile("prefetch.global.L2 [%0];" ::"l"(vals_in + sp + i));
       if (sizeof(V) > 8) asm volatile("prefetch.global.L2 [%0];" ::"l"(vals_in + sp + i + 8));
     }
   }
 
   // ---- load, warp-striped: warp w owns tile slots [w*32*ITEMS, (w+1)*32*ITEMS)
-  u64 key[ITEMS];
+  K key[ITEMS];
   const int wslot = warp * (32 * ITEMS) + lane;
   if (full) {
 #pragma unroll
@@ -241,7 +246,7 @@ k_onesweep(const u64* __restrict__ keys_in, const V* __restrict__ vals_in,
 #pragma unroll
     for (int k = 0; k < ITEMS; ++k) {
       const int idx = wslot + k * 32;
-      key[k] = idx < count ? ld_stream(kin + idx) : ~0ull;          // padding sorts last
+      key[k] = idx < count ? ld_stream(kin + idx) : (K)~(K)0;       // padding sorts last
     }
   }
 
@@ -341,7 +346,7 @@ k_onesweep(const u64* __restrict__ keys_in, const V* __restrict__ vals_in,
   for (int k = 0; k < ITEMS; ++k) {
     const int slot = k * THREADS + tid;
     if (full || slot < count) {
-      const u64 kk = sm.keys[slot];
+      const K kk = sm.keys[slot];
       const int64_t dst = sm.gbase[key_byte(kk, which)] + slot;
       st_stream(keys_out + dst, kk);
       st_stream(vals_out + dst, sm.vals[slot]);
@@ -352,12 +357,12 @@ k_onesweep(const u64* __restrict__ keys_in, const V* __restrict__ vals_in,
 // ---------------------------------------------------------------------------------
 // reduce-by-key + drop + compaction over the sorted segments
 // ---------------------------------------------------------------------------------
-template <typename V, int kRedThreads, int kRedItems>
+template <typename K, typename V, int kRedThreads, int kRedItems>
 struct ReduceSmem {
   static constexpr int kRedTile = kRedThreads * kRedItems;
   static constexpr int kRedWarps = kRedThreads / 32;
-  u64 key[kRedTile + 2];       // [0] = key before the tile, [1..cnt] = tile
   V val[kRedTile];
+  K key[kRedTile + 2];         // [0] = key before the tile, [1..cnt] = tile
   u32 opens[kRedTile / 32];    // bit j: tile slot j is the first term of a non-empty segment
   u64 scan[kRedWarps + 1];
   u64 base;
@@ -370,15 +375,16 @@ struct ReduceSmem {
 // The tile (keys, coefficients, one halo key) is staged in shared memory with coalesced
 // streaming loads, so every term is read from HBM exactly once and no thread searches the
 // offset table; only runs that cross the tile end touch global memory again.
-template <typename V, int kRedThreads, int kRedItems>
+template <typename K, typename V, int kRedThreads, int kRedItems>
 __global__ void __launch_bounds__(kRedThreads)
-k_reduce(const u64* __restrict__ keys_in, const V* __restrict__ vals_in,
+k_reduce(const K* __restrict__ keys_in, const V* __restrict__ vals_in,
          const int64_t* __restrict__ seg_in, int n_seg, u64* __restrict__ keys_out,
          V* __restrict__ vals_out, int64_t* __restrict__ seg_out, u64* status, u32* ticket,
          double eps, int debug) {
   constexpr int kRedTile = kRedThreads * kRedItems;
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  ReduceSmem<V, kRedThreads, kRedItems>& sm = *reinterpret_cast<ReduceSmem<V, kRedThreads, kRedItems>*>(smem_raw);
+  ReduceSmem<K, V, kRedThreads, kRedItems>& sm =
+      *reinterpret_cast<ReduceSmem<K, V, kRedThreads, kRedItems>*>(smem_raw);
   if (threadIdx.x == 0) sm.tile = (int)atomicAdd(ticket, 1u);
   if (threadIdx.x < kRedTile / 32) sm.opens[threadIdx.x] = 0u;
   __syncthreads();
@@ -394,7 +400,7 @@ k_reduce(const u64* __restrict__ keys_in, const V* __restrict__ vals_in,
     sm.key[1 + j] = ld_stream(keys_in + t0 + j);
     sm.val[j] = ld_stream(vals_in + t0 + j);
   }
-  if (threadIdx.x == 0) sm.key[0] = t0 > 0 ? keys_in[t0 - 1] : 0ull;
+  if (threadIdx.x == 0) sm.key[0] = t0 > 0 ? keys_in[t0 - 1] : (K)0;
   {   // segments that start inside this tile
     int lo = 0, hi = n_seg;                         // first g with seg_in[g] >= t0
     while (lo < hi) {
@@ -409,7 +415,7 @@ k_reduce(const u64* __restrict__ keys_in, const V* __restrict__ vals_in,
   }
   __syncthreads();
 
-  u64 key[kRedItems];
+  K key[kRedItems];
   V sum[kRedItems];
   u32 pre[kRedItems];          // kept heads before this item inside the warp
   u32 flags = 0;               // bit k: item k is a kept head; bit 16+k: item k opens a segment
@@ -457,7 +463,7 @@ k_reduce(const u64* __restrict__ keys_in, const V* __restrict__ vals_in,
   for (int k = 0; k < kRedItems; ++k) {
     const int64_t pos = base + pre[k];
     if (flags & (1u << k)) {
-      st_stream(keys_out + pos, key[k]);
+      st_stream(keys_out + pos, (u64)key[k]);
       st_stream(vals_out + pos, sum[k]);
     }
     if (flags & (1u << (16 + k))) {
@@ -636,18 +642,19 @@ inline int sort_prefetch_distance(int sm_count) {
   return v >= 0 ? v : 2 * sm_count;     // ~ resident CTAs (two per SM)
 }
 
-template <typename V, int THREADS, int ITEMS, int LB>
+template <typename K, typename V, int THREADS, int ITEMS, int LB, int MINB = (THREADS <= 256 ? 3 : 2)>
 int launch_pass(QxArena* ar, MergeBuffers<V>& mb, int cur, int64_t tiles_ub, const int64_t* tile_prefix,
                 const u32* digit_base, int base_stride, u32* ticket, int which) {
-  using Smem = SortSmem<V, THREADS, ITEMS>;
+  using Smem = SortSmem<K, V, THREADS, ITEMS>;
   static bool attr_set = false;
   if (!attr_set) {
-    QX_CUDA(cudaFuncSetAttribute(k_onesweep<V, THREADS, ITEMS, LB>,
+    QX_CUDA(cudaFuncSetAttribute(k_onesweep<K, V, THREADS, ITEMS, LB, MINB>,
                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(Smem)));
     attr_set = true;
   }
-  k_onesweep<V, THREADS, ITEMS, LB><<<(unsigned)tiles_ub, THREADS, sizeof(Smem), ar->stream>>>(
-      mb.keys[cur], mb.vals[cur], mb.keys[cur ^ 1], mb.vals[cur ^ 1], mb.seg[cur], mb.n_seg, tile_prefix,
+  k_onesweep<K, V, THREADS, ITEMS, LB, MINB><<<(unsigned)tiles_ub, THREADS, sizeof(Smem), ar->stream>>>(
+      reinterpret_cast<const K*>(mb.keys[cur]), mb.vals[cur], reinterpret_cast<K*>(mb.keys[cur ^ 1]),
+      mb.vals[cur ^ 1], mb.seg[cur], mb.n_seg, tile_prefix,
       digit_base, base_stride, ar->status, ticket, which, sort_prefetch_distance(ar->sm_count),
       getenv("QX_SORT_DEBUG") ? atoi(getenv("QX_SORT_DEBUG")) : 0);
   QX_CUDA(cudaGetLastError());
@@ -660,7 +667,7 @@ inline int sort_variant() {
   if (v < 0) {
     const char* e = getenv("QX_SORT_VARIANT");
     v = e ? atoi(e) : 0;
-    if (v < 0 || v > 8) v = 0;
+    if (v < 0 || v > 14) v = 0;
   }
   return v;
 }
@@ -676,32 +683,50 @@ inline int sort_tile_terms(int variant, size_t value_bytes) {
     case 6: return 768 * 6;
     case 7: return 1024 * 4;
     case 8: return 384 * 12;
+    case 10: return 384 * 12;
+    case 11: return 256 * 16;
+    case 12: return 256 * 12;
+    case 13: return 512 * 8;
+    case 14: return 512 * 12;
     default: return 384 * 12;
   }
 }
 
-template <typename V>
+template <typename K, typename V>
 int dispatch_pass(int variant, QxArena* ar, MergeBuffers<V>& mb, int cur, int64_t tiles_ub,
                   const int64_t* tile_prefix, const u32* digit_base, int base_stride, u32* ticket,
                   int which) {
   if (sizeof(V) > 8)
-    return launch_pass<V, 256, 12, 8>(ar, mb, cur, tiles_ub, tile_prefix, digit_base, base_stride, ticket, which);
+    return launch_pass<K, V, 256, 12, 8>(ar, mb, cur, tiles_ub, tile_prefix, digit_base, base_stride, ticket, which);
   switch (variant) {
-    case 1: return launch_pass<V, 384, 12, 16>(ar, mb, cur, tiles_ub, tile_prefix, digit_base, base_stride, ticket, which);
-    case 2: return launch_pass<V, 256, 12, 8>(ar, mb, cur, tiles_ub, tile_prefix, digit_base, base_stride, ticket, which);
-    case 3: return launch_pass<V, 256, 16, 8>(ar, mb, cur, tiles_ub, tile_prefix, digit_base, base_stride, ticket, which);
-    case 4: return launch_pass<V, 512, 8, 8>(ar, mb, cur, tiles_ub, tile_prefix, digit_base, base_stride, ticket, which);
-    case 5: return launch_pass<V, 384, 12, 32>(ar, mb, cur, tiles_ub, tile_prefix, digit_base, base_stride, ticket, which);
-    case 6: return launch_pass<V, 768, 6, 8>(ar, mb, cur, tiles_ub, tile_prefix, digit_base, base_stride, ticket, which);
-    case 7: return launch_pass<V, 1024, 4, 8>(ar, mb, cur, tiles_ub, tile_prefix, digit_base, base_stride, ticket, which);
-    case 8: return launch_pass<V, 384, 12, 4>(ar, mb, cur, tiles_ub, tile_prefix, digit_base, base_stride, ticket, which);
-    default: return launch_pass<V, 384, 12, 8>(ar, mb, cur, tiles_ub, tile_prefix, digit_base, base_stride, ticket, which);
+    case 1: return launch_pass<K, V, 384, 12, 16>(ar, mb, cur, tiles_ub, tile_prefix, digit_base, base_stride, ticket, which);
+    case 2: return launch_pass<K, V, 256, 12, 8>(ar, mb, cur, tiles_ub, tile_prefix, digit_base, base_stride, ticket, which);
+    case 3: return launch_pass<K, V, 256, 16, 8>(ar, mb, cur, tiles_ub, tile_prefix, digit_base, base_stride, ticket, which);
+    case 4: return launch_pass<K, V, 512, 8, 8>(ar, mb, cur, tiles_ub, tile_prefix, digit_base, base_stride, ticket, which);
+    case 5: return launch_pass<K, V, 384, 12, 32>(ar, mb, cur, tiles_ub, tile_prefix, digit_base, base_stride, ticket, which);
+    case 6: return launch_pass<K, V, 768, 6, 8>(ar, mb, cur, tiles_ub, tile_prefix, digit_base, base_stride, ticket, which);
+    case 7: return launch_pass<K, V, 1024, 4, 8>(ar, mb, cur, tiles_ub, tile_prefix, digit_base, base_stride, ticket, which);
+    case 8: return launch_pass<K, V, 384, 12, 4>(ar, mb, cur, tiles_ub, tile_prefix, digit_base, base_stride, ticket, which);
+    case 10: return launch_pass<K, V, 384, 12, 8, 3>(ar, mb, cur, tiles_ub, tile_prefix, digit_base, base_stride, ticket, which);
+    case 11: return launch_pass<K, V, 256, 16, 8, 3>(ar, mb, cur, tiles_ub, tile_prefix, digit_base, base_stride, ticket, which);
+    case 12: return launch_pass<K, V, 256, 12, 8, 4>(ar, mb, cur, tiles_ub, tile_prefix, digit_base, base_stride, ticket, which);
+    case 13: return launch_pass<K, V, 512, 8, 8, 2>(ar, mb, cur, tiles_ub, tile_prefix, digit_base, base_stride, ticket, which);
+    case 14: return launch_pass<K, V, 512, 12, 8, 2>(ar, mb, cur, tiles_ub, tile_prefix, digit_base, base_stride, ticket, which);
+    default:
+      // narrow keys: 56 registers and 68 KB of shared memory per CTA -> three CTAs (36 warps) per SM
+      // instead of two; the pass is latency-bound, not HBM-bound (profiles/r01g), so occupancy pays
+      if (sizeof(K) == 4)
+        return launch_pass<K, V, 384, 12, 8, 3>(ar, mb, cur, tiles_ub, tile_prefix, digit_base, base_stride, ticket, which);
+      return launch_pass<K, V, 384, 12, 8>(ar, mb, cur, tiles_ub, tile_prefix, digit_base, base_stride, ticket, which);
   }
 }
 
 // do_reduce = false: sort only (keys known unique and nothing to drop, e.g. after a run of
 // Clifford gates) -- the segment offsets do not change and no rank read-back is needed.
-template <typename V>
+// K = u32: the live buffer holds NARROW keys (one 32-bit word per term, 2n <= 32) as written by
+// the fused expansion kernel; every pass then moves 12 B per term instead of 16 and the reduce
+// widens back to the store's 64-bit keys.  Narrow keys never leave a merge.
+template <typename V, typename K = u64>
 int merge_large(QxArena* ar, MergeBuffers<V>& mb, double eps, int cls_reduce, bool do_reduce = true) {
   const int n_seg = mb.n_seg;
   const int passes = std::min(kMaxPasses, (2 * ar->n_qubits + QX_RADIX_BITS - 1) / QX_RADIX_BITS);
@@ -735,9 +760,9 @@ int merge_large(QxArena* ar, MergeBuffers<V>& mb, double eps, int cls_reduce, bo
   QX_CUDA(cudaGetLastError());
   {
     const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(tiles_ub, (int64_t)ar->sm_count * 4));
-    QxProfileScope prof(QX_K_SORT_HIST, ar->stream, 8.0 * (double)mb.ub_total);
-    k_sort_hist<<<grid, kSortThreads, 0, ar->stream>>>(mb.keys[cur], mb.seg[cur], n_seg, tile_prefix,
-                                                       hist, passes, tile_terms);
+    QxProfileScope prof(QX_K_SORT_HIST, ar->stream, (double)sizeof(K) * (double)mb.ub_total);
+    k_sort_hist<K><<<grid, kSortThreads, 0, ar->stream>>>(reinterpret_cast<const K*>(mb.keys[cur]), mb.seg[cur],
+                                                          n_seg, tile_prefix, hist, passes, tile_terms);
     QX_CUDA(cudaGetLastError());
   }
   k_sort_scan_hist<<<n_seg * passes, QX_RADIX, 0, ar->stream>>>(hist);
@@ -749,28 +774,30 @@ int merge_large(QxArena* ar, MergeBuffers<V>& mb, double eps, int cls_reduce, bo
   for (int p = 0; p < passes; ++p) {
     QX_CUDA(cudaMemsetAsync(ar->status, 0, sizeof(u32) * (size_t)(tiles_ub * QX_RADIX), ar->stream));
     QX_CUDA(cudaMemsetAsync(ticket, 0, sizeof(u32), ar->stream));
-    QxProfileScope prof(QX_K_SORT_PASS, ar->stream, 2.0 * (8.0 + sizeof(V)) * (double)mb.ub_total);
-    QX_TRY(dispatch_pass<V>(variant, ar, mb, cur, tiles_ub, tile_prefix, hist + (size_t)p * QX_RADIX,
-                            passes * QX_RADIX, ticket, p));
+    QxProfileScope prof(QX_K_SORT_PASS, ar->stream, 2.0 * (sizeof(K) + sizeof(V)) * (double)mb.ub_total);
+    QX_TRY((dispatch_pass<K, V>(variant, ar, mb, cur, tiles_ub, tile_prefix, hist + (size_t)p * QX_RADIX,
+                                passes * QX_RADIX, ticket, p)));
     cur ^= 1;
   }
   if (!do_reduce) {
+    if (sizeof(K) != 8) return qx_fail(QX_ERR_CONSISTENCY, "sort-only needs full-width keys (internal error)");
     mb.cur = cur;
     return QX_OK;
   }
   QX_CUDA(cudaMemsetAsync(ticket, 0, sizeof(u32), ar->stream));
   {
-    QxProfileScope prof(cls_reduce, ar->stream, (8.0 + sizeof(V)) * 2.0 * (double)mb.ub_total);
+    QxProfileScope prof(cls_reduce, ar->stream, (sizeof(K) + 8.0 + 2.0 * sizeof(V)) * (double)mb.ub_total);
 #define QX_LAUNCH_REDUCE(T, I)                                                                        \
   do {                                                                                                \
     static bool attr = false;                                                                         \
     if (!attr) {                                                                                      \
-      QX_CUDA(cudaFuncSetAttribute(k_reduce<V, T, I>, cudaFuncAttributeMaxDynamicSharedMemorySize,    \
-                                   (int)sizeof(ReduceSmem<V, T, I>)));                                \
+      QX_CUDA(cudaFuncSetAttribute(k_reduce<K, V, T, I>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
+                                   (int)sizeof(ReduceSmem<K, V, T, I>)));                             \
       attr = true;                                                                                    \
     }                                                                                                 \
-    k_reduce<V, T, I><<<(unsigned)red_tiles, T, sizeof(ReduceSmem<V, T, I>), ar->stream>>>(           \
-        mb.keys[cur], mb.vals[cur], mb.seg[cur], n_seg, mb.keys[cur ^ 1], mb.vals[cur ^ 1],           \
+    k_reduce<K, V, T, I><<<(unsigned)red_tiles, T, sizeof(ReduceSmem<K, V, T, I>), ar->stream>>>(     \
+        reinterpret_cast<const K*>(mb.keys[cur]), mb.vals[cur], mb.seg[cur], n_seg, mb.keys[cur ^ 1], \
+        mb.vals[cur ^ 1],                                                                             \
         mb.seg[cur ^ 1], red_status, ticket, eps,                                                     \
         getenv("QX_SORT_DEBUG") ? atoi(getenv("QX_SORT_DEBUG")) : 0);                                 \
   } while (0)

@@ -9,9 +9,11 @@
 // Term arrays are touched once per pass: keep them out of L1 so the 126 MB L2
 // and the look-back words are not evicted by them.
 __device__ __forceinline__ u64 ld_stream(const u64* p) { return __ldcs(p); }
+__device__ __forceinline__ u32 ld_stream(const u32* p) { return __ldcs(p); }
 __device__ __forceinline__ double ld_stream(const double* p) { return __ldcs(p); }
 __device__ __forceinline__ double2 ld_stream(const double2* p) { return __ldcs(p); }
 __device__ __forceinline__ void st_stream(u64* p, u64 v) { __stcs(p, v); }
+__device__ __forceinline__ void st_stream(u32* p, u32 v) { __stcs(p, v); }
 __device__ __forceinline__ void st_stream(double* p, double v) { __stcs(p, v); }
 __device__ __forceinline__ void st_stream(double2* p, double2 v) { __stcs(p, v); }
 

@@ -116,3 +116,10 @@ int qx_store_reserve(qx_store* s, int64_t terms, bool keep_live);
 int qx_store_refresh(qx_store* s);          // D2H of the live offsets, sets exact
 inline void qx_store_flip(qx_store* s) { s->cur ^= 1; }
 inline int qx_store_scratch(qx_store* s, int64_t bytes) { return qx_arena_scratch(s, bytes); }
+
+// clifford.cu: validate a sign-permutation program against the store's qubit count
+int qx_check_program(const qx_store* s, const uint32_t* program, int32_t n_ops);
+// the reference's CX tables (lut.py:108-134) in the packed form of qx_apply_clifford
+void qx_standard_cx(u32* cx_c, u32* cx_t, u32* cx_s);
+// merge.cu: canonicalize (or only sort) the live buffer; narrow = it holds 32-bit raw keys
+int qx_run_merge(qx_store* s, double eps, bool sort_only, bool narrow);

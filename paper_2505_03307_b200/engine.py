@@ -109,6 +109,7 @@ class _Walker:
         self.queue_has_cx = False
         self.unsorted = False          # a permutation ran since the last merge
         self.pending = None            # (step, phase) of a branching op whose merge is deferred
+        self.staged = None             # (counts, axes, weights) of a U_k not launched yet (v2/v3)
         self.open_slots: list = []     # trace rows waiting for the deferred merge
         self.pending_gates = 0         # v1 gates applied since the deferred branch
         self.ranks = [1] * len(self.ids)
@@ -151,13 +152,51 @@ class _Walker:
                     f"all terms of generator {self.ids[local]} dropped at operator step {step}"
                 )
 
+    def stage_operator(self, counts, axes, weights):
+        """v2/v3: hold a branching U_k back until the permutation ops behind it are known; they
+        are folded into its expansion kernel (qx_apply_operator_run)."""
+        self.staged = (counts, axes, weights)
+
+    def _run_staged(self, step: int, phase: str):
+        counts, axes, weights = self.staged
+        self.staged = None
+        program = np.array(self.queue, dtype=np.uint32)
+        had_cx = self.queue_has_cx
+        self.queue, self.queue_has_cx = [], False
+        t0 = time.perf_counter()
+        if self.before_merge is not None:
+            # term-partitioned runs re-home terms between the expansion and the merge
+            self.store.apply_operator(counts, axes, weights)
+            self.store.apply_clifford(program)
+            self.before_merge(self.store)
+            self.ranks = self.store.merge(self.eps)
+        else:
+            _, self.ranks = self.store.apply_operator_run(counts, axes, weights, program, self.eps)
+        if self.reduce_ranks is not None:
+            self.ranks = self.reduce_ranks(self.ranks)
+        self.timings[phase] += time.perf_counter() - t0
+        self.unsorted = False
+        self.launch_log["merges"] += 1
+        if len(program):
+            self.launch_log["clifford_runs"] += 1
+            self.launch_log["fused_runs"] = self.launch_log.get("fused_runs", 0) + 1
+        del had_cx
+        for local, r in enumerate(self.ranks):
+            if r == 0:
+                raise NumericalCollapseError(
+                    f"all terms of generator {self.ids[local]} dropped at operator step {step}"
+                )
+
     def resolve(self, trace):
         """Run the deferred merge (after the permutation ops queued behind it)."""
         if self.pending is None:
             return
         step, phase = self.pending
-        self.flush()
-        self._merge_now(step, phase, after_branch=True)
+        if self.staged is not None:
+            self._run_staged(step, phase)
+        else:
+            self.flush()
+            self._merge_now(step, phase, after_branch=True)
         self.pending = None
         for slot in self.open_slots:
             trace[slot] = list(self.ranks)
@@ -357,8 +396,8 @@ def _walk_operators(partition, lut, is_perm, tables, w: _Walker, trace, counters
                             f"dense flatten needs a 4**{n}-element buffer (> {DENSE_FLATTEN_BUDGET}); "
                             "use the ragged layout for circuits of this size"
                         )
-                w.store.apply_operator(counts, axes, weights)
                 w.timings["sub_flatten"] += time.perf_counter() - t0
+                w.stage_operator(counts, axes, weights)
                 w.branched(step, "sub_flatten", trace)
             counters["sub_flatten_ops"] += 1
             ui += 1

@@ -139,6 +139,20 @@ class DeviceStore:
                                               int(term_limit), C.byref(raw)))
         return raw.value
 
+    def apply_operator_run(self, counts, axes, weights, program, eps: float, term_limit: int = 0):
+        """U_k + the sign-permutation run behind it + merge in one call; returns (raw, ranks)."""
+        counts = np.ascontiguousarray(counts, dtype=np.int32).reshape(-1)
+        axes = np.ascontiguousarray(axes, dtype=np.int32).reshape(-1)
+        weights = np.ascontiguousarray(weights, dtype=np.float64).reshape(-1)
+        prog = np.ascontiguousarray(program, dtype=np.uint32)
+        raw = C.c_int64()
+        ranks = np.zeros(self.n_segments, dtype=np.int64)
+        c, t, s = self._cx
+        nat.check(nat.lib().qx_apply_operator_run(
+            self._h, nat.ptr(counts), nat.ptr(axes), nat.ptr(weights), nat.ptr(prog) if len(prog) else None,
+            len(prog), c, t, s, float(eps), int(term_limit), C.byref(raw), nat.ptr(ranks)))
+        return raw.value, ranks.tolist()
+
     def count_operator(self, counts) -> list:
         counts = np.ascontiguousarray(counts, dtype=np.int32).reshape(-1)
         out = np.zeros(self.n_segments, dtype=np.int64)

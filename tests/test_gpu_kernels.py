@@ -206,3 +206,78 @@ def test_zi_sums_and_norms():
     for (lam, keys), a, b in zip(gens, zi, nr):
         mask = (((keys >> np.uint64(1)) ^ keys) & np.uint64(0x5555555555555555)) == 0
         assert abs(a - lam[mask].sum()) < 1e-9 and abs(b - np.dot(lam, lam)) < 1e-9
+
+
+@pytest.mark.parametrize("n,terms,rot_qubits,n_ops", [
+    (3, 40, 3, 0), (6, 300, 6, 25),            # small merge path, 32-bit working keys
+    (12, 60, 9, 40), (16, 8, 12, 15),          # large path -> narrow (32-bit) raw keys
+    (16, 2000, 5, 200),                        # many sources per output tile
+    (20, 50, 9, 60), (32, 20, 10, 300),        # 64-bit working keys
+    (14, 30, 10, 0),                           # narrow keys without a Clifford run
+])
+def test_operator_run_equals_three_steps(n, terms, rot_qubits, n_ops):
+    """qx_apply_operator_run (Clifford run folded into the expansion, narrow raw keys) must give
+    bit-for-bit what qx_apply_operator + qx_apply_clifford + qx_merge give, which in turn are
+    checked against the oracle above."""
+    rng = np.random.default_rng(n * 1000 + terms + n_ops)
+    gens = []
+    for s in (terms, 1, max(1, terms // 3)):
+        lam, keys = random_terms(rng, n, s, s)
+        keys = np.unique(keys)
+        gens.append((lam[: len(keys)], keys))
+    qs = rng.choice(n, size=rot_qubits, replace=False)
+    gates = [qx.Instruction(str(rng.choice(["RX", "RY", "RZ"])), (int(j),), float(rng.uniform(0, 6.28))) for j in qs]
+    block = oracle.lut_blocks(oracle.partition(gates, n), n)[0]
+    counts, axes, weights = lut.operator_tables(block)
+    prog = []
+    for g in qx.gen_random(n, n_ops, rng, gates=("H", "S", "X", "SX", "CX")) if n_ops else []:
+        prog.append(lut.cx_op(n, *g.wires) if g.gate == "CX" else lut.perm_op(n, g.wires[0], lut.FIXED_PERMS[g.gate]))
+    with DeviceStore(n, len(gens), 0) as st:
+        st.upload(gens)
+        st.apply_operator(counts, axes, weights)
+        st.apply_clifford(prog)
+        want_ranks = st.merge(1e-12)
+        want = [(l.copy(), k.copy()) for l, k in st.segments()]
+    with DeviceStore(n, len(gens), 0) as st:
+        st.upload(gens)
+        raw, ranks = st.apply_operator_run(counts, axes, weights, prog, 1e-12)
+        got = [(l.copy(), k.copy()) for l, k in st.segments()]
+    assert ranks == want_ranks and raw >= sum(ranks)
+    for (gl, gk), (wl, wk) in zip(got, want):
+        assert np.array_equal(gk, wk)
+        assert np.array_equal(gl, wl)          # sign flips are exact, summation order unchanged
+
+
+def test_operator_run_with_corrupted_cx_table_is_table_driven():
+    """A CX table that is not the conjugation (mutation test, reference tests/test_cli.py:198-203)
+    must not be 'repaired' by the homomorphism shortcut: the call falls back to the table-driven
+    three-step sequence and reproduces the corrupted result."""
+    rng = np.random.default_rng(77)
+    n = 8
+    lam, keys = random_terms(rng, n, 200, 200)
+    keys = np.unique(keys)
+    lam = lam[: len(keys)]
+    gates = [qx.Instruction("RY", (j,), 0.3 + j) for j in range(5)]
+    block = oracle.lut_blocks(oracle.partition(gates, n), n)[0]
+    counts, axes, weights = lut.operator_tables(block)
+    prog = [lut.cx_op(n, 0, 1), lut.cx_op(n, 1, 2), lut.perm_op(n, 2, lut.FIXED_PERMS["H"]), lut.cx_op(n, 2, 3)]
+    bad = np.array(lut.LUT_SIGN).copy()
+    bad[1, 0] = -1
+    outs = []
+    for fused in (False, True):
+        with DeviceStore(n, 1, 0) as st:
+            st.set_cx_tables(bad)
+            st.upload([(lam, keys)])
+            if fused:
+                st.apply_operator_run(counts, axes, weights, prog, 1e-12)
+            else:
+                st.apply_operator(counts, axes, weights)
+                st.apply_clifford(prog)
+                st.merge(1e-12)
+            outs.append([(l.copy(), k.copy()) for l, k in st.segments()][0])
+    assert np.array_equal(outs[0][1], outs[1][1]) and np.array_equal(outs[0][0], outs[1][0])
+    with DeviceStore(n, 1, 0) as st:
+        st.upload([(lam, keys)])
+        st.apply_operator_run(counts, axes, weights, prog, 1e-12)
+        good = [(l.copy(), k.copy()) for l, k in st.segments()][0]
+    assert not np.array_equal(good[0], outs[0][0])
