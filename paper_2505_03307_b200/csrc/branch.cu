@@ -309,6 +309,11 @@ struct EmitSmem {
   u32 scan[kThreads / 32 + 1];
   int64_t lohi[2];
   u64 hfirst0;                 // first block id of the first source (it may start mid-way)
+  // one-source tiles: everything the 27 (or fewer) low-group branches of the source contribute
+  double low_w[27][3];         // weights of the three low digits (1.0 where absent)
+  K low_word[27];              // FUSED: composed image of the low digits; else the digits themselves
+  K low_imx[27];
+  u32 low_e[27];
 };
 
 // K = working key type, KO = type of the keys written (u32 = narrow raw terms for the sort),
@@ -333,9 +338,125 @@ k_expand_emit(const u64* __restrict__ keys_in, const double* __restrict__ lam_in
   }
   const u64 raw_total = roff[total_in];
   const int64_t ntiles = (int64_t)((raw_total + kEmitTile - 1) / kEmitTile);
-  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+  // Each CTA owns a contiguous run of tiles, so the source feeding a tile is found by stepping
+  // from the previous tile's instead of a binary search in global memory, and a source with a
+  // large fan-out (the heavy case: 3^k branches, k up to n) keeps its tables across tiles.
+  const int64_t per_cta = (ntiles + gridDim.x - 1) / gridDim.x;
+  const int64_t tile_begin = (int64_t)blockIdx.x * per_cta;
+  const int64_t tile_end = min(ntiles, tile_begin + per_cta);
+  int64_t src = -1, cached = -1;          // source of the tile's first raw term; source whose low table is in smem
+  u64 off_src = 0, off_next = 0;          // roff[src], roff[src + 1]
+  K key0 = 0;
+  LowGroup<K> g0 = {};
+  double lam0 = 0.0;
+  u32 magic = 0;                          // ceil(2^16 / L): t / L == (t * magic) >> 16 for t < 2^16 / L
+  for (int64_t tile = tile_begin; tile < tile_end; ++tile) {
     const u64 r0 = (u64)tile * kEmitTile;
     const u64 r1 = min(r0 + (u64)kEmitTile, raw_total);          // exclusive
+    if (src < 0) {
+      src = last_le(roff, total_in, r0);
+      off_src = roff[src];
+      off_next = roff[src + 1];
+    } else {
+      while (off_next <= r0) {
+        ++src;
+        off_src = off_next;
+        off_next = roff[src + 1];
+      }
+    }
+    if (off_next >= r1) {
+      // ---- one source feeds the whole tile: no searches, two barriers, ~40 instructions per output
+      if (cached != src) {
+        __syncthreads();                                         // previous tile done with the low table
+        key0 = (K)keys_in[src];
+        lam0 = lam_in[src];
+        g0 = low_group<K>(key0, sm.tb);
+        magic = 65536u / g0.L + 1u;
+        if (threadIdx.x < g0.L) {
+          u32 b = threadIdx.x, pick[3];
+          K word = 0;
+          u32 ex = 0;
+#pragma unroll
+          for (int j = 0; j < 3; ++j) {
+            pick[j] = b % g0.rad[j];
+            b /= g0.rad[j];
+          }
+#pragma unroll
+          for (int j = 2; j >= 0; --j) {
+            double w = 1.0;
+            if (g0.bit[j] >= 0) {
+              const int p = g0.bit[j] >> 1;
+              w = sm.tb.w[p][g0.dig[j]][pick[j]];
+              const u32 ax = sm.tb.axis[p][g0.dig[j]][pick[j]];
+              if (FUSED) compose<K>(word, ex, sm.im.img[p][ax - 1], sm.im.imx[p][ax - 1], sm.im.e[p][ax - 1]);
+              else word |= (K)ax << g0.bit[j];
+            }
+            sm.low_w[threadIdx.x][j] = w;
+          }
+          sm.low_word[threadIdx.x] = word;
+          sm.low_imx[threadIdx.x] = (word ^ (word >> 1)) & Plane<K>::lo;
+          sm.low_e[threadIdx.x] = ex & 3u;
+        }
+        cached = src;
+      }
+      const u64 b0 = r0 - off_src;                               // first branch of the tile
+      const u64 h0 = b0 / g0.L;                                  // its block
+      const u32 bl0 = (u32)(b0 - h0 * g0.L);
+      const u32 n_out = (u32)(r1 - r0);
+      const u32 n_blocks = (bl0 + n_out - 1u) / g0.L + 1u;
+      __syncthreads();                                           // low table visible, p_hi/k_hi free
+      for (u32 e = threadIdx.x; e < n_blocks; e += kThreads) {
+        K h = (K)(h0 + e);
+        K choice = 0;
+        for (K m = g0.hi_mask; m;) {
+          const int bit = KeyOps<K>::lowest(m);
+          m &= m - 1;
+          u32 pick;
+          divmod_small<K>(h, sm.tb.cnt[bit >> 1][(u32)((key0 >> bit) & 3u) - 1u], h, pick);
+          choice |= (K)pick << bit;
+        }
+        double v = lam0;
+        K out = 0;
+        u32 ex = 0;
+        for (K m = g0.hi_mask; m;) {                             // qubit 0 first (stabilizer.py:311-319)
+          const int bit = KeyOps<K>::highest(m);
+          m ^= (K)1 << bit;
+          const u32 d = (u32)((key0 >> bit) & 3u) - 1u, pick = (u32)(choice >> bit) & 3u;
+          v *= sm.tb.w[bit >> 1][d][pick];
+          const u32 ax = sm.tb.axis[bit >> 1][d][pick];
+          if (FUSED) compose<K>(out, ex, sm.im.img[bit >> 1][ax - 1], sm.im.imx[bit >> 1][ax - 1], sm.im.e[bit >> 1][ax - 1]);
+          else out |= (K)ax << bit;
+        }
+        sm.p_hi[e] = v;
+        sm.k_hi[e] = out;
+        if (FUSED) sm.e_hi[e] = (unsigned char)(ex & 3u);
+      }
+      __syncthreads();
+#pragma unroll
+      for (int k = 0; k < kEmitPer; ++k) {
+        const u32 idx = (u32)k * kThreads + threadIdx.x;
+        if (idx < n_out) {
+          const u32 t = bl0 + idx;
+          const u32 e = (t * magic) >> 16;                       // t / L
+          const u32 bl = t - e * g0.L;
+          double v = sm.p_hi[e];
+          v *= sm.low_w[bl][2];                                  // ((p_hi * w2) * w1) * w0, absent = 1.0
+          v *= sm.low_w[bl][1];
+          v *= sm.low_w[bl][0];
+          K out = sm.k_hi[e];
+          if (FUSED) {
+            u32 ex = (u32)sm.e_hi[e];
+            compose<K>(out, ex, sm.low_word[bl], sm.low_imx[bl], sm.low_e[bl]);
+            if (composed_sign<K>(out, ex)) v = -v;               // sign flips are exact
+          } else {
+            out |= sm.low_word[bl];
+          }
+          st_stream(keys_out + r0 + idx, (KO)out);
+          st_stream(lam_out + r0 + idx, v);
+        }
+      }
+      continue;
+    }
     __syncthreads();                                             // previous tile fully consumed
     if (threadIdx.x == 0) sm.lohi[0] = last_le(roff, total_in, r0);
     if (threadIdx.x == 32) sm.lohi[1] = last_le(roff, total_in, r1 - 1);
@@ -406,16 +527,16 @@ k_expand_emit(const u64* __restrict__ keys_in, const double* __restrict__ lam_in
     __syncthreads();
 
     // ---- 3. one raw term per thread per round, consecutive lanes = consecutive terms
-    const bool one_source = span == 1;                 // the common heavy case: hoist its digits
-    const K key0 = (K)keys_in[lo];
-    const LowGroup<K> g0 = low_group<K>(key0, sm.tb);
+    const bool one_source = span == 1;                 // hoist its digits
+    const K keyf = (K)keys_in[lo];
+    const LowGroup<K> gf = low_group<K>(keyf, sm.tb);
 #pragma unroll 2
     for (int k = 0; k < kEmitPer; ++k) {
       const u64 r = r0 + (u64)k * kThreads + threadIdx.x;
       if (r >= r1) break;
       const int rel = one_source ? 0 : (int)last_le(sm.win, span, r);
-      const K key = one_source ? key0 : (K)keys_in[lo + rel];
-      const LowGroup<K> g = one_source ? g0 : low_group<K>(key, sm.tb);
+      const K key = one_source ? keyf : (K)keys_in[lo + rel];
+      const LowGroup<K> g = one_source ? gf : low_group<K>(key, sm.tb);
       K q = (K)(r - sm.win[rel]);
       u32 pick[3];
 #pragma unroll
