@@ -73,6 +73,30 @@ __device__ __forceinline__ int tile_segment(const int64_t* tile_prefix, int n_se
   return lo;
 }
 
+// One record per sort tile, filled once per merge: the passes (and the histogram) read it with a
+// single broadcast load instead of every thread bisecting the segment table in global memory
+// (6 % of the pass's instructions and the head of its critical path, profiles/r01g).
+struct __align__(16) TileInfo {
+  int64_t start;      // first term of the tile
+  int count;          // terms in the tile (<= tile_terms)
+  int seg;            // segment; bit 31 set iff this is the segment's first tile
+};
+
+static __global__ void k_sort_tilemap(const int64_t* __restrict__ seg, int n_seg,
+                                      const int64_t* __restrict__ tile_prefix, TileInfo* __restrict__ info,
+                                      int tile_terms) {
+  const int64_t total_tiles = tile_prefix[n_seg];
+  for (int64_t tile = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; tile < total_tiles;
+       tile += (int64_t)gridDim.x * blockDim.x) {
+    const int g = tile_segment(tile_prefix, n_seg, tile);
+    TileInfo ti;
+    ti.start = seg[g] + (tile - tile_prefix[g]) * tile_terms;
+    ti.count = (int)min((int64_t)tile_terms, seg[g + 1] - ti.start);
+    ti.seg = g | (tile == tile_prefix[g] ? (int)0x80000000 : 0);
+    info[tile] = ti;
+  }
+}
+
 // ---------------------------------------------------------------------------------
 // histogram: hist[g][pass][digit], all passes in one read of the keys
 // ---------------------------------------------------------------------------------
@@ -80,16 +104,16 @@ constexpr int kMaxPasses = 8;
 
 template <typename K>
 static __global__ void __launch_bounds__(kSortThreads)
-k_sort_hist(const K* __restrict__ keys, const int64_t* __restrict__ seg, int n_seg,
-            const int64_t* __restrict__ tile_prefix, u32* __restrict__ hist, int passes,
-            int tile_terms) {
+k_sort_hist(const K* __restrict__ keys, const TileInfo* __restrict__ info,
+            const int64_t* __restrict__ n_tiles, u32* __restrict__ hist, int passes) {
   __shared__ u32 sh[kMaxPasses][QX_RADIX];
   for (int i = threadIdx.x; i < kMaxPasses * QX_RADIX; i += kSortThreads) (&sh[0][0])[i] = 0u;
   __syncthreads();
-  const int64_t total_tiles = tile_prefix[n_seg];
+  const int64_t total_tiles = *n_tiles;
   int cur_g = -1;
   for (int64_t tile = blockIdx.x; tile < total_tiles; tile += gridDim.x) {
-    const int g = tile_segment(tile_prefix, n_seg, tile);
+    const TileInfo ti = info[tile];
+    const int g = ti.seg & 0x7fffffff;
     if (g != cur_g) {
       if (cur_g >= 0) {
         __syncthreads();
@@ -102,8 +126,8 @@ k_sort_hist(const K* __restrict__ keys, const int64_t* __restrict__ seg, int n_s
       }
       cur_g = g;
     }
-    const int64_t start = seg[g] + (tile - tile_prefix[g]) * tile_terms;
-    const int count = (int)min((int64_t)tile_terms, seg[g + 1] - start);
+    const int64_t start = ti.start;
+    const int count = ti.count;
     const int rounds = (count + kSortThreads - 1) / kSortThreads;
 #pragma unroll 4
     for (int k = 0; k < rounds; ++k) {
@@ -197,9 +221,9 @@ template <typename K, typename V, int THREADS, int ITEMS, int LB, int MINB = (TH
 __global__ void __launch_bounds__(THREADS, MINB)
 k_onesweep(const K* __restrict__ keys_in, const V* __restrict__ vals_in,
            K* __restrict__ keys_out, V* __restrict__ vals_out,
-           const int64_t* __restrict__ seg, int n_seg, const int64_t* __restrict__ tile_prefix,
-           const u32* __restrict__ digit_base, int base_stride, u32* status, u32* ticket, int which,
-           int ahead, int debug) {
+           const int64_t* __restrict__ seg, const TileInfo* __restrict__ info,
+           const int64_t* __restrict__ n_tiles, const u32* __restrict__ digit_base, int base_stride,
+           u32* status, u32* ticket, int which, int ahead, int debug) {
   constexpr int WARPS = THREADS / 32;
   constexpr int TILE = THREADS * ITEMS;
   static_assert(THREADS >= QX_RADIX, "one thread per digit in the scan");
@@ -211,11 +235,13 @@ k_onesweep(const K* __restrict__ keys_in, const V* __restrict__ vals_in,
   for (int i = tid; i < WARPS * QX_RADIX; i += THREADS) (&sm.whist[0][0])[i] = 0u;
   __syncthreads();
   const int64_t tile = sm.tile;
-  if (tile >= tile_prefix[n_seg]) return;
-  const int g = tile_segment(tile_prefix, n_seg, tile);
-  const bool first = tile == tile_prefix[g];
-  const int64_t start = seg[g] + (tile - tile_prefix[g]) * TILE;
-  const int count = (int)min((int64_t)TILE, seg[g + 1] - start);
+  const int64_t total_tiles = *n_tiles;
+  if (tile >= total_tiles) return;
+  const TileInfo ti = info[tile];
+  const int g = ti.seg & 0x7fffffff;
+  const bool first = ti.seg < 0;
+  const int64_t start = ti.start;
+  const int count = ti.count;
   const bool full = count == TILE;
   const K* kin = keys_in + start;
   const V* vin = vals_in + start;
@@ -224,11 +250,10 @@ k_onesweep(const K* __restrict__ keys_in, const V* __restrict__ vals_in,
   // handed out in order, so every tile is prefetched exactly once, by the CTA `ahead` tiles
   // before it; with ahead ~ number of resident CTAs the lines arrive in L2 just before use and
   // the loads below pay L2 latency instead of HBM latency.
-  if (ahead > 0 && tile + ahead < tile_prefix[n_seg]) {
-    const int64_t tp = tile + ahead;
-    const int gp = tile_segment(tile_prefix, n_seg, tp);
-    const int64_t sp = seg[gp] + (tp - tile_prefix[gp]) * TILE;
-    const int cp = (int)min((int64_t)TILE, seg[gp + 1] - sp);
+  if (ahead > 0 && tile + ahead < total_tiles) {
+    const TileInfo tp = info[tile + ahead];
+    const int64_t sp = tp.start;
+    const int cp = tp.count;
     for (int i = tid * 16; i < cp; i += THREADS * 16) {      // one 128-byte line of doubles per step
       if (sizeof(K) == 8 || (i & 16) == 0) asm volatile("prefetch.global.L2 [%0];" ::"l"(keys_in + sp + i));
       asm volatile("prefetch.global.L2 [%0];" ::"l"(vals_in + sp + i));
@@ -316,7 +341,7 @@ k_onesweep(const K* __restrict__ keys_in, const V* __restrict__ vals_in,
     u32 excl = 0;
     if (!solo) {
       constexpr int W = LB;
-      const int64_t first_tile = tile_prefix[g];
+      const int64_t first_tile = tile - (start - seg[g]) / TILE;
       int64_t t = tile - 1;
       bool done = false;
       while (!done) {
@@ -643,8 +668,8 @@ inline int sort_prefetch_distance(int sm_count) {
 }
 
 template <typename K, typename V, int THREADS, int ITEMS, int LB, int MINB = (THREADS <= 256 ? 3 : 2)>
-int launch_pass(QxArena* ar, MergeBuffers<V>& mb, int cur, int64_t tiles_ub, const int64_t* tile_prefix,
-                const u32* digit_base, int base_stride, u32* ticket, int which) {
+int launch_pass(QxArena* ar, MergeBuffers<V>& mb, int cur, int64_t tiles_ub, const TileInfo* info,
+                const int64_t* n_tiles, const u32* digit_base, int base_stride, u32* ticket, int which) {
   using Smem = SortSmem<K, V, THREADS, ITEMS>;
   static bool attr_set = false;
   if (!attr_set) {
@@ -654,7 +679,7 @@ int launch_pass(QxArena* ar, MergeBuffers<V>& mb, int cur, int64_t tiles_ub, con
   }
   k_onesweep<K, V, THREADS, ITEMS, LB, MINB><<<(unsigned)tiles_ub, THREADS, sizeof(Smem), ar->stream>>>(
       reinterpret_cast<const K*>(mb.keys[cur]), mb.vals[cur], reinterpret_cast<K*>(mb.keys[cur ^ 1]),
-      mb.vals[cur ^ 1], mb.seg[cur], mb.n_seg, tile_prefix,
+      mb.vals[cur ^ 1], mb.seg[cur], info, n_tiles,
       digit_base, base_stride, ar->status, ticket, which, sort_prefetch_distance(ar->sm_count),
       getenv("QX_SORT_DEBUG") ? atoi(getenv("QX_SORT_DEBUG")) : 0);
   QX_CUDA(cudaGetLastError());
@@ -694,30 +719,30 @@ inline int sort_tile_terms(int variant, size_t value_bytes) {
 
 template <typename K, typename V>
 int dispatch_pass(int variant, QxArena* ar, MergeBuffers<V>& mb, int cur, int64_t tiles_ub,
-                  const int64_t* tile_prefix, const u32* digit_base, int base_stride, u32* ticket,
+                  const TileInfo* info, const int64_t* n_tiles, const u32* digit_base, int base_stride, u32* ticket,
                   int which) {
   if (sizeof(V) > 8)
-    return launch_pass<K, V, 256, 12, 8>(ar, mb, cur, tiles_ub, tile_prefix, digit_base, base_stride, ticket, which);
+    return launch_pass<K, V, 256, 12, 8>(ar, mb, cur, tiles_ub, info, n_tiles, digit_base, base_stride, ticket, which);
   switch (variant) {
-    case 1: return launch_pass<K, V, 384, 12, 16>(ar, mb, cur, tiles_ub, tile_prefix, digit_base, base_stride, ticket, which);
-    case 2: return launch_pass<K, V, 256, 12, 8>(ar, mb, cur, tiles_ub, tile_prefix, digit_base, base_stride, ticket, which);
-    case 3: return launch_pass<K, V, 256, 16, 8>(ar, mb, cur, tiles_ub, tile_prefix, digit_base, base_stride, ticket, which);
-    case 4: return launch_pass<K, V, 512, 8, 8>(ar, mb, cur, tiles_ub, tile_prefix, digit_base, base_stride, ticket, which);
-    case 5: return launch_pass<K, V, 384, 12, 32>(ar, mb, cur, tiles_ub, tile_prefix, digit_base, base_stride, ticket, which);
-    case 6: return launch_pass<K, V, 768, 6, 8>(ar, mb, cur, tiles_ub, tile_prefix, digit_base, base_stride, ticket, which);
-    case 7: return launch_pass<K, V, 1024, 4, 8>(ar, mb, cur, tiles_ub, tile_prefix, digit_base, base_stride, ticket, which);
-    case 8: return launch_pass<K, V, 384, 12, 4>(ar, mb, cur, tiles_ub, tile_prefix, digit_base, base_stride, ticket, which);
-    case 10: return launch_pass<K, V, 384, 12, 8, 3>(ar, mb, cur, tiles_ub, tile_prefix, digit_base, base_stride, ticket, which);
-    case 11: return launch_pass<K, V, 256, 16, 8, 3>(ar, mb, cur, tiles_ub, tile_prefix, digit_base, base_stride, ticket, which);
-    case 12: return launch_pass<K, V, 256, 12, 8, 4>(ar, mb, cur, tiles_ub, tile_prefix, digit_base, base_stride, ticket, which);
-    case 13: return launch_pass<K, V, 512, 8, 8, 2>(ar, mb, cur, tiles_ub, tile_prefix, digit_base, base_stride, ticket, which);
-    case 14: return launch_pass<K, V, 512, 12, 8, 2>(ar, mb, cur, tiles_ub, tile_prefix, digit_base, base_stride, ticket, which);
+    case 1: return launch_pass<K, V, 384, 12, 16>(ar, mb, cur, tiles_ub, info, n_tiles, digit_base, base_stride, ticket, which);
+    case 2: return launch_pass<K, V, 256, 12, 8>(ar, mb, cur, tiles_ub, info, n_tiles, digit_base, base_stride, ticket, which);
+    case 3: return launch_pass<K, V, 256, 16, 8>(ar, mb, cur, tiles_ub, info, n_tiles, digit_base, base_stride, ticket, which);
+    case 4: return launch_pass<K, V, 512, 8, 8>(ar, mb, cur, tiles_ub, info, n_tiles, digit_base, base_stride, ticket, which);
+    case 5: return launch_pass<K, V, 384, 12, 32>(ar, mb, cur, tiles_ub, info, n_tiles, digit_base, base_stride, ticket, which);
+    case 6: return launch_pass<K, V, 768, 6, 8>(ar, mb, cur, tiles_ub, info, n_tiles, digit_base, base_stride, ticket, which);
+    case 7: return launch_pass<K, V, 1024, 4, 8>(ar, mb, cur, tiles_ub, info, n_tiles, digit_base, base_stride, ticket, which);
+    case 8: return launch_pass<K, V, 384, 12, 4>(ar, mb, cur, tiles_ub, info, n_tiles, digit_base, base_stride, ticket, which);
+    case 10: return launch_pass<K, V, 384, 12, 8, 3>(ar, mb, cur, tiles_ub, info, n_tiles, digit_base, base_stride, ticket, which);
+    case 11: return launch_pass<K, V, 256, 16, 8, 3>(ar, mb, cur, tiles_ub, info, n_tiles, digit_base, base_stride, ticket, which);
+    case 12: return launch_pass<K, V, 256, 12, 8, 4>(ar, mb, cur, tiles_ub, info, n_tiles, digit_base, base_stride, ticket, which);
+    case 13: return launch_pass<K, V, 512, 8, 8, 2>(ar, mb, cur, tiles_ub, info, n_tiles, digit_base, base_stride, ticket, which);
+    case 14: return launch_pass<K, V, 512, 12, 8, 2>(ar, mb, cur, tiles_ub, info, n_tiles, digit_base, base_stride, ticket, which);
     default:
       // narrow keys: 56 registers and 68 KB of shared memory per CTA -> three CTAs (36 warps) per SM
       // instead of two; the pass is latency-bound, not HBM-bound (profiles/r01g), so occupancy pays
       if (sizeof(K) == 4)
-        return launch_pass<K, V, 384, 12, 8, 3>(ar, mb, cur, tiles_ub, tile_prefix, digit_base, base_stride, ticket, which);
-      return launch_pass<K, V, 384, 12, 8>(ar, mb, cur, tiles_ub, tile_prefix, digit_base, base_stride, ticket, which);
+        return launch_pass<K, V, 384, 12, 8, 3>(ar, mb, cur, tiles_ub, info, n_tiles, digit_base, base_stride, ticket, which);
+      return launch_pass<K, V, 384, 12, 8>(ar, mb, cur, tiles_ub, info, n_tiles, digit_base, base_stride, ticket, which);
   }
 }
 
@@ -739,12 +764,14 @@ int merge_large(QxArena* ar, MergeBuffers<V>& mb, double eps, int cls_reduce, bo
   static const int red_variant = getenv("QX_REDUCE_VARIANT") ? atoi(getenv("QX_REDUCE_VARIANT")) : 0;
   const int red_tile = sizeof(V) > 8 ? 2048 : (red_variant == 1 ? 1024 : red_variant == 2 ? 2048 : red_variant == 3 ? 4096 : 2048);
   const int64_t red_tiles = std::max<int64_t>(1, (mb.ub_total + red_tile - 1) / red_tile);
-  // scratch layout: ticket | tile_prefix | hist | reduce look-back
+  // scratch layout: ticket | tile_prefix | hist | reduce look-back | tile records
   const int64_t off_prefix = 256;
   const int64_t off_hist = align_up(off_prefix + 8 * ((int64_t)n_seg + 1), 256);
   const int64_t hist_bytes = 4ll * n_seg * passes * QX_RADIX;
   const int64_t off_red = align_up(off_hist + hist_bytes, 256);
-  const int64_t total_bytes = off_red + 8 * (red_tiles + 1);
+  const int64_t off_info = align_up(off_red + 8 * (red_tiles + 1), 256);
+  const int64_t zero_bytes = off_info;                       // the tile records are written, not cleared
+  const int64_t total_bytes = off_info + (int64_t)sizeof(TileInfo) * tiles_ub;
   QX_TRY(qx_arena_scratch(ar, total_bytes));
   QX_TRY(qx_arena_status(ar, tiles_ub * QX_RADIX));
   char* base = reinterpret_cast<char*>(ar->scratch);
@@ -752,17 +779,21 @@ int merge_large(QxArena* ar, MergeBuffers<V>& mb, double eps, int cls_reduce, bo
   int64_t* tile_prefix = reinterpret_cast<int64_t*>(base + off_prefix);
   u32* hist = reinterpret_cast<u32*>(base + off_hist);
   u64* red_status = reinterpret_cast<u64*>(base + off_red);
-  QX_CUDA(cudaMemsetAsync(base, 0, (size_t)total_bytes, ar->stream));
+  TileInfo* info = reinterpret_cast<TileInfo*>(base + off_info);
+  const int64_t* n_tiles = tile_prefix + n_seg;
+  QX_CUDA(cudaMemsetAsync(base, 0, (size_t)zero_bytes, ar->stream));
 
   int cur = mb.cur;
   k_sort_plan<<<1, 32, 0, ar->stream>>>(mb.seg[cur], n_seg, tile_prefix, ticket, tile_terms);
-  qx_count_launches(1);
+  k_sort_tilemap<<<(unsigned)std::max<int64_t>(1, std::min<int64_t>((tiles_ub + 255) / 256, 4096)), 256, 0, ar->stream>>>(
+      mb.seg[cur], n_seg, tile_prefix, info, tile_terms);
+  qx_count_launches(2);
   QX_CUDA(cudaGetLastError());
   {
     const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(tiles_ub, (int64_t)ar->sm_count * 4));
     QxProfileScope prof(QX_K_SORT_HIST, ar->stream, (double)sizeof(K) * (double)mb.ub_total);
-    k_sort_hist<K><<<grid, kSortThreads, 0, ar->stream>>>(reinterpret_cast<const K*>(mb.keys[cur]), mb.seg[cur],
-                                                          n_seg, tile_prefix, hist, passes, tile_terms);
+    k_sort_hist<K><<<grid, kSortThreads, 0, ar->stream>>>(reinterpret_cast<const K*>(mb.keys[cur]), info, n_tiles,
+                                                          hist, passes);
     QX_CUDA(cudaGetLastError());
   }
   k_sort_scan_hist<<<n_seg * passes, QX_RADIX, 0, ar->stream>>>(hist);
@@ -775,7 +806,7 @@ int merge_large(QxArena* ar, MergeBuffers<V>& mb, double eps, int cls_reduce, bo
     QX_CUDA(cudaMemsetAsync(ar->status, 0, sizeof(u32) * (size_t)(tiles_ub * QX_RADIX), ar->stream));
     QX_CUDA(cudaMemsetAsync(ticket, 0, sizeof(u32), ar->stream));
     QxProfileScope prof(QX_K_SORT_PASS, ar->stream, 2.0 * (sizeof(K) + sizeof(V)) * (double)mb.ub_total);
-    QX_TRY((dispatch_pass<K, V>(variant, ar, mb, cur, tiles_ub, tile_prefix, hist + (size_t)p * QX_RADIX,
+    QX_TRY((dispatch_pass<K, V>(variant, ar, mb, cur, tiles_ub, info, n_tiles, hist + (size_t)p * QX_RADIX,
                                 passes * QX_RADIX, ticket, p)));
     cur ^= 1;
   }
