@@ -189,7 +189,9 @@ typedef enum {
   QX_K_READOUT_PRODUCT = 8,
   QX_K_READOUT_REDUCE = 9,
   QX_K_PARTITION = 10,
-  QX_K_CLASSES = 11
+  QX_K_DENSE_PREP = 11,  /* grouped operator step: class words, source sort, group scan */
+  QX_K_DENSE_EMIT = 12,  /* grouped operator step: one thread per output slot */
+  QX_K_CLASSES = 13
 } qx_kernel_class;
 int qx_profile_enable(int on);
 int qx_profile_reset(void);

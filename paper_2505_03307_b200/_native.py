@@ -24,6 +24,7 @@ QX_OK, QX_ERR_INVALID, QX_ERR_RESOURCE, QX_ERR_CUDA, QX_ERR_UNSUPPORTED, QX_ERR_
 KERNEL_CLASSES = (
     "clifford", "split", "expand_count", "expand_emit", "sort_hist", "sort_pass",
     "reduce", "small_merge", "readout_product", "readout_reduce", "partition",
+    "dense_prep", "dense_emit",
 )
 
 _i32, _i64, _u32, _u64, _f64 = C.c_int32, C.c_int64, C.c_uint32, C.c_uint64, C.c_double

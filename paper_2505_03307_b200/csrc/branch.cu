@@ -23,7 +23,9 @@
 
 #include <algorithm>
 
-#include "qx_device.cuh"
+#include "expand.cuh"
+
+using namespace qxe;
 
 namespace {
 
@@ -109,22 +111,7 @@ k_split(const u64* __restrict__ keys_in, const double* __restrict__ lam_in,
 // ---------------------------------------------------------------------------------
 // v2/v3 operator
 // ---------------------------------------------------------------------------------
-// Indexed by digit position p = n-1-qubit (p = 0 is the least significant digit).
-struct OperatorTable {
-  double w[QX_MAX_QUBITS][3][3];
-  unsigned char axis[QX_MAX_QUBITS][3][3];
-  unsigned char cnt[QX_MAX_QUBITS][3];
-};
-
-__device__ __forceinline__ u64 branch_count(u64 key, const unsigned char (*cnt)[3]) {
-  u64 m = support_mask(key), c = 1;
-  while (m) {
-    const int b = __ffsll((long long)m) - 1;
-    m &= m - 1;
-    c *= cnt[b >> 1][((key >> b) & 3ull) - 1];
-  }
-  return c;
-}
+// OperatorTable, ImageTable, LowGroup and the decode helpers live in expand.cuh (shared with dense.cu)
 
 // roff[i] = raw terms produced by input terms before i (roff[total] = raw total).
 __global__ void __launch_bounds__(kThreads)
@@ -176,123 +163,7 @@ __global__ void k_gather_offsets(const int64_t* __restrict__ seg_in, int n_seg,
   if (g <= n_seg) seg_out[g] = (int64_t)roff[seg_in[g]];
 }
 
-// index of the last entry <= r in a strictly increasing array a[0..n)
-__device__ __forceinline__ int64_t last_le(const u64* a, int64_t n, u64 r) {
-  int64_t lo = 0, hi = n;                  // a[lo] <= r < a[hi] (a[n] = +inf)
-  while (hi - lo > 1) {
-    const int64_t mid = (lo + hi) >> 1;
-    if (a[mid] <= r) lo = mid; else hi = mid;
-  }
-  return lo;
-}
 
-// ---- working-key width ------------------------------------------------------------------
-// For n <= 16 a word fits 32 bits and a term has at most 3^16 < 2^32 branches, so the whole
-// enumeration runs on 32-bit registers (these kernels are ALU-bound: half the instructions).
-template <typename K> struct KeyOps;
-template <> struct KeyOps<u32> {
-  static __device__ __forceinline__ int lowest(u32 m) { return __ffs((int)m) - 1; }
-  static __device__ __forceinline__ int highest(u32 m) { return 31 - __clz((int)m); }
-  static __device__ __forceinline__ u32 support(u32 k) { return (k | (k >> 1)) & 0x55555555u; }
-};
-template <> struct KeyOps<u64> {
-  static __device__ __forceinline__ int lowest(u64 m) { return __ffsll((long long)m) - 1; }
-  static __device__ __forceinline__ int highest(u64 m) { return 63 - __clzll((long long)m); }
-  static __device__ __forceinline__ u64 support(u64 k) { return support_mask(k); }
-};
-
-// ---- Clifford run folded into the expansion ---------------------------------------------------
-// In v2/v3 every U_k is followed by a run of sign-permutation ops (the CX group V_k, Clifford
-// blocks of later U's).  Conjugation by the run is a group homomorphism on Pauli operators, so the
-// image of a raw term is the ordered product of the images of its single-digit factors: the host
-// pushes the 3n single-digit words through the run once (ImageTable) and the expansion kernel
-// composes images instead of OR-ing digits -- the raw terms leave the kernel already conjugated
-// and the separate read+write pass of the Clifford kernel disappears.
-// Bookkeeping in "XZ form": a Hermitian word with sign s is i^e X^x Z^z with e = #Y + 2s, and
-//   (i^ea X^xa Z^za)(i^eb X^xb Z^zb) = i^(ea + eb + 2|za & xb|) X^(xa^xb) Z^(za^zb);
-// on the packed base-4 code (hi = z, lo = x ^ z) the word part is one XOR, the exponent one
-// popcount.  Factors of one term act on different qubits, so they commute and the final
-// exponent minus #Y of the final word is 0 or 2: the sign, applied to lambda exactly.
-template <typename K>
-struct ImageTable {
-  K img[QX_MAX_QUBITS][3];             // image word of axis a+1 at digit position p
-  K imx[QX_MAX_QUBITS][3];             // its x plane ((w ^ w >> 1) & 0x55..), precomputed
-  unsigned char e[QX_MAX_QUBITS][3];   // (#Y of the image + 2 * sign) mod 4
-};
-
-template <typename K> struct Plane;
-template <> struct Plane<u32> {
-  static constexpr u32 lo = 0x55555555u;
-  static __device__ __forceinline__ u32 popc(u32 v) { return (u32)__popc(v); }
-};
-template <> struct Plane<u64> {
-  static constexpr u64 lo = 0x5555555555555555ull;
-  static __device__ __forceinline__ u32 popc(u64 v) { return (u32)__popcll(v); }
-};
-
-template <typename K>
-__device__ __forceinline__ void compose(K& word, u32& e, K img, K imx, u32 ie) {
-  e += ie + 2u * Plane<K>::popc((word >> 1) & imx);
-  word ^= img;
-}
-// 1 iff the composed operator is MINUS the Hermitian word
-template <typename K>
-__device__ __forceinline__ u32 composed_sign(K word, u32 e) {
-  const u32 ny = Plane<K>::popc((word >> 1) & ~word & Plane<K>::lo);
-  return ((e - ny) >> 1) & 1u;
-}
-
-// ---- two-level branch decode --------------------------------------------------------------
-// A source term with non-identity digits d_0 < d_1 < ... (least significant first) and radices
-// c_i expands into prod c_i raw terms, branch id b = mixed-radix number with d_0 fastest.
-// Split the digits into a LOW group (d_0, d_1, d_2: L = c0*c1*c2 <= 27 branches) and the HIGH
-// rest.  All L branches of one "block" h = b / L share the high digits, i.e. the partial
-// product p_hi = lambda * w(top) * ... * w(d_3) and the partial word k_hi.  Per output tile:
-//   1. every source that feeds the tile counts the blocks it touches (prefix sum in smem);
-//   2. one thread per BLOCK decodes h and folds the high digits once into (p_hi, k_hi) in smem
-//      -- the only loops over digits, amortised over up to 27 outputs;
-//   3. one thread per OUTPUT (consecutive lanes = consecutive raw terms, so stores are fully
-//      coalesced) splits b into (h, three low picks), reads its block's (p_hi, k_hi) and does
-//      three multiplies, in the reference's order: ((p_hi * w2) * w1) * w0 with qubit 0 first.
-// Control flow in step 3 is uniform across the warp: no loops, no data-dependent branches.
-template <typename K>
-struct LowGroup {
-  int bit[3];      // digit positions (bit offsets), -1 if absent
-  u32 rad[3];      // radices (1 if absent)
-  u32 dig[3];      // input axis - 1 at those positions
-  K hi_mask;       // support bits above the group
-  u32 L;           // rad[0] * rad[1] * rad[2]
-};
-
-template <typename K>
-__device__ __forceinline__ LowGroup<K> low_group(K key, const OperatorTable& tb) {
-  LowGroup<K> g;
-  K m = KeyOps<K>::support(key);
-#pragma unroll
-  for (int j = 0; j < 3; ++j) {
-    g.bit[j] = -1;
-    g.rad[j] = 1;
-    g.dig[j] = 0;
-    if (m) {
-      const int bit = KeyOps<K>::lowest(m);
-      m &= m - 1;
-      g.bit[j] = bit;
-      g.dig[j] = (u32)((key >> bit) & 3u) - 1u;
-      g.rad[j] = tb.cnt[bit >> 1][g.dig[j]];
-    }
-  }
-  g.hi_mask = m;
-  g.L = g.rad[0] * g.rad[1] * g.rad[2];
-  return g;
-}
-
-// q = b / c, r = b % c for c in {1, 2, 3} without a divide
-template <typename K>
-__device__ __forceinline__ void divmod_small(K b, u32 c, K& q, u32& r) {
-  if (c == 1) { q = b; r = 0; }
-  else if (c == 2) { q = b >> 1; r = (u32)(b & 1u); }
-  else { q = b / 3u; r = (u32)(b - 3u * q); }
-}
 
 constexpr int kEmitPer = 8;                          // outputs per thread, striped
 constexpr int kEmitTile = kThreads * kEmitPer;       // 2048 raw terms per tile
@@ -718,6 +589,25 @@ void fill_images(int n_qubits, const uint32_t* program, int n_ops, u32 cx_c, u32
     }
 }
 
+}  // namespace
+
+namespace qxe {
+void fill_images_u32(int n_qubits, const uint32_t* program, int n_ops, u32 cx_c, u32 cx_t, u32 cx_s,
+                     ImageTable<u32>* im) {
+  fill_images<u32>(n_qubits, program, n_ops, cx_c, cx_t, cx_s, im);
+}
+void fill_images_u64(int n_qubits, const uint32_t* program, int n_ops, u32 cx_c, u32 cx_t, u32 cx_s,
+                     ImageTable<u64>* im) {
+  fill_images<u64>(n_qubits, program, n_ops, cx_c, cx_t, cx_s, im);
+}
+}  // namespace qxe
+
+// dense.cu: the grouped dense operator step
+int qx_dense_operator_step(qx_store* s, const OperatorTable& nz, const uint32_t* program, int n_ops,
+                           u32 cx_c, u32 cx_t, u32 cx_s, double eps, int64_t* slots_total);
+
+namespace {
+
 template <typename K, typename KO, bool FUSED>
 int launch_emit(qx_store* s, const OperatorTable& tb, const ImageTable<K>& im, const u64* roff,
                 int64_t total_in, int64_t raw, int in, int out) {
@@ -738,8 +628,12 @@ int launch_emit(qx_store* s, const OperatorTable& tb, const ImageTable<K>& im, c
 // U_k (+ an optional Clifford run folded in).  narrow_ok: the caller merges right away with the
 // large path, so for 2n <= 32 the raw keys may be written as 32-bit words; *narrow says whether
 // they were.
+// dense_eps > 0: the caller merges right away with this drop threshold, so an operator with a
+// large fan-out may take the grouped dense path (dense.cu), which leaves the store canonical;
+// *went_dense says whether it did.
 int expand(qx_store* s, const OperatorTable& tb, const uint32_t* program, int n_ops, u32 cx_c,
-           u32 cx_t, u32 cx_s, bool narrow_ok, int64_t term_limit, int64_t* raw_total, bool* narrow) {
+           u32 cx_t, u32 cx_s, bool narrow_ok, int64_t term_limit, int64_t* raw_total, bool* narrow,
+           double dense_eps = -1.0, bool* went_dense = nullptr) {
   QX_CUDA(cudaSetDevice(s->device));
   u64* roff;
   QX_TRY(count_pass(s, tb, &roff));
@@ -756,6 +650,16 @@ int expand(qx_store* s, const OperatorTable& tb, const uint32_t* program, int n_
   if (term_limit > 0 && raw > term_limit)
     return qx_fail(QX_ERR_RESOURCE, "operator would expand %lld terms into %lld raw terms (limit %lld)",
                    (long long)total_in, (long long)raw, (long long)term_limit);
+  int64_t ub_seg = 0;
+  for (int g = 0; g < s->n_seg; ++g) ub_seg = std::max(ub_seg, s->h_pinned[g + 1] - s->h_pinned[g]);
+  if (went_dense) *went_dense = false;
+  static const bool no_dense = getenv("QX_NO_DENSE") != nullptr;
+  static const int64_t dense_fanout = getenv("QX_DENSE_FANOUT") ? atoll(getenv("QX_DENSE_FANOUT")) : 16;
+  if (dense_eps > 0.0 && !no_dense && ub_seg > QX_SMALL_MAX && raw >= dense_fanout * total_in) {
+    QX_TRY(qx_dense_operator_step(s, tb, program, n_ops, cx_c, cx_t, cx_s, dense_eps, nullptr));
+    if (went_dense) *went_dense = true;
+    return QX_OK;
+  }
   if (raw > s->cap) {
     // growing moves the live terms; the count array (scratch) and the gathered offsets stay valid
     std::vector<int64_t> raw_off(s->h_pinned, s->h_pinned + s->n_seg + 1);
@@ -764,8 +668,6 @@ int expand(qx_store* s, const OperatorTable& tb, const uint32_t* program, int n_
                             cudaMemcpyHostToDevice, s->stream));
     QX_CUDA(cudaStreamSynchronize(s->stream));
   }
-  int64_t ub_seg = 0;
-  for (int g = 0; g < s->n_seg; ++g) ub_seg = std::max(ub_seg, s->h_pinned[g + 1] - s->h_pinned[g]);
   const bool small_keys = s->n_qubits <= 16;
   const bool go_narrow = narrow_ok && small_keys && ub_seg > QX_SMALL_MAX;
   if (narrow) *narrow = go_narrow;
@@ -829,9 +731,9 @@ extern "C" int qx_apply_operator_run(qx_store* s, const int32_t* counts, const i
     return qx_merge(s, eps, ranks);
   }
   static const bool no_narrow = getenv("QX_NO_NARROW") != nullptr;
-  bool narrow = false;
-  QX_TRY(expand(s, tb, program, n_ops, cx_c, cx_t, cx_s, !no_narrow, term_limit, raw_total, &narrow));
-  QX_TRY(qx_run_merge(s, eps, false, narrow));
+  bool narrow = false, dense = false;
+  QX_TRY(expand(s, tb, program, n_ops, cx_c, cx_t, cx_s, !no_narrow, term_limit, raw_total, &narrow, eps, &dense));
+  if (!dense) QX_TRY(qx_run_merge(s, eps, false, narrow));
   if (ranks)
     for (int g = 0; g < s->n_seg; ++g) ranks[g] = s->h_seg[g + 1] - s->h_seg[g];
   return QX_OK;

@@ -1,0 +1,756 @@
+// a4 + a5 + a2 + a6 for operators with a large fan-out: grouped dense accumulation.
+//
+// The reference expands every term of a generator into its Cartesian product of branches
+// (stabilizer.py:289-322 _flatten_ragged), then canonicalize sorts the raw list and sums
+// duplicates (stabilizer.py:325-337).  Which raw terms can collide is known before anything is
+// expanded: a single-qubit block maps input axis a to the set A(a) of output axes with non-zero
+// weight; two input axes can meet on an output axis only if they are in the same connected
+// component ("class") of that relation, and a class C writes into O(C) = union of A(a), a in C.
+// Replace every non-identity digit of a term by its class id: terms of one generator with
+// different class words never produce the same output word, terms with the same class word
+// ("group") all write into the same dense box of prod_j |O(C_j)| output words ("slots").
+//
+// So instead of expand -> sort raw -> reduce, the large path is
+//   1. class word per source term, stable segmented sort of the sources by class word;
+//   2. one scan over the sorted sources: groups, their slot offsets, per-generator slot counts;
+//   3. one thread per SLOT: sum over the sources of its group of lambda * prod_j w_j, factors taken
+//      qubit 0 first like the reference (stabilizer.py:311-319), sources in input order; drop rule
+//      |sum| >= eps (stabilizer.py:336); ordered compaction (ballot prefix + decoupled look-back);
+//      the Clifford run that follows the operator is folded in as an image composition
+//      (expand.cuh), so the kept terms leave the kernel conjugated, as 32-bit keys when 2n <= 32;
+//   4. sort only (merge.cuh, do_reduce = false): slots are distinct words and the run is a
+//      bijection, so nothing is left to sum or drop.
+// The raw list is never written: HBM holds slots, not branches.  xyz_chain(10,3): 1.3e9 raw terms
+// -> 3.3e6 slots; xyz_chain(16,2): every group has one source, slots = raw = 1.72e8, 27 % of
+// them are dropped before the sort instead of after it, and the reduce pass disappears.
+//
+// A slot that no source reaches with a non-zero weight (a class whose relation is not complete)
+// sums to exactly 0 and is dropped by eps > 0; with eps == 0 the caller takes the raw path.
+#include <stdlib.h>
+#include <string.h>
+
+#include <algorithm>
+
+#include "expand.cuh"
+#include "merge.cuh"
+
+using namespace qxe;
+
+namespace {
+
+constexpr int kThreads = 256;
+constexpr int kWarps = kThreads / 32;
+constexpr int kPer = 8;
+constexpr int kTileSlots = kThreads * kPer;      // 2048 slots (or sources) per tile
+constexpr int kChunk = 16;                       // sources accumulated per round of the one-group path
+constexpr int kPhiCap = 4096;                    // partial products held per round
+
+// class id (1..3, the smallest input axis of the class) of input axis a+1 at digit position p
+struct ClassIds {
+  unsigned char cls[QX_MAX_QUBITS][3];
+};
+
+template <typename K>
+__device__ __forceinline__ K class_word(K key, const unsigned char (*cls)[3]) {
+  K m = KeyOps<K>::support(key), c = 0;
+  while (m) {
+    const int b = KeyOps<K>::lowest(m);
+    m &= m - 1;
+    c |= (K)cls[b >> 1][((u32)(key >> b) & 3u) - 1u] << b;
+  }
+  return c;
+}
+
+// ---- 1. class words ------------------------------------------------------------------------
+__global__ void __launch_bounds__(kThreads)
+k_class_words(const u64* __restrict__ keys, int64_t n, u64* __restrict__ cw, double* __restrict__ idx,
+              const __grid_constant__ ClassIds ids) {
+  __shared__ unsigned char s_cls[QX_MAX_QUBITS][3];
+  for (int i = threadIdx.x; i < QX_MAX_QUBITS * 3; i += kThreads) s_cls[i / 3][i % 3] = ids.cls[i / 3][i % 3];
+  __syncthreads();
+  for (int64_t i = (int64_t)blockIdx.x * kThreads + threadIdx.x; i < n; i += (int64_t)gridDim.x * kThreads) {
+    cw[i] = class_word<u64>(keys[i], s_cls);
+    idx[i] = __longlong_as_double(i);          // payload of the sort: moved, never computed with
+  }
+}
+
+// ---- 2. groups -----------------------------------------------------------------------------
+__device__ __forceinline__ u64 slots_of(u64 cw, const unsigned char (*cnt)[3]) {
+  u64 m = support_mask(cw), c = 1;
+  while (m) {
+    const int b = __ffsll((long long)m) - 1;
+    m &= m - 1;
+    c *= cnt[b >> 1][((cw >> b) & 3ull) - 1];
+  }
+  return c;
+}
+
+// One pass over the sources in (generator, class word) order.  A source is a group head if it
+// opens a generator or its class word differs from its predecessor's.  Two exclusive scans
+// (heads, slots of heads) give every group its index and its first slot.  Also gathers the
+// source terms into sorted order so that the slot kernel reads them without indirection.
+//   gsrc[g]  = first sorted source of group g        (gsrc[NG] = n)
+//   gslot[g] = first slot of group g                 (gslot[NG] = total slots)
+//   seg_slot = slot offsets of the generators        (n_seg + 1)
+__global__ void __launch_bounds__(kThreads)
+k_group_scan(const u64* __restrict__ cw, const double* __restrict__ idx, const u64* __restrict__ keys_in,
+             const double* __restrict__ lam_in, const int64_t* __restrict__ seg, int n_seg, int64_t n,
+             u64* __restrict__ skey, double* __restrict__ slam, u64* __restrict__ gsrc,
+             u64* __restrict__ gslot, int64_t* __restrict__ seg_slot, u64* __restrict__ totals,
+             u64* status_heads, u64* status_slots, u32* ticket, const __grid_constant__ OperatorTable tb) {
+  __shared__ int s_tile;
+  __shared__ u64 s_scan[kWarps + 1];
+  __shared__ u64 s_base[2];
+  __shared__ unsigned char s_cnt[QX_MAX_QUBITS][3];
+  for (int i = threadIdx.x; i < QX_MAX_QUBITS * 3; i += kThreads) s_cnt[i / 3][i % 3] = tb.cnt[i / 3][i % 3];
+  const int tile = take_ticket(ticket, &s_tile);
+  const int64_t ntiles = n > 0 ? (n + kTileSlots - 1) / kTileSlots : 1;
+  if (tile >= ntiles) return;
+  const int warp = threadIdx.x >> 5, lane = lane_id();
+  const int64_t wbase = (int64_t)tile * kTileSlots + (int64_t)warp * (32 * kPer);
+  u64 pre_h[kPer], pre_s[kPer];
+  u32 flags = 0;                 // bit k: head, bit 8+k: opens a generator
+  u64 run_h = 0, run_s = 0;
+#pragma unroll
+  for (int k = 0; k < kPer; ++k) {
+    const int64_t i = wbase + k * 32 + lane;
+    u64 r = 0;
+    bool head = false;
+    if (i < n) {
+      const u64 c = cw[i];
+      const int g = segment_of(seg, n_seg, i);
+      const bool opens = seg[g] == i;
+      head = opens || cw[i - 1] != c;
+      if (opens) flags |= 1u << (8 + k);
+      if (head) {
+        flags |= 1u << k;
+        r = slots_of(c, s_cnt);
+      }
+      const int64_t j = __double_as_longlong(idx[i]);
+      skey[i] = keys_in[j];
+      slam[i] = lam_in[j];
+    }
+    const u32 votes = __ballot_sync(QX_FULL_MASK, head);
+    pre_h[k] = run_h + __popc(votes & lanemask_lt());
+    run_h += __popc(votes);
+    const u64 inc = warp_inclusive_sum(r);
+    pre_s[k] = run_s + inc - r;
+    run_s += __shfl_sync(QX_FULL_MASK, inc, 31);
+  }
+  u64 tot_h, tot_s;
+  u64 wex_h = block_exclusive_sum<u64>(lane == 0 ? run_h : 0ull, s_scan, tot_h);
+  wex_h = __shfl_sync(QX_FULL_MASK, wex_h, 0);
+  u64 wex_s = block_exclusive_sum<u64>(lane == 0 ? run_s : 0ull, s_scan, tot_s);
+  wex_s = __shfl_sync(QX_FULL_MASK, wex_s, 0);
+  if (warp == 0) {
+    const u64 eh = lookback_exclusive(status_heads, tile, tot_h);
+    const u64 es = lookback_exclusive(status_slots, tile, tot_s);
+    if (lane == 0) {
+      s_base[0] = eh;
+      s_base[1] = es;
+    }
+  }
+  __syncthreads();
+  const u64 base_h = s_base[0] + wex_h, base_s = s_base[1] + wex_s;
+#pragma unroll
+  for (int k = 0; k < kPer; ++k) {
+    const int64_t i = wbase + k * 32 + lane;
+    if (flags & (1u << k)) {
+      gsrc[base_h + pre_h[k]] = (u64)i;
+      gslot[base_h + pre_h[k]] = base_s + pre_s[k];
+    }
+    if (flags & (1u << (8 + k)))
+      open_offsets(seg, seg_slot, segment_of(seg, n_seg, i), i, (int64_t)(base_s + pre_s[k]));
+  }
+  if (tile == ntiles - 1 && threadIdx.x == 0) {
+    const u64 ng = s_base[0] + tot_h, total = s_base[1] + tot_s;
+    gsrc[ng] = (u64)n;
+    gslot[ng] = total;
+    totals[0] = ng;
+    totals[1] = total;
+    close_offsets(seg, seg_slot, n_seg, n, (int64_t)total);
+  }
+}
+// group and generator of the first slot of every slot tile
+__global__ void k_tile_groups(const u64* __restrict__ gslot, const u64* __restrict__ totals,
+                              const int64_t* __restrict__ seg_slot, int n_seg,
+                              int2* __restrict__ tile_info, int64_t ntiles) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t < ntiles) {
+    const u64 r0 = (u64)t * kTileSlots;
+    tile_info[t] = make_int2((int)last_le(gslot, (int64_t)totals[0], r0), segment_of(seg_slot, n_seg, (int64_t)r0));
+  }
+}
+
+// kept counts -> compact offsets (n_seg is small: one thread)
+__global__ void k_counts_to_offsets(const u64* __restrict__ seg_count, int n_seg, int64_t* __restrict__ seg_out) {
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    int64_t run = 0;
+    for (int g = 0; g < n_seg; ++g) {
+      seg_out[g] = run;
+      run += (int64_t)seg_count[g];
+    }
+    seg_out[n_seg] = run;
+  }
+}
+
+// ---- 3. one thread per slot ----------------------------------------------------------------
+constexpr int kMaxBlocks = 512;      // blocks of one tile in the one-group path (needs L >= 4 ...)
+
+template <typename K>
+struct GroupSmem {
+  OperatorTable tb;                  // class-expanded: cnt/axis describe the class, w may hold zeros
+  ImageTable<K> im;
+  K k_hi[kMaxBlocks];                // per block of the tile: output word of the high digits
+  K choice[kMaxBlocks];              //   their picks, two bits per digit position
+  unsigned char e_hi[kMaxBlocks];
+  double p_hi[kPhiCap];              // [source of the round][block]: lambda * high weights
+  double low_w[kChunk][27][3];       // [source of the round][low branch][low digit]
+  K low_word[27];
+  K low_imx[27];
+  u32 low_e[27];
+  u32 low_pick[27];
+  u64 scan[kWarps + 1];
+  u64 base;
+};
+
+// K = working word type (u32 for n <= 16), KO = type of the keys written, FUSED = compose the
+// images of the Clifford run that follows (im) instead of placing the output digits.
+// Persistent CTAs stride over the slot tiles.  Kept terms of generator g go to
+// [seg_slot[g], seg_slot[g] + kept_g) of the output: space is handed out with one atomic per tile
+// (order inside a generator is irrelevant, the sort follows; a tile-ordered compaction would
+// chain every tile to its predecessor's FINISHED sums -- 34 % of the stall samples of the first
+// version of this kernel, profiles/r01h).
+template <typename K, typename KO, bool FUSED>
+__global__ void __launch_bounds__(kThreads, 3)
+k_group_emit(const u64* __restrict__ cw, const u64* __restrict__ skey, const double* __restrict__ slam,
+             const u64* __restrict__ gsrc, const u64* __restrict__ gslot, const u64* __restrict__ totals,
+             const int2* __restrict__ tile_info, const int64_t* __restrict__ seg_slot, int n_seg,
+             KO* __restrict__ keys_out, double* __restrict__ lam_out, u64* __restrict__ seg_count,
+             double eps, const __grid_constant__ OperatorTable tb,
+             const __grid_constant__ ImageTable<K> im) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  GroupSmem<K>& sm = *reinterpret_cast<GroupSmem<K>*>(smem_raw);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = lane_id();
+  {
+    const u32* src = reinterpret_cast<const u32*>(&tb);
+    u32* dst = reinterpret_cast<u32*>(&sm.tb);
+    for (int i = tid; i < (int)(sizeof(OperatorTable) / 4); i += kThreads) dst[i] = src[i];
+    if (FUSED) {
+      const u32* isrc = reinterpret_cast<const u32*>(&im);
+      u32* idst = reinterpret_cast<u32*>(&sm.im);
+      for (int i = tid; i < (int)(sizeof(ImageTable<K>) / 4); i += kThreads) idst[i] = isrc[i];
+    }
+  }
+  const int64_t ngroups = (int64_t)totals[0];
+  const u64 total = totals[1];
+  const int64_t ntiles = (int64_t)((total + kTileSlots - 1) / kTileSlots);
+  int cached_group = -1;              // group whose low table is in shared memory
+  LowGroup<K> lg = {};
+  K cwg = 0;
+  u32 magic = 0;
+
+  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const u64 r0 = (u64)tile * kTileSlots;
+    const u64 r1 = min(r0 + (u64)kTileSlots, total);
+    const u32 n_out = (u32)(r1 - r0);
+    const int2 ti = tile_info[tile];
+    const int g0 = ti.x, seg0 = ti.y;
+    const u64 gs0 = gslot[g0];
+    const bool one_seg = (u64)seg_slot[seg0 + 1] >= r1;
+
+    double acc[kPer];
+    K word[kPer];
+    u32 neg = 0;                                  // bit k: the composed word carries a minus sign
+#pragma unroll
+    for (int k = 0; k < kPer; ++k) {
+      acc[k] = 0.0;
+      word[k] = 0;
+    }
+    __syncthreads();                              // previous tile fully consumed (and tables copied)
+
+    bool single = gslot[g0 + 1] >= r1;
+    int n_blocks = 0;
+    u64 h0 = 0;
+    u32 bl0 = 0;
+    if (single) {
+      if (cached_group != g0) {
+        cwg = (K)cw[gsrc[g0]];
+        lg = low_group<K>(cwg, sm.tb);
+        magic = 65536u / lg.L + 1u;               // t / L == (t * magic) >> 16 for t < 2^16 / L
+      }
+      const u64 b0 = r0 - gs0;
+      h0 = b0 / lg.L;
+      bl0 = (u32)(b0 - h0 * lg.L);
+      n_blocks = (int)((bl0 + n_out - 1u) / lg.L + 1u);
+      if (n_blocks > kMaxBlocks) {                // tiny low group: take the per-slot path
+        single = false;
+        cached_group = -1;
+      }
+    }
+    if (single) {
+      // ---- the whole tile lies in one group: two-level decode shared by all its sources.  The
+      // digits split into a LOW group (three least significant, L <= 27 branches) and the HIGH
+      // rest; a "block" is the L consecutive slots that share the high picks.
+      const int64_t s0 = (int64_t)gsrc[g0];
+      const int n_src = (int)((int64_t)gsrc[g0 + 1] - s0);
+      if (cached_group != g0 && tid < (int)lg.L) {
+        u32 b = tid, picks = 0;
+        K w = 0;
+        u32 ex = 0;
+        u32 pick[3];
+#pragma unroll
+        for (int j = 0; j < 3; ++j) {
+          pick[j] = b % lg.rad[j];
+          b /= lg.rad[j];
+          picks |= pick[j] << (2 * j);
+        }
+#pragma unroll
+        for (int j = 2; j >= 0; --j) {
+          if (lg.bit[j] >= 0) {
+            const int p = lg.bit[j] >> 1;
+            const u32 ax = sm.tb.axis[p][lg.dig[j]][pick[j]];
+            if (FUSED) compose<K>(w, ex, sm.im.img[p][ax - 1], sm.im.imx[p][ax - 1], sm.im.e[p][ax - 1]);
+            else w |= (K)ax << lg.bit[j];
+          }
+        }
+        sm.low_word[tid] = w;
+        sm.low_imx[tid] = (w ^ (w >> 1)) & Plane<K>::lo;
+        sm.low_e[tid] = ex & 3u;
+        sm.low_pick[tid] = picks;
+      }
+      cached_group = g0;
+      // high digits of every block: picks, output word; with one source also its partial product
+      const K key0 = (K)skey[s0];
+      const double lam0 = slam[s0];
+      for (int e = tid; e < n_blocks; e += kThreads) {
+        K h = (K)(h0 + (u64)e);
+        K ch = 0;
+        for (K m = lg.hi_mask; m;) {
+          const int bit = KeyOps<K>::lowest(m);
+          m &= m - 1;
+          u32 pick;
+          divmod_small<K>(h, sm.tb.cnt[bit >> 1][(u32)((cwg >> bit) & 3u) - 1u], h, pick);
+          ch |= (K)pick << bit;
+        }
+        K out = 0;
+        u32 ex = 0;
+        double v = lam0;
+        for (K m = lg.hi_mask; m;) {               // qubit 0 first (stabilizer.py:311-319)
+          const int bit = KeyOps<K>::highest(m);
+          m ^= (K)1 << bit;
+          const u32 pick = (u32)(ch >> bit) & 3u;
+          const u32 ax = sm.tb.axis[bit >> 1][(u32)((cwg >> bit) & 3u) - 1u][pick];
+          v *= sm.tb.w[bit >> 1][(u32)((key0 >> bit) & 3u) - 1u][pick];
+          if (FUSED) compose<K>(out, ex, sm.im.img[bit >> 1][ax - 1], sm.im.imx[bit >> 1][ax - 1], sm.im.e[bit >> 1][ax - 1]);
+          else out |= (K)ax << bit;
+        }
+        sm.choice[e] = ch;
+        sm.k_hi[e] = out;
+        sm.e_hi[e] = (unsigned char)(ex & 3u);
+        sm.p_hi[e] = v;                            // round 0, source 0
+      }
+      if (n_src > 1) __syncthreads();             // picks visible to the other sources' folds
+      u32 eb[kPer];                               // block << 5 | low branch of my slots
+#pragma unroll
+      for (int k = 0; k < kPer; ++k) {
+        const u32 t = bl0 + (u32)(warp * (32 * kPer) + k * 32 + lane);
+        const u32 e = (t * magic) >> 16;
+        eb[k] = (e << 5) | (t - e * lg.L);
+      }
+      const int per_round = max(1, min(kChunk, kPhiCap / n_blocks));
+      for (int c0 = 0; c0 < n_src; c0 += per_round) {
+        const int nc = min(per_round, n_src - c0);
+        if (c0 > 0) __syncthreads();              // previous round consumed
+        // partial products of the round's sources (source 0 of round 0 was folded above)
+        for (int w = tid + (c0 == 0 ? n_blocks : 0); w < nc * n_blocks; w += kThreads) {
+          const int c = w / n_blocks, e = w - c * n_blocks;
+          const K key = (K)skey[s0 + c0 + c];
+          const K ch = sm.choice[e];
+          double v = slam[s0 + c0 + c];
+          for (K m = lg.hi_mask; m;) {             // qubit 0 first
+            const int bit = KeyOps<K>::highest(m);
+            m ^= (K)1 << bit;
+            v *= sm.tb.w[bit >> 1][(u32)((key >> bit) & 3u) - 1u][(u32)(ch >> bit) & 3u];
+          }
+          sm.p_hi[c * n_blocks + e] = v;
+        }
+        for (int w = tid; w < nc * (int)lg.L; w += kThreads) {
+          const int c = w / (int)lg.L, l = w - c * (int)lg.L;
+          const K key = (K)skey[s0 + c0 + c];
+          const u32 picks = sm.low_pick[l];
+#pragma unroll
+          for (int j = 0; j < 3; ++j) {
+            double wt = 1.0;
+            if (lg.bit[j] >= 0)
+              wt = sm.tb.w[lg.bit[j] >> 1][(u32)((key >> lg.bit[j]) & 3u) - 1u][(picks >> (2 * j)) & 3u];
+            sm.low_w[c][l][j] = wt;
+          }
+        }
+        __syncthreads();
+#pragma unroll
+        for (int k = 0; k < kPer; ++k) {
+          const u32 idx = (u32)(warp * (32 * kPer) + k * 32 + lane);
+          if (idx < n_out) {
+            const u32 e = eb[k] >> 5, bl = eb[k] & 31u;
+            for (int c = 0; c < nc; ++c) {
+              // ((p_hi * w2) * w1) * w0, absent = 1.0; explicit roundings: a fused multiply-add
+              // of the last product into the sum would round differently from the reference
+              double v = sm.p_hi[c * n_blocks + e];
+              v = __dmul_rn(v, sm.low_w[c][bl][2]);
+              v = __dmul_rn(v, sm.low_w[c][bl][1]);
+              v = __dmul_rn(v, sm.low_w[c][bl][0]);
+              acc[k] = (c0 + c == 0) ? v : __dadd_rn(acc[k], v);
+            }
+          }
+        }
+      }
+#pragma unroll
+      for (int k = 0; k < kPer; ++k) {
+        const u32 idx = (u32)(warp * (32 * kPer) + k * 32 + lane);
+        if (idx < n_out) {
+          const u32 e = eb[k] >> 5, bl = eb[k] & 31u;
+          K out = sm.k_hi[e];
+          if (FUSED) {
+            u32 ex = (u32)sm.e_hi[e];
+            compose<K>(out, ex, sm.low_word[bl], sm.low_imx[bl], sm.low_e[bl]);
+            neg |= composed_sign<K>(out, ex) << k;
+          } else {
+            out |= sm.low_word[bl];
+          }
+          word[k] = out;
+        }
+      }
+    } else {
+      // ---- several (small) groups in the tile: every slot finds its group and walks its sources
+#pragma unroll 1
+      for (int k = 0; k < kPer; ++k) {
+        const u32 idx = (u32)(warp * (32 * kPer) + k * 32 + lane);
+        if (idx >= n_out) continue;
+        const u64 r = r0 + idx;
+        int64_t lo = g0, hi = min(ngroups, (int64_t)g0 + (int64_t)n_out + 1);   // gslot[lo] <= r < gslot[hi]
+        while (hi - lo > 1) {
+          const int64_t mid = (lo + hi) >> 1;
+          if (gslot[mid] <= r) lo = mid; else hi = mid;
+        }
+        const int64_t s0 = (int64_t)gsrc[lo], s1 = (int64_t)gsrc[lo + 1];
+        const K cg = (K)cw[s0];
+        K b = (K)(r - gslot[lo]);
+        K ch = 0;
+        for (K m = KeyOps<K>::support(cg); m;) {
+          const int bit = KeyOps<K>::lowest(m);
+          m &= m - 1;
+          u32 pick;
+          divmod_small<K>(b, sm.tb.cnt[bit >> 1][(u32)((cg >> bit) & 3u) - 1u], b, pick);
+          ch |= (K)pick << bit;
+        }
+        K out = 0;
+        u32 ex = 0;
+        for (K m = KeyOps<K>::support(cg); m;) {
+          const int bit = KeyOps<K>::highest(m);
+          m ^= (K)1 << bit;
+          const u32 ax = sm.tb.axis[bit >> 1][(u32)((cg >> bit) & 3u) - 1u][(u32)(ch >> bit) & 3u];
+          if (FUSED) compose<K>(out, ex, sm.im.img[bit >> 1][ax - 1], sm.im.imx[bit >> 1][ax - 1], sm.im.e[bit >> 1][ax - 1]);
+          else out |= (K)ax << bit;
+        }
+        double sum = 0.0;
+        for (int64_t s = s0; s < s1; ++s) {
+          const K key = (K)skey[s];
+          double v = slam[s];
+          for (K m = KeyOps<K>::support(cg); m;) {
+            const int bit = KeyOps<K>::highest(m);
+            m ^= (K)1 << bit;
+            v = __dmul_rn(v, sm.tb.w[bit >> 1][(u32)((key >> bit) & 3u) - 1u][(u32)(ch >> bit) & 3u]);
+          }
+          sum = (s == s0) ? v : __dadd_rn(sum, v);
+        }
+        acc[k] = sum;
+        word[k] = out;
+        if (FUSED) neg |= composed_sign<K>(out, ex) << k;
+      }
+    }
+
+    // ---- drop rule and write-out
+    u32 pre[kPer];
+    u32 kept_bits = 0, running = 0;
+#pragma unroll
+    for (int k = 0; k < kPer; ++k) {
+      const u32 idx = (u32)(warp * (32 * kPer) + k * 32 + lane);
+      if (neg & (1u << k)) acc[k] = -acc[k];     // sign flips are exact
+      const bool kept = idx < n_out && fabs(acc[k]) >= eps;
+      if (kept) kept_bits |= 1u << k;
+      const u32 votes = __ballot_sync(QX_FULL_MASK, kept);
+      pre[k] = running + __popc(votes & lanemask_lt());
+      running += __popc(votes);
+    }
+    if (one_seg) {
+      u64 tile_total;
+      u64 warp_excl = block_exclusive_sum<u64>(lane == 0 ? (u64)running : 0ull, sm.scan, tile_total);
+      warp_excl = __shfl_sync(QX_FULL_MASK, warp_excl, 0);
+      if (tid == 0) sm.base = (u64)seg_slot[seg0] + atomicAdd(seg_count + seg0, tile_total);
+      __syncthreads();
+      const int64_t base = (int64_t)(sm.base + warp_excl);
+#pragma unroll
+      for (int k = 0; k < kPer; ++k) {
+        if (kept_bits & (1u << k)) {
+          const int64_t pos = base + pre[k];
+          st_stream(keys_out + pos, (KO)word[k]);
+          st_stream(lam_out + pos, acc[k]);
+        }
+      }
+    } else {
+      // the tile crosses a generator boundary (only tiny generators): one atomic per kept term
+#pragma unroll 1
+      for (int k = 0; k < kPer; ++k) {
+        if (kept_bits & (1u << k)) {
+          const int64_t r = (int64_t)(r0 + (u32)(warp * (32 * kPer) + k * 32 + lane));
+          const int g = segment_of(seg_slot, n_seg, r);
+          const int64_t pos = seg_slot[g] + (int64_t)atomicAdd(seg_count + g, 1ull);
+          st_stream(keys_out + pos, (KO)word[k]);
+          st_stream(lam_out + pos, acc[k]);
+        }
+      }
+    }
+  }
+}
+
+template <typename K, typename KO, bool FUSED>
+int launch_group_emit(qx_store* s, int64_t tiles, const u64* cw, const u64* skey, const double* slam,
+                      const u64* gsrc, const u64* gslot, const u64* totals, const int2* tile_info,
+                      const int64_t* seg_slot, int out, u64* seg_count, double eps,
+                      const OperatorTable& tb, const ImageTable<K>& im) {
+  static int per_sm = 0;
+  if (per_sm == 0) {
+    QX_CUDA(cudaFuncSetAttribute(k_group_emit<K, KO, FUSED>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)sizeof(GroupSmem<K>)));
+    QX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_group_emit<K, KO, FUSED>, kThreads,
+                                                          sizeof(GroupSmem<K>)));
+    per_sm = std::max(per_sm, 1);
+  }
+  const int grid = (int)std::min<int64_t>(tiles, (int64_t)s->sm_count * per_sm);
+  k_group_emit<K, KO, FUSED><<<grid, kThreads, sizeof(GroupSmem<K>), s->stream>>>(
+      cw, skey, slam, gsrc, gslot, totals, tile_info, seg_slot, s->n_seg,
+      reinterpret_cast<KO*>(s->keys[out]), s->lam[out], seg_count, eps, tb, im);
+  QX_CUDA(cudaGetLastError());
+  return QX_OK;
+}
+
+// Connected components of "input axes that share an output axis", per digit position; the table
+// handed to the kernels describes the class of each input axis (radix, output axes) and keeps the
+// per-axis weights, zero where the axis does not reach that output.
+void build_class_table(const OperatorTable& nz, int n_qubits, OperatorTable* ct, ClassIds* ids) {
+  *ct = nz;
+  memset(ids, 0, sizeof(*ids));
+  for (int p = 0; p < QX_MAX_QUBITS; ++p) {
+    unsigned reach[3];                            // bit (ax-1) set: input axis a reaches output ax
+    for (int a = 0; a < 3; ++a) {
+      reach[a] = 0;
+      for (int b = 0; b < nz.cnt[p][a]; ++b) reach[a] |= 1u << (nz.axis[p][a][b] - 1);
+    }
+    int parent[3] = {0, 1, 2};
+    for (int a = 0; a < 3; ++a)
+      for (int b = a + 1; b < 3; ++b)
+        if (reach[a] & reach[b]) {
+          int ra = a, rb = b;
+          while (parent[ra] != ra) ra = parent[ra];
+          while (parent[rb] != rb) rb = parent[rb];
+          if (ra != rb) parent[std::max(ra, rb)] = std::min(ra, rb);
+        }
+    // a second sweep closes chains (X~Y, Y~Z found in either order)
+    for (int a = 0; a < 3; ++a) {
+      int r = a;
+      while (parent[r] != r) r = parent[r];
+      parent[a] = r;
+    }
+    for (int a = 0; a < 3; ++a) {
+      unsigned out = 0;
+      for (int b = 0; b < 3; ++b)
+        if (parent[b] == parent[a]) out |= reach[b];
+      ids->cls[p][a] = (unsigned char)(parent[a] + 1);
+      int c = 0;
+      for (int ax = 1; ax <= 3; ++ax) {
+        if (!(out & (1u << (ax - 1)))) continue;
+        double w = 0.0;
+        for (int b = 0; b < nz.cnt[p][a]; ++b)
+          if (nz.axis[p][a][b] == ax) w = nz.w[p][a][b];
+        ct->axis[p][a][c] = (unsigned char)ax;
+        ct->w[p][a][c] = w;
+        ++c;
+      }
+      ct->cnt[p][a] = (unsigned char)c;
+      for (; c < 3; ++c) {
+        ct->axis[p][a][c] = (unsigned char)(a + 1);
+        ct->w[p][a][c] = 0.0;
+      }
+    }
+  }
+  (void)n_qubits;
+}
+
+template <typename T>
+T* carve(char*& cursor, int64_t count) {
+  T* p = reinterpret_cast<T*>(cursor);
+  cursor += (sizeof(T) * (size_t)count + 255) / 256 * 256;
+  return p;
+}
+inline int64_t padded(int64_t bytes) { return (bytes + 255) / 256 * 256; }
+
+}  // namespace
+
+namespace qxe {
+void fill_images_u32(int n_qubits, const uint32_t* program, int n_ops, u32 cx_c, u32 cx_t, u32 cx_s,
+                     ImageTable<u32>* im);
+void fill_images_u64(int n_qubits, const uint32_t* program, int n_ops, u32 cx_c, u32 cx_t, u32 cx_s,
+                     ImageTable<u64>* im);
+}  // namespace qxe
+
+// The large operator step.  On entry the store holds the merged input terms (exact offsets on
+// the host); on exit it holds the canonical result and exact offsets.  `nz` is the operator's
+// non-zero branch table (fill_table in branch.cu).
+int qx_dense_operator_step(qx_store* s, const OperatorTable& nz, const uint32_t* program, int n_ops,
+                           u32 cx_c, u32 cx_t, u32 cx_s, double eps, int64_t* slots_total) {
+  QX_CUDA(cudaSetDevice(s->device));
+  const int n_seg = s->n_seg;
+  const int64_t n = s->h_seg[n_seg];
+  OperatorTable ct;
+  ClassIds ids;
+  build_class_table(nz, s->n_qubits, &ct, &ids);
+
+  // ---- temporaries of the source side (caching allocator: microseconds after the first run)
+  const int64_t src_tiles = std::max<int64_t>(1, (n + kTileSlots - 1) / kTileSlots);
+  const int64_t bytes1 = 2 * padded(8 * n) + 2 * padded(8 * n) + padded(8 * n) + padded(8 * n) +
+                         2 * padded(8 * (n + 1)) + padded(8 * ((int64_t)n_seg + 1)) + 256 +
+                         2 * padded(8 * (src_tiles + 1)) + 256;
+  void* block1 = nullptr;
+  QX_TRY(qx_dev_alloc(&block1, bytes1, s->stream, s->device));
+  struct Release {
+    void* p;
+    cudaStream_t st;
+    ~Release() { qx_dev_free(p, st); }
+  } rel1{block1, s->stream};
+  char* cur = reinterpret_cast<char*>(block1);
+  u64* cwb[2] = {carve<u64>(cur, n), carve<u64>(cur, n)};
+  double* idb[2] = {carve<double>(cur, n), carve<double>(cur, n)};
+  u64* skey = carve<u64>(cur, n);
+  double* slam = carve<double>(cur, n);
+  u64* gsrc = carve<u64>(cur, n + 1);
+  u64* gslot = carve<u64>(cur, n + 1);
+  int64_t* seg_slot = carve<int64_t>(cur, (int64_t)n_seg + 1);
+  u64* totals = carve<u64>(cur, 2);
+  u64* st_heads = carve<u64>(cur, src_tiles + 1);
+  u64* st_slots = carve<u64>(cur, src_tiles + 1);
+  u32* ticket1 = carve<u32>(cur, 2);
+  QX_CUDA(cudaMemsetAsync(totals, 0, (size_t)(reinterpret_cast<char*>(ticket1) + 256 - reinterpret_cast<char*>(totals)),
+                          s->stream));
+
+  const int in = s->cur;
+  int sorted;
+  {
+    QxProfileScope prof(QX_K_DENSE_PREP, s->stream, 8.0 * (double)n + 16.0 * (double)n);
+    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((n + kThreads - 1) / kThreads, (int64_t)s->sm_count * 8));
+    k_class_words<<<grid, kThreads, 0, s->stream>>>(s->keys[in], n, cwb[in], idb[in], ids);
+    QX_CUDA(cudaGetLastError());
+  }
+  {
+    // stable segmented sort of (class word, source index) by class word
+    qxm::MergeBuffers<double> mb;
+    mb.keys[in] = cwb[in];
+    mb.keys[in ^ 1] = cwb[in ^ 1];
+    mb.vals[in] = idb[in];
+    mb.vals[in ^ 1] = idb[in ^ 1];
+    mb.seg[0] = s->seg[0];
+    mb.seg[1] = s->seg[1];
+    mb.cur = in;
+    mb.n_seg = n_seg;
+    mb.ub_total = n;
+    mb.ub_seg = 0;
+    for (int g = 0; g < n_seg; ++g) mb.ub_seg = std::max(mb.ub_seg, s->h_seg[g + 1] - s->h_seg[g]);
+    QX_TRY((qxm::merge_large<double, u64>(s, mb, 0.0, QX_K_REDUCE, false, QX_K_DENSE_PREP, QX_K_DENSE_PREP)));
+    sorted = mb.cur;
+  }
+  {
+    QxProfileScope prof(QX_K_DENSE_PREP, s->stream, 48.0 * (double)n);
+    k_group_scan<<<(unsigned)src_tiles, kThreads, 0, s->stream>>>(
+        cwb[sorted], idb[sorted], s->keys[in], s->lam[in], s->seg[in], n_seg, n, skey, slam, gsrc, gslot,
+        seg_slot, totals, st_heads, st_slots, ticket1, ct);
+    QX_CUDA(cudaGetLastError());
+  }
+  // slot offsets of the generators + totals -> host (sizes the output)
+  QX_CUDA(cudaMemcpyAsync(s->h_pinned, seg_slot, sizeof(int64_t) * (size_t)(n_seg + 1), cudaMemcpyDeviceToHost,
+                          s->stream));
+  QX_CUDA(cudaStreamSynchronize(s->stream));
+  const int64_t total = s->h_pinned[n_seg];
+  int64_t ub_seg = 0;
+  for (int g = 0; g < n_seg; ++g) ub_seg = std::max(ub_seg, s->h_pinned[g + 1] - s->h_pinned[g]);
+  if (slots_total) *slots_total = total;
+  // the sources live in skey/slam now: both store buffers are free for the output
+  QX_TRY(qx_store_reserve(s, total, false));
+  const int out = s->cur ^ 1;
+
+  const int64_t tiles = std::max<int64_t>(1, (total + kTileSlots - 1) / kTileSlots);
+  const int64_t bytes2 = padded(8 * tiles) + padded(8 * (int64_t)n_seg);
+  void* block2 = nullptr;
+  QX_TRY(qx_dev_alloc(&block2, bytes2, s->stream, s->device));
+  Release rel2{block2, s->stream};
+  cur = reinterpret_cast<char*>(block2);
+  int2* tile_info = carve<int2>(cur, tiles);
+  u64* seg_count = carve<u64>(cur, n_seg);
+  QX_CUDA(cudaMemsetAsync(seg_count, 0, sizeof(u64) * (size_t)n_seg, s->stream));
+  k_tile_groups<<<(unsigned)((tiles + 255) / 256), 256, 0, s->stream>>>(gslot, totals, seg_slot, n_seg, tile_info, tiles);
+  qx_count_launches(1);
+  QX_CUDA(cudaGetLastError());
+
+  const bool small_keys = s->n_qubits <= 16;
+  static const bool no_narrow = getenv("QX_NO_NARROW") != nullptr;
+  const bool narrow = small_keys && !no_narrow && ub_seg > QX_SMALL_MAX;
+  {
+    QxProfileScope prof(QX_K_DENSE_EMIT, s->stream, 16.0 * (double)n + (narrow ? 12.0 : 16.0) * (double)total);
+    if (small_keys) {
+      ImageTable<u32> im;
+      memset(&im, 0, sizeof(im));
+      if (n_ops > 0) fill_images_u32(s->n_qubits, program, n_ops, cx_c, cx_t, cx_s, &im);
+#define QX_GE(KO, F) launch_group_emit<u32, KO, F>(s, tiles, cwb[sorted], skey, slam, gsrc, gslot, totals, \
+                                                   tile_info, seg_slot, out, seg_count, eps, ct, im)
+      if (n_ops > 0 && narrow) QX_TRY((QX_GE(u32, true)));
+      else if (n_ops > 0) QX_TRY((QX_GE(u64, true)));
+      else if (narrow) QX_TRY((QX_GE(u32, false)));
+      else QX_TRY((QX_GE(u64, false)));
+#undef QX_GE
+    } else {
+      ImageTable<u64> im;
+      memset(&im, 0, sizeof(im));
+      if (n_ops > 0) {
+        fill_images_u64(s->n_qubits, program, n_ops, cx_c, cx_t, cx_s, &im);
+        QX_TRY((launch_group_emit<u64, u64, true>(s, tiles, cwb[sorted], skey, slam, gsrc, gslot, totals,
+                                                  tile_info, seg_slot, out, seg_count, eps, ct, im)));
+      } else {
+        QX_TRY((launch_group_emit<u64, u64, false>(s, tiles, cwb[sorted], skey, slam, gsrc, gslot, totals,
+                                                   tile_info, seg_slot, out, seg_count, eps, ct, im)));
+      }
+    }
+  }
+  k_counts_to_offsets<<<1, 32, 0, s->stream>>>(seg_count, n_seg, s->seg[out]);
+  qx_count_launches(1);
+  QX_CUDA(cudaGetLastError());
+  s->cur = out;
+  s->exact = false;
+  s->ub_total = total;
+  s->ub_seg = ub_seg;
+  QX_TRY(qx_store_refresh(s));                     // kept counts: exact offsets, sizes the sort
+  // ---- canonical order: distinct words, nothing left to sum or drop
+  qxm::MergeBuffers<double> mb;
+  for (int b = 0; b < 2; ++b) {
+    mb.keys[b] = s->keys[b];
+    mb.vals[b] = s->lam[b];
+    mb.seg[b] = s->seg[b];
+  }
+  mb.cur = s->cur;
+  mb.n_seg = n_seg;
+  mb.ub_total = s->ub_total;
+  mb.ub_seg = s->ub_seg;
+  // the kept terms of generator g sit at its slot offset; the first pass reads them from there
+  if (narrow) QX_TRY((qxm::merge_large<double, u32>(s, mb, eps, QX_K_REDUCE, false, QX_K_SORT_PASS, QX_K_SORT_HIST, seg_slot)));
+  else QX_TRY((qxm::merge_large<double, u64>(s, mb, eps, QX_K_REDUCE, false, QX_K_SORT_PASS, QX_K_SORT_HIST, seg_slot)));
+  s->cur = mb.cur;
+  return QX_OK;
+}

@@ -25,6 +25,7 @@
 #pragma once
 
 #include <algorithm>
+#include <type_traits>
 
 #include "qx_device.cuh"
 
@@ -77,10 +78,13 @@ __device__ __forceinline__ int tile_segment(const int64_t* tile_prefix, int n_se
 // single broadcast load instead of every thread bisecting the segment table in global memory
 // (6 % of the pass's instructions and the head of its critical path, profiles/r01g).
 struct __align__(16) TileInfo {
-  int64_t start;      // first term of the tile
+  int64_t off;        // first term of the tile, relative to the start of its segment
   int count;          // terms in the tile (<= tile_terms)
   int seg;            // segment; bit 31 set iff this is the segment's first tile
 };
+// A pass reads segment g at base_in[g] + off.  base_in is the offset array itself except for the
+// first pass after the grouped operator step (dense.cu), whose output sits at the slot offsets of
+// the generators with gaps behind the kept terms; every pass WRITES the compact layout seg[g].
 
 static __global__ void k_sort_tilemap(const int64_t* __restrict__ seg, int n_seg,
                                       const int64_t* __restrict__ tile_prefix, TileInfo* __restrict__ info,
@@ -90,8 +94,8 @@ static __global__ void k_sort_tilemap(const int64_t* __restrict__ seg, int n_seg
        tile += (int64_t)gridDim.x * blockDim.x) {
     const int g = tile_segment(tile_prefix, n_seg, tile);
     TileInfo ti;
-    ti.start = seg[g] + (tile - tile_prefix[g]) * tile_terms;
-    ti.count = (int)min((int64_t)tile_terms, seg[g + 1] - ti.start);
+    ti.off = (tile - tile_prefix[g]) * tile_terms;
+    ti.count = (int)min((int64_t)tile_terms, seg[g + 1] - seg[g] - ti.off);
     ti.seg = g | (tile == tile_prefix[g] ? (int)0x80000000 : 0);
     info[tile] = ti;
   }
@@ -104,7 +108,7 @@ constexpr int kMaxPasses = 8;
 
 template <typename K>
 static __global__ void __launch_bounds__(kSortThreads)
-k_sort_hist(const K* __restrict__ keys, const TileInfo* __restrict__ info,
+k_sort_hist(const K* __restrict__ keys, const int64_t* __restrict__ base_in, const TileInfo* __restrict__ info,
             const int64_t* __restrict__ n_tiles, u32* __restrict__ hist, int passes) {
   __shared__ u32 sh[kMaxPasses][QX_RADIX];
   for (int i = threadIdx.x; i < kMaxPasses * QX_RADIX; i += kSortThreads) (&sh[0][0])[i] = 0u;
@@ -126,7 +130,7 @@ k_sort_hist(const K* __restrict__ keys, const TileInfo* __restrict__ info,
       }
       cur_g = g;
     }
-    const int64_t start = ti.start;
+    const int64_t start = base_in[g] + ti.off;
     const int count = ti.count;
     const int rounds = (count + kSortThreads - 1) / kSortThreads;
 #pragma unroll 4
@@ -217,11 +221,15 @@ __device__ __forceinline__ u32 key_byte(u32 key, int which) {
   return __byte_perm(key, 0u, 0x4440u | (u32)(which & 3));
 }
 
-template <typename K, typename V, int THREADS, int ITEMS, int LB, int MINB = (THREADS <= 256 ? 3 : 2)>
+// KO = type of the keys written: the last pass over narrow (32-bit) keys of a sort-only merge
+// widens them to the store's 64-bit words on the way out.
+template <typename K, typename V, int THREADS, int ITEMS, int LB, int MINB = (THREADS <= 256 ? 3 : 2),
+          typename KO = K>
 __global__ void __launch_bounds__(THREADS, MINB)
 k_onesweep(const K* __restrict__ keys_in, const V* __restrict__ vals_in,
-           K* __restrict__ keys_out, V* __restrict__ vals_out,
-           const int64_t* __restrict__ seg, const TileInfo* __restrict__ info,
+           KO* __restrict__ keys_out, V* __restrict__ vals_out,
+           const int64_t* __restrict__ seg, const int64_t* __restrict__ base_in,
+           const TileInfo* __restrict__ info,
            const int64_t* __restrict__ n_tiles, const u32* __restrict__ digit_base, int base_stride,
            u32* status, u32* ticket, int which, int ahead, int debug) {
   constexpr int WARPS = THREADS / 32;
@@ -240,7 +248,7 @@ k_onesweep(const K* __restrict__ keys_in, const V* __restrict__ vals_in,
   const TileInfo ti = info[tile];
   const int g = ti.seg & 0x7fffffff;
   const bool first = ti.seg < 0;
-  const int64_t start = ti.start;
+  const int64_t start = base_in[g] + ti.off;
   const int count = ti.count;
   const bool full = count == TILE;
   const K* kin = keys_in + start;
@@ -252,7 +260,7 @@ k_onesweep(const K* __restrict__ keys_in, const V* __restrict__ vals_in,
   // the loads below pay L2 latency instead of HBM latency.
   if (ahead > 0 && tile + ahead < total_tiles) {
     const TileInfo tp = info[tile + ahead];
-    const int64_t sp = tp.start;
+    const int64_t sp = base_in[tp.seg & 0x7fffffff] + tp.off;
     const int cp = tp.count;
     for (int i = tid * 16; i < cp; i += THREADS * 16) {      // one 128-byte line of doubles per step
       if (sizeof(K) == 8 || (i & 16) == 0) asm volatile("prefetch.global.L2 [%0];" ::"l"(keys_in + sp + i));
@@ -341,7 +349,7 @@ k_onesweep(const K* __restrict__ keys_in, const V* __restrict__ vals_in,
     u32 excl = 0;
     if (!solo) {
       constexpr int W = LB;
-      const int64_t first_tile = tile - (start - seg[g]) / TILE;
+      const int64_t first_tile = tile - ti.off / TILE;
       int64_t t = tile - 1;
       bool done = false;
       while (!done) {
@@ -373,7 +381,7 @@ k_onesweep(const K* __restrict__ keys_in, const V* __restrict__ vals_in,
     if (full || slot < count) {
       const K kk = sm.keys[slot];
       const int64_t dst = sm.gbase[key_byte(kk, which)] + slot;
-      st_stream(keys_out + dst, kk);
+      st_stream(keys_out + dst, (KO)kk);
       st_stream(vals_out + dst, sm.vals[slot]);
     }
   }
@@ -667,19 +675,21 @@ inline int sort_prefetch_distance(int sm_count) {
   return v >= 0 ? v : 2 * sm_count;     // ~ resident CTAs (two per SM)
 }
 
-template <typename K, typename V, int THREADS, int ITEMS, int LB, int MINB = (THREADS <= 256 ? 3 : 2)>
+template <typename K, typename V, int THREADS, int ITEMS, int LB, int MINB = (THREADS <= 256 ? 3 : 2),
+          typename KO = K>
 int launch_pass(QxArena* ar, MergeBuffers<V>& mb, int cur, int64_t tiles_ub, const TileInfo* info,
-                const int64_t* n_tiles, const u32* digit_base, int base_stride, u32* ticket, int which) {
+                const int64_t* n_tiles, const u32* digit_base, int base_stride, u32* ticket, int which,
+                const int64_t* base_in) {
   using Smem = SortSmem<K, V, THREADS, ITEMS>;
   static bool attr_set = false;
   if (!attr_set) {
-    QX_CUDA(cudaFuncSetAttribute(k_onesweep<K, V, THREADS, ITEMS, LB, MINB>,
+    QX_CUDA(cudaFuncSetAttribute(k_onesweep<K, V, THREADS, ITEMS, LB, MINB, KO>,
                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(Smem)));
     attr_set = true;
   }
-  k_onesweep<K, V, THREADS, ITEMS, LB, MINB><<<(unsigned)tiles_ub, THREADS, sizeof(Smem), ar->stream>>>(
-      reinterpret_cast<const K*>(mb.keys[cur]), mb.vals[cur], reinterpret_cast<K*>(mb.keys[cur ^ 1]),
-      mb.vals[cur ^ 1], mb.seg[cur], info, n_tiles,
+  k_onesweep<K, V, THREADS, ITEMS, LB, MINB, KO><<<(unsigned)tiles_ub, THREADS, sizeof(Smem), ar->stream>>>(
+      reinterpret_cast<const K*>(mb.keys[cur]), mb.vals[cur], reinterpret_cast<KO*>(mb.keys[cur ^ 1]),
+      mb.vals[cur ^ 1], mb.seg[cur], base_in ? base_in : mb.seg[cur], info, n_tiles,
       digit_base, base_stride, ar->status, ticket, which, sort_prefetch_distance(ar->sm_count),
       getenv("QX_SORT_DEBUG") ? atoi(getenv("QX_SORT_DEBUG")) : 0);
   QX_CUDA(cudaGetLastError());
@@ -692,7 +702,7 @@ inline int sort_variant() {
   if (v < 0) {
     const char* e = getenv("QX_SORT_VARIANT");
     v = e ? atoi(e) : 0;
-    if (v < 0 || v > 14) v = 0;
+    if (v < 0 || v > 4) v = 0;
   }
   return v;
 }
@@ -700,49 +710,36 @@ inline int sort_variant() {
 inline int sort_tile_terms(int variant, size_t value_bytes) {
   if (value_bytes > 8) return 256 * 12;            // complex coefficients: one geometry
   switch (variant) {
-    case 1: return 384 * 12;
     case 2: return 256 * 12;
     case 3: return 256 * 16;
     case 4: return 512 * 8;
-    case 5: return 384 * 12;
-    case 6: return 768 * 6;
-    case 7: return 1024 * 4;
-    case 8: return 384 * 12;
-    case 10: return 384 * 12;
-    case 11: return 256 * 16;
-    case 12: return 256 * 12;
-    case 13: return 512 * 8;
-    case 14: return 512 * 12;
     default: return 384 * 12;
   }
 }
 
-template <typename K, typename V>
+// WIDEN: the pass reads narrow keys and writes 64-bit ones (last pass of a narrow sort-only merge)
+template <typename K, typename V, bool WIDEN = false>
 int dispatch_pass(int variant, QxArena* ar, MergeBuffers<V>& mb, int cur, int64_t tiles_ub,
                   const TileInfo* info, const int64_t* n_tiles, const u32* digit_base, int base_stride, u32* ticket,
-                  int which) {
+                  int which, const int64_t* base_in = nullptr) {
+  using KO = typename std::conditional<WIDEN, u64, K>::type;
   if (sizeof(V) > 8)
-    return launch_pass<K, V, 256, 12, 8>(ar, mb, cur, tiles_ub, info, n_tiles, digit_base, base_stride, ticket, which);
+    return launch_pass<K, V, 256, 12, 8>(ar, mb, cur, tiles_ub, info, n_tiles, digit_base, base_stride, ticket, which, base_in);
+  if (sizeof(K) == 4) {
+    // narrow keys: 56 registers and 68 KB of shared memory per CTA -> three CTAs (36 warps) per SM
+    // instead of two; the pass is latency-bound, not HBM-bound (profiles/r01g), so occupancy pays
+    switch (variant) {
+      case 2: return launch_pass<K, V, 256, 12, 8, 4, KO>(ar, mb, cur, tiles_ub, info, n_tiles, digit_base, base_stride, ticket, which, base_in);
+      case 3: return launch_pass<K, V, 256, 16, 8, 3, KO>(ar, mb, cur, tiles_ub, info, n_tiles, digit_base, base_stride, ticket, which, base_in);
+      case 4: return launch_pass<K, V, 512, 8, 8, 2, KO>(ar, mb, cur, tiles_ub, info, n_tiles, digit_base, base_stride, ticket, which, base_in);
+      default: return launch_pass<K, V, 384, 12, 8, 3, KO>(ar, mb, cur, tiles_ub, info, n_tiles, digit_base, base_stride, ticket, which, base_in);
+    }
+  }
   switch (variant) {
-    case 1: return launch_pass<K, V, 384, 12, 16>(ar, mb, cur, tiles_ub, info, n_tiles, digit_base, base_stride, ticket, which);
-    case 2: return launch_pass<K, V, 256, 12, 8>(ar, mb, cur, tiles_ub, info, n_tiles, digit_base, base_stride, ticket, which);
-    case 3: return launch_pass<K, V, 256, 16, 8>(ar, mb, cur, tiles_ub, info, n_tiles, digit_base, base_stride, ticket, which);
-    case 4: return launch_pass<K, V, 512, 8, 8>(ar, mb, cur, tiles_ub, info, n_tiles, digit_base, base_stride, ticket, which);
-    case 5: return launch_pass<K, V, 384, 12, 32>(ar, mb, cur, tiles_ub, info, n_tiles, digit_base, base_stride, ticket, which);
-    case 6: return launch_pass<K, V, 768, 6, 8>(ar, mb, cur, tiles_ub, info, n_tiles, digit_base, base_stride, ticket, which);
-    case 7: return launch_pass<K, V, 1024, 4, 8>(ar, mb, cur, tiles_ub, info, n_tiles, digit_base, base_stride, ticket, which);
-    case 8: return launch_pass<K, V, 384, 12, 4>(ar, mb, cur, tiles_ub, info, n_tiles, digit_base, base_stride, ticket, which);
-    case 10: return launch_pass<K, V, 384, 12, 8, 3>(ar, mb, cur, tiles_ub, info, n_tiles, digit_base, base_stride, ticket, which);
-    case 11: return launch_pass<K, V, 256, 16, 8, 3>(ar, mb, cur, tiles_ub, info, n_tiles, digit_base, base_stride, ticket, which);
-    case 12: return launch_pass<K, V, 256, 12, 8, 4>(ar, mb, cur, tiles_ub, info, n_tiles, digit_base, base_stride, ticket, which);
-    case 13: return launch_pass<K, V, 512, 8, 8, 2>(ar, mb, cur, tiles_ub, info, n_tiles, digit_base, base_stride, ticket, which);
-    case 14: return launch_pass<K, V, 512, 12, 8, 2>(ar, mb, cur, tiles_ub, info, n_tiles, digit_base, base_stride, ticket, which);
-    default:
-      // narrow keys: 56 registers and 68 KB of shared memory per CTA -> three CTAs (36 warps) per SM
-      // instead of two; the pass is latency-bound, not HBM-bound (profiles/r01g), so occupancy pays
-      if (sizeof(K) == 4)
-        return launch_pass<K, V, 384, 12, 8, 3>(ar, mb, cur, tiles_ub, info, n_tiles, digit_base, base_stride, ticket, which);
-      return launch_pass<K, V, 384, 12, 8>(ar, mb, cur, tiles_ub, info, n_tiles, digit_base, base_stride, ticket, which);
+    case 2: return launch_pass<K, V, 256, 12, 8>(ar, mb, cur, tiles_ub, info, n_tiles, digit_base, base_stride, ticket, which, base_in);
+    case 3: return launch_pass<K, V, 256, 16, 8>(ar, mb, cur, tiles_ub, info, n_tiles, digit_base, base_stride, ticket, which, base_in);
+    case 4: return launch_pass<K, V, 512, 8, 8>(ar, mb, cur, tiles_ub, info, n_tiles, digit_base, base_stride, ticket, which, base_in);
+    default: return launch_pass<K, V, 384, 12, 8>(ar, mb, cur, tiles_ub, info, n_tiles, digit_base, base_stride, ticket, which, base_in);
   }
 }
 
@@ -751,8 +748,12 @@ int dispatch_pass(int variant, QxArena* ar, MergeBuffers<V>& mb, int cur, int64_
 // K = u32: the live buffer holds NARROW keys (one 32-bit word per term, 2n <= 32) as written by
 // the fused expansion kernel; every pass then moves 12 B per term instead of 16 and the reduce
 // widens back to the store's 64-bit keys.  Narrow keys never leave a merge.
+// cls_pass / cls_hist: instrumentation classes of the passes (the dense operator path sorts its
+// few source terms with this routine too and books them separately).
 template <typename V, typename K = u64>
-int merge_large(QxArena* ar, MergeBuffers<V>& mb, double eps, int cls_reduce, bool do_reduce = true) {
+int merge_large(QxArena* ar, MergeBuffers<V>& mb, double eps, int cls_reduce, bool do_reduce = true,
+                int cls_pass = QX_K_SORT_PASS, int cls_hist = QX_K_SORT_HIST,
+                const int64_t* first_base_in = nullptr) {
   const int n_seg = mb.n_seg;
   const int passes = std::min(kMaxPasses, (2 * ar->n_qubits + QX_RADIX_BITS - 1) / QX_RADIX_BITS);
   if (mb.ub_seg >= (int64_t)kFlagVal)
@@ -791,9 +792,10 @@ int merge_large(QxArena* ar, MergeBuffers<V>& mb, double eps, int cls_reduce, bo
   QX_CUDA(cudaGetLastError());
   {
     const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(tiles_ub, (int64_t)ar->sm_count * 4));
-    QxProfileScope prof(QX_K_SORT_HIST, ar->stream, (double)sizeof(K) * (double)mb.ub_total);
-    k_sort_hist<K><<<grid, kSortThreads, 0, ar->stream>>>(reinterpret_cast<const K*>(mb.keys[cur]), info, n_tiles,
-                                                          hist, passes);
+    QxProfileScope prof(cls_hist, ar->stream, (double)sizeof(K) * (double)mb.ub_total);
+    k_sort_hist<K><<<grid, kSortThreads, 0, ar->stream>>>(reinterpret_cast<const K*>(mb.keys[cur]),
+                                                          first_base_in ? first_base_in : mb.seg[cur], info,
+                                                          n_tiles, hist, passes);
     QX_CUDA(cudaGetLastError());
   }
   k_sort_scan_hist<<<n_seg * passes, QX_RADIX, 0, ar->stream>>>(hist);
@@ -805,13 +807,16 @@ int merge_large(QxArena* ar, MergeBuffers<V>& mb, double eps, int cls_reduce, bo
   for (int p = 0; p < passes; ++p) {
     QX_CUDA(cudaMemsetAsync(ar->status, 0, sizeof(u32) * (size_t)(tiles_ub * QX_RADIX), ar->stream));
     QX_CUDA(cudaMemsetAsync(ticket, 0, sizeof(u32), ar->stream));
-    QxProfileScope prof(QX_K_SORT_PASS, ar->stream, 2.0 * (sizeof(K) + sizeof(V)) * (double)mb.ub_total);
-    QX_TRY((dispatch_pass<K, V>(variant, ar, mb, cur, tiles_ub, info, n_tiles, hist + (size_t)p * QX_RADIX,
-                                passes * QX_RADIX, ticket, p)));
+    QxProfileScope prof(cls_pass, ar->stream, 2.0 * (sizeof(K) + sizeof(V)) * (double)mb.ub_total);
+    if (!do_reduce && sizeof(K) == 4 && p == passes - 1)
+      QX_TRY((dispatch_pass<K, V, true>(variant, ar, mb, cur, tiles_ub, info, n_tiles, hist + (size_t)p * QX_RADIX,
+                                        passes * QX_RADIX, ticket, p, p == 0 ? first_base_in : nullptr)));
+    else
+      QX_TRY((dispatch_pass<K, V>(variant, ar, mb, cur, tiles_ub, info, n_tiles, hist + (size_t)p * QX_RADIX,
+                                  passes * QX_RADIX, ticket, p, p == 0 ? first_base_in : nullptr)));
     cur ^= 1;
   }
   if (!do_reduce) {
-    if (sizeof(K) != 8) return qx_fail(QX_ERR_CONSISTENCY, "sort-only needs full-width keys (internal error)");
     mb.cur = cur;
     return QX_OK;
   }

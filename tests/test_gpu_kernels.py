@@ -208,17 +208,20 @@ def test_zi_sums_and_norms():
         assert abs(a - lam[mask].sum()) < 1e-9 and abs(b - np.dot(lam, lam)) < 1e-9
 
 
-@pytest.mark.parametrize("n,terms,rot_qubits,n_ops", [
-    (3, 40, 3, 0), (6, 300, 6, 25),            # small merge path, 32-bit working keys
-    (12, 60, 9, 40), (16, 8, 12, 15),          # large path -> narrow (32-bit) raw keys
-    (16, 2000, 5, 200),                        # many sources per output tile
-    (20, 50, 9, 60), (32, 20, 10, 300),        # 64-bit working keys
-    (14, 30, 10, 0),                           # narrow keys without a Clifford run
+@pytest.mark.parametrize("n,terms,rot_qubits,n_ops,mix", [
+    (3, 40, 3, 0, 1), (6, 300, 6, 25, 1),         # small merge path, 32-bit working keys
+    (12, 60, 9, 40, 1), (16, 8, 12, 15, 1),       # large fan-out: grouped dense path, narrow keys
+    (16, 2000, 5, 200, 1),                        # small fan-out: raw expansion, many sources per tile
+    (20, 50, 9, 60, 1), (32, 20, 10, 300, 1),     # 64-bit working keys
+    (14, 30, 10, 0, 1),                           # narrow keys without a Clifford run
+    (8, 3000, 8, 30, 3), (10, 2000, 10, 0, 3),    # dense path: hundreds of sources per group, many tiles
+    (9, 500, 9, 12, 2), (18, 40, 11, 50, 3),      # dense path: partial mixing; 64-bit working keys
+    (7, 400, 7, 9, 3),                            # dense path: every tile spans several groups
 ])
-def test_operator_run_equals_three_steps(n, terms, rot_qubits, n_ops):
-    """qx_apply_operator_run (Clifford run folded into the expansion, narrow raw keys) must give
-    bit-for-bit what qx_apply_operator + qx_apply_clifford + qx_merge give, which in turn are
-    checked against the oracle above."""
+def test_operator_run_equals_three_steps(n, terms, rot_qubits, n_ops, mix):
+    """qx_apply_operator_run (grouped dense accumulation or raw expansion, Clifford run folded in,
+    narrow keys) must give bit-for-bit what qx_apply_operator + qx_apply_clifford + qx_merge give,
+    which in turn are checked against the oracle above.  mix = rotations stacked per qubit."""
     rng = np.random.default_rng(n * 1000 + terms + n_ops)
     gens = []
     for s in (terms, 1, max(1, terms // 3)):
@@ -226,7 +229,8 @@ def test_operator_run_equals_three_steps(n, terms, rot_qubits, n_ops):
         keys = np.unique(keys)
         gens.append((lam[: len(keys)], keys))
     qs = rng.choice(n, size=rot_qubits, replace=False)
-    gates = [qx.Instruction(str(rng.choice(["RX", "RY", "RZ"])), (int(j),), float(rng.uniform(0, 6.28))) for j in qs]
+    gates = [qx.Instruction(str(rng.choice(["RX", "RY", "RZ"])), (int(j),), float(rng.uniform(0, 6.28)))
+             for _ in range(mix) for j in qs]
     block = oracle.lut_blocks(oracle.partition(gates, n), n)[0]
     counts, axes, weights = lut.operator_tables(block)
     prog = []
