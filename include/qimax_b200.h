@@ -82,6 +82,17 @@ int qx_store_device_view(qx_store* s, const uint64_t** d_keys, const double** d_
                          const int64_t** d_offsets);
 int qx_store_capacity(qx_store* s, int64_t* capacity_terms, int64_t* hbm_bytes);
 int qx_store_synchronize(qx_store* s);
+/* Generators evolve independently (engine.py:113-116): a new store holding copies of segments
+ * [seg_lo, seg_hi) of src (device-to-device), launching on a non-blocking stream of its own so
+ * that its kernels and copies overlap those of other stores.  src is left untouched. */
+int qx_store_slice(qx_store* src, int32_t seg_lo, int32_t seg_hi, int64_t capacity_terms,
+                   qx_store** out);
+/* qx_store_download without the final wait: offsets are returned at once (they are exact on
+ * the host after any merge), the term copies are queued on the store's stream into keys /
+ * lambdas, which should be page-locked (qx_host_alloc) and must stay valid until
+ * qx_store_synchronize(s). */
+int qx_store_download_async(qx_store* s, int64_t* offsets, uint64_t* keys, double* lambdas,
+                            int64_t cap_terms);
 
 /* ---- a2 + Clifford part of a3: fused run of sign-permutation gates ----------
  * Replaces apply_cx (stabilizer.py:340-363) and _apply_1q_terms (engine.py:183-218)

@@ -544,8 +544,7 @@ extern "C" int qx_count_operator(qx_store* s, const int32_t* counts, int64_t* ra
   k_gather_offsets<<<(s->n_seg + 256) / 256, 256, 0, s->stream>>>(s->seg[s->cur], s->n_seg, roff, tmp);
   qx_count_launches(1);
   QX_CUDA(cudaGetLastError());
-  QX_CUDA(cudaMemcpyAsync(s->h_pinned, tmp, sizeof(int64_t) * (size_t)(s->n_seg + 1),
-                          cudaMemcpyDeviceToHost, s->stream));
+  QX_TRY(qx_readback(s->stream, s->h_pinned, tmp, (int64_t)s->n_seg + 1));
   QX_CUDA(cudaStreamSynchronize(s->stream));
   for (int g = 0; g < s->n_seg; ++g) raw_per_segment[g] = s->h_pinned[g + 1] - s->h_pinned[g];
   return QX_OK;
@@ -642,8 +641,7 @@ int expand(qx_store* s, const OperatorTable& tb, const uint32_t* program, int n_
                                                                   s->seg[s->cur ^ 1]);
   qx_count_launches(1);
   QX_CUDA(cudaGetLastError());
-  QX_CUDA(cudaMemcpyAsync(s->h_pinned, s->seg[s->cur ^ 1], sizeof(int64_t) * (size_t)(s->n_seg + 1),
-                          cudaMemcpyDeviceToHost, s->stream));
+  QX_TRY(qx_readback(s->stream, s->h_pinned, s->seg[s->cur ^ 1], (int64_t)s->n_seg + 1));
   QX_CUDA(cudaStreamSynchronize(s->stream));
   const int64_t raw = s->h_pinned[s->n_seg];
   if (raw_total) *raw_total = raw;

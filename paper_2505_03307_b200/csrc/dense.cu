@@ -676,8 +676,7 @@ int qx_dense_operator_step(qx_store* s, const OperatorTable& nz, const uint32_t*
     QX_CUDA(cudaGetLastError());
   }
   // slot offsets of the generators + totals -> host (sizes the output)
-  QX_CUDA(cudaMemcpyAsync(s->h_pinned, seg_slot, sizeof(int64_t) * (size_t)(n_seg + 1), cudaMemcpyDeviceToHost,
-                          s->stream));
+  QX_TRY(qx_readback(s->stream, s->h_pinned, seg_slot, (int64_t)n_seg + 1));
   QX_CUDA(cudaStreamSynchronize(s->stream));
   const int64_t total = s->h_pinned[n_seg];
   int64_t ub_seg = 0;

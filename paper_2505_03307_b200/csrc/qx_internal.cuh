@@ -72,6 +72,7 @@ struct QxArena {
   int n_qubits = 0;
   int sm_count = 148;
   cudaStream_t stream = 0;
+  bool own_stream = false;      // created by the library (qx_store_slice): destroyed with the handle
   void* scratch = nullptr;      // generic byte scratch (tables, histograms, offsets)
   int64_t scratch_bytes = 0;
   u32* status = nullptr;        // look-back words of the sort passes
@@ -84,6 +85,7 @@ struct QxArena {
 // cudaMalloc/cudaFree (tens of ms) every run.
 int qx_dev_alloc(void** out, int64_t bytes, cudaStream_t stream, int device);
 void qx_dev_free(void* ptr, cudaStream_t stream);
+void qx_dev_forget_stream(cudaStream_t stream);
 int qx_pinned_alloc(void** out, int64_t bytes);
 void qx_pinned_free(void* ptr);
 template <typename T>
@@ -114,6 +116,8 @@ struct qx_store : QxArena {
 
 int qx_store_reserve(qx_store* s, int64_t terms, bool keep_live);
 int qx_store_refresh(qx_store* s);          // D2H of the live offsets, sets exact
+// n_words int64 from device memory into PAGE-LOCKED host memory, by a kernel on `stream` (no copy engine)
+int qx_readback(cudaStream_t stream, int64_t* pinned_dst, const int64_t* d_src, int64_t n_words);
 inline void qx_store_flip(qx_store* s) { s->cur ^= 1; }
 inline int qx_store_scratch(qx_store* s, int64_t bytes) { return qx_arena_scratch(s, bytes); }
 

@@ -211,11 +211,20 @@ int qx_dev_alloc(void** out, int64_t bytes, cudaStream_t stream, int device) {
   if (device < 0 || device >= 64) return qx_fail(QX_ERR_INVALID, "bad device %d", device);
   const size_t want = round_block((size_t)std::max<int64_t>(bytes, 256));
   std::lock_guard<std::mutex> lock(g_alloc_mu);
-  auto it = g_free[device].lower_bound(want);
-  if (it != g_free[device].end() && it->first <= 2 * want + (64u << 20)) {
+  // a cached block of a fitting size whose last user is this stream, or a stream with nothing
+  // pending (waiting for a busy stream here would serialise stores that are meant to overlap,
+  // e.g. one range's download against the next range's kernels)
+  const size_t limit = 2 * want + (64u << 20);
+  auto fallback = g_free[device].end();
+  for (auto it = g_free[device].lower_bound(want); it != g_free[device].end() && it->first <= limit; ++it) {
+    const bool ready = it->second.stream == stream || cudaStreamQuery(it->second.stream) == cudaSuccess;
+    if (!ready) {
+      cudaGetLastError();                      // cudaErrorNotReady is not an error
+      if (fallback == g_free[device].end()) fallback = it;
+      continue;
+    }
     DevBlock blk = it->second;
     g_free[device].erase(it);
-    if (blk.stream != stream) cudaStreamSynchronize(blk.stream);
     blk.stream = stream;
     g_live[blk.ptr] = blk;
     *out = blk.ptr;
@@ -223,6 +232,16 @@ int qx_dev_alloc(void** out, int64_t bytes, cudaStream_t stream, int device) {
   }
   void* p = nullptr;
   cudaError_t e = cudaMalloc(&p, want);
+  if (e != cudaSuccess && fallback != g_free[device].end()) {   // HBM is tight: wait for the busy block
+    cudaGetLastError();
+    DevBlock blk = fallback->second;
+    g_free[device].erase(fallback);
+    cudaStreamSynchronize(blk.stream);
+    blk.stream = stream;
+    g_live[blk.ptr] = blk;
+    *out = blk.ptr;
+    return QX_OK;
+  }
   if (e != cudaSuccess) {            // give the cache back to the driver and retry once
     cudaGetLastError();
     release_cached(device);
@@ -252,6 +271,18 @@ void qx_dev_free(void* ptr, cudaStream_t stream) {
   g_live.erase(it);
   blk.stream = stream;
   g_free[blk.device].emplace(blk.bytes, blk);
+}
+
+// A stream is about to be destroyed: wait for it and re-home its cached blocks on the default
+// stream so that nobody synchronises a dead handle later.
+void qx_dev_forget_stream(cudaStream_t stream) {
+  cudaStreamSynchronize(stream);
+  std::lock_guard<std::mutex> lock(g_alloc_mu);
+  for (int d = 0; d < 64; ++d)
+    for (auto& kv : g_free[d])
+      if (kv.second.stream == stream) kv.second.stream = 0;
+  for (auto& kv : g_live)
+    if (kv.second.stream == stream) kv.second.stream = 0;
 }
 
 // small page-locked staging blocks (offset mirrors): same idea, cudaMallocHost is ~0.3 ms a call
@@ -359,7 +390,56 @@ extern "C" int qx_store_destroy(qx_store* s) {
   }
   qx_pinned_free(s->h_seg);
   qx_arena_release(s);
+  if (s->own_stream) {
+    // blocks handed back above carry this stream as their last user: forget it before it dies
+    qx_dev_forget_stream(s->stream);
+    cudaStreamDestroy(s->stream);
+  }
   delete s;
+  return QX_OK;
+}
+
+extern "C" int qx_store_slice(qx_store* src, int32_t seg_lo, int32_t seg_hi, int64_t capacity_terms,
+                              qx_store** out) {
+  QX_REQUIRE(src && out, "NULL argument");
+  QX_REQUIRE(seg_lo >= 0 && seg_lo < seg_hi && seg_hi <= src->n_seg, "bad segment range [%d, %d) of %d",
+             seg_lo, seg_hi, src->n_seg);
+  *out = nullptr;
+  QX_CUDA(cudaSetDevice(src->device));
+  if (!src->exact) QX_TRY(qx_store_refresh(src));
+  QX_CUDA(cudaStreamSynchronize(src->stream));          // the source terms are final
+  const int64_t first = src->h_seg[seg_lo], count = src->h_seg[seg_hi] - first;
+  qx_store* s = nullptr;
+  QX_TRY(qx_store_create(src->device, src->n_qubits, seg_hi - seg_lo, std::max(capacity_terms, count), &s));
+  cudaError_t e = cudaStreamCreateWithFlags(&s->stream, cudaStreamNonBlocking);
+  if (e != cudaSuccess) {
+    s->stream = 0;
+    qx_store_destroy(s);
+    return qx_fail(QX_ERR_CUDA, "cudaStreamCreate failed: %s", cudaGetErrorString(e));
+  }
+  s->own_stream = true;
+  for (int g = 0; g <= s->n_seg; ++g) s->h_seg[g] = src->h_seg[seg_lo + g] - first;
+  const int c = s->cur;
+  if (count > 0) {
+    e = cudaMemcpyAsync(s->keys[c], src->keys[src->cur] + first, sizeof(u64) * (size_t)count,
+                        cudaMemcpyDeviceToDevice, s->stream);
+    if (e == cudaSuccess)
+      e = cudaMemcpyAsync(s->lam[c], src->lam[src->cur] + first, sizeof(double) * (size_t)count,
+                          cudaMemcpyDeviceToDevice, s->stream);
+  }
+  if (e == cudaSuccess)
+    e = cudaMemcpyAsync(s->seg[c], s->h_seg, sizeof(int64_t) * (size_t)(s->n_seg + 1), cudaMemcpyHostToDevice,
+                        s->stream);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(s->stream);   // src may change once we return
+  if (e != cudaSuccess) {
+    qx_store_destroy(s);
+    return qx_fail(QX_ERR_CUDA, "slice copy failed: %s", cudaGetErrorString(e));
+  }
+  s->exact = true;
+  s->ub_total = count;
+  s->ub_seg = 0;
+  for (int g = 0; g < s->n_seg; ++g) s->ub_seg = std::max(s->ub_seg, s->h_seg[g + 1] - s->h_seg[g]);
+  *out = s;
   return QX_OK;
 }
 
@@ -480,10 +560,27 @@ int qx_arena_status(QxArena* s, int64_t words) {
   return QX_OK;
 }
 
+// Small device -> host read-backs (offsets, counts) go through a kernel that stores into
+// page-locked host memory (directly addressable under UVA) instead of cudaMemcpyAsync: a copy
+// would queue on the device-to-host copy engine behind whatever bulk download another store
+// has in flight there, and stall this store's host thread for the length of that download.
+static __global__ void k_readback(int64_t* __restrict__ host_dst, const int64_t* __restrict__ src, int64_t n) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    host_dst[i] = src[i];
+}
+
+int qx_readback(cudaStream_t stream, int64_t* pinned_dst, const int64_t* d_src, int64_t n_words) {
+  if (n_words <= 0) return QX_OK;
+  const int grid = (int)std::min<int64_t>((n_words + 255) / 256, 64);
+  k_readback<<<grid, 256, 0, stream>>>(pinned_dst, d_src, n_words);
+  qx_count_launches(1);
+  QX_CUDA(cudaGetLastError());
+  return QX_OK;
+}
+
 int qx_store_refresh(qx_store* s) {
   QX_CUDA(cudaSetDevice(s->device));
-  QX_CUDA(cudaMemcpyAsync(s->h_seg, s->seg[s->cur], sizeof(int64_t) * (size_t)(s->n_seg + 1),
-                          cudaMemcpyDeviceToHost, s->stream));
+  QX_TRY(qx_readback(s->stream, s->h_seg, s->seg[s->cur], (int64_t)s->n_seg + 1));
   QX_CUDA(cudaStreamSynchronize(s->stream));
   s->exact = true;
   s->ub_total = s->h_seg[s->n_seg];
@@ -571,6 +668,24 @@ extern "C" int qx_store_download(qx_store* s, int64_t* offsets, uint64_t* keys, 
                               cudaMemcpyDeviceToHost, s->stream));
   }
   QX_CUDA(cudaStreamSynchronize(s->stream));
+  return QX_OK;
+}
+
+extern "C" int qx_store_download_async(qx_store* s, int64_t* offsets, uint64_t* keys, double* lambdas,
+                                       int64_t cap_terms) {
+  QX_REQUIRE(s && offsets && keys && lambdas, "NULL argument");
+  if (!s->exact) QX_TRY(qx_store_refresh(s));
+  memcpy(offsets, s->h_seg, sizeof(int64_t) * (size_t)(s->n_seg + 1));
+  const int64_t total = s->h_seg[s->n_seg];
+  QX_REQUIRE(cap_terms >= total, "download buffer holds %lld terms, store has %lld",
+             (long long)cap_terms, (long long)total);
+  QX_CUDA(cudaSetDevice(s->device));
+  if (total > 0) {
+    QX_CUDA(cudaMemcpyAsync(keys, s->keys[s->cur], sizeof(u64) * (size_t)total, cudaMemcpyDeviceToHost,
+                            s->stream));
+    QX_CUDA(cudaMemcpyAsync(lambdas, s->lam[s->cur], sizeof(double) * (size_t)total, cudaMemcpyDeviceToHost,
+                            s->stream));
+  }
   return QX_OK;
 }
 

@@ -307,7 +307,11 @@ def run(instructions: Sequence[Instruction], n: int, mode, eps: float = DEFAULT_
             timings["lut"] = time.perf_counter() - t0
             _walk_operators(partition, lut, is_perm, tables, w, trace, counters, mode, eager)
 
-        w.finish(trace)                  # deferred merge, queued permutations, canonical order
+        streamed = None
+        if download and before_merge is None and reduce_ranks is None:
+            streamed = _finish_streamed(w, trace, pinned)
+        if streamed is None:
+            w.finish(trace)              # deferred merge, queued permutations, canonical order
         counters["operators"] = partition.k + partition.k_prime
 
         info = {"device": store.device, **w.launch_log}
@@ -315,7 +319,7 @@ def run(instructions: Sequence[Instruction], n: int, mode, eps: float = DEFAULT_
             info["updates_per_generator"] = w.updates.tolist()
         final = None
         if download:
-            segs = store.segments(pinned)
+            segs = streamed if streamed is not None else store.segments(pinned)
             final_gens = [SimpleGenerator(n, lam, keys_to_indices(keys, n)) for lam, keys in segs]
             final = GeneratorSet(n, final_gens) if len(final_gens) == n else _Shard(n, ids, final_gens)
         else:
@@ -326,6 +330,81 @@ def run(instructions: Sequence[Instruction], n: int, mode, eps: float = DEFAULT_
     finally:
         if download:
             store.close()
+
+
+_STREAM_DEBUG = bool(__import__("os").environ.get("QX_STREAM_DEBUG"))
+STREAM_MIN_RAW = 1 << 23          # below this a single download is not worth splitting
+STREAM_SHARDS = 4
+
+
+def _finish_streamed(w: _Walker, trace, pinned: bool):
+    """Last branching operator of a run whose result goes to the host: evolve contiguous
+    generator ranges one after the other, each on a store (and CUDA stream) of its own, and
+    start every range's download as soon as its merge is done, so that the PCIe copy of one
+    range overlaps the kernels of the next.  Generators are independent (reference
+    engine.py:113-116), so the result is the same.  Returns the per-generator (lambdas, keys)
+    list, or None when the plain finish applies (no staged operator, small result)."""
+    if w.pending is None or w.staged is None or len(w.ids) < 2:
+        return None
+    counts, axes, weights = w.staged
+    raw = w.store.count_operator(counts)
+    if sum(raw) < STREAM_MIN_RAW:
+        return None
+    step, phase = w.pending
+    # contiguous ranges of about equal raw size, smallest first: its copy starts early and the
+    # heavier ranges compute underneath it
+    target = sum(raw) / STREAM_SHARDS
+    bounds, acc = [0], 0
+    for g, r in enumerate(raw):
+        acc += r
+        if acc >= target and g + 1 < len(raw):
+            bounds.append(g + 1)
+            acc = 0
+    bounds.append(len(raw))
+    ranges = sorted(zip(bounds[:-1], bounds[1:]), key=lambda ab: sum(raw[ab[0]:ab[1]]))
+    program = np.array(w.queue, dtype=np.uint32)
+    w.queue, w.queue_has_cx, w.staged, w.pending = [], False, None, None
+    t0 = time.perf_counter()
+    parts, children = {}, []
+    ranks = [0] * len(w.ids)
+    try:
+        for lo, hi in ranges:
+            child = w.store.slice(lo, hi, int(sum(raw[lo:hi]) * 1.02) + 1024)
+            children.append(child)
+            _, r = child.apply_operator_run(counts, axes, weights, program, w.eps)
+            ranks[lo:hi] = r
+            for local, v in enumerate(r):
+                if v == 0:
+                    raise NumericalCollapseError(
+                        f"all terms of generator {w.ids[lo + local]} dropped at operator step {step}"
+                    )
+            parts[lo] = (hi, child.download_async(pinned))
+            if _STREAM_DEBUG:
+                print(f"  range [{lo},{hi}) issued at {1e3 * (time.perf_counter() - t0):.2f} ms, {sum(r)} terms")
+        for child in children:
+            child.synchronize()
+            if _STREAM_DEBUG:
+                print(f"  synchronized at {1e3 * (time.perf_counter() - t0):.2f} ms")
+    finally:
+        for child in children:
+            child.close()
+    w.timings[phase] += time.perf_counter() - t0
+    w.ranks = ranks
+    w.launch_log["merges"] += 1
+    w.launch_log["branch_ops"] += 0
+    w.launch_log["streamed_ranges"] = len(ranges)
+    for slot in w.open_slots:
+        trace[slot] = list(ranks)
+    w.open_slots = []
+    if w.updates is not None and w.pending_gates:
+        w.updates += np.asarray(ranks, dtype=np.int64) * w.pending_gates
+    w.pending_gates = 0
+    w.unsorted = False
+    out = []
+    for lo in sorted(parts):
+        hi, (off, keys, lam) = parts[lo]
+        out.extend((lam[off[i]:off[i + 1]], keys[off[i]:off[i + 1]]) for i in range(hi - lo))
+    return out
 
 
 @dataclass

@@ -98,6 +98,31 @@ class DeviceStore:
         nat.check(nat.lib().qx_store_download(self._h, nat.ptr(off), nat.ptr(keys), nat.ptr(lam), total))
         return off, keys, lam
 
+    def slice(self, seg_lo: int, seg_hi: int, capacity: int = 0) -> "DeviceStore":
+        """A new store with copies of segments [seg_lo, seg_hi), on a CUDA stream of its own."""
+        child = object.__new__(DeviceStore)
+        child.n, child.n_segments, child.device = self.n, int(seg_hi) - int(seg_lo), self.device
+        child._h = C.c_void_p()
+        child._cx = self._cx
+        nat.check(nat.lib().qx_store_slice(self._h, int(seg_lo), int(seg_hi), int(capacity), C.byref(child._h)))
+        return child
+
+    def download_async(self, pinned: bool = True):
+        """Like download, but the term copies are only queued on the store's stream: the arrays
+        are valid after ``synchronize()``."""
+        off = np.zeros(self.n_segments + 1, dtype=np.int64)
+        nat.check(nat.lib().qx_store_download(self._h, nat.ptr(off), None, None, 0))
+        total = int(off[-1])
+        if pinned and total > 0:
+            buf = nat.PINNED.take(16 * total)
+            keys = buf.view(np.uint64, 0, total)
+            lam = buf.view(np.float64, 8 * total, total)
+        else:
+            keys = np.empty(total, dtype=np.uint64)
+            lam = np.empty(total, dtype=np.float64)
+        nat.check(nat.lib().qx_store_download_async(self._h, nat.ptr(off), nat.ptr(keys), nat.ptr(lam), total))
+        return off, keys, lam
+
     def segments(self, pinned: bool = False) -> list:
         """[(lambdas, keys)] per segment (views into one download)."""
         off, keys, lam = self.download(pinned)
