@@ -43,7 +43,7 @@ constexpr int kWarps = kThreads / 32;
 constexpr int kPer = 8;
 constexpr int kTileSlots = kThreads * kPer;      // 2048 slots (or sources) per tile
 constexpr int kChunk = 16;                       // sources accumulated per round of the one-group path
-constexpr int kPhiCap = 4096;                    // partial products held per round
+constexpr int kPhiCap = 2048;                    // partial products held per round
 
 // class id (1..3, the smallest input axis of the class) of input axis a+1 at digit position p
 struct ClassIds {
@@ -196,23 +196,37 @@ __global__ void k_counts_to_offsets(const u64* __restrict__ seg_count, int n_seg
 
 // ---- 3. one thread per slot ----------------------------------------------------------------
 constexpr int kMaxBlocks = 512;      // blocks of one tile in the one-group path (needs L >= 4 ...)
+constexpr int kHistPasses = 8;       // digit histograms kept per CTA (8 bits each, 64-bit keys)
+
+template <typename K> struct __align__(16) HiEntry {   // per block of the tile
+  double p;        // lambda * high weights of the group's first source
+  K word;          // output word of the high digits
+  u32 e;           // its phase exponent
+};
+template <typename K> struct __align__(16) LowEntry {  // per low branch of the group
+  K word;
+  K imx;
+  u32 e;
+  u32 pick;
+};
 
 template <typename K>
 struct GroupSmem {
   OperatorTable tb;                  // class-expanded: cnt/axis describe the class, w may hold zeros
   ImageTable<K> im;
-  K k_hi[kMaxBlocks];                // per block of the tile: output word of the high digits
-  K choice[kMaxBlocks];              //   their picks, two bits per digit position
-  unsigned char e_hi[kMaxBlocks];
+  HiEntry<K> hi[kMaxBlocks];
+  K choice[kMaxBlocks];              // picks of the high digits, two bits per digit position
   double p_hi[kPhiCap];              // [source of the round][block]: lambda * high weights
-  double low_w[kChunk][27][3];       // [source of the round][low branch][low digit]
-  K low_word[27];
-  K low_imx[27];
-  u32 low_e[27];
-  u32 low_pick[27];
+  double low_w[kChunk + 1][27][4];   // [first source | source of the round][low branch][low digit], 32-byte rows
+  LowEntry<K> low[27];
+  u32 hist[kHistPasses][QX_RADIX];   // digit counts of the kept terms (all passes of the sort)
   u64 scan[kWarps + 1];
   u64 base;
 };
+
+// digit = byte `which` of the key
+__device__ __forceinline__ u32 digit_of(u32 key, int which) { return (key >> (8 * which)) & 255u; }
+__device__ __forceinline__ u32 digit_of(u64 key, int which) { return (u32)(key >> (8 * which)) & 255u; }
 
 // K = working word type (u32 for n <= 16), KO = type of the keys written, FUSED = compose the
 // images of the Clifford run that follows (im) instead of placing the output digits.
@@ -220,14 +234,15 @@ struct GroupSmem {
 // [seg_slot[g], seg_slot[g] + kept_g) of the output: space is handed out with one atomic per tile
 // (order inside a generator is irrelevant, the sort follows; a tile-ordered compaction would
 // chain every tile to its predecessor's FINISHED sums -- 34 % of the stall samples of the first
-// version of this kernel, profiles/r01h).
+// version of this kernel, profiles/r01h).  The digit histograms of the sort that follows are
+// counted here, on the keys while they are in registers (hist[g][pass][digit]).
 template <typename K, typename KO, bool FUSED>
-__global__ void __launch_bounds__(kThreads, 3)
+__global__ void __launch_bounds__(kThreads, sizeof(K) == 8 ? 2 : 3)
 k_group_emit(const u64* __restrict__ cw, const u64* __restrict__ skey, const double* __restrict__ slam,
              const u64* __restrict__ gsrc, const u64* __restrict__ gslot, const u64* __restrict__ totals,
              const int2* __restrict__ tile_info, const int64_t* __restrict__ seg_slot, int n_seg,
              KO* __restrict__ keys_out, double* __restrict__ lam_out, u64* __restrict__ seg_count,
-             double eps, const __grid_constant__ OperatorTable tb,
+             u32* __restrict__ hist, int passes, double eps, const __grid_constant__ OperatorTable tb,
              const __grid_constant__ ImageTable<K> im) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   GroupSmem<K>& sm = *reinterpret_cast<GroupSmem<K>*>(smem_raw);
@@ -241,11 +256,13 @@ k_group_emit(const u64* __restrict__ cw, const u64* __restrict__ skey, const dou
       u32* idst = reinterpret_cast<u32*>(&sm.im);
       for (int i = tid; i < (int)(sizeof(ImageTable<K>) / 4); i += kThreads) idst[i] = isrc[i];
     }
+    for (int i = tid; i < kHistPasses * QX_RADIX; i += kThreads) (&sm.hist[0][0])[i] = 0u;
   }
   const int64_t ngroups = (int64_t)totals[0];
   const u64 total = totals[1];
   const int64_t ntiles = (int64_t)((total + kTileSlots - 1) / kTileSlots);
   int cached_group = -1;              // group whose low table is in shared memory
+  int hist_seg = -1;                  // generator the shared histogram belongs to
   LowGroup<K> lg = {};
   K cwg = 0;
   u32 magic = 0;
@@ -254,6 +271,7 @@ k_group_emit(const u64* __restrict__ cw, const u64* __restrict__ skey, const dou
     const u64 r0 = (u64)tile * kTileSlots;
     const u64 r1 = min(r0 + (u64)kTileSlots, total);
     const u32 n_out = (u32)(r1 - r0);
+    const bool full = n_out == (u32)kTileSlots;
     const int2 ti = tile_info[tile];
     const int g0 = ti.x, seg0 = ti.y;
     const u64 gs0 = gslot[g0];
@@ -268,13 +286,24 @@ k_group_emit(const u64* __restrict__ cw, const u64* __restrict__ skey, const dou
       word[k] = 0;
     }
     __syncthreads();                              // previous tile fully consumed (and tables copied)
+    if (one_seg && hist_seg != seg0) {            // the shared histogram changes generator: flush
+      if (hist_seg >= 0) {
+        for (int i = tid; i < passes * QX_RADIX; i += kThreads) {
+          const u32 c = (&sm.hist[0][0])[i];
+          if (c) atomicAdd(hist + (size_t)hist_seg * passes * QX_RADIX + i, c);
+          (&sm.hist[0][0])[i] = 0u;
+        }
+      }
+      hist_seg = seg0;
+    }
 
     bool single = gslot[g0 + 1] >= r1;
     int n_blocks = 0;
     u64 h0 = 0;
     u32 bl0 = 0;
+    const bool fresh = cached_group != g0;
     if (single) {
-      if (cached_group != g0) {
+      if (fresh) {
         cwg = (K)cw[gsrc[g0]];
         lg = low_group<K>(cwg, sm.tb);
         magic = 65536u / lg.L + 1u;               // t / L == (t * magic) >> 16 for t < 2^16 / L
@@ -294,7 +323,8 @@ k_group_emit(const u64* __restrict__ cw, const u64* __restrict__ skey, const dou
       // rest; a "block" is the L consecutive slots that share the high picks.
       const int64_t s0 = (int64_t)gsrc[g0];
       const int n_src = (int)((int64_t)gsrc[g0 + 1] - s0);
-      if (cached_group != g0 && tid < (int)lg.L) {
+      const K key0 = (K)skey[s0];
+      if (fresh && tid < (int)lg.L) {
         u32 b = tid, picks = 0;
         K w = 0;
         u32 ex = 0;
@@ -307,21 +337,25 @@ k_group_emit(const u64* __restrict__ cw, const u64* __restrict__ skey, const dou
         }
 #pragma unroll
         for (int j = 2; j >= 0; --j) {
+          double wt = 1.0;
           if (lg.bit[j] >= 0) {
             const int p = lg.bit[j] >> 1;
             const u32 ax = sm.tb.axis[p][lg.dig[j]][pick[j]];
             if (FUSED) compose<K>(w, ex, sm.im.img[p][ax - 1], sm.im.imx[p][ax - 1], sm.im.e[p][ax - 1]);
             else w |= (K)ax << lg.bit[j];
+            wt = sm.tb.w[p][(u32)((key0 >> lg.bit[j]) & 3u) - 1u][pick[j]];
           }
+          sm.low_w[0][tid][j] = wt;               // weights of the first source: all of them if n_src == 1
         }
-        sm.low_word[tid] = w;
-        sm.low_imx[tid] = (w ^ (w >> 1)) & Plane<K>::lo;
-        sm.low_e[tid] = ex & 3u;
-        sm.low_pick[tid] = picks;
+        LowEntry<K> le;
+        le.word = w;
+        le.imx = (w ^ (w >> 1)) & Plane<K>::lo;
+        le.e = ex & 3u;
+        le.pick = picks;
+        sm.low[tid] = le;
       }
       cached_group = g0;
-      // high digits of every block: picks, output word; with one source also its partial product
-      const K key0 = (K)skey[s0];
+      // high digits of every block: picks, output word, partial product of the first source
       const double lam0 = slam[s0];
       for (int e = tid; e < n_blocks; e += kThreads) {
         K h = (K)(h0 + (u64)e);
@@ -345,12 +379,14 @@ k_group_emit(const u64* __restrict__ cw, const u64* __restrict__ skey, const dou
           if (FUSED) compose<K>(out, ex, sm.im.img[bit >> 1][ax - 1], sm.im.imx[bit >> 1][ax - 1], sm.im.e[bit >> 1][ax - 1]);
           else out |= (K)ax << bit;
         }
+        HiEntry<K> he;
+        he.p = v;
+        he.word = out;
+        he.e = ex & 3u;
+        sm.hi[e] = he;
         sm.choice[e] = ch;
-        sm.k_hi[e] = out;
-        sm.e_hi[e] = (unsigned char)(ex & 3u);
-        sm.p_hi[e] = v;                            // round 0, source 0
       }
-      if (n_src > 1) __syncthreads();             // picks visible to the other sources' folds
+      __syncthreads();
       u32 eb[kPer];                               // block << 5 | low branch of my slots
 #pragma unroll
       for (int k = 0; k < kPer; ++k) {
@@ -358,67 +394,76 @@ k_group_emit(const u64* __restrict__ cw, const u64* __restrict__ skey, const dou
         const u32 e = (t * magic) >> 16;
         eb[k] = (e << 5) | (t - e * lg.L);
       }
-      const int per_round = max(1, min(kChunk, kPhiCap / n_blocks));
-      for (int c0 = 0; c0 < n_src; c0 += per_round) {
-        const int nc = min(per_round, n_src - c0);
-        if (c0 > 0) __syncthreads();              // previous round consumed
-        // partial products of the round's sources (source 0 of round 0 was folded above)
-        for (int w = tid + (c0 == 0 ? n_blocks : 0); w < nc * n_blocks; w += kThreads) {
-          const int c = w / n_blocks, e = w - c * n_blocks;
-          const K key = (K)skey[s0 + c0 + c];
-          const K ch = sm.choice[e];
-          double v = slam[s0 + c0 + c];
-          for (K m = lg.hi_mask; m;) {             // qubit 0 first
-            const int bit = KeyOps<K>::highest(m);
-            m ^= (K)1 << bit;
-            v *= sm.tb.w[bit >> 1][(u32)((key >> bit) & 3u) - 1u][(u32)(ch >> bit) & 3u];
-          }
-          sm.p_hi[c * n_blocks + e] = v;
-        }
-        for (int w = tid; w < nc * (int)lg.L; w += kThreads) {
-          const int c = w / (int)lg.L, l = w - c * (int)lg.L;
-          const K key = (K)skey[s0 + c0 + c];
-          const u32 picks = sm.low_pick[l];
-#pragma unroll
-          for (int j = 0; j < 3; ++j) {
-            double wt = 1.0;
-            if (lg.bit[j] >= 0)
-              wt = sm.tb.w[lg.bit[j] >> 1][(u32)((key >> lg.bit[j]) & 3u) - 1u][(picks >> (2 * j)) & 3u];
-            sm.low_w[c][l][j] = wt;
-          }
-        }
-        __syncthreads();
-#pragma unroll
-        for (int k = 0; k < kPer; ++k) {
-          const u32 idx = (u32)(warp * (32 * kPer) + k * 32 + lane);
-          if (idx < n_out) {
-            const u32 e = eb[k] >> 5, bl = eb[k] & 31u;
-            for (int c = 0; c < nc; ++c) {
-              // ((p_hi * w2) * w1) * w0, absent = 1.0; explicit roundings: a fused multiply-add
-              // of the last product into the sum would round differently from the reference
-              double v = sm.p_hi[c * n_blocks + e];
-              v = __dmul_rn(v, sm.low_w[c][bl][2]);
-              v = __dmul_rn(v, sm.low_w[c][bl][1]);
-              v = __dmul_rn(v, sm.low_w[c][bl][0]);
-              acc[k] = (c0 + c == 0) ? v : __dadd_rn(acc[k], v);
-            }
-          }
-        }
-      }
+      // first source: straight from the packed tables (the only source of most heavy groups)
 #pragma unroll
       for (int k = 0; k < kPer; ++k) {
         const u32 idx = (u32)(warp * (32 * kPer) + k * 32 + lane);
-        if (idx < n_out) {
+        if (full || idx < n_out) {
           const u32 e = eb[k] >> 5, bl = eb[k] & 31u;
-          K out = sm.k_hi[e];
+          const HiEntry<K> he = sm.hi[e];
+          const LowEntry<K> le = sm.low[bl];
+          const double2 w01 = *reinterpret_cast<const double2*>(&sm.low_w[0][bl][0]);
+          double v = __dmul_rn(he.p, sm.low_w[0][bl][2]);   // ((p_hi * w2) * w1) * w0, absent = 1.0
+          v = __dmul_rn(v, w01.y);
+          acc[k] = __dmul_rn(v, w01.x);
+          K out = he.word;
           if (FUSED) {
-            u32 ex = (u32)sm.e_hi[e];
-            compose<K>(out, ex, sm.low_word[bl], sm.low_imx[bl], sm.low_e[bl]);
+            u32 ex = he.e;
+            compose<K>(out, ex, le.word, le.imx, le.e);
             neg |= composed_sign<K>(out, ex) << k;
           } else {
-            out |= sm.low_word[bl];
+            out |= le.word;
           }
           word[k] = out;
+        }
+      }
+      // remaining sources of the group, kChunk (or fewer) per round
+      if (n_src > 1) {
+        const int per_round = max(1, min(kChunk, kPhiCap / n_blocks));
+        for (int c0 = 1; c0 < n_src; c0 += per_round) {
+          const int nc = min(per_round, n_src - c0);
+          __syncthreads();                          // previous round (or the first source) consumed
+          for (int w = tid; w < nc * n_blocks; w += kThreads) {
+            const int c = w / n_blocks, e = w - c * n_blocks;
+            const K key = (K)skey[s0 + c0 + c];
+            const K ch = sm.choice[e];
+            double v = slam[s0 + c0 + c];
+            for (K m = lg.hi_mask; m;) {             // qubit 0 first
+              const int bit = KeyOps<K>::highest(m);
+              m ^= (K)1 << bit;
+              v *= sm.tb.w[bit >> 1][(u32)((key >> bit) & 3u) - 1u][(u32)(ch >> bit) & 3u];
+            }
+            sm.p_hi[c * n_blocks + e] = v;
+          }
+          for (int w = tid; w < nc * (int)lg.L; w += kThreads) {
+            const int c = w / (int)lg.L, l = w - c * (int)lg.L;
+            const K key = (K)skey[s0 + c0 + c];
+            const u32 picks = sm.low[l].pick;
+#pragma unroll
+            for (int j = 0; j < 3; ++j) {
+              double wt = 1.0;
+              if (lg.bit[j] >= 0)
+                wt = sm.tb.w[lg.bit[j] >> 1][(u32)((key >> lg.bit[j]) & 3u) - 1u][(picks >> (2 * j)) & 3u];
+              sm.low_w[1 + c][l][j] = wt;            // row 0 stays the first source's (cached per group)
+            }
+          }
+          __syncthreads();
+#pragma unroll
+          for (int k = 0; k < kPer; ++k) {
+            const u32 idx = (u32)(warp * (32 * kPer) + k * 32 + lane);
+            if (full || idx < n_out) {
+              const u32 e = eb[k] >> 5, bl = eb[k] & 31u;
+              for (int c = 0; c < nc; ++c) {
+                // explicit roundings: a fused multiply-add of the last product into the sum would
+                // round differently from the reference
+                double v = sm.p_hi[c * n_blocks + e];
+                v = __dmul_rn(v, sm.low_w[1 + c][bl][2]);
+                v = __dmul_rn(v, sm.low_w[1 + c][bl][1]);
+                v = __dmul_rn(v, sm.low_w[1 + c][bl][0]);
+                acc[k] = __dadd_rn(acc[k], v);
+              }
+            }
+          }
         }
       }
     } else {
@@ -477,7 +522,7 @@ k_group_emit(const u64* __restrict__ cw, const u64* __restrict__ skey, const dou
     for (int k = 0; k < kPer; ++k) {
       const u32 idx = (u32)(warp * (32 * kPer) + k * 32 + lane);
       if (neg & (1u << k)) acc[k] = -acc[k];     // sign flips are exact
-      const bool kept = idx < n_out && fabs(acc[k]) >= eps;
+      const bool kept = (full || idx < n_out) && fabs(acc[k]) >= eps;
       if (kept) kept_bits |= 1u << k;
       const u32 votes = __ballot_sync(QX_FULL_MASK, kept);
       pre[k] = running + __popc(votes & lanemask_lt());
@@ -488,6 +533,33 @@ k_group_emit(const u64* __restrict__ cw, const u64* __restrict__ skey, const dou
       u64 warp_excl = block_exclusive_sum<u64>(lane == 0 ? (u64)running : 0ull, sm.scan, tile_total);
       warp_excl = __shfl_sync(QX_FULL_MASK, warp_excl, 0);
       if (tid == 0) sm.base = (u64)seg_slot[seg0] + atomicAdd(seg_count + seg0, tile_total);
+      // digit counts: the two low bytes one shared atomic each; everything above them changes
+      // slowly along the slots (high digits of the word), so a thread counts runs of equal
+      // upper parts in a register and flushes a run with one atomic per pass
+      {
+        KO run_key = 0;
+        u32 run_cnt = 0;
+#pragma unroll
+        for (int k = 0; k < kPer; ++k) {
+          if (kept_bits & (1u << k)) {
+            const KO key = (KO)word[k];
+            atomicAdd(&sm.hist[0][digit_of(key, 0)], 1u);
+            if (passes > 1) atomicAdd(&sm.hist[1][digit_of(key, 1)], 1u);
+            if (passes > 2) {
+              if (run_cnt && (key >> 16) == (run_key >> 16)) {
+                ++run_cnt;
+              } else {
+                if (run_cnt)
+                  for (int p = 2; p < passes; ++p) atomicAdd(&sm.hist[p][digit_of(run_key, p)], run_cnt);
+                run_key = key;
+                run_cnt = 1;
+              }
+            }
+          }
+        }
+        if (run_cnt)
+          for (int p = 2; p < passes; ++p) atomicAdd(&sm.hist[p][digit_of(run_key, p)], run_cnt);
+      }
       __syncthreads();
       const int64_t base = (int64_t)(sm.base + warp_excl);
 #pragma unroll
@@ -506,10 +578,20 @@ k_group_emit(const u64* __restrict__ cw, const u64* __restrict__ skey, const dou
           const int64_t r = (int64_t)(r0 + (u32)(warp * (32 * kPer) + k * 32 + lane));
           const int g = segment_of(seg_slot, n_seg, r);
           const int64_t pos = seg_slot[g] + (int64_t)atomicAdd(seg_count + g, 1ull);
-          st_stream(keys_out + pos, (KO)word[k]);
+          const KO key = (KO)word[k];
+          st_stream(keys_out + pos, key);
           st_stream(lam_out + pos, acc[k]);
+          for (int p = 0; p < passes; ++p)
+            atomicAdd(hist + ((size_t)g * passes + p) * QX_RADIX + digit_of(key, p), 1u);
         }
       }
+    }
+  }
+  __syncthreads();
+  if (hist_seg >= 0) {
+    for (int i = tid; i < passes * QX_RADIX; i += kThreads) {
+      const u32 c = (&sm.hist[0][0])[i];
+      if (c) atomicAdd(hist + (size_t)hist_seg * passes * QX_RADIX + i, c);
     }
   }
 }
@@ -517,7 +599,7 @@ k_group_emit(const u64* __restrict__ cw, const u64* __restrict__ skey, const dou
 template <typename K, typename KO, bool FUSED>
 int launch_group_emit(qx_store* s, int64_t tiles, const u64* cw, const u64* skey, const double* slam,
                       const u64* gsrc, const u64* gslot, const u64* totals, const int2* tile_info,
-                      const int64_t* seg_slot, int out, u64* seg_count, double eps,
+                      const int64_t* seg_slot, int out, u64* seg_count, u32* hist, int passes, double eps,
                       const OperatorTable& tb, const ImageTable<K>& im) {
   static int per_sm = 0;
   if (per_sm == 0) {
@@ -530,7 +612,7 @@ int launch_group_emit(qx_store* s, int64_t tiles, const u64* cw, const u64* skey
   const int grid = (int)std::min<int64_t>(tiles, (int64_t)s->sm_count * per_sm);
   k_group_emit<K, KO, FUSED><<<grid, kThreads, sizeof(GroupSmem<K>), s->stream>>>(
       cw, skey, slam, gsrc, gslot, totals, tile_info, seg_slot, s->n_seg,
-      reinterpret_cast<KO*>(s->keys[out]), s->lam[out], seg_count, eps, tb, im);
+      reinterpret_cast<KO*>(s->keys[out]), s->lam[out], seg_count, hist, passes, eps, tb, im);
   QX_CUDA(cudaGetLastError());
   return QX_OK;
 }
@@ -687,14 +769,17 @@ int qx_dense_operator_step(qx_store* s, const OperatorTable& nz, const uint32_t*
   const int out = s->cur ^ 1;
 
   const int64_t tiles = std::max<int64_t>(1, (total + kTileSlots - 1) / kTileSlots);
-  const int64_t bytes2 = padded(8 * tiles) + padded(8 * (int64_t)n_seg);
+  const int passes = std::min(qxm::kMaxPasses, (2 * s->n_qubits + QX_RADIX_BITS - 1) / QX_RADIX_BITS);
+  const int64_t hist_words = (int64_t)n_seg * passes * QX_RADIX;
+  const int64_t bytes2 = padded(8 * tiles) + padded(8 * (int64_t)n_seg) + padded(4 * hist_words);
   void* block2 = nullptr;
   QX_TRY(qx_dev_alloc(&block2, bytes2, s->stream, s->device));
   Release rel2{block2, s->stream};
   cur = reinterpret_cast<char*>(block2);
   int2* tile_info = carve<int2>(cur, tiles);
   u64* seg_count = carve<u64>(cur, n_seg);
-  QX_CUDA(cudaMemsetAsync(seg_count, 0, sizeof(u64) * (size_t)n_seg, s->stream));
+  u32* hist = carve<u32>(cur, hist_words);
+  QX_CUDA(cudaMemsetAsync(seg_count, 0, (size_t)(padded(8 * (int64_t)n_seg) + 4 * hist_words), s->stream));
   k_tile_groups<<<(unsigned)((tiles + 255) / 256), 256, 0, s->stream>>>(gslot, totals, seg_slot, n_seg, tile_info, tiles);
   qx_count_launches(1);
   QX_CUDA(cudaGetLastError());
@@ -709,7 +794,7 @@ int qx_dense_operator_step(qx_store* s, const OperatorTable& nz, const uint32_t*
       memset(&im, 0, sizeof(im));
       if (n_ops > 0) fill_images_u32(s->n_qubits, program, n_ops, cx_c, cx_t, cx_s, &im);
 #define QX_GE(KO, F) launch_group_emit<u32, KO, F>(s, tiles, cwb[sorted], skey, slam, gsrc, gslot, totals, \
-                                                   tile_info, seg_slot, out, seg_count, eps, ct, im)
+                                                   tile_info, seg_slot, out, seg_count, hist, passes, eps, ct, im)
       if (n_ops > 0 && narrow) QX_TRY((QX_GE(u32, true)));
       else if (n_ops > 0) QX_TRY((QX_GE(u64, true)));
       else if (narrow) QX_TRY((QX_GE(u32, false)));
@@ -721,10 +806,10 @@ int qx_dense_operator_step(qx_store* s, const OperatorTable& nz, const uint32_t*
       if (n_ops > 0) {
         fill_images_u64(s->n_qubits, program, n_ops, cx_c, cx_t, cx_s, &im);
         QX_TRY((launch_group_emit<u64, u64, true>(s, tiles, cwb[sorted], skey, slam, gsrc, gslot, totals,
-                                                  tile_info, seg_slot, out, seg_count, eps, ct, im)));
+                                                  tile_info, seg_slot, out, seg_count, hist, passes, eps, ct, im)));
       } else {
         QX_TRY((launch_group_emit<u64, u64, false>(s, tiles, cwb[sorted], skey, slam, gsrc, gslot, totals,
-                                                   tile_info, seg_slot, out, seg_count, eps, ct, im)));
+                                                   tile_info, seg_slot, out, seg_count, hist, passes, eps, ct, im)));
       }
     }
   }
@@ -748,8 +833,8 @@ int qx_dense_operator_step(qx_store* s, const OperatorTable& nz, const uint32_t*
   mb.ub_total = s->ub_total;
   mb.ub_seg = s->ub_seg;
   // the kept terms of generator g sit at its slot offset; the first pass reads them from there
-  if (narrow) QX_TRY((qxm::merge_large<double, u32>(s, mb, eps, QX_K_REDUCE, false, QX_K_SORT_PASS, QX_K_SORT_HIST, seg_slot)));
-  else QX_TRY((qxm::merge_large<double, u64>(s, mb, eps, QX_K_REDUCE, false, QX_K_SORT_PASS, QX_K_SORT_HIST, seg_slot)));
+  if (narrow) QX_TRY((qxm::merge_large<double, u32>(s, mb, eps, QX_K_REDUCE, false, QX_K_SORT_PASS, QX_K_SORT_HIST, seg_slot, hist)));
+  else QX_TRY((qxm::merge_large<double, u64>(s, mb, eps, QX_K_REDUCE, false, QX_K_SORT_PASS, QX_K_SORT_HIST, seg_slot, hist)));
   s->cur = mb.cur;
   return QX_OK;
 }

@@ -753,7 +753,7 @@ int dispatch_pass(int variant, QxArena* ar, MergeBuffers<V>& mb, int cur, int64_
 template <typename V, typename K = u64>
 int merge_large(QxArena* ar, MergeBuffers<V>& mb, double eps, int cls_reduce, bool do_reduce = true,
                 int cls_pass = QX_K_SORT_PASS, int cls_hist = QX_K_SORT_HIST,
-                const int64_t* first_base_in = nullptr) {
+                const int64_t* first_base_in = nullptr, const u32* pre_hist = nullptr) {
   const int n_seg = mb.n_seg;
   const int passes = std::min(kMaxPasses, (2 * ar->n_qubits + QX_RADIX_BITS - 1) / QX_RADIX_BITS);
   if (mb.ub_seg >= (int64_t)kFlagVal)
@@ -790,7 +790,12 @@ int merge_large(QxArena* ar, MergeBuffers<V>& mb, double eps, int cls_reduce, bo
       mb.seg[cur], n_seg, tile_prefix, info, tile_terms);
   qx_count_launches(2);
   QX_CUDA(cudaGetLastError());
-  {
+  if (pre_hist) {
+    // the producer of the keys counted their digits already (dense.cu); its buffer is scanned
+    // in place and outlives the passes (no device-to-device copy: a copy engine may be busy
+    // with another store's download)
+    hist = const_cast<u32*>(pre_hist);
+  } else {
     const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(tiles_ub, (int64_t)ar->sm_count * 4));
     QxProfileScope prof(cls_hist, ar->stream, (double)sizeof(K) * (double)mb.ub_total);
     k_sort_hist<K><<<grid, kSortThreads, 0, ar->stream>>>(reinterpret_cast<const K*>(mb.keys[cur]),
