@@ -196,6 +196,7 @@ __global__ void k_counts_to_offsets(const u64* __restrict__ seg_count, int n_seg
 
 // ---- 3. one thread per slot ----------------------------------------------------------------
 constexpr int kMaxBlocks = 512;      // blocks of one tile in the one-group path (needs L >= 4 ...)
+constexpr int kRows = 9;             // one-group path: rows of A = L * (256 / L) slots, ceil(2048 / 243) = 9
 constexpr int kHistPasses = 8;       // digit histograms kept per CTA (8 bits each, 64-bit keys)
 
 template <typename K> struct __align__(16) HiEntry {   // per block of the tile
@@ -277,11 +278,16 @@ k_group_emit(const u64* __restrict__ cw, const u64* __restrict__ skey, const dou
     const u64 gs0 = gslot[g0];
     const bool one_seg = (u64)seg_slot[seg0 + 1] >= r1;
 
-    double acc[kPer];
-    K word[kPer];
+    // my slots of the tile: slot_of(k), k < kRows.  One-group path: row k, column tid of rows of
+    // A = L * (256 / L) slots, so that a thread keeps ONE low branch for the whole tile (its word,
+    // phase and weights stay in registers); per-slot path: warp-contiguous, eight per thread.
+    double acc[kRows];
+    K word[kRows];
     u32 neg = 0;                                  // bit k: the composed word carries a minus sign
+    u32 live = 0;                                 // bit k: slot k of mine exists
+    u32 row_stride = 32, slot0 = (u32)(warp * (32 * kPer) + lane);
 #pragma unroll
-    for (int k = 0; k < kPer; ++k) {
+    for (int k = 0; k < kRows; ++k) {
       acc[k] = 0.0;
       word[k] = 0;
     }
@@ -308,10 +314,12 @@ k_group_emit(const u64* __restrict__ cw, const u64* __restrict__ skey, const dou
         lg = low_group<K>(cwg, sm.tb);
         magic = 65536u / lg.L + 1u;               // t / L == (t * magic) >> 16 for t < 2^16 / L
       }
-      const u64 b0 = r0 - gs0;
-      h0 = b0 / lg.L;
-      bl0 = (u32)(b0 - h0 * lg.L);
-      n_blocks = (int)((bl0 + n_out - 1u) / lg.L + 1u);
+      // a group of a <= 16-qubit system has at most 3^16 < 2^32 slots: divide in the word's width
+      // (a 64-bit divide is ~100 instructions and every thread of the tile would run it)
+      const K b0 = (K)(r0 - gs0);
+      h0 = (u64)(b0 / (K)lg.L);
+      bl0 = (u32)(b0 - (K)h0 * (K)lg.L);
+      n_blocks = (int)(((bl0 + n_out - 1u) * magic >> 16) + 1u);
       if (n_blocks > kMaxBlocks) {                // tiny low group: take the per-slot path
         single = false;
         cached_group = -1;
@@ -387,34 +395,41 @@ k_group_emit(const u64* __restrict__ cw, const u64* __restrict__ skey, const dou
         sm.choice[e] = ch;
       }
       __syncthreads();
-      u32 eb[kPer];                               // block << 5 | low branch of my slots
+      // my column: low branch bl and first block e0; row k adds bpr blocks
+      const u32 bpr = (u32)kThreads / lg.L;       // blocks per row
+      const u32 A = bpr * lg.L;                   // slots per row (243 for L = 27)
+      const u32 t0 = bl0 + (u32)tid;
+      const u32 e0 = (t0 * magic) >> 16;
+      const u32 bl = t0 - e0 * lg.L;
+      row_stride = A;
+      slot0 = (u32)tid;
+      if ((u32)tid < A) {
 #pragma unroll
-      for (int k = 0; k < kPer; ++k) {
-        const u32 t = bl0 + (u32)(warp * (32 * kPer) + k * 32 + lane);
-        const u32 e = (t * magic) >> 16;
-        eb[k] = (e << 5) | (t - e * lg.L);
+        for (int k = 0; k < kRows; ++k)
+          if ((u32)k * A + (u32)tid < n_out) live |= 1u << k;
       }
-      // first source: straight from the packed tables (the only source of most heavy groups)
+      // first source: low branch in registers, one packed load per slot
+      {
+        const LowEntry<K> le = sm.low[bl];
+        const double2 w01 = *reinterpret_cast<const double2*>(&sm.low_w[0][bl][0]);
+        const double w2 = sm.low_w[0][bl][2];
 #pragma unroll
-      for (int k = 0; k < kPer; ++k) {
-        const u32 idx = (u32)(warp * (32 * kPer) + k * 32 + lane);
-        if (full || idx < n_out) {
-          const u32 e = eb[k] >> 5, bl = eb[k] & 31u;
-          const HiEntry<K> he = sm.hi[e];
-          const LowEntry<K> le = sm.low[bl];
-          const double2 w01 = *reinterpret_cast<const double2*>(&sm.low_w[0][bl][0]);
-          double v = __dmul_rn(he.p, sm.low_w[0][bl][2]);   // ((p_hi * w2) * w1) * w0, absent = 1.0
-          v = __dmul_rn(v, w01.y);
-          acc[k] = __dmul_rn(v, w01.x);
-          K out = he.word;
-          if (FUSED) {
-            u32 ex = he.e;
-            compose<K>(out, ex, le.word, le.imx, le.e);
-            neg |= composed_sign<K>(out, ex) << k;
-          } else {
-            out |= le.word;
+        for (int k = 0; k < kRows; ++k) {
+          if (live & (1u << k)) {
+            const HiEntry<K> he = sm.hi[e0 + (u32)k * bpr];
+            double v = __dmul_rn(he.p, w2);        // ((p_hi * w2) * w1) * w0, absent = 1.0
+            v = __dmul_rn(v, w01.y);
+            acc[k] = __dmul_rn(v, w01.x);
+            K out = he.word;
+            if (FUSED) {
+              u32 ex = he.e;
+              compose<K>(out, ex, le.word, le.imx, le.e);
+              neg |= composed_sign<K>(out, ex) << k;
+            } else {
+              out |= le.word;
+            }
+            word[k] = out;
           }
-          word[k] = out;
         }
       }
       // remaining sources of the group, kChunk (or fewer) per round
@@ -448,18 +463,18 @@ k_group_emit(const u64* __restrict__ cw, const u64* __restrict__ skey, const dou
             }
           }
           __syncthreads();
+          for (int c = 0; c < nc; ++c) {
+            const double2 w01 = *reinterpret_cast<const double2*>(&sm.low_w[1 + c][bl][0]);
+            const double w2 = sm.low_w[1 + c][bl][2];
+            const double* ph = sm.p_hi + c * n_blocks + e0;
 #pragma unroll
-          for (int k = 0; k < kPer; ++k) {
-            const u32 idx = (u32)(warp * (32 * kPer) + k * 32 + lane);
-            if (full || idx < n_out) {
-              const u32 e = eb[k] >> 5, bl = eb[k] & 31u;
-              for (int c = 0; c < nc; ++c) {
+            for (int k = 0; k < kRows; ++k) {
+              if (live & (1u << k)) {
                 // explicit roundings: a fused multiply-add of the last product into the sum would
                 // round differently from the reference
-                double v = sm.p_hi[c * n_blocks + e];
-                v = __dmul_rn(v, sm.low_w[1 + c][bl][2]);
-                v = __dmul_rn(v, sm.low_w[1 + c][bl][1]);
-                v = __dmul_rn(v, sm.low_w[1 + c][bl][0]);
+                double v = __dmul_rn(ph[(u32)k * bpr], w2);
+                v = __dmul_rn(v, w01.y);
+                v = __dmul_rn(v, w01.x);
                 acc[k] = __dadd_rn(acc[k], v);
               }
             }
@@ -472,6 +487,7 @@ k_group_emit(const u64* __restrict__ cw, const u64* __restrict__ skey, const dou
       for (int k = 0; k < kPer; ++k) {
         const u32 idx = (u32)(warp * (32 * kPer) + k * 32 + lane);
         if (idx >= n_out) continue;
+        live |= 1u << k;
         const u64 r = r0 + idx;
         int64_t lo = g0, hi = min(ngroups, (int64_t)g0 + (int64_t)n_out + 1);   // gslot[lo] <= r < gslot[hi]
         while (hi - lo > 1) {
@@ -516,13 +532,12 @@ k_group_emit(const u64* __restrict__ cw, const u64* __restrict__ skey, const dou
     }
 
     // ---- drop rule and write-out
-    u32 pre[kPer];
+    u32 pre[kRows];
     u32 kept_bits = 0, running = 0;
 #pragma unroll
-    for (int k = 0; k < kPer; ++k) {
-      const u32 idx = (u32)(warp * (32 * kPer) + k * 32 + lane);
+    for (int k = 0; k < kRows; ++k) {
       if (neg & (1u << k)) acc[k] = -acc[k];     // sign flips are exact
-      const bool kept = (full || idx < n_out) && fabs(acc[k]) >= eps;
+      const bool kept = (live & (1u << k)) && fabs(acc[k]) >= eps;
       if (kept) kept_bits |= 1u << k;
       const u32 votes = __ballot_sync(QX_FULL_MASK, kept);
       pre[k] = running + __popc(votes & lanemask_lt());
@@ -540,7 +555,7 @@ k_group_emit(const u64* __restrict__ cw, const u64* __restrict__ skey, const dou
         KO run_key = 0;
         u32 run_cnt = 0;
 #pragma unroll
-        for (int k = 0; k < kPer; ++k) {
+        for (int k = 0; k < kRows; ++k) {
           if (kept_bits & (1u << k)) {
             const KO key = (KO)word[k];
             atomicAdd(&sm.hist[0][digit_of(key, 0)], 1u);
@@ -563,7 +578,7 @@ k_group_emit(const u64* __restrict__ cw, const u64* __restrict__ skey, const dou
       __syncthreads();
       const int64_t base = (int64_t)(sm.base + warp_excl);
 #pragma unroll
-      for (int k = 0; k < kPer; ++k) {
+      for (int k = 0; k < kRows; ++k) {
         if (kept_bits & (1u << k)) {
           const int64_t pos = base + pre[k];
           st_stream(keys_out + pos, (KO)word[k]);
@@ -573,9 +588,9 @@ k_group_emit(const u64* __restrict__ cw, const u64* __restrict__ skey, const dou
     } else {
       // the tile crosses a generator boundary (only tiny generators): one atomic per kept term
 #pragma unroll 1
-      for (int k = 0; k < kPer; ++k) {
+      for (int k = 0; k < kRows; ++k) {
         if (kept_bits & (1u << k)) {
-          const int64_t r = (int64_t)(r0 + (u32)(warp * (32 * kPer) + k * 32 + lane));
+          const int64_t r = (int64_t)(r0 + slot0 + (u32)k * row_stride);
           const int g = segment_of(seg_slot, n_seg, r);
           const int64_t pos = seg_slot[g] + (int64_t)atomicAdd(seg_count + g, 1ull);
           const KO key = (KO)word[k];

@@ -67,8 +67,19 @@ def create_lut_1q(partition, workers=None) -> np.ndarray:
     lut[:] = np.eye(3)
     for ki, bucket in enumerate(partition.u_groups):
         for wire, gates in bucket.items():
-            lut[ki, wire] = compose_block(gates)
+            # cells made of fixed gates only (most cells of a Clifford+T circuit) recur with few
+            # distinct gate sequences: compose each sequence once, with the same numpy chain
+            names = tuple(g.gate for g in gates)
+            block = _FIXED_BLOCKS.get(names)
+            if block is None:
+                block = compose_block(gates)
+                if all(name in _FIXED for name in names) and len(_FIXED_BLOCKS) < 65536:
+                    _FIXED_BLOCKS[names] = block
+            lut[ki, wire] = block
     return lut
+
+
+_FIXED_BLOCKS: dict = {}
 
 
 # CX tables indexed [control axis, target axis] (reference lut.py:108-134).

@@ -4,7 +4,7 @@ import collections, csv, io, json, os, subprocess, sys
 tag = sys.argv[1]
 src = "gpurun_out"
 out = [f"# {tag}: ncu evidence (tools/ncu_round.sh {tag})\n"]
-rows = [r for r in csv.reader(open(f"{src}/{tag}_launches_c4_16_2.csv")) if len(r) > 5 and r[0].isdigit()]
+rows = [r for r in csv.reader(open(f"{src}/{tag}_launches_c4_xyz_16_2.csv")) if len(r) > 5 and r[0].isdigit()]
 agg = collections.OrderedDict()
 for r in rows:
     a = agg.setdefault(r[4].split("(")[0], [0, 0.0])
@@ -21,15 +21,16 @@ want = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum
         "sm__inst_executed_pipe_alu.avg.pct_of_peak_sustained_active", "smsp__inst_executed.sum"]
 traffic = {}
 for name in sorted(os.listdir(src)):
-    if not (name.startswith(tag + "_k_") and name.endswith(".ncu-rep")):
+    if not (name.startswith(tag + "_") and name.endswith(".ncu-rep")):
         continue
     txt = subprocess.run(["ncu", "-i", f"{src}/{name}", "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     rr = list(csv.reader(io.StringIO(txt)))
     if len(rr) < 3:
         continue
     hdr, units, r = rr[0], rr[1], rr[2]
-    wl = "xyz_chain(16,2)" if "16_2" in name else "xyz_chain(14,2)"
-    out.append(f"\n## {name[len(tag) + 1:-8]} ({wl} v3, ncu --set full, first captured launch): {r[hdr.index('Kernel Name')][:70]}\n")
+    v1 = name.startswith(tag + "_v1_")
+    wl = "xyz_chain(14,2) v1" if v1 else "xyz_chain(16,2) v3"
+    out.append(f"\n## {name[len(tag) + 1:-8]} ({wl}, ncu --set full, first captured launch): {r[hdr.index('Kernel Name')][:70]}\n")
     for w in want:
         if w in hdr:
             out.append(f"{w:78s} {r[hdr.index(w)]:>16s} {units[hdr.index(w)]}\n")
@@ -41,7 +42,7 @@ for name in sorted(os.listdir(src)):
             except ValueError:
                 pass
     out.append("stalls (warps per issue): " + ", ".join(f"{n}={v:.2f}" for v, n in sorted(stalls, reverse=True)[:6]) + "\n")
-    if "16_2" in name:
+    if "k_onesweep" in name and not v1:
         def gb(col):
             v, u = float(r[hdr.index(col)]), units[hdr.index(col)]
             return v * {"Gbyte": 1e9, "Mbyte": 1e6, "Kbyte": 1e3, "byte": 1}[u]

@@ -1,25 +1,24 @@
 #!/bin/bash
-# ncu evidence for one round: launch list at full size + full captures of the hot kernels at (14,2)
-R=${1:-r01}
+# ncu evidence for one round: launch list of the bench step + full captures of its hot kernels
+R=${1:-r01h}
+W=${2:-c4_xyz_16_2}
 mkdir -p gpurun_out
-ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/${R}_launches_c4_16_2.csv \
-    python tools/profile_step.py --workload c4_xyz_16_2 --mode v3 --warmup 1 --steps 1 > gpurun_out/${R}_launches.log 2>&1
-for k in k_onesweep k_expand_emit k_reduce k_clifford k_sort_hist; do
-  case $k in
-    k_onesweep) skip=4; cnt=2;;        # 4 passes per step: skip the warm-up step
-    k_expand_emit|k_clifford) skip=3; cnt=1;;   # 2 per step, the second one is the big one
-    k_reduce) skip=1; cnt=1;;
-    k_sort_hist) skip=1; cnt=1;;
-    *) skip=2; cnt=1;;
-  esac
-  timeout 900 ncu --set full --clock-control none --import-source on -k regex:$k -s $skip -c $cnt -f \
-      -o gpurun_out/${R}_${k} python tools/profile_step.py --workload c4_xyz_14_2 --mode v3 --warmup 1 --steps 1 \
-      > gpurun_out/${R}_${k}.log 2>&1
-  echo "$k rc=$?"
+ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/${R}_launches_${W}.csv \
+    python tools/profile_step.py --workload $W --mode v3 --warmup 1 --steps 1 > gpurun_out/${R}_launches.log 2>&1
+# the measured step is the second one: skip the launches of the warm-up step
+for spec in "k_onesweep 5 1" "k_group_emit 1 1" "k_group_scan 1 1" "k_small_merge 2 1"; do
+  set -- $spec
+  timeout 1200 ncu --set full --clock-control none --import-source on -k regex:$1 -s $2 -c $3 -f \
+      -o gpurun_out/${R}_$1 python tools/profile_step.py --workload $W --mode v3 --warmup 1 --steps 1 \
+      > gpurun_out/${R}_$1.log 2>&1
+  echo "$1 rc=$?"
 done
-# traffic of the dominant kernel at the bench workload itself (first pass of the measured step)
-timeout 1200 ncu --set full --clock-control none --import-source on -k regex:k_onesweep -s 4 -c 1 -f \
-    -o gpurun_out/${R}_k_onesweep_16_2 python tools/profile_step.py --workload c4_xyz_16_2 --mode v3 --warmup 1 --steps 1 \
-    > gpurun_out/${R}_k_onesweep_16_2.log 2>&1
-echo "onesweep@16_2 rc=$?"
+# the kernels of the gate-by-gate mode (v1) on a mid-size point of the ladder
+for spec in "k_clifford 2 1" "k_split 40 1" "k_reduce 40 1" "k_sort_hist 40 1"; do
+  set -- $spec
+  timeout 1200 ncu --set full --clock-control none --import-source on -k regex:$1 -s $2 -c $3 -f \
+      -o gpurun_out/${R}_v1_$1 python tools/profile_step.py --workload c4_xyz_14_2 --mode v1 --warmup 0 --steps 1 \
+      > gpurun_out/${R}_v1_$1.log 2>&1
+  echo "v1 $1 rc=$?"
+done
 ls -la gpurun_out | tail -20
