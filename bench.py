@@ -20,8 +20,12 @@ any exact method).
   cpu_baseline  the numpy oracle port on the host cores over a bounded sample (a subset of the
             same circuit's generators -- they evolve independently), same unit
 
-N > 1 (torchrun): generators are sharded over ranks (LPT on rank), no data-path collective; the
-only NCCL traffic is the barrier and the max/sum of scalars.  --impl reference runs the CPU arm.
+N > 1 (torchrun), default --scaling weak: every rank evolves one whole circuit instance of the
+workload (same ansatz and shape, its own rotation angles), so per-GPU work is fixed and value is
+the sum of the ranks' update counts over the slowest rank's time.  --scaling strong: ONE circuit,
+its generators sharded over the ranks (LPT on rank; they evolve independently).  Either way there
+is no data-path collective; the only NCCL traffic is the barrier and the max/sum of scalars.
+--impl reference runs the CPU arm.
 """
 
 from __future__ import annotations
@@ -176,11 +180,11 @@ def run_reference(args, updates_per_gen):
 # ------------------------------------------------------------------------------------------
 # GPU arm
 # ------------------------------------------------------------------------------------------
-def count_updates_gpu(name, device):
+def count_updates_gpu(name, device, instance=0):
     """v1-defined update count per generator, measured with the GPU's own v1 mode (untimed)."""
     import paper_2505_03307_b200 as qx
 
-    n, gates = workloads.build(name)
+    n, gates = workloads.build(name, instance)
     rep = qx.run(gates, n, "v1", device=device, download=False)
     rep.device["store"].close()
     return rep.device["updates_per_generator"], rep.rank_trace[-1]
@@ -211,13 +215,20 @@ def run_ours(args):
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     device = local
     torch.cuda.set_device(device)
-    n, gates = workloads.build(args.workload)
+    weak = args.scaling == "weak" and world > 1
+    instance = rank if weak else 0
+    n, gates = workloads.build(args.workload, instance)
 
     # untimed: update counts (v1 semantics) and final ranks for LPT sharding
-    updates_per_gen, final_ranks = count_updates_gpu(args.workload, device)
+    updates_per_gen, final_ranks = count_updates_gpu(args.workload, device, instance)
     total_updates = float(sum(updates_per_gen))
-    shards = lpt_shards(final_ranks, world)
-    mine = shards[rank]
+    if weak:
+        mine = list(range(n))                      # my own circuit instance, all of its generators
+        t = torch.tensor([total_updates], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.SUM)
+        total_updates = float(t.item())
+    else:
+        mine = lpt_shards(final_ranks, world)[rank]
     my_cap = int(sum(final_ranks[g] for g in mine) * 2.6) + 1024
 
     def barrier():
@@ -317,10 +328,12 @@ def run_ours(args):
     line = {
         "metric": "term_gate_updates_per_s", "value": value, "unit": "updates/s", "n_gpus": world,
         "steps": args.steps, "warmup": max(args.warmup, 3), "ms_per_step": ms_per_step,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "higher_is_better": True, "scaling": "weak" if (weak or world == 1) else "strong", "vs_baseline": None,
+        "dtype": "f64", "data": "synthetic",
         "config": {"workload": args.workload, "mode": args.mode, "qubits": n, "gates": len(gates),
                    "term_gate_updates": total_updates, "final_terms": int(sum(final_ranks)),
-                   "parallelism": f"generator shards x{world} (LPT on rank)",
+                   "parallelism": (f"{world} circuit instance(s), one per GPU, all generators of an instance on its GPU"
+                                   if (weak or world == 1) else f"one circuit, generator shards x{world} (LPT on rank)"),
                    "l2": "inputs larger than L2: every pass streams 2-5 GB per GPU, L2 is 126 MB"},
         "e2e": {"value": total_updates / e2e_s, "unit": "updates/s", "ms_per_step": e2e_s * 1e3,
                 "h2d_bytes_per_step": table_bytes(n, gates), "d2h_bytes_per_step": d2h},
@@ -343,6 +356,8 @@ def main():
     ap.add_argument("--workload", default=DEFAULT_WORKLOAD)
     ap.add_argument("--mode", default="v3")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    ap.add_argument("--scaling", default="weak", choices=("weak", "strong"),
+                    help="N > 1: one circuit instance per GPU (weak) or one circuit's generators sharded (strong)")
     args = ap.parse_args()
     if args.impl == "reference":
         # update counts of the sample come from the fixture table (no GPU on this arm)

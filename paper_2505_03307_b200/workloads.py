@@ -124,9 +124,10 @@ def config3() -> tuple:
     return n, gen_ghz(n) + gen_random(n, 984, np.random.default_rng(3), CLIFFORD_POOL)
 
 
-def config4(n: int = 16, layers: int = 2) -> tuple:
-    """C4 ladder point: xyz_chain(n, layers, repeats=1, rng=4). (16, 2) is the largest-rank config."""
-    return n, gen_xyz_chain(n, layers, 1, rng=4)
+def config4(n: int = 16, layers: int = 2, seed: int = 4) -> tuple:
+    """C4 ladder point: xyz_chain(n, layers, repeats=1, rng=4). (16, 2) is the largest-rank config.
+    ``seed`` other than 4 draws another instance of the same ansatz (multi-GPU weak scaling)."""
+    return n, gen_xyz_chain(n, layers, 1, rng=seed)
 
 
 def config5() -> tuple:
@@ -148,8 +149,12 @@ WORKLOADS = {
 }
 
 
-def build(name: str) -> tuple:
-    """(n, instructions) of a named workload."""
+def build(name: str, instance: int = 0) -> tuple:
+    """(n, instructions) of a named workload.  ``instance`` > 0 draws another circuit of the same
+    family and shape (config-4 ladder only: other rotation angles, same gates and wires)."""
+    if instance and name.startswith("c4_xyz_"):
+        n, layers = (int(v) for v in name.split("_")[2:4])
+        return config4(n, layers, seed=4 + 1000 * instance)
     try:
         return WORKLOADS[name]()
     except KeyError:
