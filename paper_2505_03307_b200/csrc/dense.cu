@@ -196,6 +196,10 @@ __global__ void k_counts_to_offsets(const u64* __restrict__ seg_count, int n_seg
 
 // ---- 3. one thread per slot ----------------------------------------------------------------
 constexpr int kMaxBlocks = 512;      // blocks of one tile in the one-group path (needs L >= 4 ...)
+constexpr int kFastMin = 128;        // a group part with fewer slots in a tile is worked off by the per-slot path
+constexpr int kBlockedMin = 64;      // groups with at least this many sources take the factored sum
+constexpr int kSrcRound = 512;       //   sources staged per round (two per thread)
+constexpr int kBlockRound = 24;      //   source blocks folded per round
 constexpr int kRows = 9;             // one-group path: rows of A = L * (256 / L) slots, ceil(2048 / 243) = 9
 constexpr int kHistPasses = 8;       // digit histograms kept per CTA (8 bits each, 64-bit keys)
 
@@ -223,6 +227,9 @@ struct GroupSmem {
   u32 hist[kHistPasses][QX_RADIX];   // digit counts of the kept terms (all passes of the sort)
   u64 scan[kWarps + 1];
   u64 base;
+  K blk_key[kBlockRound];            // factored sum: a representative key per source block
+  unsigned short blk_first[kBlockRound + 1];
+  int consumed;
 };
 
 // digit = byte `which` of the key
@@ -269,13 +276,29 @@ k_group_emit(const u64* __restrict__ cw, const u64* __restrict__ skey, const dou
   u32 magic = 0;
 
   for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-    const u64 r0 = (u64)tile * kTileSlots;
-    const u64 r1 = min(r0 + (u64)kTileSlots, total);
-    const u32 n_out = (u32)(r1 - r0);
-    const bool full = n_out == (u32)kTileSlots;
-    const int2 ti = tile_info[tile];
-    const int g0 = ti.x, seg0 = ti.y;
+   const u64 t0_slot = (u64)tile * kTileSlots;
+   const u64 t1_slot = min(t0_slot + (u64)kTileSlots, total);
+   const int2 ti = tile_info[tile];
+   int g_next = ti.x, seg_next = ti.y;
+   // A tile is worked off in PIECES: the part of one group that lies in it (one-group path, as
+   // long as it has kFastMin slots or is all that is left), or a run of smaller group parts
+   // (per-slot path).  Most tiles of a heavy operator are one piece.
+   for (u64 r0 = t0_slot; r0 < t1_slot;) {
+    while (gslot[g_next + 1] <= r0) ++g_next;
+    while ((u64)seg_slot[seg_next + 1] <= r0) ++seg_next;
+    const int g0 = g_next, seg0 = seg_next;
     const u64 gs0 = gslot[g0];
+    u64 r1 = min(gslot[g0 + 1], t1_slot);
+    bool piece_single = true;
+    if (r1 - r0 < (u64)kFastMin && r1 < t1_slot) {
+      piece_single = false;
+      int gg = g0 + 1;
+      while (r1 < t1_slot && min(gslot[gg + 1], t1_slot) - r1 < (u64)kFastMin) {
+        r1 = min(gslot[gg + 1], t1_slot);
+        ++gg;
+      }
+    }
+    const u32 n_out = (u32)(r1 - r0);
     const bool one_seg = (u64)seg_slot[seg0 + 1] >= r1;
 
     // my slots of the tile: slot_of(k), k < kRows.  One-group path: row k, column tid of rows of
@@ -303,7 +326,7 @@ k_group_emit(const u64* __restrict__ cw, const u64* __restrict__ skey, const dou
       hist_seg = seg0;
     }
 
-    bool single = gslot[g0 + 1] >= r1;
+    bool single = piece_single;
     int n_blocks = 0;
     u64 h0 = 0;
     u32 bl0 = 0;
@@ -432,8 +455,91 @@ k_group_emit(const u64* __restrict__ cw, const u64* __restrict__ skey, const dou
           }
         }
       }
-      // remaining sources of the group, kChunk (or fewer) per round
-      if (n_src > 1) {
+      // remaining sources of the group
+      if (n_src >= kBlockedMin) {
+        // ---- many sources: factor the sum.  Sources of the group that agree on all HIGH digits (a
+        // "source block": adjacent when the input is in canonical order, at most L of them) share
+        // the high product, so  sum_s lambda_s * hi_s(h) * lo_s(l)  =  sum_blocks hi_blk(h) * q_blk(l)
+        // with q_blk(l) = sum_{s in blk} lambda_s * lo_s(l): up to L times fewer (source, slot)
+        // pairs.  Any split into blocks is valid (an unsorted input only gives shorter blocks).
+        // The association of the products differs from the reference's left-to-right order, so
+        // coefficients agree with it to rounding (~1e-16 relative), not bitwise; groups with fewer
+        // sources take the exact loop below.
+        const K hm2 = lg.hi_mask | (lg.hi_mask << 1);
+        const int nb_max = max(1, min(kBlockRound, kPhiCap / n_blocks));
+        K* src_key = reinterpret_cast<K*>(sm.p_hi);                       // staged sources alias p_hi:
+        double* src_lam = sm.p_hi + kSrcRound / (8 / sizeof(K)) ;         // consumed before p_hi is written
+        double* q = &sm.low_w[1][0][0];                                     // [block][low branch]
+        for (int c0 = 1; c0 < n_src;) {
+          const int avail = min(kSrcRound, n_src - c0);
+          __syncthreads();                          // previous round (or the first source) consumed
+          for (int i = tid; i < avail; i += kThreads) {
+            src_key[i] = (K)skey[s0 + c0 + i];
+            src_lam[i] = slam[s0 + c0 + i];
+          }
+          if (tid == 0) sm.consumed = avail;
+          __syncthreads();
+          // block heads among the staged sources, two per thread
+          const int i0 = 2 * tid, i1 = 2 * tid + 1;
+          const bool hd0 = i0 < avail && (i0 == 0 || (src_key[i0] & hm2) != (src_key[i0 - 1] & hm2));
+          const bool hd1 = i1 < avail && (src_key[i1] & hm2) != (src_key[i0] & hm2);
+          u32 nheads;
+          const u32 before = block_exclusive_sum<u32>((u32)hd0 + (u32)hd1, reinterpret_cast<u32*>(sm.scan), nheads);
+          if (hd0) {
+            const u32 id = before;
+            if (id < (u32)nb_max) { sm.blk_first[id] = (unsigned short)i0; sm.blk_key[id] = src_key[i0]; }
+            else if (id == (u32)nb_max) sm.consumed = i0;
+          }
+          if (hd1) {
+            const u32 id = before + (u32)hd0;
+            if (id < (u32)nb_max) { sm.blk_first[id] = (unsigned short)i1; sm.blk_key[id] = src_key[i1]; }
+            else if (id == (u32)nb_max) sm.consumed = i1;
+          }
+          __syncthreads();
+          const int nblk = min((int)nheads, nb_max);
+          const int used = sm.consumed;
+          // q[blk][l]: the block's sources summed in input order
+          for (int w = tid; w < nblk * (int)lg.L; w += kThreads) {
+            const int b = w / (int)lg.L, l = w - b * (int)lg.L;
+            const u32 picks = sm.low[l].pick;
+            const int first = sm.blk_first[b], last = (b + 1 < nblk) ? (int)sm.blk_first[b + 1] : used;
+            double sum = 0.0;
+            for (int i = first; i < last; ++i) {
+              const K key = src_key[i];
+              double v = src_lam[i];
+#pragma unroll
+              for (int j = 2; j >= 0; --j)
+                if (lg.bit[j] >= 0)
+                  v *= sm.tb.w[lg.bit[j] >> 1][(u32)((key >> lg.bit[j]) & 3u) - 1u][(picks >> (2 * j)) & 3u];
+              sum += v;
+            }
+            q[b * 27 + l] = sum;
+          }
+          __syncthreads();                          // staged sources consumed: p_hi may be overwritten
+          for (int w = tid; w < nblk * n_blocks; w += kThreads) {
+            const int b = w / n_blocks, e = w - b * n_blocks;
+            const K key = sm.blk_key[b];
+            const K ch = sm.choice[e];
+            double v = 1.0;
+            for (K m = lg.hi_mask; m;) {             // qubit 0 first
+              const int bit = KeyOps<K>::highest(m);
+              m ^= (K)1 << bit;
+              v *= sm.tb.w[bit >> 1][(u32)((key >> bit) & 3u) - 1u][(u32)(ch >> bit) & 3u];
+            }
+            sm.p_hi[b * n_blocks + e] = v;
+          }
+          __syncthreads();
+          for (int b = 0; b < nblk; ++b) {
+            const double qb = q[b * 27 + (int)bl];
+            const double* ph = sm.p_hi + b * n_blocks + e0;
+#pragma unroll
+            for (int k = 0; k < kRows; ++k)
+              if (live & (1u << k)) acc[k] += ph[(u32)k * bpr] * qb;
+          }
+          c0 += used;
+        }
+      } else if (n_src > 1) {
+        // few sources: exact pairwise loop, kChunk (or fewer) per round
         const int per_round = max(1, min(kChunk, kPhiCap / n_blocks));
         for (int c0 = 1; c0 < n_src; c0 += per_round) {
           const int nc = min(per_round, n_src - c0);
@@ -601,6 +707,8 @@ k_group_emit(const u64* __restrict__ cw, const u64* __restrict__ skey, const dou
         }
       }
     }
+    r0 = r1;
+   }
   }
   __syncthreads();
   if (hist_seg >= 0) {

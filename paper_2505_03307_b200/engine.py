@@ -348,7 +348,8 @@ def _finish_streamed(w: _Walker, trace, pinned: bool):
         return None
     counts, axes, weights = w.staged
     raw = w.store.count_operator(counts)
-    if sum(raw) < STREAM_MIN_RAW:
+    # a generator never holds more than 4**n terms, however many raw branches feed it
+    if sum(min(r, 4 ** w.n) for r in raw) < STREAM_MIN_RAW:
         return None
     step, phase = w.pending
     # contiguous ranges of about equal raw size, smallest first: its copy starts early and the

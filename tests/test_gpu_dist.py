@@ -31,9 +31,13 @@ def nccl_world1():
     dist.destroy_process_group()
 
 
-def _same(a, b):
+def _same(a, b, tol=0.0):
     for ga, gb in zip(a.final.generators, b.final.generators):
-        assert np.array_equal(ga.indices, gb.indices) and np.array_equal(ga.lambdas, gb.lambdas)
+        assert np.array_equal(ga.indices, gb.indices)
+        if tol:
+            assert np.max(np.abs(ga.lambdas - gb.lambdas)) < tol
+        else:
+            assert np.array_equal(ga.lambdas, gb.lambdas)
     assert a.rank_trace == b.rank_trace
 
 
@@ -46,7 +50,9 @@ def test_sharded_and_partitioned_equal_plain(nccl_world1, name, mode):
     assert shards == [list(range(n))]
     _same(sharded, plain)
     part = qd.run_term_partitioned(gates, n, mode)
-    _same(part, plain)
+    # the partitioned run merges raw branch lists; the plain run sums groups with many sources in
+    # factored form (dense.cu): same terms, coefficients equal to rounding
+    _same(part, plain, tol=1e-12 if name.startswith("c4_") else 0.0)
 
 
 def test_exchange_terms_loopback(nccl_world1):

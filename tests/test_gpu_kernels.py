@@ -249,7 +249,12 @@ def test_operator_run_equals_three_steps(n, terms, rot_qubits, n_ops, mix):
     assert ranks == want_ranks and raw >= sum(ranks)
     for (gl, gk), (wl, wk) in zip(got, want):
         assert np.array_equal(gk, wk)
-        assert np.array_equal(gl, wl)          # sign flips are exact, summation order unchanged
+        if terms >= 400 and mix > 1:
+            # groups with >= 64 sources take the factored sum (dense.cu): same terms, products
+            # associated differently, so coefficients agree to rounding
+            assert np.max(np.abs(gl - wl)) < 1e-12
+        else:
+            assert np.array_equal(gl, wl)      # sign flips are exact, summation order unchanged
 
 
 def test_operator_run_with_corrupted_cx_table_is_table_driven():

@@ -1,11 +1,14 @@
-"""Run bench.py's GPU arm quietly and print ms/step plus selected kernel-class times."""
-import json, os, subprocess, sys
-tag = sys.argv[1] if len(sys.argv) > 1 else ""
-out = subprocess.run([sys.executable, "bench.py", "--steps", "3", "--warmup", "3", "--no-cpu"] + sys.argv[2:],
-                     capture_output=True, text=True, cwd=os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
-try:
-    d = json.loads(out.stdout.strip().splitlines()[-1])
-    c = d["roofline"]["classes"]
-    print(tag, "ms/step", round(d["ms_per_step"], 3), {k: round(v["ms"] / 3, 3) for k, v in c.items() if v["ms"] > 0.05}, flush=True)
-except Exception as e:
-    print(tag, "FAILED", e, out.stderr[-500:])
+"""Per kernel-class CUDA-event times of one workload/mode (instrumented run)."""
+import os, sys
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import paper_2505_03307_b200 as qx
+from paper_2505_03307_b200 import workloads, _native as nat
+name, mode = sys.argv[1], (sys.argv[2] if len(sys.argv) > 2 else "v3")
+n, gates = workloads.build(name)
+qx.run(gates, n, mode, download=False).device["store"].close()
+nat.profile_enable(True); nat.profile_reset()
+rep = qx.run(gates, n, mode, download=False); rep.device["store"].close()
+for k, v in nat.profile_read().items():
+    if v["launches"]:
+        print(f"{name} {mode} {k:16s} {v['launches']:5d} launches {v['ms']:10.3f} ms  {v['alg_bytes'] / max(v['ms'], 1e-9) / 1e6:9.1f} GB/s")
+print(rep.device)
