@@ -702,7 +702,7 @@ inline int sort_variant() {
   if (v < 0) {
     const char* e = getenv("QX_SORT_VARIANT");
     v = e ? atoi(e) : 0;
-    if (v < 0 || v > 4) v = 0;
+    if (v < 0 || v > 6) v = 0;
   }
   return v;
 }
@@ -713,6 +713,8 @@ inline int sort_tile_terms(int variant, size_t value_bytes) {
     case 2: return 256 * 12;
     case 3: return 256 * 16;
     case 4: return 512 * 8;
+    case 5: return 384 * 8;
+    case 6: return 384 * 10;
     default: return 384 * 12;
   }
 }
@@ -732,6 +734,8 @@ int dispatch_pass(int variant, QxArena* ar, MergeBuffers<V>& mb, int cur, int64_
       case 2: return launch_pass<K, V, 256, 12, 8, 4, KO>(ar, mb, cur, tiles_ub, info, n_tiles, digit_base, base_stride, ticket, which, base_in);
       case 3: return launch_pass<K, V, 256, 16, 8, 3, KO>(ar, mb, cur, tiles_ub, info, n_tiles, digit_base, base_stride, ticket, which, base_in);
       case 4: return launch_pass<K, V, 512, 8, 8, 2, KO>(ar, mb, cur, tiles_ub, info, n_tiles, digit_base, base_stride, ticket, which, base_in);
+      case 5: return launch_pass<K, V, 384, 8, 8, 4, KO>(ar, mb, cur, tiles_ub, info, n_tiles, digit_base, base_stride, ticket, which, base_in);
+      case 6: return launch_pass<K, V, 384, 10, 8, 3, KO>(ar, mb, cur, tiles_ub, info, n_tiles, digit_base, base_stride, ticket, which, base_in);
       default: return launch_pass<K, V, 384, 12, 8, 3, KO>(ar, mb, cur, tiles_ub, info, n_tiles, digit_base, base_stride, ticket, which, base_in);
     }
   }
@@ -739,6 +743,8 @@ int dispatch_pass(int variant, QxArena* ar, MergeBuffers<V>& mb, int cur, int64_
     case 2: return launch_pass<K, V, 256, 12, 8>(ar, mb, cur, tiles_ub, info, n_tiles, digit_base, base_stride, ticket, which, base_in);
     case 3: return launch_pass<K, V, 256, 16, 8>(ar, mb, cur, tiles_ub, info, n_tiles, digit_base, base_stride, ticket, which, base_in);
     case 4: return launch_pass<K, V, 512, 8, 8>(ar, mb, cur, tiles_ub, info, n_tiles, digit_base, base_stride, ticket, which, base_in);
+    case 5: return launch_pass<K, V, 384, 8, 8, 3>(ar, mb, cur, tiles_ub, info, n_tiles, digit_base, base_stride, ticket, which, base_in);
+    case 6: return launch_pass<K, V, 384, 10, 8>(ar, mb, cur, tiles_ub, info, n_tiles, digit_base, base_stride, ticket, which, base_in);
     default: return launch_pass<K, V, 384, 12, 8>(ar, mb, cur, tiles_ub, info, n_tiles, digit_base, base_stride, ticket, which, base_in);
   }
 }

@@ -14,7 +14,7 @@ for spec in "k_onesweep 5 1" "k_group_emit 1 1" "k_group_scan 1 1" "k_small_merg
   echo "$1 rc=$?"
 done
 # the kernels of the gate-by-gate mode (v1) on a mid-size point of the ladder
-for spec in "k_clifford 1 1" "k_split 60 1" "k_reduce 8 1" "k_sort_hist 8 1"; do
+for spec in "k_clifford 1 1" "k_split 83 1" "k_reduce 16 1" "k_sort_hist 16 1"; do
   set -- $spec
   timeout 1200 ncu --set full --clock-control none --import-source on -k regex:$1 -s $2 -c $3 -f \
       -o gpurun_out/${R}_v1_$1 python tools/profile_step.py --workload c4_xyz_14_2 --mode v1 --warmup 0 --steps 1 \

@@ -1,4 +1,4 @@
-for v in 0 2 3 4; do
+for v in ${VARIANTS:-0 5 6}; do
   QX_SORT_VARIANT=$v python bench.py --no-cpu --steps 3 2>/dev/null | python -c "
 import json,sys
 d=json.loads(sys.stdin.read()); c=d['roofline']['classes']
