@@ -138,6 +138,17 @@ int qx_apply_operator_run(qx_store* s, const int32_t* counts, const int32_t* axe
                           const double* weights, const uint32_t* program, int32_t n_ops,
                           uint32_t cx_c, uint32_t cx_t, uint32_t cx_s, double eps,
                           int64_t term_limit, int64_t* raw_total, int64_t* ranks);
+/* Host-only (no GPU work): the class decomposition qx_apply_operator_run uses for operators with
+ * a large fan-out.  Per qubit, input axes that share an output axis (stabilizer.py:209-214: the
+ * nonzero cells of a substituted row) form a class; terms whose words agree after every digit is
+ * replaced by its class can collide in the merge, all others cannot.  Inputs as in
+ * qx_apply_operator; outputs indexed [qubit*3 + axis-1]: class_id = smallest input axis of the
+ * class (1..3), class_radix = number of output axes of the class; class_axes / class_weights
+ * (may be NULL) [..*3 + b]: the class's output axes, ascending, and this input axis' weight on
+ * each (0.0 where it does not reach that axis). */
+int qx_operator_classes(int32_t n_qubits, const int32_t* counts, const int32_t* axes,
+                        const double* weights, int32_t* class_id, int32_t* class_radix,
+                        int32_t* class_axes, double* class_weights);
 /* Number of raw branches the same call would produce per segment, nothing written
  * (branch_counts, stabilizer.py:232-237). */
 int qx_count_operator(qx_store* s, const int32_t* counts, int64_t* raw_per_segment);

@@ -809,6 +809,52 @@ void fill_images_u64(int n_qubits, const uint32_t* program, int n_ops, u32 cx_c,
                      ImageTable<u64>* im);
 }  // namespace qxe
 
+// Host-only: the class decomposition the grouped path uses, for callers and tests (no GPU needed).
+extern "C" int qx_operator_classes(int32_t n_qubits, const int32_t* counts, const int32_t* axes,
+                                   const double* weights, int32_t* class_id, int32_t* class_radix,
+                                   int32_t* class_axes, double* class_weights) {
+  QX_REQUIRE(counts && axes && weights && class_id && class_radix, "NULL argument");
+  QX_REQUIRE(n_qubits >= 1 && n_qubits <= QX_MAX_QUBITS, "n_qubits=%d out of range", n_qubits);
+  OperatorTable nz;
+  for (int p = 0; p < QX_MAX_QUBITS; ++p)
+    for (int a = 0; a < 3; ++a) {
+      nz.cnt[p][a] = 1;
+      for (int b = 0; b < 3; ++b) {
+        nz.axis[p][a][b] = (unsigned char)(a + 1);
+        nz.w[p][a][b] = (b == 0) ? 1.0 : 0.0;
+      }
+    }
+  for (int j = 0; j < n_qubits; ++j) {
+    const int p = n_qubits - 1 - j;
+    for (int a = 0; a < 3; ++a) {
+      const int c = counts[j * 3 + a];
+      QX_REQUIRE(c >= 1 && c <= 3, "qubit %d axis %d: %d nonzero weights (need 1..3)", j, a + 1, c);
+      nz.cnt[p][a] = (unsigned char)c;
+      for (int b = 0; b < c; ++b) {
+        const int ax = axes[(j * 3 + a) * 3 + b];
+        QX_REQUIRE(ax >= 1 && ax <= 3, "qubit %d axis %d: output axis %d out of range", j, a + 1, ax);
+        nz.axis[p][a][b] = (unsigned char)ax;
+        nz.w[p][a][b] = weights[(j * 3 + a) * 3 + b];
+      }
+    }
+  }
+  OperatorTable ct;
+  ClassIds ids;
+  build_class_table(nz, n_qubits, &ct, &ids);
+  for (int j = 0; j < n_qubits; ++j) {
+    const int p = n_qubits - 1 - j;
+    for (int a = 0; a < 3; ++a) {
+      class_id[j * 3 + a] = ids.cls[p][a];
+      class_radix[j * 3 + a] = ct.cnt[p][a];
+      for (int b = 0; b < 3; ++b) {
+        if (class_axes) class_axes[(j * 3 + a) * 3 + b] = b < ct.cnt[p][a] ? ct.axis[p][a][b] : 0;
+        if (class_weights) class_weights[(j * 3 + a) * 3 + b] = b < ct.cnt[p][a] ? ct.w[p][a][b] : 0.0;
+      }
+    }
+  }
+  return QX_OK;
+}
+
 // The large operator step.  On entry the store holds the merged input terms (exact offsets on
 // the host); on exit it holds the canonical result and exact offsets.  `nz` is the operator's
 // non-zero branch table (fill_table in branch.cu).
