@@ -133,7 +133,10 @@ int qx_apply_operator(qx_store* s, const int32_t* counts, const int32_t* axes,
  * expansion kernel (a Clifford run is a homomorphism: the image of a raw term is the product of
  * the images of its single-digit factors), so raw terms are written once, already conjugated,
  * and for 2n <= 32 as 32-bit keys that only the sort passes see.  program/n_ops/cx_*: as in
- * qx_apply_clifford (n_ops may be 0).  ranks (may be NULL): per-segment counts after the merge. */
+ * qx_apply_clifford (n_ops may be 0).  ranks (may be NULL): per-segment counts after the merge.
+ * Operators with a large fan-out take the grouped dense path (csrc/dense.cu: sources grouped by
+ * class word, one thread per output slot, sort only); raw_total then reports the slot count, an
+ * upper bound of the merged size like the raw count. */
 int qx_apply_operator_run(qx_store* s, const int32_t* counts, const int32_t* axes,
                           const double* weights, const uint32_t* program, int32_t n_ops,
                           uint32_t cx_c, uint32_t cx_t, uint32_t cx_s, double eps,

@@ -603,7 +603,8 @@ void fill_images_u64(int n_qubits, const uint32_t* program, int n_ops, u32 cx_c,
 
 // dense.cu: the grouped dense operator step
 int qx_dense_operator_step(qx_store* s, const OperatorTable& nz, const uint32_t* program, int n_ops,
-                           u32 cx_c, u32 cx_t, u32 cx_s, double eps, int64_t* slots_total);
+                           u32 cx_c, u32 cx_t, u32 cx_s, double eps, int64_t* slots_total,
+                           int64_t probe_fanout, bool* done);
 
 namespace {
 
@@ -654,7 +655,8 @@ int expand(qx_store* s, const OperatorTable& tb, const uint32_t* program, int n_
   static const bool no_dense = getenv("QX_NO_DENSE") != nullptr;
   static const int64_t dense_fanout = getenv("QX_DENSE_FANOUT") ? atoll(getenv("QX_DENSE_FANOUT")) : 16;
   if (dense_eps > 0.0 && !no_dense && ub_seg > QX_SMALL_MAX && raw >= dense_fanout * total_in) {
-    QX_TRY(qx_dense_operator_step(s, tb, program, n_ops, cx_c, cx_t, cx_s, dense_eps, nullptr));
+    bool done = false;
+    QX_TRY(qx_dense_operator_step(s, tb, program, n_ops, cx_c, cx_t, cx_s, dense_eps, nullptr, 0, &done));
     if (went_dense) *went_dense = true;
     return QX_OK;
   }
@@ -727,6 +729,30 @@ extern "C" int qx_apply_operator_run(qx_store* s, const int32_t* counts, const i
     QX_TRY(expand(s, tb, nullptr, 0, 0, 0, 0, false, term_limit, raw_total, nullptr));
     QX_TRY(qx_apply_clifford(s, program, n_ops, cx_c, cx_t, cx_s));
     return qx_merge(s, eps, ranks);
+  }
+  // Few sources: group them first instead of counting raw branches -- the same single host
+  // round trip then already yields the slot counts the grouped path needs.
+  static const bool no_dense = getenv("QX_NO_DENSE") != nullptr;
+  static const int64_t dense_fanout = getenv("QX_DENSE_FANOUT") ? atoll(getenv("QX_DENSE_FANOUT")) : 16;
+  if (eps > 0.0 && !no_dense && term_limit <= 0) {
+    QX_CUDA(cudaSetDevice(s->device));
+    if (!s->exact) QX_TRY(qx_store_refresh(s));
+    const int64_t total_in = s->h_seg[s->n_seg];
+    // what one term can branch into at most: operators that touch a few qubits never qualify
+    int64_t max_fanout = 1;
+    for (int p = 0; p < s->n_qubits && max_fanout < (1 << 20); ++p)
+      max_fanout *= std::max({tb.cnt[p][0], tb.cnt[p][1], tb.cnt[p][2]});
+    if (total_in > 0 && total_in <= (1 << 16) && max_fanout >= dense_fanout) {
+      bool done = false;
+      int64_t slots = 0;
+      QX_TRY(qx_dense_operator_step(s, tb, program, n_ops, cx_c, cx_t, cx_s, eps, &slots, dense_fanout, &done));
+      if (done) {
+        if (raw_total) *raw_total = slots;
+        if (ranks)
+          for (int g = 0; g < s->n_seg; ++g) ranks[g] = s->h_seg[g + 1] - s->h_seg[g];
+        return QX_OK;
+      }
+    }
   }
   static const bool no_narrow = getenv("QX_NO_NARROW") != nullptr;
   bool narrow = false, dense = false;

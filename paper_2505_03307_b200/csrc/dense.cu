@@ -85,6 +85,114 @@ __device__ __forceinline__ u64 slots_of(u64 cw, const unsigned char (*cnt)[3]) {
   return c;
 }
 
+// ---- 1 + 2 for few sources: one CTA does it all ------------------------------------------------
+// Up to kPrepSmall sources: class words, bitonic sort on (generator, class word, input position)
+// in shared memory, group heads, both scans, gathers -- one launch instead of the dozen of the
+// general path (the probe of an operator costs as little as counting its raw branches).
+constexpr int kPrepSmall = 1024;
+constexpr int kPrepThreads = 256;
+
+__global__ void __launch_bounds__(kPrepThreads)
+k_group_prep_small(const u64* __restrict__ keys_in, const double* __restrict__ lam_in,
+                   const int64_t* __restrict__ seg, int n_seg, int n, u64* __restrict__ cw_out,
+                   u64* __restrict__ skey, double* __restrict__ slam, u64* __restrict__ gsrc,
+                   u64* __restrict__ gslot, int64_t* __restrict__ seg_slot, u64* __restrict__ totals,
+                   const __grid_constant__ ClassIds ids, const __grid_constant__ OperatorTable tb) {
+  __shared__ u64 s_cw[kPrepSmall];
+  __shared__ unsigned short s_seg[kPrepSmall], s_idx[kPrepSmall];
+  __shared__ u64 s_slots[kPrepSmall];          // slots of a head (0 otherwise) -> exclusive prefix
+  __shared__ unsigned short s_heads[kPrepSmall];   // head flag -> exclusive prefix
+  __shared__ unsigned char s_cls[QX_MAX_QUBITS][3], s_cnt[QX_MAX_QUBITS][3];
+  __shared__ u64 s_scan[kPrepThreads / 32 + 1];
+  const int tid = threadIdx.x;
+  for (int i = tid; i < QX_MAX_QUBITS * 3; i += kPrepThreads) {
+    s_cls[i / 3][i % 3] = ids.cls[i / 3][i % 3];
+    s_cnt[i / 3][i % 3] = tb.cnt[i / 3][i % 3];
+  }
+  __syncthreads();
+  int m = 32;
+  while (m < n) m <<= 1;
+  for (int e = tid; e < m; e += kPrepThreads) {
+    if (e < n) {
+      s_cw[e] = class_word<u64>(keys_in[e], s_cls);
+      s_seg[e] = (unsigned short)segment_of(seg, n_seg, e);
+    } else {
+      s_cw[e] = ~0ull;
+      s_seg[e] = 0xffffu;                        // padding sorts last
+    }
+    s_idx[e] = (unsigned short)e;
+  }
+  __syncthreads();
+  for (int k = 2; k <= m; k <<= 1) {
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      for (int t = tid; t < (m >> 1); t += kPrepThreads) {
+        const int lo = ((t & ~(j - 1)) << 1) | (t & (j - 1));
+        const int hi = lo | j;
+        const unsigned short sa = s_seg[lo], sb = s_seg[hi], ia = s_idx[lo], ib = s_idx[hi];
+        const u64 ca = s_cw[lo], cb = s_cw[hi];
+        const bool greater = sa != sb ? sa > sb : (ca != cb ? ca > cb : ia > ib);
+        if (greater == ((lo & k) == 0)) {
+          s_seg[lo] = sb; s_seg[hi] = sa;
+          s_cw[lo] = cb; s_cw[hi] = ca;
+          s_idx[lo] = ib; s_idx[hi] = ia;
+        }
+      }
+      __syncthreads();
+    }
+  }
+  // heads and their slot counts; four consecutive sources per thread
+  constexpr int kEach = kPrepSmall / kPrepThreads;
+  u64 my_slots = 0;
+  u32 my_heads = 0;
+  for (int r = 0; r < kEach; ++r) {
+    const int e = tid * kEach + r;
+    u64 sl = 0;
+    unsigned short hd = 0;
+    if (e < n) {
+      hd = (e == 0 || s_seg[e - 1] != s_seg[e] || s_cw[e - 1] != s_cw[e]) ? 1 : 0;
+      if (hd) sl = slots_of(s_cw[e], s_cnt);
+    }
+    s_slots[e] = sl;
+    s_heads[e] = hd;
+    my_slots += sl;
+    my_heads += hd;
+  }
+  u64 tot_s, tot_h;
+  u64 ex_s = block_exclusive_sum<u64>(my_slots, s_scan, tot_s);
+  u64 ex_h = block_exclusive_sum<u64>((u64)my_heads, s_scan, tot_h);
+  for (int r = 0; r < kEach; ++r) {
+    const int e = tid * kEach + r;
+    const u64 sl = s_slots[e];
+    const unsigned short hd = s_heads[e];
+    s_slots[e] = ex_s;                            // first slot of the group this source opens / belongs after
+    if (e < n) {
+      const int j = s_idx[e];
+      cw_out[e] = s_cw[e];
+      skey[e] = keys_in[j];
+      slam[e] = lam_in[j];
+      if (hd) {
+        gsrc[ex_h] = (u64)e;
+        gslot[ex_h] = ex_s;
+      }
+    }
+    ex_s += sl;
+    ex_h += hd;
+  }
+  __syncthreads();
+  // slot offset of every generator: the first slot of its first source (sources are in generator
+  // order), or the next generator's / the total for an empty one
+  for (int g = tid; g <= n_seg; g += kPrepThreads) {
+    const int64_t first = seg[g];                 // index of its first source in INPUT order = sorted position
+    seg_slot[g] = first < n ? (int64_t)s_slots[first] : (int64_t)tot_s;
+  }
+  if (tid == 0) {
+    gsrc[tot_h] = (u64)n;
+    gslot[tot_h] = tot_s;
+    totals[0] = tot_h;
+    totals[1] = tot_s;
+  }
+}
+
 // One pass over the sources in (generator, class word) order.  A source is a group head if it
 // opens a generator or its class word differs from its predecessor's.  Two exclusive scans
 // (heads, slots of heads) give every group its index and its first slot.  Also gathers the
@@ -858,8 +966,13 @@ extern "C" int qx_operator_classes(int32_t n_qubits, const int32_t* counts, cons
 // The large operator step.  On entry the store holds the merged input terms (exact offsets on
 // the host); on exit it holds the canonical result and exact offsets.  `nz` is the operator's
 // non-zero branch table (fill_table in branch.cu).
+// probe_fanout > 0: the caller has not counted the raw branches; group the sources first and go
+// on only if the operator is worth it (some generator above the small-merge limit and at least
+// probe_fanout slots per source), otherwise leave the store untouched and report *done = false.
 int qx_dense_operator_step(qx_store* s, const OperatorTable& nz, const uint32_t* program, int n_ops,
-                           u32 cx_c, u32 cx_t, u32 cx_s, double eps, int64_t* slots_total) {
+                           u32 cx_c, u32 cx_t, u32 cx_s, double eps, int64_t* slots_total,
+                           int64_t probe_fanout, bool* done) {
+  if (done) *done = false;
   QX_CUDA(cudaSetDevice(s->device));
   const int n_seg = s->n_seg;
   const int64_t n = s->h_seg[n_seg];
@@ -896,35 +1009,43 @@ int qx_dense_operator_step(qx_store* s, const OperatorTable& nz, const uint32_t*
 
   const int in = s->cur;
   int sorted;
-  {
-    QxProfileScope prof(QX_K_DENSE_PREP, s->stream, 8.0 * (double)n + 16.0 * (double)n);
-    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((n + kThreads - 1) / kThreads, (int64_t)s->sm_count * 8));
-    k_class_words<<<grid, kThreads, 0, s->stream>>>(s->keys[in], n, cwb[in], idb[in], ids);
+  if (n <= kPrepSmall && n_seg < 65535) {
+    QxProfileScope prof(QX_K_DENSE_PREP, s->stream, 72.0 * (double)n);
+    k_group_prep_small<<<1, kPrepThreads, 0, s->stream>>>(s->keys[in], s->lam[in], s->seg[in], n_seg, (int)n,
+                                                         cwb[in], skey, slam, gsrc, gslot, seg_slot, totals, ids, ct);
     QX_CUDA(cudaGetLastError());
-  }
-  {
-    // stable segmented sort of (class word, source index) by class word
-    qxm::MergeBuffers<double> mb;
-    mb.keys[in] = cwb[in];
-    mb.keys[in ^ 1] = cwb[in ^ 1];
-    mb.vals[in] = idb[in];
-    mb.vals[in ^ 1] = idb[in ^ 1];
-    mb.seg[0] = s->seg[0];
-    mb.seg[1] = s->seg[1];
-    mb.cur = in;
-    mb.n_seg = n_seg;
-    mb.ub_total = n;
-    mb.ub_seg = 0;
-    for (int g = 0; g < n_seg; ++g) mb.ub_seg = std::max(mb.ub_seg, s->h_seg[g + 1] - s->h_seg[g]);
-    QX_TRY((qxm::merge_large<double, u64>(s, mb, 0.0, QX_K_REDUCE, false, QX_K_DENSE_PREP, QX_K_DENSE_PREP)));
-    sorted = mb.cur;
-  }
-  {
-    QxProfileScope prof(QX_K_DENSE_PREP, s->stream, 48.0 * (double)n);
-    k_group_scan<<<(unsigned)src_tiles, kThreads, 0, s->stream>>>(
-        cwb[sorted], idb[sorted], s->keys[in], s->lam[in], s->seg[in], n_seg, n, skey, slam, gsrc, gslot,
-        seg_slot, totals, st_heads, st_slots, ticket1, ct);
-    QX_CUDA(cudaGetLastError());
+    sorted = in;
+  } else {
+    {
+      QxProfileScope prof(QX_K_DENSE_PREP, s->stream, 8.0 * (double)n + 16.0 * (double)n);
+      const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((n + kThreads - 1) / kThreads, (int64_t)s->sm_count * 8));
+      k_class_words<<<grid, kThreads, 0, s->stream>>>(s->keys[in], n, cwb[in], idb[in], ids);
+      QX_CUDA(cudaGetLastError());
+    }
+    {
+      // stable segmented sort of (class word, source index) by class word
+      qxm::MergeBuffers<double> mb;
+      mb.keys[in] = cwb[in];
+      mb.keys[in ^ 1] = cwb[in ^ 1];
+      mb.vals[in] = idb[in];
+      mb.vals[in ^ 1] = idb[in ^ 1];
+      mb.seg[0] = s->seg[0];
+      mb.seg[1] = s->seg[1];
+      mb.cur = in;
+      mb.n_seg = n_seg;
+      mb.ub_total = n;
+      mb.ub_seg = 0;
+      for (int g = 0; g < n_seg; ++g) mb.ub_seg = std::max(mb.ub_seg, s->h_seg[g + 1] - s->h_seg[g]);
+      QX_TRY((qxm::merge_large<double, u64>(s, mb, 0.0, QX_K_REDUCE, false, QX_K_DENSE_PREP, QX_K_DENSE_PREP)));
+      sorted = mb.cur;
+    }
+    {
+      QxProfileScope prof(QX_K_DENSE_PREP, s->stream, 48.0 * (double)n);
+      k_group_scan<<<(unsigned)src_tiles, kThreads, 0, s->stream>>>(
+          cwb[sorted], idb[sorted], s->keys[in], s->lam[in], s->seg[in], n_seg, n, skey, slam, gsrc, gslot,
+          seg_slot, totals, st_heads, st_slots, ticket1, ct);
+      QX_CUDA(cudaGetLastError());
+    }
   }
   // slot offsets of the generators + totals -> host (sizes the output)
   QX_TRY(qx_readback(s->stream, s->h_pinned, seg_slot, (int64_t)n_seg + 1));
@@ -933,6 +1054,8 @@ int qx_dense_operator_step(qx_store* s, const OperatorTable& nz, const uint32_t*
   int64_t ub_seg = 0;
   for (int g = 0; g < n_seg; ++g) ub_seg = std::max(ub_seg, s->h_pinned[g + 1] - s->h_pinned[g]);
   if (slots_total) *slots_total = total;
+  if (probe_fanout > 0 && !(ub_seg > QX_SMALL_MAX && total >= probe_fanout * n)) return QX_OK;
+  if (done) *done = true;
   // the sources live in skey/slam now: both store buffers are free for the output
   QX_TRY(qx_store_reserve(s, total, false));
   const int out = s->cur ^ 1;
@@ -989,7 +1112,10 @@ int qx_dense_operator_step(qx_store* s, const OperatorTable& nz, const uint32_t*
   s->exact = false;
   s->ub_total = total;
   s->ub_seg = ub_seg;
-  QX_TRY(qx_store_refresh(s));                     // kept counts: exact offsets, sizes the sort
+  // The sort only needs upper bounds from the host (it reads the offsets on the device), so it is
+  // queued behind the slot kernel without waiting for the kept counts; instrumented runs wait,
+  // so that the passes are booked with the bytes they really move.
+  if (qx_profile_on()) QX_TRY(qx_store_refresh(s));
   // ---- canonical order: distinct words, nothing left to sum or drop
   qxm::MergeBuffers<double> mb;
   for (int b = 0; b < 2; ++b) {
@@ -1005,5 +1131,6 @@ int qx_dense_operator_step(qx_store* s, const OperatorTable& nz, const uint32_t*
   if (narrow) QX_TRY((qxm::merge_large<double, u32>(s, mb, eps, QX_K_REDUCE, false, QX_K_SORT_PASS, QX_K_SORT_HIST, seg_slot, hist)));
   else QX_TRY((qxm::merge_large<double, u64>(s, mb, eps, QX_K_REDUCE, false, QX_K_SORT_PASS, QX_K_SORT_HIST, seg_slot, hist)));
   s->cur = mb.cur;
+  if (!s->exact) QX_TRY(qx_store_refresh(s));      // kept counts: exact offsets for the caller
   return QX_OK;
 }

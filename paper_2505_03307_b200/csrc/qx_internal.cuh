@@ -49,6 +49,7 @@ struct QxProfileScope {
   ~QxProfileScope();
 };
 void qx_count_launches(int n);
+bool qx_profile_on();
 
 // ----------------------------------------------------------------------------
 // geometry of the device-wide passes

@@ -115,6 +115,7 @@ void resolve(ClassStats& c) {
 }  // namespace
 
 void qx_count_launches(int n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
+bool qx_profile_on() { return g_prof_on; }
 
 QxProfileScope::QxProfileScope(int kernel_class, cudaStream_t st, double alg_bytes, int launches)
     : cls(kernel_class), stream(st), start(nullptr), stop(nullptr), active(false) {
