@@ -56,29 +56,80 @@ def compose_block(gates) -> np.ndarray:
     return np.ascontiguousarray(acc.T)
 
 
+def _fill_axis_map(out: np.ndarray, gate: str, theta: float) -> None:
+    """Write axis_map(gate, theta) into the zeroed 3x3 view ``out`` (same values, no temporaries)."""
+    fixed = _FIXED_ARRAYS.get(gate)
+    if fixed is not None:
+        out[...] = fixed
+        return
+    c, s = math.cos(theta), math.sin(theta)
+    if gate == "RX":
+        out[0, 0] = 1.0
+        out[1, 1] = c
+        out[1, 2] = -s
+        out[2, 1] = s
+        out[2, 2] = c
+    elif gate == "RY":
+        out[0, 0] = c
+        out[0, 2] = s
+        out[1, 1] = 1.0
+        out[2, 0] = -s
+        out[2, 2] = c
+    elif gate == "RZ":
+        out[0, 0] = c
+        out[0, 1] = -s
+        out[1, 0] = s
+        out[1, 1] = c
+        out[2, 2] = 1.0
+    else:
+        raise ValueError(f"no single-qubit conjugation rule for gate {gate!r}")
+
+
 def create_lut_1q(partition, workers=None) -> np.ndarray:
     """(K, n, 3, 3) tensor of composed blocks (reference lut.py:77-103).
 
     Only cells that hold gates are composed; the rest are the exact identity,
     which is what composing an empty list yields.  ``workers`` is accepted for
     signature compatibility; cells are independent so the result is the same.
+
+    Cells with the same number of gates are composed together: their i-th gate
+    matrices are stacked and multiplied with one batched ``np.matmul`` per
+    position -- numpy runs the same 3x3 product per matrix as ``compose_block``
+    does with ``@`` (bit-identical, tests/test_native_abi.py), without the
+    per-call overhead.  The first factor is taken as is: M @ I == M.
     """
     lut = np.empty((partition.k, partition.n, 3, 3))
     lut[:] = np.eye(3)
+    by_len: dict = {}
     for ki, bucket in enumerate(partition.u_groups):
         for wire, gates in bucket.items():
             # cells made of fixed gates only (most cells of a Clifford+T circuit) recur with few
             # distinct gate sequences: compose each sequence once, with the same numpy chain
             names = tuple(g.gate for g in gates)
             block = _FIXED_BLOCKS.get(names)
-            if block is None:
+            if block is None and all(name in _FIXED for name in names):
                 block = compose_block(gates)
-                if all(name in _FIXED for name in names) and len(_FIXED_BLOCKS) < 65536:
+                if len(_FIXED_BLOCKS) < 65536:
                     _FIXED_BLOCKS[names] = block
-            lut[ki, wire] = block
+            if block is not None:
+                lut[ki, wire] = block
+            else:
+                by_len.setdefault(len(gates), []).append((ki, wire, gates))
+    for length, cells in by_len.items():
+        mats = np.zeros((length, len(cells), 3, 3))
+        for ci, (_, _, gates) in enumerate(cells):
+            for gi, inst in enumerate(gates):
+                _fill_axis_map(mats[gi, ci], inst.gate, inst.theta)
+        acc = mats[0] + 0.0                     # M @ I == M (and -0.0 -> 0.0, like the product)
+        for gi in range(1, length):
+            acc = np.matmul(mats[gi], acc)
+        ks = [c[0] for c in cells]
+        ws = [c[1] for c in cells]
+        lut[ks, ws] = acc.transpose(0, 2, 1)
     return lut
 
 
+_FIXED_ARRAYS = {name: np.array(rows) for name, rows in _FIXED.items()}
 _FIXED_BLOCKS: dict = {}
 
 
