@@ -222,3 +222,43 @@ def test_generator_shards_equal_full_run():
             a, b = part.final.generators[local], full.final.generators[gi]
             assert np.array_equal(a.indices, b.indices) and np.array_equal(a.lambdas, b.lambdas)
         assert [[step[g] for g in ids] for step in full.rank_trace] == part.rank_trace
+
+
+def test_streamed_finish_equals_plain_download(monkeypatch):
+    """run() evolves the last operator per generator range and overlaps each range's download with
+    the next range's kernels when the result is large (engine._finish_streamed); the generators it
+    returns must be the ones a plain run leaves in HBM."""
+    from paper_2505_03307_b200 import engine
+
+    n, gates = workloads.build("c4_xyz_12_2")
+    monkeypatch.setattr(engine, "STREAM_MIN_RAW", 1 << 16)       # force the streamed path at this size
+    streamed = qx.run(gates, n, "v3", pinned=True)
+    assert streamed.device.get("streamed_ranges", 0) >= 2
+    plain = qx.run(gates, n, "v3", download=False)
+    try:
+        segs = plain.device["store"].segments()
+    finally:
+        plain.device["store"].close()
+    assert streamed.rank_trace == plain.rank_trace
+    for g, (lam, keys) in zip(streamed.final.generators, segs):
+        assert np.array_equal(g.keys(), keys) and np.array_equal(g.lambdas, lam)
+
+
+def test_collapse_in_the_grouped_operator_step():
+    """An eps above every coefficient empties a generator inside the grouped dense path; the engine
+    must report it like the reference (engine.py:148-152)."""
+    n, gates = workloads.build("c4_xyz_12_2")
+    with pytest.raises(qx.NumericalCollapseError, match="all terms of generator"):
+        qx.run(gates, n, "v3", eps=0.9)
+
+
+def test_eps_zero_takes_the_raw_path_and_matches_the_oracle():
+    """eps == 0 keeps exact-zero sums, which the grouped path cannot tell from unreached slots: the
+    call must fall back to expand + sort + reduce and still agree with the oracle."""
+    n = 9
+    gates = qx.gen_xyz_chain(n, 2, 1, rng=11)
+    got = qx.run(gates, n, "v3", eps=0.0)
+    want = oracle.run(gates, n, "v3", eps=0.0)
+    assert got.rank_trace == want["rank_trace"]
+    for g, (lam, idx) in zip(got.final.generators, want["final"]):
+        assert np.array_equal(g.keys(), idx) and np.max(np.abs(g.lambdas - lam)) < TOL
