@@ -42,8 +42,8 @@ constexpr int kThreads = 256;
 constexpr int kWarps = kThreads / 32;
 constexpr int kPer = 8;
 constexpr int kTileSlots = kThreads * kPer;      // 2048 slots (or sources) per tile
-constexpr int kChunk = 16;                       // sources accumulated per round of the one-group path
-constexpr int kPhiCap = 2048;                    // partial products held per round
+constexpr int kChunk = 8;                        // sources accumulated per round of the one-group path
+constexpr int kPhiCap = 1024;                    // partial products held per round
 
 // class id (1..3, the smallest input axis of the class) of input axis a+1 at digit position p
 struct ClassIds {
@@ -309,6 +309,9 @@ constexpr int kBlockedMin = 64;      // groups with at least this many sources t
 constexpr int kSrcRound = 512;       //   sources staged per round (two per thread)
 constexpr int kBlockRound = 24;      //   source blocks folded per round
 constexpr int kRows = 9;             // one-group path: rows of A = L * (256 / L) slots, ceil(2048 / 243) = 9
+#ifndef QX_EMIT_MINB
+#define QX_EMIT_MINB 5
+#endif
 constexpr int kHistPasses = 8;       // digit histograms kept per CTA (8 bits each, 64-bit keys)
 
 template <typename K> struct __align__(16) HiEntry {   // per block of the tile
@@ -332,7 +335,7 @@ struct GroupSmem {
   double p_hi[kPhiCap];              // [source of the round][block]: lambda * high weights
   double low_w[kChunk + 1][27][4];   // [first source | source of the round][low branch][low digit], 32-byte rows
   LowEntry<K> low[27];
-  u32 hist[kHistPasses][QX_RADIX];   // digit counts of the kept terms (all passes of the sort)
+  u32 hist[sizeof(K) == 4 ? 4 : kHistPasses][QX_RADIX];   // digit counts of the kept terms (all passes of the sort)
   u64 scan[kWarps + 1];
   u64 base;
   K blk_key[kBlockRound];            // factored sum: a representative key per source block
@@ -353,7 +356,7 @@ __device__ __forceinline__ u32 digit_of(u64 key, int which) { return (u32)(key >
 // version of this kernel, profiles/r01h).  The digit histograms of the sort that follows are
 // counted here, on the keys while they are in registers (hist[g][pass][digit]).
 template <typename K, typename KO, bool FUSED>
-__global__ void __launch_bounds__(kThreads, sizeof(K) == 8 ? 2 : 3)
+__global__ void __launch_bounds__(kThreads, sizeof(K) == 8 ? 2 : QX_EMIT_MINB)
 k_group_emit(const u64* __restrict__ cw, const u64* __restrict__ skey, const double* __restrict__ slam,
              const u64* __restrict__ gsrc, const u64* __restrict__ gslot, const u64* __restrict__ totals,
              const int2* __restrict__ tile_info, const int64_t* __restrict__ seg_slot, int n_seg,
@@ -372,7 +375,7 @@ k_group_emit(const u64* __restrict__ cw, const u64* __restrict__ skey, const dou
       u32* idst = reinterpret_cast<u32*>(&sm.im);
       for (int i = tid; i < (int)(sizeof(ImageTable<K>) / 4); i += kThreads) idst[i] = isrc[i];
     }
-    for (int i = tid; i < kHistPasses * QX_RADIX; i += kThreads) (&sm.hist[0][0])[i] = 0u;
+    for (int i = tid; i < (int)(sizeof(sm.hist) / 4); i += kThreads) (&sm.hist[0][0])[i] = 0u;
   }
   const int64_t ngroups = (int64_t)totals[0];
   const u64 total = totals[1];
