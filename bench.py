@@ -208,12 +208,20 @@ def run_ours(args):
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     dist = None
+    # QX_BENCH_BACKEND=gloo + QX_BENCH_SHARE_GPU=1: several ranks on ONE GPU with CPU collectives --
+    # only to exercise the multi-rank code path on a one-GPU box (tools/bench_two_ranks.sh)
+    backend = os.environ.get("QX_BENCH_BACKEND", "nccl")
+    share = os.environ.get("QX_BENCH_SHARE_GPU", "") == "1"
+    device = local % torch.cuda.device_count() if share else local
+    red_dev = "cuda" if backend == "nccl" else "cpu"
     if world > 1:
         import torch.distributed as dist
 
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    device = local
+        torch.cuda.set_device(device)
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", device))
+        else:
+            dist.init_process_group(backend)
     torch.cuda.set_device(device)
     weak = args.scaling == "weak" and world > 1
     instance = rank if weak else 0
@@ -224,7 +232,7 @@ def run_ours(args):
     total_updates = float(sum(updates_per_gen))
     if weak:
         mine = list(range(n))                      # my own circuit instance, all of its generators
-        t = torch.tensor([total_updates], device="cuda", dtype=torch.float64)
+        t = torch.tensor([total_updates], device=red_dev, dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.SUM)
         total_updates = float(t.item())
     else:
@@ -259,7 +267,7 @@ def run_ours(args):
         barrier()
     ms = ev0.elapsed_time(ev1)
     launches = nat.launch_count() - l0
-    t = torch.tensor([ms], device="cuda", dtype=torch.float64)
+    t = torch.tensor([ms], device=red_dev, dtype=torch.float64)
     if dist is not None:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms_per_step = float(t.item()) / args.steps
@@ -275,7 +283,7 @@ def run_ours(args):
         last = step_e2e()
     barrier()
     e2e_s = (time.perf_counter() - t0) / args.steps
-    t = torch.tensor([e2e_s], device="cuda", dtype=torch.float64)
+    t = torch.tensor([e2e_s], device=red_dev, dtype=torch.float64)
     if dist is not None:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     e2e_s = float(t.item())
