@@ -42,3 +42,18 @@ def test_config4_16_2_properties():
     finally:
         store.close()
     assert first == second                                                  # bitwise run-to-run determinism
+
+
+def test_gpu_only_ladder_point_18_2():
+    """xyz_chain(18, 2): 9.7e8 final terms (the reference cannot reach it).  Each generator is
+    U Z_j U^dagger, so sum(lambda^2) = 1; 64-bit keys through the grouped operator step."""
+    n, gates = workloads.build("c4_xyz_18_2")
+    rep = qx.run(gates, n, "v3", download=False)
+    st = rep.device["store"]
+    try:
+        norms = st.norms()
+        ranks = st.ranks()
+    finally:
+        st.close()
+    assert sum(ranks) == sum(rep.rank_trace[-1]) > 9e8
+    assert np.max(np.abs(norms - 1.0)) < 1e-9

@@ -6,7 +6,7 @@ mkdir -p gpurun_out
 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/${R}_launches_${W}.csv \
     python tools/profile_step.py --workload $W --mode v3 --warmup 1 --steps 1 > gpurun_out/${R}_launches.log 2>&1
 # the measured step is the second one: skip the launches of the warm-up step
-for spec in "k_onesweep 5 1" "k_group_emit 1 1" "k_group_scan 1 1" "k_small_merge 1 1"; do
+for spec in "k_onesweep 5 1" "k_group_emit 1 1" "k_group_prep_small 3 1" "k_small_merge 1 1"; do
   set -- $spec
   timeout 1200 ncu --set full --clock-control none --import-source on -k regex:$1 -s $2 -c $3 -f \
       -o gpurun_out/${R}_$1 python tools/profile_step.py --workload $W --mode v3 --warmup 1 --steps 1 \
