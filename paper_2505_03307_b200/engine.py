@@ -370,7 +370,8 @@ def _finish_streamed(w: _Walker, trace, pinned: bool):
     ranks = [0] * len(w.ids)
     try:
         for lo, hi in ranges:
-            child = w.store.slice(lo, hi, int(sum(raw[lo:hi]) * 1.02) + 1024)
+            # no capacity hint: the operator step reserves what it needs (slots, not raw branches)
+            child = w.store.slice(lo, hi, 0)
             children.append(child)
             _, r = child.apply_operator_run(counts, axes, weights, program, w.eps)
             ranks[lo:hi] = r
