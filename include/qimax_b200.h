@@ -141,6 +141,17 @@ int qx_apply_operator_run(qx_store* s, const int32_t* counts, const int32_t* axe
                           const double* weights, const uint32_t* program, int32_t n_ops,
                           uint32_t cx_c, uint32_t cx_t, uint32_t cx_s, double eps,
                           int64_t term_limit, int64_t* raw_total, int64_t* ranks);
+/* Multi-GPU form of qx_apply_operator_run for the LAST branching operator of a circuit: every
+ * device holds the same input terms and works off the part-th of `parts` contiguous ranges of
+ * output slots (slots are independent: no communication).  *partitioned = 1: the store now holds
+ * this part's share of every generator (canonical order, disjoint from the other parts' shares;
+ * ranks are the share's counts -- sum them over the parts); 0: the operator did not take the
+ * grouped path (few sources' worth of fan-out, eps == 0, ...) and the store holds the complete
+ * result, identical on every device. */
+int qx_apply_operator_run_part(qx_store* s, const int32_t* counts, const int32_t* axes,
+                               const double* weights, const uint32_t* program, int32_t n_ops,
+                               uint32_t cx_c, uint32_t cx_t, uint32_t cx_s, double eps,
+                               int32_t part, int32_t parts, int64_t* ranks, int32_t* partitioned);
 /* Host-only (no GPU work): the class decomposition qx_apply_operator_run uses for operators with
  * a large fan-out.  Per qubit, input axes that share an output axis (stabilizer.py:209-214: the
  * nonzero cells of a substituted row) form a class; terms whose words agree after every digit is

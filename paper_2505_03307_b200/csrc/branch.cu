@@ -604,7 +604,7 @@ void fill_images_u64(int n_qubits, const uint32_t* program, int n_ops, u32 cx_c,
 // dense.cu: the grouped dense operator step
 int qx_dense_operator_step(qx_store* s, const OperatorTable& nz, const uint32_t* program, int n_ops,
                            u32 cx_c, u32 cx_t, u32 cx_s, double eps, int64_t* slots_total,
-                           int64_t probe_fanout, bool* done);
+                           int64_t probe_fanout, bool* done, int part = 0, int parts = 1);
 
 namespace {
 
@@ -633,7 +633,7 @@ int launch_emit(qx_store* s, const OperatorTable& tb, const ImageTable<K>& im, c
 // *went_dense says whether it did.
 int expand(qx_store* s, const OperatorTable& tb, const uint32_t* program, int n_ops, u32 cx_c,
            u32 cx_t, u32 cx_s, bool narrow_ok, int64_t term_limit, int64_t* raw_total, bool* narrow,
-           double dense_eps = -1.0, bool* went_dense = nullptr) {
+           double dense_eps = -1.0, bool* went_dense = nullptr, int part = 0, int parts = 1) {
   QX_CUDA(cudaSetDevice(s->device));
   u64* roff;
   QX_TRY(count_pass(s, tb, &roff));
@@ -656,7 +656,7 @@ int expand(qx_store* s, const OperatorTable& tb, const uint32_t* program, int n_
   static const int64_t dense_fanout = getenv("QX_DENSE_FANOUT") ? atoll(getenv("QX_DENSE_FANOUT")) : 16;
   if (dense_eps > 0.0 && !no_dense && ub_seg > QX_SMALL_MAX && raw >= dense_fanout * total_in) {
     bool done = false;
-    QX_TRY(qx_dense_operator_step(s, tb, program, n_ops, cx_c, cx_t, cx_s, dense_eps, nullptr, 0, &done));
+    QX_TRY(qx_dense_operator_step(s, tb, program, n_ops, cx_c, cx_t, cx_s, dense_eps, nullptr, 0, &done, part, parts));
     if (went_dense) *went_dense = true;
     return QX_OK;
   }
@@ -710,10 +710,37 @@ extern "C" int qx_apply_operator(qx_store* s, const int32_t* counts, const int32
   return expand(s, tb, nullptr, 0, 0, 0, 0, false, term_limit, raw_total, nullptr);
 }
 
+static int operator_run(qx_store* s, const int32_t* counts, const int32_t* axes, const double* weights,
+                        const uint32_t* program, int32_t n_ops, uint32_t cx_c, uint32_t cx_t, uint32_t cx_s,
+                        double eps, int64_t term_limit, int64_t* raw_total, int64_t* ranks, int part, int parts,
+                        int* partitioned);
+
 extern "C" int qx_apply_operator_run(qx_store* s, const int32_t* counts, const int32_t* axes,
                                      const double* weights, const uint32_t* program, int32_t n_ops,
                                      uint32_t cx_c, uint32_t cx_t, uint32_t cx_s, double eps,
                                      int64_t term_limit, int64_t* raw_total, int64_t* ranks) {
+  return operator_run(s, counts, axes, weights, program, n_ops, cx_c, cx_t, cx_s, eps, term_limit, raw_total,
+                      ranks, 0, 1, nullptr);
+}
+
+extern "C" int qx_apply_operator_run_part(qx_store* s, const int32_t* counts, const int32_t* axes,
+                                          const double* weights, const uint32_t* program, int32_t n_ops,
+                                          uint32_t cx_c, uint32_t cx_t, uint32_t cx_s, double eps,
+                                          int32_t part, int32_t parts, int64_t* ranks, int32_t* partitioned) {
+  QX_REQUIRE(parts >= 1 && part >= 0 && part < parts, "bad part %d of %d", part, parts);
+  QX_REQUIRE(partitioned != nullptr, "partitioned is NULL");
+  int flag = 0;
+  QX_TRY(operator_run(s, counts, axes, weights, program, n_ops, cx_c, cx_t, cx_s, eps, 0, nullptr, ranks, part,
+                      parts, &flag));
+  *partitioned = flag;
+  return QX_OK;
+}
+
+static int operator_run(qx_store* s, const int32_t* counts, const int32_t* axes, const double* weights,
+                        const uint32_t* program, int32_t n_ops, uint32_t cx_c, uint32_t cx_t, uint32_t cx_s,
+                        double eps, int64_t term_limit, int64_t* raw_total, int64_t* ranks, int part, int parts,
+                        int* partitioned) {
+  if (partitioned) *partitioned = 0;
   QX_REQUIRE(s && counts && axes && weights, "NULL argument");
   QX_REQUIRE(n_ops >= 0 && (n_ops == 0 || program), "bad program");
   QX_REQUIRE(eps >= 0.0, "eps must be non-negative");
@@ -745,8 +772,10 @@ extern "C" int qx_apply_operator_run(qx_store* s, const int32_t* counts, const i
     if (total_in > 0 && total_in <= (1 << 16) && max_fanout >= dense_fanout) {
       bool done = false;
       int64_t slots = 0;
-      QX_TRY(qx_dense_operator_step(s, tb, program, n_ops, cx_c, cx_t, cx_s, eps, &slots, dense_fanout, &done));
+      QX_TRY(qx_dense_operator_step(s, tb, program, n_ops, cx_c, cx_t, cx_s, eps, &slots, dense_fanout, &done,
+                                    part, parts));
       if (done) {
+        if (partitioned) *partitioned = parts > 1;
         if (raw_total) *raw_total = slots;
         if (ranks)
           for (int g = 0; g < s->n_seg; ++g) ranks[g] = s->h_seg[g + 1] - s->h_seg[g];
@@ -756,7 +785,9 @@ extern "C" int qx_apply_operator_run(qx_store* s, const int32_t* counts, const i
   }
   static const bool no_narrow = getenv("QX_NO_NARROW") != nullptr;
   bool narrow = false, dense = false;
-  QX_TRY(expand(s, tb, program, n_ops, cx_c, cx_t, cx_s, !no_narrow, term_limit, raw_total, &narrow, eps, &dense));
+  QX_TRY(expand(s, tb, program, n_ops, cx_c, cx_t, cx_s, !no_narrow, term_limit, raw_total, &narrow, eps, &dense,
+                part, parts));
+  if (dense && partitioned) *partitioned = parts > 1;
   if (!dense) QX_TRY(qx_run_merge(s, eps, false, narrow));
   if (ranks)
     for (int g = 0; g < s->n_seg; ++g) ranks[g] = s->h_seg[g + 1] - s->h_seg[g];

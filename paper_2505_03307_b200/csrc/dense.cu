@@ -361,8 +361,8 @@ k_group_emit(const u64* __restrict__ cw, const u64* __restrict__ skey, const dou
              const u64* __restrict__ gsrc, const u64* __restrict__ gslot, const u64* __restrict__ totals,
              const int2* __restrict__ tile_info, const int64_t* __restrict__ seg_slot, int n_seg,
              KO* __restrict__ keys_out, double* __restrict__ lam_out, u64* __restrict__ seg_count,
-             u32* __restrict__ hist, int passes, double eps, const __grid_constant__ OperatorTable tb,
-             const __grid_constant__ ImageTable<K> im) {
+             u32* __restrict__ hist, int passes, double eps, int part, int parts,
+             const __grid_constant__ OperatorTable tb, const __grid_constant__ ImageTable<K> im) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   GroupSmem<K>& sm = *reinterpret_cast<GroupSmem<K>*>(smem_raw);
   const int tid = threadIdx.x, warp = tid >> 5, lane = lane_id();
@@ -380,13 +380,16 @@ k_group_emit(const u64* __restrict__ cw, const u64* __restrict__ skey, const dou
   const int64_t ngroups = (int64_t)totals[0];
   const u64 total = totals[1];
   const int64_t ntiles = (int64_t)((total + kTileSlots - 1) / kTileSlots);
+  // multi-GPU: this device works off the part-th of `parts` contiguous tile ranges (slots are
+  // independent, so the ranges need no communication)
+  const int64_t tile_lo = ntiles * part / parts, tile_hi = ntiles * (part + 1) / parts;
   int cached_group = -1;              // group whose low table is in shared memory
   int hist_seg = -1;                  // generator the shared histogram belongs to
   LowGroup<K> lg = {};
   K cwg = 0;
   u32 magic = 0;
 
-  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+  for (int64_t tile = tile_lo + blockIdx.x; tile < tile_hi; tile += gridDim.x) {
    const u64 t0_slot = (u64)tile * kTileSlots;
    const u64 t1_slot = min(t0_slot + (u64)kTileSlots, total);
    const int2 ti = tile_info[tile];
@@ -834,7 +837,7 @@ template <typename K, typename KO, bool FUSED>
 int launch_group_emit(qx_store* s, int64_t tiles, const u64* cw, const u64* skey, const double* slam,
                       const u64* gsrc, const u64* gslot, const u64* totals, const int2* tile_info,
                       const int64_t* seg_slot, int out, u64* seg_count, u32* hist, int passes, double eps,
-                      const OperatorTable& tb, const ImageTable<K>& im) {
+                      int part, int parts, const OperatorTable& tb, const ImageTable<K>& im) {
   static int per_sm = 0;
   if (per_sm == 0) {
     QX_CUDA(cudaFuncSetAttribute(k_group_emit<K, KO, FUSED>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -843,10 +846,10 @@ int launch_group_emit(qx_store* s, int64_t tiles, const u64* cw, const u64* skey
                                                           sizeof(GroupSmem<K>)));
     per_sm = std::max(per_sm, 1);
   }
-  const int grid = (int)std::min<int64_t>(tiles, (int64_t)s->sm_count * per_sm);
+  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(tiles / parts + 1, (int64_t)s->sm_count * per_sm));
   k_group_emit<K, KO, FUSED><<<grid, kThreads, sizeof(GroupSmem<K>), s->stream>>>(
       cw, skey, slam, gsrc, gslot, totals, tile_info, seg_slot, s->n_seg,
-      reinterpret_cast<KO*>(s->keys[out]), s->lam[out], seg_count, hist, passes, eps, tb, im);
+      reinterpret_cast<KO*>(s->keys[out]), s->lam[out], seg_count, hist, passes, eps, part, parts, tb, im);
   QX_CUDA(cudaGetLastError());
   return QX_OK;
 }
@@ -974,7 +977,7 @@ extern "C" int qx_operator_classes(int32_t n_qubits, const int32_t* counts, cons
 // probe_fanout slots per source), otherwise leave the store untouched and report *done = false.
 int qx_dense_operator_step(qx_store* s, const OperatorTable& nz, const uint32_t* program, int n_ops,
                            u32 cx_c, u32 cx_t, u32 cx_s, double eps, int64_t* slots_total,
-                           int64_t probe_fanout, bool* done) {
+                           int64_t probe_fanout, bool* done, int part, int parts) {
   if (done) *done = false;
   QX_CUDA(cudaSetDevice(s->device));
   const int n_seg = s->n_seg;
@@ -1089,7 +1092,7 @@ int qx_dense_operator_step(qx_store* s, const OperatorTable& nz, const uint32_t*
       memset(&im, 0, sizeof(im));
       if (n_ops > 0) fill_images_u32(s->n_qubits, program, n_ops, cx_c, cx_t, cx_s, &im);
 #define QX_GE(KO, F) launch_group_emit<u32, KO, F>(s, tiles, cwb[sorted], skey, slam, gsrc, gslot, totals, \
-                                                   tile_info, seg_slot, out, seg_count, hist, passes, eps, ct, im)
+                                                   tile_info, seg_slot, out, seg_count, hist, passes, eps, part, parts, ct, im)
       if (n_ops > 0 && narrow) QX_TRY((QX_GE(u32, true)));
       else if (n_ops > 0) QX_TRY((QX_GE(u64, true)));
       else if (narrow) QX_TRY((QX_GE(u32, false)));
@@ -1101,10 +1104,10 @@ int qx_dense_operator_step(qx_store* s, const OperatorTable& nz, const uint32_t*
       if (n_ops > 0) {
         fill_images_u64(s->n_qubits, program, n_ops, cx_c, cx_t, cx_s, &im);
         QX_TRY((launch_group_emit<u64, u64, true>(s, tiles, cwb[sorted], skey, slam, gsrc, gslot, totals,
-                                                  tile_info, seg_slot, out, seg_count, hist, passes, eps, ct, im)));
+                                                  tile_info, seg_slot, out, seg_count, hist, passes, eps, part, parts, ct, im)));
       } else {
         QX_TRY((launch_group_emit<u64, u64, false>(s, tiles, cwb[sorted], skey, slam, gsrc, gslot, totals,
-                                                   tile_info, seg_slot, out, seg_count, hist, passes, eps, ct, im)));
+                                                   tile_info, seg_slot, out, seg_count, hist, passes, eps, part, parts, ct, im)));
       }
     }
   }

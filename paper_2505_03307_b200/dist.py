@@ -15,6 +15,9 @@ the B200-native scale-out of SURVEY.md sections 5.9 / 8e.
   (``exchange_terms``), because that is the only point where equal keys must meet.
   Scalars (ranks for the trace / collapse check) are all-reduced.
 
+* ``run_slot_partitioned`` -- one circuit, every rank takes a range of the output slots of the
+  last branching operator (csrc/dense.cu): even split whatever the skew, no collective.
+
 The functions take an injected ``runner`` / tensors so the host logic (sharding,
 split sizes, gather/assemble) is testable with the gloo backend on CPU; the compute
 always goes through the CUDA library.
@@ -115,6 +118,35 @@ def run_sharded(instructions, n: int, mode, eps: float = 1e-12, *, weights=None,
     if gather:
         report.final = final
     return report, shards
+
+
+def run_slot_partitioned(instructions, n: int, mode, eps: float = 1e-12, *, group=None, runner=None, **run_kw):
+    """One circuit, every rank evolves all generators up to the LAST branching operator (cheap:
+    the rank grows geometrically, so the last operator is nearly all of the work) and then works
+    off its own contiguous range of that operator's output slots -- no data-path collective, and
+    the split is even however skewed the generators are (xyz_chain(16,2): generator 0 alone holds
+    a third of the terms, which caps generator sharding at 3x).
+
+    Returns this rank's RunReport: ``rank_trace`` is global (the shares' counts are all-reduced),
+    ``final.generators[j]`` is this rank's share of generator j in canonical order (shares of
+    different ranks are disjoint; their union is the generator) unless
+    ``report.device['partitioned']`` is False (the operator did not qualify for the grouped path;
+    every rank then holds the complete result).
+    """
+    import torch
+
+    dist = _dist()
+    if runner is None:
+        from .engine import run as runner
+    world, rank = dist.get_world_size(group), dist.get_rank(group)
+    dev = _comm_device(group)
+
+    def reduce(ranks):
+        t = torch.tensor(ranks, dtype=torch.int64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.SUM, group=group)
+        return t.cpu().tolist()
+
+    return runner(instructions, n, mode, eps, slot_part=(rank, world), slot_reduce=reduce, **run_kw)
 
 
 def _gather_generators(report, mine, shards, n, dev, group):

@@ -246,7 +246,8 @@ class _Walker:
 
 def run(instructions: Sequence[Instruction], n: int, mode, eps: float = DEFAULT_EPS, *,
         device=None, generators=None, capacity: int = 0, pinned: bool = False,
-        download: bool = True, initial=None, before_merge=None, reduce_ranks=None) -> RunReport:
+        download: bool = True, initial=None, before_merge=None, reduce_ranks=None,
+        slot_part=None, slot_reduce=None) -> RunReport:
     """Simulate a circuit; returns the canonical final generator set.
 
     Positional arguments and result are the reference's (engine.py:89).  Keyword
@@ -258,7 +259,10 @@ def run(instructions: Sequence[Instruction], n: int, mode, eps: float = DEFAULT_
     store), ``initial`` (list of (lambdas, keys) replacing init_z, for read-out
     back-propagation), ``before_merge(store)`` / ``reduce_ranks(ranks)`` (hooks of the
     term-partitioned multi-GPU mode, see dist.py: re-home terms before a merge that
-    follows a branching step, and turn local ranks into global ones).
+    follows a branching step, and turn local ranks into global ones), ``slot_part=(part,
+    parts)`` / ``slot_reduce(ranks)`` (slot-partitioned multi-GPU mode, dist.run_slot_partitioned:
+    the last branching operator only produces this part's share of every generator;
+    ``report.device['partitioned']`` says whether it did).
     """
     mode = Mode.coerce(mode)
     timings = {"partition": 0.0, "lut": 0.0, "sub_flatten": 0.0, "cx": 0.0}
@@ -308,20 +312,26 @@ def run(instructions: Sequence[Instruction], n: int, mode, eps: float = DEFAULT_
             _walk_operators(partition, lut, is_perm, tables, w, trace, counters, mode, eager)
 
         streamed = None
-        if download and before_merge is None and reduce_ranks is None:
+        partitioned = None
+        if slot_part is not None and before_merge is None and reduce_ranks is None:
+            partitioned = _finish_partitioned(w, trace, slot_part, slot_reduce)
+        elif download and before_merge is None and reduce_ranks is None:
             streamed = _finish_streamed(w, trace, pinned)
         if streamed is None:
             w.finish(trace)              # deferred merge, queued permutations, canonical order
         counters["operators"] = partition.k + partition.k_prime
 
         info = {"device": store.device, **w.launch_log}
+        if partitioned is not None:
+            info["partitioned"] = partitioned
         if w.updates is not None:
             info["updates_per_generator"] = w.updates.tolist()
         final = None
         if download:
             segs = streamed if streamed is not None else store.segments(pinned)
             final_gens = [SimpleGenerator(n, lam, keys_to_indices(keys, n)) for lam, keys in segs]
-            final = GeneratorSet(n, final_gens) if len(final_gens) == n else _Shard(n, ids, final_gens)
+            whole = len(final_gens) == n and not partitioned
+            final = GeneratorSet(n, final_gens) if whole else _Shard(n, ids, final_gens)
         else:
             info["store"] = store
         return RunReport(mode=mode, n=n, final=final, rank_trace=trace, timings=timings,
@@ -407,6 +417,42 @@ def _finish_streamed(w: _Walker, trace, pinned: bool):
         hi, (off, keys, lam) = parts[lo]
         out.extend((lam[off[i]:off[i + 1]], keys[off[i]:off[i + 1]]) for i in range(hi - lo))
     return out
+
+
+def _finish_partitioned(w: _Walker, trace, slot_part, slot_reduce):
+    """Slot-partitioned multi-GPU finish: every device holds the same terms in front of the last
+    branching operator and works off its own range of output slots (qx_apply_operator_run_part).
+    Returns True if the store now holds only this part's share, False if the operator did not take
+    the grouped path (the result is then complete and identical on every device), None if there
+    is no staged operator (the plain finish applies)."""
+    if w.pending is None or w.staged is None:
+        return None
+    part, parts = slot_part
+    counts, axes, weights = w.staged
+    step, phase = w.pending
+    program = np.array(w.queue, dtype=np.uint32)
+    w.queue, w.queue_has_cx, w.staged, w.pending = [], False, None, None
+    t0 = time.perf_counter()
+    ranks, partitioned = w.store.apply_operator_run_part(counts, axes, weights, program, w.eps, part, parts)
+    if partitioned and slot_reduce is not None:
+        ranks = slot_reduce(ranks)              # global ranks: sum of the shares
+    w.timings[phase] += time.perf_counter() - t0
+    w.ranks = list(ranks)
+    w.unsorted = False
+    w.launch_log["merges"] += 1
+    if partitioned is False or slot_reduce is not None or parts == 1:
+        for local, r in enumerate(w.ranks):
+            if r == 0:
+                raise NumericalCollapseError(
+                    f"all terms of generator {w.ids[local]} dropped at operator step {step}"
+                )
+    for slot in w.open_slots:
+        trace[slot] = list(w.ranks)
+    w.open_slots = []
+    if w.updates is not None and w.pending_gates:
+        w.updates += np.asarray(w.ranks, dtype=np.int64) * w.pending_gates
+    w.pending_gates = 0
+    return partitioned
 
 
 @dataclass

@@ -178,6 +178,21 @@ class DeviceStore:
             len(prog), c, t, s, float(eps), int(term_limit), C.byref(raw), nat.ptr(ranks)))
         return raw.value, ranks.tolist()
 
+    def apply_operator_run_part(self, counts, axes, weights, program, eps: float, part: int, parts: int):
+        """The part-th of `parts` slot ranges of U_k + run + merge (multi-GPU, last branching
+        operator); returns (ranks of this share, partitioned flag)."""
+        counts = np.ascontiguousarray(counts, dtype=np.int32).reshape(-1)
+        axes = np.ascontiguousarray(axes, dtype=np.int32).reshape(-1)
+        weights = np.ascontiguousarray(weights, dtype=np.float64).reshape(-1)
+        prog = np.ascontiguousarray(program, dtype=np.uint32)
+        ranks = np.zeros(self.n_segments, dtype=np.int64)
+        flag = C.c_int32()
+        c, t, s = self._cx
+        nat.check(nat.lib().qx_apply_operator_run_part(
+            self._h, nat.ptr(counts), nat.ptr(axes), nat.ptr(weights), nat.ptr(prog) if len(prog) else None,
+            len(prog), c, t, s, float(eps), int(part), int(parts), nat.ptr(ranks), C.byref(flag)))
+        return ranks.tolist(), bool(flag.value)
+
     def count_operator(self, counts) -> list:
         counts = np.ascontiguousarray(counts, dtype=np.int32).reshape(-1)
         out = np.zeros(self.n_segments, dtype=np.int64)

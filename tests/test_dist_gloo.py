@@ -62,6 +62,31 @@ def _worker(rank, world, port, out_dir):
         report, shards = qd.run_sharded(workloads.gen_ghz(1) if False else [], 1, "v1", runner=_fake_runner)
         assert report.rank_trace == [[1]] and int(report.final.generators[0].indices[0]) == 3
 
+        # ---- slot-partitioned run: the runner gets (rank, world) and a reduction that sums the
+        # shares' counts over the ranks; the fake answers with an index-range share of the
+        # oracle's result (what the device's slot ranges amount to after the sort)
+        def _slot_runner(instructions, n, mode, eps=1e-12, *, slot_part=None, slot_reduce=None, **kw):
+            from paper_2505_03307_b200.engine import Mode, RunReport, _Shard
+            from paper_2505_03307_b200.stabilizer import SimpleGenerator, keys_to_indices
+
+            part, parts = slot_part
+            res = oracle.run(instructions, n, mode, eps)
+            gens, local = [], []
+            for lam, idx in res["final"]:
+                sel = np.arange(len(idx)) % parts == part
+                gens.append(SimpleGenerator(n, lam[sel], keys_to_indices(idx[sel], n)))
+                local.append(int(sel.sum()))
+            trace = res["rank_trace"][:-1] + [slot_reduce(local)]
+            return RunReport(Mode.coerce(mode), n, _Shard(n, list(range(n)), gens), trace, {}, res["counters"],
+                             res["k"], res["k_prime"], res["order"], {"partitioned": True})
+
+        rep = qd.run_slot_partitioned(gates, n, "v3", runner=_slot_runner)
+        assert rep.rank_trace == want["rank_trace"] and rep.device["partitioned"] is True
+        mine = sum(g.rank for g in rep.final.generators)
+        t = torch.tensor([mine], dtype=torch.int64)
+        dist.all_reduce(t)
+        assert int(t.item()) == sum(want["rank_trace"][-1])
+
         # ---- all-to-all-v of hash-partitioned terms
         rng = np.random.default_rng(100 + rank)
         n_seg = 3

@@ -70,3 +70,32 @@ def test_exchange_terms_loopback(nccl_world1):
         assert counts.shape == (1, 3) and counts[0].tolist() == [3000, 0, 50_000]
         for (lam, keys), (gl, gk) in zip(gens, st.segments()):
             assert np.array_equal(gk, keys) and np.array_equal(gl, lam)     # world = 1: order kept
+
+
+@pytest.mark.parametrize("name,parts", [("c4_xyz_12_2", 3), ("c4_xyz_10_3", 2)])
+def test_slot_partition_shares_union_to_the_full_result(name, parts):
+    """run(..., slot_part=(p, parts)): the shares of the parts are disjoint, canonical, and their
+    union is the plain result -- checked here part by part on one GPU (what run_slot_partitioned
+    does on `parts` GPUs, where only the share counts are all-reduced)."""
+    n, gates = workloads.build(name)
+    plain = qx.run(gates, n, "v3")
+    shares = [qx.run(gates, n, "v3", slot_part=(p, parts)) for p in range(parts)]
+    assert all(s.device["partitioned"] is True for s in shares)
+    for j, g in enumerate(plain.final.generators):
+        keys = np.concatenate([s.final.generators[j].keys() for s in shares])
+        lam = np.concatenate([s.final.generators[j].lambdas for s in shares])
+        for s in shares:
+            k = s.final.generators[j].keys()
+            assert np.all(k[1:] > k[:-1])                       # every share is canonical
+        order = np.argsort(keys, kind="stable")
+        assert np.array_equal(keys[order], g.keys()) and np.array_equal(lam[order], g.lambdas)
+    assert [sum(col) for col in zip(*[s.rank_trace[-1] for s in shares])] == plain.rank_trace[-1]
+
+
+def test_run_slot_partitioned_world1(nccl_world1):
+    n, gates = workloads.build("c4_xyz_12_2")
+    plain = qx.run(gates, n, "v3")
+    rep = qd.run_slot_partitioned(gates, n, "v3")
+    assert rep.rank_trace == plain.rank_trace
+    for ga, gb in zip(rep.final.generators, plain.final.generators):
+        assert np.array_equal(ga.keys(), gb.keys()) and np.array_equal(ga.lambdas, gb.lambdas)
