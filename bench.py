@@ -22,9 +22,12 @@ any exact method).
 
 N > 1 (torchrun), default --scaling weak: every rank evolves one whole circuit instance of the
 workload (same ansatz and shape, its own rotation angles), so per-GPU work is fixed and value is
-the sum of the ranks' update counts over the slowest rank's time.  --scaling strong: ONE circuit,
-its generators sharded over the ranks (LPT on rank; they evolve independently).  Either way there
-is no data-path collective; the only NCCL traffic is the barrier and the max/sum of scalars.
+the sum of the ranks' update counts over the slowest rank's time.  --scaling strong: ONE circuit;
+every rank evolves it up to the last branching operator (a negligible share of the work) and then
+works off its own contiguous range of that operator's output slots (dist.run_slot_partitioned:
+even split however skewed the generators are; generator sharding caps at ~3x here because
+generator 0 holds a third of the terms).  Either way there is no data-path collective; the only
+NCCL traffic is the barrier and the max/sum of scalars (the shares' counts in strong mode).
 --impl reference runs the CPU arm.
 """
 
@@ -236,8 +239,11 @@ def run_ours(args):
         dist.all_reduce(t, op=dist.ReduceOp.SUM)
         total_updates = float(t.item())
     else:
-        mine = lpt_shards(final_ranks, world)[rank]
-    my_cap = int(sum(final_ranks[g] for g in mine) * 2.6) + 1024
+        mine = list(range(n))                      # strong: all generators, my range of the output slots
+    strong = world > 1 and not weak
+    my_cap = int(sum(final_ranks[g] for g in mine) * 2.6 / (world if strong else 1)) + 1024
+    if strong:
+        from paper_2505_03307_b200 import dist as qd
 
     def barrier():
         if dist is not None:
@@ -245,11 +251,16 @@ def run_ours(args):
         torch.cuda.synchronize()
 
     def step_resident():
-        rep = qx.run(gates, n, args.mode, device=device, generators=mine, capacity=my_cap, download=False)
+        if strong:
+            rep = qd.run_slot_partitioned(gates, n, args.mode, device=device, capacity=my_cap, download=False)
+        else:
+            rep = qx.run(gates, n, args.mode, device=device, generators=mine, capacity=my_cap, download=False)
         rep.device["store"].close()
         return rep
 
     def step_e2e():
+        if strong:
+            return qd.run_slot_partitioned(gates, n, args.mode, device=device, capacity=my_cap, pinned=True)
         return qx.run(gates, n, args.mode, device=device, generators=mine, capacity=my_cap, pinned=True)
 
     for _ in range(max(args.warmup, 3)):
@@ -341,7 +352,8 @@ def run_ours(args):
         "config": {"workload": args.workload, "mode": args.mode, "qubits": n, "gates": len(gates),
                    "term_gate_updates": total_updates, "final_terms": int(sum(final_ranks)),
                    "parallelism": (f"{world} circuit instance(s), one per GPU, all generators of an instance on its GPU"
-                                   if (weak or world == 1) else f"one circuit, generator shards x{world} (LPT on rank)"),
+                                   if (weak or world == 1) else
+                                   f"one circuit, output slots of the last operator split over {world} GPUs"),
                    "l2": "inputs larger than L2: every pass streams 2-5 GB per GPU, L2 is 126 MB"},
         "e2e": {"value": total_updates / e2e_s, "unit": "updates/s", "ms_per_step": e2e_s * 1e3,
                 "h2d_bytes_per_step": table_bytes(n, gates), "d2h_bytes_per_step": d2h},
