@@ -8,12 +8,13 @@ and raises ``NativeError`` if ``lib/libqimax_b200.so`` or a CUDA device is missi
 (there is no CPU fallback).
 """
 
-from .circuit import Instruction, divide_instruction
+from .circuit import CircuitParseError, Instruction, divide_instruction, parse_circuit, serialize_circuit
 from .engine import AgreementReport, Mode, RunReport, compare_reports, run, run_all_modes
 from .errors import ConsistencyError, NativeError, NumericalCollapseError, ResourceLimitError
 from .measure import PauliExpansion, density_expansion, expectation, expectation_heisenberg, prob_z
 from .stabilizer import (
     GeneratorSet,
+    generator_set_to_dict,
     SimpleGenerator,
     apply_1q,
     apply_cx,
@@ -28,10 +29,10 @@ from .workloads import gen_ghz, gen_graph, gen_random, gen_xyz_chain, near_cliff
 __version__ = "0.1.0"
 
 __all__ = [
-    "AgreementReport", "ConsistencyError", "GeneratorSet", "Instruction", "Mode", "NativeError",
+    "AgreementReport", "CircuitParseError", "ConsistencyError", "GeneratorSet", "Instruction", "Mode", "NativeError",
     "NumericalCollapseError", "PauliExpansion", "ResourceLimitError", "RunReport", "SimpleGenerator",
     "apply_1q", "apply_cx", "canonicalize", "compare_reports", "density_expansion",
     "divide_instruction", "expectation", "expectation_heisenberg", "flatten", "gen_ghz", "gen_graph",
-    "gen_random", "gen_xyz_chain", "init_z", "near_clifford", "prob_z", "rank_stats", "ring_edges",
-    "run", "run_all_modes", "sub",
+    "gen_random", "gen_xyz_chain", "generator_set_to_dict", "init_z", "near_clifford", "parse_circuit", "prob_z", "rank_stats", "ring_edges",
+    "run", "run_all_modes", "serialize_circuit", "sub",
 ]

@@ -157,3 +157,81 @@ def divide_instruction(instructions: Sequence[Instruction], n: int) -> OperatorP
         else:
             part.u_groups[-1].setdefault(inst.wires[0], []).append(inst)
     return part
+
+
+# ---------------------------------------------------------------------------------------------
+# circuit files: the reference's text and JSON formats (circuit.py:281-352)
+# ---------------------------------------------------------------------------------------------
+class CircuitParseError(ValueError):
+    """Malformed circuit text; ``line_no`` is 1-based (reference circuit.py:36-41)."""
+
+    def __init__(self, line_no: int, message: str):
+        super().__init__(f"line {line_no}: {message}")
+        self.line_no = line_no
+
+
+def serialize_circuit(instructions: Sequence[Instruction]) -> str:
+    """One instruction per line: lower-case gate, wires, and for rotations ``repr(theta)`` so
+    that the angle survives the round trip bit for bit."""
+    out = []
+    for inst in instructions:
+        fields = [inst.gate.lower(), *(str(w) for w in inst.wires)]
+        if inst.gate in ROTATIONS:
+            fields.append(repr(inst.theta))
+        out.append(" ".join(fields) + "\n")
+    return "".join(out)
+
+
+def _instruction_or_error(where: int, gate: str, wires, theta: float) -> Instruction:
+    try:
+        return Instruction(gate, tuple(wires), theta)
+    except ValueError as exc:
+        raise CircuitParseError(where, str(exc)) from None
+
+
+def parse_circuit(text: str) -> list:
+    """Text form (``#`` starts a comment, blank lines are skipped) or, if the text starts with
+    ``[``, a JSON array of ``{"gate", "wires", "theta"?}`` objects."""
+    import json
+
+    body = text.lstrip()
+    if body.startswith("["):
+        try:
+            entries = json.loads(body)
+        except json.JSONDecodeError as exc:
+            raise CircuitParseError(exc.lineno, f"invalid JSON: {exc.msg}") from None
+        result = []
+        for pos, entry in enumerate(entries, start=1):
+            if not isinstance(entry, dict) or "gate" not in entry or "wires" not in entry:
+                raise CircuitParseError(pos, "each entry needs 'gate' and 'wires'")
+            result.append(_instruction_or_error(pos, str(entry["gate"]).upper(),
+                                                (int(w) for w in entry["wires"]), float(entry.get("theta", 0.0))))
+        return result
+    result = []
+    for line_no, raw in enumerate(text.splitlines(), start=1):
+        tokens = raw.split("#", 1)[0].split()
+        if not tokens:
+            continue
+        gate = tokens[0].upper()
+        if gate not in ALL_GATES:
+            raise CircuitParseError(line_no, f"unknown gate {tokens[0]!r}")
+        n_wires = 2 if gate in TWO_QUBIT else 1
+        wire_tokens, extra = tokens[1:1 + n_wires], tokens[1 + n_wires:]
+        try:
+            wires = [int(t) for t in wire_tokens]
+        except ValueError:
+            raise CircuitParseError(line_no, f"malformed wires {wire_tokens}") from None
+        if len(wires) != n_wires:
+            raise CircuitParseError(line_no, f"{gate} takes {n_wires} wire(s)")
+        theta = 0.0
+        if gate in ROTATIONS:
+            if len(extra) != 1:
+                raise CircuitParseError(line_no, f"{gate} requires exactly one angle")
+            try:
+                theta = float(extra[0])
+            except ValueError:
+                raise CircuitParseError(line_no, f"malformed angle {extra[0]!r}") from None
+        elif extra:
+            raise CircuitParseError(line_no, f"{gate} takes no angle, got {extra}")
+        result.append(_instruction_or_error(line_no, gate, wires, theta))
+    return result
