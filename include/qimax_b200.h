@@ -20,7 +20,8 @@
  *                  axis codes I=0 X=1 Y=2 Z=3 (reference pauli.py:24-30,67-86).  With
  *                  code bits (hi,lo): z = hi, x = hi ^ lo, so this *is* the packed
  *                  2-bit x/z form, ordered so that unsigned integer order equals the
- *                  reference's canonical order.  n_qubits <= 32 (one word).
+ *                  reference's canonical order.  n_qubits <= 32 (one word); wider systems use
+ *                  several words per key on a restricted path, see "more than 32 qubits" below.
  *   lambda float64 real coefficient (reference stabilizer.py:92).
  * A store holds n_segments generators back to back; offsets[s]..offsets[s+1] is
  * generator s.  16 bytes per term.
@@ -93,6 +94,27 @@ int qx_store_slice(qx_store* src, int32_t seg_lo, int32_t seg_hi, int64_t capaci
  * qx_store_synchronize(s). */
 int qx_store_download_async(qx_store* s, int64_t* offsets, uint64_t* keys, double* lambdas,
                             int64_t cap_terms);
+
+/* ---- more than 32 qubits (reference stabilizer.py:40-59 switches to Python
+ * big-int indices there).  qx_store_create accepts n_qubits <= 256; above 32 the store is WIDE:
+ * W = ceil(2n/64) words per key.  Wide stores run the part of the path that such circuits use --
+ * Clifford runs, v1 rotations, merge/sort of generators up to 16384/W raw terms, ranks, norms --
+ * through the calls below plus qx_store_init_z / qx_merge / qx_sort / qx_store_ranks /
+ * qx_store_norms; every other entry point returns QX_ERR_UNSUPPORTED on a wide store.
+ * Host layout of wide keys: term-major uint64[term][W], word 0 least significant. */
+int qx_store_words(qx_store* s, int32_t* n_words);
+int qx_store_upload_wide(qx_store* s, const int64_t* offsets, const uint64_t* words,
+                         const double* lambdas);
+int qx_store_download_wide(qx_store* s, int64_t* offsets, uint64_t* words, double* lambdas,
+                           int64_t cap_terms);
+/* As qx_apply_clifford with 64-bit ops: low word as there (kind, image axes, signs; the shift
+ * fields unused), bits 32-47 = bit position 2*(n-1-q) of the (control) digit, 48-63 of the target. */
+int qx_apply_clifford_wide(qx_store* s, const uint64_t* ops, int32_t n_ops, uint32_t cx_c,
+                           uint32_t cx_t, uint32_t cx_s);
+/* As qx_apply_split; every term yields two entries (an absent second branch becomes a zero-weight
+ * copy of the first), so the store doubles; qx_merge follows. */
+int qx_apply_split_wide(qx_store* s, int32_t qubit, const int32_t a1[4], const double w1[4],
+                        const int32_t a2[4], const double w2[4]);
 
 /* ---- a2 + Clifford part of a3: fused run of sign-permutation gates ----------
  * Replaces apply_cx (stabilizer.py:340-363) and _apply_1q_terms (engine.py:183-218)

@@ -52,6 +52,11 @@ SIGNATURES = {
     "qx_store_capacity": (C.c_int, [_p, _P(_i64), _P(_i64)]),
     "qx_store_synchronize": (C.c_int, [_p]),
     "qx_store_slice": (C.c_int, [_p, _i32, _i32, _i64, _P(_p)]),
+    "qx_store_words": (C.c_int, [_p, _P(_i32)]),
+    "qx_store_upload_wide": (C.c_int, [_p, _p, _p, _p]),
+    "qx_store_download_wide": (C.c_int, [_p, _p, _p, _p, _i64]),
+    "qx_apply_clifford_wide": (C.c_int, [_p, _p, _i32, _u32, _u32, _u32]),
+    "qx_apply_split_wide": (C.c_int, [_p, _i32, _p, _p, _p, _p]),
     "qx_store_download_async": (C.c_int, [_p, _p, _p, _p, _i64]),
     "qx_apply_clifford": (C.c_int, [_p, _p, _i32, _u32, _u32, _u32]),
     "qx_apply_split": (C.c_int, [_p, _i32, _p, _p, _p, _p]),

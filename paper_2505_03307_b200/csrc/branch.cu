@@ -478,6 +478,7 @@ int prepare_lookback(qx_store* s, int64_t tiles, u64** status, u32** ticket) {
 extern "C" int qx_apply_split(qx_store* s, int32_t qubit, const int32_t a1[4], const double w1[4],
                               const int32_t a2[4], const double w2[4]) {
   QX_REQUIRE(s && a1 && w1 && a2 && w2, "NULL argument");
+  QX_NARROW_ONLY(s, "qx_apply_split");
   QX_REQUIRE(qubit >= 0 && qubit < s->n_qubits, "qubit %d out of range for n=%d", qubit, s->n_qubits);
   SplitTable tb;
   tb.shift = 2u * (u32)(s->n_qubits - 1 - qubit);
@@ -534,6 +535,7 @@ static int count_pass(qx_store* s, const OperatorTable& tb, u64** roff_out) {
 
 extern "C" int qx_count_operator(qx_store* s, const int32_t* counts, int64_t* raw_per_segment) {
   QX_REQUIRE(s && counts && raw_per_segment, "NULL argument");
+  QX_NARROW_ONLY(s, "qx_count_operator");
   OperatorTable tb;
   QX_TRY(fill_table(s, counts, nullptr, nullptr, &tb));
   QX_CUDA(cudaSetDevice(s->device));
@@ -705,6 +707,7 @@ int expand(qx_store* s, const OperatorTable& tb, const uint32_t* program, int n_
 extern "C" int qx_apply_operator(qx_store* s, const int32_t* counts, const int32_t* axes,
                                  const double* weights, int64_t term_limit, int64_t* raw_total) {
   QX_REQUIRE(s && counts && axes && weights, "NULL argument");
+  QX_NARROW_ONLY(s, "qx_apply_operator (branching U_k)");
   OperatorTable tb;
   QX_TRY(fill_table(s, counts, axes, weights, &tb));
   return expand(s, tb, nullptr, 0, 0, 0, 0, false, term_limit, raw_total, nullptr);
@@ -742,6 +745,7 @@ static int operator_run(qx_store* s, const int32_t* counts, const int32_t* axes,
                         int* partitioned) {
   if (partitioned) *partitioned = 0;
   QX_REQUIRE(s && counts && axes && weights, "NULL argument");
+  QX_NARROW_ONLY(s, "qx_apply_operator_run (branching U_k)");
   QX_REQUIRE(n_ops >= 0 && (n_ops == 0 || program), "bad program");
   QX_REQUIRE(eps >= 0.0, "eps must be non-negative");
   OperatorTable tb;

@@ -234,6 +234,7 @@ int qx_check_program(const qx_store* s, const uint32_t* program, int32_t n_ops) 
 extern "C" int qx_apply_clifford(qx_store* s, const uint32_t* program, int32_t n_ops, uint32_t cx_c,
                                  uint32_t cx_t, uint32_t cx_s) {
   QX_TRY(qx_check_program(s, program, n_ops));
+  QX_NARROW_ONLY(s, "qx_apply_clifford");
   if (n_ops == 0) return QX_OK;
   QX_CUDA(cudaSetDevice(s->device));
   const int64_t ub = std::max<int64_t>(s->ub_total, 1);

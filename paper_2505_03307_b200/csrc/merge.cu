@@ -4,6 +4,8 @@
 #include "merge.cuh"
 
 int qx_run_merge(qx_store* s, double eps, bool sort_only, bool narrow) {
+  // multi-word keys: one CTA per generator (wide.cu); a sort is a merge that drops nothing
+  if (s->n_words > 1) return qx_wide_merge(s, sort_only ? 0.0 : eps);
   if (s->ub_seg > QX_SMALL_MAX && !s->exact) QX_TRY(qx_store_refresh(s));
   // both paths write into the other buffer; make sure it can hold the raw terms
   qxm::MergeBuffers<double> mb;
@@ -121,5 +123,9 @@ extern "C" int qx_sort(qx_store* s) {
   return qx_run_merge(s, 0.0, true, false);
 }
 
-extern "C" int qx_store_zi_sums(qx_store* s, double* sums) { return segment_reduce<0>(s, sums); }
+extern "C" int qx_store_zi_sums(qx_store* s, double* sums) {
+  QX_REQUIRE(s != nullptr, "store is NULL");
+  QX_NARROW_ONLY(s, "qx_store_zi_sums");
+  return segment_reduce<0>(s, sums);
+}
 extern "C" int qx_store_norms(qx_store* s, double* sum_sq) { return segment_reduce<1>(s, sum_sq); }

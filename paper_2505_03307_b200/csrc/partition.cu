@@ -88,6 +88,7 @@ k_partition_select(const u64* __restrict__ keys_in, const double* __restrict__ l
 }  // namespace
 
 extern "C" int qx_store_partition_by_owner(qx_store* s, int32_t world, int64_t* send_counts) {
+  if (s) QX_NARROW_ONLY(s, "qx_store_partition_by_owner");
   QX_REQUIRE(s && send_counts, "NULL argument");
   QX_REQUIRE(world >= 1 && world <= 64, "world size %d out of range", world);
   QX_CUDA(cudaSetDevice(s->device));
@@ -134,6 +135,7 @@ extern "C" int qx_store_partition_by_owner(qx_store* s, int32_t world, int64_t* 
 
 extern "C" int qx_store_assemble(qx_store* s, const uint64_t* d_keys, const double* d_lambdas,
                                  int32_t world, const int64_t* recv_counts) {
+  if (s) QX_NARROW_ONLY(s, "qx_store_assemble");
   QX_REQUIRE(s && recv_counts, "NULL argument");
   QX_REQUIRE(world >= 1 && world <= 64, "world size %d out of range", world);
   QX_CUDA(cudaSetDevice(s->device));

@@ -54,7 +54,9 @@ bool qx_profile_on();
 // ----------------------------------------------------------------------------
 // geometry of the device-wide passes
 // ----------------------------------------------------------------------------
-constexpr int QX_MAX_QUBITS = 32;
+constexpr int QX_MAX_QUBITS = 32;         // one-word keys: every kernel
+constexpr int QX_MAX_WORDS = 8;           // multi-word keys (wide.cu): Clifford / v1 path, n <= 256
+constexpr int QX_MAX_QUBITS_WIDE = 32 * QX_MAX_WORDS;
 constexpr int QX_RADIX_BITS = 8;
 constexpr int QX_RADIX = 1 << QX_RADIX_BITS;
 constexpr int QX_SORT_THREADS = 384;     // 12 warps
@@ -108,6 +110,8 @@ struct qx_store : QxArena {
   u64* keys[2] = {nullptr, nullptr};
   double* lam[2] = {nullptr, nullptr};
   int64_t* seg[2] = {nullptr, nullptr};   // device offsets, n_seg+1 each
+  int n_words = 1;              // 64-bit words per key; > 1 = wide store (wide.cu)
+  u64* hi[2] = {nullptr, nullptr};        // words 1..n_words-1, plane-major, `cap` words per plane
   int cur = 0;                  // which of the two buffers is live
   int64_t* h_seg = nullptr;     // pinned host mirror of the live offsets
   bool exact = false;           // h_seg matches the device
@@ -128,3 +132,12 @@ int qx_check_program(const qx_store* s, const uint32_t* program, int32_t n_ops);
 void qx_standard_cx(u32* cx_c, u32* cx_t, u32* cx_s);
 // merge.cu: canonicalize (or only sort) the live buffer; narrow = it holds 32-bit raw keys
 int qx_run_merge(qx_store* s, double eps, bool sort_only, bool narrow);
+// wide.cu: the merge of a multi-word store (one CTA per generator)
+int qx_wide_merge(qx_store* s, double eps);
+// entry points that only exist for one-word keys refuse wide stores with this
+#define QX_NARROW_ONLY(s, what)                                                                      \
+  do {                                                                                               \
+    if ((s)->n_words > 1)                                                                            \
+      return qx_fail(QX_ERR_UNSUPPORTED, "%s needs one-word keys (n <= %d); this store has n = %d", \
+                     what, QX_MAX_QUBITS, (s)->n_qubits);                                            \
+  } while (0)

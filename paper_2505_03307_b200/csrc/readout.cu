@@ -268,6 +268,7 @@ extern "C" int qx_expansion_multiply(qx_expansion* e, const uint64_t* keys, cons
 extern "C" int qx_expansion_multiply_segment(qx_expansion* e, qx_store* s, int32_t segment,
                                              int64_t term_budget) {
   QX_REQUIRE(e && s, "NULL argument");
+  QX_NARROW_ONLY(s, "qx_expansion_multiply_segment");
   QX_REQUIRE(segment >= 0 && segment < s->n_seg, "segment %d out of range", segment);
   QX_REQUIRE(e->device == s->device, "store and expansion live on different devices");
   if (!s->exact) QX_TRY(qx_store_refresh(s));

@@ -345,9 +345,9 @@ extern "C" int qx_store_create(int device, int n_qubits, int n_segments, int64_t
   QX_REQUIRE(out != nullptr, "out is NULL");
   *out = nullptr;
   if (n_qubits < 1) return qx_fail(QX_ERR_INVALID, "qubit count must be positive, got %d", n_qubits);
-  if (n_qubits > QX_MAX_QUBITS)
-    return qx_fail(QX_ERR_UNSUPPORTED, "n_qubits=%d: keys are one 64-bit word (n <= %d)", n_qubits,
-                   QX_MAX_QUBITS);
+  if (n_qubits > QX_MAX_QUBITS_WIDE)
+    return qx_fail(QX_ERR_UNSUPPORTED, "n_qubits=%d: keys hold at most %d words (n <= %d)", n_qubits,
+                   QX_MAX_WORDS, QX_MAX_QUBITS_WIDE);
   QX_REQUIRE(n_segments >= 1 && n_segments <= (1 << 20), "bad segment count %d", n_segments);
   qx_store* s = new qx_store();
   {
@@ -358,8 +358,11 @@ extern "C" int qx_store_create(int device, int n_qubits, int n_segments, int64_t
     }
   }
   s->n_seg = n_segments;
+  s->n_words = n_qubits <= QX_MAX_QUBITS ? 1 : (2 * n_qubits + 63) / 64;
   s->cap = std::max<int64_t>(capacity_terms, std::max<int64_t>(4096, 2 * (int64_t)n_segments));
   int st = alloc_buffers(s, s->cap, s->keys, s->lam);
+  for (int b = 0; b < 2 && st == QX_OK && s->n_words > 1; ++b)
+    st = qx_dev_alloc_t(&s->hi[b], s->cap * (s->n_words - 1), s->stream, s->device);
   if (st == QX_OK) {
     cudaError_t e = cudaSuccess;
     for (int b = 0; b < 2 && st == QX_OK; ++b)
@@ -388,6 +391,7 @@ extern "C" int qx_store_destroy(qx_store* s) {
     qx_dev_free(s->keys[b], s->stream);
     qx_dev_free(s->lam[b], s->stream);
     qx_dev_free(s->seg[b], s->stream);
+    qx_dev_free(s->hi[b], s->stream);
   }
   qx_pinned_free(s->h_seg);
   qx_arena_release(s);
@@ -405,6 +409,7 @@ extern "C" int qx_store_slice(qx_store* src, int32_t seg_lo, int32_t seg_hi, int
   QX_REQUIRE(src && out, "NULL argument");
   QX_REQUIRE(seg_lo >= 0 && seg_lo < seg_hi && seg_hi <= src->n_seg, "bad segment range [%d, %d) of %d",
              seg_lo, seg_hi, src->n_seg);
+  QX_NARROW_ONLY(src, "qx_store_slice");
   *out = nullptr;
   QX_CUDA(cudaSetDevice(src->device));
   if (!src->exact) QX_TRY(qx_store_refresh(src));
@@ -457,6 +462,8 @@ int qx_store_reserve(qx_store* s, int64_t terms, bool keep_live) {
   QX_CUDA(cudaSetDevice(s->device));
   if (keep_live && !s->exact) QX_TRY(qx_store_refresh(s));
   const int64_t live = keep_live ? s->h_seg[s->n_seg] : 0;
+  const int64_t old_cap = s->cap;
+  const int old_cur = s->cur;
   // One buffer pair at a time so the peak is old + new, not 2x new.  Try generous growth
   // first, fall back to the exact need when HBM is tight.
   const int dead = s->cur ^ 1, old = s->cur;
@@ -502,6 +509,19 @@ int qx_store_reserve(qx_store* s, int64_t terms, bool keep_live) {
   }
   s->cur = dead;
   s->cap = want;
+  if (s->n_words > 1) {
+    // the upper words: new planes of the new capacity, live part of every plane copied across
+    u64* fresh[2] = {nullptr, nullptr};
+    for (int b = 0; b < 2; ++b) QX_TRY(qx_dev_alloc_t(&fresh[b], want * (s->n_words - 1), s->stream, s->device));
+    for (int w = 1; w < s->n_words && live > 0; ++w)
+      QX_CUDA(cudaMemcpyAsync(fresh[s->cur] + (size_t)(w - 1) * (size_t)want,
+                              s->hi[old_cur] + (size_t)(w - 1) * (size_t)old_cap, sizeof(u64) * (size_t)live,
+                              cudaMemcpyDeviceToDevice, s->stream));
+    for (int b = 0; b < 2; ++b) {
+      qx_dev_free(s->hi[b], s->stream);
+      s->hi[b] = fresh[b];
+    }
+  }
   return QX_OK;
 }
 
@@ -597,6 +617,7 @@ int qx_store_refresh(qx_store* s) {
 extern "C" int qx_store_upload(qx_store* s, const int64_t* offsets, const uint64_t* keys,
                                const double* lambdas) {
   QX_REQUIRE(s && offsets, "NULL argument");
+  QX_NARROW_ONLY(s, "qx_store_upload");
   QX_REQUIRE(offsets[0] == 0, "offsets[0] must be 0");
   for (int g = 0; g < s->n_seg; ++g)
     QX_REQUIRE(offsets[g + 1] >= offsets[g], "offsets must be non-decreasing (segment %d)", g);
@@ -628,8 +649,26 @@ extern "C" int qx_store_upload(qx_store* s, const int64_t* offsets, const uint64
   return QX_OK;
 }
 
+extern "C" int qx_store_upload_wide(qx_store* s, const int64_t* offsets, const uint64_t* words,
+                                    const double* lambdas);
+
 extern "C" int qx_store_init_z(qx_store* s, const int32_t* qubits) {
   QX_REQUIRE(s != nullptr, "store is NULL");
+  if (s->n_words > 1) {
+    const int W = s->n_words;
+    std::vector<int64_t> off(s->n_seg + 1);
+    std::vector<uint64_t> words((size_t)s->n_seg * W, 0ull);
+    std::vector<double> lam(s->n_seg, 1.0);
+    for (int g = 0; g < s->n_seg; ++g) {
+      const int q = qubits ? qubits[g] : g;
+      QX_REQUIRE(q >= 0 && q < s->n_qubits, "qubit %d out of range for n=%d", q, s->n_qubits);
+      const int pos = 2 * (s->n_qubits - 1 - q);
+      off[g] = g;
+      words[(size_t)g * W + (pos >> 6)] = 3ull << (pos & 63);
+    }
+    off[s->n_seg] = s->n_seg;
+    return qx_store_upload_wide(s, off.data(), words.data(), lam.data());
+  }
   std::vector<int64_t> off(s->n_seg + 1);
   std::vector<uint64_t> keys(s->n_seg);
   std::vector<double> lam(s->n_seg, 1.0);
@@ -657,6 +696,7 @@ extern "C" int qx_store_download(qx_store* s, int64_t* offsets, uint64_t* keys, 
   memcpy(offsets, s->h_seg, sizeof(int64_t) * (size_t)(s->n_seg + 1));
   const int64_t total = s->h_seg[s->n_seg];
   if (keys == nullptr && lambdas == nullptr) return QX_OK;
+  QX_NARROW_ONLY(s, "qx_store_download");
   QX_REQUIRE(cap_terms >= total, "download buffer holds %lld terms, store has %lld",
              (long long)cap_terms, (long long)total);
   QX_CUDA(cudaSetDevice(s->device));
@@ -675,6 +715,7 @@ extern "C" int qx_store_download(qx_store* s, int64_t* offsets, uint64_t* keys, 
 extern "C" int qx_store_download_async(qx_store* s, int64_t* offsets, uint64_t* keys, double* lambdas,
                                        int64_t cap_terms) {
   QX_REQUIRE(s && offsets && keys && lambdas, "NULL argument");
+  QX_NARROW_ONLY(s, "qx_store_download_async");
   if (!s->exact) QX_TRY(qx_store_refresh(s));
   memcpy(offsets, s->h_seg, sizeof(int64_t) * (size_t)(s->n_seg + 1));
   const int64_t total = s->h_seg[s->n_seg];
@@ -693,6 +734,7 @@ extern "C" int qx_store_download_async(qx_store* s, int64_t* offsets, uint64_t* 
 extern "C" int qx_store_device_view(qx_store* s, const uint64_t** d_keys, const double** d_lambdas,
                                     const int64_t** d_offsets) {
   QX_REQUIRE(s != nullptr, "store is NULL");
+  QX_NARROW_ONLY(s, "qx_store_device_view");
   if (d_keys) *d_keys = (const uint64_t*)s->keys[s->cur];
   if (d_lambdas) *d_lambdas = s->lam[s->cur];
   if (d_offsets) *d_offsets = s->seg[s->cur];
@@ -702,7 +744,7 @@ extern "C" int qx_store_device_view(qx_store* s, const uint64_t** d_keys, const 
 extern "C" int qx_store_capacity(qx_store* s, int64_t* capacity_terms, int64_t* hbm_bytes) {
   QX_REQUIRE(s != nullptr, "store is NULL");
   if (capacity_terms) *capacity_terms = s->cap;
-  if (hbm_bytes) *hbm_bytes = 32 * s->cap + s->scratch_bytes + 4 * s->status_words;
+  if (hbm_bytes) *hbm_bytes = (32 + 16 * (s->n_words - 1)) * s->cap + s->scratch_bytes + 4 * s->status_words;
   return QX_OK;
 }
 

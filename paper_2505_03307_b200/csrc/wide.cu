@@ -1,0 +1,394 @@
+// More than 32 qubits: multi-word keys.
+//
+// The reference switches to Python big-int indices above 31 qubits (stabilizer.py:40-59) so that
+// Clifford and near-Clifford circuits run at any width -- their stabilizer rank stays tiny.  On
+// the device a wide store keeps W = ceil(2n / 64) words per term as W planes (word 0, the least
+// significant one, in the ordinary key array; words 1..W-1 plane-major in `hi`), n <= 256.
+//
+// What runs on wide stores is the part of the path such circuits use:
+//   qx_apply_clifford_wide  fused run of sign-permutation gates (apply_cx stabilizer.py:340-363,
+//                           H/S/X/SX of engine.py:183-218): one thread per term, words in local
+//                           memory, the whole program applied before the term is written back;
+//   qx_apply_split_wide     v1 rotation (engine.py:190-217): two entries per term, the second
+//                           one (second branch weight 0) a zero-weight copy of the first, which
+//                           the merge adds into the same key without changing the sum;
+//   merge / sort            one CTA per generator: bitonic sort on (words, input position) in
+//                           shared memory, in-order run sums, drop rule, compaction across
+//                           generators by look-back -- generators up to 16384 / W raw terms.
+// Branching operators of v2/v3, the large merge, read-out and partitioning stay one-word
+// (QX_ERR_UNSUPPORTED on a wide store): states of that size do not occur at these widths.
+#include <stdlib.h>
+#include <string.h>
+
+#include <algorithm>
+#include <vector>
+
+#include "qx_device.cuh"
+
+namespace {
+
+constexpr int kThreads = 256;
+constexpr int kMaxWords = QX_MAX_WORDS;
+
+struct Planes {
+  u64* p[kMaxWords];
+};
+
+Planes planes_of(qx_store* s, int buf) {
+  Planes pl;
+  for (int w = 0; w < kMaxWords; ++w) pl.p[w] = nullptr;
+  pl.p[0] = s->keys[buf];
+  for (int w = 1; w < s->n_words; ++w) pl.p[w] = s->hi[buf] + (size_t)(w - 1) * (size_t)s->cap;
+  return pl;
+}
+
+// ---- Clifford run ----------------------------------------------------------------------------
+// op: bits 0-1 kind (0 = 1q permutation, 1 = CX); bits 16-23 image axes, 24-27 signs (as in
+// qx_apply_clifford); bits 32-47 bit position of the (control) digit; bits 48-63 of the target.
+__global__ void __launch_bounds__(kThreads)
+k_clifford_wide(Planes pl, double* __restrict__ lam, const int64_t* __restrict__ seg, int n_seg, int n_words,
+                const u64* __restrict__ ops, int n_ops, u32 cx_c, u32 cx_t, u32 cx_s) {
+  const int64_t total = seg[n_seg];
+  for (int64_t i = (int64_t)blockIdx.x * kThreads + threadIdx.x; i < total; i += (int64_t)gridDim.x * kThreads) {
+    u64 k[kMaxWords];
+    for (int w = 0; w < n_words; ++w) k[w] = pl.p[w][i];
+    u32 neg = 0;
+    for (int j = 0; j < n_ops; ++j) {
+      const u64 op = ops[j];
+      const u32 lo = (u32)op;
+      const u32 p0 = (u32)(op >> 32) & 0xffffu;
+      const u32 d0 = (u32)(k[p0 >> 6] >> (p0 & 63u)) & 3u;
+      if ((lo & 3u) == 0u) {
+        const u32 nd = (lo >> (16u + 2u * d0)) & 3u;
+        neg ^= (lo >> (24u + d0)) & 1u;
+        k[p0 >> 6] ^= (u64)(d0 ^ nd) << (p0 & 63u);
+      } else {
+        const u32 p1 = (u32)(op >> 48) & 0xffffu;
+        const u32 d1 = (u32)(k[p1 >> 6] >> (p1 & 63u)) & 3u;
+        const u32 e = d0 * 4u + d1;
+        neg ^= (cx_s >> e) & 1u;
+        k[p0 >> 6] ^= (u64)(d0 ^ ((cx_c >> (2u * e)) & 3u)) << (p0 & 63u);
+        k[p1 >> 6] ^= (u64)(d1 ^ ((cx_t >> (2u * e)) & 3u)) << (p1 & 63u);
+      }
+    }
+    for (int w = 0; w < n_words; ++w) pl.p[w][i] = k[w];
+    if (neg) lam[i] = -lam[i];
+  }
+}
+
+// ---- v1 split --------------------------------------------------------------------------------
+struct SplitTableW {
+  double w1[4], w2[4];
+  u32 a1[4], a2[4];
+  u32 pos;
+};
+
+__global__ void __launch_bounds__(kThreads)
+k_split_wide(Planes in, const double* __restrict__ lam_in, const int64_t* __restrict__ seg_in, int n_seg,
+             int n_words, Planes out, double* __restrict__ lam_out, int64_t* __restrict__ seg_out,
+             const SplitTableW tb) {
+  const int64_t total = seg_in[n_seg];
+  const int word = (int)(tb.pos >> 6), sh = (int)(tb.pos & 63u);
+  for (int64_t i = (int64_t)blockIdx.x * kThreads + threadIdx.x; i < total; i += (int64_t)gridDim.x * kThreads) {
+    const double l = lam_in[i];
+    const u64 kw = in.p[word][i];
+    const u32 d = (u32)(kw >> sh) & 3u;
+    const u64 cleared = kw & ~(3ull << sh);
+    const bool second = tb.w2[d] != 0.0;
+    for (int w = 0; w < n_words; ++w) {
+      const u64 v = in.p[w][i];
+      out.p[w][2 * i] = w == word ? (cleared | ((u64)tb.a1[d] << sh)) : v;
+      // no second branch: a zero-weight copy of the first one (the merge adds 0.0 into its key)
+      out.p[w][2 * i + 1] = w == word ? (cleared | ((u64)(second ? tb.a2[d] : tb.a1[d]) << sh)) : v;
+    }
+    lam_out[2 * i] = l * tb.w1[d];
+    lam_out[2 * i + 1] = second ? l * tb.w2[d] : 0.0;
+  }
+  for (int g = blockIdx.x * kThreads + threadIdx.x; g <= n_seg; g += gridDim.x * kThreads) seg_out[g] = 2 * seg_in[g];
+}
+
+// ---- merge: one CTA per generator ----------------------------------------------------------------
+constexpr int kMergeThreads = 512;
+
+__device__ __forceinline__ bool wide_greater(const u64* sk, int cap, int n_words, int a, int b,
+                                             unsigned short ia, unsigned short ib) {
+  for (int w = n_words - 1; w >= 0; --w) {
+    const u64 ka = sk[(size_t)w * cap + a], kb = sk[(size_t)w * cap + b];
+    if (ka != kb) return ka > kb;
+  }
+  return ia > ib;
+}
+__device__ __forceinline__ bool wide_equal(const u64* sk, int cap, int n_words, int a, int b) {
+  for (int w = 0; w < n_words; ++w)
+    if (sk[(size_t)w * cap + a] != sk[(size_t)w * cap + b]) return false;
+  return true;
+}
+
+__global__ void __launch_bounds__(kMergeThreads)
+k_small_merge_wide(Planes in, const double* __restrict__ lam_in, const int64_t* __restrict__ seg_in, int n_seg,
+                   int n_words, Planes out, double* __restrict__ lam_out, int64_t* __restrict__ seg_out,
+                   u64* status, u32* ticket, int* error, int cap, double eps) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  u64* sk = reinterpret_cast<u64*>(smem_raw);                                   // [n_words][cap]
+  unsigned short* sidx = reinterpret_cast<unsigned short*>(sk + (size_t)n_words * cap);
+  __shared__ int s_g;
+  __shared__ u64 s_scan[kMergeThreads / 32 + 1];
+  __shared__ u64 s_base;
+  if (threadIdx.x == 0) s_g = (int)atomicAdd(ticket, 1u);
+  __syncthreads();
+  const int g = s_g;
+  if (g >= n_seg) return;
+  const int64_t start = seg_in[g];
+  int len = (int)min((int64_t)0x7fffffff, seg_in[g + 1] - start);
+  if (len > cap) {
+    if (threadIdx.x == 0) atomicExch(error, 1);
+    len = 0;
+  }
+  int m = 32;
+  while (m < len) m <<= 1;
+  for (int e = threadIdx.x; e < m; e += kMergeThreads) {
+    for (int w = 0; w < n_words; ++w) sk[(size_t)w * cap + e] = e < len ? in.p[w][start + e] : ~0ull;
+    sidx[e] = (unsigned short)e;
+  }
+  __syncthreads();
+  // padding: all-ones words and position >= len, so it ends up behind every live term
+  for (int k = 2; k <= m; k <<= 1) {
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      for (int t = threadIdx.x; t < (m >> 1); t += kMergeThreads) {
+        const int lo = ((t & ~(j - 1)) << 1) | (t & (j - 1));
+        const int hi = lo | j;
+        const unsigned short ia = sidx[lo], ib = sidx[hi];
+        const bool greater = wide_greater(sk, cap, n_words, lo, hi, ia, ib);
+        if (greater == ((lo & k) == 0)) {
+          for (int w = 0; w < n_words; ++w) {
+            const u64 a = sk[(size_t)w * cap + lo];
+            sk[(size_t)w * cap + lo] = sk[(size_t)w * cap + hi];
+            sk[(size_t)w * cap + hi] = a;
+          }
+          sidx[lo] = ib;
+          sidx[hi] = ia;
+        }
+      }
+      __syncthreads();
+    }
+  }
+  const int rows = (len + kMergeThreads - 1) / kMergeThreads;
+  u64 my_count = 0;
+  for (int r = 0; r < rows; ++r) {
+    const int e = r * kMergeThreads + threadIdx.x;
+    if (e < len && (e == 0 || !wide_equal(sk, cap, n_words, e - 1, e))) {
+      double sum = lam_in[start + sidx[e]];
+      for (int j = e + 1; j < len && wide_equal(sk, cap, n_words, e, j); ++j) sum += lam_in[start + sidx[j]];
+      if (fabs(sum) >= eps) ++my_count;
+    }
+  }
+  u64 seg_total;
+  block_exclusive_sum<u64>(my_count, s_scan, seg_total);
+  if ((threadIdx.x >> 5) == 0) {
+    const u64 excl = lookback_exclusive(status, g, seg_total);
+    if (lane_id() == 0) s_base = excl;
+  }
+  __syncthreads();
+  const int64_t base = (int64_t)s_base;
+  u64 kept_before = 0;
+  for (int r = 0; r < rows; ++r) {
+    const int e = r * kMergeThreads + threadIdx.x;
+    bool kept = false;
+    double sum = 0.0;
+    if (e < len && (e == 0 || !wide_equal(sk, cap, n_words, e - 1, e))) {
+      sum = lam_in[start + sidx[e]];
+      for (int j = e + 1; j < len && wide_equal(sk, cap, n_words, e, j); ++j) sum += lam_in[start + sidx[j]];
+      kept = fabs(sum) >= eps;
+    }
+    u64 row_total;
+    const u64 excl = block_exclusive_sum<u64>(kept ? 1ull : 0ull, s_scan, row_total);
+    if (kept) {
+      const int64_t pos = base + (int64_t)(kept_before + excl);
+      for (int w = 0; w < n_words; ++w) out.p[w][pos] = sk[(size_t)w * cap + e];
+      lam_out[pos] = sum;
+    }
+    kept_before += row_total;
+  }
+  if (threadIdx.x == 0) {
+    seg_out[g] = base;
+    if (g == n_seg - 1) seg_out[n_seg] = base + (int64_t)seg_total;
+  }
+}
+
+int merge_cap(int n_words) {
+  int cap = 32;
+  while (cap * 2 * n_words <= 16384) cap <<= 1;
+  return cap;                                    // W = 2: 8192, 3-4: 4096, 5-8: 2048 raw terms per generator
+}
+
+}  // namespace
+
+int qx_wide_merge(qx_store* s, double eps) {
+  if (!s->exact && s->ub_seg > merge_cap(s->n_words)) QX_TRY(qx_store_refresh(s));
+  const int limit = merge_cap(s->n_words);
+  if (s->ub_seg > limit)
+    return qx_fail(QX_ERR_UNSUPPORTED,
+                   "n_qubits=%d (%d-word keys): a generator with %lld raw terms exceeds the %d the multi-word "
+                   "merge holds; states of that rank need n <= 32",
+                   s->n_qubits, s->n_words, (long long)s->ub_seg, limit);
+  int cap = 32;
+  while (cap < s->ub_seg) cap <<= 1;
+  const size_t smem = (size_t)cap * (8 * (size_t)s->n_words + 2);
+  const int64_t bytes = 16 + 8 * ((int64_t)s->n_seg + 1);
+  QX_TRY(qx_arena_scratch(s, bytes));
+  QX_CUDA(cudaMemsetAsync(s->scratch, 0, (size_t)bytes, s->stream));
+  u32* ticket = reinterpret_cast<u32*>(s->scratch);
+  int* error = reinterpret_cast<int*>(reinterpret_cast<char*>(s->scratch) + 8);
+  u64* status = reinterpret_cast<u64*>(reinterpret_cast<char*>(s->scratch) + 16);
+  static bool attr_set = false;
+  if (!attr_set) {
+    QX_CUDA(cudaFuncSetAttribute(k_small_merge_wide, cudaFuncAttributeMaxDynamicSharedMemorySize, 16384 * 8 + 8192 * 2 + 64));
+    attr_set = true;
+  }
+  const int in = s->cur, out = s->cur ^ 1;
+  {
+    QxProfileScope prof(QX_K_SMALL_MERGE, s->stream, (8.0 * s->n_words + 8.0) * 2.0 * (double)s->ub_total);
+    k_small_merge_wide<<<s->n_seg, kMergeThreads, smem, s->stream>>>(
+        planes_of(s, in), s->lam[in], s->seg[in], s->n_seg, s->n_words, planes_of(s, out), s->lam[out],
+        s->seg[out], status, ticket, error, cap, eps);
+    QX_CUDA(cudaGetLastError());
+  }
+  QX_TRY(qx_readback(s->stream, s->h_pinned, reinterpret_cast<const int64_t*>(reinterpret_cast<char*>(s->scratch) + 8), 1));
+  s->cur = out;
+  s->exact = false;
+  QX_TRY(qx_store_refresh(s));
+  if ((int)(s->h_pinned[0] & 0xffffffff) != 0)
+    return qx_fail(QX_ERR_CONSISTENCY, "multi-word merge: segment bound violated (internal error)");
+  return QX_OK;
+}
+
+extern "C" int qx_apply_clifford_wide(qx_store* s, const uint64_t* ops, int32_t n_ops, uint32_t cx_c,
+                                      uint32_t cx_t, uint32_t cx_s) {
+  QX_REQUIRE(s != nullptr, "store is NULL");
+  QX_REQUIRE(n_ops >= 0 && (n_ops == 0 || ops), "bad program");
+  QX_REQUIRE(s->n_words > 1, "store has one-word keys: use qx_apply_clifford");
+  if (n_ops == 0) return QX_OK;
+  const u32 limit = 2u * (u32)s->n_qubits;
+  for (int i = 0; i < n_ops; ++i) {
+    const u32 kind = (u32)ops[i] & 3u, p0 = (u32)(ops[i] >> 32) & 0xffffu, p1 = (u32)(ops[i] >> 48) & 0xffffu;
+    QX_REQUIRE(kind <= 1u, "op %d: unknown kind %u", i, kind);
+    QX_REQUIRE(p0 < limit && (p0 & 1u) == 0u, "op %d: digit position %u out of range", i, p0);
+    if (kind == 1u) QX_REQUIRE(p1 < limit && (p1 & 1u) == 0u && p1 != p0, "op %d: bad CX target position %u", i, p1);
+  }
+  QX_CUDA(cudaSetDevice(s->device));
+  QX_TRY(qx_arena_scratch(s, 8ll * n_ops));
+  QX_CUDA(cudaMemcpyAsync(s->scratch, ops, sizeof(u64) * (size_t)n_ops, cudaMemcpyHostToDevice, s->stream));
+  const int64_t total = std::max<int64_t>(s->ub_total, 1);
+  const int grid = (int)std::min<int64_t>((total + kThreads - 1) / kThreads, (int64_t)s->sm_count * 8);
+  {
+    QxProfileScope prof(QX_K_CLIFFORD, s->stream, 2.0 * (8.0 * s->n_words + 8.0) * (double)s->ub_total);
+    k_clifford_wide<<<grid, kThreads, 0, s->stream>>>(planes_of(s, s->cur), s->lam[s->cur], s->seg[s->cur], s->n_seg,
+                                                      s->n_words, reinterpret_cast<const u64*>(s->scratch), n_ops,
+                                                      cx_c, cx_t, cx_s);
+    QX_CUDA(cudaGetLastError());
+  }
+  QX_CUDA(cudaStreamSynchronize(s->stream));     // the program was copied from caller memory
+  return QX_OK;
+}
+
+extern "C" int qx_apply_split_wide(qx_store* s, int32_t qubit, const int32_t a1[4], const double w1[4],
+                                   const int32_t a2[4], const double w2[4]) {
+  QX_REQUIRE(s && a1 && w1 && a2 && w2, "NULL argument");
+  QX_REQUIRE(s->n_words > 1, "store has one-word keys: use qx_apply_split");
+  QX_REQUIRE(qubit >= 0 && qubit < s->n_qubits, "qubit %d out of range for n=%d", qubit, s->n_qubits);
+  SplitTableW tb;
+  tb.pos = 2u * (u32)(s->n_qubits - 1 - qubit);
+  for (int d = 0; d < 4; ++d) {
+    QX_REQUIRE(a1[d] >= 0 && a1[d] <= 3 && a2[d] >= 0 && a2[d] <= 3, "axis code out of range");
+    tb.a1[d] = (u32)a1[d];
+    tb.a2[d] = (u32)a2[d];
+    tb.w1[d] = w1[d];
+    tb.w2[d] = w2[d];
+  }
+  QX_CUDA(cudaSetDevice(s->device));
+  const int64_t ub_in = s->ub_total;
+  QX_TRY(qx_store_reserve(s, 2 * ub_in + 2, true));
+  const int in = s->cur, out = s->cur ^ 1;
+  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((ub_in + kThreads - 1) / kThreads, (int64_t)s->sm_count * 8));
+  {
+    QxProfileScope prof(QX_K_SPLIT, s->stream, 3.0 * (8.0 * s->n_words + 8.0) * (double)ub_in);
+    k_split_wide<<<grid, kThreads, 0, s->stream>>>(planes_of(s, in), s->lam[in], s->seg[in], s->n_seg, s->n_words,
+                                                   planes_of(s, out), s->lam[out], s->seg[out], tb);
+    QX_CUDA(cudaGetLastError());
+  }
+  qx_store_flip(s);
+  s->exact = false;
+  s->ub_total = 2 * ub_in;
+  s->ub_seg = 2 * s->ub_seg;
+  return QX_OK;
+}
+
+// content in / out: words are term-major on the host ([term][word], word 0 least significant)
+extern "C" int qx_store_upload_wide(qx_store* s, const int64_t* offsets, const uint64_t* words,
+                                    const double* lambdas) {
+  QX_REQUIRE(s && offsets, "NULL argument");
+  QX_REQUIRE(s->n_words > 1, "store has one-word keys: use qx_store_upload");
+  QX_REQUIRE(offsets[0] == 0, "offsets[0] must be 0");
+  for (int g = 0; g < s->n_seg; ++g)
+    QX_REQUIRE(offsets[g + 1] >= offsets[g], "offsets must be non-decreasing (segment %d)", g);
+  const int64_t total = offsets[s->n_seg];
+  QX_REQUIRE(total == 0 || (words && lambdas), "words/lambdas are NULL");
+  const int W = s->n_words;
+  const int top_bits = 2 * s->n_qubits - 64 * (W - 1);
+  if (top_bits < 64)
+    for (int64_t i = 0; i < total; ++i)
+      QX_REQUIRE((words[(size_t)i * W + (W - 1)] >> top_bits) == 0, "word index of term %lld out of range [0, 4**%d)",
+                 (long long)i, s->n_qubits);
+  QX_CUDA(cudaSetDevice(s->device));
+  QX_TRY(qx_store_reserve(s, total, false));
+  const int c = s->cur;
+  std::vector<u64> plane((size_t)std::max<int64_t>(total, 1));
+  const Planes pl = planes_of(s, c);
+  for (int w = 0; w < W; ++w) {
+    for (int64_t i = 0; i < total; ++i) plane[(size_t)i] = words[(size_t)i * W + w];
+    if (total > 0) QX_CUDA(cudaMemcpy(pl.p[w], plane.data(), sizeof(u64) * (size_t)total, cudaMemcpyHostToDevice));
+  }
+  if (total > 0)
+    QX_CUDA(cudaMemcpyAsync(s->lam[c], lambdas, sizeof(double) * (size_t)total, cudaMemcpyHostToDevice, s->stream));
+  memcpy(s->h_seg, offsets, sizeof(int64_t) * (size_t)(s->n_seg + 1));
+  QX_CUDA(cudaMemcpyAsync(s->seg[c], s->h_seg, sizeof(int64_t) * (size_t)(s->n_seg + 1), cudaMemcpyHostToDevice,
+                          s->stream));
+  QX_CUDA(cudaStreamSynchronize(s->stream));
+  s->exact = true;
+  s->ub_total = total;
+  s->ub_seg = 0;
+  for (int g = 0; g < s->n_seg; ++g) s->ub_seg = std::max(s->ub_seg, offsets[g + 1] - offsets[g]);
+  return QX_OK;
+}
+
+extern "C" int qx_store_download_wide(qx_store* s, int64_t* offsets, uint64_t* words, double* lambdas,
+                                      int64_t cap_terms) {
+  QX_REQUIRE(s && offsets, "NULL argument");
+  QX_REQUIRE(s->n_words > 1, "store has one-word keys: use qx_store_download");
+  if (!s->exact) QX_TRY(qx_store_refresh(s));
+  memcpy(offsets, s->h_seg, sizeof(int64_t) * (size_t)(s->n_seg + 1));
+  const int64_t total = s->h_seg[s->n_seg];
+  if (words == nullptr && lambdas == nullptr) return QX_OK;
+  QX_REQUIRE(cap_terms >= total, "download buffer holds %lld terms, store has %lld", (long long)cap_terms,
+             (long long)total);
+  QX_CUDA(cudaSetDevice(s->device));
+  QX_CUDA(cudaStreamSynchronize(s->stream));
+  const int W = s->n_words;
+  const Planes pl = planes_of(s, s->cur);
+  if (total > 0 && words) {
+    std::vector<u64> plane((size_t)total);
+    for (int w = 0; w < W; ++w) {
+      QX_CUDA(cudaMemcpy(plane.data(), pl.p[w], sizeof(u64) * (size_t)total, cudaMemcpyDeviceToHost));
+      for (int64_t i = 0; i < total; ++i) words[(size_t)i * W + w] = plane[(size_t)i];
+    }
+  }
+  if (total > 0 && lambdas)
+    QX_CUDA(cudaMemcpy(lambdas, s->lam[s->cur], sizeof(double) * (size_t)total, cudaMemcpyDeviceToHost));
+  return QX_OK;
+}
+
+extern "C" int qx_store_words(qx_store* s, int32_t* n_words) {
+  QX_REQUIRE(s && n_words, "NULL argument");
+  *n_words = s->n_words;
+  return QX_OK;
+}

@@ -129,7 +129,7 @@ class _Walker:
         if not self.queue:
             return
         t0 = time.perf_counter()
-        self.store.apply_clifford(np.array(self.queue, dtype=np.uint32))
+        self.store.apply_clifford(np.array(self.queue, dtype=_lut.op_dtype(self.n)))
         self.timings["cx" if self.queue_has_cx else "sub_flatten"] += time.perf_counter() - t0
         self.queue, self.queue_has_cx = [], False
         self.unsorted = True
@@ -510,6 +510,11 @@ def _walk_operators(partition, lut, is_perm, tables, w: _Walker, trace, counters
                     w.push_perm(int(j), int(tables[ui][j]))
                 w.step_done(step, "sub_flatten", trace)
             else:
+                if n > 32:
+                    raise ResourceLimitError(
+                        f"n = {n}: branching operators (v2/v3) need one-word keys (n <= 32); above that the "
+                        "device runs Clifford operators in every mode and rotations in v1"
+                    )
                 w.resolve(trace)               # expand merged terms only
                 w.flush()
                 counts, axes, weights = _lut.operator_tables(lut[ui])

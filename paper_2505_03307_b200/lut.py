@@ -203,13 +203,23 @@ def perm_word(block: np.ndarray):
 
 
 def perm_op(n: int, qubit: int, table: int) -> int:
-    """32-bit op word of a 1q signed permutation on ``qubit`` (include/qimax_b200.h)."""
+    """Op word of a 1q signed permutation on ``qubit`` (include/qimax_b200.h): 32 bits for n <= 32,
+    the 64-bit form of qx_apply_clifford_wide above (digit positions in the high half)."""
+    if n > 32:
+        return 0 | (table << 16) | ((2 * (n - 1 - qubit)) << 32)
     return 0 | ((2 * (n - 1 - qubit)) << 2) | (table << 16)
 
 
 def cx_op(n: int, control: int, target: int) -> int:
-    """32-bit op word of CX(control, target)."""
+    """Op word of CX(control, target); see perm_op."""
+    if n > 32:
+        return 1 | ((2 * (n - 1 - control)) << 32) | ((2 * (n - 1 - target)) << 48)
     return 1 | ((2 * (n - 1 - control)) << 2) | ((2 * (n - 1 - target)) << 8)
+
+
+def op_dtype(n: int):
+    """numpy dtype of a gate program for an n-qubit store."""
+    return np.uint64 if n > 32 else np.uint32
 
 
 IDENTITY_PERM = perm_word(np.eye(3))

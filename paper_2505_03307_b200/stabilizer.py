@@ -26,7 +26,7 @@ from .store import DeviceStore
 DEFAULT_EPS = 1e-12                 # reference stabilizer.py:38
 DENSE_FLATTEN_BUDGET = 4 ** 10      # reference stabilizer.py:45
 _INT64_MAX_QUBITS = 31              # 4**31 - 1 < 2**63
-MAX_QUBITS = 32                     # one uint64 key per term on the device
+MAX_QUBITS = 32                     # one uint64 key per term on the device; more words above (n <= 256)
 
 
 def index_dtype(n: int):
@@ -50,7 +50,15 @@ def keys_to_indices(keys: np.ndarray, n: int) -> np.ndarray:
 
 
 def indices_to_keys(indices, n: int) -> np.ndarray:
-    """Reference index array (int64 or object) -> uint64 keys, range-checked."""
+    """Reference index array (int64 or object) -> uint64 keys, range-checked; above 32 qubits an
+    object array of Python ints (the device splits them into 64-bit words, store.py)."""
+    if n > MAX_QUBITS:
+        vals = [int(v) for v in indices]
+        if any(v < 0 or v >= 4 ** n for v in vals):
+            raise ValueError(f"word index out of range [0, 4**{n})")
+        out = np.empty(len(vals), dtype=object)
+        out[:] = vals
+        return out
     if isinstance(indices, np.ndarray) and indices.dtype == np.int64:
         if len(indices) and int(indices.min()) < 0:
             raise ValueError("negative word index")

@@ -20,6 +20,7 @@ class DeviceStore:
     def __init__(self, n: int, n_segments: int, capacity: int = 0, device=None):
         self.n = int(n)
         self.n_segments = int(n_segments)
+        self.words = 1 if self.n <= 32 else (2 * self.n + 63) // 64       # > 1: multi-word keys (csrc/wide.cu)
         self.device = nat.default_device() if device is None else int(device)
         self._h = C.c_void_p()
         nat.check(nat.lib().qx_store_create(self.device, self.n, self.n_segments, int(capacity),
@@ -71,8 +72,22 @@ class DeviceStore:
             if len(lam) != len(keys):
                 raise ValueError("lambdas and indices must have equal length")
             off[i + 1] = off[i] + len(lam)
-        keys = np.empty(int(off[-1]), dtype=np.uint64)
         lam = np.empty(int(off[-1]), dtype=np.float64)
+        if self.words > 1:
+            # multi-word keys: Python ints -> little-endian 64-bit words, term-major
+            words = np.zeros((int(off[-1]), self.words), dtype=np.uint64)
+            mask = (1 << 64) - 1
+            for i, (l, k) in enumerate(gens):
+                for j, v in enumerate(k):
+                    v = int(v)
+                    if v < 0 or v >= 4 ** self.n:
+                        raise ValueError(f"word index out of range [0, 4**{self.n})")
+                    for w in range(self.words):
+                        words[off[i] + j, w] = (v >> (64 * w)) & mask
+                lam[off[i]:off[i + 1]] = l
+            nat.check(nat.lib().qx_store_upload_wide(self._h, nat.ptr(off), nat.ptr(words), nat.ptr(lam)))
+            return
+        keys = np.empty(int(off[-1]), dtype=np.uint64)
         for i, (l, k) in enumerate(gens):
             keys[off[i]:off[i + 1]] = np.asarray(k, dtype=np.uint64) if not _is_object(k) else [int(v) for v in k]
             lam[off[i]:off[i + 1]] = l
@@ -86,6 +101,16 @@ class DeviceStore:
     def download(self, pinned: bool = False):
         """(offsets int64[n_seg+1], keys uint64[total], lambdas float64[total]) on the host."""
         off = np.zeros(self.n_segments + 1, dtype=np.int64)
+        if self.words > 1:
+            nat.check(nat.lib().qx_store_download_wide(self._h, nat.ptr(off), None, None, 0))
+            total = int(off[-1])
+            words = np.zeros((total, self.words), dtype=np.uint64)
+            lam = np.empty(total, dtype=np.float64)
+            nat.check(nat.lib().qx_store_download_wide(self._h, nat.ptr(off), nat.ptr(words), nat.ptr(lam), total))
+            keys = np.empty(total, dtype=object)                  # Python ints, like the reference above 31 qubits
+            rows = words.tolist()
+            keys[:] = [sum(int(w) << (64 * i) for i, w in enumerate(row)) for row in rows]
+            return off, keys, lam
         nat.check(nat.lib().qx_store_download(self._h, nat.ptr(off), None, None, 0))
         total = int(off[-1])
         if pinned and total > 0:
@@ -102,6 +127,7 @@ class DeviceStore:
         """A new store with copies of segments [seg_lo, seg_hi), on a CUDA stream of its own."""
         child = object.__new__(DeviceStore)
         child.n, child.n_segments, child.device = self.n, int(seg_hi) - int(seg_lo), self.device
+        child.words = self.words
         child._h = C.c_void_p()
         child._cx = self._cx
         nat.check(nat.lib().qx_store_slice(self._h, int(seg_lo), int(seg_hi), int(capacity), C.byref(child._h)))
@@ -143,9 +169,14 @@ class DeviceStore:
 
     # -- kernels ----------------------------------------------------------------
     def apply_clifford(self, program):
+        c, t, s = self._cx
+        if self.words > 1:
+            prog = np.ascontiguousarray(program, dtype=np.uint64)        # lut.perm_op / cx_op wide form
+            if len(prog):
+                nat.check(nat.lib().qx_apply_clifford_wide(self._h, nat.ptr(prog), len(prog), c, t, s))
+            return
         prog = np.ascontiguousarray(program, dtype=np.uint32)
         if len(prog):
-            c, t, s = self._cx
             nat.check(nat.lib().qx_apply_clifford(self._h, nat.ptr(prog), len(prog), c, t, s))
 
     def apply_split(self, qubit: int, a1, w1, a2, w2):
@@ -153,7 +184,8 @@ class DeviceStore:
         a2 = np.ascontiguousarray(a2, dtype=np.int32)
         w1 = np.ascontiguousarray(w1, dtype=np.float64)
         w2 = np.ascontiguousarray(w2, dtype=np.float64)
-        nat.check(nat.lib().qx_apply_split(self._h, int(qubit), nat.ptr(a1), nat.ptr(w1), nat.ptr(a2), nat.ptr(w2)))
+        fn = nat.lib().qx_apply_split_wide if self.words > 1 else nat.lib().qx_apply_split
+        nat.check(fn(self._h, int(qubit), nat.ptr(a1), nat.ptr(w1), nat.ptr(a2), nat.ptr(w2)))
 
     def apply_operator(self, counts, axes, weights, term_limit: int = 0) -> int:
         counts = np.ascontiguousarray(counts, dtype=np.int32).reshape(-1)

@@ -67,8 +67,10 @@ def test_errors():
     qx.run(workloads.gen_ghz(20), 20, "v2")                   # one-hot rows: fine at any n
     with pytest.raises(ValueError):
         qx.run([ir.h(5)], 3, "v1")
+    rep = qx.run([], 33, "v1")                                 # multi-word keys above 32 qubits
+    assert int(rep.final.generators[0].indices[0]) == 3 * 4 ** 32
     with pytest.raises(qx.NativeError):
-        qx.run([], 33, "v1")                                   # one-word keys: n <= 32
+        qx.run([], 257, "v1")                                  # at most eight words per key
 
 
 # ------------------------------------------------------------------ fixtures from the reference

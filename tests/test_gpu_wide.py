@@ -1,0 +1,99 @@
+"""More than 32 qubits on the GPU (multi-word keys, csrc/wide.cu) against fixtures computed by the
+UNMODIFIED reference with Python big-int indices (tests/golden/wide.json, oracle/make_golden_wide.py):
+Clifford circuits up to 130 qubits in v1 and v3, near-Clifford circuits in v1, the apply_cx unit
+case; plus the multi-word merge/split against a big-int model on random terms, and the error a
+branching operator raises above 32 qubits."""
+
+import math
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+from gpu_util import DeviceStore, qx  # noqa: E402
+
+from paper_2505_03307_b200 import lut  # noqa: E402
+from paper_2505_03307_b200.stabilizer import SimpleGenerator, split_tables  # noqa: E402
+
+TOL = 1e-10
+
+
+def _cases(golden):
+    return golden.load_json("wide.json")
+
+
+def test_reference_circuits_above_32_qubits(golden):
+    data = _cases(golden)
+    assert len(data["cases"]) >= 15
+    for case in data["cases"]:
+        n = case["n"]
+        gates = [qx.Instruction(g, tuple(w), float.fromhex(t)) for g, w, t in case["gates"]]
+        rep = qx.run(gates, n, case["mode"])
+        assert rep.rank_trace[-1] == case["rank_trace_last"], case["name"]
+        for g, want in zip(rep.final.generators, case["final"]):
+            assert g.indices.dtype == object
+            assert [int(v) for v in g.indices] == [int(v) for v in want["idx"]], case["name"]
+            lam = np.array([float.fromhex(v) for v in want["lam"]])
+            if case["max_rank"] == 1:
+                assert np.array_equal(g.lambdas, lam), case["name"]          # Clifford: exactly +-1
+            else:
+                assert np.max(np.abs(g.lambdas - lam)) < TOL, case["name"]
+
+
+def test_apply_cx_big_int_unit(golden):
+    u = _cases(golden)["apply_cx"]
+    g = SimpleGenerator(u["n"], u["in"]["lam"], [int(v) for v in u["in"]["idx"]])
+    out = qx.apply_cx(g, u["c"], u["t"])
+    assert [int(v) for v in out.indices] == [int(v) for v in u["out"]["idx"]]
+    assert out.lambdas.tolist() == u["out"]["lam"]
+
+
+@pytest.mark.parametrize("n,terms", [(40, 3000), (70, 1500), (130, 900)])
+def test_split_and_merge_against_big_int_model(n, terms):
+    """qx_apply_split_wide + the multi-word merge on random terms (the store grows past its first
+    allocation on the way) against the reference's v1 rule done with Python ints."""
+    rng = np.random.default_rng(n)
+    keys = sorted({int.from_bytes(rng.bytes((2 * n + 7) // 8), "little") % 4 ** n for _ in range(terms)})
+    lam = rng.uniform(-1, 1, size=len(keys))
+    q, theta = n // 3, 0.77
+    block = lut.gate_branch_block("RY", theta)
+    a1, w1, a2, w2 = split_tables(block)
+    sh = 2 * (n - 1 - q)
+    model = {}
+    for k, l in zip(keys, lam):                                   # firsts then seconds, engine.py:211-217
+        d = (k >> sh) & 3
+        base = k & ~(3 << sh)
+        model[base | (int(a1[d]) << sh)] = model.get(base | (int(a1[d]) << sh), 0.0) + l * w1[d]
+    for k, l in zip(keys, lam):
+        d = (k >> sh) & 3
+        if w2[d] != 0.0:
+            base = k & ~(3 << sh)
+            model[base | (int(a2[d]) << sh)] = model.get(base | (int(a2[d]) << sh), 0.0) + l * w2[d]
+    want = sorted((k, v) for k, v in model.items() if abs(v) >= 1e-12)
+    with DeviceStore(n, 2, 0) as st:
+        obj = np.empty(len(keys), dtype=object)
+        obj[:] = keys
+        st.upload([(lam, obj), (lam[:1], obj[:1])])
+        st.apply_split(q, a1, w1, a2, w2)
+        ranks = st.merge(1e-12)
+        (gl, gk), _ = st.segments()
+        norms = st.norms()
+    assert ranks[0] == len(want) and [int(v) for v in gk] == [k for k, _ in want]
+    assert np.max(np.abs(gl - np.array([v for _, v in want]))) < 1e-12
+    assert abs(norms[0] - sum(v * v for _, v in want)) < 1e-9
+
+
+def test_limits_above_32_qubits():
+    n = 36
+    gates = [qx.Instruction("H", (0,)), qx.Instruction("RY", (0,), 0.3), qx.Instruction("CX", (0, 35))]
+    with pytest.raises(qx.ResourceLimitError, match="branching operators"):
+        qx.run(gates, n, "v3")
+    rep = qx.run(gates, n, "v1")                                  # the same circuit gate by gate is fine
+    assert rep.rank_trace[-1][0] == 2 and rep.final.generators[35].rank == 1
+    with pytest.raises(qx.NativeError, match="n <= 256|at most"):
+        qx.run([qx.Instruction("H", (0,))], 300, "v1")
+    with DeviceStore(n, 1, 0) as st:
+        st.init_z([0])
+        with pytest.raises(qx.NativeError, match="one-word keys"):
+            st.zi_sums()
