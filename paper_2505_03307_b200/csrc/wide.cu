@@ -3,7 +3,7 @@
 // The reference switches to Python big-int indices above 31 qubits (stabilizer.py:40-59) so that
 // Clifford and near-Clifford circuits run at any width -- their stabilizer rank stays tiny.  On
 // the device a wide store keeps W = ceil(2n / 64) words per term as W planes (word 0, the least
-// significant one, in the ordinary key array; words 1..W-1 plane-major in `hi`), n <= 256.
+// significant one, in the ordinary key array; words 1..W-1 plane-major in `hi`), n <= 512.
 //
 // What runs on wide stores is the part of the path such circuits use:
 //   qx_apply_clifford_wide  fused run of sign-permutation gates (apply_cx stabilizer.py:340-363,

@@ -26,7 +26,7 @@ from .store import DeviceStore
 DEFAULT_EPS = 1e-12                 # reference stabilizer.py:38
 DENSE_FLATTEN_BUDGET = 4 ** 10      # reference stabilizer.py:45
 _INT64_MAX_QUBITS = 31              # 4**31 - 1 < 2**63
-MAX_QUBITS = 32                     # one uint64 key per term on the device; more words above (n <= 256)
+MAX_QUBITS = 32                     # one uint64 key per term on the device; more words above (n <= 512)
 
 
 def index_dtype(n: int):

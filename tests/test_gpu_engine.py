@@ -70,7 +70,7 @@ def test_errors():
     rep = qx.run([], 33, "v1")                                 # multi-word keys above 32 qubits
     assert int(rep.final.generators[0].indices[0]) == 3 * 4 ** 32
     with pytest.raises(qx.NativeError):
-        qx.run([], 257, "v1")                                  # at most eight words per key
+        qx.run([], 513, "v1")                                  # at most sixteen words per key
 
 
 # ------------------------------------------------------------------ fixtures from the reference

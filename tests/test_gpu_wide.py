@@ -91,8 +91,10 @@ def test_limits_above_32_qubits():
         qx.run(gates, n, "v3")
     rep = qx.run(gates, n, "v1")                                  # the same circuit gate by gate is fine
     assert rep.rank_trace[-1][0] == 2 and rep.final.generators[35].rank == 1
-    with pytest.raises(qx.NativeError, match="n <= 256|at most"):
-        qx.run([qx.Instruction("H", (0,))], 300, "v1")
+    with pytest.raises(qx.NativeError, match="at most"):
+        qx.run([qx.Instruction("H", (0,))], 600, "v1")
+    ghz = qx.run(qx.gen_ghz(400), 400, "v1")                      # "hundreds of qubits for Clifford"
+    assert ghz.max_rank == 1 and int(ghz.final.generators[0].indices[0]) == (4 ** 400 - 1) // 3
     with DeviceStore(n, 1, 0) as st:
         st.init_z([0])
         with pytest.raises(qx.NativeError, match="one-word keys"):
