@@ -178,7 +178,7 @@ template <typename K, typename V, int THREADS, int ITEMS>
 struct SortSmem {
   u32 whist[THREADS / 32][QX_RADIX];  // per-warp digit counters -> exclusive warp offsets
   u32 tile_start[QX_RADIX];           // first slot of each digit in the tile-sorted order
-  int64_t gbase[QX_RADIX];            // global index of slot 0 of each digit, minus tile_start
+  u32 gbase[QX_RADIX];                // index inside the segment of slot 0 of each digit, minus tile_start (mod 2^32)
   u32 scan[THREADS / 32 + 1];
   int tile;
   V vals[THREADS * ITEMS];
@@ -240,7 +240,8 @@ k_onesweep(const K* __restrict__ keys_in, const V* __restrict__ vals_in,
   const int tid = threadIdx.x, warp = tid >> 5, lane = lane_id();
 
   if (tid == 0) sm.tile = (int)atomicAdd(ticket, 1u);
-  for (int i = tid; i < WARPS * QX_RADIX; i += THREADS) (&sm.whist[0][0])[i] = 0u;
+  for (int i = tid; i < WARPS * QX_RADIX / 4; i += THREADS)
+    reinterpret_cast<uint4*>(&sm.whist[0][0])[i] = make_uint4(0u, 0u, 0u, 0u);
   __syncthreads();
   const int64_t tile = sm.tile;
   const int64_t total_tiles = *n_tiles;
@@ -369,20 +370,23 @@ k_onesweep(const K* __restrict__ keys_in, const V* __restrict__ vals_in,
       }
       st_volatile_u32(mine, kFlagInc | (excl + live_total));
     }
-    sm.gbase[tid] = seg[g] + (int64_t)digit_base[(size_t)g * base_stride + tid] + (int64_t)excl -
-                    (int64_t)dstart;
+    sm.gbase[tid] = digit_base[(size_t)g * base_stride + tid] + excl - dstart;
   }
   __syncthreads();
 
-  // ---- coalesced write-out: consecutive slots of one digit are consecutive in HBM
+  // ---- coalesced write-out: consecutive slots of one digit are consecutive in HBM.  Offsets are
+  // 32-bit and relative to the segment (a segment holds < 2^30 terms): one IMAD.WIDE per store
+  // instead of 64-bit index arithmetic per item.
+  KO* kout = keys_out + seg[g];
+  V* vout = vals_out + seg[g];
 #pragma unroll
   for (int k = 0; k < ITEMS; ++k) {
     const int slot = k * THREADS + tid;
     if (full || slot < count) {
       const K kk = sm.keys[slot];
-      const int64_t dst = sm.gbase[key_byte(kk, which)] + slot;
-      st_stream(keys_out + dst, (KO)kk);
-      st_stream(vals_out + dst, sm.vals[slot]);
+      const u32 dst = sm.gbase[key_byte(kk, which)] + (u32)slot;
+      st_stream(kout + dst, (KO)kk);
+      st_stream(vout + dst, sm.vals[slot]);
     }
   }
 }
