@@ -299,7 +299,8 @@ def run_ours(args):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     e2e_s = float(t.item())
     final_terms = sum(g.rank for g in last.final.generators)
-    d2h = 16 * final_terms + 8 * (len(mine) + 1)
+    # bytes that crossed PCIe: the run reports them when it shipped 32-bit keys (n <= 16, widened on the host)
+    d2h = last.device.get("d2h_bytes", 16 * final_terms) + 8 * (len(mine) + 1)
     del last
 
     # ---- roofline of the dominant kernel: instrumented steps (CUDA events around every launch)

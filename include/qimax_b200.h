@@ -94,6 +94,18 @@ int qx_store_slice(qx_store* src, int32_t seg_lo, int32_t seg_hi, int64_t capaci
  * qx_store_synchronize(s). */
 int qx_store_download_async(qx_store* s, int64_t* offsets, uint64_t* keys, double* lambdas,
                             int64_t cap_terms);
+/* For a store that is only downloaded next (n <= 16): on != 0 lets the next large operator step
+ * leave 32-bit keys in HBM, so that 12 instead of 16 bytes per term cross PCIe.  Afterwards only
+ * qx_store_download_narrow_async, qx_store_ranks, qx_store_synchronize and qx_store_destroy are
+ * valid on the store. */
+int qx_store_set_keep_narrow(qx_store* s, int on);
+/* As qx_store_download_async for such a store: the 32-bit keys are copied into `staging`
+ * (page-locked, cap_terms words) chunk by chunk and `threads` host threads widen every chunk into
+ * `keys` as soon as it has landed, while later chunks and the coefficients are still on the wire.
+ * qx_store_synchronize(s) waits for the copies AND the widening.  Falls back to
+ * qx_store_download_async if the store holds 64-bit keys. */
+int qx_store_download_narrow_async(qx_store* s, int64_t* offsets, uint64_t* keys, double* lambdas,
+                                   int64_t cap_terms, uint32_t* staging, int32_t threads);
 
 /* ---- more than 32 qubits (reference stabilizer.py:40-59 switches to Python
  * big-int indices there).  qx_store_create accepts n_qubits <= 512; above 32 the store is WIDE:

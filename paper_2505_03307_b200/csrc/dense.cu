@@ -1134,9 +1134,13 @@ int qx_dense_operator_step(qx_store* s, const OperatorTable& nz, const uint32_t*
   mb.ub_total = s->ub_total;
   mb.ub_seg = s->ub_seg;
   // the kept terms of generator g sit at its slot offset; the first pass reads them from there
-  if (narrow) QX_TRY((qxm::merge_large<double, u32>(s, mb, eps, QX_K_REDUCE, false, QX_K_SORT_PASS, QX_K_SORT_HIST, seg_slot, hist)));
+  // a store that is only downloaded next keeps its 32-bit keys: 12 bytes per term cross PCIe
+  // instead of 16 and the host widens them while the copy runs (qx_store_download_narrow_async)
+  const bool keep_narrow = narrow && s->want_narrow;
+  if (narrow) QX_TRY((qxm::merge_large<double, u32>(s, mb, eps, QX_K_REDUCE, false, QX_K_SORT_PASS, QX_K_SORT_HIST, seg_slot, hist, !keep_narrow)));
   else QX_TRY((qxm::merge_large<double, u64>(s, mb, eps, QX_K_REDUCE, false, QX_K_SORT_PASS, QX_K_SORT_HIST, seg_slot, hist)));
   s->cur = mb.cur;
+  s->narrow_keys = keep_narrow;
   if (!s->exact) QX_TRY(qx_store_refresh(s));      // kept counts: exact offsets for the caller
   return QX_OK;
 }

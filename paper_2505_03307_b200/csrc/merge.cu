@@ -6,6 +6,7 @@
 int qx_run_merge(qx_store* s, double eps, bool sort_only, bool narrow) {
   // multi-word keys: one CTA per generator (wide.cu); a sort is a merge that drops nothing
   if (s->n_words > 1) return qx_wide_merge(s, sort_only ? 0.0 : eps);
+  QX_NARROW_ONLY(s, "merge");
   if (s->ub_seg > QX_SMALL_MAX && !s->exact) QX_TRY(qx_store_refresh(s));
   // both paths write into the other buffer; make sure it can hold the raw terms
   qxm::MergeBuffers<double> mb;

@@ -763,7 +763,7 @@ int dispatch_pass(int variant, QxArena* ar, MergeBuffers<V>& mb, int cur, int64_
 template <typename V, typename K = u64>
 int merge_large(QxArena* ar, MergeBuffers<V>& mb, double eps, int cls_reduce, bool do_reduce = true,
                 int cls_pass = QX_K_SORT_PASS, int cls_hist = QX_K_SORT_HIST,
-                const int64_t* first_base_in = nullptr, const u32* pre_hist = nullptr) {
+                const int64_t* first_base_in = nullptr, const u32* pre_hist = nullptr, bool widen_last = true) {
   const int n_seg = mb.n_seg;
   const int passes = std::min(kMaxPasses, (2 * ar->n_qubits + QX_RADIX_BITS - 1) / QX_RADIX_BITS);
   if (mb.ub_seg >= (int64_t)kFlagVal)
@@ -823,7 +823,7 @@ int merge_large(QxArena* ar, MergeBuffers<V>& mb, double eps, int cls_reduce, bo
     QX_CUDA(cudaMemsetAsync(ar->status, 0, sizeof(u32) * (size_t)(tiles_ub * QX_RADIX), ar->stream));
     QX_CUDA(cudaMemsetAsync(ticket, 0, sizeof(u32), ar->stream));
     QxProfileScope prof(cls_pass, ar->stream, 2.0 * (sizeof(K) + sizeof(V)) * (double)mb.ub_total);
-    if (!do_reduce && sizeof(K) == 4 && p == passes - 1)
+    if (!do_reduce && sizeof(K) == 4 && p == passes - 1 && widen_last)
       QX_TRY((dispatch_pass<K, V, true>(variant, ar, mb, cur, tiles_ub, info, n_tiles, hist + (size_t)p * QX_RADIX,
                                         passes * QX_RADIX, ticket, p, p == 0 ? first_base_in : nullptr)));
     else

@@ -110,6 +110,9 @@ struct qx_store : QxArena {
   u64* keys[2] = {nullptr, nullptr};
   double* lam[2] = {nullptr, nullptr};
   int64_t* seg[2] = {nullptr, nullptr};   // device offsets, n_seg+1 each
+  bool want_narrow = false;     // the caller only downloads next: the grouped step may leave 32-bit keys
+  bool narrow_keys = false;     // keys[cur] holds 32-bit keys (n <= 16); only the narrow download reads them
+  void* host_workers = nullptr; // threads widening downloaded keys on the host (store.cu), joined by synchronize
   int n_words = 1;              // 64-bit words per key; > 1 = wide store (wide.cu)
   u64* hi[2] = {nullptr, nullptr};        // words 1..n_words-1, plane-major, `cap` words per plane
   int cur = 0;                  // which of the two buffers is live
@@ -140,4 +143,7 @@ int qx_wide_merge(qx_store* s, double eps);
     if ((s)->n_words > 1)                                                                            \
       return qx_fail(QX_ERR_UNSUPPORTED, "%s needs one-word keys (n <= %d); this store has n = %d", \
                      what, QX_MAX_QUBITS, (s)->n_qubits);                                            \
+    if ((s)->narrow_keys)                                                                            \
+      return qx_fail(QX_ERR_INVALID, "%s: the store was left with 32-bit keys for download "         \
+                     "(qx_store_set_keep_narrow); only qx_store_download_narrow_async reads it", what); \
   } while (0)

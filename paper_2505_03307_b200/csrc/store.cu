@@ -9,6 +9,10 @@
 #include <atomic>
 #include <map>
 #include <mutex>
+#include <thread>
+#if defined(__x86_64__)
+#include <emmintrin.h>
+#endif
 #include <unordered_map>
 
 #include "qx_internal.cuh"
@@ -383,10 +387,15 @@ extern "C" int qx_store_create(int device, int n_qubits, int n_segments, int64_t
   return QX_OK;
 }
 
+namespace {
+void join_workers(qx_store* s);      // host threads of a narrow download (below)
+}
+
 extern "C" int qx_store_destroy(qx_store* s) {
   if (!s) return QX_OK;
   cudaSetDevice(s->device);
   cudaStreamSynchronize(s->stream);
+  join_workers(s);
   for (int b = 0; b < 2; ++b) {
     qx_dev_free(s->keys[b], s->stream);
     qx_dev_free(s->lam[b], s->stream);
@@ -748,9 +757,88 @@ extern "C" int qx_store_capacity(qx_store* s, int64_t* capacity_terms, int64_t* 
   return QX_OK;
 }
 
+// ---- narrow download: 32-bit keys over PCIe, widened on the host while the copy runs ----------
+namespace {
+struct HostWorkers {
+  std::vector<std::thread> threads;
+  std::vector<cudaEvent_t> events;
+};
+
+void join_workers(qx_store* s) {
+  HostWorkers* hw = static_cast<HostWorkers*>(s->host_workers);
+  if (!hw) return;
+  for (std::thread& t : hw->threads) t.join();
+  for (cudaEvent_t e : hw->events) cudaEventDestroy(e);
+  delete hw;
+  s->host_workers = nullptr;
+}
+}  // namespace
+
+extern "C" int qx_store_set_keep_narrow(qx_store* s, int on) {
+  QX_REQUIRE(s != nullptr, "store is NULL");
+  s->want_narrow = on != 0;
+  return QX_OK;
+}
+
+extern "C" int qx_store_download_narrow_async(qx_store* s, int64_t* offsets, uint64_t* keys, double* lambdas,
+                                              int64_t cap_terms, uint32_t* staging, int32_t threads) {
+  QX_REQUIRE(s && offsets && keys && lambdas, "NULL argument");
+  if (!s->narrow_keys) return qx_store_download_async(s, offsets, keys, lambdas, cap_terms);
+  QX_REQUIRE(staging != nullptr, "staging is NULL");
+  if (!s->exact) QX_TRY(qx_store_refresh(s));
+  memcpy(offsets, s->h_seg, sizeof(int64_t) * (size_t)(s->n_seg + 1));
+  const int64_t total = s->h_seg[s->n_seg];
+  QX_REQUIRE(cap_terms >= total, "download buffer holds %lld terms, store has %lld", (long long)cap_terms,
+             (long long)total);
+  QX_CUDA(cudaSetDevice(s->device));
+  join_workers(s);
+  if (total == 0) return QX_OK;
+  // the keys first, in a few chunks with an event behind each, then the coefficients in one
+  // copy: the host threads widen chunk c while the later chunks and the (twice as large)
+  // coefficient copy are still on the wire.  Few, large copies: every cudaMemcpyAsync costs the
+  // copy engine tens of microseconds of set-up.
+  static const int max_chunks = getenv("QX_WIDEN_CHUNKS") ? atoi(getenv("QX_WIDEN_CHUNKS")) : 2;
+  const int n_chunks = (int)std::max<int64_t>(1, std::min<int64_t>(max_chunks, total / (1 << 20)));
+  const int64_t chunk = (total + n_chunks - 1) / n_chunks;
+  HostWorkers* hw = new HostWorkers();
+  hw->events.resize(n_chunks);
+  const u32* d_keys = reinterpret_cast<const u32*>(s->keys[s->cur]);
+  for (int c = 0; c < n_chunks; ++c) {
+    const int64_t lo = c * chunk, len = std::min(chunk, total - lo);
+    cudaEventCreateWithFlags(&hw->events[c], cudaEventDisableTiming);
+    if (len > 0)
+      QX_CUDA(cudaMemcpyAsync(staging + lo, d_keys + lo, sizeof(u32) * (size_t)len, cudaMemcpyDeviceToHost, s->stream));
+    QX_CUDA(cudaEventRecord(hw->events[c], s->stream));
+  }
+  QX_CUDA(cudaMemcpyAsync(lambdas, s->lam[s->cur], sizeof(double) * (size_t)total, cudaMemcpyDeviceToHost, s->stream));
+  const int T = std::max(1, std::min<int>(threads, 64));
+  const int device = s->device;
+  static const bool skip_widen = getenv("QX_WIDEN_SKIP") != nullptr;      // timing experiments only
+  for (int t = 0; t < T; ++t)
+    hw->threads.emplace_back([=]() {
+      cudaSetDevice(device);
+      for (int c = 0; c < n_chunks; ++c) {
+        cudaEventSynchronize(hw->events[c]);
+        const int64_t lo = c * chunk, len = std::min(chunk, total - lo);
+        const int64_t a = lo + len * t / T, b = lo + len * (t + 1) / T;
+        // streaming stores: the destination is written once and not read here -- no
+        // read-for-ownership traffic competing with the DMA for host memory bandwidth
+#if defined(__x86_64__)
+        for (int64_t i = a; i < b; ++i) _mm_stream_si64(reinterpret_cast<long long*>(keys + i), (long long)staging[i]);
+        _mm_sfence();
+#else
+        for (int64_t i = a; i < b; ++i) keys[i] = staging[i];
+#endif
+      }
+    });
+  s->host_workers = hw;
+  return QX_OK;
+}
+
 extern "C" int qx_store_synchronize(qx_store* s) {
   QX_REQUIRE(s != nullptr, "store is NULL");
   QX_CUDA(cudaSetDevice(s->device));
   QX_CUDA(cudaStreamSynchronize(s->stream));
+  join_workers(s);
   return QX_OK;
 }

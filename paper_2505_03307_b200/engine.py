@@ -343,6 +343,7 @@ def run(instructions: Sequence[Instruction], n: int, mode, eps: float = DEFAULT_
 
 
 _STREAM_DEBUG = bool(__import__("os").environ.get("QX_STREAM_DEBUG"))
+_NARROW_DOWNLOAD = not __import__("os").environ.get("QX_NO_NARROW_DOWNLOAD")
 STREAM_MIN_RAW = 1 << 23          # below this a single download is not worth splitting
 STREAM_SHARDS = 4
 
@@ -383,6 +384,8 @@ def _finish_streamed(w: _Walker, trace, pinned: bool):
             # no capacity hint: the operator step reserves what it needs (slots, not raw branches)
             child = w.store.slice(lo, hi, 0)
             children.append(child)
+            if pinned and w.n <= 16 and _NARROW_DOWNLOAD:
+                child.set_keep_narrow(True)     # only downloaded next: 32-bit keys over PCIe
             _, r = child.apply_operator_run(counts, axes, weights, program, w.eps)
             ranks[lo:hi] = r
             for local, v in enumerate(r):
@@ -405,6 +408,7 @@ def _finish_streamed(w: _Walker, trace, pinned: bool):
     w.launch_log["merges"] += 1
     w.launch_log["branch_ops"] += 0
     w.launch_log["streamed_ranges"] = len(ranges)
+    w.launch_log["d2h_bytes"] = sum(getattr(c, "d2h_bytes", 0) for c in children)
     for slot in w.open_slots:
         trace[slot] = list(ranks)
     w.open_slots = []
