@@ -264,3 +264,38 @@ def test_eps_zero_takes_the_raw_path_and_matches_the_oracle():
     assert got.rank_trace == want["rank_trace"]
     for g, (lam, idx) in zip(got.final.generators, want["final"]):
         assert np.array_equal(g.keys(), idx) and np.max(np.abs(g.lambdas - lam)) < TOL
+
+
+def _mixed_layers(rng, n, heavy):
+    """Layers of per-qubit operators (generic rotation / one-axis rotation / Clifford / nothing)
+    followed by a CX chain over a random qubit order: supports spread like on the ansatz circuits,
+    so operators have large fan-outs, partial mixing and, at three layers, groups with many sources."""
+    gates = []
+    for _ in range(3 if n <= 8 else 2):
+        for q in range(n):
+            kind = rng.integers(0, 6) if rng.uniform() > heavy else 0
+            if kind <= 2:
+                gates += [qx.Instruction(g, (q,), float(rng.uniform(0, 6.28))) for g in ("RX", "RY", "RZ")]
+            elif kind == 3:
+                gates.append(qx.Instruction(str(rng.choice(["RX", "RY", "RZ"])), (q,), float(rng.uniform(0, 6.28))))
+            elif kind == 4:
+                gates.append(qx.Instruction(str(rng.choice(["H", "S", "X", "SX"])), (q,)))
+        order = rng.permutation(n)
+        gates += [qx.Instruction("CX", (int(a), int(b))) for a, b in zip(order[:-1], order[1:]) if rng.uniform() < 0.85]
+        if rng.integers(0, 2):
+            gates.append(qx.Instruction("H", (int(rng.integers(n)),)))
+    return gates
+
+
+@pytest.mark.parametrize("case", range(14))
+def test_random_entangling_circuits_against_oracle(case):
+    """The grouped operator step on operators of every shape (tools/stress_dense.py runs more)."""
+    rng = np.random.default_rng([77, case])
+    n = int(rng.integers(8, 12))
+    gates = _mixed_layers(rng, n, float(rng.choice([0.0, 0.5, 0.8])))
+    want = oracle.run(gates, n, "v3")
+    got = qx.run(gates, n, "v3")
+    assert got.rank_trace == want["rank_trace"]
+    for g, (lam, idx) in zip(got.final.generators, want["final"]):
+        assert np.array_equal(g.keys(), idx)
+        assert len(lam) == 0 or np.max(np.abs(g.lambdas - lam)) < TOL
