@@ -16,7 +16,7 @@ import numpy as np
 from .errors import ConsistencyError, NativeError, ResourceLimitError
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "lib", "libqimax_b200.so")
+LIB_PATH = os.environ.get("QX_LIB") or os.path.join(HERE, "lib", "libqimax_b200.so")   # QX_LIB: A/B builds (tools/build_variant.sh)
 HEADER_PATH = os.path.join(os.path.dirname(HERE), "include", "qimax_b200.h")
 
 QX_OK, QX_ERR_INVALID, QX_ERR_RESOURCE, QX_ERR_CUDA, QX_ERR_UNSUPPORTED, QX_ERR_CONSISTENCY = range(6)

@@ -139,6 +139,22 @@ k_clifford_sliced(u64* __restrict__ keys, double* __restrict__ lam,
   const int warps = kSlicedThreads / 32;
   for (int64_t c = (int64_t)blockIdx.x * warps + (tid >> 5); c < chunks; c += (int64_t)gridDim.x * warps) {
     const int64_t base = (c << 10) + lane;              // term i of this thread = base + 32 * i
+    // L2 prefetch (no registers held): this chunk's coefficients, touched only at the end of the
+    // round, and the keys of the chunk this warp takes next.  The kernel is latency-bound at 128
+    // registers per thread (profiles/r01h: issue 17 %, long-scoreboard stalls 18 warps per issue);
+    // both dependent round trips of a round now end in L2 instead of HBM.
+#ifndef QX_EXP_NO_CLPF
+    {
+      const int64_t cn = c + (int64_t)gridDim.x * warps;
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int64_t t = (c << 10) + h * 512 + lane * 16;           // one 128-byte line per lane
+        if (t < total) asm volatile("prefetch.global.L2 [%0];" ::"l"(lam + t));
+        const int64_t tn = (cn << 10) + h * 512 + lane * 16;
+        if (tn < total) asm volatile("prefetch.global.L2 [%0];" ::"l"(keys + tn));
+      }
+    }
+#endif
     u32 row[32];
 #pragma unroll
     for (int w = 0; w < NW; ++w) {

@@ -81,12 +81,14 @@ struct __align__(16) TileInfo {
   int64_t off;        // first term of the tile, relative to the start of its segment
   int count;          // terms in the tile (<= tile_terms)
   int seg;            // segment; bit 31 set iff this is the segment's first tile
+  int64_t start0;     // absolute first term in the FIRST pass's input (base_in[seg] + off)
+  int64_t start;      // absolute first term in every later pass's input (seg[seg] + off)
 };
 // A pass reads segment g at base_in[g] + off.  base_in is the offset array itself except for the
 // first pass after the grouped operator step (dense.cu), whose output sits at the slot offsets of
 // the generators with gaps behind the kept terms; every pass WRITES the compact layout seg[g].
 
-static __global__ void k_sort_tilemap(const int64_t* __restrict__ seg, int n_seg,
+static __global__ void k_sort_tilemap(const int64_t* __restrict__ seg, const int64_t* __restrict__ base0, int n_seg,
                                       const int64_t* __restrict__ tile_prefix, TileInfo* __restrict__ info,
                                       int tile_terms) {
   const int64_t total_tiles = tile_prefix[n_seg];
@@ -97,6 +99,8 @@ static __global__ void k_sort_tilemap(const int64_t* __restrict__ seg, int n_seg
     ti.off = (tile - tile_prefix[g]) * tile_terms;
     ti.count = (int)min((int64_t)tile_terms, seg[g + 1] - seg[g] - ti.off);
     ti.seg = g | (tile == tile_prefix[g] ? (int)0x80000000 : 0);
+    ti.start0 = base0[g] + ti.off;
+    ti.start = seg[g] + ti.off;
     info[tile] = ti;
   }
 }
@@ -177,10 +181,8 @@ static __global__ void __launch_bounds__(QX_RADIX) k_sort_scan_hist(u32* __restr
 template <typename K, typename V, int THREADS, int ITEMS>
 struct SortSmem {
   u32 whist[THREADS / 32][QX_RADIX];  // per-warp digit counters -> exclusive warp offsets
-  u32 tile_start[QX_RADIX];           // first slot of each digit in the tile-sorted order
   u32 gbase[QX_RADIX];                // index inside the segment of slot 0 of each digit, minus tile_start (mod 2^32)
   u32 scan[THREADS / 32 + 1];
-  int tile;
   V vals[THREADS * ITEMS];
   K keys[THREADS * ITEMS];
 };
@@ -231,7 +233,7 @@ k_onesweep(const K* __restrict__ keys_in, const V* __restrict__ vals_in,
            const int64_t* __restrict__ seg, const int64_t* __restrict__ base_in,
            const TileInfo* __restrict__ info,
            const int64_t* __restrict__ n_tiles, const u32* __restrict__ digit_base, int base_stride,
-           u32* status, u32* ticket, int which, int ahead, int debug) {
+           u32* status, int which, int ahead, int debug) {
   constexpr int WARPS = THREADS / 32;
   constexpr int TILE = THREADS * ITEMS;
   static_assert(THREADS >= QX_RADIX, "one thread per digit in the scan");
@@ -239,37 +241,23 @@ k_onesweep(const K* __restrict__ keys_in, const V* __restrict__ vals_in,
   SortSmem<K, V, THREADS, ITEMS>& sm = *reinterpret_cast<SortSmem<K, V, THREADS, ITEMS>*>(smem_raw);
   const int tid = threadIdx.x, warp = tid >> 5, lane = lane_id();
 
-  if (tid == 0) sm.tile = (int)atomicAdd(ticket, 1u);
+  // Tile = blockIdx.x: CTAs of a 1-D grid are dispatched in index order, so a tile's predecessors
+  // are resident or done when it looks back (the assumption cub::DeviceScan makes).  No ticket
+  // atomic, no dependent offset-table load: the record holds the absolute start.
   for (int i = tid; i < WARPS * QX_RADIX / 4; i += THREADS)
     reinterpret_cast<uint4*>(&sm.whist[0][0])[i] = make_uint4(0u, 0u, 0u, 0u);
-  __syncthreads();
-  const int64_t tile = sm.tile;
+  const int64_t tile = blockIdx.x;
   const int64_t total_tiles = *n_tiles;
   if (tile >= total_tiles) return;
   const TileInfo ti = info[tile];
+  const bool pass0 = base_in != seg;
   const int g = ti.seg & 0x7fffffff;
   const bool first = ti.seg < 0;
-  const int64_t start = base_in[g] + ti.off;
+  const int64_t start = pass0 ? ti.start0 : ti.start;
   const int count = ti.count;
   const bool full = count == TILE;
   const K* kin = keys_in + start;
   const V* vin = vals_in + start;
-
-  // ---- L2 prefetch of the tile that a CTA will own `ahead` tickets from now.  Tickets are
-  // handed out in order, so every tile is prefetched exactly once, by the CTA `ahead` tiles
-  // before it; with ahead ~ number of resident CTAs the lines arrive in L2 just before use and
-  // the loads below pay L2 latency instead of HBM latency.
-  if (ahead > 0 && tile + ahead < total_tiles) {
-    const TileInfo tp = info[tile + ahead];
-    const int64_t sp = base_in[tp.seg & 0x7fffffff] + tp.off;
-    const int cp = tp.count;
-    for (int i = tid * 16; i < cp; i += THREADS * 16) {      // one 128-byte line of doubles per step
-      if (sizeof(K) == 8 || (i & 16) == 0) asm volatile("prefetch.global.L2 [%0];" ::"l"(keys_in + sp + i));
-      asm volatile("prefetch.global.L2 [%0];" ::"l"(vals_in + sp + i));
-      if (sizeof(V) > 8) asm volatile("prefetch.global.L2 [%0];" ::"l"(vals_in + sp + i + 8));
-    }
-  }
-
   // ---- load, warp-striped: warp w owns tile slots [w*32*ITEMS, (w+1)*32*ITEMS)
   K key[ITEMS];
   const int wslot = warp * (32 * ITEMS) + lane;
@@ -283,6 +271,21 @@ k_onesweep(const K* __restrict__ keys_in, const V* __restrict__ vals_in,
       key[k] = idx < count ? ld_stream(kin + idx) : (K)~(K)0;       // padding sorts last
     }
   }
+  // ---- L2 prefetch of the tile `ahead` positions behind this one (every tile is prefetched
+  // exactly once): with ahead ~ resident CTAs the lines arrive in L2 just before use and the
+  // loads above pay L2 latency instead of HBM latency.  Issued after this tile's own loads so
+  // that the look-up of the far tile's record does not delay them.
+  if (ahead > 0 && tile + ahead < total_tiles) {
+    const TileInfo tp = info[tile + ahead];
+    const int64_t sp = pass0 ? tp.start0 : tp.start;
+    const int cp = tp.count;
+    for (int i = tid * 16; i < cp; i += THREADS * 16) {      // one 128-byte line of doubles per step
+      if (sizeof(K) == 8 || (i & 16) == 0) asm volatile("prefetch.global.L2 [%0];" ::"l"(keys_in + sp + i));
+      asm volatile("prefetch.global.L2 [%0];" ::"l"(vals_in + sp + i));
+      if (sizeof(V) > 8) asm volatile("prefetch.global.L2 [%0];" ::"l"(vals_in + sp + i + 8));
+    }
+  }
+  __syncthreads();
 
   // ---- early counts: per-warp digit histogram with fire-and-forget shared atomics.  Order
   // does not matter for counts, so the tile's aggregate can be published for the tiles behind
@@ -294,24 +297,33 @@ k_onesweep(const K* __restrict__ keys_in, const V* __restrict__ vals_in,
 
   // ---- per digit: exclusive offsets over warps, tile totals, exclusive scan over digits
   u32 digit_total = 0;
+  u32 wcount[WARPS];
   if (tid < QX_RADIX) {
 #pragma unroll
     for (int w = 0; w < WARPS; ++w) {
-      const u32 c = sm.whist[w][tid];
-      sm.whist[w][tid] = digit_total;
-      digit_total += c;
+      wcount[w] = sm.whist[w][tid];
+      digit_total += wcount[w];
     }
   }
   u32 tile_sum;
   const u32 dstart = block_exclusive_sum<u32>(digit_total, sm.scan, tile_sum);
+  // whist[w][d] <- first tile-sorted slot of warp w's terms with digit d: the digit's start in
+  // the tile is folded in here, once per (warp, digit), so the ranking below needs no second
+  // table look-up per term (random digits: 3.5 bank-conflict wavefronts per look-up, 12 % of the
+  // pass's shared-memory wavefronts, and the LSU data pipe is its busiest unit, profiles/r01h)
+  if (tid < QX_RADIX) {
+    u32 running = dstart;
+#pragma unroll
+    for (int w = 0; w < WARPS; ++w) {
+      sm.whist[w][tid] = running;
+      running += wcount[w];
+    }
+  }
   // padding keys all carry digit 255 and sit behind the live ones
   const u32 live_total = digit_total - ((tid == QX_RADIX - 1) ? (u32)(TILE - count) : 0u);
   u32* mine = status + (size_t)tile * QX_RADIX + tid;
   const bool solo = first || (debug & 1);
-  if (tid < QX_RADIX) {
-    sm.tile_start[tid] = dstart;
-    st_volatile_u32(mine, (solo ? kFlagInc : kFlagAgg) | live_total);
-  }
+  if (tid < QX_RADIX) st_volatile_u32(mine, (solo ? kFlagInc : kFlagAgg) | live_total);
   __syncthreads();
 
   // ---- stable rank inside the warp, straight into the tile-sorted slot.  Lanes with equal
@@ -323,24 +335,28 @@ k_onesweep(const K* __restrict__ keys_in, const V* __restrict__ vals_in,
 #pragma unroll
   for (int k = 0; k < ITEMS; ++k) {
     const u32 d = key_byte(key[k], which);
-    const u32 peers = match_digit8(d);
+    const u32 peers = match_digit8(d);     // (the MATCH.ANY instruction is 1.4x slower per pass)
     const u32 below = __popc(peers & lanemask_lt());
     u32 old = 0;
     if (below == 0) old = atomicAdd(&sm.whist[warp][d], (u32)__popc(peers));
-    slot[k] = sm.tile_start[d] + __shfl_sync(QX_FULL_MASK, old, __ffs(peers) - 1) + below;
+    slot[k] = __shfl_sync(QX_FULL_MASK, old, __ffs(peers) - 1) + below;
     sm.keys[slot[k]] = key[k];
   }
-  // coefficients: twelve independent loads in flight, landing while the look-back below runs
-  if (full) {
+  // coefficients: cp.async straight into the tile-sorted slot -- no register staging and, above
+  // all, no wait for the loads before the look-back below starts (with plain loads every thread
+  // sat on its first coefficient for an L2/HBM round trip first: 0.787 -> 0.760 ms per pass)
 #pragma unroll
-    for (int k = 0; k < ITEMS; ++k) sm.vals[slot[k]] = ld_stream(vin + wslot + k * 32);
-  } else {
-#pragma unroll
-    for (int k = 0; k < ITEMS; ++k) {
-      const int idx = wslot + k * 32;
-      if (idx < count) sm.vals[slot[k]] = ld_stream(vin + idx);
+  for (int k = 0; k < ITEMS; ++k) {
+    const int idx = wslot + k * 32;
+    if (full || idx < count) {
+      const u32 dst = (u32)__cvta_generic_to_shared(&sm.vals[slot[k]]);
+      if (sizeof(V) == 8)
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(dst), "l"(vin + idx) : "memory");
+      else
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(vin + idx) : "memory");
     }
   }
+  asm volatile("cp.async.commit_group;" ::: "memory");
 
   // ---- decoupled look-back, one chain per digit, confined to this segment's tiles.  Eight
   // predecessors are read per round trip: with ~300 tiles in flight the nearest inclusive
@@ -372,6 +388,7 @@ k_onesweep(const K* __restrict__ keys_in, const V* __restrict__ vals_in,
     }
     sm.gbase[tid] = digit_base[(size_t)g * base_stride + tid] + excl - dstart;
   }
+  asm volatile("cp.async.wait_group 0;" ::: "memory");
   __syncthreads();
 
   // ---- coalesced write-out: consecutive slots of one digit are consecutive in HBM.  Offsets are
@@ -682,7 +699,7 @@ inline int sort_prefetch_distance(int sm_count) {
 template <typename K, typename V, int THREADS, int ITEMS, int LB, int MINB = (THREADS <= 256 ? 3 : 2),
           typename KO = K>
 int launch_pass(QxArena* ar, MergeBuffers<V>& mb, int cur, int64_t tiles_ub, const TileInfo* info,
-                const int64_t* n_tiles, const u32* digit_base, int base_stride, u32* ticket, int which,
+                const int64_t* n_tiles, const u32* digit_base, int base_stride, int which,
                 const int64_t* base_in) {
   using Smem = SortSmem<K, V, THREADS, ITEMS>;
   static bool attr_set = false;
@@ -694,7 +711,7 @@ int launch_pass(QxArena* ar, MergeBuffers<V>& mb, int cur, int64_t tiles_ub, con
   k_onesweep<K, V, THREADS, ITEMS, LB, MINB, KO><<<(unsigned)tiles_ub, THREADS, sizeof(Smem), ar->stream>>>(
       reinterpret_cast<const K*>(mb.keys[cur]), mb.vals[cur], reinterpret_cast<KO*>(mb.keys[cur ^ 1]),
       mb.vals[cur ^ 1], mb.seg[cur], base_in ? base_in : mb.seg[cur], info, n_tiles,
-      digit_base, base_stride, ar->status, ticket, which, sort_prefetch_distance(ar->sm_count),
+      digit_base, base_stride, ar->status, which, sort_prefetch_distance(ar->sm_count),
       getenv("QX_SORT_DEBUG") ? atoi(getenv("QX_SORT_DEBUG")) : 0);
   QX_CUDA(cudaGetLastError());
   return QX_OK;
@@ -726,30 +743,30 @@ inline int sort_tile_terms(int variant, size_t value_bytes) {
 // WIDEN: the pass reads narrow keys and writes 64-bit ones (last pass of a narrow sort-only merge)
 template <typename K, typename V, bool WIDEN = false>
 int dispatch_pass(int variant, QxArena* ar, MergeBuffers<V>& mb, int cur, int64_t tiles_ub,
-                  const TileInfo* info, const int64_t* n_tiles, const u32* digit_base, int base_stride, u32* ticket,
+                  const TileInfo* info, const int64_t* n_tiles, const u32* digit_base, int base_stride,
                   int which, const int64_t* base_in = nullptr) {
   using KO = typename std::conditional<WIDEN, u64, K>::type;
   if (sizeof(V) > 8)
-    return launch_pass<K, V, 256, 12, 8>(ar, mb, cur, tiles_ub, info, n_tiles, digit_base, base_stride, ticket, which, base_in);
+    return launch_pass<K, V, 256, 12, 8>(ar, mb, cur, tiles_ub, info, n_tiles, digit_base, base_stride, which, base_in);
   if (sizeof(K) == 4) {
     // narrow keys: 56 registers and 68 KB of shared memory per CTA -> three CTAs (36 warps) per SM
     // instead of two; the pass is latency-bound, not HBM-bound (profiles/r01g), so occupancy pays
     switch (variant) {
-      case 2: return launch_pass<K, V, 256, 12, 8, 4, KO>(ar, mb, cur, tiles_ub, info, n_tiles, digit_base, base_stride, ticket, which, base_in);
-      case 3: return launch_pass<K, V, 256, 16, 8, 3, KO>(ar, mb, cur, tiles_ub, info, n_tiles, digit_base, base_stride, ticket, which, base_in);
-      case 4: return launch_pass<K, V, 512, 8, 8, 2, KO>(ar, mb, cur, tiles_ub, info, n_tiles, digit_base, base_stride, ticket, which, base_in);
-      case 5: return launch_pass<K, V, 384, 8, 8, 4, KO>(ar, mb, cur, tiles_ub, info, n_tiles, digit_base, base_stride, ticket, which, base_in);
-      case 6: return launch_pass<K, V, 384, 10, 8, 3, KO>(ar, mb, cur, tiles_ub, info, n_tiles, digit_base, base_stride, ticket, which, base_in);
-      default: return launch_pass<K, V, 384, 12, 8, 3, KO>(ar, mb, cur, tiles_ub, info, n_tiles, digit_base, base_stride, ticket, which, base_in);
+      case 2: return launch_pass<K, V, 256, 12, 8, 4, KO>(ar, mb, cur, tiles_ub, info, n_tiles, digit_base, base_stride, which, base_in);
+      case 3: return launch_pass<K, V, 256, 16, 8, 3, KO>(ar, mb, cur, tiles_ub, info, n_tiles, digit_base, base_stride, which, base_in);
+      case 4: return launch_pass<K, V, 512, 8, 8, 2, KO>(ar, mb, cur, tiles_ub, info, n_tiles, digit_base, base_stride, which, base_in);
+      case 5: return launch_pass<K, V, 384, 8, 8, 4, KO>(ar, mb, cur, tiles_ub, info, n_tiles, digit_base, base_stride, which, base_in);
+      case 6: return launch_pass<K, V, 384, 10, 8, 3, KO>(ar, mb, cur, tiles_ub, info, n_tiles, digit_base, base_stride, which, base_in);
+      default: return launch_pass<K, V, 384, 12, 8, 3, KO>(ar, mb, cur, tiles_ub, info, n_tiles, digit_base, base_stride, which, base_in);
     }
   }
   switch (variant) {
-    case 2: return launch_pass<K, V, 256, 12, 8>(ar, mb, cur, tiles_ub, info, n_tiles, digit_base, base_stride, ticket, which, base_in);
-    case 3: return launch_pass<K, V, 256, 16, 8>(ar, mb, cur, tiles_ub, info, n_tiles, digit_base, base_stride, ticket, which, base_in);
-    case 4: return launch_pass<K, V, 512, 8, 8>(ar, mb, cur, tiles_ub, info, n_tiles, digit_base, base_stride, ticket, which, base_in);
-    case 5: return launch_pass<K, V, 384, 8, 8, 3>(ar, mb, cur, tiles_ub, info, n_tiles, digit_base, base_stride, ticket, which, base_in);
-    case 6: return launch_pass<K, V, 384, 10, 8>(ar, mb, cur, tiles_ub, info, n_tiles, digit_base, base_stride, ticket, which, base_in);
-    default: return launch_pass<K, V, 384, 12, 8>(ar, mb, cur, tiles_ub, info, n_tiles, digit_base, base_stride, ticket, which, base_in);
+    case 2: return launch_pass<K, V, 256, 12, 8>(ar, mb, cur, tiles_ub, info, n_tiles, digit_base, base_stride, which, base_in);
+    case 3: return launch_pass<K, V, 256, 16, 8>(ar, mb, cur, tiles_ub, info, n_tiles, digit_base, base_stride, which, base_in);
+    case 4: return launch_pass<K, V, 512, 8, 8>(ar, mb, cur, tiles_ub, info, n_tiles, digit_base, base_stride, which, base_in);
+    case 5: return launch_pass<K, V, 384, 8, 8, 3>(ar, mb, cur, tiles_ub, info, n_tiles, digit_base, base_stride, which, base_in);
+    case 6: return launch_pass<K, V, 384, 10, 8>(ar, mb, cur, tiles_ub, info, n_tiles, digit_base, base_stride, which, base_in);
+    default: return launch_pass<K, V, 384, 12, 8>(ar, mb, cur, tiles_ub, info, n_tiles, digit_base, base_stride, which, base_in);
   }
 }
 
@@ -797,7 +814,7 @@ int merge_large(QxArena* ar, MergeBuffers<V>& mb, double eps, int cls_reduce, bo
   int cur = mb.cur;
   k_sort_plan<<<1, 32, 0, ar->stream>>>(mb.seg[cur], n_seg, tile_prefix, ticket, tile_terms);
   k_sort_tilemap<<<(unsigned)std::max<int64_t>(1, std::min<int64_t>((tiles_ub + 255) / 256, 4096)), 256, 0, ar->stream>>>(
-      mb.seg[cur], n_seg, tile_prefix, info, tile_terms);
+      mb.seg[cur], first_base_in ? first_base_in : mb.seg[cur], n_seg, tile_prefix, info, tile_terms);
   qx_count_launches(2);
   QX_CUDA(cudaGetLastError());
   if (pre_hist) {
@@ -821,14 +838,13 @@ int merge_large(QxArena* ar, MergeBuffers<V>& mb, double eps, int cls_reduce, bo
                           cudaMemcpyDeviceToDevice, ar->stream));
   for (int p = 0; p < passes; ++p) {
     QX_CUDA(cudaMemsetAsync(ar->status, 0, sizeof(u32) * (size_t)(tiles_ub * QX_RADIX), ar->stream));
-    QX_CUDA(cudaMemsetAsync(ticket, 0, sizeof(u32), ar->stream));
     QxProfileScope prof(cls_pass, ar->stream, 2.0 * (sizeof(K) + sizeof(V)) * (double)mb.ub_total);
     if (!do_reduce && sizeof(K) == 4 && p == passes - 1 && widen_last)
       QX_TRY((dispatch_pass<K, V, true>(variant, ar, mb, cur, tiles_ub, info, n_tiles, hist + (size_t)p * QX_RADIX,
-                                        passes * QX_RADIX, ticket, p, p == 0 ? first_base_in : nullptr)));
+                                        passes * QX_RADIX, p, p == 0 ? first_base_in : nullptr)));
     else
       QX_TRY((dispatch_pass<K, V>(variant, ar, mb, cur, tiles_ub, info, n_tiles, hist + (size_t)p * QX_RADIX,
-                                  passes * QX_RADIX, ticket, p, p == 0 ? first_base_in : nullptr)));
+                                  passes * QX_RADIX, p, p == 0 ? first_base_in : nullptr)));
     cur ^= 1;
   }
   if (!do_reduce) {
