@@ -106,6 +106,17 @@ int qx_store_set_keep_narrow(qx_store* s, int on);
  * qx_store_download_async if the store holds 64-bit keys. */
 int qx_store_download_narrow_async(qx_store* s, int64_t* offsets, uint64_t* keys, double* lambdas,
                                    int64_t cap_terms, uint32_t* staging, int32_t threads);
+/* qx_store_set_keep_narrow(s, 2) additionally allows the PACKED form for large results: the last
+ * sort pass writes only the low 16 bits of every key plus, per generator, a table of 65537 words
+ * first[h] = position of the first key whose high half is >= h (keys are sorted, so the high
+ * halves are the bucket index).  10 bytes per term cross PCIe.  This call downloads whichever
+ * form the store holds (packed, 32-bit, 64-bit): `staging` (page-locked, staging_words 32-bit
+ * words; cap_terms + 65537 * n_segments + 2 always suffices) receives the tables and the halves,
+ * `threads` host threads rebuild the 64-bit keys bucket by bucket while the rest is on the wire.
+ * *d2h_bytes (may be NULL) = bytes copied device -> host. */
+int qx_store_download_packed_async(qx_store* s, int64_t* offsets, uint64_t* keys, double* lambdas,
+                                   int64_t cap_terms, uint32_t* staging, int64_t staging_words,
+                                   int32_t threads, int64_t* d2h_bytes);
 
 /* ---- more than 32 qubits (reference stabilizer.py:40-59 switches to Python
  * big-int indices there).  qx_store_create accepts n_qubits <= 512; above 32 the store is WIDE:

@@ -60,6 +60,7 @@ SIGNATURES = {
     "qx_store_download_async": (C.c_int, [_p, _p, _p, _p, _i64]),
     "qx_store_set_keep_narrow": (C.c_int, [_p, C.c_int]),
     "qx_store_download_narrow_async": (C.c_int, [_p, _p, _p, _p, _i64, _p, _i32]),
+    "qx_store_download_packed_async": (C.c_int, [_p, _p, _p, _p, _i64, _p, _i64, _i32, _p]),
     "qx_apply_clifford": (C.c_int, [_p, _p, _i32, _u32, _u32, _u32]),
     "qx_apply_split": (C.c_int, [_p, _i32, _p, _p, _p, _p]),
     "qx_apply_operator": (C.c_int, [_p, _p, _p, _p, _i64, _P(_i64)]),

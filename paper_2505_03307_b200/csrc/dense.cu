@@ -1136,11 +1136,25 @@ int qx_dense_operator_step(qx_store* s, const OperatorTable& nz, const uint32_t*
   // the kept terms of generator g sit at its slot offset; the first pass reads them from there
   // a store that is only downloaded next keeps its 32-bit keys: 12 bytes per term cross PCIe
   // instead of 16 and the host widens them while the copy runs (qx_store_download_narrow_async)
-  const bool keep_narrow = narrow && s->want_narrow;
-  if (narrow) QX_TRY((qxm::merge_large<double, u32>(s, mb, eps, QX_K_REDUCE, false, QX_K_SORT_PASS, QX_K_SORT_HIST, seg_slot, hist, !keep_narrow)));
+  const bool keep_narrow = narrow && s->want_narrow != 0;
+  // ... or, for results large enough that the bucket tables do not matter (10 bytes per term on
+  // the wire): 16-bit low halves + per generator the first position of every high half.  The
+  // table sits in the output key block behind the halves (8 bytes of room per term, 2 used).
+  u32* pack_bnd = nullptr;
+  const int64_t bnd_bytes = 4ll * n_seg * (QX_PACK_BUCKETS + 1);
+  {
+    const int passes_now = std::min(qxm::kMaxPasses, (2 * s->n_qubits + QX_RADIX_BITS - 1) / QX_RADIX_BITS);
+    const int out_buf = mb.cur ^ (passes_now & 1);            // the buffer the last pass writes
+    const int64_t lo_bytes = (2 * total + 255) / 256 * 256;
+    if (keep_narrow && s->want_narrow == 2 && total >= 8ll * n_seg * QX_PACK_BUCKETS &&
+        lo_bytes + bnd_bytes <= 8 * s->cap)
+      pack_bnd = reinterpret_cast<u32*>(reinterpret_cast<char*>(s->keys[out_buf]) + lo_bytes);
+  }
+  if (narrow) QX_TRY((qxm::merge_large<double, u32>(s, mb, eps, QX_K_REDUCE, false, QX_K_SORT_PASS, QX_K_SORT_HIST, seg_slot, hist, !keep_narrow, pack_bnd)));
   else QX_TRY((qxm::merge_large<double, u64>(s, mb, eps, QX_K_REDUCE, false, QX_K_SORT_PASS, QX_K_SORT_HIST, seg_slot, hist)));
   s->cur = mb.cur;
   s->narrow_keys = keep_narrow;
+  s->pack_bnd = pack_bnd;
   if (!s->exact) QX_TRY(qx_store_refresh(s));      // kept counts: exact offsets for the caller
   return QX_OK;
 }

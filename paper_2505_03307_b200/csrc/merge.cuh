@@ -233,7 +233,7 @@ k_onesweep(const K* __restrict__ keys_in, const V* __restrict__ vals_in,
            const int64_t* __restrict__ seg, const int64_t* __restrict__ base_in,
            const TileInfo* __restrict__ info,
            const int64_t* __restrict__ n_tiles, const u32* __restrict__ digit_base, int base_stride,
-           u32* status, int which, int ahead, int debug) {
+           u32* status, int which, int ahead, int debug, u32* __restrict__ bnd) {
   constexpr int WARPS = THREADS / 32;
   constexpr int TILE = THREADS * ITEMS;
   static_assert(THREADS >= QX_RADIX, "one thread per digit in the scan");
@@ -404,6 +404,16 @@ k_onesweep(const K* __restrict__ keys_in, const V* __restrict__ vals_in,
       const u32 dst = sm.gbase[key_byte(kk, which)] + (u32)slot;
       st_stream(kout + dst, (KO)kk);
       st_stream(vout + dst, sm.vals[slot]);
+      if (sizeof(KO) == 2) {
+        // packed download format (last pass only): the key leaves as its low 16 bits; the high
+        // 16 are recovered from bucket boundaries, bnd[g][h] = first position in generator g of
+        // a key with high half h.  Tile-sorted order agrees with the final order, so a term whose
+        // tile predecessor has the same high half is never the first of its bucket: ~300
+        // candidates per tile, one RED.MIN each.
+        const u32 hi = (u32)((u64)kk >> 16);
+        if (slot == 0 || (u32)((u64)sm.keys[slot - 1] >> 16) != hi)
+          atomicMin(bnd + (size_t)g * (QX_PACK_BUCKETS + 1) + hi, dst);
+      }
     }
   }
 }
@@ -700,7 +710,7 @@ template <typename K, typename V, int THREADS, int ITEMS, int LB, int MINB = (TH
           typename KO = K>
 int launch_pass(QxArena* ar, MergeBuffers<V>& mb, int cur, int64_t tiles_ub, const TileInfo* info,
                 const int64_t* n_tiles, const u32* digit_base, int base_stride, int which,
-                const int64_t* base_in) {
+                const int64_t* base_in, u32* bnd = nullptr) {
   using Smem = SortSmem<K, V, THREADS, ITEMS>;
   static bool attr_set = false;
   if (!attr_set) {
@@ -712,9 +722,36 @@ int launch_pass(QxArena* ar, MergeBuffers<V>& mb, int cur, int64_t tiles_ub, con
       reinterpret_cast<const K*>(mb.keys[cur]), mb.vals[cur], reinterpret_cast<KO*>(mb.keys[cur ^ 1]),
       mb.vals[cur ^ 1], mb.seg[cur], base_in ? base_in : mb.seg[cur], info, n_tiles,
       digit_base, base_stride, ar->status, which, sort_prefetch_distance(ar->sm_count),
-      getenv("QX_SORT_DEBUG") ? atoi(getenv("QX_SORT_DEBUG")) : 0);
+      getenv("QX_SORT_DEBUG") ? atoi(getenv("QX_SORT_DEBUG")) : 0, bnd);
   QX_CUDA(cudaGetLastError());
   return QX_OK;
+}
+
+// Bucket table of the packed download: exclusive positions, entry QX_PACK_BUCKETS = rank.  The
+// passes left bnd[g][h] = first position of a key with high half h (or ~0 for an empty bucket);
+// a backward running minimum turns that into "first position of a key with high half >= h".
+static __global__ void __launch_bounds__(1024) k_pack_bounds(u32* __restrict__ bnd, const int64_t* __restrict__ seg) {
+  __shared__ u32 s_min[1024];
+  constexpr int PER = QX_PACK_BUCKETS / 1024;
+  u32* row = bnd + (size_t)blockIdx.x * (QX_PACK_BUCKETS + 1);
+  const u32 rank = (u32)(seg[blockIdx.x + 1] - seg[blockIdx.x]);
+  const int t = threadIdx.x;
+  u32 m = 0xffffffffu;
+  for (int i = 0; i < PER; ++i) m = min(m, row[t * PER + i]);
+  s_min[t] = m;
+  __syncthreads();
+  for (int d = 1; d < 1024; d <<= 1) {                 // suffix minimum over the chunks
+    const u32 o = t + d < 1024 ? s_min[t + d] : 0xffffffffu;
+    __syncthreads();
+    s_min[t] = min(s_min[t], o);
+    __syncthreads();
+  }
+  u32 carry = t + 1 < 1024 ? min(s_min[t + 1], rank) : rank;
+  for (int i = PER - 1; i >= 0; --i) {
+    carry = min(carry, row[t * PER + i]);
+    row[t * PER + i] = carry;
+  }
+  if (t == 0) row[QX_PACK_BUCKETS] = rank;
 }
 
 // Tile geometry of the sort pass; QX_SORT_VARIANT picks one for A/B runs on the GPU.
@@ -780,7 +817,8 @@ int dispatch_pass(int variant, QxArena* ar, MergeBuffers<V>& mb, int cur, int64_
 template <typename V, typename K = u64>
 int merge_large(QxArena* ar, MergeBuffers<V>& mb, double eps, int cls_reduce, bool do_reduce = true,
                 int cls_pass = QX_K_SORT_PASS, int cls_hist = QX_K_SORT_HIST,
-                const int64_t* first_base_in = nullptr, const u32* pre_hist = nullptr, bool widen_last = true) {
+                const int64_t* first_base_in = nullptr, const u32* pre_hist = nullptr, bool widen_last = true,
+                u32* pack_bnd = nullptr) {
   const int n_seg = mb.n_seg;
   const int passes = std::min(kMaxPasses, (2 * ar->n_qubits + QX_RADIX_BITS - 1) / QX_RADIX_BITS);
   if (mb.ub_seg >= (int64_t)kFlagVal)
@@ -839,7 +877,18 @@ int merge_large(QxArena* ar, MergeBuffers<V>& mb, double eps, int cls_reduce, bo
   for (int p = 0; p < passes; ++p) {
     QX_CUDA(cudaMemsetAsync(ar->status, 0, sizeof(u32) * (size_t)(tiles_ub * QX_RADIX), ar->stream));
     QxProfileScope prof(cls_pass, ar->stream, 2.0 * (sizeof(K) + sizeof(V)) * (double)mb.ub_total);
-    if (!do_reduce && sizeof(K) == 4 && p == passes - 1 && widen_last)
+    if (!do_reduce && sizeof(K) == 4 && p == passes - 1 && pack_bnd) {
+      // packed download: 16-bit keys + bucket table (see k_onesweep's write-out)
+      if constexpr (sizeof(K) == 4 && sizeof(V) == 8) {
+        QX_CUDA(cudaMemsetAsync(pack_bnd, 0xff, sizeof(u32) * (size_t)n_seg * (QX_PACK_BUCKETS + 1), ar->stream));
+        QX_TRY((launch_pass<u32, V, 384, 12, 8, 3, unsigned short>(
+            ar, mb, cur, tiles_ub, info, n_tiles, hist + (size_t)p * QX_RADIX, passes * QX_RADIX, p,
+            p == 0 ? first_base_in : nullptr, pack_bnd)));
+        k_pack_bounds<<<n_seg, 1024, 0, ar->stream>>>(pack_bnd, mb.seg[cur]);
+        qx_count_launches(1);
+        QX_CUDA(cudaGetLastError());
+      }
+    } else if (!do_reduce && sizeof(K) == 4 && p == passes - 1 && widen_last)
       QX_TRY((dispatch_pass<K, V, true>(variant, ar, mb, cur, tiles_ub, info, n_tiles, hist + (size_t)p * QX_RADIX,
                                         passes * QX_RADIX, p, p == 0 ? first_base_in : nullptr)));
     else

@@ -14,6 +14,7 @@ __device__ __forceinline__ double ld_stream(const double* p) { return __ldcs(p);
 __device__ __forceinline__ double2 ld_stream(const double2* p) { return __ldcs(p); }
 __device__ __forceinline__ void st_stream(u64* p, u64 v) { __stcs(p, v); }
 __device__ __forceinline__ void st_stream(u32* p, u32 v) { __stcs(p, v); }
+__device__ __forceinline__ void st_stream(unsigned short* p, unsigned short v) { __stcs(p, v); }
 __device__ __forceinline__ void st_stream(double* p, double v) { __stcs(p, v); }
 __device__ __forceinline__ void st_stream(double2* p, double2 v) { __stcs(p, v); }
 

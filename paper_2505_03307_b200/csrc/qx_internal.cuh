@@ -59,6 +59,7 @@ constexpr int QX_MAX_WORDS = 16;          // multi-word keys (wide.cu): Clifford
 constexpr int QX_MAX_QUBITS_WIDE = 32 * QX_MAX_WORDS;
 constexpr int QX_RADIX_BITS = 8;
 constexpr int QX_RADIX = 1 << QX_RADIX_BITS;
+constexpr int QX_PACK_BUCKETS = 1 << 16;  // packed download: one bucket per value of a key's high 16 bits
 constexpr int QX_SORT_THREADS = 384;     // 12 warps
 constexpr int QX_SORT_ITEMS = 12;        // keys per thread, warp-striped
 constexpr int QX_SORT_TILE = QX_SORT_THREADS * QX_SORT_ITEMS;   // 4608 terms
@@ -110,8 +111,11 @@ struct qx_store : QxArena {
   u64* keys[2] = {nullptr, nullptr};
   double* lam[2] = {nullptr, nullptr};
   int64_t* seg[2] = {nullptr, nullptr};   // device offsets, n_seg+1 each
-  bool want_narrow = false;     // the caller only downloads next: the grouped step may leave 32-bit keys
+  int want_narrow = 0;          // the caller only downloads next: the grouped step may leave 32-bit keys (1)
+                                // or 16-bit low halves + a bucket table (2)
   bool narrow_keys = false;     // keys[cur] holds 32-bit keys (n <= 16); only the narrow download reads them
+  u32* pack_bnd = nullptr;      // != nullptr: keys[cur] holds 16-bit low halves and this is the bucket table
+                                // (n_seg x (QX_PACK_BUCKETS + 1), inside the keys[cur] block behind the halves)
   void* host_workers = nullptr; // threads widening downloaded keys on the host (store.cu), joined by synchronize
   int n_words = 1;              // 64-bit words per key; > 1 = wide store (wide.cu)
   u64* hi[2] = {nullptr, nullptr};        // words 1..n_words-1, plane-major, `cap` words per plane

@@ -776,7 +776,7 @@ void join_workers(qx_store* s) {
 
 extern "C" int qx_store_set_keep_narrow(qx_store* s, int on) {
   QX_REQUIRE(s != nullptr, "store is NULL");
-  s->want_narrow = on != 0;
+  s->want_narrow = on < 0 ? 0 : (on > 2 ? 2 : on);
   return QX_OK;
 }
 
@@ -828,6 +828,96 @@ extern "C" int qx_store_download_narrow_async(qx_store* s, int64_t* offsets, uin
         _mm_sfence();
 #else
         for (int64_t i = a; i < b; ++i) keys[i] = staging[i];
+#endif
+      }
+    });
+  s->host_workers = hw;
+  return QX_OK;
+}
+
+// Packed form (qx_store_set_keep_narrow(s, 2) and a large result): per term the low 16 bits of
+// its key, per generator a table first[h] = position of its first key with high half >= h.
+// Ten bytes per term cross PCIe; the host threads rebuild the 64-bit keys bucket by bucket.
+extern "C" int qx_store_download_packed_async(qx_store* s, int64_t* offsets, uint64_t* keys, double* lambdas,
+                                              int64_t cap_terms, uint32_t* staging, int64_t staging_words,
+                                              int32_t threads, int64_t* d2h_bytes) {
+  QX_REQUIRE(s && offsets && keys && lambdas, "NULL argument");
+  if (!s->narrow_keys || !s->pack_bnd) {
+    QX_REQUIRE(!s->narrow_keys || staging_words >= cap_terms, "staging holds %lld words, need %lld",
+               (long long)staging_words, (long long)cap_terms);
+    QX_TRY(qx_store_download_narrow_async(s, offsets, keys, lambdas, cap_terms, staging, threads));
+    if (d2h_bytes) *d2h_bytes = (s->narrow_keys ? 12 : 16) * s->h_seg[s->n_seg];
+    return QX_OK;
+  }
+  QX_REQUIRE(staging != nullptr, "staging is NULL");
+  if (!s->exact) QX_TRY(qx_store_refresh(s));
+  memcpy(offsets, s->h_seg, sizeof(int64_t) * (size_t)(s->n_seg + 1));
+  const int64_t total = s->h_seg[s->n_seg];
+  const int n_seg = s->n_seg;
+  const int64_t bnd_words = (int64_t)n_seg * (QX_PACK_BUCKETS + 1);
+  const int64_t lo_words = (total + 1) / 2;
+  QX_REQUIRE(cap_terms >= total, "download buffer holds %lld terms, store has %lld", (long long)cap_terms,
+             (long long)total);
+  QX_REQUIRE(staging_words >= bnd_words + lo_words, "staging holds %lld words, the packed form needs %lld",
+             (long long)staging_words, (long long)(bnd_words + lo_words));
+  QX_CUDA(cudaSetDevice(s->device));
+  join_workers(s);
+  if (d2h_bytes) *d2h_bytes = 10 * total + 4 * bnd_words;
+  if (total == 0) return QX_OK;
+  // staging: [bucket tables][low halves]; the tables first (every chunk needs them), then the
+  // halves in a few chunks with an event behind each, then the coefficients in one copy
+  u32* h_bnd = staging;
+  unsigned short* h_lo = reinterpret_cast<unsigned short*>(staging + bnd_words);
+  static const int max_chunks = getenv("QX_WIDEN_CHUNKS") ? atoi(getenv("QX_WIDEN_CHUNKS")) : 2;
+  const int n_chunks = (int)std::max<int64_t>(1, std::min<int64_t>(max_chunks, total / (1 << 20)));
+  const int64_t chunk = (total + n_chunks - 1) / n_chunks;
+  HostWorkers* hw = new HostWorkers();
+  hw->events.resize(n_chunks);
+  QX_CUDA(cudaMemcpyAsync(h_bnd, s->pack_bnd, sizeof(u32) * (size_t)bnd_words, cudaMemcpyDeviceToHost, s->stream));
+  const unsigned short* d_lo = reinterpret_cast<const unsigned short*>(s->keys[s->cur]);
+  for (int c = 0; c < n_chunks; ++c) {
+    const int64_t lo = c * chunk, len = std::min(chunk, total - lo);
+    cudaEventCreateWithFlags(&hw->events[c], cudaEventDisableTiming);
+    if (len > 0)
+      QX_CUDA(cudaMemcpyAsync(h_lo + lo, d_lo + lo, sizeof(unsigned short) * (size_t)len, cudaMemcpyDeviceToHost, s->stream));
+    QX_CUDA(cudaEventRecord(hw->events[c], s->stream));
+  }
+  QX_CUDA(cudaMemcpyAsync(lambdas, s->lam[s->cur], sizeof(double) * (size_t)total, cudaMemcpyDeviceToHost, s->stream));
+  const int T = std::max(1, std::min<int>(threads, 64));
+  const int device = s->device;
+  std::vector<int64_t> off(offsets, offsets + n_seg + 1);
+  for (int t = 0; t < T; ++t)
+    hw->threads.emplace_back([=]() {
+      cudaSetDevice(device);
+      for (int c = 0; c < n_chunks; ++c) {
+        cudaEventSynchronize(hw->events[c]);
+        const int64_t lo = c * chunk, len = std::min(chunk, total - lo);
+        const int64_t a = lo + len * t / T, b = lo + len * (t + 1) / T;     // my global positions
+        int g = (int)(std::upper_bound(off.begin(), off.end(), a) - off.begin()) - 1;
+        for (int64_t p = a; p < b; ++g) {
+          const int64_t g0 = off[g], g1 = std::min<int64_t>(off[g + 1], b);
+          if (g1 <= p) continue;                                             // empty generator
+          const u32* first = h_bnd + (size_t)g * (QX_PACK_BUCKETS + 1);
+          const u32 lp = (u32)(p - g0), le = (u32)(g1 - g0);
+          // bucket of local position lp: first[h] <= lp < first[h + 1]
+          u32 h = (u32)(std::upper_bound(first, first + QX_PACK_BUCKETS + 1, lp) - first) - 1u;
+          u32 q = lp;
+          while (q < le) {
+            const u32 end = std::min(first[h + 1], le);
+            const u64 hi = (u64)h << 16;
+#if defined(__x86_64__)
+            for (u32 i = q; i < end; ++i)
+              _mm_stream_si64(reinterpret_cast<long long*>(keys + g0 + i), (long long)(hi | h_lo[g0 + i]));
+#else
+            for (u32 i = q; i < end; ++i) keys[g0 + i] = hi | h_lo[g0 + i];
+#endif
+            if (end > q) q = end;
+            ++h;
+          }
+          p = g1;
+        }
+#if defined(__x86_64__)
+        _mm_sfence();
 #endif
       }
     });

@@ -344,6 +344,7 @@ def run(instructions: Sequence[Instruction], n: int, mode, eps: float = DEFAULT_
 
 _STREAM_DEBUG = bool(__import__("os").environ.get("QX_STREAM_DEBUG"))
 _NARROW_DOWNLOAD = not __import__("os").environ.get("QX_NO_NARROW_DOWNLOAD")
+_NARROW_FORM = int(__import__("os").environ.get("QX_NARROW_FORM", "2"))   # 1: 32-bit keys, 2: packed allowed
 STREAM_MIN_RAW = 1 << 23          # below this a single download is not worth splitting
 STREAM_SHARDS = 4
 
@@ -385,7 +386,7 @@ def _finish_streamed(w: _Walker, trace, pinned: bool):
             child = w.store.slice(lo, hi, 0)
             children.append(child)
             if pinned and w.n <= 16 and _NARROW_DOWNLOAD:
-                child.set_keep_narrow(True)     # only downloaded next: 32-bit keys over PCIe
+                child.set_keep_narrow(_NARROW_FORM)   # only downloaded next: 16- or 32-bit keys over PCIe
             _, r = child.apply_operator_run(counts, axes, weights, program, w.eps)
             ranks[lo:hi] = r
             for local, v in enumerate(r):

@@ -139,9 +139,10 @@ class DeviceStore:
         nat.check(nat.lib().qx_store_slice(self._h, int(seg_lo), int(seg_hi), int(capacity), C.byref(child._h)))
         return child
 
-    def set_keep_narrow(self, on: bool = True):
-        """The store is only downloaded next: let the operator step leave 32-bit keys (n <= 16)."""
-        nat.check(nat.lib().qx_store_set_keep_narrow(self._h, 1 if on else 0))
+    def set_keep_narrow(self, on=True):
+        """The store is only downloaded next: let the operator step leave 32-bit keys (n <= 16);
+        ``on=2`` also allows the packed form (16-bit low halves + bucket tables) for large results."""
+        nat.check(nat.lib().qx_store_set_keep_narrow(self._h, int(on)))
         self._keep_narrow = bool(on)
 
     def download_async(self, pinned: bool = True):
@@ -153,14 +154,17 @@ class DeviceStore:
         np.cumsum(off[1:], out=off[1:])
         total = int(off[-1])
         if pinned and total > 0 and getattr(self, "_keep_narrow", False):
-            buf = nat.PINNED.take(20 * total)
+            words = total + 65537 * self.n_segments + 2            # enough for either narrow form
+            buf = nat.PINNED.take(16 * total + 4 * words)
             keys = buf.view(np.uint64, 0, total)
             lam = buf.view(np.float64, 8 * total, total)
-            staging = buf.view(np.uint32, 16 * total, total)
+            staging = buf.view(np.uint32, 16 * total, words)
             self._staging = staging                                # alive until synchronize()
-            nat.check(nat.lib().qx_store_download_narrow_async(
-                self._h, nat.ptr(off), nat.ptr(keys), nat.ptr(lam), total, nat.ptr(staging), HOST_WIDEN_THREADS))
-            self.d2h_bytes = 12 * total
+            d2h = C.c_int64()
+            nat.check(nat.lib().qx_store_download_packed_async(
+                self._h, nat.ptr(off), nat.ptr(keys), nat.ptr(lam), total, nat.ptr(staging), words,
+                HOST_WIDEN_THREADS, C.byref(d2h)))
+            self.d2h_bytes = int(d2h.value)
             return off, keys, lam
         self.d2h_bytes = 16 * total
         if pinned and total > 0:

@@ -246,6 +246,31 @@ def test_streamed_finish_equals_plain_download(monkeypatch):
         assert np.array_equal(g.keys(), keys) and np.array_equal(g.lambdas, lam)
 
 
+@pytest.mark.parametrize("form", [1, 2])
+def test_narrow_and_packed_downloads_equal_plain_download(monkeypatch, form):
+    """Streamed results of n <= 16 cross PCIe as 32-bit keys (form 1) or, when large, as 16-bit
+    low halves + per-generator bucket tables written by the last sort pass (form 2); host threads
+    rebuild the 64-bit keys.  Either way run() must return exactly what a plain download gives."""
+    from paper_2505_03307_b200 import engine
+
+    n, gates = workloads.build("c4_xyz_14_2")
+    monkeypatch.setattr(engine, "_NARROW_FORM", form)
+    streamed = qx.run(gates, n, "v3", pinned=True)
+    assert streamed.device.get("streamed_ranges", 0) >= 2
+    total = sum(g.rank for g in streamed.final.generators)
+    if form == 2:
+        assert streamed.device["d2h_bytes"] < 12 * total        # at least one range went packed
+    else:
+        assert streamed.device["d2h_bytes"] == 12 * total
+    plain = qx.run(gates, n, "v3", download=False)
+    try:
+        segs = plain.device["store"].segments()
+    finally:
+        plain.device["store"].close()
+    for g, (lam, keys) in zip(streamed.final.generators, segs):
+        assert np.array_equal(g.keys(), keys) and np.array_equal(g.lambdas, lam)
+
+
 def test_collapse_in_the_grouped_operator_step():
     """An eps above every coefficient empties a generator inside the grouped dense path; the engine
     must report it like the reference (engine.py:148-152)."""

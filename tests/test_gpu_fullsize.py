@@ -42,6 +42,13 @@ def test_config4_16_2_properties():
     finally:
         store.close()
     assert first == second                                                  # bitwise run-to-run determinism
+    # the public-API path of the bench (streamed ranges, packed 16-bit keys + bucket tables over
+    # PCIe, keys rebuilt by host threads) returns the same bytes
+    rep3 = qx.run(gates, n, "v3", pinned=True)
+    assert rep3.device["d2h_bytes"] < 11 * 125_430_039
+    keys3 = np.concatenate([g.keys() for g in rep3.final.generators])
+    lam3 = np.concatenate([g.lambdas for g in rep3.final.generators])
+    assert (hashlib.sha256(keys3.tobytes()).hexdigest(), hashlib.sha256(lam3.tobytes()).hexdigest()) == first
 
 
 def test_gpu_only_ladder_point_18_2():
