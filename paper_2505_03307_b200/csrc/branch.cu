@@ -58,6 +58,14 @@ k_split(const u64* __restrict__ keys_in, const double* __restrict__ lam_in,
   if (tile >= ntiles) return;
   const int warp = threadIdx.x >> 5, lane = lane_id();
   const int64_t wbase = (int64_t)tile * kTile + (int64_t)warp * (32 * kItems);
+  {   // the tile a CTA kPrefetchAhead positions later will read: have it in L2 by then
+    const int64_t far = ((int64_t)tile + kPrefetchAhead) * kTile;
+    if (far < total) {
+      const int cnt = (int)min((int64_t)kTile, total - far);
+      prefetch_l2(keys_in + far, cnt);
+      prefetch_l2(lam_in + far, cnt);
+    }
+  }
 
   u64 key[kItems];
   double lam[kItems];

@@ -449,16 +449,23 @@ k_reduce(const K* __restrict__ keys_in, const V* __restrict__ vals_in,
   extern __shared__ __align__(16) unsigned char smem_raw[];
   ReduceSmem<K, V, kRedThreads, kRedItems>& sm =
       *reinterpret_cast<ReduceSmem<K, V, kRedThreads, kRedItems>*>(smem_raw);
-  if (threadIdx.x == 0) sm.tile = (int)atomicAdd(ticket, 1u);
   if (threadIdx.x < kRedTile / 32) sm.opens[threadIdx.x] = 0u;
-  __syncthreads();
-  const int tile = sm.tile;
+  const int tile = (int)blockIdx.x;                 // in-order dispatch, see take_ticket
   const int64_t total = seg_in[n_seg];
   const int64_t ntiles = total > 0 ? (total + kRedTile - 1) / kRedTile : 1;
   if (tile >= ntiles) return;
+  __syncthreads();
   const int warp = threadIdx.x >> 5, lane = lane_id();
   const int64_t t0 = (int64_t)tile * kRedTile;
   const int cnt = (int)min((int64_t)kRedTile, total - t0);
+  {
+    const int64_t far = ((int64_t)tile + kPrefetchAhead) * kRedTile;
+    if (far < total) {
+      const int fc = (int)min((int64_t)kRedTile, total - far);
+      prefetch_l2(keys_in + far, fc);
+      prefetch_l2(vals_in + far, fc);
+    }
+  }
 
   for (int j = threadIdx.x; j < cnt; j += kRedThreads) {
     sm.key[1 + j] = ld_stream(keys_in + t0 + j);
@@ -557,9 +564,7 @@ k_small_merge(const u64* __restrict__ keys_in, const V* __restrict__ vals_in,
   __shared__ int s_g;
   __shared__ u64 s_scan[kSmallWarps + 1];
   __shared__ u64 s_base;
-  if (threadIdx.x == 0) s_g = (int)atomicAdd(ticket, 1u);
-  __syncthreads();
-  const int g = s_g;
+  const int g = (int)blockIdx.x;         // in-order dispatch, see take_ticket
   if (g >= n_seg) return;
   const int64_t start = seg_in[g];
   int len = (int)min((int64_t)0x7fffffff, seg_in[g + 1] - start);

@@ -154,13 +154,23 @@ __device__ __forceinline__ bool zi_only(u64 key) {
 // ---- tile tickets and segment-offset bookkeeping of the single-pass kernels ------------
 // Dynamic tile id: tiles are handed out in launch order so look-back never waits on
 // a tile that has not started.
-__device__ __forceinline__ int take_ticket(u32* ticket, int* smem_slot) {
-  if (threadIdx.x == 0) *smem_slot = (int)atomicAdd(ticket, 1u);
+// Tile id of a look-back kernel: blockIdx.x.  CTAs of a 1-D grid are dispatched in index order,
+// so every predecessor a tile may wait for is resident or finished (the assumption
+// cub::DeviceScan makes); an atomic ticket per CTA cost a ~700-cycle round trip at the head of
+// every tile.  The barrier is kept: callers publish shared state before it.
+__device__ __forceinline__ int take_ticket(u32*, int*) {
   __syncthreads();
-  const int t = *smem_slot;
-  __syncthreads();
-  return t;
+  return (int)blockIdx.x;
 }
+
+// L2 prefetch of `count` elements starting at p (whole 128-byte lines, all threads of the CTA)
+template <typename T>
+__device__ __forceinline__ void prefetch_l2(const T* p, int count) {
+  constexpr int kPerLine = 128 / (int)sizeof(T);
+  for (int i = (int)threadIdx.x * kPerLine; i < count; i += (int)blockDim.x * kPerLine)
+    asm volatile("prefetch.global.L2 [%0];" ::"l"(p + i));
+}
+constexpr int kPrefetchAhead = 592;     // tiles: about the CTAs resident on the device
 
 // After the last real term: every segment starting at `total_in` (trailing empties
 // and the end sentinel) starts at `total_out`.
