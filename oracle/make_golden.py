@@ -72,7 +72,8 @@ def mix64(keys):
 
 
 def digest(g):
-    keys = np.array([int(v) for v in g.indices], dtype=np.uint64)
+    idx = np.asarray(g.indices)
+    keys = idx.astype(np.uint64) if idx.dtype != object else np.array([int(v) for v in idx], dtype=np.uint64)
     lam = np.asarray(g.lambdas, dtype=np.float64)
     step = max(1, len(keys) // 64)
     return {
@@ -299,9 +300,21 @@ def make_configs(big):
     return store, digests
 
 
+def make_ladder_point(name, mode="v3"):
+    """One more ladder digest, merged into digests.json (used for the bench workload itself,
+    c4_xyz_16_2: 1.25e8 terms, ~3 minutes and ~20 GB for the reference)."""
+    n, mine = workloads.build(name)
+    t0 = time.perf_counter()
+    rep = reng.run(to_ref(mine), n, mode)
+    print(f"{name}/{mode}: reference took {time.perf_counter() - t0:.1f}s ranks={rep.rank_trace[-1]}", flush=True)
+    return {f"{name}/{mode}": {"n": n, "trace_last": rep.rank_trace[-1], "max_rank": rep.max_rank,
+                               "gens": [digest(g) for g in rep.final.generators]}}
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--big", action="store_true", help="also run the minutes-long reference cases")
+    ap.add_argument("--ladder", default="", help="only add the digest of this ladder point (e.g. c4_xyz_16_2)")
     ap.add_argument("--only", default="", help="comma list of: circuits,units,campaign,configs")
     args = ap.parse_args()
     only = set(filter(None, args.only.split(",")))
@@ -314,6 +327,13 @@ def main():
             json.dump({"_meta": meta, "data": obj}, fh, separators=(",", ":"))
         print("wrote", name, os.path.getsize(os.path.join(OUT, name)), "bytes", flush=True)
 
+    if args.ladder:
+        path = os.path.join(OUT, "digests.json")
+        with open(path) as fh:
+            old = json.load(fh)["data"]
+        old.update(make_ladder_point(args.ladder))
+        dump("digests.json", old)
+        return
     if not only or "circuits" in only:
         dump("circuits.json", make_circuits())
     if not only or "units" in only:

@@ -1,10 +1,12 @@
 """BASELINE.json's largest-rank config at full size: xyz_chain(16, 2) (1.25e8 final terms).
 
 The reference needs ~3 minutes and the oracle cannot finish in seconds, so parity here is through
-size-independent properties: every generator is U Z_j U^dagger so sum(lambda^2) = 1;
-the final ranks are the ones the reference reported (125 430 039 terms, max 55 284 529);
-keys are strictly ascending inside every generator; two runs are bitwise identical; and the same
-circuit at (14, 2) matches the reference digests term for term (test_gpu_engine.py)."""
+(a) size-independent properties: every generator is U Z_j U^dagger so sum(lambda^2)
+= 1; the final ranks are the ones the reference reported (125 430 039 terms, max
+55 284 529); keys are strictly ascending inside every generator; two runs are bitwise identical;
+and (b) digests of the reference's own run of this very circuit (tests/golden/digests.json,
+generated here by oracle/make_golden.py --ladder c4_xyz_16_2): key sets bit-exact per generator
+(sha256), sampled coefficients and moments within 1e-10."""
 
 import hashlib
 
@@ -18,7 +20,7 @@ from gpu_util import qx  # noqa: E402
 from paper_2505_03307_b200 import workloads  # noqa: E402
 
 
-def test_config4_16_2_properties():
+def test_config4_16_2_properties(golden):
     n, gates = workloads.build("c4_xyz_16_2")
     rep = qx.run(gates, n, "v3", download=False)
     store = rep.device["store"]
@@ -49,6 +51,13 @@ def test_config4_16_2_properties():
     keys3 = np.concatenate([g.keys() for g in rep3.final.generators])
     lam3 = np.concatenate([g.lambdas for g in rep3.final.generators])
     assert (hashlib.sha256(keys3.tobytes()).hexdigest(), hashlib.sha256(lam3.tobytes()).hexdigest()) == first
+    # ... and they are the REFERENCE's terms: digests of stabsim's own v3 run of this circuit
+    # (oracle/make_golden.py --ladder c4_xyz_16_2, 185 s on one core): per generator the sha256 of
+    # the sorted keys (bit-exact), 64 strided coefficients and three moments within 1e-10
+    d = golden.load_json("digests.json")["c4_xyz_16_2/v3"]
+    assert rep3.rank_trace[-1] == d["trace_last"] and rep3.max_rank == d["max_rank"]
+    for g, dg in zip(rep3.final.generators, d["gens"]):
+        golden.check_digest(dg, g.lambdas, g.keys(), tol=1e-10)
 
 
 def test_gpu_only_ladder_point_18_2():
