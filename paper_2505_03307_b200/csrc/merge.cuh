@@ -366,23 +366,24 @@ k_onesweep(const K* __restrict__ keys_in, const V* __restrict__ vals_in,
     u32 excl = 0;
     if (!solo) {
       constexpr int W = LB;
-      const int64_t first_tile = tile - ti.off / TILE;
-      int64_t t = tile - 1;
+      // predecessor j sits j * QX_RADIX words below sp: constant offsets, one compare per load
+      const u32* sp = status + (size_t)(tile - 1) * QX_RADIX + tid;
+      int avail = (int)(ti.off / TILE);           // predecessors inside this segment
       bool done = false;
       while (!done) {
         u32 w[W];
 #pragma unroll
-        for (int j = 0; j < W; ++j)
-          w[j] = (t - j >= first_tile) ? ld_volatile_u32(status + (size_t)(t - j) * QX_RADIX + tid) : kFlagInc;
+        for (int j = 0; j < W; ++j) w[j] = j < avail ? ld_volatile_u32(sp - j * QX_RADIX) : kFlagInc;
 #pragma unroll
         for (int j = 0; j < W; ++j) {
           if (!done) {
-            while ((w[j] >> 30) == 0u) w[j] = ld_volatile_u32(status + (size_t)(t - j) * QX_RADIX + tid);
+            while ((w[j] >> 30) == 0u) w[j] = ld_volatile_u32(sp - j * QX_RADIX);
             excl += w[j] & kFlagVal;
             done = (w[j] >> 30) == 2u;
           }
         }
-        t -= W;
+        sp -= W * QX_RADIX;
+        avail -= W;
       }
       st_volatile_u32(mine, kFlagInc | (excl + live_total));
     }
