@@ -58,8 +58,13 @@ CPU_SAMPLE = {"c4_xyz_16_2": list(range(2, 16)), "c4_xyz_18_2": list(range(4, 18
 def peaks():
     path = os.path.join(ROOT, "MEASURED_PEAKS.json")
     if os.path.exists(path):
-        with open(path) as fh:
-            return float(json.load(fh)["hbm_gbs"]), "measured (MEASURED_PEAKS.json)"
+        try:
+            with open(path) as fh:
+                v = float(json.load(fh)["hbm_gbs"])
+            if v > 0:
+                return v, "measured (MEASURED_PEAKS.json)"
+        except (OSError, ValueError, KeyError, TypeError):
+            pass
     return 6650.0, "fallback (B200_PROFILING.md)"
 
 

@@ -143,19 +143,34 @@ def create_chain(k: int, k_prime: int, first_is_single: bool) -> list:
 def divide_instruction(instructions: Sequence[Instruction], n: int) -> OperatorPartition:
     """Split a gate list into maximal runs of equal arity (reference circuit.py:158-182)."""
     part = OperatorPartition(n=n)
+    order, u_groups, v_groups = part.order, part.u_groups, part.v_groups
     last = None
+    cur = None                                   # the open group: list (V_k) or dict (U_k)
     for inst in instructions:
-        if max(inst.wires) >= n:
-            raise ValueError(f"wire out of range for n={n}: {inst}")
-        kind = 1 if inst.is_two_qubit else 0
-        if kind != last:
-            part.order.append(kind)
-            (part.v_groups if kind else part.u_groups).append([] if kind else {})
-            last = kind
-        if kind:
-            part.v_groups[-1].append(inst)
+        wires = inst.wires
+        if len(wires) == 2:
+            if wires[0] >= n or wires[1] >= n:
+                raise ValueError(f"wire out of range for n={n}: {inst}")
+            if last != 1:
+                order.append(1)
+                cur = []
+                v_groups.append(cur)
+                last = 1
+            cur.append(inst)
         else:
-            part.u_groups[-1].setdefault(inst.wires[0], []).append(inst)
+            q = wires[0]
+            if q >= n:
+                raise ValueError(f"wire out of range for n={n}: {inst}")
+            if last != 0:
+                order.append(0)
+                cur = {}
+                u_groups.append(cur)
+                last = 0
+            cell = cur.get(q)
+            if cell is None:
+                cur[q] = [inst]
+            else:
+                cell.append(inst)
     return part
 
 

@@ -112,6 +112,7 @@ class _Walker:
         self.staged = None             # (counts, axes, weights) of a U_k not launched yet (v2/v3)
         self.open_slots: list = []     # trace rows waiting for the deferred merge
         self.pending_gates = 0         # v1 gates applied since the deferred branch
+        self.clean_gates = 0           # v1 gates that saw the current (merged) ranks, not yet booked
         self.ranks = [1] * len(self.ids)
         self.launch_log = {"clifford_runs": 0, "branch_ops": 0, "merges": 0, "sorts": 0}
         self.updates = None            # v1 only: term-gate updates per generator
@@ -136,7 +137,16 @@ class _Walker:
         self.launch_log["clifford_runs"] += 1
 
     # -- merges ----------------------------------------------------------------------
+    def book_gates(self):
+        """v1 update counts: gates counted since the ranks last changed see exactly these ranks.
+        Called before every assignment to ``self.ranks`` (one array operation per merge instead of
+        one per gate)."""
+        if self.updates is not None and self.clean_gates:
+            self.updates += np.asarray(self.ranks, dtype=np.int64) * self.clean_gates
+        self.clean_gates = 0
+
     def _merge_now(self, step: int, phase: str, after_branch: bool):
+        self.book_gates()
         t0 = time.perf_counter()
         if after_branch and self.before_merge is not None:
             self.before_merge(self.store)      # term-partitioned runs: equal keys must meet first
@@ -158,6 +168,7 @@ class _Walker:
         self.staged = (counts, axes, weights)
 
     def _run_staged(self, step: int, phase: str):
+        self.book_gates()
         counts, axes, weights = self.staged
         self.staged = None
         program = np.array(self.queue, dtype=np.uint32)
@@ -228,12 +239,13 @@ class _Walker:
     def count_gate(self):
         """v1: one more gate sees the current terms."""
         if self.pending is None:
-            self.updates += np.asarray(self.ranks, dtype=np.int64)
+            self.clean_gates += 1
         else:
             self.pending_gates += 1
 
     def finish(self, trace):
         self.resolve(trace)
+        self.book_gates()
         self.flush()
         if self.unsorted:
             # only permutations since the last merge: canonicalize can only re-sort
@@ -306,8 +318,7 @@ def run(instructions: Sequence[Instruction], n: int, mode, eps: float = DEFAULT_
             _walk_v1(instructions, partition, w, trace, counters, eager)
         else:
             t0 = time.perf_counter()
-            lut = _lut.create_lut_1q(partition)
-            is_perm, tables = _lut.classify_lut(lut) if partition.k else (None, None)
+            lut, is_perm, tables = _lut.build_lut(partition)
             timings["lut"] = time.perf_counter() - t0
             _walk_operators(partition, lut, is_perm, tables, w, trace, counters, mode, eager)
 
@@ -325,6 +336,7 @@ def run(instructions: Sequence[Instruction], n: int, mode, eps: float = DEFAULT_
         if partitioned is not None:
             info["partitioned"] = partitioned
         if w.updates is not None:
+            w.book_gates()
             info["updates_per_generator"] = w.updates.tolist()
         final = None
         if download:
@@ -377,6 +389,7 @@ def _finish_streamed(w: _Walker, trace, pinned: bool):
     ranges = sorted(zip(bounds[:-1], bounds[1:]), key=lambda ab: sum(raw[ab[0]:ab[1]]))
     program = np.array(w.queue, dtype=np.uint32)
     w.queue, w.queue_has_cx, w.staged, w.pending = [], False, None, None
+    w.book_gates()
     t0 = time.perf_counter()
     parts, children = {}, []
     ranks = [0] * len(w.ids)
@@ -437,6 +450,7 @@ def _finish_partitioned(w: _Walker, trace, slot_part, slot_reduce):
     step, phase = w.pending
     program = np.array(w.queue, dtype=np.uint32)
     w.queue, w.queue_has_cx, w.staged, w.pending = [], False, None, None
+    w.book_gates()
     t0 = time.perf_counter()
     ranks, partitioned = w.store.apply_operator_run_part(counts, axes, weights, program, w.eps, part, parts)
     if partitioned and slot_reduce is not None:
@@ -474,23 +488,31 @@ def _walk_v1(instructions, partition, w: _Walker, trace, counters, eager):
     """Gate by gate (reference engine.py:155-180): rank snapshots at operator boundaries."""
     boundaries = set(np.cumsum(partition.operator_sizes()).tolist())
     w.updates = np.zeros(len(w.ids), dtype=np.int64)
+    n = w.n
+    fixed = _lut.FIXED_PERMS
+    n_cx = n_1q = 0
     for pos, inst in enumerate(instructions, start=1):
-        if inst.is_two_qubit:
+        wires = inst.wires
+        if len(wires) == 2:
             w.count_gate()
-            w.push_cx(*inst.wires)
-            counters["cx_applications"] += 1
-            w.step_done(pos - 1, "cx", trace)
+            w.queue.append(_lut.cx_op(n, wires[0], wires[1]))
+            w.queue_has_cx = True
+            n_cx += 1
+            if eager:
+                w.step_done(pos - 1, "cx", trace)
         else:
-            q = inst.wires[0]
-            table = _lut.FIXED_PERMS.get(inst.gate)
+            q = wires[0]
+            table = fixed.get(inst.gate)
             block = None
             if table is None:
                 block = _lut.gate_branch_block(inst.gate, inst.theta)
                 table = _lut.perm_word(block)
             if table is not None:
                 w.count_gate()
-                w.push_perm(q, table)
-                w.step_done(pos - 1, "sub_flatten", trace)
+                if table != _lut.IDENTITY_PERM:
+                    w.queue.append(_lut.perm_op(n, q, table))
+                if eager:
+                    w.step_done(pos - 1, "sub_flatten", trace)
             else:
                 w.resolve(trace)               # this gate must see merged terms
                 w.count_gate()
@@ -499,20 +521,32 @@ def _walk_v1(instructions, partition, w: _Walker, trace, counters, eager):
                 w.store.apply_split(q, *split_tables(block))
                 w.timings["sub_flatten"] += time.perf_counter() - t0
                 w.branched(pos - 1, "sub_flatten", trace)
-            counters["v1_gate_applications"] = counters.get("v1_gate_applications", 0) + 1
+            n_1q += 1
         if pos in boundaries:
             w.snapshot(trace)
+    counters["cx_applications"] += n_cx
+    if n_1q:
+        counters["v1_gate_applications"] = counters.get("v1_gate_applications", 0) + n_1q
 
 
 def _walk_operators(partition, lut, is_perm, tables, w: _Walker, trace, counters, mode, eager):
     """Operator chain (reference engine.py:110-132): U_k = substitute + flatten, V_k = CX run."""
     n = w.n
     ui = vi = 0
+    if partition.k:
+        # op words of every permutation cell of the circuit in one go (lut.perm_op, vectorised):
+        # the walk below only slices a Python list per operator
+        all_perm = is_perm.all(axis=1).tolist()
+        shifts = (2 * (n - 1 - np.arange(n, dtype=np.uint64)))[None, :]
+        wide = tables.astype(np.uint64) << np.uint64(16)
+        ops_all = (wide | (shifts << np.uint64(32))) if n > 32 else (wide | (shifts << np.uint64(2)))
+        live = tables != _lut.IDENTITY_PERM
+        perm_ops = ops_all[live].tolist()
+        perm_off = np.concatenate(([0], np.cumsum(live.sum(axis=1)))).tolist()
     for step, bit in enumerate(partition.order):
         if bit == 0:
-            if bool(is_perm[ui].all()):
-                for j in np.flatnonzero(tables[ui] != _lut.IDENTITY_PERM):
-                    w.push_perm(int(j), int(tables[ui][j]))
+            if all_perm[ui]:
+                w.queue.extend(perm_ops[perm_off[ui]:perm_off[ui + 1]])
                 w.step_done(step, "sub_flatten", trace)
             else:
                 if n > 32:

@@ -98,23 +98,40 @@ def create_lut_1q(partition, workers=None) -> np.ndarray:
     does with ``@`` (bit-identical, tests/test_native_abi.py), without the
     per-call overhead.  The first factor is taken as is: M @ I == M.
     """
+    return build_lut(partition)[0]
+
+
+def build_lut(partition) -> tuple:
+    """``create_lut_1q`` plus the classification the engine needs, in one walk over the cells:
+    (lut[K, n, 3, 3], is_perm bool[K, n], table uint32[K, n]) with ``table`` as in
+    ``classify_lut``.  Cells made of fixed gates only -- nearly all cells of a Clifford+T circuit
+    -- recur with few distinct gate sequences: block and permutation word of a sequence are
+    composed once (same numpy chain as ``compose_block``) and looked up afterwards."""
     lut = np.empty((partition.k, partition.n, 3, 3))
     lut[:] = np.eye(3)
+    is_perm = np.ones((partition.k, partition.n), dtype=bool)
+    table = np.full((partition.k, partition.n), IDENTITY_PERM, dtype=np.uint32)
     by_len: dict = {}
+    fixed_k, fixed_w, fixed_b, fixed_t = [], [], [], []
     for ki, bucket in enumerate(partition.u_groups):
         for wire, gates in bucket.items():
-            # cells made of fixed gates only (most cells of a Clifford+T circuit) recur with few
-            # distinct gate sequences: compose each sequence once, with the same numpy chain
-            names = tuple(g.gate for g in gates)
-            block = _FIXED_BLOCKS.get(names)
-            if block is None and all(name in _FIXED for name in names):
+            names = tuple([g.gate for g in gates])
+            hit = _FIXED_BLOCKS.get(names)
+            if hit is None and all(name in _FIXED for name in names):
                 block = compose_block(gates)
+                hit = (block, perm_word(block))      # products of signed permutations: always a word
                 if len(_FIXED_BLOCKS) < 65536:
-                    _FIXED_BLOCKS[names] = block
-            if block is not None:
-                lut[ki, wire] = block
+                    _FIXED_BLOCKS[names] = hit
+            if hit is not None:
+                fixed_k.append(ki)
+                fixed_w.append(wire)
+                fixed_b.append(hit[0])
+                fixed_t.append(hit[1])
             else:
                 by_len.setdefault(len(gates), []).append((ki, wire, gates))
+    if fixed_k:
+        lut[fixed_k, fixed_w] = np.array(fixed_b)     # one scatter instead of one assignment per cell
+        table[fixed_k, fixed_w] = np.array(fixed_t, dtype=np.uint32)
     for length, cells in by_len.items():
         mats = np.zeros((length, len(cells), 3, 3))
         for ci, (_, _, gates) in enumerate(cells):
@@ -125,8 +142,12 @@ def create_lut_1q(partition, workers=None) -> np.ndarray:
             acc = np.matmul(mats[gi], acc)
         ks = [c[0] for c in cells]
         ws = [c[1] for c in cells]
-        lut[ks, ws] = acc.transpose(0, 2, 1)
-    return lut
+        blocks = acc.transpose(0, 2, 1)
+        lut[ks, ws] = blocks
+        p, t = classify_lut(np.ascontiguousarray(blocks)[None])
+        is_perm[ks, ws] = p[0]
+        table[ks, ws] = t[0]
+    return lut, is_perm, table
 
 
 _FIXED_ARRAYS = {name: np.array(rows) for name, rows in _FIXED.items()}
