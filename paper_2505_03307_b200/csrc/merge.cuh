@@ -136,6 +136,13 @@ k_sort_hist(const K* __restrict__ keys, const int64_t* __restrict__ base_in, con
     }
     const int64_t start = base_in[g] + ti.off;
     const int count = ti.count;
+    {   // this CTA's next tile: have it in L2 by then
+      const int64_t nt = tile + gridDim.x;
+      if (nt < total_tiles) {
+        const TileInfo tn = info[nt];
+        prefetch_l2(keys + base_in[tn.seg & 0x7fffffff] + tn.off, tn.count);
+      }
+    }
     const int rounds = (count + kSortThreads - 1) / kSortThreads;
 #pragma unroll 4
     for (int k = 0; k < rounds; ++k) {
@@ -441,7 +448,7 @@ struct ReduceSmem {
 // streaming loads, so every term is read from HBM exactly once and no thread searches the
 // offset table; only runs that cross the tile end touch global memory again.
 template <typename K, typename V, int kRedThreads, int kRedItems>
-__global__ void __launch_bounds__(kRedThreads)
+__global__ void __launch_bounds__(kRedThreads, (sizeof(V) == 8 && kRedThreads == 256) ? 6 : 1)
 k_reduce(const K* __restrict__ keys_in, const V* __restrict__ vals_in,
          const int64_t* __restrict__ seg_in, int n_seg, u64* __restrict__ keys_out,
          V* __restrict__ vals_out, int64_t* __restrict__ seg_out, u64* status, u32* ticket,
@@ -487,8 +494,10 @@ k_reduce(const K* __restrict__ keys_in, const V* __restrict__ vals_in,
   }
   __syncthreads();
 
-  K key[kRedItems];
-  V sum[kRedItems];
+  // A kept head leaves its sum in sm.val[j] (no other thread's run contains a head) and its key
+  // stays in sm.key: the write-out re-reads both, so only `pre` and the flags live across the
+  // look-back -- 40 registers instead of 62, six CTAs per SM instead of four (the kernel waits on
+  // barriers and the look-back, occupancy is what hides that).
   u32 pre[kRedItems];          // kept heads before this item inside the warp
   u32 flags = 0;               // bit k: item k is a kept head; bit 16+k: item k opens a segment
   u32 running = 0;
@@ -497,22 +506,22 @@ k_reduce(const K* __restrict__ keys_in, const V* __restrict__ vals_in,
     const int j = warp * (32 * kRedItems) + k * 32 + lane;
     bool kept = false;
     if (j < cnt) {
-      key[k] = sm.key[1 + j];
+      const K key = sm.key[1 + j];
       const bool opens = (sm.opens[j >> 5] >> (j & 31)) & 1u;
       if (opens) flags |= 1u << (16 + k);
-      if (opens || sm.key[j] != key[k]) {
+      if (opens || sm.key[j] != key) {
         V s = sm.val[j];
         int e = j + 1;
-        while (e < cnt && sm.key[1 + e] == key[k] && !((sm.opens[e >> 5] >> (e & 31)) & 1u)) {
+        while (e < cnt && sm.key[1 + e] == key && !((sm.opens[e >> 5] >> (e & 31)) & 1u)) {
           acc(s, sm.val[e]);
           ++e;
         }
         if (e == cnt && t0 + cnt < total) {          // the run may continue past the tile
           const int g = segment_of(seg_in, n_seg, t0 + j);
           const int64_t end = seg_in[g + 1];
-          for (int64_t i = t0 + cnt; i < end && keys_in[i] == key[k]; ++i) acc(s, vals_in[i]);
+          for (int64_t i = t0 + cnt; i < end && keys_in[i] == key; ++i) acc(s, vals_in[i]);
         }
-        sum[k] = s;
+        sm.val[j] = s;
         kept = keep(s, eps);
       }
     }
@@ -535,8 +544,9 @@ k_reduce(const K* __restrict__ keys_in, const V* __restrict__ vals_in,
   for (int k = 0; k < kRedItems; ++k) {
     const int64_t pos = base + pre[k];
     if (flags & (1u << k)) {
-      st_stream(keys_out + pos, (u64)key[k]);
-      st_stream(vals_out + pos, sum[k]);
+      const int j = warp * (32 * kRedItems) + k * 32 + lane;
+      st_stream(keys_out + pos, (u64)sm.key[1 + j]);
+      st_stream(vals_out + pos, sm.val[j]);
     }
     if (flags & (1u << (16 + k))) {
       const int64_t i = t0 + warp * (32 * kRedItems) + k * 32 + lane;
