@@ -5,7 +5,7 @@
 
 The numpy oracle port keeps uint64 keys (n <= 32), so parity of the multi-word device path
 (csrc/wide.cu) is pinned directly on what the reference computes: Clifford circuits (rank 1 per
-generator at any width), near-Clifford circuits in v1 (a few T gates), Clifford circuits through the
+generator at any width), near-Clifford circuits in v1 and v3 (a few T gates), Clifford circuits through the
 operator pipeline (v3, every U_k a signed permutation), and the apply_cx big-int unit case of the
 reference's own tests (tests/test_stabilizer.py:262-267).
 """
@@ -69,6 +69,9 @@ def main():
         cases.append(case(f"clifford_{n}_v3", n, gates, "v3"))
     for n, m, t, seed in ((34, 300, 6, 21), (40, 500, 8, 22), (64, 400, 7, 23)):
         cases.append(case(f"near_clifford_{n}_t{t}", n, near_clifford(n, m, t, seed), "v1"))
+    # the same kind of circuit through the operator pipeline: branching U_k on big-int indices
+    for n, m, t, seed in ((34, 300, 6, 21), (40, 500, 8, 22), (70, 300, 9, 24)):
+        cases.append(case(f"near_clifford_{n}_t{t}_v3", n, near_clifford(n, m, t, seed), "v3"))
     # unit: CX on a 40-qubit word (reference tests/test_stabilizer.py:262-267 style)
     n = 40
     g = rstab.SimpleGenerator(n, np.array([1.0, -0.5]), [4 ** 39 + 3, 2 * 4 ** 39 + 4 ** 20])

@@ -548,12 +548,38 @@ def _walk_operators(partition, lut, is_perm, tables, w: _Walker, trace, counters
             if all_perm[ui]:
                 w.queue.extend(perm_ops[perm_off[ui]:perm_off[ui + 1]])
                 w.step_done(step, "sub_flatten", trace)
-            else:
-                if n > 32:
+            elif n > 32:
+                # Multi-word keys: the operator is applied gate by gate, wire by wire, with the
+                # v1 kernels and merged ONCE, where the reference merges its flattened expansion
+                # (stabilizer.py:240-256).  The raw terms are the same Cartesian product (a path
+                # per non-zero product of gate entries instead of a branch per non-zero block
+                # entry: paths to the same word are summed by the merge, to rounding what the
+                # reference's 3x3 products sum), so term sets after the drop rule agree.
+                w.resolve(trace)               # expand merged terms only
+                bucket = partition.u_groups[ui]
+                t0 = time.perf_counter()
+                for wire in sorted(bucket):
+                    for inst in bucket[wire]:
+                        table = _lut.FIXED_PERMS.get(inst.gate)
+                        block = None
+                        if table is None:
+                            block = _lut.gate_branch_block(inst.gate, inst.theta)
+                            table = _lut.perm_word(block)
+                        if table is not None:
+                            w.push_perm(wire, table)
+                        else:
+                            w.flush()
+                            w.store.apply_split(wire, *split_tables(block))
+                if mode is Mode.V2 and any(r > have for r, have in zip(w.store.ranks(), w.ranks)):
+                    # dense layout: a row that is not one-hot needs the 4**n scatter buffer
+                    # (reference stabilizer.py:264-276)
                     raise ResourceLimitError(
-                        f"n = {n}: branching operators (v2/v3) need one-word keys (n <= 32); above that the "
-                        "device runs Clifford operators in every mode and rotations in v1"
+                        f"dense flatten needs a 4**{n}-element buffer (> {DENSE_FLATTEN_BUDGET}); "
+                        "use the ragged layout for circuits of this size"
                     )
+                w.timings["sub_flatten"] += time.perf_counter() - t0
+                w.branched(step, "sub_flatten", trace)
+            else:
                 w.resolve(trace)               # expand merged terms only
                 w.flush()
                 counts, axes, weights = _lut.operator_tables(lut[ui])

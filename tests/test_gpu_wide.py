@@ -1,8 +1,8 @@
 """More than 32 qubits on the GPU (multi-word keys, csrc/wide.cu) against fixtures computed by the
 UNMODIFIED reference with Python big-int indices (tests/golden/wide.json, oracle/make_golden_wide.py):
-Clifford circuits up to 130 qubits in v1 and v3, near-Clifford circuits in v1, the apply_cx unit
-case; plus the multi-word merge/split against a big-int model on random terms, and the error a
-branching operator raises above 32 qubits."""
+Clifford circuits up to 130 qubits in v1 and v3, near-Clifford circuits in v1 and v3, the apply_cx unit
+case; plus the multi-word merge/split against a big-int model on random terms, and the limits
+above 32 qubits."""
 
 import math
 
@@ -25,7 +25,7 @@ def _cases(golden):
 
 def test_reference_circuits_above_32_qubits(golden):
     data = _cases(golden)
-    assert len(data["cases"]) >= 15
+    assert len(data["cases"]) >= 18
     for case in data["cases"]:
         n = case["n"]
         gates = [qx.Instruction(g, tuple(w), float.fromhex(t)) for g, w, t in case["gates"]]
@@ -87,10 +87,11 @@ def test_split_and_merge_against_big_int_model(n, terms):
 def test_limits_above_32_qubits():
     n = 36
     gates = [qx.Instruction("H", (0,)), qx.Instruction("RY", (0,), 0.3), qx.Instruction("CX", (0, 35))]
-    with pytest.raises(qx.ResourceLimitError, match="branching operators"):
-        qx.run(gates, n, "v3")
-    rep = qx.run(gates, n, "v1")                                  # the same circuit gate by gate is fine
-    assert rep.rank_trace[-1][0] == 2 and rep.final.generators[35].rank == 1
+    with pytest.raises(qx.ResourceLimitError, match="dense flatten"):
+        qx.run(gates, n, "v2")                                    # reference stabilizer.py:264-276
+    for mode in ("v1", "v3"):
+        rep = qx.run(gates, n, mode)
+        assert rep.rank_trace[-1][0] == 2 and rep.final.generators[35].rank == 1
     with pytest.raises(qx.NativeError, match="at most"):
         qx.run([qx.Instruction("H", (0,))], 600, "v1")
     ghz = qx.run(qx.gen_ghz(400), 400, "v1")                      # "hundreds of qubits for Clifford"
