@@ -40,6 +40,24 @@ int qx_run_merge(qx_store* s, double eps, bool sort_only, bool narrow) {
   return QX_OK;
 }
 
+int qx_sort_pairs(qx_store* s, u64* keys[2], double* vals[2], int64_t* seg[2], int* cur, int64_t total,
+                  int64_t largest_seg, int bits) {
+  qxm::MergeBuffers<double> mb;
+  for (int b = 0; b < 2; ++b) {
+    mb.keys[b] = keys[b];
+    mb.vals[b] = vals[b];
+    mb.seg[b] = seg[b];
+  }
+  mb.cur = *cur;
+  mb.n_seg = s->n_seg;
+  mb.ub_total = total;
+  mb.ub_seg = largest_seg;
+  QX_TRY((qxm::merge_large<double, u64>(s, mb, 0.0, QX_K_REDUCE, false, QX_K_SORT_PASS, QX_K_SORT_HIST, nullptr,
+                                        nullptr, true, nullptr, bits)));
+  *cur = mb.cur;
+  return QX_OK;
+}
+
 namespace {
 
 // ---- per-segment deterministic reductions -------------------------------------------

@@ -834,9 +834,11 @@ template <typename V, typename K = u64>
 int merge_large(QxArena* ar, MergeBuffers<V>& mb, double eps, int cls_reduce, bool do_reduce = true,
                 int cls_pass = QX_K_SORT_PASS, int cls_hist = QX_K_SORT_HIST,
                 const int64_t* first_base_in = nullptr, const u32* pre_hist = nullptr, bool widen_last = true,
-                u32* pack_bnd = nullptr) {
+                u32* pack_bnd = nullptr, int key_bits = 0) {
   const int n_seg = mb.n_seg;
-  const int passes = std::min(kMaxPasses, (2 * ar->n_qubits + QX_RADIX_BITS - 1) / QX_RADIX_BITS);
+  // key_bits: bits of the key that can be set (default: the 2n of a one-word Pauli word)
+  if (key_bits <= 0) key_bits = 2 * ar->n_qubits;
+  const int passes = std::min(kMaxPasses, (key_bits + QX_RADIX_BITS - 1) / QX_RADIX_BITS);
   if (mb.ub_seg >= (int64_t)kFlagVal)
     return qx_fail(QX_ERR_RESOURCE, "a generator with %lld raw terms exceeds the sort's 2^30 limit",
                    (long long)mb.ub_seg);

@@ -139,8 +139,12 @@ int qx_check_program(const qx_store* s, const uint32_t* program, int32_t n_ops);
 void qx_standard_cx(u32* cx_c, u32* cx_t, u32* cx_s);
 // merge.cu: canonicalize (or only sort) the live buffer; narrow = it holds 32-bit raw keys
 int qx_run_merge(qx_store* s, double eps, bool sort_only, bool narrow);
-// wide.cu: the merge of a multi-word store (one CTA per generator)
+// wide.cu: the merge of a multi-word store
 int qx_wide_merge(qx_store* s, double eps);
+// merge.cu: stable segmented sort of (64-bit key, opaque 8-byte payload) pairs by the low `bits`
+// bits of the key with the onesweep passes; buffers ping-pong, *cur names the live pair
+int qx_sort_pairs(qx_store* s, u64* keys[2], double* vals[2], int64_t* seg[2], int* cur, int64_t total,
+                  int64_t largest_seg, int bits);
 // entry points that only exist for one-word keys refuse wide stores with this
 #define QX_NARROW_ONLY(s, what)                                                                      \
   do {                                                                                               \

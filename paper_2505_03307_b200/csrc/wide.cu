@@ -12,11 +12,13 @@
 //   qx_apply_split_wide     v1 rotation (engine.py:190-217): two entries per term, the second
 //                           one (second branch weight 0) a zero-weight copy of the first, which
 //                           the merge adds into the same key without changing the sum;
-//   merge / sort            one CTA per generator: bitonic sort on (words, input position) in
-//                           shared memory, in-order run sums, drop rule, compaction across
-//                           generators by look-back -- generators up to 16384 / W raw terms.
-// Branching operators of v2/v3, the large merge, read-out and partitioning stay one-word
-// (QX_ERR_UNSUPPORTED on a wide store): states of that size do not occur at these widths.
+//   merge / sort            generators up to 16384 / W raw terms: one CTA per generator, bitonic
+//                           sort on (words, input position) in shared memory, in-order run sums,
+//                           drop rule, compaction across generators by look-back.  Larger ones:
+//                           a permutation sorted word by word with the one-word onesweep passes
+//                           (stable LSD over the W words), then one reduce + compaction pass.
+// Branching operators of v2/v3 are applied gate by gate with these kernels (engine.py); the
+// grouped operator step, read-out and partitioning stay one-word (QX_ERR_UNSUPPORTED).
 #include <stdlib.h>
 #include <string.h>
 
@@ -221,16 +223,157 @@ int merge_cap(int n_words) {
   return cap;                                    // W = 2: 8192, 3-4: 4096, 5-8: 2048 raw terms per generator
 }
 
+
+// ---- merge of generators beyond one CTA's shared memory ----------------------------------------
+// LSD over the W words: a permutation (input positions, carried as the 8-byte payload of the
+// one-word onesweep passes of merge.cuh) is sorted stably by word 0, then word 1, ... word W-1,
+// each time on the plane gathered through the permutation so far.  Stable passes leave equal
+// words in input order, so the runs below are summed in the order np.add.at uses
+// (stabilizer.py:333-335).  The terms themselves move once, in k_wide_reduce.
+__global__ void k_wide_iota(double* __restrict__ perm, int64_t total) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x)
+    perm[i] = __longlong_as_double((long long)i);
+}
+
+__global__ void k_wide_gather(const u64* __restrict__ plane, const double* __restrict__ perm, u64* __restrict__ out,
+                              int64_t total) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = plane[__double_as_longlong(perm[i])];
+}
+
+constexpr int kWrThreads = 256;
+constexpr int kWrRows = 4;
+constexpr int kWrTile = kWrThreads * kWrRows;
+
+__device__ __forceinline__ bool wide_same(const Planes& pl, int n_words, int64_t a, int64_t b) {
+  for (int w = 0; w < n_words; ++w)
+    if (pl.p[w][a] != pl.p[w][b]) return false;
+  return true;
+}
+
+// One thread per sorted position: heads (first of a run of equal words inside the generator) sum
+// their run in order, apply the drop rule (stabilizer.py:336) and are compacted by a block scan +
+// decoupled look-back over tiles (tile = blockIdx.x, see qx_device.cuh).
+__global__ void __launch_bounds__(kWrThreads)
+k_wide_reduce(Planes in, const double* __restrict__ lam_in, const double* __restrict__ perm,
+              const int64_t* __restrict__ seg_in, int n_seg, int n_words, Planes out, double* __restrict__ lam_out,
+              int64_t* __restrict__ seg_out, u64* status, double eps) {
+  __shared__ u64 s_scan[kWrThreads / 32 + 1];
+  __shared__ u64 s_base;
+  const int tile = blockIdx.x;
+  const int64_t total = seg_in[n_seg];
+  const int64_t tbase = (int64_t)tile * kWrTile;
+  bool kept[kWrRows], opens[kWrRows];
+  double sum[kWrRows];
+  int seg_id[kWrRows];
+  u64 mine = 0;
+#pragma unroll
+  for (int r = 0; r < kWrRows; ++r) {
+    const int64_t i = tbase + r * kWrThreads + threadIdx.x;
+    kept[r] = opens[r] = false;
+    sum[r] = 0.0;
+    seg_id[r] = 0;
+    if (i < total) {
+      const int g = segment_of(seg_in, n_seg, i);
+      const int64_t lo = seg_in[g], hi = seg_in[g + 1];
+      const int64_t pi = __double_as_longlong(perm[i]);
+      seg_id[r] = g;
+      opens[r] = i == lo;
+      if (i == lo || !wide_same(in, n_words, pi, __double_as_longlong(perm[i - 1]))) {
+        double acc = lam_in[pi];
+        for (int64_t j = i + 1; j < hi; ++j) {
+          const int64_t pj = __double_as_longlong(perm[j]);
+          if (!wide_same(in, n_words, pi, pj)) break;
+          acc += lam_in[pj];
+        }
+        sum[r] = acc;
+        kept[r] = fabs(acc) >= eps;
+      }
+    }
+    mine += kept[r] ? 1ull : 0ull;
+  }
+  u64 tile_total;
+  block_exclusive_sum<u64>(mine, s_scan, tile_total);
+  if ((threadIdx.x >> 5) == 0) {
+    const u64 excl = lookback_exclusive(status, tile, tile_total);
+    if (lane_id() == 0) s_base = excl;
+  }
+  __syncthreads();
+  const int64_t base = (int64_t)s_base;
+  u64 before = 0;
+#pragma unroll
+  for (int r = 0; r < kWrRows; ++r) {
+    const int64_t i = tbase + r * kWrThreads + threadIdx.x;
+    u64 row_total;
+    const u64 excl = block_exclusive_sum<u64>(kept[r] ? 1ull : 0ull, s_scan, row_total);
+    const int64_t pos = base + (int64_t)(before + excl);
+    if (opens[r]) open_offsets(seg_in, seg_out, seg_id[r], i, pos);
+    if (kept[r]) {
+      const int64_t pi = __double_as_longlong(perm[i]);
+      for (int w = 0; w < n_words; ++w) out.p[w][pos] = in.p[w][pi];
+      lam_out[pos] = sum[r];
+    }
+    before += row_total;
+  }
+  if (threadIdx.x == 0 && tbase + kWrTile >= total) close_offsets(seg_in, seg_out, n_seg, total, base + (int64_t)tile_total);
+}
+
+struct DevBlock {
+  void* p = nullptr;
+  cudaStream_t st = 0;
+  ~DevBlock() {
+    if (p) qx_dev_free(p, st);
+  }
+};
+
+int wide_merge_large(qx_store* s, double eps) {
+  if (!s->exact) QX_TRY(qx_store_refresh(s));
+  const int64_t total = s->h_seg[s->n_seg];
+  int64_t largest = 0;
+  for (int g = 0; g < s->n_seg; ++g) largest = std::max(largest, s->h_seg[g + 1] - s->h_seg[g]);
+  const int in = s->cur, out = s->cur ^ 1;
+  const int64_t tiles = std::max<int64_t>(1, (total + kWrTile - 1) / kWrTile);
+  // one block: two key buffers, two permutation buffers, the spare offsets, the look-back words
+  const int64_t n_al = (total + 31) & ~31ll;
+  const int64_t seg_words = ((int64_t)s->n_seg + 1 + 31) & ~31ll;
+  DevBlock blk;
+  blk.st = s->stream;
+  QX_TRY(qx_dev_alloc(&blk.p, 8 * (4 * n_al + seg_words + tiles), s->stream, s->device));
+  u64* kbuf[2] = {reinterpret_cast<u64*>(blk.p), reinterpret_cast<u64*>(blk.p) + n_al};
+  double* pbuf[2] = {reinterpret_cast<double*>(kbuf[1] + n_al), reinterpret_cast<double*>(kbuf[1] + 2 * n_al)};
+  int64_t* seg_spare = reinterpret_cast<int64_t*>(kbuf[1] + 3 * n_al);
+  u64* status = reinterpret_cast<u64*>(seg_spare + seg_words);
+  int64_t* segs[2] = {s->seg[in], seg_spare};
+  const Planes pin = planes_of(s, in);
+  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((total + 255) / 256, (int64_t)s->sm_count * 8));
+  int cur = 0;
+  k_wide_iota<<<grid, 256, 0, s->stream>>>(pbuf[cur], total);
+  QX_CUDA(cudaGetLastError());
+  for (int w = 0; w < s->n_words; ++w) {
+    k_wide_gather<<<grid, 256, 0, s->stream>>>(pin.p[w], pbuf[cur], kbuf[cur], total);
+    QX_CUDA(cudaGetLastError());
+    // bits of this word that can be set: the top word of the key holds 2n - 64 (W - 1) of them
+    const int bits = std::min(64, 2 * s->n_qubits - 64 * w);
+    QX_TRY(qx_sort_pairs(s, kbuf, pbuf, segs, &cur, total, largest, bits));
+  }
+  QX_CUDA(cudaMemsetAsync(status, 0, sizeof(u64) * (size_t)tiles, s->stream));
+  {
+    QxProfileScope prof(QX_K_REDUCE, s->stream, (8.0 * s->n_words + 8.0) * 2.0 * (double)total);
+    k_wide_reduce<<<(unsigned)tiles, kWrThreads, 0, s->stream>>>(pin, s->lam[in], pbuf[cur], segs[cur], s->n_seg,
+                                                                s->n_words, planes_of(s, out), s->lam[out],
+                                                                s->seg[out], status, eps);
+    QX_CUDA(cudaGetLastError());
+  }
+  s->cur = out;
+  s->exact = false;
+  return qx_store_refresh(s);      // synchronises: the scratch block may go back to the allocator
+}
+
 }  // namespace
 
 int qx_wide_merge(qx_store* s, double eps) {
   if (!s->exact && s->ub_seg > merge_cap(s->n_words)) QX_TRY(qx_store_refresh(s));
-  const int limit = merge_cap(s->n_words);
-  if (s->ub_seg > limit)
-    return qx_fail(QX_ERR_UNSUPPORTED,
-                   "n_qubits=%d (%d-word keys): a generator with %lld raw terms exceeds the %d the multi-word "
-                   "merge holds; states of that rank need n <= 32",
-                   s->n_qubits, s->n_words, (long long)s->ub_seg, limit);
+  if (s->ub_seg > merge_cap(s->n_words)) return wide_merge_large(s, eps);
   int cap = 32;
   while (cap < s->ub_seg) cap <<= 1;
   const size_t smem = (size_t)cap * (8 * (size_t)s->n_words + 2);

@@ -529,6 +529,10 @@ def _walk_v1(instructions, partition, w: _Walker, trace, counters, eager):
         counters["v1_gate_applications"] = counters.get("v1_gate_applications", 0) + n_1q
 
 
+# raw terms a multi-word operator walk may pile up before duplicates are summed (eps = 0)
+WIDE_RAW_BUDGET = 1 << 16
+
+
 def _walk_operators(partition, lut, is_perm, tables, w: _Walker, trace, counters, mode, eager):
     """Operator chain (reference engine.py:110-132): U_k = substitute + flatten, V_k = CX run."""
     n = w.n
@@ -555,9 +559,13 @@ def _walk_operators(partition, lut, is_perm, tables, w: _Walker, trace, counters
                 # per non-zero product of gate entries instead of a branch per non-zero block
                 # entry: paths to the same word are summed by the merge, to rounding what the
                 # reference's 3x3 products sum), so term sets after the drop rule agree.
+                # Every split doubles the raw list (multi-word splits write both branches of every
+                # term), so a long operator is summed in between with eps = 0: nothing is dropped
+                # before the operator's own merge, only duplicates meet earlier.
                 w.resolve(trace)               # expand merged terms only
                 bucket = partition.u_groups[ui]
                 t0 = time.perf_counter()
+                raw = sum(w.ranks)
                 for wire in sorted(bucket):
                     for inst in bucket[wire]:
                         table = _lut.FIXED_PERMS.get(inst.gate)
@@ -570,6 +578,11 @@ def _walk_operators(partition, lut, is_perm, tables, w: _Walker, trace, counters
                         else:
                             w.flush()
                             w.store.apply_split(wire, *split_tables(block))
+                            raw *= 2
+                    if raw > WIDE_RAW_BUDGET:
+                        w.flush()
+                        raw = sum(w.store.merge(0.0))
+                        w.unsorted = False
                 if mode is Mode.V2 and any(r > have for r, have in zip(w.store.ranks(), w.ranks)):
                     # dense layout: a row that is not one-hot needs the 4**n scatter buffer
                     # (reference stabilizer.py:264-276)

@@ -49,7 +49,7 @@ def test_apply_cx_big_int_unit(golden):
     assert out.lambdas.tolist() == u["out"]["lam"]
 
 
-@pytest.mark.parametrize("n,terms", [(40, 3000), (70, 1500), (130, 900)])
+@pytest.mark.parametrize("n,terms", [(40, 3000), (70, 1500), (130, 900), (40, 60000), (100, 20000), (130, 9000)])
 def test_split_and_merge_against_big_int_model(n, terms):
     """qx_apply_split_wide + the multi-word merge on random terms (the store grows past its first
     allocation on the way) against the reference's v1 rule done with Python ints."""
@@ -82,6 +82,59 @@ def test_split_and_merge_against_big_int_model(n, terms):
     assert ranks[0] == len(want) and [int(v) for v in gk] == [k for k, _ in want]
     assert np.max(np.abs(gl - np.array([v for _, v in want]))) < 1e-12
     assert abs(norms[0] - sum(v * v for _, v in want)) < 1e-9
+
+
+@pytest.mark.parametrize("n,sizes,pool", [(40, (50000, 0, 7, 20000), 9000), (70, (3, 30000, 30000), 50000),
+                                          (200, (12000, 1), 4000)])
+def test_large_multiword_merge_sums_runs_in_input_order(n, sizes, pool):
+    """Generators beyond one CTA's shared memory: permutation sorted word by word (stable LSD over
+    the words), then one reduce pass.  Raw terms drawn from a small pool of words (runs of many
+    duplicates), some in exactly cancelling pairs; sums must be BITWISE what sequential addition
+    in input order gives (np.add.at, reference stabilizer.py:333-335), empty generators included."""
+    rng = np.random.default_rng([n, pool])
+    words = [int.from_bytes(rng.bytes((2 * n + 7) // 8), "little") % 4 ** n for _ in range(pool)]
+    words[0], words[1] = 0, 4 ** n - 1                            # extremes of the key range
+    segs, want = [], []
+    for size in sizes:
+        pick = rng.integers(0, pool, size=size)
+        lam = rng.uniform(-1, 1, size=size)
+        for j in range(0, size - 1, 7):                           # cancelling pairs -> dropped or partial
+            pick[j + 1], lam[j + 1] = pick[j], -lam[j]
+        obj = np.empty(size, dtype=object)
+        obj[:] = [words[p] for p in pick]
+        segs.append((lam, obj))
+        model = {}
+        for k, l in zip(obj, lam):
+            model[k] = model.get(k, 0.0) + float(l)
+        want.append(sorted((k, v) for k, v in model.items() if abs(v) >= 1e-12))
+    with DeviceStore(n, len(sizes), 0) as st:
+        st.upload(segs)
+        ranks = st.merge(1e-12)
+        got = st.segments()
+    assert list(ranks) == [len(w) for w in want]
+    for (gl, gk), w in zip(got, want):
+        assert [int(v) for v in gk] == [k for k, _ in w]
+        assert gl.tolist() == [v for _, v in w]                   # bitwise
+
+
+@pytest.mark.parametrize("n,mode", [(36, "v1"), (36, "v3"), (70, "v3")])
+def test_high_rank_circuit_embedded_above_32_qubits(n, mode):
+    """The whole multi-word pipeline at a rank where every merge is the large one (generators of
+    up to 7.9e4 terms): xyz_chain(10,2) on the first ten of n qubits must give the one-word run's
+    generators with every word shifted by the idle qubits (word * 4**(n-10)); the one-word path is
+    itself pinned on the reference (tests/test_gpu_configs.py)."""
+    from paper_2505_03307_b200 import workloads
+    gates = workloads.gen_xyz_chain(10, 2, 1, 4)
+    narrow = qx.run(gates, 10, mode)
+    wide = qx.run(gates, n, mode)
+    assert wide.rank_trace[-1][:10] == narrow.rank_trace[-1] and set(wide.rank_trace[-1][10:]) == {1}
+    shift = 4 ** (n - 10)
+    for gw, gn in zip(wide.final.generators, narrow.final.generators):
+        assert [int(v) for v in gw.indices] == [int(v) * shift for v in gn.indices]
+        assert np.max(np.abs(gw.lambdas - gn.lambdas)) < 1e-12
+    for j in range(10, n):
+        g = wide.final.generators[j]
+        assert [int(v) for v in g.indices] == [3 * 4 ** (n - 1 - j)] and g.lambdas.tolist() == [1.0]
 
 
 def test_limits_above_32_qubits():
