@@ -121,7 +121,8 @@ int qx_store_download_packed_async(qx_store* s, int64_t* offsets, uint64_t* keys
 /* ---- more than 32 qubits (reference stabilizer.py:40-59 switches to Python
  * big-int indices there).  qx_store_create accepts n_qubits <= 512; above 32 the store is WIDE:
  * W = ceil(2n/64) words per key.  Wide stores run the part of the path that such circuits use --
- * Clifford runs, v1 rotations, merge/sort of generators up to 16384/W raw terms, ranks, norms --
+ * Clifford runs, v1 rotations (and with them branching v2/v3 operators, applied gate by gate),
+ * merge/sort of generators of any size, ranks, norms --
  * through the calls below plus qx_store_init_z / qx_merge / qx_sort / qx_store_ranks /
  * qx_store_norms; every other entry point returns QX_ERR_UNSUPPORTED on a wide store.
  * Host layout of wide keys: term-major uint64[term][W], word 0 least significant. */

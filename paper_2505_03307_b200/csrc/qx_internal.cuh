@@ -55,7 +55,7 @@ bool qx_profile_on();
 // geometry of the device-wide passes
 // ----------------------------------------------------------------------------
 constexpr int QX_MAX_QUBITS = 32;         // one-word keys: every kernel
-constexpr int QX_MAX_WORDS = 16;          // multi-word keys (wide.cu): Clifford / v1 path, n <= 512
+constexpr int QX_MAX_WORDS = 16;          // multi-word keys (wide.cu), n <= 512
 constexpr int QX_MAX_QUBITS_WIDE = 32 * QX_MAX_WORDS;
 constexpr int QX_RADIX_BITS = 8;
 constexpr int QX_RADIX = 1 << QX_RADIX_BITS;
