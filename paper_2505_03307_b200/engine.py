@@ -172,7 +172,6 @@ class _Walker:
         counts, axes, weights = self.staged
         self.staged = None
         program = np.array(self.queue, dtype=np.uint32)
-        had_cx = self.queue_has_cx
         self.queue, self.queue_has_cx = [], False
         t0 = time.perf_counter()
         if self.before_merge is not None:
@@ -191,7 +190,6 @@ class _Walker:
         if len(program):
             self.launch_log["clifford_runs"] += 1
             self.launch_log["fused_runs"] = self.launch_log.get("fused_runs", 0) + 1
-        del had_cx
         for local, r in enumerate(self.ranks):
             if r == 0:
                 raise NumericalCollapseError(
@@ -565,6 +563,22 @@ def _walk_operators(partition, lut, is_perm, tables, w: _Walker, trace, counters
                 w.resolve(trace)               # expand merged terms only
                 bucket = partition.u_groups[ui]
                 t0 = time.perf_counter()
+                if mode is Mode.V2:
+                    # dense layout: a row of the substituted block that is not one-hot needs the
+                    # 4**n scatter buffer (reference stabilizer.py:264-276).  Nothing has ever
+                    # branched when this is reached, so the generators are a handful of terms.
+                    counts, _, _ = _lut.operator_tables(lut[ui])
+                    wires_ = np.flatnonzero(counts.max(axis=1) > 1).tolist()
+                    w.flush()
+                    for _, words in w.store.segments():
+                        for word in words:
+                            for q in wires_:
+                                d = (int(word) >> (2 * (n - 1 - q))) & 3
+                                if d and counts[q, d - 1] > 1:
+                                    raise ResourceLimitError(
+                                        f"dense flatten needs a 4**{n}-element buffer (> {DENSE_FLATTEN_BUDGET}); "
+                                        "use the ragged layout for circuits of this size"
+                                    )
                 raw = sum(w.ranks)
                 for wire in sorted(bucket):
                     for inst in bucket[wire]:
@@ -583,13 +597,6 @@ def _walk_operators(partition, lut, is_perm, tables, w: _Walker, trace, counters
                         w.flush()
                         raw = sum(w.store.merge(0.0))
                         w.unsorted = False
-                if mode is Mode.V2 and any(r > have for r, have in zip(w.store.ranks(), w.ranks)):
-                    # dense layout: a row that is not one-hot needs the 4**n scatter buffer
-                    # (reference stabilizer.py:264-276)
-                    raise ResourceLimitError(
-                        f"dense flatten needs a 4**{n}-element buffer (> {DENSE_FLATTEN_BUDGET}); "
-                        "use the ragged layout for circuits of this size"
-                    )
                 w.timings["sub_flatten"] += time.perf_counter() - t0
                 w.branched(step, "sub_flatten", trace)
             else:

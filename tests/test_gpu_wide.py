@@ -142,6 +142,9 @@ def test_limits_above_32_qubits():
     gates = [qx.Instruction("H", (0,)), qx.Instruction("RY", (0,), 0.3), qx.Instruction("CX", (0, 35))]
     with pytest.raises(qx.ResourceLimitError, match="dense flatten"):
         qx.run(gates, n, "v2")                                    # reference stabilizer.py:264-276
+    # ... but only for rows that are not one-hot: RZ leaves every Z_j alone (dense fast path)
+    calm = [qx.Instruction("RZ", (3,), 0.4), qx.Instruction("CX", (3, 4)), qx.Instruction("RZ", (4,), 1.1)]
+    assert qx.run(calm, n, "v2").rank_trace[-1] == [1] * n
     for mode in ("v1", "v3"):
         rep = qx.run(gates, n, mode)
         assert rep.rank_trace[-1][0] == 2 and rep.final.generators[35].rank == 1
