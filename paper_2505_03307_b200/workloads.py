@@ -145,6 +145,8 @@ WORKLOADS = {
     "c4_xyz_14_2": lambda: config4(14, 2),
     "c4_xyz_16_2": lambda: config4(16, 2),
     "c4_xyz_18_2": lambda: config4(18, 2),
+    "c4_xyz_20_2": lambda: config4(20, 2),      # ~1.0e10 terms, ~330 GB: beyond one GPU
+    "c4_xyz_20_4": lambda: config4(20, 4),      # BASELINE config 4 as written: infeasible
     "c5_32q_clifford_t": config5,
 }
 

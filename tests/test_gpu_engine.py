@@ -73,6 +73,17 @@ def test_errors():
         qx.run([], 513, "v1")                                  # at most sixteen words per key
 
 
+def test_oversized_ansatz_is_refused_cleanly():
+    """BASELINE config 4 as written (n = 20, four layers) and its two-layer point need > 300 GB of
+    terms: ResourceLimitError before anything is allocated, device usable after."""
+    for name in ("c4_xyz_20_2", "c4_xyz_20_4"):
+        n, gates = workloads.build(name)
+        with pytest.raises(qx.ResourceLimitError, match="GB of HBM"):
+            qx.run(gates, n, "v3", download=False)
+    rep = qx.run(workloads.gen_xyz_chain(8, 2, 1, 4), 8, "v3")
+    assert sum(rep.rank_trace[-1]) == 19734
+
+
 # ------------------------------------------------------------------ fixtures from the reference
 def test_campaign_all_modes(golden):
     for entry in golden.load_json("campaign.json"):
