@@ -17,6 +17,10 @@ the B200-native scale-out of SURVEY.md sections 5.9 / 8e.
 
 * ``run_slot_partitioned`` -- one circuit, every rank takes a range of the output slots of the
   last branching operator (csrc/dense.cu): even split whatever the skew, no collective.
+* ``expectation_sharded`` / ``prob_z_sharded`` -- read-out, observable-parallel:
+  the words are independent back-propagations (``measure.expectation_heisenberg``), each rank
+  takes every world-th word, and ONE all-reduce of the result vector hands every rank all
+  scalars (each scalar is owned by one rank, the others add +0.0: the sum is exact).
 
 The functions take an injected ``runner`` / tensors so the host logic (sharding,
 split sizes, gather/assemble) is testable with the gloo backend on CPU; the compute
@@ -296,3 +300,54 @@ def _gather_partitioned(final, n, group):
         order = np.argsort(keys, kind="stable")
         out.append(SimpleGenerator(n, lam[order], keys_to_indices(keys[order], n)))
     return GeneratorSet(n, out)
+
+
+# ------------------------------------------------------------------------------------
+# read-out, observable-parallel
+# ------------------------------------------------------------------------------------
+def expectation_sharded(instructions, n: int, words, mode="v1", eps: float = 1e-12, *, group=None,
+                        evaluator=None, **kw) -> np.ndarray:
+    """<psi|W|psi> for every word of ``words`` on every rank; rank r evaluates words r, r + world, ...
+
+    The words never interact (each is pushed back through the inverse circuit on its own,
+    ``measure.expectation_heisenberg``), so the only collective is the final all-reduce of
+    len(words) float64 scalars -- the read-out reduction BASELINE.json's north star names.
+    ``evaluator(instructions, n, words, mode, eps)`` defaults to ``expectation_heisenberg``.
+    """
+    import torch
+
+    dist = _dist()
+    if evaluator is None:
+        from .measure import expectation_heisenberg as evaluator
+    words = [int(w) for w in words]
+    for w in words:
+        if not 0 <= w < 4 ** n:
+            raise ValueError(f"word index {w} out of range [0, 4**{n})")
+    world, rank = dist.get_world_size(group), dist.get_rank(group)
+    mine = list(range(rank, len(words), world))
+    out = np.zeros(len(words), dtype=np.float64)
+    if mine:
+        out[mine] = np.asarray(evaluator(instructions, n, [words[i] for i in mine], mode, eps, **kw),
+                               dtype=np.float64)
+    if len(words):
+        t = torch.from_numpy(out).to(_comm_device(group))
+        dist.all_reduce(t, op=dist.ReduceOp.SUM, group=group)
+        out = t.cpu().numpy()
+    return out
+
+
+def prob_z_sharded(instructions, n: int, mode="v1", eps: float = 1e-12, *, group=None, evaluator=None,
+                   **kw) -> np.ndarray:
+    """(n, 2) array of (p0, p1) for every qubit: p0 = (1 + <Z_k>) / 2, the same number the
+    reference reads from the expansion (measure.py:94-111: p0 = 1/2 + 2^(n-1) coeff(Z_k), and
+    <Z_k> = 2^n coeff(Z_k)), with its consistency check and clamp."""
+    from .errors import ConsistencyError
+
+    z = expectation_sharded(instructions, n, [3 * 4 ** (n - 1 - k) for k in range(n)], mode, eps,
+                            group=group, evaluator=evaluator, **kw)
+    p0 = 0.5 + 0.5 * z
+    for k, p in enumerate(p0):
+        if not -1e-10 <= p <= 1.0 + 1e-10:
+            raise ConsistencyError(f"probability {p} for qubit {k} outside [0, 1]")
+    p0 = np.clip(p0, 0.0, 1.0)
+    return np.stack([p0, 1.0 - p0], axis=1)

@@ -87,6 +87,27 @@ def _worker(rank, world, port, out_dir):
         dist.all_reduce(t)
         assert int(t.item()) == sum(want["rank_trace"][-1])
 
+        # ---- observable-parallel read-out: words dealt round-robin, one all-reduce of the scalars
+        n5, circ = 5, workloads.gen_random(5, 40, 11)
+        words = [0, 3, 4 ** 5 - 1] + [int(v) for v in np.random.default_rng(5).integers(0, 4 ** 5, size=14)]
+        seen = []
+
+        def _evaluator(instructions, n, ws, mode, eps):
+            seen.extend(ws)
+            return oracle.expectation_heisenberg(instructions, n, ws, mode, eps)
+
+        got = qd.expectation_sharded(circ, n5, words, "v1", evaluator=_evaluator)
+        assert seen == words[rank::world]                       # this rank evaluated only its share
+        assert np.array_equal(got, oracle.expectation_heisenberg(circ, n5, words, "v1"))
+        assert len(qd.expectation_sharded(circ, n5, [], evaluator=_evaluator)) == 0
+        pz = qd.prob_z_sharded(circ, n5, evaluator=_evaluator)
+        final = oracle.run(circ, n5, "v3")["final"]
+        ex = oracle.density_expansion(final, n5)
+        for k in range(n5):
+            assert abs(pz[k, 0] - oracle.prob_z(final, n5, k, ex)[0]) < 1e-10 and pz[k, 0] + pz[k, 1] == 1.0
+        with pytest.raises(ValueError):
+            qd.expectation_sharded(circ, n5, [4 ** 5], evaluator=_evaluator)
+
         # ---- all-to-all-v of hash-partitioned terms
         rng = np.random.default_rng(100 + rank)
         n_seg = 3

@@ -99,3 +99,18 @@ def test_run_slot_partitioned_world1(nccl_world1):
     assert rep.rank_trace == plain.rank_trace
     for ga, gb in zip(rep.final.generators, plain.final.generators):
         assert np.array_equal(ga.keys(), gb.keys()) and np.array_equal(ga.lambdas, gb.lambdas)
+
+
+def test_sharded_readout_equals_the_expansion_route(nccl_world1):
+    """dist.expectation_sharded / prob_z_sharded (Heisenberg back-propagation per word, scalars
+    all-reduced over NCCL) against the reference's route, the density expansion, on config 1:
+    all 256 words and every qubit's probabilities."""
+    n, gates = workloads.build("c1_4q_clifford_t")
+    final = qx.run(gates, n, "v3").final
+    ex = qx.density_expansion(final)
+    got = qd.expectation_sharded(gates, n, range(4 ** n))
+    want = np.array([qx.expectation(final, w, ex) for w in range(4 ** n)])
+    assert np.max(np.abs(got - want)) < 1e-10
+    pz = qd.prob_z_sharded(gates, n)
+    for k in range(n):
+        assert abs(pz[k, 0] - qx.prob_z(final, k, ex)[0]) < 1e-10
