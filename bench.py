@@ -129,6 +129,20 @@ def lpt_shards(weights, world):
 # ------------------------------------------------------------------------------------------
 # CPU arm (numpy oracle port): also the cpu_baseline leg of the GPU arm
 # ------------------------------------------------------------------------------------------
+def host_cpu() -> str:
+    """Model name and logical core count of the host (state them beside the CPU arm)."""
+    model = "unknown CPU"
+    try:
+        with open("/proc/cpuinfo") as fh:
+            for line in fh:
+                if line.lower().startswith("model name"):
+                    model = line.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
+    return f"{model}, {os.cpu_count() or 1} logical cores"
+
+
 def _cpu_worker(args):
     name, mode, gens = args
     sys.path.insert(0, os.path.join(ROOT, "oracle"))
@@ -178,7 +192,8 @@ def run_reference(args, updates_per_gen):
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": sec * 1e3,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic", "config": {"workload": args.workload, "mode": args.mode, "sample": sample},
-        "cpu_baseline": {"value": value, "unit": "updates/s", "cores": procs, "kind": "port", "sample": sample},
+        "cpu_baseline": {"value": value, "unit": "updates/s", "cores": procs, "kind": "port", "sample": sample,
+                         "host": host_cpu()},
         "e2e": {"value": value, "unit": "updates/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "gpu_launches": 0,
     }
@@ -346,7 +361,7 @@ def run_ours(args):
         gens = CPU_SAMPLE.get(args.workload) or list(range(n))
         sec = cpu_step(args.workload, args.mode, gens, 1)
         cpu = {"value": float(sum(updates_per_gen[g] for g in gens)) / sec, "unit": "updates/s", "cores": 1,
-               "kind": "port",
+               "kind": "port", "host": host_cpu(),
                "sample": f"generators {gens[0]}..{gens[-1]} of {args.workload} ({len(gens)} of {n}), {args.mode}, "
                          f"numpy port of the reference (oracle/stabsim_port.py), {sec:.1f} s on 1 core"}
 
