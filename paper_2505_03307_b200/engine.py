@@ -38,6 +38,7 @@ from .stabilizer import (
     GeneratorSet,
     SimpleGenerator,
     keys_to_indices,
+    pad_dense,
     rank_stats,
     split_tables,
 )
@@ -613,8 +614,18 @@ def _walk_operators(partition, lut, is_perm, tables, w: _Walker, trace, counters
                             f"dense flatten needs a 4**{n}-element buffer (> {DENSE_FLATTEN_BUDGET}); "
                             "use the ragged layout for circuits of this size"
                         )
+                dense_gens = []
+                if mode is Mode.V2 and w.eps == 0.0 and 4 ** n <= DENSE_FLATTEN_BUDGET and w.before_merge is None:
+                    # dense layout, eps = 0: a generator with a branching row comes back from the
+                    # reference's 4**n buffer with every word, zeros included (stabilizer.py:277-286)
+                    raw = w.store.count_operator(counts)
+                    dense_gens = [g for g, (r, have) in enumerate(zip(raw, w.store.ranks())) if r > have]
+                if dense_gens:
+                    w.store.apply_operator(counts, axes, weights)
+                    pad_dense(w.store, n, dense_gens)
+                else:
+                    w.stage_operator(counts, axes, weights)
                 w.timings["sub_flatten"] += time.perf_counter() - t0
-                w.stage_operator(counts, axes, weights)
                 w.branched(step, "sub_flatten", trace)
             counters["sub_flatten_ops"] += 1
             ui += 1

@@ -241,6 +241,20 @@ def branch_counts(cg: ComplexForm) -> np.ndarray:
         return np.array(st.count_operator(counts), dtype=np.int64)
 
 
+def pad_dense(st: DeviceStore, n: int, segments) -> None:
+    """Dense layout with eps = 0: a generator that went through the reference's 4**n scatter
+    buffer keeps EVERY word, exact zeros included (``keep = |out| >= 0``, stabilizer.py:277-286).
+    Appends one zero-coefficient term per word to the raw lists of ``segments``; the merge that
+    follows adds 0.0 into the words that exist and keeps the rest as zeros.  Only reachable for
+    4**n <= DENSE_FLATTEN_BUDGET; the lists take a round trip through the host (no arithmetic)."""
+    segs = [(lam.copy(), keys.copy()) for lam, keys in st.segments()]
+    every = np.arange(4 ** n, dtype=np.uint64)
+    for g in segments:
+        lam, keys = segs[g]
+        segs[g] = (np.concatenate([lam, np.zeros(len(every))]), np.concatenate([keys, every]))
+    st.upload(segs)
+
+
 def flatten(cg: ComplexForm, eps: float = DEFAULT_EPS, canonical: bool = True) -> SimpleGenerator:
     """Expand a complex form back into a simple form (reference stabilizer.py:240-256).
 
@@ -260,7 +274,11 @@ def flatten(cg: ComplexForm, eps: float = DEFAULT_EPS, canonical: bool = True) -
                     f"dense flatten needs a 4**{n}-element buffer (> {DENSE_FLATTEN_BUDGET}); "
                     "use the ragged layout for circuits of this size"
                 )
+        dense_zeros = (cg.layout == "dense" and canonical and eps == 0.0
+                       and st.count_operator(counts)[0] > len(cg.lambdas))
         st.apply_operator(counts, axes, weights)
+        if dense_zeros:
+            pad_dense(st, n, [0])
         if canonical:
             st.merge(eps)
         return _fetch(st, n)

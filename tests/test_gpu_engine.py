@@ -335,3 +335,21 @@ def test_random_entangling_circuits_against_oracle(case):
     for g, (lam, idx) in zip(got.final.generators, want["final"]):
         assert np.array_equal(g.keys(), idx)
         assert len(lam) == 0 or np.max(np.abs(g.lambdas - lam)) < TOL
+
+
+def test_dense_layout_with_eps_zero_keeps_every_word():
+    """v2 with eps = 0: a generator that branches goes through the reference's 4**n scatter buffer and
+    comes back with EVERY word, exact zeros included (stabilizer.py:277-286); found by
+    tools/fuzz_engine.py.  Checked against the oracle port (which equals the reference here)."""
+    for seed, n, m in ((1, 1, 27), (2, 2, 39), (3, 3, 15), (4, 5, 30)):
+        gates = workloads.gen_random(n, m, seed)
+        got = qx.run(gates, n, "v2", eps=0.0)
+        want = oracle.run(gates, n, "v2", 0.0)
+        assert got.rank_trace == want["rank_trace"]
+        for g, (lam, idx) in zip(got.final.generators, want["final"]):
+            assert np.array_equal(g.keys(), idx) and np.max(np.abs(g.lambdas - lam), initial=0.0) < TOL
+    g = qx.SimpleGenerator(2, [1.0], [5])                        # XX through RY on both qubits
+    block = np.broadcast_to(lut.axis_map("RY", 0.7).T, (2, 3, 3)).copy()
+    dense = qx.flatten(qx.sub(g, block, "dense"), eps=0.0)
+    assert dense.rank == 16 and int((dense.lambdas == 0.0).sum()) == 12
+    assert qx.flatten(qx.sub(g, block, "ragged"), eps=0.0).rank == 4
