@@ -212,6 +212,16 @@ int qx_operator_classes(int32_t n_qubits, const int32_t* counts, const int32_t* 
 /* Number of raw branches the same call would produce per segment, nothing written
  * (branch_counts, stabilizer.py:232-237). */
 int qx_count_operator(qx_store* s, const int32_t* counts, int64_t* raw_per_segment);
+/* Put the terms of every segment into the order in which the reference's ragged flatten walks
+ * its strings (_flatten_ragged, stabilizer.py:294-296): strings grouped by their per-qubit branch
+ * counts (count vectors ascending lexicographically, qubit 0 first), inside a group by word
+ * (by_key = 1: the canonical order of engine.run's generators, whatever permutation the store
+ * is in) or by input position (by_key = 0: the stable order of the kernel-level flatten).  Sums
+ * of three or more contributions to one word are then added in the reference's order, so a
+ * following qx_apply_operator(_run) + merge gives its coefficients bit for bit.  Segments of
+ * more than 2048 terms are left as they are (large groups are summed in factored form anyway).
+ * Asynchronous; nothing is read back. */
+int qx_store_order_for_operator(qx_store* s, const int32_t* counts, int32_t by_key);
 
 /* ---- a6: duplicate-term merge (canonicalize, stabilizer.py:325-337).
  * Per segment: stable sort by key, in-order segmented sum, keep |sum| >= eps,

@@ -67,6 +67,7 @@ SIGNATURES = {
     "qx_apply_operator_run": (C.c_int, [_p, _p, _p, _p, _p, _i32, _u32, _u32, _u32, _f64, _i64, _P(_i64), _p]),
     "qx_apply_operator_run_part": (C.c_int, [_p, _p, _p, _p, _p, _i32, _u32, _u32, _u32, _f64, _i32, _i32, _p, _P(_i32)]),
     "qx_count_operator": (C.c_int, [_p, _p, _p]),
+    "qx_store_order_for_operator": (C.c_int, [_p, _p, C.c_int32]),
     "qx_operator_classes": (C.c_int, [_i32, _p, _p, _p, _p, _p, _p, _p]),
     "qx_merge": (C.c_int, [_p, _f64, _p]),
     "qx_sort": (C.c_int, [_p]),

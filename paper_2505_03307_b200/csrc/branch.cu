@@ -541,6 +541,98 @@ static int count_pass(qx_store* s, const OperatorTable& tb, u64** roff_out) {
   return QX_OK;
 }
 
+// ---- source order of the reference's ragged flatten ---------------------------------------------
+// One CTA per segment of at most kOrdCap terms: pattern word (branch count minus one of every
+// digit, two bits each, qubit 0 most significant: numeric order = lexicographic order of the
+// count vectors np.unique(axis=0) produces, stabilizer.py:294), bitonic sort on (pattern, tie) in
+// shared memory, terms written back in place.  Segments already in that order are not touched.
+constexpr int kOrdCap = 2048;
+constexpr int kOrdThreads = 256;
+struct OrdSmem {
+  u64 pat[kOrdCap];
+  u64 tie[kOrdCap];
+  u64 key[kOrdCap];
+  double lam[kOrdCap];
+};
+
+__global__ void __launch_bounds__(kOrdThreads)
+k_order_by_pattern(u64* __restrict__ keys, double* __restrict__ lam, const int64_t* __restrict__ seg, int by_key,
+                   const __grid_constant__ OperatorTable tb) {
+  extern __shared__ __align__(16) unsigned char ord_raw[];
+  OrdSmem& sm = *reinterpret_cast<OrdSmem*>(ord_raw);
+  __shared__ unsigned char s_cnt[QX_MAX_QUBITS][3];
+  const int64_t lo = seg[blockIdx.x], len64 = seg[blockIdx.x + 1] - lo;
+  if (len64 < 3 || len64 > kOrdCap) return;       // two contributions add up the same in either order
+  for (int i = threadIdx.x; i < QX_MAX_QUBITS * 3; i += kOrdThreads) s_cnt[i / 3][i % 3] = tb.cnt[i / 3][i % 3];
+  __syncthreads();
+  const int len = (int)len64;
+  int m = 32;
+  while (m < len) m <<= 1;
+  for (int e = threadIdx.x; e < m; e += kOrdThreads) {
+    u64 key = ~0ull, pat = ~0ull;                // padding sorts behind every term
+    double l = 0.0;
+    if (e < len) {
+      key = keys[lo + e];
+      l = lam[lo + e];
+      pat = 0;
+      for (u64 sup = support_mask(key); sup;) {
+        const int b = __ffsll((long long)sup) - 1;
+        sup &= sup - 1;
+        pat |= (u64)(s_cnt[b >> 1][((key >> b) & 3ull) - 1] - 1) << b;
+      }
+    }
+    sm.pat[e] = pat;
+    sm.key[e] = key;
+    sm.lam[e] = l;
+    sm.tie[e] = by_key ? key : (u64)e;
+  }
+  __syncthreads();
+  int bad = 0;
+  for (int e = threadIdx.x + 1; e < len; e += kOrdThreads)
+    bad |= sm.pat[e - 1] > sm.pat[e] || (sm.pat[e - 1] == sm.pat[e] && sm.tie[e - 1] > sm.tie[e]);
+  if (!__syncthreads_or(bad)) return;
+  for (int k = 2; k <= m; k <<= 1) {
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      for (int t = threadIdx.x; t < (m >> 1); t += kOrdThreads) {
+        const int a = ((t & ~(j - 1)) << 1) | (t & (j - 1));
+        const int b = a | j;
+        const u64 pa = sm.pat[a], pb = sm.pat[b], ta = sm.tie[a], tb2 = sm.tie[b];
+        const bool greater = pa > pb || (pa == pb && ta > tb2);
+        if (greater == ((a & k) == 0)) {
+          sm.pat[a] = pb; sm.pat[b] = pa;
+          sm.tie[a] = tb2; sm.tie[b] = ta;
+          const u64 ka = sm.key[a]; sm.key[a] = sm.key[b]; sm.key[b] = ka;
+          const double la = sm.lam[a]; sm.lam[a] = sm.lam[b]; sm.lam[b] = la;
+        }
+      }
+      __syncthreads();
+    }
+  }
+  for (int e = threadIdx.x; e < len; e += kOrdThreads) {
+    keys[lo + e] = sm.key[e];
+    lam[lo + e] = sm.lam[e];
+  }
+}
+
+extern "C" int qx_store_order_for_operator(qx_store* s, const int32_t* counts, int32_t by_key) {
+  QX_REQUIRE(s && counts, "NULL argument");
+  QX_NARROW_ONLY(s, "qx_store_order_for_operator");
+  OperatorTable tb;
+  QX_TRY(fill_table(s, counts, nullptr, nullptr, &tb));
+  if (s->ub_seg < 3 || s->n_seg == 0) return QX_OK;
+  QX_CUDA(cudaSetDevice(s->device));
+  static bool attr_set = false;
+  if (!attr_set) {
+    QX_CUDA(cudaFuncSetAttribute(k_order_by_pattern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(OrdSmem)));
+    attr_set = true;
+  }
+  k_order_by_pattern<<<s->n_seg, kOrdThreads, sizeof(OrdSmem), s->stream>>>(s->keys[s->cur], s->lam[s->cur],
+                                                                         s->seg[s->cur], by_key ? 1 : 0, tb);
+  qx_count_launches(1);
+  QX_CUDA(cudaGetLastError());
+  return QX_OK;
+}
+
 extern "C" int qx_count_operator(qx_store* s, const int32_t* counts, int64_t* raw_per_segment) {
   QX_REQUIRE(s && counts && raw_per_segment, "NULL argument");
   QX_NARROW_ONLY(s, "qx_count_operator");

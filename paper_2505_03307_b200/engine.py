@@ -614,6 +614,12 @@ def _walk_operators(partition, lut, is_perm, tables, w: _Walker, trace, counters
                             f"dense flatten needs a 4**{n}-element buffer (> {DENSE_FLATTEN_BUDGET}); "
                             "use the ragged layout for circuits of this size"
                         )
+                if mode is Mode.V3:
+                    # the reference's ragged flatten walks the strings grouped by their branch-count
+                    # pattern (stabilizer.py:294-296); same order here, so that sums of three or more
+                    # contributions round the same way (the store may also sit in a permuted order:
+                    # the re-sort after the last Clifford run is deferred)
+                    w.store.order_for_operator(counts)
                 dense_gens = []
                 if mode is Mode.V2 and w.eps == 0.0 and 4 ** n <= DENSE_FLATTEN_BUDGET and w.before_merge is None:
                     # dense layout, eps = 0: a generator with a branching row comes back from the

@@ -258,7 +258,8 @@ def pad_dense(st: DeviceStore, n: int, segments) -> None:
 def flatten(cg: ComplexForm, eps: float = DEFAULT_EPS, canonical: bool = True) -> SimpleGenerator:
     """Expand a complex form back into a simple form (reference stabilizer.py:240-256).
 
-    ``canonical=False`` returns the raw branch list (term-major, C order).  The
+    ``canonical=False`` returns the raw branch list in the reference's order (strings grouped by
+    branch-count pattern, stable inside a group, each string's branches in C order).  The
     dense layout keeps the reference's budget guard (stabilizer.py:272-276): it
     refuses a branching expansion when 4**n exceeds DENSE_FLATTEN_BUDGET.
     """
@@ -274,6 +275,8 @@ def flatten(cg: ComplexForm, eps: float = DEFAULT_EPS, canonical: bool = True) -
                     f"dense flatten needs a 4**{n}-element buffer (> {DENSE_FLATTEN_BUDGET}); "
                     "use the ragged layout for circuits of this size"
                 )
+        if cg.layout == "ragged" or not canonical:
+            st.order_for_operator(counts, by_key=False)      # raw order of _flatten_ragged (:294-296)
         dense_zeros = (cg.layout == "dense" and canonical and eps == 0.0
                        and st.count_operator(counts)[0] > len(cg.lambdas))
         st.apply_operator(counts, axes, weights)

@@ -259,6 +259,11 @@ class DeviceStore:
         nat.check(nat.lib().qx_count_operator(self._h, nat.ptr(counts), nat.ptr(out)))
         return out.tolist()
 
+    def order_for_operator(self, counts, by_key: bool = True):
+        """Source order of the reference's ragged flatten (qx_store_order_for_operator)."""
+        counts = np.ascontiguousarray(counts, dtype=np.int32).reshape(-1)
+        nat.check(nat.lib().qx_store_order_for_operator(self._h, nat.ptr(counts), 1 if by_key else 0))
+
     def merge(self, eps: float) -> list:
         out = np.zeros(self.n_segments, dtype=np.int64)
         nat.check(nat.lib().qx_merge(self._h, float(eps), nat.ptr(out)))

@@ -353,3 +353,35 @@ def test_dense_layout_with_eps_zero_keeps_every_word():
     dense = qx.flatten(qx.sub(g, block, "dense"), eps=0.0)
     assert dense.rank == 16 and int((dense.lambdas == 0.0).sum()) == 12
     assert qx.flatten(qx.sub(g, block, "ragged"), eps=0.0).rank == 4
+
+
+def test_v1_and_v3_coefficients_are_bitwise_the_oracles():
+    """Sums of three or more contributions to one word are added in the reference's order -- sources
+    grouped by branch-count pattern (stabilizer.py:294-296), canonical inside a group -- so small
+    circuits reproduce the oracle (= the reference) bit for bit in v3 as they do in v1.  Without
+    qx_store_order_for_operator 9 of these 250 circuits differ in the last bit."""
+    for case in range(250):
+        rng = np.random.default_rng([1, 19800 + case])
+        n = int(rng.integers(1, 8))
+        gates = workloads.gen_random(n, int(rng.integers(0, 50)), rng)
+        for mode in ("v1", "v3"):
+            got = qx.run(gates, n, mode).final
+            want = oracle.run(gates, n, mode)["final"]
+            for g, (lam, idx) in zip(got.generators, want):
+                assert np.array_equal(g.keys(), idx) and np.array_equal(g.lambdas, lam), (case, mode)
+
+
+def test_raw_flatten_order_is_the_references():
+    """flatten(canonical=False): strings grouped by branch-count pattern, stable inside a group,
+    branches in C order (stabilizer.py:289-322) -- the oracle's expand_operator, element for element."""
+    rng = np.random.default_rng(77)
+    for _ in range(20):
+        n = int(rng.integers(2, 6))
+        idx = rng.choice(4 ** n, size=min(4 ** n, int(rng.integers(3, 30))), replace=False)
+        g = qx.SimpleGenerator(n, rng.uniform(-1, 1, size=len(idx)), idx)
+        names = [str(v) for v in rng.choice(["H", "RX", "RY", "RZ", "S"], size=n)]
+        block = np.stack([lut.compose_block([ir.Instruction(name, (q,), float(rng.uniform(0, 6.3)) if name[0] == "R" else 0.0)])
+                          for q, name in enumerate(names)])
+        raw = qx.flatten(qx.sub(g, block), canonical=False)
+        wl, wi = oracle.expand_operator(g.lambdas, g.keys(), n, block)
+        assert np.array_equal(raw.keys(), wi) and np.array_equal(raw.lambdas, wl)
