@@ -485,8 +485,71 @@ class _Shard:
 
 def _walk_v1(instructions, partition, w: _Walker, trace, counters, eager):
     """Gate by gate (reference engine.py:155-180): rank snapshots at operator boundaries."""
-    boundaries = set(np.cumsum(partition.operator_sizes()).tolist())
     w.updates = np.zeros(len(w.ids), dtype=np.int64)
+    if eager:
+        return _walk_v1_eager(instructions, partition, w, trace, counters)
+    # Gates that are exact signed permutations only queue an op word; the loop below does nothing
+    # else for them (op words from per-qubit shift tables, gate counts booked in bulk at the next
+    # branching gate or operator boundary -- the ranks cannot change in between).
+    n = w.n
+    sh1, sh2 = (32, 48) if n > 32 else (2, 8)
+    pos_a = [(2 * (n - 1 - q)) << sh1 for q in range(n)]
+    pos_b = [(2 * (n - 1 - q)) << sh2 for q in range(n)]
+    fixed = {g: t << 16 for g, t in _lut.FIXED_PERMS.items()}
+    fixed_get = fixed.get
+    bounds = iter(np.cumsum(partition.operator_sizes()).tolist())
+    nb = next(bounds, -1)
+    push = w.queue.append
+    n_cx = cnt = 0
+
+    def book(count):
+        if w.pending is None:
+            w.clean_gates += count
+        else:
+            w.pending_gates += count
+
+    for pos, inst in enumerate(instructions, start=1):
+        wires = inst.wires
+        if len(wires) == 2:
+            push(1 | pos_a[wires[0]] | pos_b[wires[1]])
+            w.queue_has_cx = True
+            n_cx += 1
+            cnt += 1
+        else:
+            op = fixed_get(inst.gate)
+            if op is not None:
+                push(op | pos_a[wires[0]])
+                cnt += 1
+            else:
+                block = _lut.gate_branch_block(inst.gate, inst.theta)
+                table = _lut.perm_word(block)
+                if table is not None:
+                    if table != _lut.IDENTITY_PERM:
+                        push(_lut.perm_op(n, wires[0], table))
+                    cnt += 1
+                else:
+                    book(cnt)
+                    cnt = 0
+                    w.resolve(trace)               # this gate must see merged terms
+                    w.count_gate()
+                    w.flush()
+                    t0 = time.perf_counter()
+                    w.store.apply_split(wires[0], *split_tables(block))
+                    w.timings["sub_flatten"] += time.perf_counter() - t0
+                    w.branched(pos - 1, "sub_flatten", trace)
+                    push = w.queue.append          # flush starts a new queue
+        if pos == nb:
+            w.snapshot(trace)
+            nb = next(bounds, -1)
+    book(cnt)
+    counters["cx_applications"] += n_cx
+    if len(instructions) > n_cx:
+        counters["v1_gate_applications"] = counters.get("v1_gate_applications", 0) + len(instructions) - n_cx
+
+
+def _walk_v1_eager(instructions, partition, w: _Walker, trace, counters):
+    """The same walk with a merge after every gate (eps could drop an input term)."""
+    boundaries = set(np.cumsum(partition.operator_sizes()).tolist())
     n = w.n
     fixed = _lut.FIXED_PERMS
     n_cx = n_1q = 0
@@ -497,8 +560,7 @@ def _walk_v1(instructions, partition, w: _Walker, trace, counters, eager):
             w.queue.append(_lut.cx_op(n, wires[0], wires[1]))
             w.queue_has_cx = True
             n_cx += 1
-            if eager:
-                w.step_done(pos - 1, "cx", trace)
+            w.step_done(pos - 1, "cx", trace)
         else:
             q = wires[0]
             table = fixed.get(inst.gate)
@@ -510,8 +572,7 @@ def _walk_v1(instructions, partition, w: _Walker, trace, counters, eager):
                 w.count_gate()
                 if table != _lut.IDENTITY_PERM:
                     w.queue.append(_lut.perm_op(n, q, table))
-                if eager:
-                    w.step_done(pos - 1, "sub_flatten", trace)
+                w.step_done(pos - 1, "sub_flatten", trace)
             else:
                 w.resolve(trace)               # this gate must see merged terms
                 w.count_gate()
