@@ -655,10 +655,9 @@ def _walk_operators(partition, lut, is_perm, tables, w: _Walker, trace, counters
                             w.flush()
                             w.store.apply_split(wire, *split_tables(block))
                             raw *= 2
-                    if raw > WIDE_RAW_BUDGET:
-                        w.flush()
-                        raw = sum(w.store.merge(0.0))
-                        w.unsorted = False
+                            if raw > WIDE_RAW_BUDGET:
+                                raw = sum(w.store.merge(0.0))
+                                w.unsorted = False
                 w.timings["sub_flatten"] += time.perf_counter() - t0
                 w.branched(step, "sub_flatten", trace)
             else:

@@ -137,6 +137,20 @@ def test_high_rank_circuit_embedded_above_32_qubits(n, mode):
         assert [int(v) for v in g.indices] == [3 * 4 ** (n - 1 - j)] and g.lambdas.tolist() == [1.0]
 
 
+def test_long_single_wire_operator_above_32_qubits():
+    """Forty rotations on ONE wire inside one operator: the multi-word walk doubles the raw list per
+    split and must sum duplicates in between (found by tools/fuzz_wide.py: it ran out of memory)."""
+    n = 70
+    rng = np.random.default_rng(3)
+    gates = [qx.Instruction(str(rng.choice(["RX", "RY", "RZ"])), (0,), float(rng.uniform(0, 6.3))) for _ in range(40)]
+    narrow = qx.run(gates, 1, "v3")
+    wide = qx.run(gates, n, "v3")
+    assert wide.rank_trace[-1] == narrow.rank_trace[-1] + [1] * (n - 1)
+    g, want = wide.final.generators[0], narrow.final.generators[0]
+    assert [int(v) for v in g.indices] == [int(v) * 4 ** (n - 1) for v in want.indices]
+    assert np.max(np.abs(g.lambdas - want.lambdas)) < 1e-12
+
+
 def test_limits_above_32_qubits():
     n = 36
     gates = [qx.Instruction("H", (0,)), qx.Instruction("RY", (0,), 0.3), qx.Instruction("CX", (0, 35))]
