@@ -21,6 +21,14 @@ while time.time() < t_end:
     if kind == 0:
         n = int(rng.choice([31, 32]))
         gates = workloads.near_clifford(n, int(rng.integers(20, 200)), int(rng.integers(0, 6)), int(rng.integers(0, 1 << 30)))
+    elif kind == 1:
+        # mid-size near-Clifford: Clifford base, a few rotations of any axis (quarter turns included)
+        n = int(rng.integers(12, 31))
+        gates = workloads.gen_random(n, int(rng.integers(50, 300)), rng, gates=("H", "S", "X", "SX", "CX"))
+        for _ in range(int(rng.integers(0, 9))):
+            theta = float(rng.choice([math.pi / 4, math.pi / 2, math.pi, -math.pi / 2, rng.uniform(0, 6.3)]))
+            rot = qx.Instruction(str(rng.choice(["RX", "RY", "RZ"])), (int(rng.integers(0, n)),), theta)
+            gates.insert(int(rng.integers(0, len(gates) + 1)), rot)
     else:
         n = int(rng.integers(1, 12))
         m = int(rng.integers(0, 70 if n <= 8 else 40))
