@@ -209,6 +209,12 @@ int qx_apply_operator_run_part(qx_store* s, const int32_t* counts, const int32_t
 int qx_operator_classes(int32_t n_qubits, const int32_t* counts, const int32_t* axes,
                         const double* weights, int32_t* class_id, int32_t* class_radix,
                         int32_t* class_axes, double* class_weights);
+/* Host-only: what the last bucketed operator step of this process did (csrc/bucket.cuh: the
+ * operator step of stabilizer.py:289-337 whose slots leave the kernel in canonical order, so that
+ * canonicalize's sort disappears).  out[0..7] = groups, tiles, buckets, slots of the largest
+ * bucket, slots, low key bits ranked inside a bucket, bucket capacity (0: the step did not
+ * qualify and the grouped step + sort ran), CTAs per SM. */
+int qx_bucket_last(int64_t out[8]);
 /* Number of raw branches the same call would produce per segment, nothing written
  * (branch_counts, stabilizer.py:232-237). */
 int qx_count_operator(qx_store* s, const int32_t* counts, int64_t* raw_per_segment);
@@ -283,7 +289,8 @@ typedef enum {
   QX_K_PARTITION = 10,
   QX_K_DENSE_PREP = 11,  /* grouped operator step: class words, source sort, group scan */
   QX_K_DENSE_EMIT = 12,  /* grouped operator step: one thread per output slot */
-  QX_K_CLASSES = 13
+  QX_K_BUCKET_EMIT = 13, /* bucketed operator step: slots computed, ranked and written in final order */
+  QX_K_CLASSES = 14
 } qx_kernel_class;
 int qx_profile_enable(int on);
 int qx_profile_reset(void);

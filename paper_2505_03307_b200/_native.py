@@ -24,7 +24,7 @@ QX_OK, QX_ERR_INVALID, QX_ERR_RESOURCE, QX_ERR_CUDA, QX_ERR_UNSUPPORTED, QX_ERR_
 KERNEL_CLASSES = (
     "clifford", "split", "expand_count", "expand_emit", "sort_hist", "sort_pass",
     "reduce", "small_merge", "readout_product", "readout_reduce", "partition",
-    "dense_prep", "dense_emit",
+    "dense_prep", "dense_emit", "bucket_emit",
 )
 
 _i32, _i64, _u32, _u64, _f64 = C.c_int32, C.c_int64, C.c_uint32, C.c_uint64, C.c_double
@@ -69,6 +69,7 @@ SIGNATURES = {
     "qx_count_operator": (C.c_int, [_p, _p, _p]),
     "qx_store_order_for_operator": (C.c_int, [_p, _p, C.c_int32]),
     "qx_operator_classes": (C.c_int, [_i32, _p, _p, _p, _p, _p, _p, _p]),
+    "qx_bucket_last": (C.c_int, [_P(_i64)]),
     "qx_merge": (C.c_int, [_p, _f64, _p]),
     "qx_sort": (C.c_int, [_p]),
     "qx_store_zi_sums": (C.c_int, [_p, _p]),

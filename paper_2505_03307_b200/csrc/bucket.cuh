@@ -1,0 +1,760 @@
+// a4 + a5 + a2 + a6 in ONE pass for operators whose groups are large boxes with few sources and
+// whose Clifford run leaves the high key bits independent of a block of low qubits: the
+// BUCKETED operator step.  The grouped step of dense.cu writes every kept slot once and then
+// sorts the result (four onesweep passes for 2n = 32: 96 bytes moved per term to place 12).
+// Here the slots leave the kernel already in canonical order, so the sort disappears.
+//
+// Reference semantics kept (bitwise): coefficient of a slot = sum over the group's sources, in
+// input order, of lambda * prod_j w_j with the factors taken qubit 0 first
+// (stabilizer.py:311-319); drop rule |sum| >= eps (stabilizer.py:336); ascending unique keys
+// (stabilizer.py:337).  The CX run behind the operator (stabilizer.py:340-363) is composed in
+// as images of the single-digit factors (expand.cuh).
+//
+// How.  A group (dense.cu) is a box: every non-identity digit of its class word picks one of the
+// class's output axes.  Split a group's digits into the tile-local ones L (a run of the LOWEST
+// digits, prod radix <= 729) and the high rest H.  A TILE is one choice of the H digits: <= 729
+// slots.  The output word of a slot is  image(H picks) ^ image(L picks)  (conjugation is linear
+// on the x/z bits), so if the images of the L digits only touch the low ELL bits of the word,
+// the TOP bits of every slot of a tile are known from its H picks alone.  Tiles that share
+// (generator, top bits) form a BUCKET; buckets in (generator, top) order are key ranges in
+// canonical order.  One CTA per bucket:
+//   1. for every tile of the bucket: mid table (the L digits above the lowest three, folded onto
+//      the tile's precomputed high word / high products), then one thread per slot: three
+//      multiplies per source, image composition, sign, drop rule; a kept slot sets bit
+//      (word & (2^ELL - 1)) of a bitmap in shared memory and parks (low bits, sum) in slot order;
+//   2. the keys of a generator's slots are DISTINCT (different groups never share an output
+//      word, slots of a group are different words, the run is a bijection), so the rank of a
+//      kept slot inside the bucket is the number of set bits below its own: one popcount scan
+//      of the bitmap, then rank = prefix[word] + popc(bits below) -- no comparison sort;
+//   3. the bucket's first output position comes from a decoupled look-back over the buckets in
+//      order (one 64-bit status word per bucket), so the output is written compact, coalesced,
+//      in final order, in the store's own format.
+// What does not qualify (a group with >= 64 sources -> factored sums of dense.cu; images of the
+// low digits that reach the top bits, e.g. a CX ladder running the other way; a bucket above
+// the shared-memory cap) takes the grouped step + sort of dense.cu; results are identical.
+#pragma once
+
+#include <stdlib.h>
+#include <string.h>
+
+#include <algorithm>
+#include <vector>
+
+#include "expand.cuh"
+#include "merge.cuh"
+
+namespace qxb {
+
+using namespace qxe;
+
+constexpr int kBThreads = 256;
+constexpr int kBWarps = kBThreads / 32;
+constexpr int kBRows = 3;                    // slots per thread per tile: tile <= kBRows * A
+constexpr int kNgCap = 4096;                 // groups the host plans
+constexpr int kMaxMid = 128;                 // mid entries per tile
+constexpr int kSrcChunk = 4;                 // sources folded per round
+constexpr int kPerThread = 12;               // parked slots per thread
+constexpr int kCapMax = kBThreads * kPerThread;   // slots per bucket (3072)
+constexpr int kSrcMax = 63;                  // sources per group (above: factored sums of dense.cu)
+constexpr int kTileIdBits = 40;
+
+template <typename K>
+struct __align__(16) BGroup {                // one per group, planned on the host
+  K cw;                // class word
+  K l_mask;            // support bits (even positions) of the tile-local digits
+  K h_mask;            // support bits of the high digits
+  u32 src0, n_src;     // its sorted sources
+  u32 seg;
+  u32 T;               // slots per tile
+  u32 Lw, n_mid;       // low branches (<= 27), mid entries
+  u32 pad;
+  u64 tile0;           // id of its first tile
+  u64 phi0;            // its first high product
+};
+
+template <typename K>
+struct __align__(16) TileDesc {
+  K word;              // image of the high picks
+  u32 e;               // its phase exponent
+  u32 group;
+};
+
+template <typename K> struct __align__(16) BMid {
+  K word;
+  u32 e;
+  u32 picks;           // two bits per mid digit
+};
+template <typename K> struct __align__(16) BLow {
+  K word;
+  K imx;
+  u32 e;
+  u32 picks;
+};
+
+// ---- tiles: high picks -> image word, bucket key, high products ------------------------------
+template <typename K>
+__global__ void __launch_bounds__(256)
+k_tile_desc(const BGroup<K>* __restrict__ groups, int ng, u64 n_tiles, const u64* __restrict__ skey,
+            const double* __restrict__ slam, TileDesc<K>* __restrict__ desc, double* __restrict__ phi,
+            u64* __restrict__ sort_key, double* __restrict__ sort_val, int ell, int top_bits,
+            const __grid_constant__ OperatorTable tb, const __grid_constant__ ImageTable<K> im) {
+  const u64 t = (u64)blockIdx.x * 256 + threadIdx.x;
+  if (t >= n_tiles) return;
+  int lo = 0, hi = ng;                          // groups[lo].tile0 <= t < groups[hi].tile0
+  while (hi - lo > 1) {
+    const int mid = (lo + hi) >> 1;
+    if (groups[mid].tile0 <= t) lo = mid; else hi = mid;
+  }
+  const BGroup<K> g = groups[lo];
+  u64 h = t - g.tile0;
+  const u64 h_index = h;
+  K picks = 0;                                  // two bits per high digit
+  for (K m = g.h_mask; m;) {
+    const int bit = KeyOps<K>::lowest(m);
+    m &= m - 1;
+    const u32 c = tb.cnt[bit >> 1][(u32)((g.cw >> bit) & 3u) - 1u];
+    const u32 pick = (u32)(h % c);
+    h /= c;
+    picks |= (K)pick << bit;
+  }
+  K word = 0;
+  u32 e = 0;
+  for (K m = g.h_mask; m;) {                    // qubit 0 first (stabilizer.py:311-319)
+    const int bit = KeyOps<K>::highest(m);
+    m ^= (K)1 << bit;
+    const u32 ax = tb.axis[bit >> 1][(u32)((g.cw >> bit) & 3u) - 1u][(u32)(picks >> bit) & 3u];
+    compose<K>(word, e, im.img[bit >> 1][ax - 1], im.imx[bit >> 1][ax - 1], im.e[bit >> 1][ax - 1]);
+  }
+  TileDesc<K> d;
+  d.word = word;
+  d.e = e & 3u;
+  d.group = (u32)lo;
+  desc[t] = d;
+  for (u32 s = 0; s < g.n_src; ++s) {
+    const K key = (K)skey[g.src0 + s];
+    double v = slam[g.src0 + s];
+    for (K m = g.h_mask; m;) {
+      const int bit = KeyOps<K>::highest(m);
+      m ^= (K)1 << bit;
+      v = __dmul_rn(v, tb.w[bit >> 1][(u32)((key >> bit) & 3u) - 1u][(u32)(picks >> bit) & 3u]);
+    }
+    phi[g.phi0 + h_index * g.n_src + s] = v;
+  }
+  sort_key[t] = ((u64)g.seg << top_bits) | (u64)(word >> ell);
+  sort_val[t] = __longlong_as_double((long long)(t | ((u64)g.T << kTileIdBits)));
+}
+
+// ---- buckets: heads of runs of equal (generator, top) among the sorted tiles ---------------------
+//   unit_tile0[u] = first sorted tile of bucket u        (unit_tile0[NU] = n_tiles)
+//   seg_first[g]  = first bucket of generator g          (untouched for a generator without slots)
+//   info[0] = NU, info[1] = largest bucket (slots)
+__global__ void __launch_bounds__(256)
+k_unit_scan(const u64* __restrict__ sort_key, const double* __restrict__ sort_val, u64 n_tiles, int top_bits,
+            u32* __restrict__ unit_tile0, u32* __restrict__ seg_first, u64* __restrict__ status,
+            u64* __restrict__ info) {
+  __shared__ u64 s_scan[kBWarps + 1];
+  __shared__ u64 s_base;
+  const int tile = (int)blockIdx.x;
+  constexpr int kPer = 8;
+  const int warp = threadIdx.x >> 5, lane = lane_id();
+  const u64 wbase = (u64)tile * (256 * kPer) + (u64)warp * (32 * kPer);
+  u32 pre[kPer];
+  u32 flags = 0, run = 0;
+#pragma unroll
+  for (int k = 0; k < kPer; ++k) {
+    const u64 i = wbase + k * 32 + lane;
+    bool head = false;
+    if (i < n_tiles) {
+      const u64 key = sort_key[i];
+      head = i == 0 || sort_key[i - 1] != key;
+      if (head) flags |= 1u << k;
+      if (i == 0 || (sort_key[i - 1] >> top_bits) != (key >> top_bits)) flags |= 1u << (8 + k);
+    }
+    const u32 votes = __ballot_sync(QX_FULL_MASK, head);
+    pre[k] = run + __popc(votes & lanemask_lt());
+    run += __popc(votes);
+  }
+  u64 tot;
+  u64 wex = block_exclusive_sum<u64>(lane == 0 ? (u64)run : 0ull, s_scan, tot);
+  wex = __shfl_sync(QX_FULL_MASK, wex, 0);
+  if (warp == 0) {
+    const u64 ex = lookback_exclusive(status, tile, tot);
+    if (lane == 0) s_base = ex;
+  }
+  __syncthreads();
+  const u64 base = s_base + wex;
+#pragma unroll
+  for (int k = 0; k < kPer; ++k) {
+    const u64 i = wbase + k * 32 + lane;
+    if (flags & (1u << k)) unit_tile0[base + pre[k]] = (u32)i;
+    if (flags & (1u << (8 + k))) seg_first[(u32)(sort_key[i] >> top_bits)] = (u32)(base + pre[k]);
+  }
+  if ((u64)(tile + 1) * (256 * kPer) >= n_tiles && threadIdx.x == 0) {
+    const u64 nu = s_base + tot;
+    unit_tile0[nu] = (u32)n_tiles;
+    info[0] = nu;
+  }
+}
+
+__global__ void k_unit_sizes(const u32* __restrict__ unit_tile0, const double* __restrict__ sort_val,
+                             u64* __restrict__ info) {
+  const u64 nu = info[0];
+  u32 worst = 0;
+  for (u64 u = (u64)blockIdx.x * blockDim.x + threadIdx.x; u < nu; u += (u64)gridDim.x * blockDim.x) {
+    u32 slots = 0;
+    for (u32 i = unit_tile0[u]; i < unit_tile0[u + 1]; ++i)
+      slots += (u32)((u64)__double_as_longlong(sort_val[i]) >> kTileIdBits);
+    worst = max(worst, slots);
+  }
+  worst = __reduce_max_sync(QX_FULL_MASK, worst);
+  if (lane_id() == 0 && worst) atomicMax(reinterpret_cast<unsigned long long*>(info + 1), (unsigned long long)worst);
+}
+
+// generator offsets of the compact output from the inclusive prefixes the buckets left behind
+__global__ void k_bucket_offsets(const u64* __restrict__ status, u32* __restrict__ seg_first, int n_seg,
+                                 u32 u_lo, u32 u_hi, u32 n_units, int64_t* __restrict__ seg_out) {
+  if (blockIdx.x != 0 || threadIdx.x != 0) return;
+  u32 next = n_units;
+  for (int g = n_seg - 1; g >= 0; --g) {
+    if (seg_first[g] == 0xffffffffu) seg_first[g] = next;
+    else next = seg_first[g];
+  }
+  for (int g = 0; g <= n_seg; ++g) {
+    u32 u = g < n_seg ? seg_first[g] : n_units;
+    u = min(max(u, u_lo), u_hi);
+    seg_out[g] = u == u_lo ? 0 : (int64_t)(status[u - 1 - u_lo] & QX_LB_VAL);
+  }
+}
+
+// ---- the bucket kernel ---------------------------------------------------------------------------
+template <typename K>
+struct BSmem {
+  OperatorTable tb;                  // class-expanded (dense.cu build_class_table)
+  ImageTable<K> im;
+  BLow<K> low[27];
+  BMid<K> mid[kMaxMid];
+  double low_w[kSrcChunk][27][4];    // [source of the round][low branch][low digit]
+  double p_mid[kSrcChunk * kMaxMid]; // [source of the round][mid entry]: lambda * high * mid weights
+  u64 scan[kBWarps + 1];
+  u64 base;
+  u32 unit;
+  u32 kept;
+};
+
+inline size_t bucket_smem_bytes(size_t fixed, int ell, int cap) {
+  const size_t words = (size_t)1 << (ell - 5);
+  return fixed + 4 * words + 2 * words + 8 * (size_t)cap + 2 * (size_t)cap + 64;
+}
+
+template <typename K, typename KO>
+__global__ void __launch_bounds__(kBThreads, 4)
+k_bucket_emit(const BGroup<K>* __restrict__ groups, const TileDesc<K>* __restrict__ desc,
+              const double* __restrict__ phi, const u64* __restrict__ sort_key,
+              const double* __restrict__ sort_val, const u32* __restrict__ unit_tile0, u32 u_lo, u32 u_hi,
+              const u64* __restrict__ skey, const double* __restrict__ slam, KO* __restrict__ keys_out,
+              double* __restrict__ lam_out, u64* __restrict__ status, u32* __restrict__ ticket, int ell,
+              int top_bits, int cap, double eps, const __grid_constant__ OperatorTable tb,
+              const __grid_constant__ ImageTable<K> im) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  BSmem<K>& sm = *reinterpret_cast<BSmem<K>*>(smem_raw);
+  const int words = 1 << (ell - 5);
+  double* st_lam = reinterpret_cast<double*>(smem_raw + ((sizeof(BSmem<K>) + 15) & ~(size_t)15));
+  u32* bitmap = reinterpret_cast<u32*>(st_lam + cap);
+  unsigned short* prefix = reinterpret_cast<unsigned short*>(bitmap + words);
+  unsigned short* st_key = prefix + words;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = lane_id();
+  {
+    const u32* src = reinterpret_cast<const u32*>(&tb);
+    u32* dst = reinterpret_cast<u32*>(&sm.tb);
+    for (int i = tid; i < (int)(sizeof(OperatorTable) / 4); i += kBThreads) dst[i] = src[i];
+    const u32* isrc = reinterpret_cast<const u32*>(&im);
+    u32* idst = reinterpret_cast<u32*>(&sm.im);
+    for (int i = tid; i < (int)(sizeof(ImageTable<K>) / 4); i += kBThreads) idst[i] = isrc[i];
+  }
+  const K low_bits = (K)(((u64)1 << ell) - 1);
+  int cached_group = -1;
+  // per-group state in registers: digit positions of the low three and the mid digits
+  int lbit[3] = {-1, -1, -1};
+  u32 lrad[3] = {1, 1, 1};
+  K mid_mask = 0, cwg = 0;
+  u32 Lw = 1, n_mid = 1, bpr = kBThreads, A = kBThreads, n_src = 0, src0 = 0, T = 0;
+  u64 phi0 = 0, tile0 = 0;
+  u32 my_bl = 0, my_m0 = 0;
+
+  for (;;) {
+    __syncthreads();                              // previous bucket written out (and tables copied)
+    if (tid == 0) sm.unit = u_lo + atomicAdd(ticket, 1u);
+    __syncthreads();
+    const u32 unit = sm.unit;
+    if (unit >= u_hi) break;
+    const u32 t_begin = unit_tile0[unit], t_end = unit_tile0[unit + 1];
+    const u64 bucket = sort_key[t_begin];
+    for (int i = tid; i < words; i += kBThreads) bitmap[i] = 0u;
+    u32 parked = 0;                               // slots of the bucket so far
+
+    for (u32 ti = t_begin; ti < t_end; ++ti) {
+      const u64 tile = (u64)__double_as_longlong(sort_val[ti]) & (((u64)1 << kTileIdBits) - 1);
+      const TileDesc<K> td = desc[tile];
+      __syncthreads();                            // previous tile's tables consumed; bitmap cleared
+      if ((int)td.group != cached_group) {
+        const BGroup<K> g = groups[td.group];
+        cached_group = (int)td.group;
+        cwg = g.cw;
+        n_src = g.n_src;
+        src0 = g.src0;
+        T = g.T;
+        Lw = g.Lw;
+        n_mid = g.n_mid;
+        phi0 = g.phi0;
+        tile0 = g.tile0;
+        K m = g.l_mask;
+#pragma unroll
+        for (int j = 0; j < 3; ++j) {
+          lbit[j] = -1;
+          lrad[j] = 1;
+          if (m) {
+            lbit[j] = KeyOps<K>::lowest(m);
+            m &= m - 1;
+            lrad[j] = sm.tb.cnt[lbit[j] >> 1][(u32)((cwg >> lbit[j]) & 3u) - 1u];
+          }
+        }
+        mid_mask = m;
+        bpr = (u32)kBThreads / Lw;                // mid entries per row
+        A = bpr * Lw;                             // slots per row
+        my_m0 = (u32)tid / Lw;
+        my_bl = (u32)tid - my_m0 * Lw;
+        if ((u32)tid < Lw) {                      // low branches of the group
+          u32 b = (u32)tid, picks = 0;
+          K w = 0;
+          u32 ex = 0;
+          u32 pick[3];
+#pragma unroll
+          for (int j = 0; j < 3; ++j) {
+            pick[j] = b % lrad[j];
+            b /= lrad[j];
+            picks |= pick[j] << (2 * j);
+          }
+#pragma unroll
+          for (int j = 2; j >= 0; --j) {
+            if (lbit[j] >= 0) {
+              const int p = lbit[j] >> 1;
+              const u32 ax = sm.tb.axis[p][(u32)((cwg >> lbit[j]) & 3u) - 1u][pick[j]];
+              compose<K>(w, ex, sm.im.img[p][ax - 1], sm.im.imx[p][ax - 1], sm.im.e[p][ax - 1]);
+            }
+          }
+          BLow<K> le;
+          le.word = w;
+          le.imx = (w ^ (w >> 1)) & Plane<K>::lo;
+          le.e = ex & 3u;
+          le.picks = picks;
+          sm.low[tid] = le;
+        }
+      }
+      const u64 h_index = tile - tile0;
+      // mid entries: the tile's high word with the mid picks composed in
+      if ((u32)tid < n_mid) {
+        u32 b = (u32)tid, picks = 0;
+        int idx = 0;
+        for (K m = mid_mask; m; ++idx) {
+          const int bit = KeyOps<K>::lowest(m);
+          m &= m - 1;
+          const u32 c = sm.tb.cnt[bit >> 1][(u32)((cwg >> bit) & 3u) - 1u];
+          const u32 q = b / c;
+          picks |= (b - q * c) << (2 * idx);
+          b = q;
+        }
+        K w = td.word;
+        u32 ex = td.e;
+        idx = (int)Plane<K>::popc(mid_mask) - 1;
+        for (K m = mid_mask; m; --idx) {
+          const int bit = KeyOps<K>::highest(m);
+          m ^= (K)1 << bit;
+          const u32 ax = sm.tb.axis[bit >> 1][(u32)((cwg >> bit) & 3u) - 1u][(picks >> (2 * idx)) & 3u];
+          compose<K>(w, ex, sm.im.img[bit >> 1][ax - 1], sm.im.imx[bit >> 1][ax - 1], sm.im.e[bit >> 1][ax - 1]);
+        }
+        BMid<K> me;
+        me.word = w;
+        me.e = ex & 3u;
+        me.picks = picks;
+        sm.mid[tid] = me;
+      }
+      double acc[kBRows];
+#pragma unroll
+      for (int k = 0; k < kBRows; ++k) acc[k] = 0.0;
+      u32 live = 0;
+      if ((u32)tid < A) {
+#pragma unroll
+        for (int k = 0; k < kBRows; ++k)
+          if (my_m0 + (u32)k * bpr < n_mid) live |= 1u << k;
+      }
+      // sources, kSrcChunk per round, in input order
+      for (u32 c0 = 0; c0 < n_src; c0 += kSrcChunk) {
+        const u32 nc = min((u32)kSrcChunk, n_src - c0);
+        __syncthreads();                          // mid picks written; previous round consumed
+        for (u32 w = (u32)tid; w < nc * n_mid; w += kBThreads) {
+          const u32 c = w / n_mid, m = w - c * n_mid;
+          const K key = (K)skey[src0 + c0 + c];
+          const u32 picks = sm.mid[m].picks;
+          double v = phi[phi0 + h_index * n_src + c0 + c];
+          int idx = (int)Plane<K>::popc(mid_mask) - 1;
+          for (K mm = mid_mask; mm; --idx) {      // qubit 0 first
+            const int bit = KeyOps<K>::highest(mm);
+            mm ^= (K)1 << bit;
+            v = __dmul_rn(v, sm.tb.w[bit >> 1][(u32)((key >> bit) & 3u) - 1u][(picks >> (2 * idx)) & 3u]);
+          }
+          sm.p_mid[c * kMaxMid + m] = v;
+        }
+        for (u32 w = (u32)tid; w < nc * Lw; w += kBThreads) {
+          const u32 c = w / Lw, l = w - c * Lw;
+          const K key = (K)skey[src0 + c0 + c];
+          const u32 picks = sm.low[l].picks;
+#pragma unroll
+          for (int j = 0; j < 3; ++j) {
+            double wt = 1.0;
+            if (lbit[j] >= 0)
+              wt = sm.tb.w[lbit[j] >> 1][(u32)((key >> lbit[j]) & 3u) - 1u][(picks >> (2 * j)) & 3u];
+            sm.low_w[c][l][j] = wt;
+          }
+        }
+        __syncthreads();
+        if (live) {
+          for (u32 c = 0; c < nc; ++c) {
+            const double2 w01 = *reinterpret_cast<const double2*>(&sm.low_w[c][my_bl][0]);
+            const double w2 = sm.low_w[c][my_bl][2];
+            const double* pm = sm.p_mid + c * kMaxMid + my_m0;
+            const bool first = c0 + c == 0;
+#pragma unroll
+            for (int k = 0; k < kBRows; ++k) {
+              if (live & (1u << k)) {
+                // ((p * w2) * w1) * w0 with explicit roundings: no fused multiply-add into the sum
+                double v = __dmul_rn(pm[(u32)k * bpr], w2);
+                v = __dmul_rn(v, w01.y);
+                v = __dmul_rn(v, w01.x);
+                acc[k] = first ? v : __dadd_rn(acc[k], v);
+              }
+            }
+          }
+        }
+      }
+      // words, signs, drop rule; kept slots mark the bitmap; every slot is parked in slot order
+      if (live) {
+        const BLow<K> le = sm.low[my_bl];
+#pragma unroll
+        for (int k = 0; k < kBRows; ++k) {
+          if (live & (1u << k)) {
+            const u32 m = my_m0 + (u32)k * bpr;
+            const BMid<K> me = sm.mid[m];
+            K out = me.word;
+            u32 ex = me.e;
+            compose<K>(out, ex, le.word, le.imx, le.e);
+            double v = acc[k];
+            if (composed_sign<K>(out, ex)) v = -v;            // sign flips are exact
+            const u32 y = (u32)(out & low_bits);
+            const bool kept = fabs(v) >= eps;
+            if (kept) atomicOr(&bitmap[y >> 5], 1u << (y & 31u));
+            const u32 at = parked + m * Lw + my_bl;
+            st_key[at] = (unsigned short)y;
+            st_lam[at] = kept ? v : 0.0;                       // eps > 0: a kept sum is never 0
+          }
+        }
+      }
+      parked += T;
+    }
+    __syncthreads();
+    // ranks: popcount scan of the bitmap
+    {
+      const int per = max(1, words / kBThreads);
+      const int w0 = tid * per;
+      u32 cnt = 0;
+      if (w0 < words)
+        for (int i = 0; i < per; ++i) cnt += __popc(bitmap[w0 + i]);
+      u64 total;
+      u64 ex = block_exclusive_sum<u64>((u64)cnt, sm.scan, total);
+      if (w0 < words) {
+        u32 run = (u32)ex;
+        for (int i = 0; i < per; ++i) {
+          prefix[w0 + i] = (unsigned short)run;
+          run += __popc(bitmap[w0 + i]);
+        }
+      }
+      if (tid == 0) sm.kept = (u32)total;
+    }
+    __syncthreads();
+    const u32 kept_total = sm.kept;
+    if (warp == 0) {
+      const u64 ex = lookback_exclusive(status, (int)(unit - u_lo), (u64)kept_total);
+      if (lane == 0) sm.base = ex;
+    }
+    // parked slots -> rank order, in place through registers
+    unsigned short rk[kPerThread];
+    double rl[kPerThread];
+#pragma unroll
+    for (int j = 0; j < kPerThread; ++j) {
+      const u32 i = (u32)tid + (u32)j * kBThreads;
+      rl[j] = 0.0;
+      rk[j] = 0;
+      if (i < parked) {
+        rl[j] = st_lam[i];
+        rk[j] = st_key[i];
+      }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int j = 0; j < kPerThread; ++j) {
+      if (rl[j] != 0.0) {
+        const u32 y = rk[j];
+        const u32 r = (u32)prefix[y >> 5] + __popc(bitmap[y >> 5] & ((1u << (y & 31u)) - 1u));
+        st_key[r] = rk[j];
+        st_lam[r] = rl[j];
+      }
+    }
+    __syncthreads();
+    const int64_t base = (int64_t)sm.base;
+    const u64 top = (bucket & (((u64)1 << top_bits) - 1)) << ell;
+    for (u32 r = (u32)tid; r < kept_total; r += kBThreads) {
+      st_stream(keys_out + base + r, (KO)(top | (u64)st_key[r]));
+      st_stream(lam_out + base + r, st_lam[r]);
+    }
+  }
+}
+
+
+// ---- host side -------------------------------------------------------------------------------------
+template <typename T>
+inline T* bcarve(char*& cursor, int64_t count) {
+  T* p = reinterpret_cast<T*>(cursor);
+  cursor += (sizeof(T) * (size_t)count + 255) / 256 * 256;
+  return p;
+}
+inline int64_t bpadded(int64_t bytes) { return (bytes + 255) / 256 * 256; }
+
+struct BucketStats {           // what the last bucketed step did (qx_bucket_last, tools and tests)
+  int64_t groups, tiles, units, max_unit, slots;
+  int ell, cap, ctas_per_sm;
+};
+inline BucketStats& bucket_stats() {
+  static BucketStats st = {};
+  return st;
+}
+
+// Plan the groups for `ell` low bits.  Returns false if the operator does not qualify.
+template <typename K>
+bool plan_groups(int n_qubits, int n_seg, int ell, const OperatorTable& ct, const ImageTable<K>& im, int ng,
+                 const u64* h_cw, const u64* h_gsrc, const u64* h_gslot, const int64_t* h_seg_slot,
+                 std::vector<BGroup<K>>& out, u64* n_tiles, u64* n_phi) {
+  out.resize((size_t)ng + 1);
+  u64 tiles = 0, phis = 0;
+  int seg = 0;
+  for (int g = 0; g < ng; ++g) {
+    BGroup<K> d;
+    memset(&d, 0, sizeof(d));
+    const K cw = (K)h_cw[g];
+    const u64 n_src = h_gsrc[g + 1] - h_gsrc[g];
+    const u64 slots = h_gslot[g + 1] - h_gslot[g];
+    if (n_src == 0 || n_src > (u64)kSrcMax || slots == 0) return false;
+    while (seg + 1 < n_seg && (u64)h_seg_slot[seg + 1] <= h_gslot[g]) ++seg;
+    u32 T = 1, Lw = 1, n_mid = 1;
+    int nl = 0;
+    K l_mask = 0, h_mask = 0;
+    bool open = true;
+    for (int p = 0; p < n_qubits; ++p) {
+      const u32 cls = (u32)((cw >> (2 * p)) & 3u);
+      if (!cls) continue;
+      const u32 radix = ct.cnt[p][cls - 1];
+      if (open) {
+        K infl = 0;
+        for (u32 c = 0; c < radix; ++c) infl |= im.img[p][ct.axis[p][cls - 1][c] - 1];
+        bool fits = ell >= (int)(8 * sizeof(K)) || (infl >> ell) == 0;
+        if (fits) {
+          if (nl < 3) {
+            Lw *= radix;
+          } else {
+            const u32 nm = n_mid * radix;
+            if (nm > (u32)kMaxMid || nm > (u32)kBRows * ((u32)kBThreads / Lw)) fits = false;
+            else n_mid = nm;
+          }
+        }
+        if (fits) {
+          T *= radix;
+          ++nl;
+          l_mask |= (K)1 << (2 * p);
+          continue;
+        }
+        open = false;
+      }
+      h_mask |= (K)1 << (2 * p);
+    }
+    d.cw = cw;
+    d.l_mask = l_mask;
+    d.h_mask = h_mask;
+    d.src0 = (u32)h_gsrc[g];
+    d.n_src = (u32)n_src;
+    d.seg = (u32)seg;
+    d.T = T;
+    d.Lw = Lw;
+    d.n_mid = n_mid;
+    d.tile0 = tiles;
+    d.phi0 = phis;
+    out[g] = d;
+    tiles += slots / T;
+    phis += (slots / T) * n_src;
+  }
+  BGroup<K> end;
+  memset(&end, 0, sizeof(end));
+  end.tile0 = tiles;
+  end.phi0 = phis;
+  out[ng] = end;
+  *n_tiles = tiles;
+  *n_phi = phis;
+  return true;
+}
+
+// The bucketed step.  On entry: sorted sources in skey/slam, groups on the host (class word, first
+// source, first slot; ng + 1 entries of gsrc/gslot), slot offsets of the generators on the host,
+// the output buffer `out` of the store can hold `total` terms.  *handled = false: nothing was
+// written, take the grouped step + sort.  On success the store's buffer `out` holds the
+// canonical result of this part and s->seg[out] its offsets.
+template <typename K>
+int bucket_step(qx_store* s, const OperatorTable& ct, const ImageTable<K>& im, int ng, const u64* h_cw,
+                const u64* h_gsrc, const u64* h_gslot, const int64_t* h_seg_slot, int64_t total,
+                const u64* skey, const double* slam, int64_t n_sources, int out, bool narrow_out, double eps,
+                int part, int parts, bool* handled) {
+  *handled = false;
+  static const int env_ell = getenv("QX_BUCKET_ELL") ? atoi(getenv("QX_BUCKET_ELL")) : 14;
+  const int n_seg = s->n_seg;
+  const int ell = std::min(std::max(env_ell, 5), 16);
+  const int top_bits = 2 * s->n_qubits - ell;
+  if (top_bits <= 0 || ng <= 0 || ng > kNgCap || total <= 0) return QX_OK;
+  int seg_bits = 1;
+  while ((1ll << seg_bits) < n_seg) ++seg_bits;
+  if (top_bits + seg_bits > 62) return QX_OK;
+  std::vector<BGroup<K>> groups;
+  u64 n_tiles = 0, n_phi = 0;
+  if (!plan_groups<K>(s->n_qubits, n_seg, ell, ct, im, ng, h_cw, h_gsrc, h_gslot, h_seg_slot, groups, &n_tiles, &n_phi))
+    return QX_OK;
+  // tiles must be worth a CTA's while, and their ids must fit the payload of the tile sort
+  if (n_tiles == 0 || n_tiles >= (1ull << 31) || (u64)total < 128 * n_tiles || n_phi > (1ull << 28)) return QX_OK;
+
+  const int64_t scan_tiles = (int64_t)((n_tiles + 2047) / 2048);
+  const int64_t bytes = bpadded((int64_t)sizeof(BGroup<K>) * (ng + 1)) + bpadded((int64_t)sizeof(TileDesc<K>) * (int64_t)n_tiles) +
+                        bpadded(8 * (int64_t)n_phi) + 4 * bpadded(8 * (int64_t)n_tiles) + 2 * 256 +
+                        bpadded(4 * ((int64_t)n_tiles + 1)) + bpadded(4 * (int64_t)n_seg) +
+                        bpadded(8 * (scan_tiles + 1)) + 256 + bpadded(8 * ((int64_t)n_tiles + 1)) + 256;
+  void* block = nullptr;
+  QX_TRY(qx_dev_alloc(&block, bytes, s->stream, s->device));
+  struct Release {
+    void* p;
+    cudaStream_t st;
+    ~Release() { qx_dev_free(p, st); }
+  } rel{block, s->stream};
+  char* cur = reinterpret_cast<char*>(block);
+  BGroup<K>* d_groups = bcarve<BGroup<K>>(cur, ng + 1);
+  TileDesc<K>* d_desc = bcarve<TileDesc<K>>(cur, (int64_t)n_tiles);
+  double* d_phi = bcarve<double>(cur, (int64_t)n_phi);
+  u64* skeys[2] = {bcarve<u64>(cur, (int64_t)n_tiles), bcarve<u64>(cur, (int64_t)n_tiles)};
+  double* svals[2] = {bcarve<double>(cur, (int64_t)n_tiles), bcarve<double>(cur, (int64_t)n_tiles)};
+  int64_t* sseg[2] = {bcarve<int64_t>(cur, 2), bcarve<int64_t>(cur, 2)};
+  u32* unit_tile0 = bcarve<u32>(cur, (int64_t)n_tiles + 1);
+  u32* seg_first = bcarve<u32>(cur, n_seg);
+  u64* scan_status = bcarve<u64>(cur, scan_tiles + 1);
+  u64* info = bcarve<u64>(cur, 2);
+  u64* unit_status = bcarve<u64>(cur, (int64_t)n_tiles + 1);
+  u32* ticket = bcarve<u32>(cur, 2);
+
+  // groups and the offsets of the one-segment tile sort: host -> device through pinned staging
+  const int64_t stage_bytes = (int64_t)sizeof(BGroup<K>) * (ng + 1) + 16;
+  void* h_stage = nullptr;
+  QX_TRY(qx_pinned_alloc(&h_stage, stage_bytes));
+  struct ReleasePinned {
+    void* p;
+    ~ReleasePinned() { qx_pinned_free(p); }
+  } relp{h_stage};
+  memcpy(h_stage, groups.data(), sizeof(BGroup<K>) * (size_t)(ng + 1));
+  int64_t* h_off = reinterpret_cast<int64_t*>(reinterpret_cast<char*>(h_stage) + sizeof(BGroup<K>) * (size_t)(ng + 1));
+  h_off[0] = 0;
+  h_off[1] = (int64_t)n_tiles;
+  QX_CUDA(cudaMemcpyAsync(d_groups, h_stage, sizeof(BGroup<K>) * (size_t)(ng + 1), cudaMemcpyHostToDevice, s->stream));
+  QX_CUDA(cudaMemcpyAsync(sseg[0], h_off, 16, cudaMemcpyHostToDevice, s->stream));
+  QX_CUDA(cudaMemsetAsync(seg_first, 0xff, 4 * (size_t)n_seg, s->stream));
+  QX_CUDA(cudaMemsetAsync(scan_status, 0, (size_t)(reinterpret_cast<char*>(ticket) + 256 - reinterpret_cast<char*>(scan_status)),
+                          s->stream));
+  int sorted = 0;
+  {
+    QxProfileScope prof(QX_K_DENSE_PREP, s->stream, 48.0 * (double)n_tiles + 16.0 * (double)n_sources);
+    k_tile_desc<K><<<(unsigned)((n_tiles + 255) / 256), 256, 0, s->stream>>>(
+        d_groups, ng, n_tiles, skey, slam, d_desc, d_phi, skeys[0], svals[0], ell, top_bits, ct, im);
+    QX_CUDA(cudaGetLastError());
+  }
+  {
+    // tiles into (generator, top bits) order: the merge's own onesweep, sort only, one segment
+    qxm::MergeBuffers<double> mb;
+    for (int b = 0; b < 2; ++b) {
+      mb.keys[b] = skeys[b];
+      mb.vals[b] = svals[b];
+      mb.seg[b] = sseg[b];
+    }
+    mb.cur = 0;
+    mb.n_seg = 1;
+    mb.ub_total = (int64_t)n_tiles;
+    mb.ub_seg = (int64_t)n_tiles;
+    QX_TRY((qxm::merge_large<double, u64>(s, mb, 0.0, QX_K_REDUCE, false, QX_K_DENSE_PREP, QX_K_DENSE_PREP, nullptr,
+                                          nullptr, true, nullptr, top_bits + seg_bits)));
+    sorted = mb.cur;
+  }
+  {
+    QxProfileScope prof(QX_K_DENSE_PREP, s->stream, 20.0 * (double)n_tiles, 2);
+    k_unit_scan<<<(unsigned)scan_tiles, 256, 0, s->stream>>>(skeys[sorted], svals[sorted], n_tiles, top_bits,
+                                                            unit_tile0, seg_first, scan_status, info);
+    QX_CUDA(cudaGetLastError());
+    k_unit_sizes<<<(unsigned)std::max<int64_t>(1, std::min<int64_t>(((int64_t)n_tiles + 255) / 256, 1024)), 256, 0, s->stream>>>(
+        unit_tile0, svals[sorted], info);
+    QX_CUDA(cudaGetLastError());
+  }
+  QX_TRY(qx_readback(s->stream, s->h_pinned, reinterpret_cast<const int64_t*>(info), 2));
+  QX_CUDA(cudaStreamSynchronize(s->stream));
+  const int64_t n_units = s->h_pinned[0], max_unit = s->h_pinned[1];
+  BucketStats& st = bucket_stats();
+  st.groups = ng;
+  st.tiles = (int64_t)n_tiles;
+  st.units = n_units;
+  st.max_unit = max_unit;
+  st.slots = total;
+  st.ell = ell;
+  st.cap = 0;
+  st.ctas_per_sm = 0;
+  if (n_units <= 0 || max_unit > kCapMax) return QX_OK;
+  const int cap = (int)std::max<int64_t>(256, (max_unit + 255) / 256 * 256);
+  const size_t fixed = (sizeof(BSmem<K>) + 15) & ~(size_t)15;
+  const size_t smem = bucket_smem_bytes(fixed, ell, cap);
+  const u32 u_lo = (u32)(n_units * part / parts), u_hi = (u32)(n_units * (part + 1) / parts);
+  int per_sm = 0;
+  auto launch = [&](auto kernel, auto* keys_out) -> int {
+    QX_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    QX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, kBThreads, smem));
+    per_sm = std::max(per_sm, 1);
+    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)u_hi - u_lo, (int64_t)s->sm_count * per_sm));
+    kernel<<<grid, kBThreads, smem, s->stream>>>(d_groups, d_desc, d_phi, skeys[sorted], svals[sorted], unit_tile0,
+                                                  u_lo, u_hi, skey, slam, keys_out, s->lam[out], unit_status, ticket,
+                                                  ell, top_bits, cap, eps, ct, im);
+    QX_CUDA(cudaGetLastError());
+    return QX_OK;
+  };
+  {
+    QxProfileScope prof(QX_K_BUCKET_EMIT, s->stream, 16.0 * (double)n_sources + (narrow_out ? 12.0 : 16.0) * (double)total);
+    if (narrow_out) {
+      if constexpr (sizeof(K) == 4) QX_TRY(launch(k_bucket_emit<K, u32>, reinterpret_cast<u32*>(s->keys[out])));
+      else return qx_fail(QX_ERR_CONSISTENCY, "narrow output needs 32-bit working keys (internal error)");
+    } else {
+      QX_TRY(launch(k_bucket_emit<K, u64>, reinterpret_cast<u64*>(s->keys[out])));
+    }
+  }
+  k_bucket_offsets<<<1, 32, 0, s->stream>>>(unit_status, seg_first, n_seg, u_lo, u_hi, (u32)n_units, s->seg[out]);
+  qx_count_launches(1);
+  QX_CUDA(cudaGetLastError());
+  st.cap = cap;
+  st.ctas_per_sm = per_sm;
+  *handled = true;
+  return QX_OK;
+}
+
+}  // namespace qxb

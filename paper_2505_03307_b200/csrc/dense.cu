@@ -31,6 +31,7 @@
 
 #include <algorithm>
 
+#include "bucket.cuh"
 #include "expand.cuh"
 #include "merge.cuh"
 
@@ -288,6 +289,25 @@ __global__ void k_tile_groups(const u64* __restrict__ gslot, const u64* __restri
     const u64 r0 = (u64)t * kTileSlots;
     tile_info[t] = make_int2((int)last_le(gslot, (int64_t)totals[0], r0), segment_of(seg_slot, n_seg, (int64_t)r0));
   }
+}
+
+// groups -> page-locked host memory for the planner of the bucketed step (bucket.cuh):
+// [0] = groups, [1] = slots, then class word / first source / first slot of up to `cap` groups
+__global__ void k_group_export(const u64* __restrict__ cw, const u64* __restrict__ gsrc, const u64* __restrict__ gslot,
+                               const u64* __restrict__ totals, u64* __restrict__ host, int cap) {
+  const u64 ng = totals[0];
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i == 0) {
+    host[0] = ng;
+    host[1] = totals[1];
+  }
+  if (ng > (u64)cap || (u64)i > ng) return;
+  u64* h_cw = host + 2;
+  u64* h_src = h_cw + (cap + 1);
+  u64* h_slot = h_src + (cap + 1);
+  h_src[i] = gsrc[i];
+  h_slot[i] = gslot[i];
+  h_cw[i] = (u64)i < ng ? cw[gsrc[i]] : 0ull;
 }
 
 // kept counts -> compact offsets (n_seg is small: one thread)
@@ -969,6 +989,20 @@ extern "C" int qx_operator_classes(int32_t n_qubits, const int32_t* counts, cons
   return QX_OK;
 }
 
+extern "C" int qx_bucket_last(int64_t out[8]) {
+  QX_REQUIRE(out != nullptr, "NULL argument");
+  const qxb::BucketStats& st = qxb::bucket_stats();
+  out[0] = st.groups;
+  out[1] = st.tiles;
+  out[2] = st.units;
+  out[3] = st.max_unit;
+  out[4] = st.slots;
+  out[5] = st.ell;
+  out[6] = st.cap;
+  out[7] = st.ctas_per_sm;
+  return QX_OK;
+}
+
 // The large operator step.  On entry the store holds the merged input terms (exact offsets on
 // the host); on exit it holds the canonical result and exact offsets.  `nz` is the operator's
 // non-zero branch table (fill_table in branch.cu).
@@ -1053,7 +1087,23 @@ int qx_dense_operator_step(qx_store* s, const OperatorTable& nz, const uint32_t*
       QX_CUDA(cudaGetLastError());
     }
   }
-  // slot offsets of the generators + totals -> host (sizes the output)
+  // slot offsets of the generators + totals -> host (sizes the output); the groups go along for
+  // the planner of the bucketed step
+  static const bool no_bucket = getenv("QX_NO_BUCKET") != nullptr;
+  const bool bucket_ok = !no_bucket && eps > 0.0 && s->want_narrow != 2;
+  u64* h_groups = nullptr;
+  struct ReleasePinned {
+    void* p;
+    ~ReleasePinned() { if (p) qx_pinned_free(p); }
+  } relg{nullptr};
+  if (bucket_ok) {
+    QX_TRY(qx_pinned_alloc(reinterpret_cast<void**>(&h_groups), 8ll * (2 + 3 * (qxb::kNgCap + 1))));
+    relg.p = h_groups;
+    k_group_export<<<(qxb::kNgCap + 1 + 255) / 256, 256, 0, s->stream>>>(cwb[sorted], gsrc, gslot, totals, h_groups,
+                                                                       qxb::kNgCap);
+    qx_count_launches(1);
+    QX_CUDA(cudaGetLastError());
+  }
   QX_TRY(qx_readback(s->stream, s->h_pinned, seg_slot, (int64_t)n_seg + 1));
   QX_CUDA(cudaStreamSynchronize(s->stream));
   const int64_t total = s->h_pinned[n_seg];
@@ -1065,6 +1115,38 @@ int qx_dense_operator_step(qx_store* s, const OperatorTable& nz, const uint32_t*
   // the sources live in skey/slam now: both store buffers are free for the output
   QX_TRY(qx_store_reserve(s, total, false));
   const int out = s->cur ^ 1;
+
+  // ---- bucketed step: slots leave the kernel in canonical order, no sort (bucket.cuh)
+  if (bucket_ok && h_groups[0] >= 1 && h_groups[0] <= (u64)qxb::kNgCap && ub_seg > QX_SMALL_MAX) {
+    const int ng = (int)h_groups[0];
+    const u64* h_cw = h_groups + 2;
+    const u64* h_src = h_cw + (qxb::kNgCap + 1);
+    const u64* h_slot = h_src + (qxb::kNgCap + 1);
+    std::vector<int64_t> h_seg_slot(s->h_pinned, s->h_pinned + n_seg + 1);   // the step reuses h_pinned
+    const bool narrow_out = s->n_qubits <= 16 && s->want_narrow != 0;
+    bool handled = false;
+    if (s->n_qubits <= 16) {
+      ImageTable<u32> im;
+      fill_images_u32(s->n_qubits, program, n_ops, cx_c, cx_t, cx_s, &im);
+      QX_TRY((qxb::bucket_step<u32>(s, ct, im, ng, h_cw, h_src, h_slot, h_seg_slot.data(), total, skey, slam, n, out,
+                                    narrow_out, eps, part, parts, &handled)));
+    } else {
+      ImageTable<u64> im;
+      fill_images_u64(s->n_qubits, program, n_ops, cx_c, cx_t, cx_s, &im);
+      QX_TRY((qxb::bucket_step<u64>(s, ct, im, ng, h_cw, h_src, h_slot, h_seg_slot.data(), total, skey, slam, n, out,
+                                    false, eps, part, parts, &handled)));
+    }
+    if (handled) {
+      s->cur = out;
+      s->exact = false;
+      s->ub_total = total;
+      s->ub_seg = ub_seg;
+      s->narrow_keys = narrow_out;
+      s->pack_bnd = nullptr;
+      QX_TRY(qx_store_refresh(s));                  // kept counts: exact offsets for the caller
+      return QX_OK;
+    }
+  }
 
   const int64_t tiles = std::max<int64_t>(1, (total + kTileSlots - 1) / kTileSlots);
   const int passes = std::min(qxm::kMaxPasses, (2 * s->n_qubits + QX_RADIX_BITS - 1) / QX_RADIX_BITS);
