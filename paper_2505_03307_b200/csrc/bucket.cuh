@@ -227,18 +227,64 @@ __global__ void k_bucket_offsets(const u64* __restrict__ status, u32* __restrict
 }
 
 // ---- the bucket kernel ---------------------------------------------------------------------------
+// Everything a CTA needs to start a tile, in sorted (bucket) order: one coalesced load per bucket
+// instead of the chain tile id -> descriptor -> group -> sources.
+template <typename K>
+struct __align__(16) TileFat {
+  K word;              // image of the high picks
+  K cw;                // class word of the group
+  K l_mask;            // its tile-local digits
+  K key01[2];          // keys of the group's first two sources
+  u32 e;               // phase exponent of `word`
+  u32 src0, n_src;
+  u32 T;               // slots of the tile
+  u32 Lw, n_mid;
+  u64 phi_at;          // index of the tile's first high product
+  double phi01[2];     // high products of the first two sources
+};
+
+template <typename K>
+__global__ void __launch_bounds__(256)
+k_tile_fat(const BGroup<K>* __restrict__ groups, const TileDesc<K>* __restrict__ desc,
+           const double* __restrict__ phi, const double* __restrict__ sort_val, const u64* __restrict__ skey,
+           u64 n_tiles, TileFat<K>* __restrict__ fat) {
+  const u64 i = (u64)blockIdx.x * 256 + threadIdx.x;
+  if (i >= n_tiles) return;
+  const u64 tile = (u64)__double_as_longlong(sort_val[i]) & (((u64)1 << kTileIdBits) - 1);
+  const TileDesc<K> d = desc[tile];
+  const BGroup<K> g = groups[d.group];
+  TileFat<K> f;
+  f.word = d.word;
+  f.cw = g.cw;
+  f.l_mask = g.l_mask;
+  f.e = d.e;
+  f.src0 = g.src0;
+  f.n_src = g.n_src;
+  f.T = g.T;
+  f.Lw = g.Lw;
+  f.n_mid = g.n_mid;
+  f.phi_at = g.phi0 + (tile - g.tile0) * g.n_src;
+  f.key01[0] = (K)skey[g.src0];
+  f.phi01[0] = phi[f.phi_at];
+  f.key01[1] = g.n_src > 1 ? (K)skey[g.src0 + 1] : (K)0;
+  f.phi01[1] = g.n_src > 1 ? phi[f.phi_at + 1] : 0.0;
+  fat[i] = f;
+}
+
+constexpr int kTrip = 3;                     // tiles whose slots a thread keeps in registers
+constexpr int kHeld = kTrip * kBRows;        // 9
+
 template <typename K>
 struct BSmem {
   OperatorTable tb;                  // class-expanded (dense.cu build_class_table)
   ImageTable<K> im;
-  BLow<K> low[27];
-  BMid<K> mid[kMaxMid];
-  double low_w[kSrcChunk][27][4];    // [source of the round][low branch][low digit]
-  double p_mid[kSrcChunk * kMaxMid]; // [source of the round][mid entry]: lambda * high * mid weights
-  u64 scan[kBWarps + 1];
+  BLow<K> low[2][27];                // tables of the tile in flight, double-buffered by tile parity
+  BMid<K> mid[2][kMaxMid];
+  double low_w[2][2][27][4];         // [parity][source of the round][low branch][low digit]
+  double p_mid[2][2][kMaxMid];       // [parity][source of the round][mid entry]: lambda * high * mid weights
+  u32 warp_tot[kBWarps + 1];
   u64 base;
   u32 unit;
-  u32 kept;
 };
 
 inline size_t bucket_smem_bytes(size_t fixed, int ell, int cap) {
@@ -246,15 +292,57 @@ inline size_t bucket_smem_bytes(size_t fixed, int ell, int cap) {
   return fixed + 4 * words + 2 * words + 8 * (size_t)cap + 2 * (size_t)cap + 64;
 }
 
+// status words of the buckets: bits 63-62 = 0 not counted yet, 1 kept count, 2 inclusive prefix
+__device__ __forceinline__ void bucket_publish(u64* status, u32 idx, u64 kept) {
+  st_volatile_u64(status + idx, (idx == 0 ? QX_LB_INC : QX_LB_AGG) | kept);
+}
+// all 32 lanes of one warp: exclusive prefix of bucket idx (its own count is published already)
+__device__ __forceinline__ u64 bucket_resolve(u64* status, u32 idx, u64 kept) {
+  if (idx == 0) return 0;
+  constexpr int R = 8;
+  u64 excl = 0;
+  int base = (int)idx - 1;
+  bool done = false;
+  while (!done) {
+    u64 w[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      const int t = base - r * 32 - (int)lane_id();
+      w[r] = t >= 0 ? ld_volatile_u64(status + t) : QX_LB_INC;
+    }
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      if (!done) {
+        const int t = base - r * 32 - (int)lane_id();
+        while ((w[r] >> 62) == 0) w[r] = ld_volatile_u64(status + t);
+        const u32 inc = __ballot_sync(QX_FULL_MASK, (w[r] >> 62) == 2);
+        u64 v = w[r] & QX_LB_VAL;
+        if (inc) {
+          const int first = __ffs(inc) - 1;
+          if ((int)lane_id() > first) v = 0;
+          done = true;
+        }
+        excl += warp_sum(v);
+      }
+    }
+    base -= 32 * R;
+  }
+  if (lane_id() == 0) st_volatile_u64(status + idx, QX_LB_INC | (excl + kept));
+  return excl;
+}
+
+// One CTA per bucket, buckets handed out in order by a ticket.  A bucket's kept count is known
+// only after all its sums, and its first output position needs the counts of every bucket
+// before it: the CTA does not wait -- it publishes the count, keeps the ranked terms in shared
+// memory, goes on with its NEXT bucket (whose sums stay in registers meanwhile) and writes the
+// previous one out after that, when its predecessors have long published theirs.
 template <typename K, typename KO>
 __global__ void __launch_bounds__(kBThreads, 4)
-k_bucket_emit(const BGroup<K>* __restrict__ groups, const TileDesc<K>* __restrict__ desc,
-              const double* __restrict__ phi, const u64* __restrict__ sort_key,
-              const double* __restrict__ sort_val, const u32* __restrict__ unit_tile0, u32 u_lo, u32 u_hi,
-              const u64* __restrict__ skey, const double* __restrict__ slam, KO* __restrict__ keys_out,
-              double* __restrict__ lam_out, u64* __restrict__ status, u32* __restrict__ ticket, int ell,
-              int top_bits, int cap, double eps, const __grid_constant__ OperatorTable tb,
-              const __grid_constant__ ImageTable<K> im) {
+k_bucket_emit(const TileFat<K>* __restrict__ fat, const double* __restrict__ phi,
+              const u64* __restrict__ sort_key, const u32* __restrict__ unit_tile0, u32 u_lo, u32 u_hi,
+              const u64* __restrict__ skey, KO* __restrict__ keys_out, double* __restrict__ lam_out,
+              u64* __restrict__ status, u32* __restrict__ ticket, int ell, int top_bits, int cap, double eps,
+              const __grid_constant__ OperatorTable tb, const __grid_constant__ ImageTable<K> im) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   BSmem<K>& sm = *reinterpret_cast<BSmem<K>*>(smem_raw);
   const int words = 1 << (ell - 5);
@@ -272,252 +360,357 @@ k_bucket_emit(const BGroup<K>* __restrict__ groups, const TileDesc<K>* __restric
     for (int i = tid; i < (int)(sizeof(ImageTable<K>) / 4); i += kBThreads) idst[i] = isrc[i];
   }
   const K low_bits = (K)(((u64)1 << ell) - 1);
-  int cached_group = -1;
-  // per-group state in registers: digit positions of the low three and the mid digits
-  int lbit[3] = {-1, -1, -1};
-  u32 lrad[3] = {1, 1, 1};
-  K mid_mask = 0, cwg = 0;
-  u32 Lw = 1, n_mid = 1, bpr = kBThreads, A = kBThreads, n_src = 0, src0 = 0, T = 0;
-  u64 phi0 = 0, tile0 = 0;
-  u32 my_bl = 0, my_m0 = 0;
+  const u64 top_mask = ((u64)1 << top_bits) - 1;
+  int par = 0;
+  bool pending = false;                          // a ranked bucket sits in st_key / st_lam
+  u32 pend_idx = 0, pend_kept = 0;
+  u64 pend_top = 0;
+
+  // the previous bucket: first output position, then out (coalesced, final order, store format)
+  auto flush_pending = [&]() {
+    if (warp == 0) {
+      const u64 ex = bucket_resolve(status, pend_idx, (u64)pend_kept);
+      if (lane == 0) sm.base = ex;
+    }
+    __syncthreads();
+    const int64_t base = (int64_t)sm.base;
+    for (u32 r = (u32)tid; r < pend_kept; r += kBThreads) {
+      st_stream(keys_out + base + r, (KO)(pend_top | (u64)st_key[r]));
+      st_stream(lam_out + base + r, st_lam[r]);
+    }
+    __syncthreads();
+    pending = false;
+  };
 
   for (;;) {
-    __syncthreads();                              // previous bucket written out (and tables copied)
+    __syncthreads();                              // ranks of the previous bucket taken; tables copied
     if (tid == 0) sm.unit = u_lo + atomicAdd(ticket, 1u);
     __syncthreads();
     const u32 unit = sm.unit;
     if (unit >= u_hi) break;
     const u32 t_begin = unit_tile0[unit], t_end = unit_tile0[unit + 1];
-    const u64 bucket = sort_key[t_begin];
+    const bool slow = t_end - t_begin > (u32)kTrip;   // more tiles than the registers hold: park them
     for (int i = tid; i < words; i += kBThreads) bitmap[i] = 0u;
-    u32 parked = 0;                               // slots of the bucket so far
+    if (slow && pending) flush_pending();         // parking needs the staging area
+    u32 parked = 0;
+    double held[kHeld];
+    u32 held_y[kHeld];
 
-    for (u32 ti = t_begin; ti < t_end; ++ti) {
-      const u64 tile = (u64)__double_as_longlong(sort_val[ti]) & (((u64)1 << kTileIdBits) - 1);
-      const TileDesc<K> td = desc[tile];
-      __syncthreads();                            // previous tile's tables consumed; bitmap cleared
-      if ((int)td.group != cached_group) {
-        const BGroup<K> g = groups[td.group];
-        cached_group = (int)td.group;
-        cwg = g.cw;
-        n_src = g.n_src;
-        src0 = g.src0;
-        T = g.T;
-        Lw = g.Lw;
-        n_mid = g.n_mid;
-        phi0 = g.phi0;
-        tile0 = g.tile0;
-        K m = g.l_mask;
+    for (u32 t0 = t_begin; t0 < t_end; t0 += kTrip) {
+#pragma unroll
+      for (int k = 0; k < kHeld; ++k) {
+        held[k] = 0.0;
+        held_y[k] = 0;
+      }
+      u32 park_at[kTrip];
+      u32 park_lw[kTrip];
+      u32 live_all = 0;                           // bit t * kBRows + k: that slot of mine exists
+#pragma unroll
+      for (int t = 0; t < kTrip; ++t) {
+        park_at[t] = parked;
+        park_lw[t] = 1;
+        if (t0 + t >= t_end) continue;            // uniform
+        const TileFat<K> tf = fat[t0 + t];
+        const K cwg = tf.cw;
+        const u32 Lw = tf.Lw, n_mid = tf.n_mid, n_src = tf.n_src;
+        park_lw[t] = Lw;
+        parked += tf.T;
+        int lbit[3];
+        u32 lrad[3];
+        K mm = tf.l_mask;
 #pragma unroll
         for (int j = 0; j < 3; ++j) {
           lbit[j] = -1;
           lrad[j] = 1;
-          if (m) {
-            lbit[j] = KeyOps<K>::lowest(m);
-            m &= m - 1;
+          if (mm) {
+            lbit[j] = KeyOps<K>::lowest(mm);
+            mm &= mm - 1;
             lrad[j] = sm.tb.cnt[lbit[j] >> 1][(u32)((cwg >> lbit[j]) & 3u) - 1u];
           }
         }
-        mid_mask = m;
-        bpr = (u32)kBThreads / Lw;                // mid entries per row
-        A = bpr * Lw;                             // slots per row
-        my_m0 = (u32)tid / Lw;
-        my_bl = (u32)tid - my_m0 * Lw;
-        if ((u32)tid < Lw) {                      // low branches of the group
+        const K mid_mask = mm;
+        const int n_mid_digits = (int)Plane<K>::popc(mid_mask);
+        const u32 magic = 65536u / Lw + 1u;       // t / Lw == (t * magic) >> 16 for t < 2^16 / Lw
+        const u32 bpr = ((u32)kBThreads * magic) >> 16;   // mid entries per row
+        const u32 A = bpr * Lw;                   // slots per row
+        const u32 my_m0 = ((u32)tid * magic) >> 16;
+        const u32 my_bl = (u32)tid - my_m0 * Lw;
+        const u32 ns2 = min(n_src, 2u);
+        // ---- tables of the tile: mid entries by the first threads, low branches by warp 4 on
+        if ((u32)tid < n_mid) {
           u32 b = (u32)tid, picks = 0;
+          int idx = 0;
+          for (K m = mid_mask; m; ++idx) {
+            const int bit = KeyOps<K>::lowest(m);
+            m &= m - 1;
+            u32 q, r;
+            divmod_small<u32>(b, sm.tb.cnt[bit >> 1][(u32)((cwg >> bit) & 3u) - 1u], q, r);
+            picks |= r << (2 * idx);
+            b = q;
+          }
+          K w = tf.word;
+          u32 ex = tf.e;
+          double v0 = tf.phi01[0], v1 = tf.phi01[1];
+          idx = n_mid_digits - 1;
+          for (K m = mid_mask; m; --idx) {          // qubit 0 first (stabilizer.py:311-319)
+            const int bit = KeyOps<K>::highest(m);
+            m ^= (K)1 << bit;
+            const int p = bit >> 1;
+            const u32 pick = (picks >> (2 * idx)) & 3u;
+            const u32 ax = sm.tb.axis[p][(u32)((cwg >> bit) & 3u) - 1u][pick];
+            compose<K>(w, ex, sm.im.img[p][ax - 1], sm.im.imx[p][ax - 1], sm.im.e[p][ax - 1]);
+            v0 = __dmul_rn(v0, sm.tb.w[p][(u32)((tf.key01[0] >> bit) & 3u) - 1u][pick]);
+            if (ns2 > 1) v1 = __dmul_rn(v1, sm.tb.w[p][(u32)((tf.key01[1] >> bit) & 3u) - 1u][pick]);
+          }
+          BMid<K> me;
+          me.word = w;
+          me.e = ex & 3u;
+          me.picks = picks;
+          sm.mid[par][tid] = me;
+          sm.p_mid[par][0][tid] = v0;
+          sm.p_mid[par][1][tid] = v1;
+        }
+        if (tid >= 128 && (u32)(tid - 128) < Lw) {
+          const int l = tid - 128;
+          u32 b = (u32)l, picks = 0;
           K w = 0;
           u32 ex = 0;
           u32 pick[3];
 #pragma unroll
           for (int j = 0; j < 3; ++j) {
-            pick[j] = b % lrad[j];
-            b /= lrad[j];
+            u32 q;
+            divmod_small<u32>(b, lrad[j], q, pick[j]);
+            b = q;
             picks |= pick[j] << (2 * j);
           }
 #pragma unroll
           for (int j = 2; j >= 0; --j) {
+            double w0 = 1.0, w1 = 1.0;
             if (lbit[j] >= 0) {
               const int p = lbit[j] >> 1;
               const u32 ax = sm.tb.axis[p][(u32)((cwg >> lbit[j]) & 3u) - 1u][pick[j]];
               compose<K>(w, ex, sm.im.img[p][ax - 1], sm.im.imx[p][ax - 1], sm.im.e[p][ax - 1]);
+              w0 = sm.tb.w[p][(u32)((tf.key01[0] >> lbit[j]) & 3u) - 1u][pick[j]];
+              if (ns2 > 1) w1 = sm.tb.w[p][(u32)((tf.key01[1] >> lbit[j]) & 3u) - 1u][pick[j]];
             }
+            sm.low_w[par][0][l][j] = w0;
+            sm.low_w[par][1][l][j] = w1;
           }
           BLow<K> le;
           le.word = w;
           le.imx = (w ^ (w >> 1)) & Plane<K>::lo;
           le.e = ex & 3u;
           le.picks = picks;
-          sm.low[tid] = le;
-        }
-      }
-      const u64 h_index = tile - tile0;
-      // mid entries: the tile's high word with the mid picks composed in
-      if ((u32)tid < n_mid) {
-        u32 b = (u32)tid, picks = 0;
-        int idx = 0;
-        for (K m = mid_mask; m; ++idx) {
-          const int bit = KeyOps<K>::lowest(m);
-          m &= m - 1;
-          const u32 c = sm.tb.cnt[bit >> 1][(u32)((cwg >> bit) & 3u) - 1u];
-          const u32 q = b / c;
-          picks |= (b - q * c) << (2 * idx);
-          b = q;
-        }
-        K w = td.word;
-        u32 ex = td.e;
-        idx = (int)Plane<K>::popc(mid_mask) - 1;
-        for (K m = mid_mask; m; --idx) {
-          const int bit = KeyOps<K>::highest(m);
-          m ^= (K)1 << bit;
-          const u32 ax = sm.tb.axis[bit >> 1][(u32)((cwg >> bit) & 3u) - 1u][(picks >> (2 * idx)) & 3u];
-          compose<K>(w, ex, sm.im.img[bit >> 1][ax - 1], sm.im.imx[bit >> 1][ax - 1], sm.im.e[bit >> 1][ax - 1]);
-        }
-        BMid<K> me;
-        me.word = w;
-        me.e = ex & 3u;
-        me.picks = picks;
-        sm.mid[tid] = me;
-      }
-      double acc[kBRows];
-#pragma unroll
-      for (int k = 0; k < kBRows; ++k) acc[k] = 0.0;
-      u32 live = 0;
-      if ((u32)tid < A) {
-#pragma unroll
-        for (int k = 0; k < kBRows; ++k)
-          if (my_m0 + (u32)k * bpr < n_mid) live |= 1u << k;
-      }
-      // sources, kSrcChunk per round, in input order
-      for (u32 c0 = 0; c0 < n_src; c0 += kSrcChunk) {
-        const u32 nc = min((u32)kSrcChunk, n_src - c0);
-        __syncthreads();                          // mid picks written; previous round consumed
-        for (u32 w = (u32)tid; w < nc * n_mid; w += kBThreads) {
-          const u32 c = w / n_mid, m = w - c * n_mid;
-          const K key = (K)skey[src0 + c0 + c];
-          const u32 picks = sm.mid[m].picks;
-          double v = phi[phi0 + h_index * n_src + c0 + c];
-          int idx = (int)Plane<K>::popc(mid_mask) - 1;
-          for (K mm = mid_mask; mm; --idx) {      // qubit 0 first
-            const int bit = KeyOps<K>::highest(mm);
-            mm ^= (K)1 << bit;
-            v = __dmul_rn(v, sm.tb.w[bit >> 1][(u32)((key >> bit) & 3u) - 1u][(picks >> (2 * idx)) & 3u]);
-          }
-          sm.p_mid[c * kMaxMid + m] = v;
-        }
-        for (u32 w = (u32)tid; w < nc * Lw; w += kBThreads) {
-          const u32 c = w / Lw, l = w - c * Lw;
-          const K key = (K)skey[src0 + c0 + c];
-          const u32 picks = sm.low[l].picks;
-#pragma unroll
-          for (int j = 0; j < 3; ++j) {
-            double wt = 1.0;
-            if (lbit[j] >= 0)
-              wt = sm.tb.w[lbit[j] >> 1][(u32)((key >> lbit[j]) & 3u) - 1u][(picks >> (2 * j)) & 3u];
-            sm.low_w[c][l][j] = wt;
-          }
+          sm.low[par][l] = le;
         }
         __syncthreads();
-        if (live) {
-          for (u32 c = 0; c < nc; ++c) {
-            const double2 w01 = *reinterpret_cast<const double2*>(&sm.low_w[c][my_bl][0]);
-            const double w2 = sm.low_w[c][my_bl][2];
-            const double* pm = sm.p_mid + c * kMaxMid + my_m0;
-            const bool first = c0 + c == 0;
+        u32 live = 0;
+        if ((u32)tid < A) {
 #pragma unroll
-            for (int k = 0; k < kBRows; ++k) {
-              if (live & (1u << k)) {
-                // ((p * w2) * w1) * w0 with explicit roundings: no fused multiply-add into the sum
-                double v = __dmul_rn(pm[(u32)k * bpr], w2);
-                v = __dmul_rn(v, w01.y);
-                v = __dmul_rn(v, w01.x);
-                acc[k] = first ? v : __dadd_rn(acc[k], v);
+          for (int k = 0; k < kBRows; ++k)
+            if (my_m0 + (u32)k * bpr < n_mid) live |= 1u << k;
+        }
+        live_all |= live << (t * kBRows);
+        double acc[kBRows];
+#pragma unroll
+        for (int k = 0; k < kBRows; ++k) acc[k] = 0.0;
+        if (live) {
+          // ((p * w2) * w1) * w0 with explicit roundings: no fused multiply-add into the sum
+#pragma unroll
+          for (u32 c = 0; c < 2; ++c) {
+            if (c < ns2) {
+              const double2 w01 = *reinterpret_cast<const double2*>(&sm.low_w[par][c][my_bl][0]);
+              const double w2 = sm.low_w[par][c][my_bl][2];
+              const double* pm = &sm.p_mid[par][c][my_m0];
+#pragma unroll
+              for (int k = 0; k < kBRows; ++k) {
+                if (live & (1u << k)) {
+                  double v = __dmul_rn(pm[(u32)k * bpr], w2);
+                  v = __dmul_rn(v, w01.y);
+                  v = __dmul_rn(v, w01.x);
+                  acc[k] = c == 0 ? v : __dadd_rn(acc[k], v);
+                }
               }
             }
           }
         }
-      }
-      // words, signs, drop rule; kept slots mark the bitmap; every slot is parked in slot order
-      if (live) {
-        const BLow<K> le = sm.low[my_bl];
+        // further sources of the group, two per round, in input order (rare: the tables of the
+        // round replace those of the first two behind a barrier)
+        for (u32 c0 = 2; c0 < n_src; c0 += 2) {
+          const u32 nc = min(2u, n_src - c0);
+          __syncthreads();
+          for (u32 w = (u32)tid; w < nc * n_mid; w += kBThreads) {
+            const u32 c = w >= n_mid ? 1u : 0u, m = w - c * n_mid;
+            const K key = (K)skey[tf.src0 + c0 + c];
+            const u32 picks = sm.mid[par][m].picks;
+            double v = phi[tf.phi_at + c0 + c];
+            int idx = n_mid_digits - 1;
+            for (K m2 = mid_mask; m2; --idx) {
+              const int bit = KeyOps<K>::highest(m2);
+              m2 ^= (K)1 << bit;
+              v = __dmul_rn(v, sm.tb.w[bit >> 1][(u32)((key >> bit) & 3u) - 1u][(picks >> (2 * idx)) & 3u]);
+            }
+            sm.p_mid[par][c][m] = v;
+          }
+          for (u32 w = (u32)tid; w < nc * Lw; w += kBThreads) {
+            const u32 c = w >= Lw ? 1u : 0u, l = w - c * Lw;
+            const K key = (K)skey[tf.src0 + c0 + c];
+            const u32 picks = sm.low[par][l].picks;
 #pragma unroll
-        for (int k = 0; k < kBRows; ++k) {
-          if (live & (1u << k)) {
-            const u32 m = my_m0 + (u32)k * bpr;
-            const BMid<K> me = sm.mid[m];
-            K out = me.word;
-            u32 ex = me.e;
-            compose<K>(out, ex, le.word, le.imx, le.e);
-            double v = acc[k];
-            if (composed_sign<K>(out, ex)) v = -v;            // sign flips are exact
-            const u32 y = (u32)(out & low_bits);
-            const bool kept = fabs(v) >= eps;
-            if (kept) atomicOr(&bitmap[y >> 5], 1u << (y & 31u));
-            const u32 at = parked + m * Lw + my_bl;
-            st_key[at] = (unsigned short)y;
-            st_lam[at] = kept ? v : 0.0;                       // eps > 0: a kept sum is never 0
+            for (int j = 0; j < 3; ++j) {
+              double wt = 1.0;
+              if (lbit[j] >= 0)
+                wt = sm.tb.w[lbit[j] >> 1][(u32)((key >> lbit[j]) & 3u) - 1u][(picks >> (2 * j)) & 3u];
+              sm.low_w[par][c][l][j] = wt;
+            }
+          }
+          __syncthreads();
+          if (live) {
+            for (u32 c = 0; c < nc; ++c) {
+              const double2 w01 = *reinterpret_cast<const double2*>(&sm.low_w[par][c][my_bl][0]);
+              const double w2 = sm.low_w[par][c][my_bl][2];
+              const double* pm = &sm.p_mid[par][c][my_m0];
+#pragma unroll
+              for (int k = 0; k < kBRows; ++k) {
+                if (live & (1u << k)) {
+                  double v = __dmul_rn(pm[(u32)k * bpr], w2);
+                  v = __dmul_rn(v, w01.y);
+                  v = __dmul_rn(v, w01.x);
+                  acc[k] = __dadd_rn(acc[k], v);
+                }
+              }
+            }
+          }
+        }
+        // words, signs, drop rule; a kept slot marks the bitmap and stays in registers
+        if (live) {
+          const BLow<K> le = sm.low[par][my_bl];
+#pragma unroll
+          for (int k = 0; k < kBRows; ++k) {
+            if (live & (1u << k)) {
+              const BMid<K> me = sm.mid[par][my_m0 + (u32)k * bpr];
+              K out = me.word;
+              u32 ex = me.e;
+              compose<K>(out, ex, le.word, le.imx, le.e);
+              double v = acc[k];
+              if (composed_sign<K>(out, ex)) v = -v;            // sign flips are exact
+              const u32 y = (u32)(out & low_bits);
+              if (fabs(v) >= eps) {                              // eps > 0: a kept sum is never 0
+                atomicOr(&bitmap[y >> 5], 1u << (y & 31u));
+                held[t * kBRows + k] = v;
+                held_y[t * kBRows + k] = y;
+              }
+            }
+          }
+        }
+        if (n_src > 2) __syncthreads();             // the round tables are not double-buffered
+        par ^= 1;
+      }
+      if (slow) {
+        // park this triple in slot order (any order would do: ranks come from the bitmap); dropped
+        // slots are parked as 0.0 so that nothing stale is taken for a kept sum later
+#pragma unroll
+        for (int t = 0; t < kTrip; ++t) {
+          const u32 Lw = park_lw[t];
+          const u32 magic = 65536u / Lw + 1u;
+          const u32 bpr = ((u32)kBThreads * magic) >> 16;
+          const u32 my_m0 = ((u32)tid * magic) >> 16;
+          const u32 my_bl = (u32)tid - my_m0 * Lw;
+#pragma unroll
+          for (int k = 0; k < kBRows; ++k) {
+            const double v = held[t * kBRows + k];
+            if (live_all & (1u << (t * kBRows + k))) {
+              const u32 at = park_at[t] + (my_m0 + (u32)k * bpr) * Lw + my_bl;
+              st_key[at] = (unsigned short)held_y[t * kBRows + k];
+              st_lam[at] = v;
+            }
           }
         }
       }
-      parked += T;
     }
     __syncthreads();
     // ranks: popcount scan of the bitmap
+    u32 kept_total;
     {
       const int per = max(1, words / kBThreads);
       const int w0 = tid * per;
       u32 cnt = 0;
       if (w0 < words)
         for (int i = 0; i < per; ++i) cnt += __popc(bitmap[w0 + i]);
-      u64 total;
-      u64 ex = block_exclusive_sum<u64>((u64)cnt, sm.scan, total);
+      u32 incl = cnt;
+#pragma unroll
+      for (int d = 1; d < 32; d <<= 1) {
+        const u32 o = __shfl_up_sync(QX_FULL_MASK, incl, d);
+        if (lane >= d) incl += o;
+      }
+      if (lane == 31) sm.warp_tot[warp] = incl;
+      __syncthreads();
+      u32 before = 0, total = 0;
+#pragma unroll
+      for (int w = 0; w < kBWarps; ++w) {
+        const u32 wt = sm.warp_tot[w];
+        if (w < warp) before += wt;
+        total += wt;
+      }
+      kept_total = total;
       if (w0 < words) {
-        u32 run = (u32)ex;
+        u32 run = before + incl - cnt;
         for (int i = 0; i < per; ++i) {
           prefix[w0 + i] = (unsigned short)run;
           run += __popc(bitmap[w0 + i]);
         }
       }
-      if (tid == 0) sm.kept = (u32)total;
     }
-    __syncthreads();
-    const u32 kept_total = sm.kept;
-    if (warp == 0) {
-      const u64 ex = lookback_exclusive(status, (int)(unit - u_lo), (u64)kept_total);
-      if (lane == 0) sm.base = ex;
-    }
-    // parked slots -> rank order, in place through registers
-    unsigned short rk[kPerThread];
-    double rl[kPerThread];
+    if (tid == 0) bucket_publish(status, unit - u_lo, (u64)kept_total);
+    if (!slow) {
+      if (pending) flush_pending();               // barriers inside: prefix[] is visible after them
+      else __syncthreads();
+      // kept sums -> rank order in the staging area
 #pragma unroll
-    for (int j = 0; j < kPerThread; ++j) {
-      const u32 i = (u32)tid + (u32)j * kBThreads;
-      rl[j] = 0.0;
-      rk[j] = 0;
-      if (i < parked) {
-        rl[j] = st_lam[i];
-        rk[j] = st_key[i];
+      for (int k = 0; k < kHeld; ++k) {
+        if (held[k] != 0.0) {
+          const u32 y = held_y[k];
+          const u32 r = (u32)prefix[y >> 5] + __popc(bitmap[y >> 5] & ((1u << (y & 31u)) - 1u));
+          st_key[r] = (unsigned short)y;
+          st_lam[r] = held[k];
+        }
+      }
+    } else {
+      // parked slots -> rank order, in place through registers
+      __syncthreads();
+      unsigned short rk[kPerThread];
+      double rl[kPerThread];
+#pragma unroll
+      for (int j = 0; j < kPerThread; ++j) {
+        const u32 i = (u32)tid + (u32)j * kBThreads;
+        rl[j] = 0.0;
+        rk[j] = 0;
+        if (i < parked) {
+          rl[j] = st_lam[i];
+          rk[j] = st_key[i];
+        }
+      }
+      __syncthreads();
+#pragma unroll
+      for (int j = 0; j < kPerThread; ++j) {
+        if (rl[j] != 0.0) {
+          const u32 y = rk[j];
+          const u32 r = (u32)prefix[y >> 5] + __popc(bitmap[y >> 5] & ((1u << (y & 31u)) - 1u));
+          st_key[r] = rk[j];
+          st_lam[r] = rl[j];
+        }
       }
     }
+    pending = true;
+    pend_idx = unit - u_lo;
+    pend_kept = kept_total;
+    pend_top = (sort_key[t_begin] & top_mask) << ell;
+  }
+  if (pending) {
     __syncthreads();
-#pragma unroll
-    for (int j = 0; j < kPerThread; ++j) {
-      if (rl[j] != 0.0) {
-        const u32 y = rk[j];
-        const u32 r = (u32)prefix[y >> 5] + __popc(bitmap[y >> 5] & ((1u << (y & 31u)) - 1u));
-        st_key[r] = rk[j];
-        st_lam[r] = rl[j];
-      }
-    }
-    __syncthreads();
-    const int64_t base = (int64_t)sm.base;
-    const u64 top = (bucket & (((u64)1 << top_bits) - 1)) << ell;
-    for (u32 r = (u32)tid; r < kept_total; r += kBThreads) {
-      st_stream(keys_out + base + r, (KO)(top | (u64)st_key[r]));
-      st_stream(lam_out + base + r, st_lam[r]);
-    }
+    flush_pending();
   }
 }
-
 
 // ---- host side -------------------------------------------------------------------------------------
 template <typename T>
@@ -639,7 +832,8 @@ int bucket_step(qx_store* s, const OperatorTable& ct, const ImageTable<K>& im, i
   const int64_t bytes = bpadded((int64_t)sizeof(BGroup<K>) * (ng + 1)) + bpadded((int64_t)sizeof(TileDesc<K>) * (int64_t)n_tiles) +
                         bpadded(8 * (int64_t)n_phi) + 4 * bpadded(8 * (int64_t)n_tiles) + 2 * 256 +
                         bpadded(4 * ((int64_t)n_tiles + 1)) + bpadded(4 * (int64_t)n_seg) +
-                        bpadded(8 * (scan_tiles + 1)) + 256 + bpadded(8 * ((int64_t)n_tiles + 1)) + 256;
+                        bpadded(8 * (scan_tiles + 1)) + 256 + bpadded(8 * ((int64_t)n_tiles + 1)) + 256 +
+                        bpadded((int64_t)sizeof(TileFat<K>) * (int64_t)n_tiles);
   void* block = nullptr;
   QX_TRY(qx_dev_alloc(&block, bytes, s->stream, s->device));
   struct Release {
@@ -660,6 +854,7 @@ int bucket_step(qx_store* s, const OperatorTable& ct, const ImageTable<K>& im, i
   u64* info = bcarve<u64>(cur, 2);
   u64* unit_status = bcarve<u64>(cur, (int64_t)n_tiles + 1);
   u32* ticket = bcarve<u32>(cur, 2);
+  TileFat<K>* d_fat = bcarve<TileFat<K>>(cur, (int64_t)n_tiles);
 
   // groups and the offsets of the one-segment tile sort: host -> device through pinned staging
   const int64_t stage_bytes = (int64_t)sizeof(BGroup<K>) * (ng + 1) + 16;
@@ -702,7 +897,10 @@ int bucket_step(qx_store* s, const OperatorTable& ct, const ImageTable<K>& im, i
     sorted = mb.cur;
   }
   {
-    QxProfileScope prof(QX_K_DENSE_PREP, s->stream, 20.0 * (double)n_tiles, 2);
+    QxProfileScope prof(QX_K_DENSE_PREP, s->stream, 20.0 * (double)n_tiles + (double)sizeof(TileFat<K>) * (double)n_tiles, 3);
+    k_tile_fat<K><<<(unsigned)((n_tiles + 255) / 256), 256, 0, s->stream>>>(d_groups, d_desc, d_phi, svals[sorted], skey,
+                                                                          n_tiles, d_fat);
+    QX_CUDA(cudaGetLastError());
     k_unit_scan<<<(unsigned)scan_tiles, 256, 0, s->stream>>>(skeys[sorted], svals[sorted], n_tiles, top_bits,
                                                             unit_tile0, seg_first, scan_status, info);
     QX_CUDA(cudaGetLastError());
@@ -733,9 +931,8 @@ int bucket_step(qx_store* s, const OperatorTable& ct, const ImageTable<K>& im, i
     QX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, kBThreads, smem));
     per_sm = std::max(per_sm, 1);
     const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)u_hi - u_lo, (int64_t)s->sm_count * per_sm));
-    kernel<<<grid, kBThreads, smem, s->stream>>>(d_groups, d_desc, d_phi, skeys[sorted], svals[sorted], unit_tile0,
-                                                  u_lo, u_hi, skey, slam, keys_out, s->lam[out], unit_status, ticket,
-                                                  ell, top_bits, cap, eps, ct, im);
+    kernel<<<grid, kBThreads, smem, s->stream>>>(d_fat, d_phi, skeys[sorted], unit_tile0, u_lo, u_hi, skey, keys_out,
+                                                  s->lam[out], unit_status, ticket, ell, top_bits, cap, eps, ct, im);
     QX_CUDA(cudaGetLastError());
     return QX_OK;
   };
