@@ -215,6 +215,10 @@ int qx_operator_classes(int32_t n_qubits, const int32_t* counts, const int32_t* 
  * bucket, slots, low key bits ranked inside a bucket, bucket capacity (0: the step did not
  * qualify and the grouped step + sort ran), CTAs per SM. */
 int qx_bucket_last(int64_t out[8]);
+/* Host-only: switch the bucketed step on or off for this process (tests and A/B runs compare it
+ * with the grouped step + sort; results are bit-identical).  Returns the previous setting (1/0).
+ * QX_NO_BUCKET in the environment starts the process with it off. */
+int qx_bucket_enable(int32_t on);
 /* Number of raw branches the same call would produce per segment, nothing written
  * (branch_counts, stabilizer.py:232-237). */
 int qx_count_operator(qx_store* s, const int32_t* counts, int64_t* raw_per_segment);

@@ -70,6 +70,7 @@ SIGNATURES = {
     "qx_store_order_for_operator": (C.c_int, [_p, _p, C.c_int32]),
     "qx_operator_classes": (C.c_int, [_i32, _p, _p, _p, _p, _p, _p, _p]),
     "qx_bucket_last": (C.c_int, [_P(_i64)]),
+    "qx_bucket_enable": (C.c_int, [_i32]),
     "qx_merge": (C.c_int, [_p, _f64, _p]),
     "qx_sort": (C.c_int, [_p]),
     "qx_store_zi_sums": (C.c_int, [_p, _p]),
@@ -251,3 +252,16 @@ def launch_count() -> int:
     n = _i64()
     check(lib().qx_launch_count(C.byref(n)))
     return n.value
+
+
+def bucket_enable(on: bool) -> bool:
+    """Switch the bucketed operator step (csrc/bucket.cuh) on/off; returns the previous setting."""
+    return bool(lib().qx_bucket_enable(1 if on else 0))
+
+
+def bucket_last() -> dict:
+    """Geometry of the last bucketed operator step (cap == 0: it fell back to grouped step + sort)."""
+    out = (_i64 * 8)()
+    check(lib().qx_bucket_last(out))
+    keys = ("groups", "tiles", "buckets", "max_bucket", "slots", "ell", "cap", "ctas_per_sm")
+    return dict(zip(keys, (int(v) for v in out)))

@@ -196,8 +196,9 @@ k_unit_scan(const u64* __restrict__ sort_key, const double* __restrict__ sort_va
   }
 }
 
-__global__ void k_unit_sizes(const u32* __restrict__ unit_tile0, const double* __restrict__ sort_val,
-                             u64* __restrict__ info) {
+struct UnitHdr;
+__global__ void k_unit_sizes(const u32* __restrict__ unit_tile0, const u64* __restrict__ sort_key,
+                             const double* __restrict__ sort_val, uint4* __restrict__ hdr, u64* __restrict__ info) {
   const u64 nu = info[0];
   u32 worst = 0;
   for (u64 u = (u64)blockIdx.x * blockDim.x + threadIdx.x; u < nu; u += (u64)gridDim.x * blockDim.x) {
@@ -205,6 +206,9 @@ __global__ void k_unit_sizes(const u32* __restrict__ unit_tile0, const double* _
     for (u32 i = unit_tile0[u]; i < unit_tile0[u + 1]; ++i)
       slots += (u32)((u64)__double_as_longlong(sort_val[i]) >> kTileIdBits);
     worst = max(worst, slots);
+    const u32 first = unit_tile0[u];
+    const u64 key = sort_key[first];
+    hdr[u] = make_uint4(first, unit_tile0[u + 1] - first, (u32)key, (u32)(key >> 32));   // UnitHdr
   }
   worst = __reduce_max_sync(QX_FULL_MASK, worst);
   if (lane_id() == 0 && worst) atomicMax(reinterpret_cast<unsigned long long*>(info + 1), (unsigned long long)worst);
@@ -228,19 +232,25 @@ __global__ void k_bucket_offsets(const u64* __restrict__ status, u32* __restrict
 
 // ---- the bucket kernel ---------------------------------------------------------------------------
 // Everything a CTA needs to start a tile, in sorted (bucket) order: one coalesced load per bucket
-// instead of the chain tile id -> descriptor -> group -> sources.
+// instead of the chain tile id -> descriptor -> group -> sources.  The first 16 bytes are what
+// every thread reads; the rest is for the threads that build the tile's tables.
 template <typename K>
 struct __align__(16) TileFat {
+  u32 Lw, n_mid, n_src, T;   // low branches, mid entries, sources, slots
   K word;              // image of the high picks
   K cw;                // class word of the group
   K l_mask;            // its tile-local digits
-  K key01[2];          // keys of the group's first two sources
   u32 e;               // phase exponent of `word`
-  u32 src0, n_src;
-  u32 T;               // slots of the tile
-  u32 Lw, n_mid;
+  K key01[2];          // keys of the group's first two sources
+  u32 src0, pad;
   u64 phi_at;          // index of the tile's first high product
   double phi01[2];     // high products of the first two sources
+  u64 pad2;
+};
+
+struct __align__(16) UnitHdr {
+  u32 tile0, n_tiles;  // its tiles in sorted order
+  u64 top;             // (generator, top bits): the sort key of its tiles
 };
 
 template <typename K>
@@ -259,6 +269,8 @@ k_tile_fat(const BGroup<K>* __restrict__ groups, const TileDesc<K>* __restrict__
   f.l_mask = g.l_mask;
   f.e = d.e;
   f.src0 = g.src0;
+  f.pad = 0;
+  f.pad2 = 0;
   f.n_src = g.n_src;
   f.T = g.T;
   f.Lw = g.Lw;
@@ -282,7 +294,7 @@ struct BSmem {
   BMid<K> mid[2][kMaxMid];
   double low_w[2][2][27][4];         // [parity][source of the round][low branch][low digit]
   double p_mid[2][2][kMaxMid];       // [parity][source of the round][mid entry]: lambda * high * mid weights
-  u32 warp_tot[kBWarps + 1];
+  __align__(16) u32 warp_tot[kBWarps + 4];
   u64 base;
   u32 unit;
 };
@@ -297,7 +309,7 @@ __device__ __forceinline__ void bucket_publish(u64* status, u32 idx, u64 kept) {
   st_volatile_u64(status + idx, (idx == 0 ? QX_LB_INC : QX_LB_AGG) | kept);
 }
 // all 32 lanes of one warp: exclusive prefix of bucket idx (its own count is published already)
-__device__ __forceinline__ u64 bucket_resolve(u64* status, u32 idx, u64 kept) {
+__device__ __noinline__ u64 bucket_resolve(u64* status, u32 idx, u64 kept) {
   if (idx == 0) return 0;
   constexpr int R = 8;
   u64 excl = 0;
@@ -339,9 +351,9 @@ __device__ __forceinline__ u64 bucket_resolve(u64* status, u32 idx, u64 kept) {
 template <typename K, typename KO>
 __global__ void __launch_bounds__(kBThreads, 4)
 k_bucket_emit(const TileFat<K>* __restrict__ fat, const double* __restrict__ phi,
-              const u64* __restrict__ sort_key, const u32* __restrict__ unit_tile0, u32 u_lo, u32 u_hi,
-              const u64* __restrict__ skey, KO* __restrict__ keys_out, double* __restrict__ lam_out,
-              u64* __restrict__ status, u32* __restrict__ ticket, int ell, int top_bits, int cap, double eps,
+              const UnitHdr* __restrict__ units, u32 u_lo, u32 u_hi, const u64* __restrict__ skey,
+              KO* __restrict__ keys_out, double* __restrict__ lam_out, u64* __restrict__ status,
+              u32* __restrict__ ticket, int ell, int top_bits, int cap, double eps,
               const __grid_constant__ OperatorTable tb, const __grid_constant__ ImageTable<K> im) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   BSmem<K>& sm = *reinterpret_cast<BSmem<K>*>(smem_raw);
@@ -365,6 +377,9 @@ k_bucket_emit(const TileFat<K>* __restrict__ fat, const double* __restrict__ phi
   bool pending = false;                          // a ranked bucket sits in st_key / st_lam
   u32 pend_idx = 0, pend_kept = 0;
   u64 pend_top = 0;
+  // my column of a tile: low branch my_bl, first mid entry my_m0; row k adds bpr mid entries.
+  // Depends on the tile's Lw only, which rarely changes from one tile to the next.
+  u32 geo_Lw = 0, bpr = 0, A = 0, my_m0 = 0, my_bl = 0;
 
   // the previous bucket: first output position, then out (coalesced, final order, store format)
   auto flush_pending = [&]() {
@@ -373,10 +388,12 @@ k_bucket_emit(const TileFat<K>* __restrict__ fat, const double* __restrict__ phi
       if (lane == 0) sm.base = ex;
     }
     __syncthreads();
-    const int64_t base = (int64_t)sm.base;
-    for (u32 r = (u32)tid; r < pend_kept; r += kBThreads) {
-      st_stream(keys_out + base + r, (KO)(pend_top | (u64)st_key[r]));
-      st_stream(lam_out + base + r, st_lam[r]);
+    KO* kp = keys_out + (int64_t)sm.base + tid;
+    double* lp = lam_out + (int64_t)sm.base + tid;
+#pragma unroll 1
+    for (u32 r = (u32)tid; r < pend_kept; r += kBThreads, kp += kBThreads, lp += kBThreads) {
+      st_stream(kp, (KO)(pend_top | (u64)st_key[r]));
+      st_stream(lp, st_lam[r]);
     }
     __syncthreads();
     pending = false;
@@ -384,13 +401,23 @@ k_bucket_emit(const TileFat<K>* __restrict__ fat, const double* __restrict__ phi
 
   for (;;) {
     __syncthreads();                              // ranks of the previous bucket taken; tables copied
+    // a bucket id is taken right before its sums start: an id taken earlier would stay uncounted
+    // for longer and stall the look-back of every bucket behind it
     if (tid == 0) sm.unit = u_lo + atomicAdd(ticket, 1u);
     __syncthreads();
     const u32 unit = sm.unit;
     if (unit >= u_hi) break;
-    const u32 t_begin = unit_tile0[unit], t_end = unit_tile0[unit + 1];
-    const bool slow = t_end - t_begin > (u32)kTrip;   // more tiles than the registers hold: park them
+    const UnitHdr hdr = units[unit];
+    const u32 t_begin = hdr.tile0, t_end = hdr.tile0 + hdr.n_tiles;
+    const u32 n_tiles_unit = hdr.n_tiles;
+    const u64 unit_top = hdr.top;
+    const bool slow = n_tiles_unit > (u32)kTrip;  // more tiles than the registers hold: park them
     for (int i = tid; i < words; i += kBThreads) bitmap[i] = 0u;
+    if (n_tiles_unit > 1) {                       // descriptors of the later tiles: on their way to L1
+      const u32 bytes = (min(n_tiles_unit, (u32)kTrip) - 1u) * (u32)sizeof(TileFat<K>);
+      if ((u32)tid * 32u < bytes)
+        asm volatile("prefetch.global.L1 [%0];" ::"l"(reinterpret_cast<const char*>(fat + t_begin + 1) + tid * 32));
+    }
     if (slow && pending) flush_pending();         // parking needs the staging area
     u32 parked = 0;
     double held[kHeld];
@@ -398,10 +425,7 @@ k_bucket_emit(const TileFat<K>* __restrict__ fat, const double* __restrict__ phi
 
     for (u32 t0 = t_begin; t0 < t_end; t0 += kTrip) {
 #pragma unroll
-      for (int k = 0; k < kHeld; ++k) {
-        held[k] = 0.0;
-        held_y[k] = 0;
-      }
+      for (int k = 0; k < kHeld; ++k) held[k] = 0.0;
       u32 park_at[kTrip];
       u32 park_lw[kTrip];
       u32 live_all = 0;                           // bit t * kBRows + k: that slot of mine exists
@@ -410,34 +434,28 @@ k_bucket_emit(const TileFat<K>* __restrict__ fat, const double* __restrict__ phi
         park_at[t] = parked;
         park_lw[t] = 1;
         if (t0 + t >= t_end) continue;            // uniform
-        const TileFat<K> tf = fat[t0 + t];
-        const K cwg = tf.cw;
-        const u32 Lw = tf.Lw, n_mid = tf.n_mid, n_src = tf.n_src;
+        const TileFat<K>* tfp = fat + (t0 + t);
+        const uint4 geo = *reinterpret_cast<const uint4*>(tfp);
+        const u32 Lw = geo.x, n_mid = geo.y, n_src = geo.z;
         park_lw[t] = Lw;
-        parked += tf.T;
-        int lbit[3];
-        u32 lrad[3];
-        K mm = tf.l_mask;
-#pragma unroll
-        for (int j = 0; j < 3; ++j) {
-          lbit[j] = -1;
-          lrad[j] = 1;
-          if (mm) {
-            lbit[j] = KeyOps<K>::lowest(mm);
-            mm &= mm - 1;
-            lrad[j] = sm.tb.cnt[lbit[j] >> 1][(u32)((cwg >> lbit[j]) & 3u) - 1u];
-          }
-        }
-        const K mid_mask = mm;
-        const int n_mid_digits = (int)Plane<K>::popc(mid_mask);
-        const u32 magic = 65536u / Lw + 1u;       // t / Lw == (t * magic) >> 16 for t < 2^16 / Lw
-        const u32 bpr = ((u32)kBThreads * magic) >> 16;   // mid entries per row
-        const u32 A = bpr * Lw;                   // slots per row
-        const u32 my_m0 = ((u32)tid * magic) >> 16;
-        const u32 my_bl = (u32)tid - my_m0 * Lw;
+        parked += geo.w;
         const u32 ns2 = min(n_src, 2u);
-        // ---- tables of the tile: mid entries by the first threads, low branches by warp 4 on
+        if (Lw != geo_Lw) {                       // uniform
+          geo_Lw = Lw;
+          const u32 magic = 65536u / Lw + 1u;     // t / Lw == (t * magic) >> 16 for t < 2^16 / Lw
+          bpr = ((u32)kBThreads * magic) >> 16;   // mid entries per row
+          A = bpr * Lw;                           // slots per row
+          my_m0 = ((u32)tid * magic) >> 16;
+          my_bl = (u32)tid - my_m0 * Lw;
+        }
+        // ---- tables of the tile: mid entries by the first threads, low branches by warp 4
         if ((u32)tid < n_mid) {
+          const K cwg = tfp->cw;
+          K mid_mask = tfp->l_mask;
+          mid_mask &= mid_mask - 1;               // without the three lowest digits
+          mid_mask &= mid_mask - 1;
+          mid_mask &= mid_mask - 1;
+          const K key0 = tfp->key01[0], key1 = tfp->key01[1];
           u32 b = (u32)tid, picks = 0;
           int idx = 0;
           for (K m = mid_mask; m; ++idx) {
@@ -448,10 +466,10 @@ k_bucket_emit(const TileFat<K>* __restrict__ fat, const double* __restrict__ phi
             picks |= r << (2 * idx);
             b = q;
           }
-          K w = tf.word;
-          u32 ex = tf.e;
-          double v0 = tf.phi01[0], v1 = tf.phi01[1];
-          idx = n_mid_digits - 1;
+          K w = tfp->word;
+          u32 ex = tfp->e;
+          double v0 = tfp->phi01[0], v1 = tfp->phi01[1];
+          --idx;
           for (K m = mid_mask; m; --idx) {          // qubit 0 first (stabilizer.py:311-319)
             const int bit = KeyOps<K>::highest(m);
             m ^= (K)1 << bit;
@@ -459,8 +477,8 @@ k_bucket_emit(const TileFat<K>* __restrict__ fat, const double* __restrict__ phi
             const u32 pick = (picks >> (2 * idx)) & 3u;
             const u32 ax = sm.tb.axis[p][(u32)((cwg >> bit) & 3u) - 1u][pick];
             compose<K>(w, ex, sm.im.img[p][ax - 1], sm.im.imx[p][ax - 1], sm.im.e[p][ax - 1]);
-            v0 = __dmul_rn(v0, sm.tb.w[p][(u32)((tf.key01[0] >> bit) & 3u) - 1u][pick]);
-            if (ns2 > 1) v1 = __dmul_rn(v1, sm.tb.w[p][(u32)((tf.key01[1] >> bit) & 3u) - 1u][pick]);
+            v0 = __dmul_rn(v0, sm.tb.w[p][(u32)((key0 >> bit) & 3u) - 1u][pick]);
+            if (ns2 > 1) v1 = __dmul_rn(v1, sm.tb.w[p][(u32)((key1 >> bit) & 3u) - 1u][pick]);
           }
           BMid<K> me;
           me.word = w;
@@ -469,19 +487,28 @@ k_bucket_emit(const TileFat<K>* __restrict__ fat, const double* __restrict__ phi
           sm.mid[par][tid] = me;
           sm.p_mid[par][0][tid] = v0;
           sm.p_mid[par][1][tid] = v1;
-        }
-        if (tid >= 128 && (u32)(tid - 128) < Lw) {
+        } else if (tid >= 128 && (u32)(tid - 128) < Lw) {
           const int l = tid - 128;
+          const K cwg = tfp->cw;
+          const K key0 = tfp->key01[0], key1 = tfp->key01[1];
+          K mm = tfp->l_mask;
           u32 b = (u32)l, picks = 0;
           K w = 0;
           u32 ex = 0;
+          int lbit[3];
           u32 pick[3];
 #pragma unroll
           for (int j = 0; j < 3; ++j) {
-            u32 q;
-            divmod_small<u32>(b, lrad[j], q, pick[j]);
-            b = q;
-            picks |= pick[j] << (2 * j);
+            lbit[j] = -1;
+            pick[j] = 0;
+            if (mm) {
+              lbit[j] = KeyOps<K>::lowest(mm);
+              mm &= mm - 1;
+              u32 q;
+              divmod_small<u32>(b, sm.tb.cnt[lbit[j] >> 1][(u32)((cwg >> lbit[j]) & 3u) - 1u], q, pick[j]);
+              b = q;
+              picks |= pick[j] << (2 * j);
+            }
           }
 #pragma unroll
           for (int j = 2; j >= 0; --j) {
@@ -490,8 +517,8 @@ k_bucket_emit(const TileFat<K>* __restrict__ fat, const double* __restrict__ phi
               const int p = lbit[j] >> 1;
               const u32 ax = sm.tb.axis[p][(u32)((cwg >> lbit[j]) & 3u) - 1u][pick[j]];
               compose<K>(w, ex, sm.im.img[p][ax - 1], sm.im.imx[p][ax - 1], sm.im.e[p][ax - 1]);
-              w0 = sm.tb.w[p][(u32)((tf.key01[0] >> lbit[j]) & 3u) - 1u][pick[j]];
-              if (ns2 > 1) w1 = sm.tb.w[p][(u32)((tf.key01[1] >> lbit[j]) & 3u) - 1u][pick[j]];
+              w0 = sm.tb.w[p][(u32)((key0 >> lbit[j]) & 3u) - 1u][pick[j]];
+              if (ns2 > 1) w1 = sm.tb.w[p][(u32)((key1 >> lbit[j]) & 3u) - 1u][pick[j]];
             }
             sm.low_w[par][0][l][j] = w0;
             sm.low_w[par][1][l][j] = w1;
@@ -516,71 +543,100 @@ k_bucket_emit(const TileFat<K>* __restrict__ fat, const double* __restrict__ phi
         for (int k = 0; k < kBRows; ++k) acc[k] = 0.0;
         if (live) {
           // ((p * w2) * w1) * w0 with explicit roundings: no fused multiply-add into the sum
+          {
+            const double2 w01 = *reinterpret_cast<const double2*>(&sm.low_w[par][0][my_bl][0]);
+            const double w2 = sm.low_w[par][0][my_bl][2];
+            const double* pm = &sm.p_mid[par][0][my_m0];
 #pragma unroll
-          for (u32 c = 0; c < 2; ++c) {
-            if (c < ns2) {
-              const double2 w01 = *reinterpret_cast<const double2*>(&sm.low_w[par][c][my_bl][0]);
-              const double w2 = sm.low_w[par][c][my_bl][2];
-              const double* pm = &sm.p_mid[par][c][my_m0];
+            for (int k = 0; k < kBRows; ++k) {
+              if (live & (1u << k)) {
+                double v = __dmul_rn(pm[(u32)k * bpr], w2);
+                v = __dmul_rn(v, w01.y);
+                acc[k] = __dmul_rn(v, w01.x);
+              }
+            }
+          }
+          if (ns2 > 1) {
+            const double2 w01 = *reinterpret_cast<const double2*>(&sm.low_w[par][1][my_bl][0]);
+            const double w2 = sm.low_w[par][1][my_bl][2];
+            const double* pm = &sm.p_mid[par][1][my_m0];
 #pragma unroll
-              for (int k = 0; k < kBRows; ++k) {
-                if (live & (1u << k)) {
-                  double v = __dmul_rn(pm[(u32)k * bpr], w2);
-                  v = __dmul_rn(v, w01.y);
-                  v = __dmul_rn(v, w01.x);
-                  acc[k] = c == 0 ? v : __dadd_rn(acc[k], v);
-                }
+            for (int k = 0; k < kBRows; ++k) {
+              if (live & (1u << k)) {
+                double v = __dmul_rn(pm[(u32)k * bpr], w2);
+                v = __dmul_rn(v, w01.y);
+                v = __dmul_rn(v, w01.x);
+                acc[k] = __dadd_rn(acc[k], v);
               }
             }
           }
         }
         // further sources of the group, two per round, in input order (rare: the tables of the
         // round replace those of the first two behind a barrier)
-        for (u32 c0 = 2; c0 < n_src; c0 += 2) {
-          const u32 nc = min(2u, n_src - c0);
-          __syncthreads();
-          for (u32 w = (u32)tid; w < nc * n_mid; w += kBThreads) {
-            const u32 c = w >= n_mid ? 1u : 0u, m = w - c * n_mid;
-            const K key = (K)skey[tf.src0 + c0 + c];
-            const u32 picks = sm.mid[par][m].picks;
-            double v = phi[tf.phi_at + c0 + c];
-            int idx = n_mid_digits - 1;
-            for (K m2 = mid_mask; m2; --idx) {
-              const int bit = KeyOps<K>::highest(m2);
-              m2 ^= (K)1 << bit;
-              v = __dmul_rn(v, sm.tb.w[bit >> 1][(u32)((key >> bit) & 3u) - 1u][(picks >> (2 * idx)) & 3u]);
-            }
-            sm.p_mid[par][c][m] = v;
-          }
-          for (u32 w = (u32)tid; w < nc * Lw; w += kBThreads) {
-            const u32 c = w >= Lw ? 1u : 0u, l = w - c * Lw;
-            const K key = (K)skey[tf.src0 + c0 + c];
-            const u32 picks = sm.low[par][l].picks;
+        if (n_src > 2) {
+          const K cwg = tfp->cw;
+          K mid_mask = tfp->l_mask;
+          int lbit[3];
 #pragma unroll
-            for (int j = 0; j < 3; ++j) {
-              double wt = 1.0;
-              if (lbit[j] >= 0)
-                wt = sm.tb.w[lbit[j] >> 1][(u32)((key >> lbit[j]) & 3u) - 1u][(picks >> (2 * j)) & 3u];
-              sm.low_w[par][c][l][j] = wt;
+          for (int j = 0; j < 3; ++j) {
+            lbit[j] = -1;
+            if (mid_mask) {
+              lbit[j] = KeyOps<K>::lowest(mid_mask);
+              mid_mask &= mid_mask - 1;
             }
           }
-          __syncthreads();
-          if (live) {
-            for (u32 c = 0; c < nc; ++c) {
-              const double2 w01 = *reinterpret_cast<const double2*>(&sm.low_w[par][c][my_bl][0]);
-              const double w2 = sm.low_w[par][c][my_bl][2];
-              const double* pm = &sm.p_mid[par][c][my_m0];
+          const int n_mid_digits = (int)Plane<K>::popc(mid_mask);
+          const u32 src0 = tfp->src0;
+          const u64 phi_at = tfp->phi_at;
+          (void)cwg;
+#pragma unroll 1
+          for (u32 c0 = 2; c0 < n_src; c0 += 2) {
+            const u32 nc = min(2u, n_src - c0);
+            __syncthreads();
+            for (u32 w = (u32)tid; w < nc * n_mid; w += kBThreads) {
+              const u32 c = w >= n_mid ? 1u : 0u, m = w - c * n_mid;
+              const K key = (K)skey[src0 + c0 + c];
+              const u32 picks = sm.mid[par][m].picks;
+              double v = phi[phi_at + c0 + c];
+              int idx = n_mid_digits - 1;
+              for (K m2 = mid_mask; m2; --idx) {
+                const int bit = KeyOps<K>::highest(m2);
+                m2 ^= (K)1 << bit;
+                v = __dmul_rn(v, sm.tb.w[bit >> 1][(u32)((key >> bit) & 3u) - 1u][(picks >> (2 * idx)) & 3u]);
+              }
+              sm.p_mid[par][c][m] = v;
+            }
+            for (u32 w = (u32)tid; w < nc * Lw; w += kBThreads) {
+              const u32 c = w >= Lw ? 1u : 0u, l = w - c * Lw;
+              const K key = (K)skey[src0 + c0 + c];
+              const u32 picks = sm.low[par][l].picks;
 #pragma unroll
-              for (int k = 0; k < kBRows; ++k) {
-                if (live & (1u << k)) {
-                  double v = __dmul_rn(pm[(u32)k * bpr], w2);
-                  v = __dmul_rn(v, w01.y);
-                  v = __dmul_rn(v, w01.x);
-                  acc[k] = __dadd_rn(acc[k], v);
+              for (int j = 0; j < 3; ++j) {
+                double wt = 1.0;
+                if (lbit[j] >= 0)
+                  wt = sm.tb.w[lbit[j] >> 1][(u32)((key >> lbit[j]) & 3u) - 1u][(picks >> (2 * j)) & 3u];
+                sm.low_w[par][c][l][j] = wt;
+              }
+            }
+            __syncthreads();
+            if (live) {
+              for (u32 c = 0; c < nc; ++c) {
+                const double2 w01 = *reinterpret_cast<const double2*>(&sm.low_w[par][c][my_bl][0]);
+                const double w2 = sm.low_w[par][c][my_bl][2];
+                const double* pm = &sm.p_mid[par][c][my_m0];
+#pragma unroll
+                for (int k = 0; k < kBRows; ++k) {
+                  if (live & (1u << k)) {
+                    double v = __dmul_rn(pm[(u32)k * bpr], w2);
+                    v = __dmul_rn(v, w01.y);
+                    v = __dmul_rn(v, w01.x);
+                    acc[k] = __dadd_rn(acc[k], v);
+                  }
                 }
               }
             }
           }
+          __syncthreads();                          // the round tables are not double-buffered
         }
         // words, signs, drop rule; a kept slot marks the bitmap and stays in registers
         if (live) {
@@ -603,7 +659,6 @@ k_bucket_emit(const TileFat<K>* __restrict__ fat, const double* __restrict__ phi
             }
           }
         }
-        if (n_src > 2) __syncthreads();             // the round tables are not double-buffered
         par ^= 1;
       }
       if (slow) {
@@ -613,16 +668,15 @@ k_bucket_emit(const TileFat<K>* __restrict__ fat, const double* __restrict__ phi
         for (int t = 0; t < kTrip; ++t) {
           const u32 Lw = park_lw[t];
           const u32 magic = 65536u / Lw + 1u;
-          const u32 bpr = ((u32)kBThreads * magic) >> 16;
-          const u32 my_m0 = ((u32)tid * magic) >> 16;
-          const u32 my_bl = (u32)tid - my_m0 * Lw;
+          const u32 pb = ((u32)kBThreads * magic) >> 16;
+          const u32 pm0 = ((u32)tid * magic) >> 16;
+          const u32 pbl = (u32)tid - pm0 * Lw;
 #pragma unroll
           for (int k = 0; k < kBRows; ++k) {
-            const double v = held[t * kBRows + k];
             if (live_all & (1u << (t * kBRows + k))) {
-              const u32 at = park_at[t] + (my_m0 + (u32)k * bpr) * Lw + my_bl;
+              const u32 at = park_at[t] + (pm0 + (u32)k * pb) * Lw + pbl;
               st_key[at] = (unsigned short)held_y[t * kBRows + k];
-              st_lam[at] = v;
+              st_lam[at] = held[t * kBRows + k];
             }
           }
         }
@@ -632,11 +686,21 @@ k_bucket_emit(const TileFat<K>* __restrict__ fat, const double* __restrict__ phi
     // ranks: popcount scan of the bitmap
     u32 kept_total;
     {
-      const int per = max(1, words / kBThreads);
+      u32 cnt, c0 = 0;
+      const int per = words / kBThreads;          // words is a power of two
       const int w0 = tid * per;
-      u32 cnt = 0;
-      if (w0 < words)
-        for (int i = 0; i < per; ++i) cnt += __popc(bitmap[w0 + i]);
+      if (per == 2) {
+        const uint2 b = *reinterpret_cast<const uint2*>(bitmap + w0);
+        c0 = __popc(b.x);
+        cnt = c0 + __popc(b.y);
+      } else {
+        cnt = 0;
+        if (per == 0) {
+          if (tid < words) cnt = __popc(bitmap[tid]);
+        } else {
+          for (int i = 0; i < per; ++i) cnt += __popc(bitmap[w0 + i]);
+        }
+      }
       u32 incl = cnt;
 #pragma unroll
       for (int d = 1; d < 32; d <<= 1) {
@@ -645,16 +709,22 @@ k_bucket_emit(const TileFat<K>* __restrict__ fat, const double* __restrict__ phi
       }
       if (lane == 31) sm.warp_tot[warp] = incl;
       __syncthreads();
+      const uint4 ta = *reinterpret_cast<const uint4*>(&sm.warp_tot[0]);
+      const uint4 tb4 = *reinterpret_cast<const uint4*>(&sm.warp_tot[4]);
+      const u32 wt[kBWarps] = {ta.x, ta.y, ta.z, ta.w, tb4.x, tb4.y, tb4.z, tb4.w};
       u32 before = 0, total = 0;
 #pragma unroll
       for (int w = 0; w < kBWarps; ++w) {
-        const u32 wt = sm.warp_tot[w];
-        if (w < warp) before += wt;
-        total += wt;
+        if (w < warp) before += wt[w];
+        total += wt[w];
       }
       kept_total = total;
-      if (w0 < words) {
-        u32 run = before + incl - cnt;
+      u32 run = before + incl - cnt;
+      if (per == 2) {
+        *reinterpret_cast<u32*>(prefix + w0) = run | ((run + c0) << 16);
+      } else if (per == 0) {
+        if (tid < words) prefix[tid] = (unsigned short)run;
+      } else {
         for (int i = 0; i < per; ++i) {
           prefix[w0 + i] = (unsigned short)run;
           run += __popc(bitmap[w0 + i]);
@@ -667,12 +737,18 @@ k_bucket_emit(const TileFat<K>* __restrict__ fat, const double* __restrict__ phi
       else __syncthreads();
       // kept sums -> rank order in the staging area
 #pragma unroll
-      for (int k = 0; k < kHeld; ++k) {
-        if (held[k] != 0.0) {
-          const u32 y = held_y[k];
-          const u32 r = (u32)prefix[y >> 5] + __popc(bitmap[y >> 5] & ((1u << (y & 31u)) - 1u));
-          st_key[r] = (unsigned short)y;
-          st_lam[r] = held[k];
+      for (int t = 0; t < kTrip; ++t) {
+        if ((u32)t < n_tiles_unit) {              // uniform
+#pragma unroll
+          for (int k = 0; k < kBRows; ++k) {
+            const double v = held[t * kBRows + k];
+            if (v != 0.0) {
+              const u32 y = held_y[t * kBRows + k];
+              const u32 r = (u32)prefix[y >> 5] + __popc(bitmap[y >> 5] & ((1u << (y & 31u)) - 1u));
+              st_key[r] = (unsigned short)y;
+              st_lam[r] = v;
+            }
+          }
         }
       }
     } else {
@@ -704,7 +780,7 @@ k_bucket_emit(const TileFat<K>* __restrict__ fat, const double* __restrict__ phi
     pending = true;
     pend_idx = unit - u_lo;
     pend_kept = kept_total;
-    pend_top = (sort_key[t_begin] & top_mask) << ell;
+    pend_top = (unit_top & top_mask) << ell;
   }
   if (pending) {
     __syncthreads();
@@ -833,7 +909,7 @@ int bucket_step(qx_store* s, const OperatorTable& ct, const ImageTable<K>& im, i
                         bpadded(8 * (int64_t)n_phi) + 4 * bpadded(8 * (int64_t)n_tiles) + 2 * 256 +
                         bpadded(4 * ((int64_t)n_tiles + 1)) + bpadded(4 * (int64_t)n_seg) +
                         bpadded(8 * (scan_tiles + 1)) + 256 + bpadded(8 * ((int64_t)n_tiles + 1)) + 256 +
-                        bpadded((int64_t)sizeof(TileFat<K>) * (int64_t)n_tiles);
+                        bpadded((int64_t)sizeof(TileFat<K>) * (int64_t)n_tiles) + bpadded(16 * ((int64_t)n_tiles + 1));
   void* block = nullptr;
   QX_TRY(qx_dev_alloc(&block, bytes, s->stream, s->device));
   struct Release {
@@ -855,6 +931,7 @@ int bucket_step(qx_store* s, const OperatorTable& ct, const ImageTable<K>& im, i
   u64* unit_status = bcarve<u64>(cur, (int64_t)n_tiles + 1);
   u32* ticket = bcarve<u32>(cur, 2);
   TileFat<K>* d_fat = bcarve<TileFat<K>>(cur, (int64_t)n_tiles);
+  UnitHdr* d_units = bcarve<UnitHdr>(cur, (int64_t)n_tiles + 1);
 
   // groups and the offsets of the one-segment tile sort: host -> device through pinned staging
   const int64_t stage_bytes = (int64_t)sizeof(BGroup<K>) * (ng + 1) + 16;
@@ -905,7 +982,7 @@ int bucket_step(qx_store* s, const OperatorTable& ct, const ImageTable<K>& im, i
                                                             unit_tile0, seg_first, scan_status, info);
     QX_CUDA(cudaGetLastError());
     k_unit_sizes<<<(unsigned)std::max<int64_t>(1, std::min<int64_t>(((int64_t)n_tiles + 255) / 256, 1024)), 256, 0, s->stream>>>(
-        unit_tile0, svals[sorted], info);
+        unit_tile0, skeys[sorted], svals[sorted], reinterpret_cast<uint4*>(d_units), info);
     QX_CUDA(cudaGetLastError());
   }
   QX_TRY(qx_readback(s->stream, s->h_pinned, reinterpret_cast<const int64_t*>(info), 2));
@@ -931,8 +1008,8 @@ int bucket_step(qx_store* s, const OperatorTable& ct, const ImageTable<K>& im, i
     QX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, kBThreads, smem));
     per_sm = std::max(per_sm, 1);
     const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)u_hi - u_lo, (int64_t)s->sm_count * per_sm));
-    kernel<<<grid, kBThreads, smem, s->stream>>>(d_fat, d_phi, skeys[sorted], unit_tile0, u_lo, u_hi, skey, keys_out,
-                                                  s->lam[out], unit_status, ticket, ell, top_bits, cap, eps, ct, im);
+    kernel<<<grid, kBThreads, smem, s->stream>>>(d_fat, d_phi, d_units, u_lo, u_hi, skey, keys_out, s->lam[out],
+                                                  unit_status, ticket, ell, top_bits, cap, eps, ct, im);
     QX_CUDA(cudaGetLastError());
     return QX_OK;
   };

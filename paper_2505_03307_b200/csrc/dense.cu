@@ -989,6 +989,20 @@ extern "C" int qx_operator_classes(int32_t n_qubits, const int32_t* counts, cons
   return QX_OK;
 }
 
+namespace {
+int g_bucket_on = -1;          // -1: not decided yet (QX_NO_BUCKET in the environment switches it off)
+bool bucket_enabled() {
+  if (g_bucket_on < 0) g_bucket_on = getenv("QX_NO_BUCKET") ? 0 : 1;
+  return g_bucket_on != 0;
+}
+}  // namespace
+
+extern "C" int qx_bucket_enable(int32_t on) {
+  const int before = bucket_enabled() ? 1 : 0;
+  g_bucket_on = on ? 1 : 0;
+  return before;
+}
+
 extern "C" int qx_bucket_last(int64_t out[8]) {
   QX_REQUIRE(out != nullptr, "NULL argument");
   const qxb::BucketStats& st = qxb::bucket_stats();
@@ -1089,8 +1103,8 @@ int qx_dense_operator_step(qx_store* s, const OperatorTable& nz, const uint32_t*
   }
   // slot offsets of the generators + totals -> host (sizes the output); the groups go along for
   // the planner of the bucketed step
-  static const bool no_bucket = getenv("QX_NO_BUCKET") != nullptr;
-  const bool bucket_ok = !no_bucket && eps > 0.0 && s->want_narrow != 2;
+  const bool bucket_ok = bucket_enabled() && eps > 0.0 && s->want_narrow != 2;
+  qxb::bucket_stats().cap = 0;
   u64* h_groups = nullptr;
   struct ReleasePinned {
     void* p;
