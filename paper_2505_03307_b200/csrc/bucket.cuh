@@ -348,8 +348,11 @@ __device__ __noinline__ u64 bucket_resolve(u64* status, u32 idx, u64 kept) {
 // before it: the CTA does not wait -- it publishes the count, keeps the ranked terms in shared
 // memory, goes on with its NEXT bucket (whose sums stay in registers meanwhile) and writes the
 // previous one out after that, when its predecessors have long published theirs.
+#ifndef QX_BUCKET_MINB
+#define QX_BUCKET_MINB 4
+#endif
 template <typename K, typename KO>
-__global__ void __launch_bounds__(kBThreads, 4)
+__global__ void __launch_bounds__(kBThreads, QX_BUCKET_MINB)
 k_bucket_emit(const TileFat<K>* __restrict__ fat, const double* __restrict__ phi,
               const UnitHdr* __restrict__ units, u32 u_lo, u32 u_hi, const u64* __restrict__ skey,
               KO* __restrict__ keys_out, double* __restrict__ lam_out, u64* __restrict__ status,
