@@ -20,14 +20,15 @@ any exact method).
   cpu_baseline  the numpy oracle port on the host cores over a bounded sample (a subset of the
             same circuit's generators -- they evolve independently), same unit
 
-N > 1 (torchrun), default --scaling weak: every rank evolves one whole circuit instance of the
-workload (same ansatz and shape, its own rotation angles), so per-GPU work is fixed and value is
-the sum of the ranks' update counts over the slowest rank's time.  --scaling strong: ONE circuit;
-every rank evolves it up to the last branching operator (a negligible share of the work) and then
-works off its own contiguous range of that operator's output slots (dist.run_slot_partitioned:
-even split however skewed the generators are; generator sharding caps at ~3x here because
-generator 0 holds a third of the terms).  Either way there is no data-path collective; the only
-NCCL traffic is the barrier and the max/sum of scalars (the shares' counts in strong mode).
+N > 1 (torchrun), default --scaling strong: ONE circuit; every rank evolves it up to the last
+branching operator (a negligible share of the work) and then works off its own contiguous range
+of that operator's buckets, i.e. of (generator, key) order (dist.run_slot_partitioned: even split
+however skewed the generators are; generator sharding caps at ~3x here because generator 0 holds
+a third of the terms).  --scaling weak (replicas, only on request): every rank evolves one whole
+circuit instance of the workload (same ansatz and shape, its own rotation angles), so per-GPU work
+is fixed and value is the sum of the ranks' update counts over the slowest rank's time.  Either
+way there is no data-path collective; the only NCCL traffic is the barrier, the agreement on
+errors and the max/sum of scalars (the shares' counts in strong mode).
 --impl reference runs the CPU arm.
 """
 
@@ -374,11 +375,12 @@ def run_ours(args):
                    "term_gate_updates": total_updates, "final_terms": int(sum(final_ranks)),
                    "parallelism": (f"{world} circuit instance(s), one per GPU, all generators of an instance on its GPU"
                                    if (weak or world == 1) else
-                                   f"one circuit, output slots of the last operator split over {world} GPUs"),
+                                   f"one circuit, buckets of the last operator split over {world} GPUs"),
                    "l2": "inputs larger than L2: every pass streams 2-5 GB per GPU, L2 is 126 MB"},
         "e2e": {"value": total_updates / e2e_s, "unit": "updates/s", "ms_per_step": e2e_s * 1e3,
                 "h2d_bytes_per_step": table_bytes(n, gates), "d2h_bytes_per_step": d2h},
         "gpu_launches": launches,
+        "ranks": {"world": world, "backend": backend if world > 1 else None},
         "clocks": clocks.summary(),
         "roofline": roof,
         "cpu_baseline": cpu,
@@ -397,8 +399,9 @@ def main():
     ap.add_argument("--workload", default=DEFAULT_WORKLOAD)
     ap.add_argument("--mode", default="v3")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
-    ap.add_argument("--scaling", default="weak", choices=("weak", "strong"),
-                    help="N > 1: one circuit instance per GPU (weak) or one circuit's generators sharded (strong)")
+    ap.add_argument("--scaling", default="strong", choices=("weak", "strong"),
+                    help="N > 1: ONE circuit, the buckets of its last operator split over the GPUs (strong, the "
+                         "north star's sharding; default) or replicas, one circuit instance per GPU (weak)")
     args = ap.parse_args()
     if args.impl == "reference":
         # update counts of the sample come from the fixture table (no GPU on this arm)

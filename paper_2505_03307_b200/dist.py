@@ -79,6 +79,32 @@ def _comm_device(group=None):
     return torch.device("cuda", torch.cuda.current_device()) if "nccl" in str(backend) else torch.device("cpu")
 
 
+class RemoteRankError(RuntimeError):
+    """Another rank of the job failed; raised on the ranks that did not, so that nobody is left
+    waiting in a collective."""
+
+
+def agree_on_errors(exc, group=None):
+    """Every rank calls this with its own exception (or None) BEFORE the next collective.  If any
+    rank failed, all of them raise: the failing ranks their own exception, the others a
+    ``RemoteRankError`` naming the first failing rank and its message.  One small all-gather."""
+    dist = _dist()
+    world, rank = dist.get_world_size(group), dist.get_rank(group)
+    mine = None if exc is None else (type(exc).__name__, str(exc))
+    if world == 1:
+        everyone = [mine]
+    else:
+        everyone = [None] * world
+        dist.all_gather_object(everyone, mine, group=group)
+    failed = [(r, e) for r, e in enumerate(everyone) if e is not None]
+    if not failed:
+        return
+    if exc is not None:
+        raise exc
+    r, (kind, msg) = failed[0]
+    raise RemoteRankError(f"rank {r} failed with {kind}: {msg} (this is rank {rank})")
+
+
 def run_sharded(instructions, n: int, mode, eps: float = 1e-12, *, weights=None, gather: bool = True,
                 group=None, runner=None, **run_kw):
     """Generator-sharded run.  Returns (report, shards).
@@ -96,7 +122,12 @@ def run_sharded(instructions, n: int, mode, eps: float = 1e-12, *, weights=None,
     world, rank = dist.get_world_size(group), dist.get_rank(group)
     shards = lpt_shards(weights if weights is not None else [1.0] * n, world)
     mine = shards[rank]
-    report = runner(instructions, n, mode, eps, generators=mine, **run_kw) if mine else None
+    report, failure = None, None
+    try:
+        report = runner(instructions, n, mode, eps, generators=mine, **run_kw) if mine else None
+    except Exception as exc:          # a shard's collapse / resource error: the others must not wait for it
+        failure = exc
+    agree_on_errors(failure, group)
 
     dev = _comm_device(group)
     # ---- rank trace: every rank contributes its columns (a few integers per step)
@@ -139,18 +170,35 @@ def run_slot_partitioned(instructions, n: int, mode, eps: float = 1e-12, *, grou
     """
     import torch
 
+    from .errors import NumericalCollapseError
+
     dist = _dist()
     if runner is None:
         from .engine import run as runner
     world, rank = dist.get_world_size(group), dist.get_rank(group)
     dev = _comm_device(group)
-
-    def reduce(ranks):
-        t = torch.tensor(ranks, dtype=torch.int64, device=dev)
+    # No collective inside the run: a rank that fails (out of memory, ...) would otherwise leave
+    # the others waiting in it.  The shares' counts are summed afterwards, behind an agreement
+    # on errors, and the trace rows the share filled in are patched with the global ranks.
+    report, failure = None, None
+    try:
+        report = runner(instructions, n, mode, eps, slot_part=(rank, world), slot_reduce=None, **run_kw)
+    except Exception as exc:
+        failure = exc
+    agree_on_errors(failure, group)
+    rows = report.device.get("partition_rows") or []
+    if report.device.get("partitioned") and rows:
+        t = torch.tensor(report.rank_trace[rows[0]], dtype=torch.int64, device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.SUM, group=group)
-        return t.cpu().tolist()
-
-    return runner(instructions, n, mode, eps, slot_part=(rank, world), slot_reduce=reduce, **run_kw)
+        total = t.cpu().tolist()
+        for row in rows:
+            report.rank_trace[row] = list(total)
+        for g, r in enumerate(total):
+            if r == 0:
+                raise NumericalCollapseError(
+                    f"all terms of generator {g} dropped at operator step {report.device.get('partition_step')}"
+                )
+    return report
 
 
 def _gather_generators(report, mine, shards, n, dev, group):
@@ -250,7 +298,12 @@ def exchange_terms(store, group=None):
     else:
         keys = torch.empty(0, dtype=torch.int64, device=dev)
         lam = torch.empty(0, dtype=torch.float64, device=dev)
-    recv_keys, recv_lam, recv_counts = exchange_partitioned(keys, lam, counts, group)
+    if _comm_device(group).type == "cpu":
+        # gloo (tests: several ranks sharing one GPU): the collective runs on host copies
+        rk, rl, recv_counts = exchange_partitioned(keys.cpu(), lam.cpu(), counts, group)
+        recv_keys, recv_lam = rk.to(dev), rl.to(dev)
+    else:
+        recv_keys, recv_lam, recv_counts = exchange_partitioned(keys, lam, counts, group)
     torch.cuda.current_stream(dev).synchronize()
     store.assemble(recv_keys.data_ptr(), recv_lam.data_ptr(), recv_counts)
     return recv_counts

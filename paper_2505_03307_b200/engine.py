@@ -117,6 +117,8 @@ class _Walker:
         self.ranks = [1] * len(self.ids)
         self.launch_log = {"clifford_runs": 0, "branch_ops": 0, "merges": 0, "sorts": 0}
         self.updates = None            # v1 only: term-gate updates per generator
+        self.partition_rows = []       # slot-partitioned finish: trace rows that hold this share's counts
+        self.partition_step = None
 
     # -- queue ---------------------------------------------------------------------
     def push_perm(self, qubit: int, table: int):
@@ -334,6 +336,9 @@ def run(instructions: Sequence[Instruction], n: int, mode, eps: float = DEFAULT_
         info = {"device": store.device, **w.launch_log}
         if partitioned is not None:
             info["partitioned"] = partitioned
+            if w.partition_step is not None:
+                info["partition_rows"] = w.partition_rows
+                info["partition_step"] = w.partition_step
         if w.updates is not None:
             w.book_gates()
             info["updates_per_generator"] = w.updates.tolist()
@@ -466,6 +471,11 @@ def _finish_partitioned(w: _Walker, trace, slot_part, slot_reduce):
                 )
     for slot in w.open_slots:
         trace[slot] = list(w.ranks)
+    if partitioned and slot_reduce is None and parts > 1:
+        # the caller sums the shares' counts itself (dist.run_slot_partitioned): these rows and the
+        # rows appended from now on hold this share's counts
+        w.partition_rows = list(w.open_slots)
+        w.partition_step = step
     w.open_slots = []
     if w.updates is not None and w.pending_gates:
         w.updates += np.asarray(w.ranks, dtype=np.int64) * w.pending_gates
@@ -669,7 +679,12 @@ def _walk_operators(partition, lut, is_perm, tables, w: _Walker, trace, counters
                     # dense layout: a branching substitution needs a 4**n scatter buffer
                     # (reference stabilizer.py:264-276); one-hot rows take the fast path
                     raw = w.store.count_operator(counts)
-                    if any(r > have for r, have in zip(raw, w.store.ranks())):
+                    over = any(r > have for r, have in zip(raw, w.store.ranks()))
+                    if w.reduce_ranks is not None:
+                        # term-partitioned runs: a rank that holds no branching term of a generator
+                        # must raise too, or it would wait for the others in the next collective
+                        over = w.reduce_ranks([int(over)])[0] > 0
+                    if over:
                         raise ResourceLimitError(
                             f"dense flatten needs a 4**{n}-element buffer (> {DENSE_FLATTEN_BUDGET}); "
                             "use the ragged layout for circuits of this size"

@@ -62,13 +62,15 @@ def _worker(rank, world, port, out_dir):
         report, shards = qd.run_sharded(workloads.gen_ghz(1) if False else [], 1, "v1", runner=_fake_runner)
         assert report.rank_trace == [[1]] and int(report.final.generators[0].indices[0]) == 3
 
-        # ---- slot-partitioned run: the runner gets (rank, world) and a reduction that sums the
-        # shares' counts over the ranks; the fake answers with an index-range share of the
-        # oracle's result (what the device's slot ranges amount to after the sort)
+        # ---- slot-partitioned run: the runner gets (rank, world) and does NO collective; the fake
+        # answers with an index-range share of the oracle's result (what the device's bucket
+        # ranges amount to) and names the trace rows that hold its share's counts; the driver sums
+        # them over the ranks behind an agreement on errors
         def _slot_runner(instructions, n, mode, eps=1e-12, *, slot_part=None, slot_reduce=None, **kw):
             from paper_2505_03307_b200.engine import Mode, RunReport, _Shard
             from paper_2505_03307_b200.stabilizer import SimpleGenerator, keys_to_indices
 
+            assert slot_reduce is None
             part, parts = slot_part
             res = oracle.run(instructions, n, mode, eps)
             gens, local = [], []
@@ -76,9 +78,10 @@ def _worker(rank, world, port, out_dir):
                 sel = np.arange(len(idx)) % parts == part
                 gens.append(SimpleGenerator(n, lam[sel], keys_to_indices(idx[sel], n)))
                 local.append(int(sel.sum()))
-            trace = res["rank_trace"][:-1] + [slot_reduce(local)]
+            trace = res["rank_trace"][:-1] + [local]
             return RunReport(Mode.coerce(mode), n, _Shard(n, list(range(n)), gens), trace, {}, res["counters"],
-                             res["k"], res["k_prime"], res["order"], {"partitioned": True})
+                             res["k"], res["k_prime"], res["order"],
+                             {"partitioned": True, "partition_rows": [len(trace) - 1], "partition_step": len(trace) - 2})
 
         rep = qd.run_slot_partitioned(gates, n, "v3", runner=_slot_runner)
         assert rep.rank_trace == want["rank_trace"] and rep.device["partitioned"] is True
@@ -86,6 +89,27 @@ def _worker(rank, world, port, out_dir):
         t = torch.tensor([mine], dtype=torch.int64)
         dist.all_reduce(t)
         assert int(t.item()) == sum(want["rank_trace"][-1])
+
+        # ---- a failure on ONE rank reaches every rank instead of leaving the others in a collective
+        def _failing_runner(instructions, n, mode, eps=1e-12, **kw):
+            if rank == 1:
+                raise ResourceLimitError("out of memory on this rank only")
+            return _slot_runner(instructions, n, mode, eps, **kw)
+
+        from paper_2505_03307_b200.errors import ResourceLimitError
+
+        with pytest.raises((ResourceLimitError, qd.RemoteRankError)) as caught:
+            qd.run_slot_partitioned(gates, n, "v3", runner=_failing_runner)
+        assert (caught.type is ResourceLimitError) == (rank == 1)
+        assert rank == 1 or "rank 1 failed with ResourceLimitError" in str(caught.value)
+
+        def _failing_shard(instructions, n, mode, eps=1e-12, *, generators=None, **kw):
+            if 0 in generators:
+                raise ResourceLimitError("this shard ran out of memory")
+            return _fake_runner(instructions, n, mode, eps, generators=generators, **kw)
+
+        with pytest.raises((ResourceLimitError, qd.RemoteRankError)):
+            qd.run_sharded(gates, n, "v3", weights=weights, runner=_failing_shard)
 
         # ---- observable-parallel read-out: words dealt round-robin, one all-reduce of the scalars
         n5, circ = 5, workloads.gen_random(5, 40, 11)
