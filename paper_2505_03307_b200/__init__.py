@@ -12,8 +12,11 @@ from .circuit import CircuitParseError, Instruction, divide_instruction, parse_c
 from .engine import AgreementReport, Mode, RunReport, compare_reports, run, run_all_modes
 from .errors import ConsistencyError, NativeError, NumericalCollapseError, ResourceLimitError
 from .measure import PauliExpansion, density_expansion, expectation, expectation_heisenberg, prob_z
+from .pauli import Axis
 from .stabilizer import (
+    DenseComplexGenerator,
     GeneratorSet,
+    RaggedComplexGenerator,
     generator_set_to_dict,
     SimpleGenerator,
     apply_1q,
@@ -29,7 +32,7 @@ from .workloads import gen_ghz, gen_graph, gen_random, gen_xyz_chain, near_cliff
 __version__ = "0.1.0"
 
 __all__ = [
-    "AgreementReport", "CircuitParseError", "ConsistencyError", "GeneratorSet", "Instruction", "Mode", "NativeError",
+    "AgreementReport", "Axis", "CircuitParseError", "DenseComplexGenerator", "RaggedComplexGenerator", "ConsistencyError", "GeneratorSet", "Instruction", "Mode", "NativeError",
     "NumericalCollapseError", "PauliExpansion", "ResourceLimitError", "RunReport", "SimpleGenerator",
     "apply_1q", "apply_cx", "canonicalize", "compare_reports", "density_expansion",
     "divide_instruction", "expectation", "expectation_heisenberg", "flatten", "gen_ghz", "gen_graph",

@@ -1242,7 +1242,9 @@ int qx_dense_operator_step(qx_store* s, const OperatorTable& nz, const uint32_t*
     const int passes_now = std::min(qxm::kMaxPasses, (2 * s->n_qubits + QX_RADIX_BITS - 1) / QX_RADIX_BITS);
     const int out_buf = mb.cur ^ (passes_now & 1);            // the buffer the last pass writes
     const int64_t lo_bytes = (2 * total + 255) / 256 * 256;
-    if (keep_narrow && s->want_narrow == 2 && total >= 8ll * n_seg * QX_PACK_BUCKETS &&
+    // positions inside a generator are 32-bit in the bucket table: a generator of 2^32 terms
+    // (n = 16, every word present) keeps 32-bit keys instead
+    if (keep_narrow && s->want_narrow == 2 && total >= 8ll * n_seg * QX_PACK_BUCKETS && ub_seg < (1ll << 32) - 1 &&
         lo_bytes + bnd_bytes <= 8 * s->cap)
       pack_bnd = reinterpret_cast<u32*>(reinterpret_cast<char*>(s->keys[out_buf]) + lo_bytes);
   }

@@ -141,7 +141,7 @@ int reserve(qx_expansion* e, int64_t terms) {
 int multiply_device(qx_expansion* e, const u64* d_keys, const double* d_lam, int64_t ng,
                     int64_t term_budget) {
   const int64_t raw = e->count * (1 + ng);
-  if (term_budget > 0 && raw > term_budget)
+  if (term_budget >= 0 && raw > term_budget)      // negative: no budget (the reference has no such value)
     return qx_fail(QX_ERR_RESOURCE, "density expansion exceeded the term budget (%lld)",
                    (long long)term_budget);
   QX_TRY(reserve(e, raw));

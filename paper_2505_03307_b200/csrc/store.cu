@@ -768,7 +768,8 @@ void join_workers(qx_store* s) {
   HostWorkers* hw = static_cast<HostWorkers*>(s->host_workers);
   if (!hw) return;
   for (std::thread& t : hw->threads) t.join();
-  for (cudaEvent_t e : hw->events) cudaEventDestroy(e);
+  for (cudaEvent_t e : hw->events)
+    if (e) cudaEventDestroy(e);
   delete hw;
   s->host_workers = nullptr;
 }
@@ -801,7 +802,8 @@ extern "C" int qx_store_download_narrow_async(qx_store* s, int64_t* offsets, uin
   const int n_chunks = (int)std::max<int64_t>(1, std::min<int64_t>(max_chunks, total / (1 << 20)));
   const int64_t chunk = (total + n_chunks - 1) / n_chunks;
   HostWorkers* hw = new HostWorkers();
-  hw->events.resize(n_chunks);
+  hw->events.resize(n_chunks, nullptr);
+  s->host_workers = hw;             // owned by the store from here on: an error below cannot leak it
   const u32* d_keys = reinterpret_cast<const u32*>(s->keys[s->cur]);
   for (int c = 0; c < n_chunks; ++c) {
     const int64_t lo = c * chunk, len = std::min(chunk, total - lo);
@@ -872,7 +874,8 @@ extern "C" int qx_store_download_packed_async(qx_store* s, int64_t* offsets, uin
   const int n_chunks = (int)std::max<int64_t>(1, std::min<int64_t>(max_chunks, total / (1 << 20)));
   const int64_t chunk = (total + n_chunks - 1) / n_chunks;
   HostWorkers* hw = new HostWorkers();
-  hw->events.resize(n_chunks);
+  hw->events.resize(n_chunks, nullptr);
+  s->host_workers = hw;             // owned by the store from here on: an error below cannot leak it
   QX_CUDA(cudaMemcpyAsync(h_bnd, s->pack_bnd, sizeof(u32) * (size_t)bnd_words, cudaMemcpyDeviceToHost, s->stream));
   const unsigned short* d_lo = reinterpret_cast<const unsigned short*>(s->keys[s->cur]);
   for (int c = 0; c < n_chunks; ++c) {

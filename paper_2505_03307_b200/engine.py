@@ -281,6 +281,8 @@ def run(instructions: Sequence[Instruction], n: int, mode, eps: float = DEFAULT_
     timings = {"partition": 0.0, "lut": 0.0, "sub_flatten": 0.0, "cx": 0.0}
     counters = {"gates": len(instructions), "sub_flatten_ops": 0, "cx_applications": 0}
 
+    if n < 1:
+        raise ValueError(f"qubit count must be positive, got {n}")
     t0 = time.perf_counter()
     partition = divide_instruction(instructions, n)
     timings["partition"] = time.perf_counter() - t0
@@ -291,10 +293,9 @@ def run(instructions: Sequence[Instruction], n: int, mode, eps: float = DEFAULT_
         ids = list(range(n)) if generators is None else [int(g) for g in generators]
         if any(g < 0 or g >= n for g in ids):
             raise ValueError(f"generator ids {ids} out of range for n={n}")
-    if n < 1:
-        raise ValueError(f"qubit count must be positive, got {n}")
 
     store = DeviceStore(n, max(len(ids), 1), capacity, device)
+    handed_over = False
     try:
         if initial is not None:
             store.upload(initial)
@@ -350,11 +351,14 @@ def run(instructions: Sequence[Instruction], n: int, mode, eps: float = DEFAULT_
             final = GeneratorSet(n, final_gens) if whole else _Shard(n, ids, final_gens)
         else:
             info["store"] = store
+            handed_over = True
         return RunReport(mode=mode, n=n, final=final, rank_trace=trace, timings=timings,
                          counters=counters, k=partition.k, k_prime=partition.k_prime,
                          order=list(partition.order), device=info)
     finally:
-        if download:
+        # the store leaves with the report only on success; an error frees its HBM right away
+        # instead of leaving it to the garbage collector (a retry near the capacity limit)
+        if not handed_over:
             store.close()
 
 

@@ -44,6 +44,20 @@ def axis_map(gate: str, theta: float = 0.0) -> np.ndarray:
     return np.array(rows)
 
 
+def conjugate_axis(gate: str, theta: float, w) -> np.ndarray:
+    """One gate on an (X, Y, Z) weight row (reference lut.py:55-64); the identity component never
+    appears: conjugation fixes I and no axis acquires an I part."""
+    w = np.asarray(w, dtype=float)
+    if w.shape != (3,):
+        raise ValueError(f"weight row must have 3 components, got shape {w.shape}")
+    return axis_map(gate, theta) @ w
+
+
+def lut_to_json(lut: np.ndarray) -> list:
+    """Nested lists of a LUT tensor (reference lut.py:142-144)."""
+    return np.asarray(lut).tolist()
+
+
 def compose_block(gates) -> np.ndarray:
     """One U_{k,j} block: row p = image of axis p after all gates in circuit order.
 

@@ -36,8 +36,14 @@ class PauliExpansion:
     dict view on demand.
     """
 
-    def __init__(self, n: int, codes: np.ndarray, values: np.ndarray):
+    def __init__(self, n: int, codes, values=None):
+        # reference signature: PauliExpansion(n, coeffs: dict) (measure.py:31-33); the device
+        # read-out hands over the sorted arrays directly
         self.n = n
+        if values is None:
+            items = sorted((int(c), float(v)) for c, v in dict(codes).items())
+            codes = np.array([c for c, _ in items], dtype=np.uint64)
+            values = np.array([v for _, v in items], dtype=np.float64)
         self.codes = codes
         self.values = values
         self._dict = None
@@ -75,8 +81,10 @@ def density_expansion(gs: GeneratorSet, max_qubits: int = DENSITY_MAX_QUBITS,
         for g in gs.generators:
             keys = np.ascontiguousarray(indices_to_keys(g.indices, n))
             lam = np.ascontiguousarray(g.lambdas, dtype=np.float64)
+            # reference measure.py:59: raise as soon as the raw list is longer than the budget,
+            # whatever the budget (0 or negative budgets fail on the first generator)
             nat.check(lib.qx_expansion_multiply(handle, nat.ptr(keys), nat.ptr(lam), len(lam),
-                                                int(term_budget)))
+                                                max(int(term_budget), 0)))
         worst = C.c_double()
         nat.check(lib.qx_expansion_max_abs_imag(handle, C.byref(worst)))
         if worst.value > _IMAG_TOL:

@@ -15,7 +15,7 @@ gates instead of round-tripping per call.
 
 from __future__ import annotations
 
-from dataclasses import dataclass
+from dataclasses import dataclass, field
 
 import numpy as np
 
@@ -205,40 +205,143 @@ def split_tables(block: np.ndarray) -> tuple:
     return a1, w1, a2, w2
 
 
-@dataclass(eq=False)
-class ComplexForm:
-    """A generator with one U_k block substituted but not yet flattened.
+def indices_to_digits(indices: np.ndarray, n: int) -> np.ndarray:
+    """Packed word indices -> (S, n) axis codes, qubit 0 first (reference stabilizer.py:62-69)."""
+    idx = np.asarray(indices)
+    out = np.empty((len(idx), n), dtype=np.int64)
+    if idx.dtype == object or n > _INT64_MAX_QUBITS:
+        for s, v in enumerate(idx):
+            v = int(v)
+            for j in range(n):
+                out[s, j] = (v >> (2 * (n - 1 - j))) & 3
+        return out
+    vals = idx.astype(np.int64)
+    for j in range(n):
+        out[:, j] = (vals >> np.int64(2 * (n - 1 - j))) & np.int64(3)
+    return out
 
-    Stands in for the reference's Dense/RaggedComplexGenerator
-    (stabilizer.py:112-154): on the device the (S, n, 4) weight tensor is never
-    materialised, so this only records the operands; ``flatten`` runs the
-    expansion kernel.
-    """
+
+def digits_to_indices(digits: np.ndarray, n: int) -> np.ndarray:
+    """(S, n) axis codes -> packed word indices (reference stabilizer.py:72-80)."""
+    digits = np.asarray(digits)
+    if index_dtype(n) is object:
+        out = np.empty(len(digits), dtype=object)
+        for s in range(len(digits)):
+            v = 0
+            for j in range(n):
+                v = (v << 2) | int(digits[s, j])
+            out[s] = v
+        return out
+    acc = np.zeros(len(digits), dtype=np.int64)
+    for j in range(n):
+        acc = (acc << np.int64(2)) | digits[:, j].astype(np.int64)
+    return acc
+
+
+@dataclass(eq=False)
+class DenseComplexGenerator:
+    """Complex form, dense layout: (S, n, 4) zero-padded weights (reference stabilizer.py:112-120).
+
+    A host-side view for callers and tests: ``sub`` fills it in, ``flatten`` takes it back.  The
+    engine never builds it -- on the device the (S, n, 4) tensor is never materialised (a4)."""
 
     n: int
     lambdas: np.ndarray
-    keys: np.ndarray
-    block: np.ndarray
-    layout: str = "ragged"
+    weights: np.ndarray
+    _source: tuple = field(default=None, repr=False)
+
+    layout = "dense"
 
 
-def sub(g: SimpleGenerator, block: np.ndarray, layout: str = "ragged") -> ComplexForm:
-    """Substitute an (n, 3, 3) operator block (reference stabilizer.py:189-206)."""
+@dataclass(eq=False)
+class RaggedComplexGenerator:
+    """Complex form, ragged layout (reference stabilizer.py:123-154): nonzero weights and their axis
+    codes of all (string, qubit) cells in C order, ``counts[s, j]`` entries per cell, ascending
+    axes inside a cell, no zero stored."""
+
+    n: int
+    lambdas: np.ndarray
+    values: np.ndarray
+    axes: np.ndarray
+    counts: np.ndarray
+    _offsets: np.ndarray = field(default=None, repr=False)
+    _source: tuple = field(default=None, repr=False)
+
+    layout = "ragged"
+
+    @property
+    def offsets(self) -> np.ndarray:
+        if self._offsets is None:
+            flat = self.counts.astype(np.int64).ravel()
+            self._offsets = (np.cumsum(flat) - flat).reshape(self.counts.shape)
+        return self._offsets
+
+    def entries(self, s: int, j: int) -> tuple:
+        """(axis codes, weights) of string s at qubit j."""
+        lo = int(self.offsets[s, j])
+        hi = lo + int(self.counts[s, j])
+        return self.axes[lo:hi], self.values[lo:hi]
+
+
+ComplexForm = (DenseComplexGenerator, RaggedComplexGenerator)
+
+
+def _ragged_from_weights(n: int, lambdas: np.ndarray, weights: np.ndarray, source=None) -> RaggedComplexGenerator:
+    nz = weights != 0.0
+    return RaggedComplexGenerator(n, lambdas, weights[nz], np.nonzero(nz)[2].astype(np.uint8),
+                                  nz.sum(axis=2).astype(np.uint8), None, source)
+
+
+def to_ragged(g: DenseComplexGenerator) -> RaggedComplexGenerator:
+    """Dense layout -> ragged layout (reference stabilizer.py:217-219)."""
+    return _ragged_from_weights(g.n, g.lambdas.copy(), g.weights)
+
+
+def to_dense(g: RaggedComplexGenerator) -> DenseComplexGenerator:
+    """Ragged layout -> dense layout (reference stabilizer.py:222-229)."""
+    s = len(g.lambdas)
+    weights = np.zeros((s, g.n, 4))
+    per_cell = g.counts.astype(np.int64).ravel()
+    cell = np.repeat(np.arange(s * g.n), per_cell)
+    weights[cell // g.n, cell % g.n, g.axes.astype(np.int64)] = g.values
+    return DenseComplexGenerator(g.n, g.lambdas.copy(), weights)
+
+
+def _fingerprint(arr: np.ndarray) -> tuple:
+    return arr.shape, float(np.sum(arr))
+
+
+def sub(g: SimpleGenerator, block: np.ndarray, layout: str = "ragged"):
+    """Substitute an (n, 3, 3) operator block (reference stabilizer.py:189-206): every non-identity
+    axis of every string becomes its conjugated (X, Y, Z) weight row.  The returned form also
+    remembers (keys, block), so that ``flatten`` of an untouched form runs as ONE device expansion
+    with per-qubit tables instead of string by string."""
+    n = g.n
     block = np.asarray(block, dtype=np.float64)
-    if block.shape != (g.n, 3, 3):
-        raise ValueError(f"expected block shape ({g.n}, 3, 3), got {block.shape}")
+    if block.shape != (n, 3, 3):
+        raise ValueError(f"expected block shape ({n}, 3, 3), got {block.shape}")
     if layout not in ("dense", "ragged"):
         raise ValueError(f"unknown layout {layout!r}")
-    return ComplexForm(g.n, g.lambdas.copy(), g.keys(), block.copy(), layout)
+    rows = np.zeros((n, 4, 4))
+    rows[:, 0, 0] = 1.0
+    rows[:, 1:, 1:] = block
+    weights = rows[np.arange(n)[None, :], indices_to_digits(g.indices, n)]
+    if layout == "dense":
+        out = DenseComplexGenerator(n, g.lambdas.copy(), weights)
+        out._source = (g.keys(), block.copy(), _fingerprint(out.weights), _fingerprint(out.lambdas))
+        return out
+    out = _ragged_from_weights(n, g.lambdas.copy(), weights)
+    out._source = (g.keys(), block.copy(), _fingerprint(out.values), _fingerprint(out.lambdas))
+    return out
 
 
-def branch_counts(cg: ComplexForm) -> np.ndarray:
-    """Raw branches the whole generator would expand into (sum of the reference's
-    per-string ``branch_counts``, stabilizer.py:232-237)."""
-    counts, _, _ = _lut.operator_tables(cg.block)
-    with DeviceStore(cg.n, 1, len(cg.lambdas) + 2) as st:
-        st.upload([(cg.lambdas, cg.keys)])
-        return np.array(st.count_operator(counts), dtype=np.int64)
+def branch_counts(g) -> np.ndarray:
+    """Raw branches every string contributes when flattened (reference stabilizer.py:232-237)."""
+    if isinstance(g, RaggedComplexGenerator):
+        return g.counts.astype(np.int64).prod(axis=1)
+    if isinstance(g, DenseComplexGenerator):
+        return (g.weights != 0.0).sum(axis=2).astype(np.int64).prod(axis=1)
+    raise TypeError(f"cannot count the branches of {type(g).__name__}")
 
 
 def pad_dense(st: DeviceStore, n: int, segments) -> None:
@@ -255,7 +358,102 @@ def pad_dense(st: DeviceStore, n: int, segments) -> None:
     st.upload(segs)
 
 
-def flatten(cg: ComplexForm, eps: float = DEFAULT_EPS, canonical: bool = True) -> SimpleGenerator:
+def _untouched_source(g):
+    """(keys, block) of a form that still is what ``sub`` returned, else None."""
+    src = getattr(g, "_source", None)
+    if src is None:
+        return None
+    keys, block, fp_w, fp_l = src
+    body = g.weights if isinstance(g, DenseComplexGenerator) else g.values
+    if _fingerprint(body) != fp_w or _fingerprint(g.lambdas) != fp_l or len(keys) != len(g.lambdas):
+        return None
+    return keys, block
+
+
+def _flatten_block(g, keys, block, eps: float, canonical: bool) -> SimpleGenerator:
+    """flatten(sub(g, block)): one device expansion with per-qubit branch tables."""
+    n = g.n
+    dense = isinstance(g, DenseComplexGenerator)
+    counts, axes, weights = _lut.operator_tables(block)
+    with DeviceStore(n, 1, 2 * len(g.lambdas) + 2) as st:
+        st.upload([(g.lambdas, keys)])
+        if dense and canonical and 4 ** n > DENSE_FLATTEN_BUDGET:
+            if st.count_operator(counts)[0] > len(g.lambdas):
+                raise ResourceLimitError(
+                    f"dense flatten needs a 4**{n}-element buffer (> {DENSE_FLATTEN_BUDGET}); "
+                    "use the ragged layout for circuits of this size"
+                )
+        if not dense or not canonical:
+            st.order_for_operator(counts, by_key=False)      # raw order of _flatten_ragged (:294-296)
+        dense_zeros = (dense and canonical and eps == 0.0
+                       and st.count_operator(counts)[0] > len(g.lambdas))
+        st.apply_operator(counts, axes, weights)
+        if dense_zeros:
+            pad_dense(st, n, [0])
+        if canonical:
+            st.merge(eps)
+        return _fetch(st, n)
+
+
+def _flatten_cells(g: RaggedComplexGenerator, dense: bool, eps: float, canonical: bool) -> SimpleGenerator:
+    """A complex form built cell by cell (every string with weights of its own, as the reference's
+    unit tests do): the device expansion kernel takes per-QUBIT tables, so each string is expanded
+    on its own -- its non-trivial cells become the table rows of a stand-in word -- and the raw
+    lists are concatenated in the reference's order (strings grouped by their branch-count
+    pattern, stable inside a group, stabilizer.py:294-296) and merged on the device."""
+    n, s_count = g.n, len(g.lambdas)
+    counts_all = g.counts.astype(np.int64)
+    if dense and canonical and 4 ** n > DENSE_FLATTEN_BUDGET and np.any(counts_all != 1):
+        raise ResourceLimitError(
+            f"dense flatten needs a 4**{n}-element buffer (> {DENSE_FLATTEN_BUDGET}); "
+            "use the ragged layout for circuits of this size"
+        )
+    if s_count:
+        _, inverse = np.unique(counts_all, axis=0, return_inverse=True)
+        order = np.argsort(np.asarray(inverse).reshape(-1), kind="stable")
+    else:
+        order = []
+    raw_l, raw_k = [np.zeros(0)], [np.zeros(0, dtype=np.uint64 if n <= MAX_QUBITS else object)]
+    for s in order:
+        key = 0
+        lam = float(g.lambdas[s])
+        tab_c = np.ones((n, 3), dtype=np.int32)
+        tab_a = np.tile(np.array([[1, 0, 0], [2, 0, 0], [3, 0, 0]], dtype=np.int32), (n, 1, 1))
+        tab_w = np.zeros((n, 3, 3))
+        tab_w[:, :, 0] = 1.0
+        for j in range(n):
+            ax, vals = g.entries(int(s), j)
+            ax = np.asarray(ax, dtype=np.int64)
+            if len(ax) == 1 and ax[0] == 0:
+                lam = lam * float(vals[0])        # an identity cell: a scalar, exactly 1.0 from sub()
+                continue
+            if len(ax) == 0 or np.any(ax == 0):
+                raise ValueError(f"cell ({s}, {j}) mixes the identity with other axes: not a conjugated Pauli row")
+            key |= 1 << (2 * (n - 1 - j))         # stand-in digit X; its table row is this cell
+            tab_c[j, 0] = len(ax)
+            tab_a[j, 0, :len(ax)] = ax
+            tab_w[j, 0, :] = 0.0
+            tab_w[j, 0, :len(ax)] = vals
+        keys = np.array([key], dtype=np.uint64) if n <= MAX_QUBITS else np.array([key], dtype=object)
+        with DeviceStore(n, 1, 4) as st:
+            st.upload([(np.array([lam]), keys)])
+            st.apply_operator(tab_c, tab_a, tab_w)
+            (l, k), = st.segments()
+            raw_l.append(l.copy())
+            raw_k.append(k.copy())
+    lam_all = np.concatenate(raw_l)
+    keys_all = np.concatenate(raw_k) if n <= MAX_QUBITS else np.array([int(v) for part in raw_k for v in part], dtype=object)
+    raw = SimpleGenerator(n, lam_all, keys_to_indices(keys_all, n) if n <= MAX_QUBITS else keys_all)
+    if not canonical:
+        return raw
+    if dense and eps == 0.0 and np.any(counts_all != 1):
+        every = np.arange(4 ** n, dtype=np.uint64)
+        raw = SimpleGenerator(n, np.concatenate([raw.lambdas, np.zeros(len(every))]),
+                              keys_to_indices(np.concatenate([raw.keys(), every]), n))
+    return canonicalize(raw, eps)
+
+
+def flatten(cg, eps: float = DEFAULT_EPS, canonical: bool = True) -> SimpleGenerator:
     """Expand a complex form back into a simple form (reference stabilizer.py:240-256).
 
     ``canonical=False`` returns the raw branch list in the reference's order (strings grouped by
@@ -265,23 +463,9 @@ def flatten(cg: ComplexForm, eps: float = DEFAULT_EPS, canonical: bool = True) -
     """
     if not isinstance(cg, ComplexForm):
         raise TypeError(f"cannot flatten {type(cg).__name__}")
-    n = cg.n
-    counts, axes, weights = _lut.operator_tables(cg.block)
-    with DeviceStore(n, 1, 2 * len(cg.lambdas) + 2) as st:
-        st.upload([(cg.lambdas, cg.keys)])
-        if cg.layout == "dense" and canonical and 4 ** n > DENSE_FLATTEN_BUDGET:
-            if st.count_operator(counts)[0] > len(cg.lambdas):
-                raise ResourceLimitError(
-                    f"dense flatten needs a 4**{n}-element buffer (> {DENSE_FLATTEN_BUDGET}); "
-                    "use the ragged layout for circuits of this size"
-                )
-        if cg.layout == "ragged" or not canonical:
-            st.order_for_operator(counts, by_key=False)      # raw order of _flatten_ragged (:294-296)
-        dense_zeros = (cg.layout == "dense" and canonical and eps == 0.0
-                       and st.count_operator(counts)[0] > len(cg.lambdas))
-        st.apply_operator(counts, axes, weights)
-        if dense_zeros:
-            pad_dense(st, n, [0])
-        if canonical:
-            st.merge(eps)
-        return _fetch(st, n)
+    src = _untouched_source(cg)
+    if src is not None:
+        return _flatten_block(cg, src[0], src[1], eps, canonical)
+    if isinstance(cg, DenseComplexGenerator):
+        return _flatten_cells(to_ragged(cg), True, eps, canonical)
+    return _flatten_cells(cg, False, eps, canonical)
