@@ -117,6 +117,16 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
+def job_config(name, mode, n, n_gates, total_updates, final_terms, world, strong):
+    """The `config` object of BOTH arms (ours and --impl reference): what the job is, nothing
+    about how an arm runs it (the CPU arm's bounded sample is described in its cpu_baseline)."""
+    return {"workload": name, "mode": mode, "qubits": n, "gates": n_gates,
+            "term_gate_updates": float(total_updates), "final_terms": int(final_terms),
+            "parallelism": (f"one circuit, buckets of the last operator split over {world} GPUs" if strong else
+                            f"{world} circuit instance(s), one per GPU, all generators of an instance on its GPU"),
+            "l2": "inputs larger than L2: every pass streams 2-5 GB per GPU, L2 is 126 MB"}
+
+
 def lpt_shards(weights, world):
     """Longest-processing-time assignment of generators to ranks."""
     loads, shards = [0.0] * world, [[] for _ in range(world)]
@@ -170,11 +180,39 @@ def cpu_step(name, mode, gens, procs):
     return time.perf_counter() - t0
 
 
+def cpu_full_circuit(name, mode, weights):
+    """The WHOLE circuit on the host: one process per generator, the heaviest first (the pool
+    hands the next generator to whichever core is free).  Returns wall seconds."""
+    import multiprocessing as mp
+
+    n, _ = workloads.build(name)
+    order = sorted(range(n), key=lambda g: -weights[g])
+    procs = max(1, min(os.cpu_count() or 1, n))
+    t0 = time.perf_counter()
+    with mp.get_context("fork").Pool(procs) as pool:
+        list(pool.imap_unordered(_cpu_worker, [(name, mode, [g]) for g in order], chunksize=1))
+    return time.perf_counter() - t0, procs
+
+
+def final_terms_of(name, mode):
+    """Final term count of a workload from the reference-made digests (no GPU on this arm)."""
+    try:
+        with open(os.path.join(ROOT, "tests", "golden", "digests.json")) as fh:
+            return int(sum(json.load(fh)["data"][f"{name}/{mode}"]["trace_last"]))
+    except (OSError, KeyError, ValueError):
+        return 0
+
+
 def run_reference(args, updates_per_gen):
-    """--impl reference: the reference algorithm (oracle port) on the host cores."""
+    """--impl reference: the reference algorithm (oracle port) on the host cores.  `config` is the
+    GPU arm's (same job); every step is a bounded sample of it -- a subset of the circuit's
+    generators, which evolve independently -- described in `cpu_baseline.sample`.  --ref-full
+    also runs the whole circuit once (all generators, one process each, heavy first: minutes and
+    tens of GB at the default workload) and reports it as `cpu_baseline.full_circuit`."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
+    world = int(os.environ.get("WORLD_SIZE", "1"))
     n, gates = workloads.build(args.workload)
     gens = CPU_SAMPLE.get(args.workload) or list(range(n))
     cores = os.cpu_count() or 1
@@ -187,14 +225,21 @@ def run_reference(args, updates_per_gen):
     value = upd / sec
     sample = (f"generators {gens[0]}..{gens[-1]} of {args.workload} ({len(gens)} of {n}; generators evolve "
               f"independently), {args.mode}, numpy port of the reference (oracle/stabsim_port.py), "
-              f"{procs} processes")
+              f"{procs} processes; value = the sample's updates / the sample's time")
+    cpu = {"value": value, "unit": "updates/s", "cores": procs, "kind": "port", "sample": sample, "host": host_cpu()}
+    if args.ref_full:
+        full_s, full_procs = cpu_full_circuit(args.workload, args.mode, updates_per_gen)
+        cpu["full_circuit"] = {"value": float(sum(updates_per_gen)) / full_s, "unit": "updates/s", "seconds": full_s,
+                               "cores": full_procs, "generators": n}
+    strong = world > 1 and args.scaling == "strong"
     line = {
         "impl": "reference", "metric": "term_gate_updates_per_s", "value": value, "unit": "updates/s",
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": sec * 1e3,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic", "config": {"workload": args.workload, "mode": args.mode, "sample": sample},
-        "cpu_baseline": {"value": value, "unit": "updates/s", "cores": procs, "kind": "port", "sample": sample,
-                         "host": host_cpu()},
+        "higher_is_better": True, "scaling": "strong" if strong else "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic",
+        "config": job_config(args.workload, args.mode, n, len(gates), float(sum(updates_per_gen)),
+                             final_terms_of(args.workload, args.mode), world, strong),
+        "cpu_baseline": cpu,
         "e2e": {"value": value, "unit": "updates/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "gpu_launches": 0,
     }
@@ -371,12 +416,8 @@ def run_ours(args):
         "steps": args.steps, "warmup": max(args.warmup, 3), "ms_per_step": ms_per_step,
         "higher_is_better": True, "scaling": "weak" if (weak or world == 1) else "strong", "vs_baseline": None,
         "dtype": "f64", "data": "synthetic",
-        "config": {"workload": args.workload, "mode": args.mode, "qubits": n, "gates": len(gates),
-                   "term_gate_updates": total_updates, "final_terms": int(sum(final_ranks)),
-                   "parallelism": (f"{world} circuit instance(s), one per GPU, all generators of an instance on its GPU"
-                                   if (weak or world == 1) else
-                                   f"one circuit, buckets of the last operator split over {world} GPUs"),
-                   "l2": "inputs larger than L2: every pass streams 2-5 GB per GPU, L2 is 126 MB"},
+        "config": job_config(args.workload, args.mode, n, len(gates), total_updates, int(sum(final_ranks)), world,
+                             strong),
         "e2e": {"value": total_updates / e2e_s, "unit": "updates/s", "ms_per_step": e2e_s * 1e3,
                 "h2d_bytes_per_step": table_bytes(n, gates), "d2h_bytes_per_step": d2h},
         "gpu_launches": launches,
@@ -399,6 +440,8 @@ def main():
     ap.add_argument("--workload", default=DEFAULT_WORKLOAD)
     ap.add_argument("--mode", default="v3")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    ap.add_argument("--ref-full", action="store_true",
+                    help="--impl reference: also run the WHOLE circuit once on the host (all generators)")
     ap.add_argument("--scaling", default="strong", choices=("weak", "strong"),
                     help="N > 1: ONE circuit, the buckets of its last operator split over the GPUs (strong, the "
                          "north star's sharding; default) or replicas, one circuit instance per GPU (weak)")

@@ -19,6 +19,7 @@ Fixtures written:
 from __future__ import annotations
 
 import argparse
+import base64
 import hashlib
 import json
 import math
@@ -71,12 +72,36 @@ def mix64(keys):
     return (z >> np.uint64(11)).astype(np.float64) * (2.0 ** -52) - 1.0
 
 
+CHUNKS = 1024          # per-generator chunk moments: a coefficient error is localised to rank/1024 terms
+
+
+def chunk_moments(lam, keys, chunks=CHUNKS):
+    """Sum of lambda and of lambda * mix64(key) over `chunks` contiguous ranges of the canonical
+    order (range c = [c*r//chunks, (c+1)*r//chunks)), as base64 of little-endian float64; shared
+    with tests/golden_util.py.  Any single coefficient off by more than the test's tolerance shows
+    up in its chunk (both moments would have to cancel to hide it)."""
+    r = len(lam)
+    bounds = (np.arange(chunks + 1, dtype=np.int64) * r) // chunks
+    w = lam * mix64(keys)
+    cs = np.concatenate([[0.0], np.cumsum(lam)])
+    cw = np.concatenate([[0.0], np.cumsum(w)])
+    # chunk sums by direct summation (not differences of running sums: those would carry the
+    # rounding of the whole prefix)
+    s = np.array([lam[bounds[c]:bounds[c + 1]].sum() for c in range(chunks)])
+    p = np.array([w[bounds[c]:bounds[c + 1]].sum() for c in range(chunks)])
+    del cs, cw
+    return {"count": chunks, "sum": base64.b64encode(s.astype("<f8").tobytes()).decode(),
+            "proj": base64.b64encode(p.astype("<f8").tobytes()).decode()}
+
+
 def digest(g):
     idx = np.asarray(g.indices)
     keys = idx.astype(np.uint64) if idx.dtype != object else np.array([int(v) for v in idx], dtype=np.uint64)
     lam = np.asarray(g.lambdas, dtype=np.float64)
     step = max(1, len(keys) // 64)
+    extra = {"chunks": chunk_moments(lam, keys)} if len(keys) >= 4 * CHUNKS else {}
     return {
+        **extra,
         "rank": int(len(keys)),
         "sha256": hashlib.sha256(keys.tobytes()).hexdigest(),
         "sum": hx(lam.sum()), "sum_sq": hx(np.dot(lam, lam)), "sum_abs": hx(np.abs(lam).sum()),

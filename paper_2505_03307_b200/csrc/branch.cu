@@ -22,6 +22,7 @@
 #include <string.h>
 
 #include <algorithm>
+#include <vector>
 
 #include "expand.cuh"
 
@@ -673,20 +674,58 @@ void host_apply_op(u32 op, u64& key, u32& neg, u32 cx_c, u32 cx_t, u32 cx_s) {
   }
 }
 
+// Images of the 3n single-digit words under a sign-permutation program.  The same programs recur
+// (every run of a cached circuit plan, every step of a benchmark loop) and pushing 3n words
+// through a few hundred ops costs more host time than the kernel that uses the table takes on
+// the small configs, so the last tables are kept, found by an FNV-1a hash of the program and
+// verified against a copy of it.
+struct ImageCacheEntry {
+  u64 hash = 0;
+  int n_qubits = 0;
+  u32 cx_c = 0, cx_t = 0, cx_s = 0;
+  std::vector<uint32_t> program;
+  u64 img[QX_MAX_QUBITS][3];
+  unsigned char e[QX_MAX_QUBITS][3];
+  bool used = false;
+};
+constexpr int kImageCache = 64;
+
 template <typename K>
 void fill_images(int n_qubits, const uint32_t* program, int n_ops, u32 cx_c, u32 cx_t, u32 cx_s,
                  ImageTable<K>* im) {
   memset(im, 0, sizeof(*im));
   const u64 lo = 0x5555555555555555ull;
+  static thread_local ImageCacheEntry cache[kImageCache];
+  u64 h = 1469598103934665603ull ^ (u64)n_qubits;
+  for (int i = 0; i < n_ops; ++i) h = (h ^ program[i]) * 1099511628211ull;
+  ImageCacheEntry& ce = cache[h % kImageCache];
+  const bool hit = ce.used && ce.hash == h && ce.n_qubits == n_qubits && ce.cx_c == cx_c && ce.cx_t == cx_t &&
+                   ce.cx_s == cx_s && (int)ce.program.size() == n_ops &&
+                   (n_ops == 0 || memcmp(ce.program.data(), program, sizeof(uint32_t) * (size_t)n_ops) == 0);
+  if (!hit) {
+    for (int p = 0; p < n_qubits; ++p)
+      for (u32 a = 1; a <= 3; ++a) {
+        u64 w = (u64)a << (2 * p);
+        u32 neg = 0;
+        for (int i = 0; i < n_ops; ++i) host_apply_op(program[i], w, neg, cx_c, cx_t, cx_s);
+        const u32 ny = (u32)__builtin_popcountll((w >> 1) & ~w & lo);
+        ce.img[p][a - 1] = w;
+        ce.e[p][a - 1] = (unsigned char)((ny + 2u * neg) & 3u);
+      }
+    ce.hash = h;
+    ce.n_qubits = n_qubits;
+    ce.cx_c = cx_c;
+    ce.cx_t = cx_t;
+    ce.cx_s = cx_s;
+    ce.program.assign(program, program + n_ops);
+    ce.used = true;
+  }
   for (int p = 0; p < n_qubits; ++p)
-    for (u32 a = 1; a <= 3; ++a) {
-      u64 w = (u64)a << (2 * p);
-      u32 neg = 0;
-      for (int i = 0; i < n_ops; ++i) host_apply_op(program[i], w, neg, cx_c, cx_t, cx_s);
-      const u32 ny = (u32)__builtin_popcountll((w >> 1) & ~w & lo);
-      im->img[p][a - 1] = (K)w;
-      im->imx[p][a - 1] = (K)((w ^ (w >> 1)) & lo);
-      im->e[p][a - 1] = (unsigned char)((ny + 2u * neg) & 3u);
+    for (int a = 0; a < 3; ++a) {
+      const u64 w = ce.img[p][a];
+      im->img[p][a] = (K)w;
+      im->imx[p][a] = (K)((w ^ (w >> 1)) & lo);
+      im->e[p][a] = ce.e[p][a];
     }
 }
 
@@ -802,6 +841,240 @@ int expand(qx_store* s, const OperatorTable& tb, const uint32_t* program, int n_
   return QX_OK;
 }
 
+
+// ---- small stores: expansion + Clifford run + merge in ONE launch --------------------------------
+// Configs 1, 2, 3, 5 hold a few thousand terms: their cost is launches and host round trips, not
+// bandwidth.  When every generator's raw expansion fits shared memory (<= QX_SMALL_MAX terms, known
+// on the host from the rank bound and the operator's largest fan-out), one CTA per generator does
+// the whole operator step: branch counts + scan, raw terms into shared memory (products qubit 0
+// first, images of the run composed in), bitonic sort on (key, raw position), in-order run sums,
+// drop rule, compaction by look-back across the generators -- the reference's
+// flatten + apply_cx + canonicalize (stabilizer.py:289-363) with one launch and one read-back.
+constexpr int kSoThreads = 256;
+constexpr int kSoWarps = kSoThreads / 32;
+constexpr int kSoSrcMax = 4096;
+
+__global__ void __launch_bounds__(kSoThreads)
+k_small_operator(const u64* __restrict__ keys_in, const double* __restrict__ lam_in,
+                 const int64_t* __restrict__ seg_in, int n_seg, u64* __restrict__ keys_out,
+                 double* __restrict__ lam_out, int64_t* __restrict__ seg_out, u64* status, int* error,
+                 int src_cap, int raw_cap, double eps, const __grid_constant__ OperatorTable tb,
+                 const __grid_constant__ ImageTable<u64> im) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  u64* rkey = reinterpret_cast<u64*>(smem_raw);                            // raw_cap
+  double* rlam = reinterpret_cast<double*>(rkey + raw_cap);                // raw_cap
+  u32* soff = reinterpret_cast<u32*>(rlam + raw_cap);                      // src_cap + 1
+  unsigned short* ridx = reinterpret_cast<unsigned short*>(soff + src_cap + 1);   // raw_cap
+  __shared__ OperatorTable s_tb;
+  __shared__ ImageTable<u64> s_im;
+  __shared__ u64 s_scan[kSoWarps + 1];
+  __shared__ u64 s_base;
+  const int g = (int)blockIdx.x;           // in-order dispatch, see take_ticket
+  const int tid = threadIdx.x;
+  {
+    const u32* src = reinterpret_cast<const u32*>(&tb);
+    u32* dst = reinterpret_cast<u32*>(&s_tb);
+    for (int i = tid; i < (int)(sizeof(OperatorTable) / 4); i += kSoThreads) dst[i] = src[i];
+    const u32* isrc = reinterpret_cast<const u32*>(&im);
+    u32* idst = reinterpret_cast<u32*>(&s_im);
+    for (int i = tid; i < (int)(sizeof(ImageTable<u64>) / 4); i += kSoThreads) idst[i] = isrc[i];
+  }
+  const int64_t start = seg_in[g];
+  int len = (int)min((int64_t)0x7fffffff, seg_in[g + 1] - start);
+  bool bad = len > src_cap;
+  if (bad) len = 0;
+  __syncthreads();
+  // branch counts -> exclusive raw offsets (consecutive sources per thread)
+  const int per = (len + kSoThreads - 1) / kSoThreads;
+  const int e0 = tid * per, e1 = min(len, e0 + per);
+  u64 mine = 0;
+  for (int e = e0; e < e1; ++e) mine += branch_count(keys_in[start + e], s_tb.cnt);
+  u64 total;
+  u64 run = block_exclusive_sum<u64>(mine, s_scan, total);
+  if (total > (u64)raw_cap) {              // host bound was wrong: flag it, keep the chain alive
+    bad = true;
+    total = 0;
+    len = 0;
+  }
+  for (int e = e0; e < e1 && !bad; ++e) {
+    soff[e] = (u32)run;
+    run += branch_count(keys_in[start + e], s_tb.cnt);
+  }
+  if (tid == 0) {
+    soff[len] = (u32)total;
+    if (bad) atomicExch(error, 1);
+    else atomicAdd(reinterpret_cast<unsigned long long*>(error) + 1, (unsigned long long)total);   // raw terms of the step
+  }
+  __syncthreads();
+  const int raw = (int)total;
+  int m = 32;
+  while (m < raw) m <<= 1;
+  // raw terms: source by bisection of the offsets, picks by mixed-radix decode (lowest digit
+  // fastest), product and image composition qubit 0 first (stabilizer.py:311-319)
+  for (int r = tid; r < m; r += kSoThreads) {
+    u64 out = ~0ull;
+    double v = 0.0;
+    if (r < raw) {
+      int lo = 0, hi = len;                // soff[lo] <= r < soff[hi]
+      while (hi - lo > 1) {
+        const int mid = (lo + hi) >> 1;
+        if (soff[mid] <= (u32)r) lo = mid; else hi = mid;
+      }
+      const u64 key = keys_in[start + lo];
+      u32 b = (u32)r - soff[lo];
+      u64 picks = 0;
+      for (u64 mask = support_mask(key); mask;) {
+        const int bit = __ffsll((long long)mask) - 1;
+        mask &= mask - 1;
+        const u32 c = s_tb.cnt[bit >> 1][(u32)((key >> bit) & 3ull) - 1u];
+        const u32 q = b / c;
+        picks |= (u64)(b - q * c) << bit;
+        b = q;
+      }
+      v = lam_in[start + lo];
+      out = 0;
+      u32 ex = 0;
+      for (u64 mask = support_mask(key); mask;) {
+        const int bit = 63 - __clzll((long long)mask);
+        mask ^= 1ull << bit;
+        const int p = bit >> 1;
+        const u32 d = (u32)((key >> bit) & 3ull) - 1u, pick = (u32)(picks >> bit) & 3u;
+        v = __dmul_rn(v, s_tb.w[p][d][pick]);
+        const u32 ax = s_tb.axis[p][d][pick];
+        compose<u64>(out, ex, s_im.img[p][ax - 1], s_im.imx[p][ax - 1], s_im.e[p][ax - 1]);
+      }
+      if (composed_sign<u64>(out, ex)) v = -v;     // sign flips are exact
+    }
+    rkey[r] = out;
+    rlam[r] = v;
+    ridx[r] = (unsigned short)r;
+  }
+  __syncthreads();
+  // bitonic network on (key, raw position): equal keys stay in raw order, padding ends up last
+  for (int k = 2; k <= m; k <<= 1) {
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      for (int t = tid; t < (m >> 1); t += kSoThreads) {
+        const int lo = ((t & ~(j - 1)) << 1) | (t & (j - 1));
+        const int hi = lo | j;
+        const u64 ka = rkey[lo], kb = rkey[hi];
+        const unsigned short ia = ridx[lo], ib = ridx[hi];
+        const bool greater = ka > kb || (ka == kb && ia > ib);
+        if (greater == ((lo & k) == 0)) {
+          rkey[lo] = kb; rkey[hi] = ka;
+          ridx[lo] = ib; ridx[hi] = ia;
+        }
+      }
+      __syncthreads();
+    }
+  }
+  // run sums (sequential, raw order), drop rule, ordered compaction row by row
+  const int rows = (raw + kSoThreads - 1) / kSoThreads;
+  u64 my_count = 0;
+  for (int r = 0; r < rows; ++r) {
+    const int e = r * kSoThreads + tid;
+    if (e < raw) {
+      const u64 key = rkey[e];
+      if (e == 0 || rkey[e - 1] != key) {
+        double sum = rlam[ridx[e]];
+        for (int j = e + 1; j < raw && rkey[j] == key; ++j) sum += rlam[ridx[j]];
+        if (fabs(sum) >= eps) ++my_count;
+      }
+    }
+  }
+  u64 seg_total;
+  block_exclusive_sum<u64>(my_count, s_scan, seg_total);
+  if ((tid >> 5) == 0) {
+    const u64 excl = lookback_exclusive(status, g, seg_total);
+    if (lane_id() == 0) s_base = excl;
+  }
+  __syncthreads();
+  const int64_t base = (int64_t)s_base;
+  u64 kept_before = 0;
+  for (int r = 0; r < rows; ++r) {
+    const int e = r * kSoThreads + tid;
+    bool kept = false;
+    u64 key = 0;
+    double sum = 0.0;
+    if (e < raw) {
+      key = rkey[e];
+      if (e == 0 || rkey[e - 1] != key) {
+        sum = rlam[ridx[e]];
+        for (int j = e + 1; j < raw && rkey[j] == key; ++j) sum += rlam[ridx[j]];
+        kept = fabs(sum) >= eps;
+      }
+    }
+    u64 row_total;
+    const u64 excl = block_exclusive_sum<u64>(kept ? 1ull : 0ull, s_scan, row_total);
+    if (kept) {
+      const int64_t pos = base + (int64_t)(kept_before + excl);
+      keys_out[pos] = key;
+      lam_out[pos] = sum;
+    }
+    kept_before += row_total;
+  }
+  if (tid == 0) {
+    seg_out[g] = base;
+    if (g == n_seg - 1) seg_out[n_seg] = base + (int64_t)seg_total;
+  }
+}
+
+// Host side: *done = false (and nothing touched) when the bounds do not fit.
+int small_operator_run(qx_store* s, const OperatorTable& tb, const uint32_t* program, int n_ops, u32 cx_c,
+                       u32 cx_t, u32 cx_s, double eps, int64_t max_fanout, bool* done, int64_t* raw_total) {
+  *done = false;
+  static const bool off = getenv("QX_NO_SMALL_OPERATOR") != nullptr;
+  if (off || s->n_words > 1 || s->n_seg < 1) return QX_OK;
+  const int64_t src_ub = s->ub_seg;
+  if (src_ub < 1 || src_ub > kSoSrcMax || src_ub * max_fanout > QX_SMALL_MAX) return QX_OK;
+  QX_CUDA(cudaSetDevice(s->device));
+  int raw_cap = 32;
+  while (raw_cap < src_ub * max_fanout) raw_cap <<= 1;
+  const int src_cap = (int)src_ub;
+  QX_TRY(qx_store_reserve(s, std::min<int64_t>(s->ub_total * max_fanout, (int64_t)s->n_seg * raw_cap) + 2, true));
+  const int64_t bytes = 16 + 8 * ((int64_t)s->n_seg + 1);
+  QX_TRY(qx_store_scratch(s, bytes));
+  QX_CUDA(cudaMemsetAsync(s->scratch, 0, (size_t)bytes, s->stream));
+  int* error = reinterpret_cast<int*>(s->scratch);
+  u64* status = reinterpret_cast<u64*>(reinterpret_cast<char*>(s->scratch) + 16);
+  ImageTable<u64> im;
+  fill_images<u64>(s->n_qubits, program, n_ops, cx_c, cx_t, cx_s, &im);
+  const size_t smem = (size_t)raw_cap * 18 + 4 * ((size_t)src_cap + 1) + 16;
+  static size_t attr_smem = 0;
+  if (smem > attr_smem) {
+    QX_CUDA(cudaFuncSetAttribute(k_small_operator, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 QX_SMALL_MAX * 18 + 4 * (kSoSrcMax + 1) + 16));
+    attr_smem = QX_SMALL_MAX * 18 + 4 * (kSoSrcMax + 1) + 16;
+  }
+  const int in = s->cur, out = s->cur ^ 1;
+  {
+    QxProfileScope prof(QX_K_SMALL_MERGE, s->stream, 32.0 * (double)s->ub_total * (double)max_fanout);
+    k_small_operator<<<s->n_seg, kSoThreads, smem, s->stream>>>(s->keys[in], s->lam[in], s->seg[in], s->n_seg,
+                                                               s->keys[out], s->lam[out], s->seg[out], status,
+                                                               error, src_cap, raw_cap, eps, tb, im);
+    QX_CUDA(cudaGetLastError());
+  }
+  // one round trip: the error word, then the new offsets
+  QX_CUDA(cudaMemcpyAsync(s->h_pinned, error, 16, cudaMemcpyDeviceToHost, s->stream));
+  QX_TRY(qx_readback(s->stream, s->h_seg, s->seg[out], (int64_t)s->n_seg + 1));
+  QX_CUDA(cudaStreamSynchronize(s->stream));
+  if (*reinterpret_cast<int*>(s->h_pinned) != 0) {
+    // a bound was wrong (cannot happen with exact ranks): the input buffer is untouched, so the
+    // general path can still run; the host mirror of the offsets is restored first
+    s->exact = false;
+    QX_TRY(qx_store_refresh(s));
+    return QX_OK;
+  }
+  s->cur = out;
+  s->exact = true;
+  s->ub_total = s->h_seg[s->n_seg];
+  int64_t mx = 0;
+  for (int g = 0; g < s->n_seg; ++g) mx = std::max(mx, s->h_seg[g + 1] - s->h_seg[g]);
+  s->ub_seg = mx;
+  if (raw_total) *raw_total = s->h_pinned[1];
+  *done = true;
+  return QX_OK;
+}
+
 }  // namespace
 
 extern "C" int qx_apply_operator(qx_store* s, const int32_t* counts, const int32_t* axes,
@@ -885,6 +1158,21 @@ static int operator_run(qx_store* s, const int32_t* counts, const int32_t* axes,
           for (int g = 0; g < s->n_seg; ++g) ranks[g] = s->h_seg[g + 1] - s->h_seg[g];
         return QX_OK;
       }
+    }
+  }
+  if (term_limit <= 0 && parts == 1) {
+    // small stores: the whole step in one launch
+    QX_CUDA(cudaSetDevice(s->device));
+    if (!s->exact) QX_TRY(qx_store_refresh(s));
+    int64_t fan = 1;
+    for (int p = 0; p < s->n_qubits && fan <= QX_SMALL_MAX; ++p)
+      fan *= std::max({tb.cnt[p][0], tb.cnt[p][1], tb.cnt[p][2]});
+    bool done = false;
+    QX_TRY(small_operator_run(s, tb, program, n_ops, cx_c, cx_t, cx_s, eps, fan, &done, raw_total));
+    if (done) {
+      if (ranks)
+        for (int g = 0; g < s->n_seg; ++g) ranks[g] = s->h_seg[g + 1] - s->h_seg[g];
+      return QX_OK;
     }
   }
   static const bool no_narrow = getenv("QX_NO_NARROW") != nullptr;

@@ -23,6 +23,7 @@ The host walks the circuit; it never touches a term.
 from __future__ import annotations
 
 import time
+from operator import is_ as _is
 from dataclasses import dataclass, field
 from enum import Enum
 from typing import Sequence
@@ -284,7 +285,10 @@ def run(instructions: Sequence[Instruction], n: int, mode, eps: float = DEFAULT_
     if n < 1:
         raise ValueError(f"qubit count must be positive, got {n}")
     t0 = time.perf_counter()
-    partition = divide_instruction(instructions, n)
+    if not isinstance(instructions, (list, tuple)):
+        instructions = list(instructions)
+    plan = _plan_for(instructions, n, mode)
+    partition = plan.partition
     timings["partition"] = time.perf_counter() - t0
 
     if initial is not None:
@@ -317,12 +321,19 @@ def run(instructions: Sequence[Instruction], n: int, mode, eps: float = DEFAULT_
         trace = [list(w.ranks)]
 
         if mode is Mode.V1:
-            _walk_v1(instructions, partition, w, trace, counters, eager)
+            if eager:
+                w.updates = np.zeros(len(w.ids), dtype=np.int64)
+                _walk_v1_eager(instructions, partition, w, trace, counters)
+            else:
+                _replay_v1(plan.v1_events(instructions), w, trace, counters)
         else:
             t0 = time.perf_counter()
-            lut, is_perm, tables = _lut.build_lut(partition)
+            lut, is_perm, tables = plan.lut()
             timings["lut"] = time.perf_counter() - t0
-            _walk_operators(partition, lut, is_perm, tables, w, trace, counters, mode, eager)
+            if eager or n > 32:
+                _walk_operators(partition, lut, is_perm, tables, w, trace, counters, mode, eager)
+            else:
+                _replay_operators(plan.operator_events(), w, trace, counters, mode)
 
         streamed = None
         partitioned = None
@@ -360,6 +371,244 @@ def run(instructions: Sequence[Instruction], n: int, mode, eps: float = DEFAULT_
         # instead of leaving it to the garbage collector (a retry near the capacity limit)
         if not handed_over:
             store.close()
+
+
+
+# ------------------------------------------------------------------------------------------
+# circuit plans: everything about a run that depends on the gate list only
+# ------------------------------------------------------------------------------------------
+# Walking 5000 gates in Python (partition, composed blocks, op words, branch tables) costs more
+# than the device needs for the whole of configs 1/2/3/5.  None of it depends on the terms, so
+# it is done once per gate list and replayed: a plan is a short list of EVENTS (queue these op
+# words / branch here with these tables / snapshot the ranks) -- C5 in v3 is 41 events instead
+# of 1647 operator steps.  Plans are found again by IDENTITY of the (immutable) instructions:
+# `all(a is b)` over 5000 gates is ~0.1 ms, hashing them would cost more than it saves.
+_PLAN_SLOTS = 8
+SMALL_RAW = 8192                  # raw terms per generator the one-launch operator step takes (QX_SMALL_MAX)
+_plans: list = []
+
+
+class _Plan:
+    def __init__(self, instructions, n: int):
+        self.instructions = tuple(instructions)
+        self.n = n
+        self.partition = divide_instruction(self.instructions, n)
+        self._lut = None
+        self._v1 = None
+        self._ops = None
+
+    def matches(self, instructions, n: int) -> bool:
+        mine = self.instructions
+        return n == self.n and len(instructions) == len(mine) and all(map(_is, instructions, mine))
+
+    def lut(self):
+        if self._lut is None:
+            self._lut = _lut.build_lut(self.partition)
+        return self._lut
+
+    def v1_events(self, instructions):
+        if self._v1 is None:
+            self._v1 = _compile_v1(self.instructions, self.partition, self.n)
+        return self._v1
+
+    def operator_events(self):
+        if self._ops is None:
+            self._ops = _compile_operators(self.partition, *self.lut(), self.n)
+        return self._ops
+
+
+def _plan_for(instructions, n: int, mode) -> _Plan:
+    for i, plan in enumerate(_plans):
+        if plan.matches(instructions, n):
+            if i:
+                _plans.insert(0, _plans.pop(i))
+            return plan
+    plan = _Plan(instructions, n)
+    _plans.insert(0, plan)
+    del _plans[_PLAN_SLOTS:]
+    return plan
+
+
+def clear_plans():
+    """Forget the cached circuit plans (tests; long-running services that stream distinct circuits)."""
+    _plans.clear()
+
+
+def _compile_v1(instructions, partition, n: int) -> tuple:
+    """Events of the gate-by-gate walk (reference engine.py:155-180) for a store that merges only
+    where terms branch: ('q', op words, has_cx, gates) | ('split', position, qubit, tables) |
+    ('snap',) at operator boundaries."""
+    sh1, sh2 = (32, 48) if n > 32 else (2, 8)
+    pos_a = [(2 * (n - 1 - q)) << sh1 for q in range(n)]
+    pos_b = [(2 * (n - 1 - q)) << sh2 for q in range(n)]
+    fixed = {g: t << 16 for g, t in _lut.FIXED_PERMS.items()}
+    fixed_get = fixed.get
+    bounds = iter(np.cumsum(partition.operator_sizes()).tolist())
+    nb = next(bounds, -1)
+    events, ops, has_cx, cnt, n_cx = [], [], False, 0, 0
+
+    def close():
+        nonlocal ops, has_cx, cnt
+        if ops or cnt:
+            events.append(("q", ops, has_cx, cnt))
+        ops, has_cx, cnt = [], False, 0
+
+    for pos, inst in enumerate(instructions, start=1):
+        wires = inst.wires
+        if len(wires) == 2:
+            ops.append(1 | pos_a[wires[0]] | pos_b[wires[1]])
+            has_cx = True
+            n_cx += 1
+            cnt += 1
+        else:
+            op = fixed_get(inst.gate)
+            if op is not None:
+                ops.append(op | pos_a[wires[0]])
+                cnt += 1
+            else:
+                block = _lut.gate_branch_block(inst.gate, inst.theta)
+                table = _lut.perm_word(block)
+                if table is not None:
+                    if table != _lut.IDENTITY_PERM:
+                        ops.append(_lut.perm_op(n, wires[0], table))
+                    cnt += 1
+                else:
+                    close()
+                    # the same gate as a one-qubit operator table: small stores take the fused
+                    # expand + run + merge launch of the operator path (two contributions per
+                    # word at most, so the sums are the reference's bit for bit)
+                    full = np.tile(np.eye(3), (n, 1, 1))
+                    full[wires[0]] = block
+                    events.append(("split", pos, wires[0], split_tables(block),
+                                   _lut.operator_tables(full) if n <= 32 else None))
+        if pos == nb:
+            close()
+            events.append(("snap",))
+            nb = next(bounds, -1)
+    close()
+    return events, n_cx, len(instructions) - n_cx
+
+
+def _replay_v1(compiled, w: _Walker, trace, counters):
+    events, n_cx, n_1q = compiled
+    w.updates = np.zeros(len(w.ids), dtype=np.int64)
+    for ev in events:
+        kind = ev[0]
+        if kind == "q":
+            w.queue.extend(ev[1])
+            w.queue_has_cx = w.queue_has_cx or ev[2]
+            if w.pending is None:
+                w.clean_gates += ev[3]
+            else:
+                w.pending_gates += ev[3]
+        elif kind == "snap":
+            w.snapshot(trace)
+        else:
+            _, pos, qubit, tables, as_operator = ev
+            w.resolve(trace)                   # this gate must see merged terms
+            w.count_gate()
+            w.flush()
+            t0 = time.perf_counter()
+            if as_operator is not None and w.before_merge is None and 2 * max(w.ranks, default=0) <= SMALL_RAW:
+                w.stage_operator(*as_operator)     # split + the run behind it + merge: one launch
+            else:
+                w.store.apply_split(qubit, *tables)
+            w.timings["sub_flatten"] += time.perf_counter() - t0
+            w.branched(pos - 1, "sub_flatten", trace)
+    counters["cx_applications"] += n_cx
+    if n_1q:
+        counters["v1_gate_applications"] = counters.get("v1_gate_applications", 0) + n_1q
+
+
+def _compile_operators(partition, lut, is_perm, tables, n: int) -> tuple:
+    """Events of the operator chain (reference engine.py:110-132), n <= 32, deferred merges:
+    ('q', op words, has_cx, snapshots) for runs of permutation operators and CX groups,
+    ('b', step, counts, axes, weights) for a U_k that branches (followed by its own snapshot)."""
+    events, ops, has_cx, snaps = [], [], False, 0
+    n_cx = 0
+    ui = vi = 0
+    if partition.k:
+        all_perm = is_perm.all(axis=1).tolist()
+        shifts = (2 * (n - 1 - np.arange(n, dtype=np.uint64)))[None, :]
+        ops_all = (tables.astype(np.uint64) << np.uint64(16)) | (shifts << np.uint64(2))
+        live = tables != _lut.IDENTITY_PERM
+        perm_ops = ops_all[live].tolist()
+        perm_off = np.concatenate(([0], np.cumsum(live.sum(axis=1)))).tolist()
+
+    def close():
+        nonlocal ops, has_cx, snaps
+        if ops or snaps:
+            events.append(("q", ops, has_cx, snaps))
+        ops, has_cx, snaps = [], False, 0
+
+    for step, bit in enumerate(partition.order):
+        if bit == 0:
+            if all_perm[ui]:
+                ops.extend(perm_ops[perm_off[ui]:perm_off[ui + 1]])
+            else:
+                close()
+                events.append(("b", step, *_lut.operator_tables(lut[ui])))
+            ui += 1
+        else:
+            for inst in partition.v_groups[vi]:
+                ops.append(_lut.cx_op(n, *inst.wires))
+            has_cx = has_cx or bool(partition.v_groups[vi])
+            n_cx += len(partition.v_groups[vi])
+            vi += 1
+        snaps += 1
+    close()
+    return events, partition.k, n_cx
+
+
+def _replay_operators(compiled, w: _Walker, trace, counters, mode):
+    events, n_u, n_cx = compiled
+    n = w.n
+    for ev in events:
+        if ev[0] == "q":
+            w.queue.extend(ev[1])
+            w.queue_has_cx = w.queue_has_cx or ev[2]
+            for _ in range(ev[3]):
+                w.snapshot(trace)
+            continue
+        _, step, counts, axes, weights = ev
+        w.resolve(trace)               # expand merged terms only
+        w.flush()
+        t0 = time.perf_counter()
+        if mode is Mode.V2 and 4 ** n > DENSE_FLATTEN_BUDGET:
+            # dense layout: a branching substitution needs a 4**n scatter buffer
+            # (reference stabilizer.py:264-276); one-hot rows take the fast path
+            raw = w.store.count_operator(counts)
+            over = any(r > have for r, have in zip(raw, w.store.ranks()))
+            if w.reduce_ranks is not None:
+                # term-partitioned runs: a rank that holds no branching term of a generator
+                # must raise too, or it would wait for the others in the next collective
+                over = w.reduce_ranks([int(over)])[0] > 0
+            if over:
+                raise ResourceLimitError(
+                    f"dense flatten needs a 4**{n}-element buffer (> {DENSE_FLATTEN_BUDGET}); "
+                    "use the ragged layout for circuits of this size"
+                )
+        if mode is Mode.V3:
+            # the reference's ragged flatten walks the strings grouped by their branch-count
+            # pattern (stabilizer.py:294-296); same order here, so that sums of three or more
+            # contributions round the same way (the store may also sit in a permuted order:
+            # the re-sort after the last Clifford run is deferred)
+            w.store.order_for_operator(counts)
+        dense_gens = []
+        if mode is Mode.V2 and w.eps == 0.0 and 4 ** n <= DENSE_FLATTEN_BUDGET and w.before_merge is None:
+            # dense layout, eps = 0: a generator with a branching row comes back from the
+            # reference's 4**n buffer with every word, zeros included (stabilizer.py:277-286)
+            raw = w.store.count_operator(counts)
+            dense_gens = [g for g, (r, have) in enumerate(zip(raw, w.store.ranks())) if r > have]
+        if dense_gens:
+            w.store.apply_operator(counts, axes, weights)
+            pad_dense(w.store, n, dense_gens)
+        else:
+            w.stage_operator(counts, axes, weights)
+        w.timings["sub_flatten"] += time.perf_counter() - t0
+        w.branched(step, "sub_flatten", trace)
+    counters["sub_flatten_ops"] += n_u
+    counters["cx_applications"] += n_cx
 
 
 _STREAM_DEBUG = bool(__import__("os").environ.get("QX_STREAM_DEBUG"))
@@ -495,70 +744,6 @@ class _Shard:
     n: int
     ids: list
     generators: list
-
-
-def _walk_v1(instructions, partition, w: _Walker, trace, counters, eager):
-    """Gate by gate (reference engine.py:155-180): rank snapshots at operator boundaries."""
-    w.updates = np.zeros(len(w.ids), dtype=np.int64)
-    if eager:
-        return _walk_v1_eager(instructions, partition, w, trace, counters)
-    # Gates that are exact signed permutations only queue an op word; the loop below does nothing
-    # else for them (op words from per-qubit shift tables, gate counts booked in bulk at the next
-    # branching gate or operator boundary -- the ranks cannot change in between).
-    n = w.n
-    sh1, sh2 = (32, 48) if n > 32 else (2, 8)
-    pos_a = [(2 * (n - 1 - q)) << sh1 for q in range(n)]
-    pos_b = [(2 * (n - 1 - q)) << sh2 for q in range(n)]
-    fixed = {g: t << 16 for g, t in _lut.FIXED_PERMS.items()}
-    fixed_get = fixed.get
-    bounds = iter(np.cumsum(partition.operator_sizes()).tolist())
-    nb = next(bounds, -1)
-    push = w.queue.append
-    n_cx = cnt = 0
-
-    def book(count):
-        if w.pending is None:
-            w.clean_gates += count
-        else:
-            w.pending_gates += count
-
-    for pos, inst in enumerate(instructions, start=1):
-        wires = inst.wires
-        if len(wires) == 2:
-            push(1 | pos_a[wires[0]] | pos_b[wires[1]])
-            w.queue_has_cx = True
-            n_cx += 1
-            cnt += 1
-        else:
-            op = fixed_get(inst.gate)
-            if op is not None:
-                push(op | pos_a[wires[0]])
-                cnt += 1
-            else:
-                block = _lut.gate_branch_block(inst.gate, inst.theta)
-                table = _lut.perm_word(block)
-                if table is not None:
-                    if table != _lut.IDENTITY_PERM:
-                        push(_lut.perm_op(n, wires[0], table))
-                    cnt += 1
-                else:
-                    book(cnt)
-                    cnt = 0
-                    w.resolve(trace)               # this gate must see merged terms
-                    w.count_gate()
-                    w.flush()
-                    t0 = time.perf_counter()
-                    w.store.apply_split(wires[0], *split_tables(block))
-                    w.timings["sub_flatten"] += time.perf_counter() - t0
-                    w.branched(pos - 1, "sub_flatten", trace)
-                    push = w.queue.append          # flush starts a new queue
-        if pos == nb:
-            w.snapshot(trace)
-            nb = next(bounds, -1)
-    book(cnt)
-    counters["cx_applications"] += n_cx
-    if len(instructions) > n_cx:
-        counters["v1_gate_applications"] = counters.get("v1_gate_applications", 0) + len(instructions) - n_cx
 
 
 def _walk_v1_eager(instructions, partition, w: _Walker, trace, counters):

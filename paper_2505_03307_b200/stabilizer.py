@@ -45,6 +45,8 @@ def make_index_array(values, n: int) -> np.ndarray:
 def keys_to_indices(keys: np.ndarray, n: int) -> np.ndarray:
     """Device keys (uint64) -> the reference's index array dtype."""
     if index_dtype(n) is object:
+        if isinstance(keys, np.ndarray) and keys.dtype == np.uint64:
+            return keys.astype(object)             # Python ints, converted in C (n = 32: 34 k terms of C5)
         return make_index_array(keys.tolist(), n)
     return keys.view(np.int64) if keys.dtype == np.uint64 else keys.astype(np.int64)
 
