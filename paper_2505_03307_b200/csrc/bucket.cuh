@@ -386,6 +386,9 @@ k_bucket_emit(const TileFat<K>* __restrict__ fat, const double* __restrict__ phi
 
   // the previous bucket: first output position, then out (coalesced, final order, store format)
   auto flush_pending = [&]() {
+    // (a look-back by the whole CTA -- 2048 status words per round trip instead of 256 by one warp --
+    // was slower: the status loads of all threads sit in registers next to the held sums, which
+    // spills, and the extra L2 reads cost more than the dependent round trips they save)
     if (warp == 0) {
       const u64 ex = bucket_resolve(status, pend_idx, (u64)pend_kept);
       if (lane == 0) sm.base = ex;
@@ -402,12 +405,13 @@ k_bucket_emit(const TileFat<K>* __restrict__ fat, const double* __restrict__ phi
     pending = false;
   };
 
+  // A bucket id is taken when the previous bucket has been written out, right before the ranks of
+  // the current one are applied: the atomic's round trip hides behind that step.  Not earlier: a
+  // CTA that holds an id while it WAITS for its predecessors (flush_pending) leaves that bucket
+  // uncounted for as long, and the look-back of every bucket behind it stalls on it.
+  if (tid == 0) sm.unit = u_lo + atomicAdd(ticket, 1u);
   for (;;) {
-    __syncthreads();                              // ranks of the previous bucket taken; tables copied
-    // a bucket id is taken right before its sums start: an id taken earlier would stay uncounted
-    // for longer and stall the look-back of every bucket behind it
-    if (tid == 0) sm.unit = u_lo + atomicAdd(ticket, 1u);
-    __syncthreads();
+    __syncthreads();                              // ranks of the previous bucket taken; tables copied; id visible
     const u32 unit = sm.unit;
     if (unit >= u_hi) break;
     const UnitHdr hdr = units[unit];
@@ -738,6 +742,7 @@ k_bucket_emit(const TileFat<K>* __restrict__ fat, const double* __restrict__ phi
     if (!slow) {
       if (pending) flush_pending();               // barriers inside: prefix[] is visible after them
       else __syncthreads();
+      if (tid == 0) sm.unit = u_lo + atomicAdd(ticket, 1u);   // every thread has read this bucket's id long ago
       // kept sums -> rank order in the staging area
 #pragma unroll
       for (int t = 0; t < kTrip; ++t) {
@@ -757,6 +762,7 @@ k_bucket_emit(const TileFat<K>* __restrict__ fat, const double* __restrict__ phi
     } else {
       // parked slots -> rank order, in place through registers
       __syncthreads();
+      if (tid == 0) sm.unit = u_lo + atomicAdd(ticket, 1u);
       unsigned short rk[kPerThread];
       double rl[kPerThread];
 #pragma unroll
@@ -1010,6 +1016,8 @@ int bucket_step(qx_store* s, const OperatorTable& ct, const ImageTable<K>& im, i
     QX_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     QX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, kBThreads, smem));
     per_sm = std::max(per_sm, 1);
+    static const int cap_per_sm = getenv("QX_BUCKET_CTAS") ? atoi(getenv("QX_BUCKET_CTAS")) : 0;   // experiments
+    if (cap_per_sm > 0) per_sm = std::min(per_sm, cap_per_sm);
     const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)u_hi - u_lo, (int64_t)s->sm_count * per_sm));
     kernel<<<grid, kBThreads, smem, s->stream>>>(d_fat, d_phi, d_units, u_lo, u_hi, skey, keys_out, s->lam[out],
                                                   unit_status, ticket, ell, top_bits, cap, eps, ct, im);

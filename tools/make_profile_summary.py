@@ -3,7 +3,7 @@ import collections, csv, io, json, os, subprocess, sys
 
 tag = sys.argv[1]
 src = "gpurun_out"
-out = [f"# {tag}: ncu evidence (tools/ncu_round.sh {tag})\n"]
+out = [f"# {tag}: ncu evidence (tools/r02_evidence.sh {tag} / tools/ncu_round.sh {tag})\n"]
 rows = [r for r in csv.reader(open(f"{src}/{tag}_launches_c4_xyz_16_2.csv")) if len(r) > 5 and r[0].isdigit()]
 agg = collections.OrderedDict()
 for r in rows:
@@ -42,12 +42,16 @@ for name in sorted(os.listdir(src)):
             except ValueError:
                 pass
     out.append("stalls (warps per issue): " + ", ".join(f"{n}={v:.2f}" for v, n in sorted(stalls, reverse=True)[:6]) + "\n")
+    def gb(col):
+        v, u = float(r[hdr.index(col)]), units[hdr.index(col)]
+        return v * {"Gbyte": 1e9, "Mbyte": 1e6, "Kbyte": 1e3, "byte": 1}[u]
     if "k_onesweep" in name and not v1:
-        def gb(col):
-            v, u = float(r[hdr.index(col)]), units[hdr.index(col)]
-            return v * {"Gbyte": 1e9, "Mbyte": 1e6, "Kbyte": 1e3, "byte": 1}[u]
         traffic["sort_pass"] = gb("dram__bytes_read.sum") + gb("dram__bytes_write.sum")
+    if "k_bucket_emit" in name and not v1:
+        traffic["bucket_emit"] = gb("dram__bytes_read.sum") + gb("dram__bytes_write.sum")
 open(f"profiles/{tag}_summary.txt", "w").writelines(out)
 if traffic:
-    json.dump(traffic, open("profiles/traffic.json", "w"))
+    old = json.load(open("profiles/traffic.json")) if os.path.exists("profiles/traffic.json") else {}
+    old.update(traffic)
+    json.dump(old, open("profiles/traffic.json", "w"))
 print("".join(out))
