@@ -233,6 +233,45 @@ int qx_count_operator(qx_store* s, const int32_t* counts, int64_t* raw_per_segme
  * Asynchronous; nothing is read back. */
 int qx_store_order_for_operator(qx_store* s, const int32_t* counts, int32_t by_key);
 
+/* ---- a7 on the device: the reference's sequential chain (engine.py:110-132 for
+ * v2/v3, :155-180 for v1) compiled into a device-resident step list and walked by ONE launch, one
+ * CTA per generator, terms in shared memory from the first step to the last (csrc/program.cuh).
+ * Steps (kinds[i]): 0 = a run of sign-permutation ops (apply_cx / fixed 1q gates,
+ * stabilizer.py:340-363), 1 = a branching operator U_k + the run behind it + the merge (what
+ * qx_apply_operator_run does: stabilizer.py:189-206, 289-337), with order[i] != 0 preceded by the
+ * reference's string order (qx_store_order_for_operator with by_key = 1, stabilizer.py:294-296),
+ * 2 = canonical order (what canonicalize amounts to after permutation steps).  ops[ops_off[i] ..
+ * ops_off[i+1]) are step i's op words (as in qx_apply_clifford; standard CX tables);
+ * counts/axes/weights hold n_steps operator tables of the qx_apply_operator layout back to back
+ * (read for kind 1 only; may be NULL if there is none).  The program owns device memory on
+ * `device` until qx_program_destroy. */
+typedef struct qx_program qx_program;
+int qx_program_create(int device, int32_t n_qubits, int32_t n_steps, const int32_t* kinds,
+                      const int32_t* order, const int32_t* counts, const int32_t* axes,
+                      const double* weights, const uint32_t* ops, const int64_t* ops_off,
+                      qx_program** out);
+int qx_program_destroy(qx_program* p);
+/* Number of kind-1 steps = rows of the ranks table qx_store_run_program fills. */
+int qx_program_rows(const qx_program* p, int32_t* rows);
+/* Run the program on every generator of the store.  *fitted = 1: the store holds the result and
+ * ranks[row * n_segments + g] = terms of generator g after the row-th kind-1 step (0 = all its
+ * terms were dropped there -- the caller raises the reference's NumericalCollapseError,
+ * engine.py:148-152 -- and its later rows stay 0); raw_total (may be NULL) = raw branches of all
+ * kind-1 steps; offsets (may be NULL) = n_segments + 1 offsets of the result.  *fitted = 0: some
+ * generator outgrew shared memory (more than 4096 terms between steps or 8192 raw branches in one
+ * step); the store is exactly as before the call and the caller replays the steps one by one.
+ * init_qubits != NULL (n_segments <= 32): the store's content is ignored and generator g starts as
+ * Z on qubit init_qubits[g] -- what qx_store_init_z would have uploaded (init_z,
+ * stabilizer.py:169-174; if the program then does not fit, the store is left as qx_store_init_z
+ * leaves it).  host_keys / host_lambdas != NULL (PAGE-LOCKED memory from qx_host_alloc, room for
+ * host_cap terms): the kernel also writes the result there, store layout; *host_filled = 1 if all
+ * of it fit.  One launch and one stream synchronize: ranks, offsets and the host copy of the
+ * result are written by the kernel itself into page-locked memory. */
+int qx_store_run_program(qx_store* s, const qx_program* p, const int32_t* init_qubits, double eps,
+                         int64_t* ranks, int64_t* raw_total, int32_t* fitted, int64_t* offsets,
+                         uint64_t* host_keys, double* host_lambdas, int64_t host_cap,
+                         int32_t* host_filled);
+
 /* ---- a6: duplicate-term merge (canonicalize, stabilizer.py:325-337).
  * Per segment: stable sort by key, in-order segmented sum, keep |sum| >= eps,
  * ascending.  ranks (may be NULL) receives the new per-segment counts. */

@@ -1075,7 +1075,190 @@ int small_operator_run(qx_store* s, const OperatorTable& tb, const uint32_t* pro
   return QX_OK;
 }
 
+#include "program.cuh"
+
 }  // namespace
+
+// ---- circuit programs (program.cuh) ----------------------------------------------------------------
+struct qx_program {
+  int device = 0;
+  int n_qubits = 0;
+  int n_steps = 0;
+  int n_rows = 0;             // oprun steps = rows of the ranks table
+  PgStep* d_steps = nullptr;
+};
+
+extern "C" int qx_program_create(int device, int32_t n_qubits, int32_t n_steps, const int32_t* kinds,
+                                 const int32_t* order, const int32_t* counts, const int32_t* axes,
+                                 const double* weights, const uint32_t* ops, const int64_t* ops_off,
+                                 qx_program** out) {
+  QX_REQUIRE(out != nullptr, "out is NULL");
+  *out = nullptr;
+  QX_REQUIRE(n_qubits >= 1 && n_qubits <= QX_MAX_QUBITS, "circuit programs need one-word keys (1 <= n <= %d), got %d",
+             QX_MAX_QUBITS, n_qubits);
+  QX_REQUIRE(n_steps >= 1 && kinds && ops_off, "bad step list");
+  qx_store shape;                        // fill_table / qx_check_program only look at the qubit count
+  shape.n_qubits = n_qubits;
+  u32 cx_c, cx_t, cx_s;
+  qx_standard_cx(&cx_c, &cx_t, &cx_s);
+  std::vector<PgStep> steps((size_t)n_steps);
+  int rows = 0;
+  for (int i = 0; i < n_steps; ++i) {
+    PgStep& st = steps[i];
+    memset(&st, 0, sizeof(st));
+    st.kind = kinds[i];
+    QX_REQUIRE(st.kind == PG_CLIFFORD || st.kind == PG_OPRUN || st.kind == PG_SORT, "step %d: unknown kind %d", i, st.kind);
+    const int64_t o0 = ops_off[i], o1 = ops_off[i + 1];
+    QX_REQUIRE(o0 >= 0 && o1 >= o0 && o1 - o0 < (1ll << 30) && (o1 == o0 || ops), "step %d: bad op range", i);
+    if (st.kind == PG_SORT) continue;
+    const uint32_t* prog = o1 > o0 ? ops + o0 : nullptr;
+    QX_TRY(qx_check_program(&shape, prog, (int32_t)(o1 - o0)));
+    fill_images<u64>(n_qubits, prog, (int)(o1 - o0), cx_c, cx_t, cx_s, &st.im);
+    if (st.kind == PG_OPRUN) {
+      QX_REQUIRE(counts && axes && weights, "step %d: operator tables missing", i);
+      QX_TRY(fill_table(&shape, counts + (size_t)i * n_qubits * 3, axes + (size_t)i * n_qubits * 9,
+                        weights + (size_t)i * n_qubits * 9, &st.tb));
+      st.order = order ? (order[i] != 0) : 0;
+      st.rank_row = rows++;
+    }
+  }
+  QX_CUDA(cudaSetDevice(device));
+  qx_program* p = new qx_program;
+  p->device = device;
+  p->n_qubits = n_qubits;
+  p->n_steps = n_steps;
+  p->n_rows = rows;
+  cudaError_t e = cudaMalloc(reinterpret_cast<void**>(&p->d_steps), sizeof(PgStep) * (size_t)n_steps);
+  if (e == cudaSuccess) e = cudaMemcpy(p->d_steps, steps.data(), sizeof(PgStep) * (size_t)n_steps, cudaMemcpyHostToDevice);
+  if (e != cudaSuccess) {
+    if (p->d_steps) cudaFree(p->d_steps);
+    delete p;
+    return qx_fail(QX_ERR_CUDA, "uploading a circuit program failed: %s", cudaGetErrorString(e));
+  }
+  *out = p;
+  return QX_OK;
+}
+
+extern "C" int qx_program_destroy(qx_program* p) {
+  if (!p) return QX_OK;
+  if (p->d_steps) {
+    cudaSetDevice(p->device);
+    cudaFree(p->d_steps);
+  }
+  delete p;
+  return QX_OK;
+}
+
+extern "C" int qx_program_rows(const qx_program* p, int32_t* rows) {
+  QX_REQUIRE(p && rows, "NULL argument");
+  *rows = p->n_rows;
+  return QX_OK;
+}
+
+// One launch for the whole program.  *fitted = 0: some generator outgrew shared memory; the store
+// is as it was before the call and `ranks` is undefined.  *fitted = 1: the store holds the result
+// (canonical if the program ends in an oprun or a sort step), ranks[row * n_segments + g] = terms
+// of generator g after the row-th branching step (a 0 = collapsed there; later rows of it are 0).
+extern "C" int qx_store_run_program(qx_store* s, const qx_program* p, const int32_t* init_qubits, double eps,
+                                    int64_t* ranks, int64_t* raw_total, int32_t* fitted, int64_t* offsets,
+                                    uint64_t* host_keys, double* host_lambdas, int64_t host_cap,
+                                    int32_t* host_filled) {
+  QX_REQUIRE(s && p && fitted, "NULL argument");
+  QX_NARROW_ONLY(s, "qx_store_run_program");
+  QX_REQUIRE(p->n_qubits == s->n_qubits && p->device == s->device, "program was compiled for n=%d on device %d",
+             p->n_qubits, p->device);
+  QX_REQUIRE(eps >= 0.0, "eps must be non-negative");
+  QX_REQUIRE(p->n_rows == 0 || ranks, "ranks is NULL");
+  QX_REQUIRE((host_keys == nullptr) == (host_lambdas == nullptr), "host_keys and host_lambdas go together");
+  *fitted = 0;
+  if (host_filled) *host_filled = 0;
+  static const bool off = getenv("QX_NO_PROGRAM") != nullptr;
+  if (off || s->n_seg < 1) return QX_OK;
+  PgInit init;
+  memset(&init, 0, sizeof(init));
+  if (init_qubits) {
+    QX_REQUIRE(s->n_seg <= QX_MAX_QUBITS, "init_qubits: at most %d generators", QX_MAX_QUBITS);
+    init.on = 1;
+    init.n_qubits = s->n_qubits;
+    for (int g = 0; g < s->n_seg; ++g) {
+      QX_REQUIRE(init_qubits[g] >= 0 && init_qubits[g] < s->n_qubits, "qubit %d out of range for n=%d", init_qubits[g],
+                 s->n_qubits);
+      init.qubit[g] = init_qubits[g];
+    }
+  }
+  QX_CUDA(cudaSetDevice(s->device));
+  if (!init.on) {
+    if (!s->exact) QX_TRY(qx_store_refresh(s));
+    if (s->ub_seg > kPgSrcCap) return QX_OK;
+  }
+  QX_TRY(qx_store_reserve(s, (int64_t)s->n_seg * kPgSrcCap + 2, !init.on));
+  const int64_t status_bytes = 8 * ((int64_t)s->n_seg + 1);
+  QX_TRY(qx_store_scratch(s, status_bytes));
+  QX_CUDA(cudaMemsetAsync(s->scratch, 0, (size_t)status_bytes, s->stream));
+  u64* status = reinterpret_cast<u64*>(s->scratch);
+  // what the kernel reports, in page-locked host memory
+  const int64_t rank_words = (int64_t)p->n_rows * s->n_seg;
+  const int64_t need = 3 * (int64_t)s->n_seg + 1 + rank_words;
+  int64_t* h = s->h_pinned;
+  void* h_big = nullptr;
+  if (need > s->h_pinned_words) {
+    QX_TRY(qx_pinned_alloc(&h_big, 8 * need));
+    h = reinterpret_cast<int64_t*>(h_big);
+  }
+  struct ReleasePinned {
+    void* p;
+    ~ReleasePinned() { if (p) qx_pinned_free(p); }
+  } relp{h_big};
+  memset(h, 0, 8 * (size_t)need);
+  PgHost host;
+  host.flags = h;
+  host.raw = h + s->n_seg;
+  host.seg = h + 2 * s->n_seg;
+  host.ranks = h + 3 * s->n_seg + 1;
+  host.keys = reinterpret_cast<u64*>(host_keys);
+  host.lam = host_lambdas;
+  host.cap = host_keys ? host_cap : 0;
+  static bool attr_set = false;
+  if (!attr_set) {
+    QX_CUDA(cudaFuncSetAttribute(k_small_circuit, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(PgSmem)));
+    attr_set = true;
+  }
+  const int in = s->cur, out = s->cur ^ 1;
+  {
+    QxProfileScope prof(QX_K_SMALL_MERGE, s->stream, 32.0 * (double)std::max<int64_t>(s->ub_total, s->n_seg));
+    k_small_circuit<<<s->n_seg, kPgThreads, sizeof(PgSmem), s->stream>>>(
+        s->keys[in], s->lam[in], s->seg[in], s->n_seg, p->d_steps, p->n_steps, s->keys[out], s->lam[out],
+        s->seg[out], status, eps, init, host);
+    QX_CUDA(cudaGetLastError());
+  }
+  QX_CUDA(cudaStreamSynchronize(s->stream));
+  int64_t flags = 0, raw = 0;
+  for (int g = 0; g < s->n_seg; ++g) {
+    flags |= host.flags[g];
+    raw += host.raw[g];
+  }
+  if (flags & 1) {
+    // did not fit: the live buffer is untouched -- unless there was none (init_qubits): make it
+    if (init.on) return qx_store_init_z(s, init_qubits);
+    return QX_OK;
+  }
+  for (int g = 0; g <= s->n_seg; ++g) s->h_seg[g] = host.seg[g];
+  if (offsets)
+    for (int g = 0; g <= s->n_seg; ++g) offsets[g] = host.seg[g];
+  for (int64_t i = 0; i < rank_words; ++i) ranks[i] = host.ranks[i];
+  if (raw_total) *raw_total = raw;
+  if (host_filled) *host_filled = (host_keys && !(flags & 2)) ? 1 : 0;
+  s->cur = out;
+  s->exact = true;
+  s->narrow_keys = false;
+  s->pack_bnd = nullptr;
+  s->ub_total = s->h_seg[s->n_seg];
+  int64_t mx = 0;
+  for (int g = 0; g < s->n_seg; ++g) mx = std::max(mx, s->h_seg[g + 1] - s->h_seg[g]);
+  s->ub_seg = mx;
+  *fitted = 1;
+  return QX_OK;
+}
 
 extern "C" int qx_apply_operator(qx_store* s, const int32_t* counts, const int32_t* axes,
                                  const double* weights, int64_t term_limit, int64_t* raw_total) {

@@ -43,7 +43,7 @@ from .stabilizer import (
     rank_stats,
     split_tables,
 )
-from .store import DeviceStore
+from .store import CircuitProgram, DeviceStore
 
 
 class Mode(Enum):
@@ -211,8 +211,9 @@ class _Walker:
             self.flush()
             self._merge_now(step, phase, after_branch=True)
         self.pending = None
+        row = list(self.ranks)
         for slot in self.open_slots:
-            trace[slot] = list(self.ranks)
+            trace[slot] = row.copy()
         self.open_slots = []
         if self.updates is not None and self.pending_gates:
             self.updates += np.asarray(self.ranks, dtype=np.int64) * self.pending_gates
@@ -237,6 +238,15 @@ class _Walker:
         else:
             self.open_slots.append(len(trace))
             trace.append(None)
+
+    def snapshots(self, trace, k: int):
+        """k rank-trace rows at once (runs of permutation operators)."""
+        if self.pending is None:
+            row = list(self.ranks)
+            trace.extend([row.copy() for _ in range(k)])
+        else:
+            self.open_slots.extend(range(len(trace), len(trace) + k))
+            trace.extend([None] * k)
 
     def count_gate(self):
         """v1: one more gate sees the current terms."""
@@ -306,7 +316,6 @@ def run(instructions: Sequence[Instruction], n: int, mode, eps: float = DEFAULT_
             walker_ranks = [len(l) for l, _ in initial]
             min_abs = min((float(np.min(np.abs(l))) for l, _ in initial if len(l)), default=1.0)
         else:
-            store.init_z(ids)
             walker_ranks = [1] * len(ids)
             min_abs = 1.0
         w = _Walker(store, n, ids, eps, timings, before_merge, reduce_ranks)
@@ -320,7 +329,40 @@ def run(instructions: Sequence[Instruction], n: int, mode, eps: float = DEFAULT_
         w.eager = eager
         trace = [list(w.ranks)]
 
-        if mode is Mode.V1:
+        # One launch for the whole circuit while every generator stays small (csrc/program.cuh);
+        # v2 only where its dense layout needs no term-dependent decision (stabilizer.py:264-286)
+        programmed, program_segs, made = False, None, initial is not None
+        if (not eager and n <= 32 and before_merge is None and reduce_ranks is None and slot_part is None
+                and _PROGRAMS_ON and ids and max(walker_ranks, default=0) <= PROGRAM_MAX_TERMS
+                and store._cx == _lut.STANDARD_CX
+                and (mode is not Mode.V2 or (4 ** n <= DENSE_FLATTEN_BUDGET and eps > 0.0))):
+            t0 = time.perf_counter()
+            if mode is not Mode.V1:
+                plan.lut()
+            program = _program_for(plan, instructions, n, mode, store.device)
+            timings["lut"] = time.perf_counter() - t0
+            if program is not None:
+                t0 = time.perf_counter()
+                # generators that start as Z words are made in the kernel (no upload); a run that
+                # does not fit leaves the store as init_z would have
+                fitted, rows, _, program_segs = store.run_program(
+                    program, eps, init_qubits=None if made else ids, to_host=download, pinned=pinned)
+                made = True
+                dt = time.perf_counter() - t0
+                if fitted:
+                    programmed = True
+                    w.store = _ReplayStore(rows, store.device)
+                    _walk_events(w, _program_events(plan, instructions, mode), mode, trace, counters)
+                    w.store = store
+                    timings["sub_flatten" if program.rows else "cx"] += dt
+                    w.launch_log["program_steps"] = program.steps
+                else:
+                    plan._programs[(mode, store.device)] = None      # a generator outgrew it: step by step from now on
+        if not made:
+            store.init_z(ids)
+        if programmed:
+            pass
+        elif mode is Mode.V1:
             if eager:
                 w.updates = np.zeros(len(w.ids), dtype=np.int64)
                 _walk_v1_eager(instructions, partition, w, trace, counters)
@@ -337,11 +379,13 @@ def run(instructions: Sequence[Instruction], n: int, mode, eps: float = DEFAULT_
 
         streamed = None
         partitioned = None
-        if slot_part is not None and before_merge is None and reduce_ranks is None:
+        if programmed:
+            pass
+        elif slot_part is not None and before_merge is None and reduce_ranks is None:
             partitioned = _finish_partitioned(w, trace, slot_part, slot_reduce)
         elif download and before_merge is None and reduce_ranks is None:
             streamed = _finish_streamed(w, trace, pinned)
-        if streamed is None:
+        if streamed is None and not programmed:
             w.finish(trace)              # deferred merge, queued permutations, canonical order
         counters["operators"] = partition.k + partition.k_prime
 
@@ -356,7 +400,7 @@ def run(instructions: Sequence[Instruction], n: int, mode, eps: float = DEFAULT_
             info["updates_per_generator"] = w.updates.tolist()
         final = None
         if download:
-            segs = streamed if streamed is not None else store.segments(pinned)
+            segs = streamed if streamed is not None else program_segs if program_segs is not None else store.segments(pinned)
             final_gens = [SimpleGenerator(n, lam, keys_to_indices(keys, n)) for lam, keys in segs]
             whole = len(final_gens) == n and not partitioned
             final = GeneratorSet(n, final_gens) if whole else _Shard(n, ids, final_gens)
@@ -384,6 +428,7 @@ def run(instructions: Sequence[Instruction], n: int, mode, eps: float = DEFAULT_
 # of 1647 operator steps.  Plans are found again by IDENTITY of the (immutable) instructions:
 # `all(a is b)` over 5000 gates is ~0.1 ms, hashing them would cost more than it saves.
 _PLAN_SLOTS = 8
+_PROGRAMS_ON = not __import__("os").environ.get("QX_NO_PROGRAM")
 SMALL_RAW = 8192                  # raw terms per generator the one-launch operator step takes (QX_SMALL_MAX)
 _plans: list = []
 
@@ -396,6 +441,7 @@ class _Plan:
         self._lut = None
         self._v1 = None
         self._ops = None
+        self._programs = {}            # (mode, device) -> CircuitProgram | None (does not qualify / did not fit)
 
     def matches(self, instructions, n: int) -> bool:
         mine = self.instructions
@@ -415,6 +461,103 @@ class _Plan:
         if self._ops is None:
             self._ops = _compile_operators(self.partition, *self.lut(), self.n)
         return self._ops
+
+
+# ------------------------------------------------------------------------------------------
+# whole-circuit programs (csrc/program.cuh)
+# ------------------------------------------------------------------------------------------
+# What a plan's events make the walker do on the device does not depend on the terms (as long as
+# every generator stays small, nothing is term-partitioned and eps cannot drop an input term):
+# the walker is run ONCE against a store that only records the calls, the record becomes a
+# device-resident step list, and from then on a run is one launch + one read-back; the walker is
+# then replayed against the recorded ranks for the rank trace, the update counts and the
+# collapse error -- the same code that books them in the step-by-step path.
+PROGRAM_MAX_TERMS = 4096          # terms per generator the one-launch path holds (kPgSrcCap)
+
+
+class _RecordingStore:
+    """Stands in for a DeviceStore while a plan is compiled: records the device steps."""
+
+    def __init__(self, n: int, n_gen: int):
+        self.n, self.n_gen = n, n_gen
+        self.steps, self.order_next = [], False
+
+    def apply_clifford(self, program):
+        if len(program):
+            self.steps.append(("clifford", [int(v) for v in program]))
+
+    def order_for_operator(self, counts, by_key: bool = True):
+        if not by_key:
+            raise _NoProgram
+        self.order_next = True
+
+    def apply_operator_run(self, counts, axes, weights, program, eps, term_limit: int = 0):
+        self.steps.append(("oprun", self.order_next, counts, axes, weights, [int(v) for v in program]))
+        self.order_next = False
+        return 0, [1] * self.n_gen
+
+    def sort(self):
+        self.steps.append(("sort",))
+
+    def __getattr__(self, name):      # anything else (merge, apply_split, count_operator ...): no program
+        raise _NoProgram
+
+
+class _ReplayStore:
+    """Stands in for the store after the program ran: hands the recorded ranks to the walker."""
+
+    def __init__(self, rows, device):
+        self.rows, self.next, self.device = rows, 0, device
+
+    def apply_clifford(self, program):
+        pass
+
+    def order_for_operator(self, counts, by_key: bool = True):
+        pass
+
+    def sort(self):
+        pass
+
+    def apply_operator_run(self, counts, axes, weights, program, eps, term_limit: int = 0):
+        row = self.rows[self.next]
+        self.next += 1
+        return 0, list(row)
+
+
+class _NoProgram(Exception):
+    pass
+
+
+def _program_events(plan: "_Plan", instructions, mode):
+    if mode is Mode.V1:
+        return plan.v1_events(instructions)
+    return plan.operator_events()
+
+
+def _walk_events(w: _Walker, compiled, mode, trace, counters):
+    if mode is Mode.V1:
+        _replay_v1(compiled, w, trace, counters)
+    else:
+        _replay_operators(compiled, w, trace, counters, mode)
+    w.finish(trace)
+
+
+def _program_for(plan: "_Plan", instructions, n: int, mode, device: int):
+    """The plan's device program for this mode, compiled on first use; None if it has none."""
+    key = (mode, device)
+    if key not in plan._programs:
+        program = None
+        try:
+            rec = _RecordingStore(n, n)
+            w = _Walker(rec, n, range(n), DEFAULT_EPS, {"partition": 0.0, "lut": 0.0, "sub_flatten": 0.0, "cx": 0.0})
+            _walk_events(w, _program_events(plan, instructions, mode), mode, [list(w.ranks)],
+                         {"sub_flatten_ops": 0, "cx_applications": 0})
+            if rec.steps:
+                program = CircuitProgram(n, rec.steps, device)
+        except _NoProgram:
+            program = None
+        plan._programs[key] = program
+    return plan._programs[key]
 
 
 def _plan_for(instructions, n: int, mode) -> _Plan:
@@ -567,8 +710,7 @@ def _replay_operators(compiled, w: _Walker, trace, counters, mode):
         if ev[0] == "q":
             w.queue.extend(ev[1])
             w.queue_has_cx = w.queue_has_cx or ev[2]
-            for _ in range(ev[3]):
-                w.snapshot(trace)
+            w.snapshots(trace, ev[3])
             continue
         _, step, counts, axes, weights = ev
         w.resolve(trace)               # expand merged terms only

@@ -213,6 +213,9 @@ def cx_device_words(sign_table=None) -> tuple:
     return wc, wt, ws
 
 
+STANDARD_CX = cx_device_words()   # the reference's tables; folded runs and circuit programs assume them
+
+
 def perm_word(block: np.ndarray):
     """Pack a 3x3 block as a signed axis permutation, or None if it is not one.
 

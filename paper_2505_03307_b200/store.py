@@ -17,6 +17,7 @@ from . import lut
 
 # host threads of a narrow download: four saturate what the host memory system spares next to the DMA
 # (more only contend with it: 35.4 ms with 4, 39.8 ms with 8 on a 16-core host)
+PROGRAM_TERMS = 4096              # terms per generator a one-launch run can return (kPgSrcCap, csrc/program.cuh)
 HOST_WIDEN_THREADS = int(os.environ.get("QX_WIDEN_THREADS", 0)) or max(1, min(4, (os.cpu_count() or 2) // 2))
 
 
@@ -253,6 +254,39 @@ class DeviceStore:
             len(prog), c, t, s, float(eps), int(part), int(parts), nat.ptr(ranks), C.byref(flag)))
         return ranks.tolist(), bool(flag.value)
 
+    def run_program(self, program: "CircuitProgram", eps: float, init_qubits=None, to_host: bool = False,
+                    pinned: bool = False):
+        """The whole compiled circuit in one launch (qx_store_run_program).  Returns (fitted, ranks,
+        raw, segments): ranks[row][g] after the row-th branching step; fitted False = the store is
+        untouched (or holds init_z if init_qubits was given).  init_qubits: start from Z words made in
+        the kernel instead of the store's content.  to_host: the kernel also writes the result into
+        page-locked host memory; segments = [(lambdas, keys)] then (views of the pinned block if
+        ``pinned``, fresh arrays otherwise), else None."""
+        ranks = np.zeros((max(program.rows, 1), self.n_segments), dtype=np.int64)
+        raw, fitted, filled = C.c_int64(), C.c_int32(), C.c_int32()
+        off = np.zeros(self.n_segments + 1, dtype=np.int64)
+        init = None if init_qubits is None else np.ascontiguousarray(init_qubits, dtype=np.int32)
+        keys = lam = None
+        cap = 0
+        if to_host:
+            cap = self.n_segments * PROGRAM_TERMS
+            buf = nat.PINNED.take(16 * cap)
+            keys = buf.view(np.uint64, 0, cap)
+            lam = buf.view(np.float64, 8 * cap, cap)
+        nat.check(nat.lib().qx_store_run_program(self._h, program.handle, nat.ptr(init), float(eps), nat.ptr(ranks),
+                                                 C.byref(raw), C.byref(fitted), nat.ptr(off), nat.ptr(keys), nat.ptr(lam),
+                                                 cap, C.byref(filled)))
+        segs = None
+        if fitted.value and filled.value:
+            o = off.tolist()
+            if pinned:
+                segs = [(lam[o[i]:o[i + 1]], keys[o[i]:o[i + 1]]) for i in range(self.n_segments)]
+            else:
+                total = o[-1]
+                k2, l2 = keys[:total].copy(), lam[:total].copy()
+                segs = [(l2[o[i]:o[i + 1]], k2[o[i]:o[i + 1]]) for i in range(self.n_segments)]
+        return bool(fitted.value), ranks[:program.rows].tolist(), raw.value, segs
+
     def count_operator(self, counts) -> list:
         counts = np.ascontiguousarray(counts, dtype=np.int32).reshape(-1)
         out = np.zeros(self.n_segments, dtype=np.int64)
@@ -295,3 +329,54 @@ class DeviceStore:
 
 def _is_object(arr) -> bool:
     return isinstance(arr, np.ndarray) and arr.dtype == object
+
+
+class CircuitProgram:
+    """Device-resident step list of a circuit plan (``qx_program`` in include/qimax_b200.h).
+    steps: ("clifford", ops) | ("oprun", order, counts, axes, weights, ops) | ("sort",)."""
+
+    KINDS = {"clifford": 0, "oprun": 1, "sort": 2}
+
+    def __init__(self, n: int, steps, device=None):
+        self.n, self.device = int(n), nat.default_device() if device is None else int(device)
+        ns = len(steps)
+        kinds = np.zeros(ns, dtype=np.int32)
+        order = np.zeros(ns, dtype=np.int32)
+        counts = np.ones((ns, n, 3), dtype=np.int32)
+        axes = np.zeros((ns, n, 3, 3), dtype=np.int32)
+        weights = np.zeros((ns, n, 3, 3), dtype=np.float64)
+        ops, off = [], [0]
+        for i, st in enumerate(steps):
+            kinds[i] = self.KINDS[st[0]]
+            if st[0] == "clifford":
+                ops.extend(st[1])
+            elif st[0] == "oprun":
+                order[i] = 1 if st[1] else 0
+                counts[i] = np.asarray(st[2], dtype=np.int32).reshape(n, 3)
+                axes[i] = np.asarray(st[3], dtype=np.int32).reshape(n, 3, 3)
+                weights[i] = np.asarray(st[4], dtype=np.float64).reshape(n, 3, 3)
+                ops.extend(st[5])
+            off.append(len(ops))
+        ops = np.asarray(ops, dtype=np.uint32)
+        off = np.asarray(off, dtype=np.int64)
+        self.rows = int((kinds == 1).sum())
+        self.steps = ns
+        self._h = C.c_void_p()
+        nat.check(nat.lib().qx_program_create(self.device, self.n, ns, nat.ptr(kinds), nat.ptr(order), nat.ptr(counts),
+                                              nat.ptr(axes), nat.ptr(weights), nat.ptr(ops) if len(ops) else None,
+                                              nat.ptr(off), C.byref(self._h)))
+
+    @property
+    def handle(self):
+        return self._h
+
+    def close(self):
+        h, self._h = self._h, None
+        if h is not None and h.value:
+            nat.check(nat.lib().qx_program_destroy(h))
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

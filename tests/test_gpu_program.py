@@ -1,0 +1,139 @@
+"""Whole-circuit programs (csrc/program.cuh, qx_store_run_program): one launch per
+run for circuits whose generators stay small, against the step-by-step replay of the same plan --
+final generators bit for bit (keys and coefficients), rank trace, counters, v1 update counts, the
+collapse error (reference engine.py:148-152: generator and step) -- and against the oracle.  Covers
+every step kind (Clifford run, branching operator with and without the v3 source order, final
+re-sort), the three modes, caller-supplied initial generators (read-out back-propagation), the
+"did not fit" fallback and the BASELINE configs 1, 2, 3, 5."""
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+from gpu_util import oracle, qx, report_gens  # noqa: E402
+
+from paper_2505_03307_b200 import _native, engine, workloads  # noqa: E402
+from paper_2505_03307_b200.errors import NumericalCollapseError  # noqa: E402
+
+
+def _both(gates, n, mode, **kw):
+    """(programmed run, step-by-step run) of the same circuit; asserts the first took one launch."""
+    engine.clear_plans()
+    engine._PROGRAMS_ON = True
+    try:
+        qx.run(gates, n, mode, **kw)                     # compiles the plan and its program
+        before = _native.launch_count()
+        a = qx.run(gates, n, mode, **kw)
+        launches = _native.launch_count() - before
+    finally:
+        engine._PROGRAMS_ON = False
+    try:
+        engine.clear_plans()
+        b = qx.run(gates, n, mode, **kw)
+    finally:
+        engine._PROGRAMS_ON = True
+    return a, b, launches
+
+
+def _same(a, b):
+    assert a.rank_trace == b.rank_trace
+    assert a.counters == b.counters
+    assert a.device.get("updates_per_generator") == b.device.get("updates_per_generator")
+    for (la, ka), (lb, kb) in zip(report_gens(a), report_gens(b)):
+        assert np.array_equal(ka, kb)
+        assert np.array_equal(la, lb)                    # bit for bit
+
+
+@pytest.mark.parametrize("mode", ["v1", "v2", "v3"])
+def test_random_circuits_one_launch_equals_step_by_step(mode):
+    for case in range(40):
+        rng = np.random.default_rng([77, case])
+        n = int(rng.integers(2, 9))
+        gates = qx.gen_random(n, int(rng.integers(1, 60)), rng)
+        a, b, launches = _both(gates, n, mode)
+        _same(a, b)
+        assert "program_steps" in a.device and "program_steps" not in b.device
+        assert launches <= 3, launches                   # the circuit kernel + the read-back kernel(s)
+        want = oracle.run(gates, n, mode)
+        assert a.rank_trace == want["rank_trace"]
+        for (lam, keys), (wl, wk) in zip(report_gens(a), want["final"]):
+            assert np.array_equal(keys, wk) and np.max(np.abs(lam - wl), initial=0.0) < 1e-10
+
+
+@pytest.mark.parametrize("name", ["c1_4q_clifford_t", "c2_10q_near_clifford", "c3_16q_clifford", "c5_32q_clifford_t"])
+@pytest.mark.parametrize("mode", ["v1", "v3"])
+def test_baseline_configs_one_launch(name, mode):
+    n, gates = workloads.build(name)
+    a, b, launches = _both(gates, n, mode)
+    _same(a, b)
+    assert "program_steps" in a.device
+    assert launches <= 3, launches
+
+
+def test_v1_and_v3_bitwise_the_oracles_through_programs():
+    for case in range(30):
+        rng = np.random.default_rng([78, case])
+        n = int(rng.integers(3, 8))
+        gates = qx.gen_random(n, 40, rng)
+        for mode in ("v1", "v3"):
+            got = qx.run(gates, n, mode)
+            assert "program_steps" in got.device
+            want = oracle.run(gates, n, mode)
+            for (lam, keys), (wl, wk) in zip(report_gens(got), want["final"]):
+                assert np.array_equal(keys, wk) and np.array_equal(lam, wl)
+
+
+def test_collapse_message_matches_step_by_step():
+    # eps below the initial coefficient (no eager schedule) but above cos(pi/4): both branches of
+    # the first rotation drop
+    n = 3
+    gates = [qx.Instruction("H", (0,)), qx.Instruction("CX", (0, 1)), qx.Instruction("RZ", (1,), np.pi / 4),
+             qx.Instruction("H", (2,))]
+    msgs = []
+    for on in (True, False):
+        engine.clear_plans()
+        engine._PROGRAMS_ON = on
+        try:
+            for mode in ("v1", "v3"):
+                with pytest.raises(NumericalCollapseError) as err:
+                    qx.run(gates, n, mode, eps=0.8)
+                msgs.append((on, mode, str(err.value)))
+        finally:
+            engine._PROGRAMS_ON = True
+    assert [m for on, _, m in msgs if on] == [m for on, _, m in msgs if not on]
+    want = None
+    try:
+        oracle.run(gates, n, "v3", eps=0.8)
+    except Exception as exc:                              # the port raises the reference's message
+        want = str(exc)
+    assert want is not None and msgs[1][2] == want
+
+
+def test_too_large_a_circuit_falls_back_and_remembers():
+    n, gates = 8, qx.gen_xyz_chain(8, 2, 1, rng=4)        # 3**8 branches per term: no program fits
+    engine.clear_plans()
+    a = qx.run(gates, n, "v3")
+    assert "program_steps" not in a.device
+    plan = engine._plan_for(gates, n, engine.Mode.V3)
+    assert plan._programs[(engine.Mode.V3, a.device["device"])] is None
+    want = oracle.run(gates, n, "v3")
+    assert a.rank_trace == want["rank_trace"]
+    for (lam, keys), (wl, wk) in zip(report_gens(a), want["final"]):
+        assert np.array_equal(keys, wk) and np.max(np.abs(lam - wl)) < 1e-10
+
+
+def test_initial_generators_and_shards_go_through_programs():
+    n, gates = workloads.build("c2_10q_near_clifford")
+    full = qx.run(gates, n, "v3")
+    part = qx.run(gates, n, "v3", generators=[7, 2, 9])
+    assert "program_steps" in part.device
+    for g, (lam, keys) in zip([7, 2, 9], report_gens(part)):
+        assert np.array_equal(keys, full.final.generators[g].keys())
+        assert np.array_equal(lam, full.final.generators[g].lambdas)
+    rng = np.random.default_rng(5)
+    init = [(rng.uniform(0.5, 1.0, size=4), np.sort(rng.choice(4 ** n, size=4, replace=False)).astype(np.uint64))
+            for _ in range(5)]
+    a, b, _ = _both(gates, n, "v3", initial=init)
+    _same(a, b)
+    assert "program_steps" in a.device
