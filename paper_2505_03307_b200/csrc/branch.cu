@@ -1086,6 +1086,7 @@ struct qx_program {
   int n_steps = 0;
   int n_rows = 0;             // oprun steps = rows of the ranks table
   PgStep* d_steps = nullptr;
+  int small_fits = -1;        // what the last run found: 1 = the small kernel variant is enough, 0 = it is not
 };
 
 extern "C" int qx_program_create(int device, int32_t n_qubits, int32_t n_steps, const int32_t* kinds,
@@ -1194,7 +1195,6 @@ extern "C" int qx_store_run_program(qx_store* s, const qx_program* p, const int3
   QX_TRY(qx_store_reserve(s, (int64_t)s->n_seg * kPgSrcCap + 2, !init.on));
   const int64_t status_bytes = 8 * ((int64_t)s->n_seg + 1);
   QX_TRY(qx_store_scratch(s, status_bytes));
-  QX_CUDA(cudaMemsetAsync(s->scratch, 0, (size_t)status_bytes, s->stream));
   u64* status = reinterpret_cast<u64*>(s->scratch);
   // what the kernel reports, in page-locked host memory
   const int64_t rank_words = (int64_t)p->n_rows * s->n_seg;
@@ -1209,7 +1209,6 @@ extern "C" int qx_store_run_program(qx_store* s, const qx_program* p, const int3
     void* p;
     ~ReleasePinned() { if (p) qx_pinned_free(p); }
   } relp{h_big};
-  memset(h, 0, 8 * (size_t)need);
   PgHost host;
   host.flags = h;
   host.raw = h + s->n_seg;
@@ -1220,22 +1219,38 @@ extern "C" int qx_store_run_program(qx_store* s, const qx_program* p, const int3
   host.cap = host_keys ? host_cap : 0;
   static bool attr_set = false;
   if (!attr_set) {
-    QX_CUDA(cudaFuncSetAttribute(k_small_circuit, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(PgSmem)));
+    QX_CUDA(cudaFuncSetAttribute(k_small_circuit<PgSmem>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(PgSmem)));
     attr_set = true;
   }
   const int in = s->cur, out = s->cur ^ 1;
-  {
-    QxProfileScope prof(QX_K_SMALL_MERGE, s->stream, 32.0 * (double)std::max<int64_t>(s->ub_total, s->n_seg));
-    k_small_circuit<<<s->n_seg, kPgThreads, sizeof(PgSmem), s->stream>>>(
-        s->keys[in], s->lam[in], s->seg[in], s->n_seg, p->d_steps, p->n_steps, s->keys[out], s->lam[out],
-        s->seg[out], status, eps, init, host);
-    QX_CUDA(cudaGetLastError());
-  }
-  QX_CUDA(cudaStreamSynchronize(s->stream));
+  // the small variant first unless the last run of this program outgrew it (a circuit's ranks do
+  // not change from run to run); the full one if it does not fit
+  qx_program* pm = const_cast<qx_program*>(p);
   int64_t flags = 0, raw = 0;
-  for (int g = 0; g < s->n_seg; ++g) {
-    flags |= host.flags[g];
-    raw += host.raw[g];
+  for (int variant = (pm->small_fits == 0 || s->ub_seg > PgSmemSmall::kSrcCap) ? 1 : 0; variant < 2; ++variant) {
+    memset(h, 0, 8 * (size_t)need);
+    QX_CUDA(cudaMemsetAsync(s->scratch, 0, (size_t)status_bytes, s->stream));
+    {
+      QxProfileScope prof(QX_K_SMALL_MERGE, s->stream, 32.0 * (double)std::max<int64_t>(s->ub_total, s->n_seg));
+      if (variant == 0)
+        k_small_circuit<PgSmemSmall><<<s->n_seg, kPgThreads, sizeof(PgSmemSmall), s->stream>>>(
+            s->keys[in], s->lam[in], s->seg[in], s->n_seg, p->d_steps, p->n_steps, s->keys[out], s->lam[out],
+            s->seg[out], status, eps, init, host);
+      else
+        k_small_circuit<PgSmem><<<s->n_seg, kPgThreads, sizeof(PgSmem), s->stream>>>(
+            s->keys[in], s->lam[in], s->seg[in], s->n_seg, p->d_steps, p->n_steps, s->keys[out], s->lam[out],
+            s->seg[out], status, eps, init, host);
+      QX_CUDA(cudaGetLastError());
+    }
+    QX_CUDA(cudaStreamSynchronize(s->stream));
+    flags = 0;
+    raw = 0;
+    for (int g = 0; g < s->n_seg; ++g) {
+      flags |= host.flags[g];
+      raw += host.raw[g];
+    }
+    if (variant == 0) pm->small_fits = (flags & 1) ? 0 : 1;
+    if (!(flags & 1)) break;
   }
   if (flags & 1) {
     // did not fit: the live buffer is untouched -- unless there was none (init_qubits): make it

@@ -43,18 +43,30 @@ struct __align__(16) PgStep {
   ImageTable<u64> im;   // clifford, oprun (identity images: no run behind the operator)
 };
 
-struct PgSmem {
-  u64 rkey[kPgRawCap];
-  double rlam[kPgRawCap];
-  u64 ckey[kPgSrcCap];
-  double clam[kPgSrcCap];
-  unsigned short ridx[kPgRawCap];
-  unsigned short soff[kPgSrcCap + 8];
-  OperatorTable tb;
-  ImageTable<u64> im;
+template <int kSrc, int kRaw>
+struct PgSmemT {
+  static constexpr int kSrcCap = kSrc, kRawCap = kRaw;
+  u64 rkey[kRaw];
+  double rlam[kRaw];
+  u64 ckey[kSrc];
+  double clam[kSrc];
+  unsigned short ridx[kRaw];
+  unsigned short soff[kSrc + 8];
+  PgStep st;                   // the step being executed (header, operator table, images)
   u64 scan[kPgWarps + 1];
   u64 base;
+  u32 kept_tab[(kRaw + kPgThreads - 1) / kPgThreads * kPgWarps];
+  u32 kept_total;
+  u64 bmask;
+  int fast;
 };
+
+// Two sizes: the full one fills an SM's shared memory (one CTA per SM, and the launch switches the
+// SM's shared-memory carve-out: ~10 us on an otherwise idle GPU); circuits whose generators stay
+// below 256 terms (configs 1, 2, 3) take the small one.
+typedef PgSmemT<kPgSrcCap, kPgRawCap> PgSmem;
+typedef PgSmemT<256, 512> PgSmemSmall;
+static_assert(sizeof(PgSmem) <= 227 * 1024, "one CTA's shared memory");
 
 template <typename T>
 __device__ __forceinline__ T pg_block_exclusive_sum(T v, u64* scan, T& total) {
@@ -73,6 +85,131 @@ __device__ __forceinline__ T pg_block_exclusive_sum(T v, u64* scan, T& total) {
   total = (T)scan[kPgWarps];
   __syncthreads();
   return out;
+}
+
+// Bitonic network over the m = 2^x >= 32 pairs (rkey[e], ridx[e]) in shared memory, ascending by
+// key, ties by index (a stable sort of whatever the indices stand for).  All three orderings of
+// the kernel go through it; the payloads are gathered through the sorted indices afterwards.
+//   * pairs at distance <= 32 lie inside one 64-element chunk, and a chunk always belongs to the
+//     same warp: those substeps (all of the phases k <= 64, the last six of every later phase) run
+//     warp by warp with __syncwarp only -- m = 8192 costs 36 CTA barriers instead of 91;
+//   * a thread's compare-exchanges of one substep are independent: their loads are issued in
+//     batches before the first compare (the network is latency-bound: one CTA per SM, 16 warps).
+constexpr int kPgBatch = 4;
+
+// compare-exchange of the pairs t, t + stride, ... (kPgBatch of them, those below `limit`) of the
+// substep (k, j); pair t of a substep touches lo = t with a zero inserted at bit log2(j), hi = lo | j
+template <typename SM>
+__device__ __forceinline__ void pg_cmpxchg_batch(SM& sm, int t0, int stride, int limit, int k, int j) {
+  u64 ka[kPgBatch], kb[kPgBatch];
+  unsigned short ia[kPgBatch], ib[kPgBatch];
+#pragma unroll
+  for (int i = 0; i < kPgBatch; ++i) {
+    const int t = t0 + i * stride;
+    if (t < limit) {
+      const int lo = ((t & ~(j - 1)) << 1) | (t & (j - 1));
+      ka[i] = sm.rkey[lo];
+      kb[i] = sm.rkey[lo | j];
+      ia[i] = sm.ridx[lo];
+      ib[i] = sm.ridx[lo | j];
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < kPgBatch; ++i) {
+    const int t = t0 + i * stride;
+    if (t < limit) {
+      const int lo = ((t & ~(j - 1)) << 1) | (t & (j - 1));
+      const bool greater = ka[i] > kb[i] || (ka[i] == kb[i] && ia[i] > ib[i]);
+      if (greater == ((lo & k) == 0)) {
+        sm.rkey[lo] = kb[i];
+        sm.rkey[lo | j] = ka[i];
+        sm.ridx[lo] = ib[i];
+        sm.ridx[lo | j] = ia[i];
+      }
+    }
+  }
+}
+
+template <typename SM>
+__device__ __noinline__ void pg_sort_pairs(SM& sm, int m) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (m <= 128) {
+    // a handful of terms (configs 1, 2, 3 never leave this branch): every element counts the
+    // elements in front of it -- m broadcast reads, two barriers, no network.  Callers hand the
+    // pairs over with ridx[e] == e, so ties go by position.
+    u64 mine = 0;
+    int rank = 0;
+    if (tid < m) {
+      mine = sm.rkey[tid];
+#pragma unroll 8
+      for (int j = 0; j < m; ++j) {
+        const u64 kj = sm.rkey[j];
+        rank += (kj < mine || (kj == mine && j < tid)) ? 1 : 0;
+      }
+    }
+    __syncthreads();
+    if (tid < m) {
+      sm.rkey[rank] = mine;
+      sm.ridx[rank] = (unsigned short)tid;
+    }
+    __syncthreads();
+    return;
+  }
+  const int pairs = m >> 1;
+  // pair index t = 32 * chunk + lane covers chunk `chunk` of 64 elements (m >= 64); for m = 32 the
+  // first half-warp covers the only chunk
+  auto warp_part = [&](int k_lo, int k_hi) {
+    for (int k = k_lo; k <= k_hi; k <<= 1) {
+      for (int j = min(k >> 1, 32); j > 0; j >>= 1) {
+        for (int t0 = warp * 32 + lane; t0 < pairs; t0 += 32 * kPgWarps * kPgBatch)
+          pg_cmpxchg_batch(sm, t0, 32 * kPgWarps, pairs, k, j);
+        __syncwarp();
+      }
+    }
+  };
+  warp_part(2, min(m, 64));
+  __syncthreads();
+  for (int k = 128; k <= m; k <<= 1) {
+    for (int j = k >> 1; j >= 64; j >>= 1) {
+      for (int t0 = tid; t0 < pairs; t0 += kPgThreads * kPgBatch) pg_cmpxchg_batch(sm, t0, kPgThreads, pairs, k, j);
+      __syncthreads();
+    }
+    warp_part(k, k);
+    __syncthreads();
+  }
+}
+
+// the generator's terms into the order of the sorted indices (payload gather behind pg_sort_pairs);
+// take_keys: the sorted rkey ARE the new keys, otherwise they are gathered like the coefficients
+template <typename SM>
+__device__ __forceinline__ void pg_gather_terms(SM& sm, int len, bool take_keys) {
+  const int tid = threadIdx.x;
+  for (int e = tid; e < len; e += kPgThreads) {
+    const int from = sm.ridx[e];
+    sm.rlam[e] = sm.clam[from];
+    if (!take_keys) sm.rkey[e] = sm.ckey[from];
+  }
+  __syncthreads();
+  for (int e = tid; e < len; e += kPgThreads) {
+    sm.ckey[e] = sm.rkey[e];
+    sm.clam[e] = sm.rlam[e];
+  }
+  __syncthreads();
+}
+
+// canonical order of the generator's terms (keys are unique)
+template <typename SM>
+__device__ __forceinline__ void pg_sort_terms(SM& sm, int len) {
+  const int tid = threadIdx.x;
+  int m = 32;
+  while (m < len) m <<= 1;
+  for (int e = tid; e < m; e += kPgThreads) {
+    sm.rkey[e] = e < len ? sm.ckey[e] : ~0ull;
+    sm.ridx[e] = (unsigned short)e;
+  }
+  __syncthreads();
+  pg_sort_pairs(sm, m);
+  pg_gather_terms(sm, len, true);
 }
 
 // image of one term under the step's run: digits composed qubit 0 first; returns the sign flip
@@ -110,17 +247,20 @@ struct PgHost {
   int64_t cap;
 };
 
+template <typename SM>
 __global__ void __launch_bounds__(kPgThreads, 1)
 k_small_circuit(const u64* __restrict__ keys_in, const double* __restrict__ lam_in,
                 const int64_t* __restrict__ seg_in, int n_seg, const PgStep* __restrict__ steps, int n_steps,
                 u64* __restrict__ keys_out, double* __restrict__ lam_out, int64_t* __restrict__ seg_out,
                 u64* status, double eps, const __grid_constant__ PgInit init, const __grid_constant__ PgHost host) {
   extern __shared__ __align__(16) unsigned char pg_raw[];
-  PgSmem& sm = *reinterpret_cast<PgSmem*>(pg_raw);
+  SM& sm = *reinterpret_cast<SM*>(pg_raw);
+  constexpr int kSrcCap = SM::kSrcCap, kRawCap = SM::kRawCap;
   const int g = (int)blockIdx.x;             // in-order dispatch (look-back at the very end only)
   const int tid = threadIdx.x;
   int len;
   bool bad = false;
+  bool sorted = init.on != 0;                // the terms are in word order (a single Z word is)
   u64 raw_sum = 0;
   if (init.on) {
     len = 1;
@@ -131,7 +271,7 @@ k_small_circuit(const u64* __restrict__ keys_in, const double* __restrict__ lam_
   } else {
     const int64_t start = seg_in[g];
     len = (int)min((int64_t)0x7fffffff, seg_in[g + 1] - start);
-    bad = len > kPgSrcCap;
+    bad = len > kSrcCap;
     if (bad) len = 0;
     for (int e = tid; e < len; e += kPgThreads) {
       sm.ckey[e] = keys_in[start + e];
@@ -140,57 +280,58 @@ k_small_circuit(const u64* __restrict__ keys_in, const double* __restrict__ lam_
   }
   __syncthreads();
 
-  for (int si = 0; si < n_steps && !bad && len > 0; ++si) {
-    const PgStep* st = steps + si;
-    const int kind = st->kind;
-    if (kind == PG_SORT) {
-      int m = 32;
-      while (m < len) m <<= 1;
-      for (int e = len + tid; e < m; e += kPgThreads) sm.ckey[e] = ~0ull;
-      __syncthreads();
-      for (int k = 2; k <= m; k <<= 1) {
-        for (int j = k >> 1; j > 0; j >>= 1) {
-          for (int t = tid; t < (m >> 1); t += kPgThreads) {
-            const int lo = ((t & ~(j - 1)) << 1) | (t & (j - 1));
-            const int hi = lo | j;
-            const u64 ka = sm.ckey[lo], kb = sm.ckey[hi];
-            if ((ka > kb) == ((lo & k) == 0)) {
-              sm.ckey[lo] = kb; sm.ckey[hi] = ka;
-              const double la = sm.clam[lo]; sm.clam[lo] = sm.clam[hi]; sm.clam[hi] = la;
-            }
-          }
-          __syncthreads();
-        }
-      }
-      continue;
+  // The record of a step (16-byte header, operator table, images: 4.3 KB) is loaded into
+  // registers one step AHEAD and only stored to shared memory when its step begins: the global
+  // round trip hides behind the previous step instead of standing in front of every step.
+  constexpr int kStepWords = (int)(sizeof(PgStep) / 4);
+  constexpr int kPre = (kStepWords + kPgThreads - 1) / kPgThreads;
+  u32 pre[kPre];
+  auto prefetch = [&](int si) {
+    const u32* src = reinterpret_cast<const u32*>(steps + si);
+#pragma unroll
+    for (int i = 0; i < kPre; ++i) {
+      const int at = tid + i * kPgThreads;
+      pre[i] = at < kStepWords ? __ldg(src + at) : 0u;
     }
-    // tables of the step
+  };
+  if (n_steps > 0) prefetch(0);
+  __syncthreads();
+
+  for (int si = 0; si < n_steps && !bad && len > 0; ++si) {
     {
-      const u32* isrc = reinterpret_cast<const u32*>(&st->im);
-      u32* idst = reinterpret_cast<u32*>(&sm.im);
-      for (int i = tid; i < (int)(sizeof(ImageTable<u64>) / 4); i += kPgThreads) idst[i] = isrc[i];
-      if (kind == PG_OPRUN) {
-        const u32* src = reinterpret_cast<const u32*>(&st->tb);
-        u32* dst = reinterpret_cast<u32*>(&sm.tb);
-        for (int i = tid; i < (int)(sizeof(OperatorTable) / 4); i += kPgThreads) dst[i] = src[i];
+      u32* dst = reinterpret_cast<u32*>(&sm.st);
+#pragma unroll
+      for (int i = 0; i < kPre; ++i) {
+        const int at = tid + i * kPgThreads;
+        if (at < kStepWords) dst[at] = pre[i];
       }
     }
     __syncthreads();
+    if (si + 1 < n_steps) prefetch(si + 1);
+    const PgStep* st = &sm.st;
+    const int kind = st->kind;
+    if (kind == PG_SORT) {
+      pg_sort_terms(sm, len);
+      sorted = true;
+      continue;
+    }
     if (kind == PG_CLIFFORD) {
       for (int e = tid; e < len; e += kPgThreads) {
         u64 out;
-        if (pg_image(sm.im, sm.ckey[e], out)) sm.clam[e] = -sm.clam[e];
+        if (pg_image(sm.st.im, sm.ckey[e], out)) sm.clam[e] = -sm.clam[e];
         sm.ckey[e] = out;
       }
       __syncthreads();
+      sorted = false;
       continue;
     }
     // ---- oprun
-    if (st->order && len >= 3 && len <= kPgOrdCap) {
-      // the reference's string order: pattern word (branch count minus one of every digit), then word
+    if (st->order && len >= 3 && len <= kPgOrdCap) {   // (the small variant never reaches the cap)
+      // the reference's string order: pattern word (branch count minus one of every digit), then
+      // word -- a stable sort by pattern of terms that are in word order
+      if (!sorted) pg_sort_terms(sm, len);
       int m = 32;
       while (m < len) m <<= 1;
-      u64* pat = sm.rkey;
       for (int e = tid; e < m; e += kPgThreads) {
         u64 p = ~0ull;
         if (e < len) {
@@ -199,45 +340,58 @@ k_small_circuit(const u64* __restrict__ keys_in, const double* __restrict__ lam_
           for (u64 sup = support_mask(key); sup;) {
             const int b = __ffsll((long long)sup) - 1;
             sup &= sup - 1;
-            p |= (u64)(sm.tb.cnt[b >> 1][((key >> b) & 3ull) - 1] - 1) << b;
+            p |= (u64)(sm.st.tb.cnt[b >> 1][((key >> b) & 3ull) - 1] - 1) << b;
           }
-        } else {
-          sm.ckey[e] = ~0ull;
         }
-        pat[e] = p;
+        sm.rkey[e] = p;
+        sm.ridx[e] = (unsigned short)e;
       }
       __syncthreads();
-      for (int k = 2; k <= m; k <<= 1) {
-        for (int j = k >> 1; j > 0; j >>= 1) {
-          for (int t = tid; t < (m >> 1); t += kPgThreads) {
-            const int a = ((t & ~(j - 1)) << 1) | (t & (j - 1));
-            const int b = a | j;
-            const u64 pa = pat[a], pb = pat[b], ka = sm.ckey[a], kb = sm.ckey[b];
-            const bool greater = pa > pb || (pa == pb && ka > kb);
-            if (greater == ((a & k) == 0)) {
-              pat[a] = pb; pat[b] = pa;
-              sm.ckey[a] = kb; sm.ckey[b] = ka;
-              const double la = sm.clam[a]; sm.clam[a] = sm.clam[b]; sm.clam[b] = la;
-            }
-          }
-          __syncthreads();
-        }
+      pg_sort_pairs(sm, m);
+      pg_gather_terms(sm, len, false);
+    }
+    // qubits on which the operator branches at all; on the others every cell has one output axis.
+    // fast: all those single weights are exactly +-1 (Clifford cells), so they only flip signs
+    if (tid < 32) {
+      bool br = false, unit = true;
+      for (int a = 0; a < 3; ++a) {
+        if (sm.st.tb.cnt[tid][a] > 1) br = true;
+        else unit = unit && fabs(sm.st.tb.w[tid][a][0]) == 1.0;
+      }
+      u64 mine = br ? 1ull << (2 * tid) : 0ull;
+#pragma unroll
+      for (int d = 16; d > 0; d >>= 1) mine |= __shfl_xor_sync(QX_FULL_MASK, mine, d);
+      const u32 oks = __ballot_sync(QX_FULL_MASK, br || unit);
+      if (tid == 0) {
+        sm.bmask = mine;
+        sm.fast = oks == 0xffffffffu ? 1 : 0;
       }
     }
+    __syncthreads();
+    const u64 bmask = sm.bmask;
     // branch counts -> exclusive raw offsets (consecutive sources per thread)
+    auto branches = [&](u64 key) {
+      u32 c = 1;
+      for (u64 mk = support_mask(key) & bmask; mk;) {
+        const int bit = __ffsll((long long)mk) - 1;
+        mk &= mk - 1;
+        c *= sm.st.tb.cnt[bit >> 1][((key >> bit) & 3ull) - 1];
+      }
+      return c;
+    };
     const int per = (len + kPgThreads - 1) / kPgThreads;
     const int e0 = tid * per, e1 = min(len, e0 + per);
     u64 mine = 0;
-    for (int e = e0; e < e1; ++e) mine += branch_count(sm.ckey[e], sm.tb.cnt);
+    for (int e = e0; e < e1; ++e) mine += branches(sm.ckey[e]);
     u64 total;
     u64 run = pg_block_exclusive_sum<u64>(mine, sm.scan, total);
-    if (total > (u64)kPgRawCap) {
+    if (total > (u64)kRawCap) {
       bad = true;
       break;
     }
     for (int e = e0; e < e1; ++e) {
       sm.soff[e] = (unsigned short)run;
-      run += branch_count(sm.ckey[e], sm.tb.cnt);
+      run += branches(sm.ckey[e]);
     }
     if (tid == 0) sm.soff[len] = (unsigned short)total;
     raw_sum += total;
@@ -245,96 +399,172 @@ k_small_circuit(const u64* __restrict__ keys_in, const double* __restrict__ lam_
     const int raw = (int)total;
     int m = 32;
     while (m < raw) m <<= 1;
-    // raw terms: source by bisection of the offsets, picks by mixed-radix decode (lowest digit
-    // fastest), product and image composition qubit 0 first (stabilizer.py:311-319)
-    for (int r = tid; r < m; r += kPgThreads) {
-      u64 out = ~0ull;
-      double v = 0.0;
-      if (r < raw) {
-        int lo = 0, hi = len;                // soff[lo] <= r < soff[hi]
-        while (hi - lo > 1) {
-          const int mid = (lo + hi) >> 1;
-          if ((int)sm.soff[mid] <= r) lo = mid; else hi = mid;
-        }
-        const u64 key = sm.ckey[lo];
-        u32 b = (u32)r - (u32)sm.soff[lo];
-        u64 picks = 0;
-        for (u64 mask = support_mask(key); mask;) {
-          const int bit = __ffsll((long long)mask) - 1;
-          mask &= mask - 1;
-          const u32 c = sm.tb.cnt[bit >> 1][(u32)((key >> bit) & 3ull) - 1u];
-          const u32 q = b / c;
-          picks |= (u64)(b - q * c) << bit;
-          b = q;
-        }
-        v = sm.clam[lo];
-        out = 0;
-        u32 ex = 0;
-        for (u64 mask = support_mask(key); mask;) {
-          const int bit = 63 - __clzll((long long)mask);
-          mask ^= 1ull << bit;
+    if (sm.fast && raw <= 4 * len) {
+      // Few branches per source (near-Clifford circuits: one rotation in the operator): one thread
+      // per SOURCE.  The digits the operator does not branch on contribute a fixed image and a
+      // sign -- composed once per source, not once per raw term; factors on different qubits
+      // commute, and multiplying by +-1 is exact wherever it happens in the product, so the
+      // coefficient is bitwise lambda * w_q0 * w_q1 * ... in qubit order (stabilizer.py:311-319).
+      for (int e = tid; e < len; e += kPgThreads) {
+        const u64 key = sm.ckey[e];
+        const double lam = sm.clam[e];
+        u64 wb = 0;
+        u32 eb = 0, neg = 0;
+        for (u64 mk = support_mask(key) & ~bmask; mk;) {
+          const int bit = 63 - __clzll((long long)mk);
+          mk ^= 1ull << bit;
           const int p = bit >> 1;
-          const u32 d = (u32)((key >> bit) & 3ull) - 1u, pick = (u32)(picks >> bit) & 3u;
-          v = __dmul_rn(v, sm.tb.w[p][d][pick]);
-          const u32 ax = sm.tb.axis[p][d][pick];
-          compose<u64>(out, ex, sm.im.img[p][ax - 1], sm.im.imx[p][ax - 1], sm.im.e[p][ax - 1]);
+          const u32 d = (u32)((key >> bit) & 3ull) - 1u;
+          neg ^= sm.st.tb.w[p][d][0] < 0.0 ? 1u : 0u;
+          const u32 ax = sm.st.tb.axis[p][d][0];
+          compose<u64>(wb, eb, sm.st.im.img[p][ax - 1], sm.st.im.imx[p][ax - 1], sm.st.im.e[p][ax - 1]);
         }
-        if (composed_sign<u64>(out, ex)) v = -v;     // sign flips are exact
+        const u64 bm = support_mask(key) & bmask;
+        const u32 r0 = sm.soff[e], r1 = sm.soff[e + 1];
+        for (u32 r = r0; r < r1; ++r) {
+          u32 b = r - r0;
+          u64 picks = 0;
+          for (u64 mk = bm; mk;) {
+            const int bit = __ffsll((long long)mk) - 1;
+            mk &= mk - 1;
+            u32 q, pick;
+            divmod_small<u32>(b, sm.st.tb.cnt[bit >> 1][(u32)((key >> bit) & 3ull) - 1u], q, pick);
+            picks |= (u64)pick << bit;
+            b = q;
+          }
+          double v = lam;
+          u64 out = wb;
+          u32 ex = eb;
+          for (u64 mk = bm; mk;) {
+            const int bit = 63 - __clzll((long long)mk);
+            mk ^= 1ull << bit;
+            const int p = bit >> 1;
+            const u32 d = (u32)((key >> bit) & 3ull) - 1u, pick = (u32)(picks >> bit) & 3u;
+            v = __dmul_rn(v, sm.st.tb.w[p][d][pick]);
+            const u32 ax = sm.st.tb.axis[p][d][pick];
+            compose<u64>(out, ex, sm.st.im.img[p][ax - 1], sm.st.im.imx[p][ax - 1], sm.st.im.e[p][ax - 1]);
+          }
+          if (composed_sign<u64>(out, ex) ^ neg) v = -v;     // sign flips are exact
+          sm.rkey[r] = out;
+          sm.rlam[r] = v;
+          sm.ridx[r] = (unsigned short)r;
+        }
       }
-      sm.rkey[r] = out;
-      sm.rlam[r] = v;
-      sm.ridx[r] = (unsigned short)r;
+      for (int r = raw + tid; r < m; r += kPgThreads) {
+        sm.rkey[r] = ~0ull;
+        sm.rlam[r] = 0.0;
+        sm.ridx[r] = (unsigned short)r;
+      }
+    } else {
+      // raw terms: source by bisection of the offsets, picks by mixed-radix decode (lowest digit
+      // fastest), product and image composition qubit 0 first (stabilizer.py:311-319)
+      for (int r = tid; r < m; r += kPgThreads) {
+        u64 out = ~0ull;
+        double v = 0.0;
+        if (r < raw) {
+          int lo = 0, hi = len;                // soff[lo] <= r < soff[hi]
+          while (hi - lo > 1) {
+            const int mid = (lo + hi) >> 1;
+            if ((int)sm.soff[mid] <= r) lo = mid; else hi = mid;
+          }
+          const u64 key = sm.ckey[lo];
+          u32 b = (u32)r - (u32)sm.soff[lo];
+          u64 picks = 0;
+          for (u64 mask = support_mask(key) & bmask; mask;) {
+            const int bit = __ffsll((long long)mask) - 1;
+            mask &= mask - 1;
+            u32 q, pick;
+            divmod_small<u32>(b, sm.st.tb.cnt[bit >> 1][(u32)((key >> bit) & 3ull) - 1u], q, pick);
+            picks |= (u64)pick << bit;
+            b = q;
+          }
+          v = sm.clam[lo];
+          out = 0;
+          u32 ex = 0;
+          for (u64 mask = support_mask(key); mask;) {
+            const int bit = 63 - __clzll((long long)mask);
+            mask ^= 1ull << bit;
+            const int p = bit >> 1;
+            const u32 d = (u32)((key >> bit) & 3ull) - 1u, pick = (u32)(picks >> bit) & 3u;
+            v = __dmul_rn(v, sm.st.tb.w[p][d][pick]);
+            const u32 ax = sm.st.tb.axis[p][d][pick];
+            compose<u64>(out, ex, sm.st.im.img[p][ax - 1], sm.st.im.imx[p][ax - 1], sm.st.im.e[p][ax - 1]);
+          }
+          if (composed_sign<u64>(out, ex)) v = -v;     // sign flips are exact
+        }
+        sm.rkey[r] = out;
+        sm.rlam[r] = v;
+        sm.ridx[r] = (unsigned short)r;
+      }
     }
     __syncthreads();
     // bitonic network on (key, raw position): equal keys stay in raw order, padding ends up last
-    for (int k = 2; k <= m; k <<= 1) {
-      for (int j = k >> 1; j > 0; j >>= 1) {
-        for (int t = tid; t < (m >> 1); t += kPgThreads) {
-          const int lo = ((t & ~(j - 1)) << 1) | (t & (j - 1));
-          const int hi = lo | j;
-          const u64 ka = sm.rkey[lo], kb = sm.rkey[hi];
-          const unsigned short ia = sm.ridx[lo], ib = sm.ridx[hi];
-          const bool greater = ka > kb || (ka == kb && ia > ib);
-          if (greater == ((lo & k) == 0)) {
-            sm.rkey[lo] = kb; sm.rkey[hi] = ka;
-            sm.ridx[lo] = ib; sm.ridx[hi] = ia;
-          }
-        }
-        __syncthreads();
-      }
-    }
-    // run sums (sequential, raw order), drop rule, ordered compaction row by row into the
-    // generator's own arrays
-    const int rows = (raw + kPgThreads - 1) / kPgThreads;
-    int kept_before = 0;
+    pg_sort_pairs(sm, m);
+    // run sums (sequential, raw order), drop rule, ordered compaction into the generator's own
+    // arrays: kept flags of all rows first (one table of per-warp counts, scanned once), then the
+    // sums again for the kept heads -- duplicates are rare, two barriers instead of one per row
+    const int rows = (raw + kPgThreads - 1) / kPgThreads;      // <= kRawCap / kPgThreads = 16
+    auto run_sum = [&](int e, u64 key) {
+      double sum = sm.rlam[sm.ridx[e]];
+      for (int j = e + 1; j < raw && sm.rkey[j] == key; ++j) sum += sm.rlam[sm.ridx[j]];
+      return sum;
+    };
+    u32 kept_rows = 0;
     for (int r = 0; r < rows; ++r) {
       const int e = r * kPgThreads + tid;
       bool kept = false;
-      u64 key = 0;
-      double sum = 0.0;
       if (e < raw) {
-        key = sm.rkey[e];
-        if (e == 0 || sm.rkey[e - 1] != key) {
-          sum = sm.rlam[sm.ridx[e]];
-          for (int j = e + 1; j < raw && sm.rkey[j] == key; ++j) sum += sm.rlam[sm.ridx[j]];
-          kept = fabs(sum) >= eps;
+        const u64 key = sm.rkey[e];
+        if (e == 0 || sm.rkey[e - 1] != key) kept = fabs(run_sum(e, key)) >= eps;
+      }
+      const u32 votes = __ballot_sync(QX_FULL_MASK, kept);
+      if (lane_id() == 0) sm.kept_tab[r * kPgWarps + (tid >> 5)] = __popc(votes);
+      if (kept) kept_rows |= 1u << r;
+    }
+    __syncthreads();
+    if (tid < 32) {
+      constexpr int kEach = ((kRawCap + kPgThreads - 1) / kPgThreads * kPgWarps + 31) / 32;     // table entries per lane
+      const int n_ent = rows * kPgWarps;
+      u32 loc[kEach], sum = 0;
+#pragma unroll
+      for (int i = 0; i < kEach; ++i) {
+        const int at = tid * kEach + i;
+        loc[i] = at < n_ent ? sm.kept_tab[at] : 0u;
+        sum += loc[i];
+      }
+      u32 incl = warp_inclusive_sum(sum);
+      u32 runx = incl - sum;
+#pragma unroll
+      for (int i = 0; i < kEach; ++i) {
+        const int at = tid * kEach + i;
+        if (at < n_ent) sm.kept_tab[at] = runx;
+        runx += loc[i];
+      }
+      if (tid == 31) sm.kept_total = incl;
+    }
+    __syncthreads();
+    const int kept_before = (int)sm.kept_total;
+    for (int r = 0; r < rows; ++r) {
+      const bool kept = (kept_rows >> r) & 1u;
+      const u32 votes = __ballot_sync(QX_FULL_MASK, kept);
+      if (kept) {
+        const int e = r * kPgThreads + tid;
+        const int pos = (int)sm.kept_tab[r * kPgWarps + (tid >> 5)] + __popc(votes & lanemask_lt());
+        if (pos < kSrcCap) {
+          const u64 key = sm.rkey[e];
+          sm.ckey[pos] = key;
+          sm.clam[pos] = run_sum(e, key);
         }
       }
-      int row_total;
-      const int excl = pg_block_exclusive_sum<int>(kept ? 1 : 0, sm.scan, row_total);
-      const int pos = kept_before + excl;
-      if (kept && pos < kPgSrcCap) {
-        sm.ckey[pos] = key;
-        sm.clam[pos] = sum;
-      }
-      kept_before += row_total;
     }
+    __syncthreads();
     if (tid == 0) host.ranks[(int64_t)st->rank_row * n_seg + g] = kept_before;
-    if (kept_before > kPgSrcCap) {
+    if (kept_before > kSrcCap) {
       bad = true;
       break;
     }
     len = kept_before;
+    sorted = true;
     __syncthreads();
   }
   if (bad) len = 0;

@@ -107,6 +107,7 @@ class _Walker:
         self.timings = timings
         self.before_merge, self.reduce_ranks = before_merge, reduce_ranks
         self.eager = False             # merge after every step (eps could drop an input term)
+        self.dry = False               # replaying bookkeeping against recorded ranks: op words are not needed
         self.queue: list = []
         self.queue_has_cx = False
         self.unsorted = False          # a permutation ran since the last merge
@@ -351,9 +352,9 @@ def run(instructions: Sequence[Instruction], n: int, mode, eps: float = DEFAULT_
                 dt = time.perf_counter() - t0
                 if fitted:
                     programmed = True
-                    w.store = _ReplayStore(rows, store.device)
+                    w.store, w.dry = _ReplayStore(rows, store.device), True
                     _walk_events(w, _program_events(plan, instructions, mode), mode, trace, counters)
-                    w.store = store
+                    w.store, w.dry = store, False
                     timings["sub_flatten" if program.rows else "cx"] += dt
                     w.launch_log["program_steps"] = program.steps
                 else:
@@ -635,19 +636,26 @@ def _compile_v1(instructions, partition, n: int) -> tuple:
 def _replay_v1(compiled, w: _Walker, trace, counters):
     events, n_cx, n_1q = compiled
     w.updates = np.zeros(len(w.ids), dtype=np.int64)
+    snaps = 0                          # rows that only repeat the current ranks: appended in bulk
     for ev in events:
         kind = ev[0]
         if kind == "q":
-            w.queue.extend(ev[1])
+            if w.dry:
+                w.queue.extend(ev[1][:1])      # only whether there are ops matters to the bookkeeping
+            else:
+                w.queue.extend(ev[1])
             w.queue_has_cx = w.queue_has_cx or ev[2]
             if w.pending is None:
                 w.clean_gates += ev[3]
             else:
                 w.pending_gates += ev[3]
         elif kind == "snap":
-            w.snapshot(trace)
+            snaps += 1
         else:
             _, pos, qubit, tables, as_operator = ev
+            if snaps:
+                w.snapshots(trace, snaps)
+                snaps = 0
             w.resolve(trace)                   # this gate must see merged terms
             w.count_gate()
             w.flush()
@@ -658,6 +666,8 @@ def _replay_v1(compiled, w: _Walker, trace, counters):
                 w.store.apply_split(qubit, *tables)
             w.timings["sub_flatten"] += time.perf_counter() - t0
             w.branched(pos - 1, "sub_flatten", trace)
+    if snaps:
+        w.snapshots(trace, snaps)
     counters["cx_applications"] += n_cx
     if n_1q:
         counters["v1_gate_applications"] = counters.get("v1_gate_applications", 0) + n_1q
@@ -708,7 +718,10 @@ def _replay_operators(compiled, w: _Walker, trace, counters, mode):
     n = w.n
     for ev in events:
         if ev[0] == "q":
-            w.queue.extend(ev[1])
+            if w.dry:
+                w.queue.extend(ev[1][:1])      # only whether there are ops matters to the bookkeeping
+            else:
+                w.queue.extend(ev[1])
             w.queue_has_cx = w.queue_has_cx or ev[2]
             w.snapshots(trace, ev[3])
             continue
