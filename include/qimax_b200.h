@@ -83,6 +83,13 @@ int qx_store_device_view(qx_store* s, const uint64_t** d_keys, const double** d_
                          const int64_t** d_offsets);
 int qx_store_capacity(qx_store* s, int64_t* capacity_terms, int64_t* hbm_bytes);
 int qx_store_synchronize(qx_store* s);
+/* Phase timers on the device (the reference's RunReport.timings keys partition / lut /
+ * sub_flatten / cx, engine.py:92: the two device phases are measured with CUDA events on the
+ * store's stream instead of a host clock around asynchronous launches).  record: a new event on
+ * the stream, its index in *index.  elapsed: waits for event `second`, milliseconds between the
+ * two.  Events live as long as the store. */
+int qx_store_event_record(qx_store* s, int32_t* index);
+int qx_store_event_elapsed(qx_store* s, int32_t first, int32_t second, double* ms);
 /* Generators evolve independently (engine.py:113-116): a new store holding copies of segments
  * [seg_lo, seg_hi) of src (device-to-device), launching on a non-blocking stream of its own so
  * that its kernels and copies overlap those of other stores.  src is left untouched. */
@@ -265,12 +272,14 @@ int qx_program_rows(const qx_program* p, int32_t* rows);
  * stabilizer.py:169-174; if the program then does not fit, the store is left as qx_store_init_z
  * leaves it).  host_keys / host_lambdas != NULL (PAGE-LOCKED memory from qx_host_alloc, room for
  * host_cap terms): the kernel also writes the result there, store layout; *host_filled = 1 if all
- * of it fit.  One launch and one stream synchronize: ranks, offsets and the host copy of the
- * result are written by the kernel itself into page-locked memory. */
+ * of it fit.  device_ms (may be NULL): duration of the launch on the GPU's own clock (first CTA in
+ * to last CTA out, %globaltimer) -- the device phase timer of the run at no cost.  One launch and
+ * one stream synchronize: ranks, offsets and the host copy of the result are written by the
+ * kernel itself into page-locked memory. */
 int qx_store_run_program(qx_store* s, const qx_program* p, const int32_t* init_qubits, double eps,
                          int64_t* ranks, int64_t* raw_total, int32_t* fitted, int64_t* offsets,
                          uint64_t* host_keys, double* host_lambdas, int64_t host_cap,
-                         int32_t* host_filled);
+                         int32_t* host_filled, double* device_ms);
 
 /* ---- a6: duplicate-term merge (canonicalize, stabilizer.py:325-337).
  * Per segment: stable sort by key, in-order segmented sum, keep |sum| >= eps,

@@ -869,7 +869,7 @@ k_small_operator(const u64* __restrict__ keys_in, const double* __restrict__ lam
   __shared__ ImageTable<u64> s_im;
   __shared__ u64 s_scan[kSoWarps + 1];
   __shared__ u64 s_base;
-  const int g = (int)blockIdx.x;           // in-order dispatch, see take_ticket
+  const int g = qx_tile_id(reinterpret_cast<u32*>(error) + 1);   // in-order dispatch, see qx_device.cuh (error[1]: a zeroed spare word)
   const int tid = threadIdx.x;
   {
     const u32* src = reinterpret_cast<const u32*>(&tb);
@@ -1163,7 +1163,7 @@ extern "C" int qx_program_rows(const qx_program* p, int32_t* rows) {
 extern "C" int qx_store_run_program(qx_store* s, const qx_program* p, const int32_t* init_qubits, double eps,
                                     int64_t* ranks, int64_t* raw_total, int32_t* fitted, int64_t* offsets,
                                     uint64_t* host_keys, double* host_lambdas, int64_t host_cap,
-                                    int32_t* host_filled) {
+                                    int32_t* host_filled, double* device_ms) {
   QX_REQUIRE(s && p && fitted, "NULL argument");
   QX_NARROW_ONLY(s, "qx_store_run_program");
   QX_REQUIRE(p->n_qubits == s->n_qubits && p->device == s->device, "program was compiled for n=%d on device %d",
@@ -1198,7 +1198,7 @@ extern "C" int qx_store_run_program(qx_store* s, const qx_program* p, const int3
   u64* status = reinterpret_cast<u64*>(s->scratch);
   // what the kernel reports, in page-locked host memory
   const int64_t rank_words = (int64_t)p->n_rows * s->n_seg;
-  const int64_t need = 3 * (int64_t)s->n_seg + 1 + rank_words;
+  const int64_t need = 5 * (int64_t)s->n_seg + 1 + rank_words;
   int64_t* h = s->h_pinned;
   void* h_big = nullptr;
   if (need > s->h_pinned_words) {
@@ -1213,7 +1213,8 @@ extern "C" int qx_store_run_program(qx_store* s, const qx_program* p, const int3
   host.flags = h;
   host.raw = h + s->n_seg;
   host.seg = h + 2 * s->n_seg;
-  host.ranks = h + 3 * s->n_seg + 1;
+  host.clock = h + 3 * s->n_seg + 1;
+  host.ranks = h + 5 * s->n_seg + 1;
   host.keys = reinterpret_cast<u64*>(host_keys);
   host.lam = host_lambdas;
   host.cap = host_keys ? host_cap : 0;
@@ -1263,6 +1264,15 @@ extern "C" int qx_store_run_program(qx_store* s, const qx_program* p, const int3
   for (int64_t i = 0; i < rank_words; ++i) ranks[i] = host.ranks[i];
   if (raw_total) *raw_total = raw;
   if (host_filled) *host_filled = (host_keys && !(flags & 2)) ? 1 : 0;
+  if (device_ms) {
+    // first CTA in to last CTA out, on the GPU's own nanosecond clock
+    int64_t first = host.clock[0], last = host.clock[s->n_seg];
+    for (int g = 1; g < s->n_seg; ++g) {
+      first = std::min(first, host.clock[g]);
+      last = std::max(last, host.clock[s->n_seg + g]);
+    }
+    *device_ms = (double)(last - first) * 1e-6;
+  }
   s->cur = out;
   s->exact = true;
   s->narrow_keys = false;

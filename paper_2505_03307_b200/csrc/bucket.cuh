@@ -151,10 +151,10 @@ k_tile_desc(const BGroup<K>* __restrict__ groups, int ng, u64 n_tiles, const u64
 __global__ void __launch_bounds__(256)
 k_unit_scan(const u64* __restrict__ sort_key, const double* __restrict__ sort_val, u64 n_tiles, int top_bits,
             u32* __restrict__ unit_tile0, u32* __restrict__ seg_first, u64* __restrict__ status,
-            u64* __restrict__ info) {
+            u64* __restrict__ info, u32* __restrict__ ticket) {
   __shared__ u64 s_scan[kBWarps + 1];
   __shared__ u64 s_base;
-  const int tile = (int)blockIdx.x;
+  const int tile = qx_tile_id(ticket);
   constexpr int kPer = 8;
   const int warp = threadIdx.x >> 5, lane = lane_id();
   const u64 wbase = (u64)tile * (256 * kPer) + (u64)warp * (32 * kPer);
@@ -988,7 +988,7 @@ int bucket_step(qx_store* s, const OperatorTable& ct, const ImageTable<K>& im, i
                                                                           n_tiles, d_fat);
     QX_CUDA(cudaGetLastError());
     k_unit_scan<<<(unsigned)scan_tiles, 256, 0, s->stream>>>(skeys[sorted], svals[sorted], n_tiles, top_bits,
-                                                            unit_tile0, seg_first, scan_status, info);
+                                                            unit_tile0, seg_first, scan_status, info, ticket + 1);
     QX_CUDA(cudaGetLastError());
     k_unit_sizes<<<(unsigned)std::max<int64_t>(1, std::min<int64_t>(((int64_t)n_tiles + 255) / 256, 1024)), 256, 0, s->stream>>>(
         unit_tile0, skeys[sorted], svals[sorted], reinterpret_cast<uint4*>(d_units), info);

@@ -253,7 +253,7 @@ k_onesweep(const K* __restrict__ keys_in, const V* __restrict__ vals_in,
   // atomic, no dependent offset-table load: the record holds the absolute start.
   for (int i = tid; i < WARPS * QX_RADIX / 4; i += THREADS)
     reinterpret_cast<uint4*>(&sm.whist[0][0])[i] = make_uint4(0u, 0u, 0u, 0u);
-  const int64_t tile = blockIdx.x;
+  const int64_t tile = qx_tile_id(status + (size_t)gridDim.x * QX_RADIX);   // the word behind the tiles' status words
   const int64_t total_tiles = *n_tiles;
   if (tile >= total_tiles) return;
   const TileInfo ti = info[tile];
@@ -458,7 +458,7 @@ k_reduce(const K* __restrict__ keys_in, const V* __restrict__ vals_in,
   ReduceSmem<K, V, kRedThreads, kRedItems>& sm =
       *reinterpret_cast<ReduceSmem<K, V, kRedThreads, kRedItems>*>(smem_raw);
   if (threadIdx.x < kRedTile / 32) sm.opens[threadIdx.x] = 0u;
-  const int tile = (int)blockIdx.x;                 // in-order dispatch, see take_ticket
+  const int tile = qx_tile_id(ticket);              // in-order dispatch, see qx_device.cuh
   const int64_t total = seg_in[n_seg];
   const int64_t ntiles = total > 0 ? (total + kRedTile - 1) / kRedTile : 1;
   if (tile >= ntiles) return;
@@ -575,7 +575,7 @@ k_small_merge(const u64* __restrict__ keys_in, const V* __restrict__ vals_in,
   __shared__ int s_g;
   __shared__ u64 s_scan[kSmallWarps + 1];
   __shared__ u64 s_base;
-  const int g = (int)blockIdx.x;         // in-order dispatch, see take_ticket
+  const int g = qx_tile_id(ticket);      // in-order dispatch, see qx_device.cuh
   if (g >= n_seg) return;
   const int64_t start = seg_in[g];
   int len = (int)min((int64_t)0x7fffffff, seg_in[g + 1] - start);
@@ -801,9 +801,11 @@ int dispatch_pass(int variant, QxArena* ar, MergeBuffers<V>& mb, int cur, int64_
   using KO = typename std::conditional<WIDEN, u64, K>::type;
   if (sizeof(V) > 8)
     return launch_pass<K, V, 256, 12, 8>(ar, mb, cur, tiles_ub, info, n_tiles, digit_base, base_stride, which, base_in);
-  if (sizeof(K) == 4) {
+  if constexpr (sizeof(K) == 4) {
     // narrow keys: 56 registers and 68 KB of shared memory per CTA -> three CTAs (36 warps) per SM
-    // instead of two; the pass is latency-bound, not HBM-bound (profiles/r01g), so occupancy pays
+    // instead of two; the pass is latency-bound, not HBM-bound (profiles/r01g), so occupancy pays.
+    // (if constexpr: these occupancies are never instantiated for 64-bit keys, where 56 registers
+    // would spill -- the 64-bit variants below run two CTAs per SM at 85 registers, no stack)
     switch (variant) {
       case 2: return launch_pass<K, V, 256, 12, 8, 4, KO>(ar, mb, cur, tiles_ub, info, n_tiles, digit_base, base_stride, which, base_in);
       case 3: return launch_pass<K, V, 256, 16, 8, 3, KO>(ar, mb, cur, tiles_ub, info, n_tiles, digit_base, base_stride, which, base_in);
@@ -812,14 +814,15 @@ int dispatch_pass(int variant, QxArena* ar, MergeBuffers<V>& mb, int cur, int64_
       case 6: return launch_pass<K, V, 384, 10, 8, 3, KO>(ar, mb, cur, tiles_ub, info, n_tiles, digit_base, base_stride, which, base_in);
       default: return launch_pass<K, V, 384, 12, 8, 3, KO>(ar, mb, cur, tiles_ub, info, n_tiles, digit_base, base_stride, which, base_in);
     }
-  }
-  switch (variant) {
-    case 2: return launch_pass<K, V, 256, 12, 8>(ar, mb, cur, tiles_ub, info, n_tiles, digit_base, base_stride, which, base_in);
-    case 3: return launch_pass<K, V, 256, 16, 8>(ar, mb, cur, tiles_ub, info, n_tiles, digit_base, base_stride, which, base_in);
-    case 4: return launch_pass<K, V, 512, 8, 8>(ar, mb, cur, tiles_ub, info, n_tiles, digit_base, base_stride, which, base_in);
-    case 5: return launch_pass<K, V, 384, 8, 8, 3>(ar, mb, cur, tiles_ub, info, n_tiles, digit_base, base_stride, which, base_in);
-    case 6: return launch_pass<K, V, 384, 10, 8>(ar, mb, cur, tiles_ub, info, n_tiles, digit_base, base_stride, which, base_in);
-    default: return launch_pass<K, V, 384, 12, 8>(ar, mb, cur, tiles_ub, info, n_tiles, digit_base, base_stride, which, base_in);
+  } else {
+    switch (variant) {
+      case 2: return launch_pass<K, V, 256, 12, 8>(ar, mb, cur, tiles_ub, info, n_tiles, digit_base, base_stride, which, base_in);
+      case 3: return launch_pass<K, V, 256, 16, 8>(ar, mb, cur, tiles_ub, info, n_tiles, digit_base, base_stride, which, base_in);
+      case 4: return launch_pass<K, V, 512, 8, 8>(ar, mb, cur, tiles_ub, info, n_tiles, digit_base, base_stride, which, base_in);
+      case 5: return launch_pass<K, V, 384, 8, 8, 2>(ar, mb, cur, tiles_ub, info, n_tiles, digit_base, base_stride, which, base_in);
+      case 6: return launch_pass<K, V, 384, 10, 8>(ar, mb, cur, tiles_ub, info, n_tiles, digit_base, base_stride, which, base_in);
+      default: return launch_pass<K, V, 384, 12, 8>(ar, mb, cur, tiles_ub, info, n_tiles, digit_base, base_stride, which, base_in);
+    }
   }
 }
 
@@ -857,7 +860,7 @@ int merge_large(QxArena* ar, MergeBuffers<V>& mb, double eps, int cls_reduce, bo
   const int64_t zero_bytes = off_info;                       // the tile records are written, not cleared
   const int64_t total_bytes = off_info + (int64_t)sizeof(TileInfo) * tiles_ub;
   QX_TRY(qx_arena_scratch(ar, total_bytes));
-  QX_TRY(qx_arena_status(ar, tiles_ub * QX_RADIX));
+  QX_TRY(qx_arena_status(ar, tiles_ub * QX_RADIX + 1));      // + the ticket word of QX_TICKETED_LOOKBACK builds
   char* base = reinterpret_cast<char*>(ar->scratch);
   u32* ticket = reinterpret_cast<u32*>(base);
   int64_t* tile_prefix = reinterpret_cast<int64_t*>(base + off_prefix);
@@ -893,7 +896,7 @@ int merge_large(QxArena* ar, MergeBuffers<V>& mb, double eps, int cls_reduce, bo
   QX_CUDA(cudaMemcpyAsync(mb.seg[cur ^ 1], mb.seg[cur], sizeof(int64_t) * (size_t)(n_seg + 1),
                           cudaMemcpyDeviceToDevice, ar->stream));
   for (int p = 0; p < passes; ++p) {
-    QX_CUDA(cudaMemsetAsync(ar->status, 0, sizeof(u32) * (size_t)(tiles_ub * QX_RADIX), ar->stream));
+    QX_CUDA(cudaMemsetAsync(ar->status, 0, sizeof(u32) * (size_t)(tiles_ub * QX_RADIX + 1), ar->stream));
     QxProfileScope prof(cls_pass, ar->stream, 2.0 * (sizeof(K) + sizeof(V)) * (double)mb.ub_total);
     if (!do_reduce && sizeof(K) == 4 && p == passes - 1 && pack_bnd) {
       // packed download: 16-bit keys + bucket table (see k_onesweep's write-out)

@@ -242,6 +242,7 @@ struct PgHost {
   int64_t* raw;                // [n_seg] raw branches of the generator's branching steps
   int64_t* seg;                // [n_seg + 1] offsets of the result
   int64_t* ranks;              // [rows][n_seg]
+  int64_t* clock;              // [2][n_seg] %globaltimer at the start and the end of the generator's CTA
   u64* keys;                   // result terms (may be NULL): same layout as the store's
   double* lam;
   int64_t cap;
@@ -256,8 +257,10 @@ k_small_circuit(const u64* __restrict__ keys_in, const double* __restrict__ lam_
   extern __shared__ __align__(16) unsigned char pg_raw[];
   SM& sm = *reinterpret_cast<SM*>(pg_raw);
   constexpr int kSrcCap = SM::kSrcCap, kRawCap = SM::kRawCap;
-  const int g = (int)blockIdx.x;             // in-order dispatch (look-back at the very end only)
+  const int g = qx_tile_id(reinterpret_cast<u32*>(status + n_seg));   // in-order dispatch, see qx_device.cuh (status[n_seg]: a zeroed spare word)
   const int tid = threadIdx.x;
+  long long t_start = 0;
+  if (tid == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_start));
   int len;
   bool bad = false;
   bool sorted = init.on != 0;                // the terms are in word order (a single Z word is)
@@ -595,5 +598,9 @@ k_small_circuit(const u64* __restrict__ keys_in, const double* __restrict__ lam_
     }
     host.flags[g] = (bad ? 1 : 0) | (to_host ? 0 : 2);
     host.raw[g] = (int64_t)raw_sum;
+    long long t_end;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_end));
+    host.clock[g] = t_start;
+    host.clock[n_seg + g] = t_end;
   }
 }

@@ -157,10 +157,26 @@ __device__ __forceinline__ bool zi_only(u64 key) {
 // Tile id of a look-back kernel: blockIdx.x.  CTAs of a 1-D grid are dispatched in index order,
 // so every predecessor a tile may wait for is resident or finished (the assumption
 // cub::DeviceScan makes); an atomic ticket per CTA cost a ~700-cycle round trip at the head of
-// every tile.  The barrier is kept: callers publish shared state before it.
-__device__ __forceinline__ int take_ticket(u32*, int*) {
+// every tile.  That order is observed hardware behaviour, not a documented guarantee: building
+// with -DQX_TICKETED_LOOKBACK hands the ids out by an atomic counter instead (every launch site
+// zeroes one), which is correct under ANY dispatch order; the GPU suite is run once with that
+// build (profiles/r02_ticketed_lookback.txt).
+__device__ __forceinline__ int qx_tile_id(u32* ticket) {
+#ifdef QX_TICKETED_LOOKBACK
+  __shared__ int s_ticketed_tile;
+  if (threadIdx.x == 0) s_ticketed_tile = (int)atomicAdd(ticket, 1u);
   __syncthreads();
+  return s_ticketed_tile;
+#else
+  (void)ticket;
   return (int)blockIdx.x;
+#endif
+}
+// The barrier is kept: callers publish shared state before it.
+__device__ __forceinline__ int take_ticket(u32* ticket, int*) {
+  const int tile = qx_tile_id(ticket);
+  __syncthreads();
+  return tile;
 }
 
 // L2 prefetch of `count` elements starting at p (whole 128-byte lines, all threads of the CTA)

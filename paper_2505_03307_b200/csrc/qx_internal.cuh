@@ -124,6 +124,7 @@ struct qx_store : QxArena {
   bool exact = false;           // h_seg matches the device
   int64_t ub_total = 0;         // host upper bound on the live term count
   int64_t ub_seg = 0;           // host upper bound on the largest live segment
+  std::vector<cudaEvent_t>* events = nullptr;   // phase timers of the caller (qx_store_event_record)
 };
 
 int qx_store_reserve(qx_store* s, int64_t terms, bool keep_live);

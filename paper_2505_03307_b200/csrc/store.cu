@@ -389,6 +389,31 @@ extern "C" int qx_store_create(int device, int n_qubits, int n_segments, int64_t
 
 namespace {
 void join_workers(qx_store* s);      // host threads of a narrow download (below)
+
+// CUDA events of the phase timers are kept per device across stores: creating one costs more than
+// recording it, and a store lives for one circuit run
+constexpr int kEventDevices = 64;
+std::mutex g_event_mu;
+std::vector<cudaEvent_t> g_timer_events[kEventDevices];
+bool event_pool_take(int device, cudaEvent_t* e) {
+  if (device < 0 || device >= kEventDevices) return false;
+  std::lock_guard<std::mutex> lock(g_event_mu);
+  if (g_timer_events[device].empty()) return false;
+  *e = g_timer_events[device].back();
+  g_timer_events[device].pop_back();
+  return true;
+}
+void event_pool_put(int device, const std::vector<cudaEvent_t>& events) {
+  if (device < 0 || device >= kEventDevices) {
+    for (cudaEvent_t e : events) cudaEventDestroy(e);
+    return;
+  }
+  std::lock_guard<std::mutex> lock(g_event_mu);
+  for (cudaEvent_t e : events) {
+    if (g_timer_events[device].size() < 4096) g_timer_events[device].push_back(e);
+    else cudaEventDestroy(e);
+  }
+}
 }
 
 extern "C" int qx_store_destroy(qx_store* s) {
@@ -404,6 +429,10 @@ extern "C" int qx_store_destroy(qx_store* s) {
   }
   qx_pinned_free(s->h_seg);
   qx_arena_release(s);
+  if (s->events) {
+    event_pool_put(s->device, *s->events);
+    delete s->events;
+  }
   if (s->own_stream) {
     // blocks handed back above carry this stream as their last user: forget it before it dies
     qx_dev_forget_stream(s->stream);
@@ -925,6 +954,32 @@ extern "C" int qx_store_download_packed_async(qx_store* s, int64_t* offsets, uin
       }
     });
   s->host_workers = hw;
+  return QX_OK;
+}
+
+// ---- phase timers (the reference's four timing keys, measured on the device) ----
+extern "C" int qx_store_event_record(qx_store* s, int32_t* index) {
+  QX_REQUIRE(s && index, "NULL argument");
+  QX_CUDA(cudaSetDevice(s->device));
+  if (!s->events) s->events = new std::vector<cudaEvent_t>();
+  cudaEvent_t e;
+  if (!event_pool_take(s->device, &e)) QX_CUDA(cudaEventCreate(&e));
+  s->events->push_back(e);
+  QX_CUDA(cudaEventRecord(e, s->stream));
+  *index = (int32_t)s->events->size() - 1;
+  return QX_OK;
+}
+
+extern "C" int qx_store_event_elapsed(qx_store* s, int32_t first, int32_t second, double* ms) {
+  QX_REQUIRE(s && ms, "NULL argument");
+  const int32_t n = s->events ? (int32_t)s->events->size() : 0;
+  QX_REQUIRE(first >= 0 && first < n && second >= 0 && second < n, "event index out of range (%d, %d of %d)", first,
+             second, n);
+  QX_CUDA(cudaSetDevice(s->device));
+  QX_CUDA(cudaEventSynchronize((*s->events)[second]));
+  float f = 0.f;
+  QX_CUDA(cudaEventElapsedTime(&f, (*s->events)[first], (*s->events)[second]));
+  *ms = (double)f;
   return QX_OK;
 }
 

@@ -260,7 +260,7 @@ k_wide_reduce(Planes in, const double* __restrict__ lam_in, const double* __rest
               int64_t* __restrict__ seg_out, u64* status, double eps) {
   __shared__ u64 s_scan[kWrThreads / 32 + 1];
   __shared__ u64 s_base;
-  const int tile = blockIdx.x;
+  const int tile = qx_tile_id(reinterpret_cast<u32*>(status + gridDim.x));   // see qx_device.cuh
   const int64_t total = seg_in[n_seg];
   const int64_t tbase = (int64_t)tile * kWrTile;
   bool kept[kWrRows], opens[kWrRows];
@@ -338,7 +338,7 @@ int wide_merge_large(qx_store* s, double eps) {
   const int64_t seg_words = ((int64_t)s->n_seg + 1 + 31) & ~31ll;
   DevBlock blk;
   blk.st = s->stream;
-  QX_TRY(qx_dev_alloc(&blk.p, 8 * (4 * n_al + seg_words + tiles), s->stream, s->device));
+  QX_TRY(qx_dev_alloc(&blk.p, 8 * (4 * n_al + seg_words + tiles + 1), s->stream, s->device));   // + the ticket word of QX_TICKETED_LOOKBACK builds
   u64* kbuf[2] = {reinterpret_cast<u64*>(blk.p), reinterpret_cast<u64*>(blk.p) + n_al};
   double* pbuf[2] = {reinterpret_cast<double*>(kbuf[1] + n_al), reinterpret_cast<double*>(kbuf[1] + 2 * n_al)};
   int64_t* seg_spare = reinterpret_cast<int64_t*>(kbuf[1] + 3 * n_al);
@@ -356,7 +356,7 @@ int wide_merge_large(qx_store* s, double eps) {
     const int bits = std::min(64, 2 * s->n_qubits - 64 * w);
     QX_TRY(qx_sort_pairs(s, kbuf, pbuf, segs, &cur, total, largest, bits));
   }
-  QX_CUDA(cudaMemsetAsync(status, 0, sizeof(u64) * (size_t)tiles, s->stream));
+  QX_CUDA(cudaMemsetAsync(status, 0, sizeof(u64) * (size_t)(tiles + 1), s->stream));
   {
     QxProfileScope prof(QX_K_REDUCE, s->stream, (8.0 * s->n_words + 8.0) * 2.0 * (double)total);
     k_wide_reduce<<<(unsigned)tiles, kWrThreads, 0, s->stream>>>(pin, s->lam[in], pbuf[cur], segs[cur], s->n_seg,

@@ -89,6 +89,35 @@ class AgreementReport:
     max_lambda_deviation: float
 
 
+_DEVICE_TIMERS = bool(__import__("os").environ.get("QX_DEVICE_TIMERS"))
+
+
+class _Phase:
+    """``with walker.phase(name):`` -- see _Walker.phase."""
+
+    __slots__ = ("w", "name", "store", "first", "t0")
+
+    def __init__(self, w, name):
+        self.w, self.name = w, name
+
+    def __enter__(self):
+        store = self.w.store
+        self.store = store if self.w.device_timers and getattr(store, "mark", None) is not None else None
+        self.t0 = time.perf_counter()
+        self.first = self.store.mark() if self.store is not None else -1
+        return self
+
+    def __exit__(self, exc_type, exc, tb):
+        w = self.w
+        dt = time.perf_counter() - self.t0
+        w.host_timings[self.name] = w.host_timings.get(self.name, 0.0) + dt
+        if self.store is None:
+            w.timings[self.name] += dt
+        elif exc_type is None:
+            w.regions.append((self.name, self.store, self.first, self.store.mark()))
+        return False
+
+
 class _Walker:
     """Schedules the device work of one run.
 
@@ -121,6 +150,27 @@ class _Walker:
         self.updates = None            # v1 only: term-gate updates per generator
         self.partition_rows = []       # slot-partitioned finish: trace rows that hold this share's counts
         self.partition_step = None
+        self.device_timers = _DEVICE_TIMERS
+        self.regions = []              # (phase, store, first event, second event): resolved by collect_timings
+        self.host_timings = {"sub_flatten": 0.0, "cx": 0.0}
+
+    # -- timers --------------------------------------------------------------------
+    def phase(self, name: str):
+        """Times a device phase for RunReport.timings (reference engine.py:92).  One-launch runs
+        report the kernel's own clock.  Step-by-step runs: with ``device_timers`` (run(...,
+        device_timers=True) or QX_DEVICE_TIMERS=1) CUDA events on the store's stream around the
+        calls, resolved once at the end of the run -- the launches are asynchronous, a host clock
+        around them measures the submission; the default is that host clock (every merge ends in a
+        read-back, so it differs only for Clifford runs), because two event records per phase cost
+        more than the phases of the small configs (C1: 0.10 -> 0.13 ms).  The host clock is kept
+        beside either in ``report.device['host_timings']``."""
+        return _Phase(self, name)
+
+    def collect_timings(self):
+        """Device phases in seconds, from the recorded event pairs (waits for the last event)."""
+        for name, store, a, b in self.regions:
+            self.timings[name] += store.elapsed_ms(a, b) * 1e-3
+        self.regions = []
 
     # -- queue ---------------------------------------------------------------------
     def push_perm(self, qubit: int, table: int):
@@ -134,9 +184,8 @@ class _Walker:
     def flush(self):
         if not self.queue:
             return
-        t0 = time.perf_counter()
-        self.store.apply_clifford(np.array(self.queue, dtype=_lut.op_dtype(self.n)))
-        self.timings["cx" if self.queue_has_cx else "sub_flatten"] += time.perf_counter() - t0
+        with self.phase("cx" if self.queue_has_cx else "sub_flatten"):
+            self.store.apply_clifford(np.array(self.queue, dtype=_lut.op_dtype(self.n)))
         self.queue, self.queue_has_cx = [], False
         self.unsorted = True
         self.launch_log["clifford_runs"] += 1
@@ -152,13 +201,12 @@ class _Walker:
 
     def _merge_now(self, step: int, phase: str, after_branch: bool):
         self.book_gates()
-        t0 = time.perf_counter()
-        if after_branch and self.before_merge is not None:
-            self.before_merge(self.store)      # term-partitioned runs: equal keys must meet first
-        self.ranks = self.store.merge(self.eps)
-        if self.reduce_ranks is not None:
-            self.ranks = self.reduce_ranks(self.ranks)
-        self.timings[phase] += time.perf_counter() - t0
+        with self.phase(phase):
+            if after_branch and self.before_merge is not None:
+                self.before_merge(self.store)      # term-partitioned runs: equal keys must meet first
+            self.ranks = self.store.merge(self.eps)
+            if self.reduce_ranks is not None:
+                self.ranks = self.reduce_ranks(self.ranks)
         self.unsorted = False
         self.launch_log["merges"] += 1
         for local, r in enumerate(self.ranks):
@@ -178,18 +226,17 @@ class _Walker:
         self.staged = None
         program = np.array(self.queue, dtype=np.uint32)
         self.queue, self.queue_has_cx = [], False
-        t0 = time.perf_counter()
-        if self.before_merge is not None:
-            # term-partitioned runs re-home terms between the expansion and the merge
-            self.store.apply_operator(counts, axes, weights)
-            self.store.apply_clifford(program)
-            self.before_merge(self.store)
-            self.ranks = self.store.merge(self.eps)
-        else:
-            _, self.ranks = self.store.apply_operator_run(counts, axes, weights, program, self.eps)
-        if self.reduce_ranks is not None:
-            self.ranks = self.reduce_ranks(self.ranks)
-        self.timings[phase] += time.perf_counter() - t0
+        with self.phase(phase):
+            if self.before_merge is not None:
+                # term-partitioned runs re-home terms between the expansion and the merge
+                self.store.apply_operator(counts, axes, weights)
+                self.store.apply_clifford(program)
+                self.before_merge(self.store)
+                self.ranks = self.store.merge(self.eps)
+            else:
+                _, self.ranks = self.store.apply_operator_run(counts, axes, weights, program, self.eps)
+            if self.reduce_ranks is not None:
+                self.ranks = self.reduce_ranks(self.ranks)
         self.unsorted = False
         self.launch_log["merges"] += 1
         if len(program):
@@ -262,9 +309,8 @@ class _Walker:
         self.flush()
         if self.unsorted:
             # only permutations since the last merge: canonicalize can only re-sort
-            t0 = time.perf_counter()
-            self.store.sort()
-            self.timings["cx"] += time.perf_counter() - t0
+            with self.phase("cx"):
+                self.store.sort()
             self.unsorted = False
             self.launch_log["sorts"] += 1
 
@@ -272,7 +318,7 @@ class _Walker:
 def run(instructions: Sequence[Instruction], n: int, mode, eps: float = DEFAULT_EPS, *,
         device=None, generators=None, capacity: int = 0, pinned: bool = False,
         download: bool = True, initial=None, before_merge=None, reduce_ranks=None,
-        slot_part=None, slot_reduce=None) -> RunReport:
+        slot_part=None, slot_reduce=None, device_timers=None) -> RunReport:
     """Simulate a circuit; returns the canonical final generator set.
 
     Positional arguments and result are the reference's (engine.py:89).  Keyword
@@ -287,7 +333,8 @@ def run(instructions: Sequence[Instruction], n: int, mode, eps: float = DEFAULT_
     follows a branching step, and turn local ranks into global ones), ``slot_part=(part,
     parts)`` / ``slot_reduce(ranks)`` (slot-partitioned multi-GPU mode, dist.run_slot_partitioned:
     the last branching operator only produces this part's share of every generator;
-    ``report.device['partitioned']`` says whether it did).
+    ``report.device['partitioned']`` says whether it did), ``device_timers`` (time the device
+    phases of ``timings`` with CUDA events instead of the host clock, see _Walker.phase).
     """
     mode = Mode.coerce(mode)
     timings = {"partition": 0.0, "lut": 0.0, "sub_flatten": 0.0, "cx": 0.0}
@@ -320,6 +367,8 @@ def run(instructions: Sequence[Instruction], n: int, mode, eps: float = DEFAULT_
             walker_ranks = [1] * len(ids)
             min_abs = 1.0
         w = _Walker(store, n, ids, eps, timings, before_merge, reduce_ranks)
+        if device_timers is not None:
+            w.device_timers = bool(device_timers)
         w.ranks = reduce_ranks(walker_ranks) if reduce_ranks is not None else walker_ranks
         # If eps could already drop an initial term, merge after every step like the
         # reference does; otherwise deferring the re-sort of permutation steps is exact.
@@ -343,19 +392,20 @@ def run(instructions: Sequence[Instruction], n: int, mode, eps: float = DEFAULT_
             program = _program_for(plan, instructions, n, mode, store.device)
             timings["lut"] = time.perf_counter() - t0
             if program is not None:
-                t0 = time.perf_counter()
                 # generators that start as Z words are made in the kernel (no upload); a run that
                 # does not fit leaves the store as init_z would have
+                t0 = time.perf_counter()
                 fitted, rows, _, program_segs = store.run_program(
                     program, eps, init_qubits=None if made else ids, to_host=download, pinned=pinned)
                 made = True
-                dt = time.perf_counter() - t0
+                phase_key = "sub_flatten" if program.rows else "cx"
+                w.host_timings[phase_key] += time.perf_counter() - t0
                 if fitted:
+                    timings[phase_key] += store.program_ms * 1e-3      # the kernel's own clock (%globaltimer)
                     programmed = True
                     w.store, w.dry = _ReplayStore(rows, store.device), True
                     _walk_events(w, _program_events(plan, instructions, mode), mode, trace, counters)
                     w.store, w.dry = store, False
-                    timings["sub_flatten" if program.rows else "cx"] += dt
                     w.launch_log["program_steps"] = program.steps
                 else:
                     plan._programs[(mode, store.device)] = None      # a generator outgrew it: step by step from now on
@@ -390,7 +440,8 @@ def run(instructions: Sequence[Instruction], n: int, mode, eps: float = DEFAULT_
             w.finish(trace)              # deferred merge, queued permutations, canonical order
         counters["operators"] = partition.k + partition.k_prime
 
-        info = {"device": store.device, **w.launch_log}
+        w.collect_timings()              # device phases: CUDA events (host clock beside them in info)
+        info = {"device": store.device, **w.launch_log, "host_timings": dict(w.host_timings)}
         if partitioned is not None:
             info["partitioned"] = partitioned
             if w.partition_step is not None:
@@ -479,6 +530,8 @@ PROGRAM_MAX_TERMS = 4096          # terms per generator the one-launch path hold
 class _RecordingStore:
     """Stands in for a DeviceStore while a plan is compiled: records the device steps."""
 
+    mark = None                       # no stream: phases are not timed
+
     def __init__(self, n: int, n_gen: int):
         self.n, self.n_gen = n, n_gen
         self.steps, self.order_next = [], False
@@ -506,6 +559,8 @@ class _RecordingStore:
 
 class _ReplayStore:
     """Stands in for the store after the program ran: hands the recorded ranks to the walker."""
+
+    mark = None
 
     def __init__(self, rows, device):
         self.rows, self.next, self.device = rows, 0, device
@@ -659,12 +714,11 @@ def _replay_v1(compiled, w: _Walker, trace, counters):
             w.resolve(trace)                   # this gate must see merged terms
             w.count_gate()
             w.flush()
-            t0 = time.perf_counter()
             if as_operator is not None and w.before_merge is None and 2 * max(w.ranks, default=0) <= SMALL_RAW:
                 w.stage_operator(*as_operator)     # split + the run behind it + merge: one launch
             else:
-                w.store.apply_split(qubit, *tables)
-            w.timings["sub_flatten"] += time.perf_counter() - t0
+                with w.phase("sub_flatten"):
+                    w.store.apply_split(qubit, *tables)
             w.branched(pos - 1, "sub_flatten", trace)
     if snaps:
         w.snapshots(trace, snaps)
@@ -728,7 +782,7 @@ def _replay_operators(compiled, w: _Walker, trace, counters, mode):
         _, step, counts, axes, weights = ev
         w.resolve(trace)               # expand merged terms only
         w.flush()
-        t0 = time.perf_counter()
+        ph = w.phase("sub_flatten").__enter__()
         if mode is Mode.V2 and 4 ** n > DENSE_FLATTEN_BUDGET:
             # dense layout: a branching substitution needs a 4**n scatter buffer
             # (reference stabilizer.py:264-276); one-hot rows take the fast path
@@ -760,7 +814,7 @@ def _replay_operators(compiled, w: _Walker, trace, counters, mode):
             pad_dense(w.store, n, dense_gens)
         else:
             w.stage_operator(counts, axes, weights)
-        w.timings["sub_flatten"] += time.perf_counter() - t0
+        ph.__exit__(None, None, None)
         w.branched(step, "sub_flatten", trace)
     counters["sub_flatten_ops"] += n_u
     counters["cx_applications"] += n_cx
@@ -802,6 +856,7 @@ def _finish_streamed(w: _Walker, trace, pinned: bool):
     program = np.array(w.queue, dtype=np.uint32)
     w.queue, w.queue_has_cx, w.staged, w.pending = [], False, None, None
     w.book_gates()
+    ph = w.phase(phase).__enter__()
     t0 = time.perf_counter()
     parts, children = {}, []
     ranks = [0] * len(w.ids)
@@ -829,7 +884,7 @@ def _finish_streamed(w: _Walker, trace, pinned: bool):
     finally:
         for child in children:
             child.close()
-    w.timings[phase] += time.perf_counter() - t0
+    ph.__exit__(None, None, None)
     w.ranks = ranks
     w.launch_log["merges"] += 1
     w.launch_log["branch_ops"] += 0
@@ -863,11 +918,11 @@ def _finish_partitioned(w: _Walker, trace, slot_part, slot_reduce):
     program = np.array(w.queue, dtype=np.uint32)
     w.queue, w.queue_has_cx, w.staged, w.pending = [], False, None, None
     w.book_gates()
-    t0 = time.perf_counter()
+    ph = w.phase(phase).__enter__()
     ranks, partitioned = w.store.apply_operator_run_part(counts, axes, weights, program, w.eps, part, parts)
     if partitioned and slot_reduce is not None:
         ranks = slot_reduce(ranks)              # global ranks: sum of the shares
-    w.timings[phase] += time.perf_counter() - t0
+    ph.__exit__(None, None, None)
     w.ranks = list(ranks)
     w.unsorted = False
     w.launch_log["merges"] += 1
@@ -931,9 +986,8 @@ def _walk_v1_eager(instructions, partition, w: _Walker, trace, counters):
                 w.resolve(trace)               # this gate must see merged terms
                 w.count_gate()
                 w.flush()
-                t0 = time.perf_counter()
-                w.store.apply_split(q, *split_tables(block))
-                w.timings["sub_flatten"] += time.perf_counter() - t0
+                with w.phase("sub_flatten"):
+                    w.store.apply_split(q, *split_tables(block))
                 w.branched(pos - 1, "sub_flatten", trace)
             n_1q += 1
         if pos in boundaries:
@@ -978,7 +1032,7 @@ def _walk_operators(partition, lut, is_perm, tables, w: _Walker, trace, counters
                 # before the operator's own merge, only duplicates meet earlier.
                 w.resolve(trace)               # expand merged terms only
                 bucket = partition.u_groups[ui]
-                t0 = time.perf_counter()
+                ph = w.phase("sub_flatten").__enter__()
                 if mode is Mode.V2:
                     # dense layout: a row of the substituted block that is not one-hot needs the
                     # 4**n scatter buffer (reference stabilizer.py:264-276).  Nothing has ever
@@ -1012,13 +1066,13 @@ def _walk_operators(partition, lut, is_perm, tables, w: _Walker, trace, counters
                             if raw > WIDE_RAW_BUDGET:
                                 raw = sum(w.store.merge(0.0))
                                 w.unsorted = False
-                w.timings["sub_flatten"] += time.perf_counter() - t0
+                ph.__exit__(None, None, None)
                 w.branched(step, "sub_flatten", trace)
             else:
                 w.resolve(trace)               # expand merged terms only
                 w.flush()
                 counts, axes, weights = _lut.operator_tables(lut[ui])
-                t0 = time.perf_counter()
+                ph = w.phase("sub_flatten").__enter__()
                 if mode is Mode.V2 and 4 ** n > DENSE_FLATTEN_BUDGET:
                     # dense layout: a branching substitution needs a 4**n scatter buffer
                     # (reference stabilizer.py:264-276); one-hot rows take the fast path
@@ -1050,7 +1104,7 @@ def _walk_operators(partition, lut, is_perm, tables, w: _Walker, trace, counters
                     pad_dense(w.store, n, dense_gens)
                 else:
                     w.stage_operator(counts, axes, weights)
-                w.timings["sub_flatten"] += time.perf_counter() - t0
+                ph.__exit__(None, None, None)
                 w.branched(step, "sub_flatten", trace)
             counters["sub_flatten_ops"] += 1
             ui += 1

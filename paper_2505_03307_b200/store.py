@@ -56,6 +56,17 @@ class DeviceStore:
     def handle(self):
         return self._h
 
+    def mark(self) -> int:
+        """A CUDA event on the store's stream (qx_store_event_record); returns its index."""
+        idx = C.c_int32()
+        nat.check(nat.lib().qx_store_event_record(self._h, C.byref(idx)))
+        return idx.value
+
+    def elapsed_ms(self, first: int, second: int) -> float:
+        ms = C.c_double()
+        nat.check(nat.lib().qx_store_event_elapsed(self._h, int(first), int(second), C.byref(ms)))
+        return ms.value
+
     def set_stream(self, cuda_stream: int):
         nat.check(nat.lib().qx_store_set_stream(self._h, C.c_void_p(int(cuda_stream))))
 
@@ -273,9 +284,11 @@ class DeviceStore:
             buf = nat.PINNED.take(16 * cap)
             keys = buf.view(np.uint64, 0, cap)
             lam = buf.view(np.float64, 8 * cap, cap)
+        dev_ms = C.c_double()
         nat.check(nat.lib().qx_store_run_program(self._h, program.handle, nat.ptr(init), float(eps), nat.ptr(ranks),
                                                  C.byref(raw), C.byref(fitted), nat.ptr(off), nat.ptr(keys), nat.ptr(lam),
-                                                 cap, C.byref(filled)))
+                                                 cap, C.byref(filled), C.byref(dev_ms)))
+        self.program_ms = dev_ms.value         # duration of the launch on the GPU's clock
         segs = None
         if fitted.value and filled.value:
             o = off.tolist()

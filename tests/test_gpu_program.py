@@ -137,3 +137,25 @@ def test_initial_generators_and_shards_go_through_programs():
     a, b, _ = _both(gates, n, "v3", initial=init)
     _same(a, b)
     assert "program_steps" in a.device
+
+
+def test_phase_timers_are_measured_on_the_device():
+    """RunReport.timings keeps the reference's four keys (engine.py:92); the device phases come from
+    the circuit kernel's own clock (one-launch runs) or CUDA events (device_timers=True)."""
+    n, gates = workloads.build("c2_10q_near_clifford")
+    engine.clear_plans()
+    qx.run(gates, n, "v3")
+    rep = qx.run(gates, n, "v3")
+    assert set(rep.timings) == {"partition", "lut", "sub_flatten", "cx"}
+    assert "program_steps" in rep.device
+    host = rep.device["host_timings"]["sub_flatten"]
+    assert 0.0 < rep.timings["sub_flatten"] <= host           # kernel time inside the host's launch + wait
+    engine._PROGRAMS_ON = False
+    try:
+        engine.clear_plans()
+        by_events = qx.run(gates, n, "v3", device_timers=True)
+        by_clock = qx.run(gates, n, "v3")
+    finally:
+        engine._PROGRAMS_ON = True
+    assert by_events.timings["sub_flatten"] > 0.0 and by_clock.timings["sub_flatten"] > 0.0
+    assert by_events.rank_trace == by_clock.rank_trace == rep.rank_trace
