@@ -138,6 +138,25 @@ int qx_store_upload_wide(qx_store* s, const int64_t* offsets, const uint64_t* wo
                          const double* lambdas);
 int qx_store_download_wide(qx_store* s, int64_t* offsets, uint64_t* words, double* lambdas,
                            int64_t cap_terms);
+/* The grouped operator step above 32 qubits (the reference's big-int path,
+ * stabilizer.py:40-59, 289-322).  qx_store_support: per segment, OR of the support masks of its
+ * terms -- n_segments x n_words words (bit 2p set: some term has a non-identity digit at bit
+ * position 2p; works on one-word stores too).  qx_store_compact: the terms of the segments with
+ * take[g] != 0 as one-word keys over the n_sel selected qubits (ascending; every taken term's
+ * support must lie inside them) into `narrow`, a one-word store of n_sel qubits and as many
+ * segments (the segments not taken are empty there); the order of the terms is kept, and so is
+ * canonical order.  qx_store_expand: the inverse -- the taken segments of the multi-word store are
+ * REPLACED by the one-word store's segments spread back over the selected qubits, the others keep
+ * their terms.  Between the two the caller runs the one-word operator step
+ * (qx_apply_operator_run) with the selected rows of the operator tables; identity digits
+ * contribute a factor of exactly 1, so the result is what the reference computes at full width,
+ * bit for bit. */
+int qx_store_support(qx_store* s, uint64_t* words);
+int qx_store_compact(qx_store* wide, const int32_t* qubits, int32_t n_sel, const uint8_t* take,
+                     qx_store* narrow);
+int qx_store_expand(qx_store* narrow, const int32_t* qubits, int32_t n_sel, const uint8_t* take,
+                    qx_store* wide);
+
 /* As qx_apply_clifford with 64-bit ops: low word as there (kind, image axes, signs; the shift
  * fields unused), bits 32-47 = bit position 2*(n-1-q) of the (control) digit, 48-63 of the target. */
 int qx_apply_clifford_wide(qx_store* s, const uint64_t* ops, int32_t n_ops, uint32_t cx_c,

@@ -57,6 +57,9 @@ SIGNATURES = {
     "qx_store_words": (C.c_int, [_p, _P(_i32)]),
     "qx_store_upload_wide": (C.c_int, [_p, _p, _p, _p]),
     "qx_store_download_wide": (C.c_int, [_p, _p, _p, _p, _i64]),
+    "qx_store_support": (C.c_int, [_p, _p]),
+    "qx_store_compact": (C.c_int, [_p, _p, _i32, _p, _p]),
+    "qx_store_expand": (C.c_int, [_p, _p, _i32, _p, _p]),
     "qx_apply_clifford_wide": (C.c_int, [_p, _p, _i32, _u32, _u32, _u32]),
     "qx_apply_split_wide": (C.c_int, [_p, _i32, _p, _p, _p, _p]),
     "qx_store_download_async": (C.c_int, [_p, _p, _p, _p, _i64]),

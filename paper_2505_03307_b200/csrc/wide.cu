@@ -535,3 +535,230 @@ extern "C" int qx_store_words(qx_store* s, int32_t* n_words) {
   *n_words = s->n_words;
   return QX_OK;
 }
+
+// ---- compaction onto the support (the grouped operator step above 32 qubits) ---------------------
+// The reference runs v2/v3 operators at any width with big-int indices (stabilizer.py:40-59,
+// 289-322).  A branching operator only ever acts on the digits a term HAS, and the circuits that
+// are feasible above 32 qubits keep their generators on few qubits.  A generator none of whose
+// terms has a digit on a qubit the operator touches is not changed by it at all; when the support
+// of the OTHER generators is at most 32 qubits wide, their terms are packed into one-word keys over
+// those qubits -- ascending qubit order, so the order of the words is kept -- the one-word
+// operator step runs on them (grouped / bucketed / one-launch paths, all of it), and the result is
+// spread back between the untouched generators.  Identity digits contribute a factor of exactly 1
+// and no branch, so the coefficients are the reference's bit for bit.
+namespace {
+
+struct QubitMap {
+  int n_sel;
+  int wide_pos[QX_MAX_QUBITS];     // bit position of selected qubit j in the wide key (j ascending = qubit ascending)
+};
+
+// one CTA per segment: OR of the support masks of its terms, n_words words
+__global__ void __launch_bounds__(kThreads)
+k_wide_support(Planes pl, const int64_t* __restrict__ seg, int n_words, u64* __restrict__ out) {
+  __shared__ u64 s_acc[kThreads / 32];
+  const int g = blockIdx.x;
+  const int64_t lo = seg[g], hi = seg[g + 1];
+  for (int w = 0; w < n_words; ++w) {
+    u64 acc = 0;
+    for (int64_t i = lo + threadIdx.x; i < hi; i += kThreads) acc |= support_mask(pl.p[w][i]);
+#pragma unroll
+    for (int d = 16; d > 0; d >>= 1) acc |= __shfl_xor_sync(QX_FULL_MASK, acc, d);
+    if (lane_id() == 0) s_acc[threadIdx.x >> 5] = acc;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      u64 all = 0;
+      for (int i = 0; i < kThreads / 32; ++i) all |= s_acc[i];
+      out[(size_t)g * n_words + w] = all;
+    }
+    __syncthreads();
+  }
+}
+
+// index of the segment that holds term i (offsets ascending, empty segments allowed)
+__device__ __forceinline__ int segment_holding(const int64_t* off, int n_seg, int64_t i) {
+  int lo = 0, hi = n_seg;                       // off[lo] <= i < off[hi]
+  while (hi - lo > 1) {
+    const int mid = (lo + hi) >> 1;
+    if (off[mid] <= i) lo = mid; else hi = mid;
+  }
+  return lo;
+}
+
+// narrow term i (offsets n_off: taken segments only, the others empty) <- wide term
+__global__ void __launch_bounds__(kThreads)
+k_wide_compact(Planes in, const double* __restrict__ lam_in, const int64_t* __restrict__ w_off,
+               const int64_t* __restrict__ n_off, int n_seg, int n_words, u64* __restrict__ keys_out,
+               double* __restrict__ lam_out, int* __restrict__ error, const __grid_constant__ QubitMap map) {
+  const int64_t total = n_off[n_seg];
+  for (int64_t i = (int64_t)blockIdx.x * kThreads + threadIdx.x; i < total; i += (int64_t)gridDim.x * kThreads) {
+    const int g = segment_holding(n_off, n_seg, i);
+    const int64_t src = w_off[g] + (i - n_off[g]);
+    u64 k[kMaxWords];
+    for (int w = 0; w < n_words; ++w) k[w] = in.p[w][src];
+    u64 out = 0;
+    for (int j = 0; j < map.n_sel; ++j) {
+      const int pos = map.wide_pos[j];
+      const u64 d = (k[pos >> 6] >> (pos & 63)) & 3ull;
+      k[pos >> 6] &= ~(3ull << (pos & 63));
+      out |= d << (2 * (map.n_sel - 1 - j));
+    }
+    u64 rest = 0;
+    for (int w = 0; w < n_words; ++w) rest |= k[w];
+    if (rest) atomicExch(error, 1);                 // a digit outside the selection
+    keys_out[i] = out;
+    lam_out[i] = lam_in[src];
+  }
+}
+
+// new wide term i (offsets o_off) <- the one-word store's term (taken segments) or the old wide term
+__global__ void __launch_bounds__(kThreads)
+k_wide_expand(const u64* __restrict__ keys_in, const double* __restrict__ lam_in, const int64_t* __restrict__ n_off,
+              Planes old, const double* __restrict__ lam_old, const int64_t* __restrict__ w_off,
+              const int64_t* __restrict__ o_off, const unsigned char* __restrict__ take, int n_seg, int n_words,
+              Planes out, double* __restrict__ lam_out, const __grid_constant__ QubitMap map) {
+  const int64_t total = o_off[n_seg];
+  for (int64_t i = (int64_t)blockIdx.x * kThreads + threadIdx.x; i < total; i += (int64_t)gridDim.x * kThreads) {
+    const int g = segment_holding(o_off, n_seg, i);
+    const int64_t r = i - o_off[g];
+    if (take[g]) {
+      u64 k[kMaxWords];
+      for (int w = 0; w < n_words; ++w) k[w] = 0;
+      const u64 key = keys_in[n_off[g] + r];
+      for (int j = 0; j < map.n_sel; ++j) {
+        const int pos = map.wide_pos[j];
+        k[pos >> 6] |= ((key >> (2 * (map.n_sel - 1 - j))) & 3ull) << (pos & 63);
+      }
+      for (int w = 0; w < n_words; ++w) out.p[w][i] = k[w];
+      lam_out[i] = lam_in[n_off[g] + r];
+    } else {
+      for (int w = 0; w < n_words; ++w) out.p[w][i] = old.p[w][w_off[g] + r];
+      lam_out[i] = lam_old[w_off[g] + r];
+    }
+  }
+}
+
+int fill_map(const qx_store* wide, const int32_t* qubits, int32_t n_sel, QubitMap* map) {
+  QX_REQUIRE(qubits && n_sel >= 1 && n_sel <= QX_MAX_QUBITS, "need 1..%d selected qubits, got %d", QX_MAX_QUBITS, n_sel);
+  map->n_sel = n_sel;
+  for (int j = 0; j < n_sel; ++j) {
+    QX_REQUIRE(qubits[j] >= 0 && qubits[j] < wide->n_qubits && (j == 0 || qubits[j] > qubits[j - 1]),
+               "selected qubits must ascend within [0, %d)", wide->n_qubits);
+    map->wide_pos[j] = 2 * (wide->n_qubits - 1 - qubits[j]);
+  }
+  return QX_OK;
+}
+
+int grid_for(const qx_store* s, int64_t total) {
+  return (int)std::max<int64_t>(1, std::min<int64_t>((total + kThreads - 1) / kThreads, (int64_t)s->sm_count * 8));
+}
+
+int check_pair(const qx_store* wide, const qx_store* narrow, int32_t n_sel, const uint8_t* take) {
+  QX_REQUIRE(wide && narrow && take, "NULL argument");
+  QX_REQUIRE(narrow->n_words == 1 && narrow->n_qubits == n_sel && narrow->n_seg == wide->n_seg &&
+                 narrow->device == wide->device,
+             "the one-word store must have %d qubits and %d segments on device %d", n_sel, wide->n_seg, wide->device);
+  QX_REQUIRE(!wide->narrow_keys && !narrow->narrow_keys, "a store was left with narrow keys for download");
+  return QX_OK;
+}
+
+}  // namespace
+
+extern "C" int qx_store_support(qx_store* s, uint64_t* words) {
+  QX_REQUIRE(s && words, "NULL argument");
+  QX_REQUIRE(!s->narrow_keys, "qx_store_support: the store was left with narrow keys for download");
+  QX_CUDA(cudaSetDevice(s->device));
+  const size_t bytes = 8 * (size_t)s->n_words * (size_t)s->n_seg;
+  QX_TRY(qx_store_scratch(s, (int64_t)bytes));
+  k_wide_support<<<s->n_seg, kThreads, 0, s->stream>>>(planes_of(s, s->cur), s->seg[s->cur], s->n_words,
+                                                      reinterpret_cast<u64*>(s->scratch));
+  qx_count_launches(1);
+  QX_CUDA(cudaGetLastError());
+  QX_CUDA(cudaMemcpyAsync(words, s->scratch, bytes, cudaMemcpyDeviceToHost, s->stream));
+  QX_CUDA(cudaStreamSynchronize(s->stream));
+  return QX_OK;
+}
+
+extern "C" int qx_store_compact(qx_store* wide, const int32_t* qubits, int32_t n_sel, const uint8_t* take,
+                                qx_store* narrow) {
+  QX_TRY(check_pair(wide, narrow, n_sel, take));
+  QubitMap map;
+  QX_TRY(fill_map(wide, qubits, n_sel, &map));
+  QX_CUDA(cudaSetDevice(wide->device));
+  if (!wide->exact) QX_TRY(qx_store_refresh(wide));
+  const int n_seg = wide->n_seg;
+  std::vector<int64_t> n_off((size_t)n_seg + 1, 0);
+  int64_t largest = 0;
+  for (int g = 0; g < n_seg; ++g) {
+    const int64_t len = take[g] ? wide->h_seg[g + 1] - wide->h_seg[g] : 0;
+    n_off[g + 1] = n_off[g] + len;
+    largest = std::max(largest, len);
+  }
+  const int64_t total = n_off[n_seg];
+  QX_TRY(qx_store_reserve(narrow, total, false));
+  QX_TRY(qx_store_scratch(wide, 16));
+  int* error = reinterpret_cast<int*>(wide->scratch);
+  QX_CUDA(cudaMemsetAsync(error, 0, 16, wide->stream));
+  const int c = narrow->cur;
+  QX_CUDA(cudaMemcpyAsync(narrow->seg[c], n_off.data(), sizeof(int64_t) * (size_t)(n_seg + 1), cudaMemcpyHostToDevice,
+                          wide->stream));
+  if (total > 0) {
+    k_wide_compact<<<grid_for(wide, total), kThreads, 0, wide->stream>>>(
+        planes_of(wide, wide->cur), wide->lam[wide->cur], wide->seg[wide->cur], narrow->seg[c], n_seg, wide->n_words,
+        narrow->keys[c], narrow->lam[c], error, map);
+    qx_count_launches(1);
+    QX_CUDA(cudaGetLastError());
+  }
+  int h_error = 0;
+  QX_CUDA(cudaMemcpyAsync(&h_error, error, sizeof(int), cudaMemcpyDeviceToHost, wide->stream));
+  QX_CUDA(cudaStreamSynchronize(wide->stream));      // n_off is read by the copy above; the one-word store runs on its own stream
+  QX_REQUIRE(h_error == 0, "qx_store_compact: a taken term has a non-identity digit outside the selected qubits");
+  memcpy(narrow->h_seg, n_off.data(), sizeof(int64_t) * (size_t)(n_seg + 1));
+  narrow->exact = true;
+  narrow->pack_bnd = nullptr;
+  narrow->ub_total = total;
+  narrow->ub_seg = largest;
+  return QX_OK;
+}
+
+extern "C" int qx_store_expand(qx_store* narrow, const int32_t* qubits, int32_t n_sel, const uint8_t* take,
+                               qx_store* wide) {
+  QX_TRY(check_pair(wide, narrow, n_sel, take));
+  QubitMap map;
+  QX_TRY(fill_map(wide, qubits, n_sel, &map));
+  QX_CUDA(cudaSetDevice(wide->device));
+  if (!narrow->exact) QX_TRY(qx_store_refresh(narrow));
+  if (!wide->exact) QX_TRY(qx_store_refresh(wide));
+  QX_CUDA(cudaStreamSynchronize(narrow->stream));
+  const int n_seg = wide->n_seg;
+  std::vector<int64_t> o_off((size_t)n_seg + 1, 0);
+  int64_t largest = 0;
+  for (int g = 0; g < n_seg; ++g) {
+    const int64_t len = take[g] ? narrow->h_seg[g + 1] - narrow->h_seg[g] : wide->h_seg[g + 1] - wide->h_seg[g];
+    o_off[g + 1] = o_off[g] + len;
+    largest = std::max(largest, len);
+  }
+  const int64_t total = o_off[n_seg];
+  QX_TRY(qx_store_reserve(wide, std::max(total, wide->h_seg[n_seg]), true));   // both buffers: old content stays live
+  const int in = wide->cur, out = wide->cur ^ 1;
+  QX_TRY(qx_store_scratch(wide, (int64_t)n_seg + 64));
+  unsigned char* d_take = reinterpret_cast<unsigned char*>(wide->scratch);
+  QX_CUDA(cudaMemcpyAsync(d_take, take, (size_t)n_seg, cudaMemcpyHostToDevice, wide->stream));
+  QX_CUDA(cudaMemcpyAsync(wide->seg[out], o_off.data(), sizeof(int64_t) * (size_t)(n_seg + 1), cudaMemcpyHostToDevice,
+                          wide->stream));
+  if (total > 0) {
+    k_wide_expand<<<grid_for(wide, total), kThreads, 0, wide->stream>>>(
+        narrow->keys[narrow->cur], narrow->lam[narrow->cur], narrow->seg[narrow->cur], planes_of(wide, in),
+        wide->lam[in], wide->seg[in], wide->seg[out], d_take, n_seg, wide->n_words, planes_of(wide, out), wide->lam[out],
+        map);
+    qx_count_launches(1);
+    QX_CUDA(cudaGetLastError());
+  }
+  QX_CUDA(cudaStreamSynchronize(wide->stream));       // host arrays above; the one-word store may be destroyed right away
+  wide->cur = out;
+  memcpy(wide->h_seg, o_off.data(), sizeof(int64_t) * (size_t)(n_seg + 1));
+  wide->exact = true;
+  wide->ub_total = total;
+  wide->ub_seg = largest;
+  return QX_OK;
+}

@@ -90,6 +90,7 @@ class AgreementReport:
 
 
 _DEVICE_TIMERS = bool(__import__("os").environ.get("QX_DEVICE_TIMERS"))
+_WIDE_COMPACT = not __import__("os").environ.get("QX_NO_WIDE_COMPACT")
 
 
 class _Phase:
@@ -1001,6 +1002,61 @@ def _walk_v1_eager(instructions, partition, w: _Walker, trace, counters):
 WIDE_RAW_BUDGET = 1 << 16
 
 
+def _operator_on_support(w: _Walker, block, step: int, mode) -> bool:
+    """A branching U_k on a multi-word store whose terms live on at most 32 qubits: pack them into
+    one-word keys over their support (csrc/wide.cu qx_store_compact), run the one-word operator
+    step there -- the reference's sub + flatten + canonicalize (stabilizer.py:189-337), with its
+    string order in v3 (stabilizer.py:294-296) -- and spread the result back.  Identity digits
+    neither branch nor change a coefficient, so this is what the reference computes with big-int
+    indices (stabilizer.py:40-59).  Generators without a digit on a qubit the operator touches are
+    left alone (every such term maps to itself with weight exactly 1).  Returns False (nothing
+    touched but the queue flushed) when the support of the others is wider than a word or the
+    run is term-partitioned."""
+    if w.before_merge is not None or w.reduce_ranks is not None or w.store.words <= 1 or not _WIDE_COMPACT:
+        return False
+    w.flush()                          # queued permutations move the support
+    counts, axes, weights = _lut.operator_tables(block)
+    # qubits the operator touches at all (any cell that is not "this axis, weight +1")
+    ident_axes = np.arange(1, 4)
+    touched = 0
+    for q in range(w.n):
+        if not (np.all(counts[q] == 1) and np.all(axes[q][:, 0] == ident_axes) and np.all(weights[q][:, 0] == 1.0)):
+            touched |= 1 << q
+    masks = w.store.support()
+    take = [bool(m & touched) for m in masks]
+    union = 0
+    for m, t in zip(masks, take):
+        if t:
+            union |= m
+    sel = [q for q in range(w.n) if (union >> q) & 1]
+    if not any(take):
+        return True                    # no generator has a digit the operator touches: nothing changes
+    if len(sel) > 32:
+        return False
+    c, a, wt = counts[sel], axes[sel], weights[sel]
+    w.book_gates()
+    narrow = w.store.compact(sel, take)
+    try:
+        if mode is Mode.V3:
+            narrow.order_for_operator(c)
+        _, nranks = narrow.apply_operator_run(c, a, wt, np.zeros(0, dtype=np.uint32), w.eps)
+        w.store.expand_from(narrow, sel, take)
+    finally:
+        narrow.close()
+    ranks = [nr if t else old for nr, old, t in zip(nranks, w.ranks, take)]
+    w.ranks = list(ranks)
+    # the generators that went through the operator step are canonical now; the others sit as the
+    # last permutation run left them
+    w.unsorted = w.unsorted and not all(take)
+    w.launch_log["branch_ops"] += 1
+    w.launch_log["merges"] += 1
+    w.launch_log["compacted_operators"] = w.launch_log.get("compacted_operators", 0) + 1
+    for local, r in enumerate(w.ranks):
+        if r == 0:
+            raise NumericalCollapseError(f"all terms of generator {w.ids[local]} dropped at operator step {step}")
+    return True
+
+
 def _walk_operators(partition, lut, is_perm, tables, w: _Walker, trace, counters, mode, eager):
     """Operator chain (reference engine.py:110-132): U_k = substitute + flatten, V_k = CX run."""
     n = w.n
@@ -1049,25 +1105,30 @@ def _walk_operators(partition, lut, is_perm, tables, w: _Walker, trace, counters
                                         f"dense flatten needs a 4**{n}-element buffer (> {DENSE_FLATTEN_BUDGET}); "
                                         "use the ragged layout for circuits of this size"
                                     )
-                raw = sum(w.ranks)
-                for wire in sorted(bucket):
-                    for inst in bucket[wire]:
-                        table = _lut.FIXED_PERMS.get(inst.gate)
-                        block = None
-                        if table is None:
-                            block = _lut.gate_branch_block(inst.gate, inst.theta)
-                            table = _lut.perm_word(block)
-                        if table is not None:
-                            w.push_perm(wire, table)
-                        else:
-                            w.flush()
-                            w.store.apply_split(wire, *split_tables(block))
-                            raw *= 2
-                            if raw > WIDE_RAW_BUDGET:
-                                raw = sum(w.store.merge(0.0))
-                                w.unsorted = False
-                ph.__exit__(None, None, None)
-                w.branched(step, "sub_flatten", trace)
+                if _operator_on_support(w, lut[ui], step, mode):
+                    # the store's support fits one word: the grouped one-word operator step ran on
+                    # the compacted terms (sub + flatten + merge, exactly where the reference merges)
+                    ph.__exit__(None, None, None)
+                else:
+                    raw = sum(w.ranks)
+                    for wire in sorted(bucket):
+                        for inst in bucket[wire]:
+                            table = _lut.FIXED_PERMS.get(inst.gate)
+                            block = None
+                            if table is None:
+                                block = _lut.gate_branch_block(inst.gate, inst.theta)
+                                table = _lut.perm_word(block)
+                            if table is not None:
+                                w.push_perm(wire, table)
+                            else:
+                                w.flush()
+                                w.store.apply_split(wire, *split_tables(block))
+                                raw *= 2
+                                if raw > WIDE_RAW_BUDGET:
+                                    raw = sum(w.store.merge(0.0))
+                                    w.unsorted = False
+                    ph.__exit__(None, None, None)
+                    w.branched(step, "sub_flatten", trace)
             else:
                 w.resolve(trace)               # expand merged terms only
                 w.flush()

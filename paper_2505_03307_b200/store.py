@@ -56,6 +56,40 @@ class DeviceStore:
     def handle(self):
         return self._h
 
+    def support(self) -> list:
+        """Per segment, the qubits on which some term has a non-identity digit (qx_store_support),
+        as integer masks with bit q set for qubit q."""
+        words = np.zeros((self.n_segments, self.words), dtype=np.uint64)
+        nat.check(nat.lib().qx_store_support(self._h, nat.ptr(words)))
+        out = []
+        for row in words.tolist():
+            key_mask = sum(int(w) << (64 * i) for i, w in enumerate(row))
+            m = 0
+            for q in range(self.n):
+                if (key_mask >> (2 * (self.n - 1 - q))) & 1:
+                    m |= 1 << q
+            out.append(m)
+        return out
+
+    def compact(self, qubits, take) -> "DeviceStore":
+        """A one-word store over the selected qubits holding the terms of the segments in ``take``
+        (bool per segment); the other segments are empty in it."""
+        sel = np.ascontiguousarray(qubits, dtype=np.int32)
+        flags = np.ascontiguousarray(take, dtype=np.uint8)
+        narrow = DeviceStore(len(sel), self.n_segments, 0, self.device)
+        try:
+            nat.check(nat.lib().qx_store_compact(self._h, nat.ptr(sel), len(sel), nat.ptr(flags), narrow._h))
+        except BaseException:
+            narrow.close()
+            raise
+        return narrow
+
+    def expand_from(self, narrow: "DeviceStore", qubits, take):
+        """Replace the segments in ``take`` by the one-word store's, spread back over the selected qubits."""
+        sel = np.ascontiguousarray(qubits, dtype=np.int32)
+        flags = np.ascontiguousarray(take, dtype=np.uint8)
+        nat.check(nat.lib().qx_store_expand(narrow._h, nat.ptr(sel), len(sel), nat.ptr(flags), self._h))
+
     def mark(self) -> int:
         """A CUDA event on the store's stream (qx_store_event_record); returns its index."""
         idx = C.c_int32()

@@ -132,6 +132,12 @@ def test_high_rank_circuit_embedded_above_32_qubits(n, mode):
     for gw, gn in zip(wide.final.generators, narrow.final.generators):
         assert [int(v) for v in gw.indices] == [int(v) * shift for v in gn.indices]
         assert np.max(np.abs(gw.lambdas - gn.lambdas)) < 1e-12
+    if mode == "v3":
+        # the operators ran as grouped one-word steps on the generators' support (qx_store_compact /
+        # qx_store_expand): same kernels, same order of every sum as the one-word run -- bit for bit
+        assert wide.device.get("compacted_operators", 0) == 2
+        for gw, gn in zip(wide.final.generators, narrow.final.generators):
+            assert np.array_equal(gw.lambdas, gn.lambdas)
     for j in range(10, n):
         g = wide.final.generators[j]
         assert [int(v) for v in g.indices] == [3 * 4 ** (n - 1 - j)] and g.lambdas.tolist() == [1.0]
@@ -170,3 +176,102 @@ def test_limits_above_32_qubits():
         st.init_z([0])
         with pytest.raises(qx.NativeError, match="one-word keys"):
             st.zi_sums()
+
+
+
+def test_compact_and_expand_round_trip_on_a_segment_subset():
+    """qx_store_support / qx_store_compact / qx_store_expand against a big-int model: supports per
+    segment, taken segments packed over the selected qubits in order, the others left alone."""
+    n, rng = 90, np.random.default_rng(11)
+    sel = sorted(rng.choice(n, size=20, replace=False).tolist())
+    segs, take = [], []
+    for g in range(7):
+        inside = g % 3 != 1
+        pool = sel if inside else list(range(n))
+        size = int(rng.integers(0 if g == 4 else 1, 400))
+        words = set()
+        while len(words) < size:
+            w = 0
+            for q in rng.choice(pool, size=int(rng.integers(1, 9)), replace=False):
+                w |= int(rng.integers(1, 4)) << (2 * (n - 1 - int(q)))
+            words.add(w)
+        obj = np.empty(size, dtype=object)
+        obj[:] = sorted(words)
+        segs.append((rng.uniform(-1, 1, size=size), obj))
+        take.append(inside)
+    with DeviceStore(n, len(segs), 0) as st:
+        st.upload(segs)
+        masks = st.support()
+        for (lam, keys), m in zip(segs, masks):
+            want = 0
+            for k in keys:
+                for q in range(n):
+                    if (int(k) >> (2 * (n - 1 - q))) & 3:
+                        want |= 1 << q
+            assert m == want
+        narrow = st.compact(sel, take)
+        try:
+            got = narrow.segments()
+            for (lam, keys), (nl, nk), t in zip(segs, got, take):
+                if not t:
+                    assert len(nl) == 0
+                    continue
+                packed = [sum(((int(k) >> (2 * (n - 1 - q))) & 3) << (2 * (len(sel) - 1 - j)) for j, q in enumerate(sel))
+                          for k in keys]
+                assert [int(v) for v in nk] == packed and packed == sorted(packed)
+                assert np.array_equal(nl, lam)
+            narrow.merge(0.0)                                   # a step on the one-word side (order kept: keys unique)
+            st.expand_from(narrow, sel, take)
+        finally:
+            narrow.close()
+        back = st.segments()
+    for (lam, keys), (bl, bk) in zip(segs, back):
+        assert [int(v) for v in bk] == [int(v) for v in keys] and np.array_equal(bl, lam)
+    with DeviceStore(n, len(segs), 0) as st:
+        st.upload(segs)
+        with pytest.raises(ValueError, match="outside the selected"):
+            st.compact(sel, [True] * len(segs)).close()
+
+
+def test_operator_on_support_with_idle_and_clifford_only_generators():
+    """v3 above 32 qubits on a circuit whose operators mix rotations with Clifford gates on far
+    qubits: generators the operator does not touch are left alone, the others go through the
+    one-word grouped step; against the same circuit on relabelled (adjacent) qubits."""
+    n = 80
+    place = [3, 17, 40, 41, 66, 79]
+    rng = np.random.default_rng(21)
+    small = qx.gen_random(len(place), 60, rng)
+    big = [qx.Instruction(g.gate, tuple(place[w] for w in g.wires), g.theta) for g in small]
+    a = qx.run(small, len(place), "v3")
+    b = qx.run(big, n, "v3")
+    assert b.device.get("compacted_operators", 0) >= 1
+    for j, q in enumerate(place):
+        ga, gb = a.final.generators[j], b.final.generators[q]
+        spread = []
+        for v in ga.indices:
+            w = 0
+            for jj, qq in enumerate(place):
+                w |= ((int(v) >> (2 * (len(place) - 1 - jj))) & 3) << (2 * (n - 1 - qq))
+            spread.append(w)
+        assert [int(v) for v in gb.indices] == spread
+        assert np.array_equal(gb.lambdas, ga.lambdas)
+    for q in range(n):
+        if q not in place:
+            g = b.final.generators[q]
+            assert [int(v) for v in g.indices] == [3 * 4 ** (n - 1 - q)] and g.lambdas.tolist() == [1.0]
+
+
+def test_generators_an_operator_leaves_alone_are_still_sorted_at_the_end():
+    """Found by tools/fuzz_wide.py: a generator that a compacted operator step does not touch keeps
+    the order the last Clifford run left it in -- the deferred re-sort must still happen."""
+    from paper_2505_03307_b200 import workloads
+    for case in (16865, 17061):
+        rng = np.random.default_rng([7, case])
+        k = int(rng.integers(1, 9))
+        n = int(rng.choice([33, 40, 64, 70, 130]))
+        gates = workloads.gen_random(k, int(rng.integers(0, 60 if k <= 6 else 35)), rng)
+        narrow, wide = qx.run(gates, k, "v3"), qx.run(gates, n, "v3")
+        shift = 4 ** (n - k)
+        for gw, gn in zip(wide.final.generators, narrow.final.generators):
+            assert [int(v) for v in gw.indices] == [int(v) * shift for v in gn.indices]
+            assert np.array_equal(gw.lambdas, gn.lambdas)
