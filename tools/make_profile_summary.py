@@ -29,7 +29,7 @@ for name in sorted(os.listdir(src)):
         continue
     hdr, units, r = rr[0], rr[1], rr[2]
     v1 = name.startswith(tag + "_v1_")
-    wl = "xyz_chain(14,2) v1" if v1 else "xyz_chain(16,2) v3"
+    wl = "xyz_chain(14,2) v1" if v1 else "config 5 (32 qubits, 5000 gates) v3, the whole circuit" if "k_small_circuit" in name else "xyz_chain(16,2) v3"
     out.append(f"\n## {name[len(tag) + 1:-8]} ({wl}, ncu --set full, first captured launch): {r[hdr.index('Kernel Name')][:70]}\n")
     for w in want:
         if w in hdr:

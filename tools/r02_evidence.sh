@@ -15,3 +15,9 @@ for spec in "k_bucket_emit 1 1" "k_tile_desc 1 1"; do
       > gpurun_out/${R}_$1.log 2>&1
   echo "$1 rc=$?"
 done
+# the one-launch circuit kernel on config 5 (whole circuit = one launch of k_small_circuit)
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:k_small_circuit -s 2 -c 1 -f \
+    -o gpurun_out/${R}_k_small_circuit python tools/profile_step.py --workload c5_32q_clifford_t --mode v3 --warmup 2 --steps 1 \
+    > gpurun_out/${R}_k_small_circuit.log 2>&1
+echo "k_small_circuit rc=$?"
+python tools/program_times.py > gpurun_out/${R}_program_times.txt 2>&1
