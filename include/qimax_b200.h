@@ -294,11 +294,14 @@ int qx_program_rows(const qx_program* p, int32_t* rows);
  * of it fit.  device_ms (may be NULL): duration of the launch on the GPU's own clock (first CTA in
  * to last CTA out, %globaltimer) -- the device phase timer of the run at no cost.  One launch and
  * one stream synchronize: ranks, offsets and the host copy of the result are written by the
- * kernel itself into page-locked memory. */
+ * kernel itself into page-locked memory.  max_steps > 0: only the first max_steps steps (a circuit
+ * whose generators outgrow shared memory later starts with one launch and goes on step by step);
+ * *stopped_step (may be NULL), when *fitted = 0: the first step that did not fit. */
 int qx_store_run_program(qx_store* s, const qx_program* p, const int32_t* init_qubits, double eps,
                          int64_t* ranks, int64_t* raw_total, int32_t* fitted, int64_t* offsets,
                          uint64_t* host_keys, double* host_lambdas, int64_t host_cap,
-                         int32_t* host_filled, double* device_ms);
+                         int32_t* host_filled, double* device_ms, int32_t max_steps,
+                         int32_t* stopped_step);
 
 /* ---- a6: duplicate-term merge (canonicalize, stabilizer.py:325-337).
  * Per segment: stable sort by key, in-order segmented sum, keep |sum| >= eps,

@@ -79,7 +79,8 @@ SIGNATURES = {
     "qx_program_create": (C.c_int, [C.c_int, _i32, _i32, _p, _p, _p, _p, _p, _p, _p, _P(_p)]),
     "qx_program_destroy": (C.c_int, [_p]),
     "qx_program_rows": (C.c_int, [_p, _P(_i32)]),
-    "qx_store_run_program": (C.c_int, [_p, _p, _p, _f64, _p, _P(_i64), _P(_i32), _p, _p, _p, _i64, _P(_i32), _P(_f64)]),
+    "qx_store_run_program": (C.c_int, [_p, _p, _p, _f64, _p, _P(_i64), _P(_i32), _p, _p, _p, _i64, _P(_i32), _P(_f64),
+                                       _i32, _P(_i32)]),
     "qx_merge": (C.c_int, [_p, _f64, _p]),
     "qx_sort": (C.c_int, [_p]),
     "qx_store_zi_sums": (C.c_int, [_p, _p]),

@@ -1163,7 +1163,8 @@ extern "C" int qx_program_rows(const qx_program* p, int32_t* rows) {
 extern "C" int qx_store_run_program(qx_store* s, const qx_program* p, const int32_t* init_qubits, double eps,
                                     int64_t* ranks, int64_t* raw_total, int32_t* fitted, int64_t* offsets,
                                     uint64_t* host_keys, double* host_lambdas, int64_t host_cap,
-                                    int32_t* host_filled, double* device_ms) {
+                                    int32_t* host_filled, double* device_ms, int32_t max_steps,
+                                    int32_t* stopped_step) {
   QX_REQUIRE(s && p && fitted, "NULL argument");
   QX_NARROW_ONLY(s, "qx_store_run_program");
   QX_REQUIRE(p->n_qubits == s->n_qubits && p->device == s->device, "program was compiled for n=%d on device %d",
@@ -1173,6 +1174,10 @@ extern "C" int qx_store_run_program(qx_store* s, const qx_program* p, const int3
   QX_REQUIRE((host_keys == nullptr) == (host_lambdas == nullptr), "host_keys and host_lambdas go together");
   *fitted = 0;
   if (host_filled) *host_filled = 0;
+  if (stopped_step) *stopped_step = 0;
+  QX_REQUIRE(max_steps >= 0 && max_steps <= p->n_steps, "max_steps %d out of range (program has %d steps)", max_steps,
+             p->n_steps);
+  const int run_steps = max_steps > 0 ? max_steps : p->n_steps;
   static const bool off = getenv("QX_NO_PROGRAM") != nullptr;
   if (off || s->n_seg < 1) return QX_OK;
   PgInit init;
@@ -1235,11 +1240,11 @@ extern "C" int qx_store_run_program(qx_store* s, const qx_program* p, const int3
       QxProfileScope prof(QX_K_SMALL_MERGE, s->stream, 32.0 * (double)std::max<int64_t>(s->ub_total, s->n_seg));
       if (variant == 0)
         k_small_circuit<PgSmemSmall><<<s->n_seg, kPgThreads, sizeof(PgSmemSmall), s->stream>>>(
-            s->keys[in], s->lam[in], s->seg[in], s->n_seg, p->d_steps, p->n_steps, s->keys[out], s->lam[out],
+            s->keys[in], s->lam[in], s->seg[in], s->n_seg, p->d_steps, run_steps, s->keys[out], s->lam[out],
             s->seg[out], status, eps, init, host);
       else
         k_small_circuit<PgSmem><<<s->n_seg, kPgThreads, sizeof(PgSmem), s->stream>>>(
-            s->keys[in], s->lam[in], s->seg[in], s->n_seg, p->d_steps, p->n_steps, s->keys[out], s->lam[out],
+            s->keys[in], s->lam[in], s->seg[in], s->n_seg, p->d_steps, run_steps, s->keys[out], s->lam[out],
             s->seg[out], status, eps, init, host);
       QX_CUDA(cudaGetLastError());
     }
@@ -1254,6 +1259,13 @@ extern "C" int qx_store_run_program(qx_store* s, const qx_program* p, const int3
     if (!(flags & 1)) break;
   }
   if (flags & 1) {
+    if (stopped_step) {
+      // the first step some generator outgrew shared memory at: the steps in front of it fit
+      int64_t first = p->n_steps;
+      for (int g = 0; g < s->n_seg; ++g)
+        if (host.flags[g] & 1) first = std::min<int64_t>(first, host.flags[g] >> 8);
+      *stopped_step = (int32_t)first;
+    }
     // did not fit: the live buffer is untouched -- unless there was none (init_qubits): make it
     if (init.on) return qx_store_init_z(s, init_qubits);
     return QX_OK;

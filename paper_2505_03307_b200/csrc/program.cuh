@@ -238,7 +238,7 @@ struct PgInit {
 // What the host reads, written by the kernel straight into page-locked host memory (UVA): no
 // read-back launch, no copy-engine round trip -- the stream synchronize is the only wait.
 struct PgHost {
-  int64_t* flags;              // [n_seg] bit 0: did not fit, bit 1: result did not fit the host buffers
+  int64_t* flags;              // [n_seg] bit 0: did not fit, bit 1: result did not fit the host buffers, bits 8..: the step that did not fit
   int64_t* raw;                // [n_seg] raw branches of the generator's branching steps
   int64_t* seg;                // [n_seg + 1] offsets of the result
   int64_t* ranks;              // [rows][n_seg]
@@ -263,6 +263,7 @@ k_small_circuit(const u64* __restrict__ keys_in, const double* __restrict__ lam_
   if (tid == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_start));
   int len;
   bool bad = false;
+  int bad_step = 0;                          // the step that did not fit (reported to the host)
   bool sorted = init.on != 0;                // the terms are in word order (a single Z word is)
   u64 raw_sum = 0;
   if (init.on) {
@@ -390,6 +391,7 @@ k_small_circuit(const u64* __restrict__ keys_in, const double* __restrict__ lam_
     u64 run = pg_block_exclusive_sum<u64>(mine, sm.scan, total);
     if (total > (u64)kRawCap) {
       bad = true;
+      bad_step = si;
       break;
     }
     for (int e = e0; e < e1; ++e) {
@@ -564,6 +566,7 @@ k_small_circuit(const u64* __restrict__ keys_in, const double* __restrict__ lam_
     if (tid == 0) host.ranks[(int64_t)st->rank_row * n_seg + g] = kept_before;
     if (kept_before > kSrcCap) {
       bad = true;
+      bad_step = si;
       break;
     }
     len = kept_before;
@@ -596,7 +599,7 @@ k_small_circuit(const u64* __restrict__ keys_in, const double* __restrict__ lam_
       seg_out[n_seg] = base + len;
       host.seg[n_seg] = base + len;
     }
-    host.flags[g] = (bad ? 1 : 0) | (to_host ? 0 : 2);
+    host.flags[g] = (bad ? 1 : 0) | (to_host ? 0 : 2) | ((int64_t)bad_step << 8);
     host.raw[g] = (int64_t)raw_sum;
     long long t_end;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_end));

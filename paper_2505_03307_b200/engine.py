@@ -32,7 +32,7 @@ import numpy as np
 
 from . import lut as _lut
 from .circuit import Instruction, divide_instruction
-from .errors import NumericalCollapseError, ResourceLimitError
+from .errors import ConsistencyError, NumericalCollapseError, ResourceLimitError
 from .stabilizer import (
     DEFAULT_EPS,
     DENSE_FLATTEN_BUDGET,
@@ -382,7 +382,7 @@ def run(instructions: Sequence[Instruction], n: int, mode, eps: float = DEFAULT_
 
         # One launch for the whole circuit while every generator stays small (csrc/program.cuh);
         # v2 only where its dense layout needs no term-dependent decision (stabilizer.py:264-286)
-        programmed, program_segs, made = False, None, initial is not None
+        programmed, program_segs, made, prefixed = False, None, initial is not None, 0
         if (not eager and n <= 32 and before_merge is None and reduce_ranks is None and slot_part is None
                 and _PROGRAMS_ON and ids and max(walker_ranks, default=0) <= PROGRAM_MAX_TERMS
                 and store._cx == _lut.STANDARD_CX
@@ -392,24 +392,37 @@ def run(instructions: Sequence[Instruction], n: int, mode, eps: float = DEFAULT_
                 plan.lut()
             program = _program_for(plan, instructions, n, mode, store.device)
             timings["lut"] = time.perf_counter() - t0
-            if program is not None:
+            if program is not None and program.fit_steps != 0:
                 # generators that start as Z words are made in the kernel (no upload); a run that
-                # does not fit leaves the store as init_z would have
+                # does not fit leaves the store as init_z would have.  fit_steps: what an earlier
+                # run of this plan found -- None: every step fits (or nothing is known yet), K > 0:
+                # some generator outgrows shared memory at step K, so only the first K steps are
+                # the one launch and the walk goes on step by step behind them
+                prefix = program.fit_steps or 0
+                whole = prefix == 0
                 t0 = time.perf_counter()
                 fitted, rows, _, program_segs = store.run_program(
-                    program, eps, init_qubits=None if made else ids, to_host=download, pinned=pinned)
+                    program, eps, init_qubits=None if made else ids, to_host=download and whole, pinned=pinned,
+                    max_steps=prefix)
                 made = True
                 phase_key = "sub_flatten" if program.rows else "cx"
                 w.host_timings[phase_key] += time.perf_counter() - t0
-                if fitted:
+                if fitted and whole:
                     timings[phase_key] += store.program_ms * 1e-3      # the kernel's own clock (%globaltimer)
                     programmed = True
                     w.store, w.dry = _ReplayStore(rows, store.device), True
                     _walk_events(w, _program_events(plan, instructions, mode), mode, trace, counters)
                     w.store, w.dry = store, False
                     w.launch_log["program_steps"] = program.steps
+                elif fitted:
+                    timings[phase_key] += store.program_ms * 1e-3
+                    prefixed = prefix
+                    w.store = _PrefixStore(rows, prefix, store)
+                    w.launch_log["program_steps"] = prefix
                 else:
-                    plan._programs[(mode, store.device)] = None      # a generator outgrew it: step by step from now on
+                    # a generator outgrew it at this step: from the next run on only the steps in
+                    # front of it are the one launch (0: none fits, never tried again)
+                    program.fit_steps = min(store.program_stopped, prefix) if prefix else store.program_stopped
         if not made:
             store.init_z(ids)
         if programmed:
@@ -429,6 +442,12 @@ def run(instructions: Sequence[Instruction], n: int, mode, eps: float = DEFAULT_
             else:
                 _replay_operators(plan.operator_events(), w, trace, counters, mode)
 
+        if prefixed:
+            # the walk has passed the steps the launch did: they come first, and the step that did
+            # not fit -- a branching operator -- is the earliest the tail below can still owe
+            if w.store.seen != prefixed:
+                raise ConsistencyError(f"one-launch prefix of {prefixed} steps, the walk consumed {w.store.seen}")
+            w.store = store
         streamed = None
         partitioned = None
         if programmed:
@@ -579,6 +598,45 @@ class _ReplayStore:
         row = self.rows[self.next]
         self.next += 1
         return 0, list(row)
+
+
+class _PrefixStore:
+    """The store of a run whose first ``done`` device steps were ONE launch (a circuit whose
+    generators outgrow shared memory later): those steps hand out the recorded ranks, everything
+    behind them goes to the real store.  Steps are counted exactly as _RecordingStore records them."""
+
+    def __init__(self, rows, done: int, real):
+        self.rows, self.done, self.real = rows, done, real
+        self.seen = self.next = 0
+
+    def apply_clifford(self, program):
+        if not len(program):
+            return
+        if self.seen < self.done:
+            self.seen += 1
+        else:
+            self.real.apply_clifford(program)
+
+    def order_for_operator(self, counts, by_key: bool = True):
+        if self.seen >= self.done:           # otherwise part of the recorded operator step
+            self.real.order_for_operator(counts, by_key)
+
+    def apply_operator_run(self, counts, axes, weights, program, eps, term_limit: int = 0):
+        if self.seen < self.done:
+            self.seen += 1
+            row = self.rows[self.next]
+            self.next += 1
+            return 0, list(row)
+        return self.real.apply_operator_run(counts, axes, weights, program, eps, term_limit)
+
+    def sort(self):
+        if self.seen < self.done:
+            self.seen += 1
+        else:
+            self.real.sort()
+
+    def __getattr__(self, name):
+        return getattr(self.real, name)
 
 
 class _NoProgram(Exception):

@@ -300,13 +300,13 @@ class DeviceStore:
         return ranks.tolist(), bool(flag.value)
 
     def run_program(self, program: "CircuitProgram", eps: float, init_qubits=None, to_host: bool = False,
-                    pinned: bool = False):
+                    pinned: bool = False, max_steps: int = 0):
         """The whole compiled circuit in one launch (qx_store_run_program).  Returns (fitted, ranks,
         raw, segments): ranks[row][g] after the row-th branching step; fitted False = the store is
         untouched (or holds init_z if init_qubits was given).  init_qubits: start from Z words made in
         the kernel instead of the store's content.  to_host: the kernel also writes the result into
         page-locked host memory; segments = [(lambdas, keys)] then (views of the pinned block if
-        ``pinned``, fresh arrays otherwise), else None."""
+        ``pinned``, fresh arrays otherwise), else None.  max_steps > 0: only the first max_steps steps."""
         ranks = np.zeros((max(program.rows, 1), self.n_segments), dtype=np.int64)
         raw, fitted, filled = C.c_int64(), C.c_int32(), C.c_int32()
         off = np.zeros(self.n_segments + 1, dtype=np.int64)
@@ -318,11 +318,12 @@ class DeviceStore:
             buf = nat.PINNED.take(16 * cap)
             keys = buf.view(np.uint64, 0, cap)
             lam = buf.view(np.float64, 8 * cap, cap)
-        dev_ms = C.c_double()
+        dev_ms, stopped = C.c_double(), C.c_int32()
         nat.check(nat.lib().qx_store_run_program(self._h, program.handle, nat.ptr(init), float(eps), nat.ptr(ranks),
                                                  C.byref(raw), C.byref(fitted), nat.ptr(off), nat.ptr(keys), nat.ptr(lam),
-                                                 cap, C.byref(filled), C.byref(dev_ms)))
+                                                 cap, C.byref(filled), C.byref(dev_ms), int(max_steps), C.byref(stopped)))
         self.program_ms = dev_ms.value         # duration of the launch on the GPU's clock
+        self.program_stopped = stopped.value   # not fitted: the first step that outgrew shared memory
         segs = None
         if fitted.value and filled.value:
             o = off.tolist()
@@ -408,6 +409,7 @@ class CircuitProgram:
         off = np.asarray(off, dtype=np.int64)
         self.rows = int((kinds == 1).sum())
         self.steps = ns
+        self.fit_steps = None         # None: all steps fit one launch (as far as known); K: only the first K do
         self._h = C.c_void_p()
         nat.check(nat.lib().qx_program_create(self.device, self.n, ns, nat.ptr(kinds), nat.ptr(order), nat.ptr(counts),
                                               nat.ptr(axes), nat.ptr(weights), nat.ptr(ops) if len(ops) else None,

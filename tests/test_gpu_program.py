@@ -110,16 +110,38 @@ def test_collapse_message_matches_step_by_step():
     assert want is not None and msgs[1][2] == want
 
 
-def test_too_large_a_circuit_falls_back_and_remembers():
-    n, gates = 8, qx.gen_xyz_chain(8, 2, 1, rng=4)        # 3**8 branches per term: no program fits
+@pytest.mark.parametrize("mode", ["v1", "v3"])
+def test_a_circuit_that_outgrows_shared_memory_starts_with_one_launch(mode):
+    """xyz_chain(8,2): the first operator steps fit one launch, a later one does not.  The first run
+    finds that out (and replays everything step by step); from the second run on the steps in
+    front are ONE launch and the walk goes on step by step behind them.  All three runs and the
+    run without programs agree bit for bit."""
+    n, gates = 8, qx.gen_xyz_chain(8, 2, 1, rng=4)
     engine.clear_plans()
-    a = qx.run(gates, n, "v3")
-    assert "program_steps" not in a.device
-    plan = engine._plan_for(gates, n, engine.Mode.V3)
-    assert plan._programs[(engine.Mode.V3, a.device["device"])] is None
-    want = oracle.run(gates, n, "v3")
-    assert a.rank_trace == want["rank_trace"]
-    for (lam, keys), (wl, wk) in zip(report_gens(a), want["final"]):
+    first = qx.run(gates, n, mode)
+    assert "program_steps" not in first.device
+    plan = engine._plan_for(gates, n, engine.Mode.coerce(mode))
+    program = plan._programs[(engine.Mode.coerce(mode), first.device["device"])]
+    assert program is not None and 0 < program.fit_steps < program.steps
+    before = _native.launch_count()
+    second = qx.run(gates, n, mode)
+    launches_prefixed = _native.launch_count() - before
+    assert second.device["program_steps"] == program.fit_steps
+    third = qx.run(gates, n, mode)
+    engine._PROGRAMS_ON = False
+    try:
+        engine.clear_plans()
+        before = _native.launch_count()
+        plain = qx.run(gates, n, mode)
+        launches_plain = _native.launch_count() - before
+    finally:
+        engine._PROGRAMS_ON = True
+    assert launches_prefixed < launches_plain
+    for rep in (first, second, third):
+        _same(rep, plain)
+    want = oracle.run(gates, n, mode)
+    assert second.rank_trace == want["rank_trace"]
+    for (lam, keys), (wl, wk) in zip(report_gens(second), want["final"]):
         assert np.array_equal(keys, wk) and np.max(np.abs(lam - wl)) < 1e-10
 
 
