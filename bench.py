@@ -391,6 +391,20 @@ def run_ours(args):
                 "classes": {k: {"ms": round(v["ms"], 4), "launches": v["launches"],
                                 "gbs": round(v["alg_bytes"] / max(v["ms"], 1e-9) / 1e6, 1)}
                             for k, v in busy.items()}}
+        # the whole step by SURVEY.md 8d's UNFUSED measure (B_term = 16): every step where ranks change
+        # counted as operator-apply 16 B x (N_in + N_raw) + merge 16 B x (N_raw + N_out), N_raw = what
+        # the step reports (output slots where the grouped step ran) -- the traffic separate
+        # expand / sort / reduce passes would need at the very least, over the measured step time
+        rep = step_resident()
+        trace = [sum(r) for r in rep.rank_trace]
+        n_in = sum(a for a, b in zip(trace, trace[1:]) if a != b)
+        n_out = sum(b for a, b in zip(trace, trace[1:]) if a != b)
+        raw = int(rep.device.get("raw_terms", 0))
+        step_bytes = 16.0 * (n_in + raw) + 16.0 * (raw + n_out)
+        step_gbs = step_bytes / (ms_per_step * 1e-3) / 1e9
+        roof["step"] = {"alg_bytes": step_bytes, "achieved": step_gbs, "frac": step_gbs / peak, "unit": "GB/s",
+                        "measure": "SURVEY 8d unfused: 16 B x (N_in + N_raw) + 16 B x (N_raw + N_out) per rank-changing "
+                                   "step, over ms_per_step", "raw_terms": raw}
         traffic_file = os.path.join(ROOT, "profiles", "traffic.json")
         if os.path.exists(traffic_file):
             with open(traffic_file) as fh:

@@ -235,7 +235,9 @@ class _Walker:
                 self.before_merge(self.store)
                 self.ranks = self.store.merge(self.eps)
             else:
-                _, self.ranks = self.store.apply_operator_run(counts, axes, weights, program, self.eps)
+                raw, self.ranks = self.store.apply_operator_run(counts, axes, weights, program, self.eps)
+                # raw branches of the step (slots where the grouped step ran: the raw list is never written)
+                self.launch_log["raw_terms"] = self.launch_log.get("raw_terms", 0) + int(raw)
             if self.reduce_ranks is not None:
                 self.ranks = self.reduce_ranks(self.ranks)
         self.unsorted = False
@@ -401,7 +403,7 @@ def run(instructions: Sequence[Instruction], n: int, mode, eps: float = DEFAULT_
                 prefix = program.fit_steps or 0
                 whole = prefix == 0
                 t0 = time.perf_counter()
-                fitted, rows, _, program_segs = store.run_program(
+                fitted, rows, program_raw, program_segs = store.run_program(
                     program, eps, init_qubits=None if made else ids, to_host=download and whole, pinned=pinned,
                     max_steps=prefix)
                 made = True
@@ -414,11 +416,13 @@ def run(instructions: Sequence[Instruction], n: int, mode, eps: float = DEFAULT_
                     _walk_events(w, _program_events(plan, instructions, mode), mode, trace, counters)
                     w.store, w.dry = store, False
                     w.launch_log["program_steps"] = program.steps
+                    w.launch_log["raw_terms"] = w.launch_log.get("raw_terms", 0) + int(program_raw)
                 elif fitted:
                     timings[phase_key] += store.program_ms * 1e-3
                     prefixed = prefix
                     w.store = _PrefixStore(rows, prefix, store)
                     w.launch_log["program_steps"] = prefix
+                    w.launch_log["raw_terms"] = w.launch_log.get("raw_terms", 0) + int(program_raw)
                 else:
                     # a generator outgrew it at this step: from the next run on only the steps in
                     # front of it are the one launch (0: none fits, never tried again)
