@@ -249,6 +249,43 @@ def run_reference(args, updates_per_gen):
 # ------------------------------------------------------------------------------------------
 # GPU arm
 # ------------------------------------------------------------------------------------------
+def gate_kernel_rooflines(device, peak, terms=60_000_000, n=16):
+    """GB/s by algorithmic bytes of the v1 kernels on one generator of `terms` distinct
+    random terms: {class: {"ms", "launches", "gbs", "frac"}} from CUDA events around every launch."""
+    from paper_2505_03307_b200 import _native as nat, lut
+    from paper_2505_03307_b200.stabilizer import split_tables
+    from paper_2505_03307_b200.store import DeviceStore
+
+    # distinct pseudo-random words: an odd multiplier is a bijection on 32-bit words
+    keys = (np.arange(terms, dtype=np.uint64) * np.uint64(2654435761)) & np.uint64(4 ** n - 1)
+    lam = np.random.default_rng(3).uniform(-1, 1, size=terms)
+    prog = [lut.cx_op(n, q, q + 1) for q in range(n - 1)] + [lut.perm_op(n, q, lut.FIXED_PERMS["H"]) for q in range(0, n, 3)]
+    prog = np.array(prog, dtype=lut.op_dtype(n))
+    tabs = split_tables(lut.gate_branch_block("RZ", 0.7))
+    for rep in range(3):
+        with DeviceStore(n, 1, 2 * terms + 16, device) as st:
+            st.upload([(lam, keys)])
+            st.synchronize()
+            if rep == 1:
+                nat.profile_enable(True)
+                nat.profile_reset()
+            st.apply_clifford(prog)
+            st.sort()
+            st.apply_split(n // 2, *tabs)
+            st.merge(1e-12)
+            st.synchronize()
+    prof = nat.profile_read()
+    nat.profile_enable(False)
+    out = {"terms": terms, "qubits": n}
+    for k, v in prof.items():
+        if v["launches"]:
+            gbs = v["alg_bytes"] / max(v["ms"], 1e-9) / 1e6
+            out[k] = {"ms": round(v["ms"] / v["launches"], 4), "launches": v["launches"], "gbs": round(gbs, 1),
+                      "frac": round(gbs / peak, 3)}
+    return out
+
+
+
 def count_updates_gpu(name, device, instance=0):
     """v1-defined update count per generator, measured with the GPU's own v1 mode (untimed)."""
     import paper_2505_03307_b200 as qx
@@ -410,6 +447,12 @@ def run_ours(args):
             with open(traffic_file) as fh:
                 roof["traffic"] = json.load(fh).get(dom)
 
+    # ---- the gate-by-gate (v1) kernels of north-star subsystems (2) and (3) at scale, measured live:
+    # one generator of 6e7 random terms through a 21-op Clifford run (bit-sliced kernel), a re-sort
+    # (radix passes), an RZ split and the merge behind it (passes + segmented reduce)
+    if roof is not None and world == 1 and not args.no_gate_kernels:
+        roof["gate_kernels"] = gate_kernel_rooflines(device, peak)
+
     if rank != 0:
         if dist is not None:
             dist.destroy_process_group()
@@ -454,6 +497,7 @@ def main():
     ap.add_argument("--workload", default=DEFAULT_WORKLOAD)
     ap.add_argument("--mode", default="v3")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    ap.add_argument("--no-gate-kernels", action="store_true", help="skip the live roofline of the v1 gate kernels")
     ap.add_argument("--ref-full", action="store_true",
                     help="--impl reference: also run the WHOLE circuit once on the host (all generators)")
     ap.add_argument("--scaling", default="strong", choices=("weak", "strong"),

@@ -283,7 +283,10 @@ k_tile_fat(const BGroup<K>* __restrict__ groups, const TileDesc<K>* __restrict__
   fat[i] = f;
 }
 
-constexpr int kTrip = 3;                     // tiles whose slots a thread keeps in registers
+#ifndef QX_BUCKET_TRIP
+#define QX_BUCKET_TRIP 3
+#endif
+constexpr int kTrip = QX_BUCKET_TRIP;        // tiles whose slots a thread keeps in registers
 constexpr int kHeld = kTrip * kBRows;        // 9
 
 template <typename K>

@@ -20,7 +20,7 @@ def wrap(obj, attr, label=None):
     setattr(obj, attr, timed)
 
 for m in ("__init__", "init_z", "apply_clifford", "apply_split", "apply_operator", "apply_operator_run",
-          "count_operator", "merge", "sort", "ranks", "synchronize"):
+          "count_operator", "merge", "sort", "ranks", "synchronize", "run_program", "order_for_operator", "close"):
     if hasattr(store_mod.DeviceStore, m):
         wrap(store_mod.DeviceStore, m)
 wrap(lut_mod, "build_lut")
