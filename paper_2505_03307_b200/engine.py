@@ -412,9 +412,29 @@ def run(instructions: Sequence[Instruction], n: int, mode, eps: float = DEFAULT_
                 if fitted and whole:
                     timings[phase_key] += store.program_ms * 1e-3      # the kernel's own clock (%globaltimer)
                     programmed = True
-                    w.store, w.dry = _ReplayStore(rows, store.device), True
-                    _walk_events(w, _program_events(plan, instructions, mode), mode, trace, counters)
-                    w.store, w.dry = store, False
+                    # the bookkeeping is a pure function of the plan's events and the recorded ranks:
+                    # a run that recorded the ranks of the plan's previous run (the usual case: same
+                    # circuit again) takes that run's trace, counters and update counts as they are
+                    memo_key = (mode, tuple(walker_ranks))
+                    memo = plan._replays.get(memo_key)
+                    if memo is not None and memo[0] == rows:
+                        _, tail, counter_delta, log_after, updates, last_ranks = memo
+                        trace.extend([r.copy() for r in tail])
+                        for k, v in counter_delta.items():
+                            counters[k] = counters.get(k, 0) + v
+                        w.launch_log.update(log_after)
+                        w.updates = None if updates is None else updates.copy()
+                        w.ranks = list(last_ranks)
+                    else:
+                        n0, c0 = len(trace), dict(counters)
+                        w.store, w.dry = _ReplayStore(rows, store.device), True
+                        _walk_events(w, _program_events(plan, instructions, mode), mode, trace, counters)
+                        w.store, w.dry = store, False
+                        w.book_gates()
+                        plan._replays[memo_key] = (
+                            rows, [r.copy() for r in trace[n0:]],
+                            {k: v - c0.get(k, 0) for k, v in counters.items() if v != c0.get(k, 0)},
+                            dict(w.launch_log), None if w.updates is None else w.updates.copy(), list(w.ranks))
                     w.launch_log["program_steps"] = program.steps
                     w.launch_log["raw_terms"] = w.launch_log.get("raw_terms", 0) + int(program_raw)
                 elif fitted:
@@ -518,6 +538,7 @@ class _Plan:
         self._v1 = None
         self._ops = None
         self._programs = {}            # (mode, device) -> CircuitProgram | None (does not qualify / did not fit)
+        self._replays = {}             # (mode, initial ranks) -> bookkeeping of the last one-launch run
 
     def matches(self, instructions, n: int) -> bool:
         mine = self.instructions
