@@ -1182,6 +1182,7 @@ extern "C" int qx_store_run_program(qx_store* s, const qx_program* p, const int3
   if (off || s->n_seg < 1) return QX_OK;
   PgInit init;
   memset(&init, 0, sizeof(init));
+  init.n_qubits = s->n_qubits;
   if (init_qubits) {
     QX_REQUIRE(s->n_seg <= QX_MAX_QUBITS, "init_qubits: at most %d generators", QX_MAX_QUBITS);
     init.on = 1;

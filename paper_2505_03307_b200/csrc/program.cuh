@@ -130,9 +130,116 @@ __device__ __forceinline__ void pg_cmpxchg_batch(SM& sm, int t0, int stride, int
   }
 }
 
+// Stable LSD radix sort of the first `count` pairs (rkey[e], ridx[e] == e) for the large cases: the
+// bitonic network does m/2 * log2(m) * (log2(m) + 1) / 2 compare-exchanges (3.7e5 at 8192 elements,
+// 37 us on one SM), a byte-wise LSD pass touches every element twice and only the bytes that differ
+// need a pass.  Only the 16-bit indices move between the passes (keys are read through them); the
+// keys are brought into the sorted order once at the end, so the state left behind is the
+// network's: rkey ascending, ridx = where each pair came from, ties in input order (LSD is stable).
+// A pass: every warp owns a contiguous block of the list and walks it 32 elements at a time --
+// MATCH.ANY gives each element its rank among the equal digits of its round, the round's leader of
+// a digit bumps the warp's private count -- then the counts are scanned over (digit, warp) and a
+// second walk scatters.  `scratch`: 64 KB that is dead during the sort (the generator's own arrays
+// while its raw list is sorted, the raw coefficients while its terms are).
 template <typename SM>
-__device__ __noinline__ void pg_sort_pairs(SM& sm, int m) {
+__device__ __noinline__ void pg_radix_sort(SM& sm, int count, void* scratch, int key_bits) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  unsigned short* idx2 = reinterpret_cast<unsigned short*>(scratch);               // count
+  unsigned short* off = idx2 + SM::kRawCap;                                        // count
+  u32* whist = reinterpret_cast<u32*>(off + SM::kRawCap);                          // [kPgWarps][256]
+  u32* flag = whist + kPgWarps * 256;
+  const int per_warp = ((count + kPgWarps - 1) / kPgWarps + 31) & ~31;
+  const int w_lo = warp * per_warp, w_hi = min(count, w_lo + per_warp);
+  unsigned short* cur = sm.ridx;
+  unsigned short* nxt = idx2;
+  for (int shift = 0; shift < key_bits; shift += 8) {
+    for (int i = tid; i < kPgWarps * 256; i += kPgThreads) whist[i] = 0u;
+    if (tid == 0) *flag = 0u;
+    __syncthreads();
+    u32* mine = whist + warp * 256;
+    for (int e0 = w_lo; e0 < w_hi; e0 += 32) {
+      const int e = e0 + lane;
+      const bool valid = e < w_hi;
+      const u32 d = valid ? (u32)(sm.rkey[cur[e]] >> shift) & 255u : 256u + (u32)lane;
+      const u32 peers = __match_any_sync(QX_FULL_MASK, d);
+      const int leader = __ffs(peers) - 1;
+      u32 old = 0;
+      if (valid && lane == leader) {
+        old = mine[d];
+        mine[d] = old + __popc(peers);
+      }
+      old = __shfl_sync(QX_FULL_MASK, old, leader);
+      if (valid) off[e] = (unsigned short)(old + __popc(peers & lanemask_lt()));
+      __syncwarp();
+    }
+    __syncthreads();
+    // digit totals -> exclusive start of every (digit, warp) bin; a pass whose digit is the same
+    // for every element moves nothing and is skipped
+    u32 tot = 0;
+    if (tid < 256)
+      for (int w = 0; w < kPgWarps; ++w) tot += whist[w * 256 + tid];
+    if (tid < 256 && tot == (u32)count) *flag = 1u;
+    u32 total_all;
+    u32 run = pg_block_exclusive_sum<u32>(tid < 256 ? tot : 0u, sm.scan, total_all);
+    const bool skip = *flag != 0u;                // uniform: read behind the scan's barriers ...
+    __syncthreads();                              // ... and in front of the next pass, which clears it
+    if (skip) continue;
+    if (tid < 256) {
+      for (int w = 0; w < kPgWarps; ++w) {
+        const u32 c = whist[w * 256 + tid];
+        whist[w * 256 + tid] = run;
+        run += c;
+      }
+    }
+    __syncthreads();
+    for (int e0 = w_lo; e0 < w_hi; e0 += 32) {
+      const int e = e0 + lane;
+      if (e < w_hi) {
+        const unsigned short from = cur[e];
+        const u32 d = (u32)(sm.rkey[from] >> shift) & 255u;
+        nxt[mine[d] + off[e]] = from;
+      }
+    }
+    __syncthreads();
+    unsigned short* t = cur;
+    cur = nxt;
+    nxt = t;
+  }
+  // keys into the sorted order through the scratch block, indices into their home
+  u64* tmp = reinterpret_cast<u64*>(scratch);
+  if (cur != sm.ridx) {
+    // the scratch block is about to hold the keys: move the indices first
+    unsigned short hold[(SM::kRawCap + kPgThreads - 1) / kPgThreads];
+#pragma unroll
+    for (int i = 0; i < (SM::kRawCap + kPgThreads - 1) / kPgThreads; ++i) {
+      const int e = tid + i * kPgThreads;
+      hold[i] = e < count ? cur[e] : (unsigned short)0;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int i = 0; i < (SM::kRawCap + kPgThreads - 1) / kPgThreads; ++i) {
+      const int e = tid + i * kPgThreads;
+      if (e < count) sm.ridx[e] = hold[i];
+    }
+    __syncthreads();
+  }
+  for (int e = tid; e < count; e += kPgThreads) tmp[e] = sm.rkey[sm.ridx[e]];
+  __syncthreads();
+  for (int e = tid; e < count; e += kPgThreads) sm.rkey[e] = tmp[e];
+  __syncthreads();
+}
+
+// count: the real pairs (the rest up to m, a power of two, is padding that sorts last);
+// scratch / key_bits: see pg_radix_sort (scratch may be NULL: network only)
+template <typename SM>
+__device__ __noinline__ void pg_sort_pairs(SM& sm, int m, int count, void* scratch, int key_bits) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if constexpr (SM::kRawCap >= 8192) {
+    if (m >= 1024 && scratch != nullptr) {
+      pg_radix_sort(sm, count, scratch, key_bits);
+      return;
+    }
+  }
   if (m <= 128) {
     // a handful of terms (configs 1, 2, 3 never leave this branch): every element counts the
     // elements in front of it -- m broadcast reads, two barriers, no network.  Callers hand the
@@ -199,7 +306,7 @@ __device__ __forceinline__ void pg_gather_terms(SM& sm, int len, bool take_keys)
 
 // canonical order of the generator's terms (keys are unique)
 template <typename SM>
-__device__ __forceinline__ void pg_sort_terms(SM& sm, int len) {
+__device__ __forceinline__ void pg_sort_terms(SM& sm, int len, int key_bits) {
   const int tid = threadIdx.x;
   int m = 32;
   while (m < len) m <<= 1;
@@ -208,7 +315,7 @@ __device__ __forceinline__ void pg_sort_terms(SM& sm, int len) {
     sm.ridx[e] = (unsigned short)e;
   }
   __syncthreads();
-  pg_sort_pairs(sm, m);
+  pg_sort_pairs(sm, m, len, sm.rlam, key_bits);        // the raw coefficients are dead here
   pg_gather_terms(sm, len, true);
 }
 
@@ -261,6 +368,7 @@ k_small_circuit(const u64* __restrict__ keys_in, const double* __restrict__ lam_
   const int tid = threadIdx.x;
   long long t_start = 0;
   if (tid == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_start));
+  const int key_bits = 2 * init.n_qubits;    // bits of a word that can be set
   int len;
   bool bad = false;
   int bad_step = 0;                          // the step that did not fit (reported to the host)
@@ -315,7 +423,7 @@ k_small_circuit(const u64* __restrict__ keys_in, const double* __restrict__ lam_
     const PgStep* st = &sm.st;
     const int kind = st->kind;
     if (kind == PG_SORT) {
-      pg_sort_terms(sm, len);
+      pg_sort_terms(sm, len, key_bits);
       sorted = true;
       continue;
     }
@@ -333,7 +441,7 @@ k_small_circuit(const u64* __restrict__ keys_in, const double* __restrict__ lam_
     if (st->order && len >= 3 && len <= kPgOrdCap) {   // (the small variant never reaches the cap)
       // the reference's string order: pattern word (branch count minus one of every digit), then
       // word -- a stable sort by pattern of terms that are in word order
-      if (!sorted) pg_sort_terms(sm, len);
+      if (!sorted) pg_sort_terms(sm, len, key_bits);
       int m = 32;
       while (m < len) m <<= 1;
       for (int e = tid; e < m; e += kPgThreads) {
@@ -351,7 +459,7 @@ k_small_circuit(const u64* __restrict__ keys_in, const double* __restrict__ lam_
         sm.ridx[e] = (unsigned short)e;
       }
       __syncthreads();
-      pg_sort_pairs(sm, m);
+      pg_sort_pairs(sm, m, len, sm.rlam, key_bits);
       pg_gather_terms(sm, len, false);
     }
     // qubits on which the operator branches at all; on the others every cell has one output axis.
@@ -504,7 +612,7 @@ k_small_circuit(const u64* __restrict__ keys_in, const double* __restrict__ lam_
     }
     __syncthreads();
     // bitonic network on (key, raw position): equal keys stay in raw order, padding ends up last
-    pg_sort_pairs(sm, m);
+    pg_sort_pairs(sm, m, raw, sm.ckey, key_bits);        // the sources are dead: ckey + clam are one 64 KB block
     // run sums (sequential, raw order), drop rule, ordered compaction into the generator's own
     // arrays: kept flags of all rows first (one table of per-warp counts, scanned once), then the
     // sums again for the kept heads -- duplicates are rare, two barriers instead of one per row
