@@ -431,24 +431,23 @@ k_bucket_emit(const TileFat<K>* __restrict__ fat, const double* __restrict__ phi
     if (slow && pending) flush_pending();         // parking needs the staging area
     u32 parked = 0;
     double held[kHeld];
-    u32 held_y[kHeld];
+    // low key bits of the held slots, two per register (ELL <= 16)
+    u32 held_y[(kHeld + 1) / 2];
+    auto put_y = [&](int i, u32 y) {               // i is a compile-time constant where this is called
+      if (i & 1) held_y[i >> 1] = (held_y[i >> 1] & 0xffffu) | (y << 16);
+      else held_y[i >> 1] = (held_y[i >> 1] & 0xffff0000u) | y;
+    };
+    auto get_y = [&](int i) -> u32 { return (i & 1) ? held_y[i >> 1] >> 16 : held_y[i >> 1] & 0xffffu; };
 
     for (u32 t0 = t_begin; t0 < t_end; t0 += kTrip) {
 #pragma unroll
       for (int k = 0; k < kHeld; ++k) held[k] = 0.0;
-      u32 park_at[kTrip];
-      u32 park_lw[kTrip];
-      u32 live_all = 0;                           // bit t * kBRows + k: that slot of mine exists
 #pragma unroll
       for (int t = 0; t < kTrip; ++t) {
-        park_at[t] = parked;
-        park_lw[t] = 1;
         if (t0 + t >= t_end) continue;            // uniform
         const TileFat<K>* tfp = fat + (t0 + t);
         const uint4 geo = *reinterpret_cast<const uint4*>(tfp);
         const u32 Lw = geo.x, n_mid = geo.y, n_src = geo.z;
-        park_lw[t] = Lw;
-        parked += geo.w;
         const u32 ns2 = min(n_src, 2u);
         if (Lw != geo_Lw) {                       // uniform
           geo_Lw = Lw;
@@ -547,7 +546,6 @@ k_bucket_emit(const TileFat<K>* __restrict__ fat, const double* __restrict__ phi
           for (int k = 0; k < kBRows; ++k)
             if (my_m0 + (u32)k * bpr < n_mid) live |= 1u << k;
         }
-        live_all |= live << (t * kBRows);
         double acc[kBRows];
 #pragma unroll
         for (int k = 0; k < kBRows; ++k) acc[k] = 0.0;
@@ -664,7 +662,7 @@ k_bucket_emit(const TileFat<K>* __restrict__ fat, const double* __restrict__ phi
               if (fabs(v) >= eps) {                              // eps > 0: a kept sum is never 0
                 atomicOr(&bitmap[y >> 5], 1u << (y & 31u));
                 held[t * kBRows + k] = v;
-                held_y[t * kBRows + k] = y;
+                put_y(t * kBRows + k, y);
               }
             }
           }
@@ -674,21 +672,28 @@ k_bucket_emit(const TileFat<K>* __restrict__ fat, const double* __restrict__ phi
       if (slow) {
         // park this triple in slot order (any order would do: ranks come from the bitmap); dropped
         // slots are parked as 0.0 so that nothing stale is taken for a kept sum later
+        // (the tiles' geometry is read again here, not carried through the sums in registers: the
+        // fast path -- buckets of at most kTrip tiles -- never needs it)
 #pragma unroll
         for (int t = 0; t < kTrip; ++t) {
-          const u32 Lw = park_lw[t];
+          if (t0 + t >= t_end) continue;          // uniform
+          const uint4 geo = *reinterpret_cast<const uint4*>(fat + (t0 + t));
+          const u32 Lw = geo.x, n_mid = geo.y;
           const u32 magic = 65536u / Lw + 1u;
           const u32 pb = ((u32)kBThreads * magic) >> 16;
           const u32 pm0 = ((u32)tid * magic) >> 16;
           const u32 pbl = (u32)tid - pm0 * Lw;
+          if ((u32)tid < pb * Lw) {
 #pragma unroll
-          for (int k = 0; k < kBRows; ++k) {
-            if (live_all & (1u << (t * kBRows + k))) {
-              const u32 at = park_at[t] + (pm0 + (u32)k * pb) * Lw + pbl;
-              st_key[at] = (unsigned short)held_y[t * kBRows + k];
-              st_lam[at] = held[t * kBRows + k];
+            for (int k = 0; k < kBRows; ++k) {
+              if (pm0 + (u32)k * pb < n_mid) {
+                const u32 at = parked + (pm0 + (u32)k * pb) * Lw + pbl;
+                st_key[at] = (unsigned short)get_y(t * kBRows + k);
+                st_lam[at] = held[t * kBRows + k];
+              }
             }
           }
+          parked += geo.w;
         }
       }
     }
@@ -754,7 +759,7 @@ k_bucket_emit(const TileFat<K>* __restrict__ fat, const double* __restrict__ phi
           for (int k = 0; k < kBRows; ++k) {
             const double v = held[t * kBRows + k];
             if (v != 0.0) {
-              const u32 y = held_y[t * kBRows + k];
+              const u32 y = get_y(t * kBRows + k);
               const u32 r = (u32)prefix[y >> 5] + __popc(bitmap[y >> 5] & ((1u << (y & 31u)) - 1u));
               st_key[r] = (unsigned short)y;
               st_lam[r] = v;
