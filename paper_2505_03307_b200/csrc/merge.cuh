@@ -433,13 +433,46 @@ template <typename K, typename V, int kRedThreads, int kRedItems>
 struct ReduceSmem {
   static constexpr int kRedTile = kRedThreads * kRedItems;
   static constexpr int kRedWarps = kRedThreads / 32;
-  V val[kRedTile];
-  K key[kRedTile + 2];         // [0] = key before the tile, [1..cnt] = tile
+  alignas(16) V val[kRedTile];
+  alignas(16) K key[kRedTile + 4];   // [kKeyAt - 1] = key before the tile, [kKeyAt ..] = tile (16-byte aligned: bulk copies)
   u32 opens[kRedTile / 32];    // bit j: tile slot j is the first term of a non-empty segment
   u64 scan[kRedWarps + 1];
   u64 base;
+  alignas(8) u64 mbar;         // completion of the tile's bulk copies
   int tile;
+  static constexpr int kKeyAt = 16 / (int)sizeof(K);   // 2 (64-bit keys) or 4 (32-bit keys)
 };
+
+// ---- TMA-style bulk copies (cp.async.bulk, sm_90+): a contiguous, 16-byte aligned block moves from
+// global to shared memory without passing through registers or the LSU's per-thread path; one
+// thread issues it, completion is counted in bytes on an mbarrier that every thread waits on.
+__device__ __forceinline__ u32 smem_addr(const void* p) { return (u32)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(u64* bar, u32 arrivals) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(bar)), "r"(arrivals));
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect(u64* bar, u32 bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void bulk_load(void* dst_smem, const void* src_global, u32 bytes, u64* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_addr(dst_smem)),
+               "l"(src_global), "r"(bytes), "r"(smem_addr(bar))
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(u64* bar, u32 parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "QX_MBAR_WAIT:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@p bra QX_MBAR_DONE;\n"
+      "bra QX_MBAR_WAIT;\n"
+      "QX_MBAR_DONE:\n"
+      "}\n" ::"r"(smem_addr(bar)),
+      "r"(parity)
+      : "memory");
+}
 
 // One pass over the sorted segments: a term is a head if it opens a segment or its key differs
 // from its predecessor's; the head sums its run sequentially (input order = np.add.at order),
@@ -475,11 +508,28 @@ k_reduce(const K* __restrict__ keys_in, const V* __restrict__ vals_in,
     }
   }
 
-  for (int j = threadIdx.x; j < cnt; j += kRedThreads) {
-    sm.key[1 + j] = ld_stream(keys_in + t0 + j);
-    sm.val[j] = ld_stream(vals_in + t0 + j);
+  constexpr int kKeyAt = ReduceSmem<K, V, kRedThreads, kRedItems>::kKeyAt;
+#ifndef QX_NO_BULK_COPY
+  // full tiles: two bulk copies (keys, coefficients) issued by one thread; the tile starts at a
+  // multiple of kRedTile terms, so both sides are 16-byte aligned.  The last, partial tile takes
+  // the per-thread loads.
+  const bool bulk = cnt == kRedTile;
+  if (bulk && threadIdx.x == 0) {
+    mbar_init(&sm.mbar, 1);
+    mbar_expect(&sm.mbar, (u32)(kRedTile * (sizeof(K) + sizeof(V))));
+    bulk_load(&sm.key[kKeyAt], keys_in + t0, (u32)(kRedTile * sizeof(K)), &sm.mbar);
+    bulk_load(&sm.val[0], vals_in + t0, (u32)(kRedTile * sizeof(V)), &sm.mbar);
   }
-  if (threadIdx.x == 0) sm.key[0] = t0 > 0 ? keys_in[t0 - 1] : (K)0;
+#else
+  const bool bulk = false;
+#endif
+  if (!bulk) {
+    for (int j = threadIdx.x; j < cnt; j += kRedThreads) {
+      sm.key[kKeyAt + j] = ld_stream(keys_in + t0 + j);
+      sm.val[j] = ld_stream(vals_in + t0 + j);
+    }
+  }
+  if (threadIdx.x == 0) sm.key[kKeyAt - 1] = t0 > 0 ? keys_in[t0 - 1] : (K)0;
   {   // segments that start inside this tile
     int lo = 0, hi = n_seg;                         // first g with seg_in[g] >= t0
     while (lo < hi) {
@@ -492,7 +542,8 @@ k_reduce(const K* __restrict__ keys_in, const V* __restrict__ vals_in,
       if (seg_in[g + 1] > at) atomicOr(&sm.opens[(at - t0) >> 5], 1u << ((at - t0) & 31));
     }
   }
-  __syncthreads();
+  __syncthreads();                                  // (also: the barrier's init is visible to the waiters)
+  if (bulk) mbar_wait(&sm.mbar, 0);
 
   // A kept head leaves its sum in sm.val[j] (no other thread's run contains a head) and its key
   // stays in sm.key: the write-out re-reads both, so only `pre` and the flags live across the
@@ -506,13 +557,13 @@ k_reduce(const K* __restrict__ keys_in, const V* __restrict__ vals_in,
     const int j = warp * (32 * kRedItems) + k * 32 + lane;
     bool kept = false;
     if (j < cnt) {
-      const K key = sm.key[1 + j];
+      const K key = sm.key[kKeyAt + j];
       const bool opens = (sm.opens[j >> 5] >> (j & 31)) & 1u;
       if (opens) flags |= 1u << (16 + k);
-      if (opens || sm.key[j] != key) {
+      if (opens || sm.key[kKeyAt - 1 + j] != key) {
         V s = sm.val[j];
         int e = j + 1;
-        while (e < cnt && sm.key[1 + e] == key && !((sm.opens[e >> 5] >> (e & 31)) & 1u)) {
+        while (e < cnt && sm.key[kKeyAt + e] == key && !((sm.opens[e >> 5] >> (e & 31)) & 1u)) {
           acc(s, sm.val[e]);
           ++e;
         }
@@ -545,7 +596,7 @@ k_reduce(const K* __restrict__ keys_in, const V* __restrict__ vals_in,
     const int64_t pos = base + pre[k];
     if (flags & (1u << k)) {
       const int j = warp * (32 * kRedItems) + k * 32 + lane;
-      st_stream(keys_out + pos, (u64)sm.key[1 + j]);
+      st_stream(keys_out + pos, (u64)sm.key[kKeyAt + j]);
       st_stream(vals_out + pos, sm.val[j]);
     }
     if (flags & (1u << (16 + k))) {
