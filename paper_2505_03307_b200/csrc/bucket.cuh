@@ -144,14 +144,68 @@ k_tile_desc(const BGroup<K>* __restrict__ groups, int ng, u64 n_tiles, const u64
   sort_val[t] = __longlong_as_double((long long)(t | ((u64)g.T << kTileIdBits)));
 }
 
+// ---- tile records of the bucket kernel -------------------------------------------------------------
+// Everything a CTA needs to start a tile, in sorted (bucket) order: one coalesced load per bucket
+// instead of the chain tile id -> descriptor -> group -> sources.  The first 16 bytes are what
+// every thread reads; the rest is for the threads that build the tile's tables.
+template <typename K>
+struct __align__(16) TileFat {
+  u32 Lw, n_mid, n_src, T;   // low branches, mid entries, sources, slots
+  K word;              // image of the high picks
+  K cw;                // class word of the group
+  K l_mask;            // its tile-local digits
+  u32 e;               // phase exponent of `word`
+  K key01[2];          // keys of the group's first two sources
+  u32 src0, pad;
+  u64 phi_at;          // index of the tile's first high product
+  double phi01[2];     // high products of the first two sources
+  u64 pad2;
+};
+
+struct __align__(16) UnitHdr {
+  u32 tile0, n_tiles;  // its tiles in sorted order
+  u64 top;             // (generator, top bits): the sort key of its tiles
+};
+
+// sorted tile i -> its self-contained record (done inside k_unit_scan: one launch less)
+template <typename K>
+__device__ __forceinline__ void make_tile_fat(const BGroup<K>* __restrict__ groups, const TileDesc<K>* __restrict__ desc,
+                                              const double* __restrict__ phi, const double* __restrict__ sort_val,
+                                              const u64* __restrict__ skey, u64 i, TileFat<K>* __restrict__ fat) {
+  const u64 tile = (u64)__double_as_longlong(sort_val[i]) & (((u64)1 << kTileIdBits) - 1);
+  const TileDesc<K> d = desc[tile];
+  const BGroup<K> g = groups[d.group];
+  TileFat<K> f;
+  f.word = d.word;
+  f.cw = g.cw;
+  f.l_mask = g.l_mask;
+  f.e = d.e;
+  f.src0 = g.src0;
+  f.pad = 0;
+  f.pad2 = 0;
+  f.n_src = g.n_src;
+  f.T = g.T;
+  f.Lw = g.Lw;
+  f.n_mid = g.n_mid;
+  f.phi_at = g.phi0 + (tile - g.tile0) * g.n_src;
+  f.key01[0] = (K)skey[g.src0];
+  f.phi01[0] = phi[f.phi_at];
+  f.key01[1] = g.n_src > 1 ? (K)skey[g.src0 + 1] : (K)0;
+  f.phi01[1] = g.n_src > 1 ? phi[f.phi_at + 1] : 0.0;
+  fat[i] = f;
+}
+
 // ---- buckets: heads of runs of equal (generator, top) among the sorted tiles ---------------------
 //   unit_tile0[u] = first sorted tile of bucket u        (unit_tile0[NU] = n_tiles)
 //   seg_first[g]  = first bucket of generator g          (untouched for a generator without slots)
 //   info[0] = NU, info[1] = largest bucket (slots)
+template <typename K>
 __global__ void __launch_bounds__(256)
 k_unit_scan(const u64* __restrict__ sort_key, const double* __restrict__ sort_val, u64 n_tiles, int top_bits,
             u32* __restrict__ unit_tile0, u32* __restrict__ seg_first, u64* __restrict__ status,
-            u64* __restrict__ info, u32* __restrict__ ticket) {
+            u64* __restrict__ info, u32* __restrict__ ticket, const BGroup<K>* __restrict__ groups,
+            const TileDesc<K>* __restrict__ desc, const double* __restrict__ phi, const u64* __restrict__ skey,
+            TileFat<K>* __restrict__ fat) {
   __shared__ u64 s_scan[kBWarps + 1];
   __shared__ u64 s_base;
   const int tile = qx_tile_id(ticket);
@@ -173,6 +227,7 @@ k_unit_scan(const u64* __restrict__ sort_key, const double* __restrict__ sort_va
     const u32 votes = __ballot_sync(QX_FULL_MASK, head);
     pre[k] = run + __popc(votes & lanemask_lt());
     run += __popc(votes);
+    if (i < n_tiles) make_tile_fat<K>(groups, desc, phi, sort_val, skey, i, fat);
   }
   u64 tot;
   u64 wex = block_exclusive_sum<u64>(lane == 0 ? (u64)run : 0ull, s_scan, tot);
@@ -228,59 +283,6 @@ __global__ void k_bucket_offsets(const u64* __restrict__ status, u32* __restrict
     u = min(max(u, u_lo), u_hi);
     seg_out[g] = u == u_lo ? 0 : (int64_t)(status[u - 1 - u_lo] & QX_LB_VAL);
   }
-}
-
-// ---- the bucket kernel ---------------------------------------------------------------------------
-// Everything a CTA needs to start a tile, in sorted (bucket) order: one coalesced load per bucket
-// instead of the chain tile id -> descriptor -> group -> sources.  The first 16 bytes are what
-// every thread reads; the rest is for the threads that build the tile's tables.
-template <typename K>
-struct __align__(16) TileFat {
-  u32 Lw, n_mid, n_src, T;   // low branches, mid entries, sources, slots
-  K word;              // image of the high picks
-  K cw;                // class word of the group
-  K l_mask;            // its tile-local digits
-  u32 e;               // phase exponent of `word`
-  K key01[2];          // keys of the group's first two sources
-  u32 src0, pad;
-  u64 phi_at;          // index of the tile's first high product
-  double phi01[2];     // high products of the first two sources
-  u64 pad2;
-};
-
-struct __align__(16) UnitHdr {
-  u32 tile0, n_tiles;  // its tiles in sorted order
-  u64 top;             // (generator, top bits): the sort key of its tiles
-};
-
-template <typename K>
-__global__ void __launch_bounds__(256)
-k_tile_fat(const BGroup<K>* __restrict__ groups, const TileDesc<K>* __restrict__ desc,
-           const double* __restrict__ phi, const double* __restrict__ sort_val, const u64* __restrict__ skey,
-           u64 n_tiles, TileFat<K>* __restrict__ fat) {
-  const u64 i = (u64)blockIdx.x * 256 + threadIdx.x;
-  if (i >= n_tiles) return;
-  const u64 tile = (u64)__double_as_longlong(sort_val[i]) & (((u64)1 << kTileIdBits) - 1);
-  const TileDesc<K> d = desc[tile];
-  const BGroup<K> g = groups[d.group];
-  TileFat<K> f;
-  f.word = d.word;
-  f.cw = g.cw;
-  f.l_mask = g.l_mask;
-  f.e = d.e;
-  f.src0 = g.src0;
-  f.pad = 0;
-  f.pad2 = 0;
-  f.n_src = g.n_src;
-  f.T = g.T;
-  f.Lw = g.Lw;
-  f.n_mid = g.n_mid;
-  f.phi_at = g.phi0 + (tile - g.tile0) * g.n_src;
-  f.key01[0] = (K)skey[g.src0];
-  f.phi01[0] = phi[f.phi_at];
-  f.key01[1] = g.n_src > 1 ? (K)skey[g.src0 + 1] : (K)0;
-  f.phi01[1] = g.n_src > 1 ? phi[f.phi_at + 1] : 0.0;
-  fat[i] = f;
 }
 
 #ifndef QX_BUCKET_TRIP
@@ -991,12 +993,10 @@ int bucket_step(qx_store* s, const OperatorTable& ct, const ImageTable<K>& im, i
     sorted = mb.cur;
   }
   {
-    QxProfileScope prof(QX_K_DENSE_PREP, s->stream, 20.0 * (double)n_tiles + (double)sizeof(TileFat<K>) * (double)n_tiles, 3);
-    k_tile_fat<K><<<(unsigned)((n_tiles + 255) / 256), 256, 0, s->stream>>>(d_groups, d_desc, d_phi, svals[sorted], skey,
-                                                                          n_tiles, d_fat);
-    QX_CUDA(cudaGetLastError());
-    k_unit_scan<<<(unsigned)scan_tiles, 256, 0, s->stream>>>(skeys[sorted], svals[sorted], n_tiles, top_bits,
-                                                            unit_tile0, seg_first, scan_status, info, ticket + 1);
+    QxProfileScope prof(QX_K_DENSE_PREP, s->stream, 20.0 * (double)n_tiles + (double)sizeof(TileFat<K>) * (double)n_tiles, 2);
+    k_unit_scan<K><<<(unsigned)scan_tiles, 256, 0, s->stream>>>(skeys[sorted], svals[sorted], n_tiles, top_bits,
+                                                               unit_tile0, seg_first, scan_status, info, ticket + 1,
+                                                               d_groups, d_desc, d_phi, skey, d_fat);
     QX_CUDA(cudaGetLastError());
     k_unit_sizes<<<(unsigned)std::max<int64_t>(1, std::min<int64_t>(((int64_t)n_tiles + 255) / 256, 1024)), 256, 0, s->stream>>>(
         unit_tile0, skeys[sorted], svals[sorted], reinterpret_cast<uint4*>(d_units), info);
@@ -1021,9 +1021,21 @@ int bucket_step(qx_store* s, const OperatorTable& ct, const ImageTable<K>& im, i
   const u32 u_lo = (u32)(n_units * part / parts), u_hi = (u32)(n_units * (part + 1) / parts);
   int per_sm = 0;
   auto launch = [&](auto kernel, auto* keys_out) -> int {
-    QX_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    QX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, kBThreads, smem));
-    per_sm = std::max(per_sm, 1);
+    // attribute + occupancy of (kernel, shared-memory size): asked once, the answers do not change
+    // (two driver calls on the critical path of every step otherwise: the GPU is idle behind the
+    // read-back of the bucket sizes)
+    static thread_local const void* cached_kernel = nullptr;
+    static thread_local size_t cached_smem = 0;
+    static thread_local int cached_per_sm = 0;
+    static thread_local int cached_device = -1;
+    if (cached_kernel != reinterpret_cast<const void*>(kernel) || cached_smem != smem || cached_device != s->device) {
+      QX_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      QX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&cached_per_sm, kernel, kBThreads, smem));
+      cached_kernel = reinterpret_cast<const void*>(kernel);
+      cached_smem = smem;
+      cached_device = s->device;
+    }
+    per_sm = std::max(cached_per_sm, 1);
     static const int cap_per_sm = getenv("QX_BUCKET_CTAS") ? atoi(getenv("QX_BUCKET_CTAS")) : 0;   // experiments
     if (cap_per_sm > 0) per_sm = std::min(per_sm, cap_per_sm);
     const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)u_hi - u_lo, (int64_t)s->sm_count * per_sm));

@@ -314,7 +314,9 @@ class DeviceStore:
         keys = lam = None
         cap = 0
         if to_host:
-            cap = self.n_segments * PROGRAM_TERMS
+            # room for every generator at the kernel's limit, but never more than 64 MB of pinned
+            # memory: a result that does not fit is downloaded the ordinary way
+            cap = min(self.n_segments * PROGRAM_TERMS, 1 << 22)
             buf = nat.PINNED.take(16 * cap)
             keys = buf.view(np.uint64, 0, cap)
             lam = buf.view(np.float64, 8 * cap, cap)
