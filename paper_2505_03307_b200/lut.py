@@ -196,6 +196,9 @@ def cx_lookup(c: int, t: int) -> tuple:
     return int(LUT_C[c, t]), int(LUT_T[c, t]), int(LUT_SIGN[c, t])
 
 
+_cx_words_for = [None, None]      # (bytes of the sign table the cached words were packed from, the words)
+
+
 def cx_device_words(sign_table=None) -> tuple:
     """The three CX tables packed for the kernel: 2 bits (axes) / 1 bit (sign) per entry.
 
@@ -203,6 +206,9 @@ def cx_device_words(sign_table=None) -> tuple:
     mutation check, tests/test_cli.py:198-203) and see parity fail.
     """
     sign = LUT_SIGN if sign_table is None else sign_table
+    stamp = sign.tobytes()                        # every store asks; the tables only change in mutation tests
+    if stamp == _cx_words_for[0]:
+        return _cx_words_for[1]
     wc = wt = ws = 0
     for dc in range(4):
         for dt in range(4):
@@ -210,6 +216,7 @@ def cx_device_words(sign_table=None) -> tuple:
             wc |= int(LUT_C[dc, dt]) << (2 * e)
             wt |= int(LUT_T[dc, dt]) << (2 * e)
             ws |= (1 if sign[dc, dt] < 0 else 0) << e
+    _cx_words_for[0], _cx_words_for[1] = stamp, (wc, wt, ws)
     return wc, wt, ws
 
 
