@@ -66,6 +66,9 @@ k_partition_select(const u64* __restrict__ keys_in, const double* __restrict__ l
   }
   __syncthreads();
   const int64_t base = (int64_t)(s_base + warp_excl);
+  // one segment search per warp instead of one per term (see k_split): almost no warp holds a boundary
+  const int g_warp = segment_of(seg_in, n_seg, min(wbase, total - 1));
+  const bool no_opens = seg_in[g_warp] < wbase && seg_in[g_warp + 1] >= wbase + 32 * kItems;
 #pragma unroll
   for (int k = 0; k < kItems; ++k) {
     const int64_t i = wbase + k * 32 + lane;
@@ -75,8 +78,10 @@ k_partition_select(const u64* __restrict__ keys_in, const double* __restrict__ l
       keys_out[placed + rel] = key[k];
       lam_out[placed + rel] = lam_in[i];
     }
-    const int g = segment_of(seg_in, n_seg, i);
-    if (seg_in[g] == i) open_offsets(seg_in, seg_pos, g, i, rel);
+    if (!no_opens) {
+      const int g = segment_of(seg_in, n_seg, i);
+      if (seg_in[g] == i) open_offsets(seg_in, seg_pos, g, i, rel);
+    }
   }
   if (tile == ntiles - 1 && threadIdx.x == 0) {
     const int64_t sel_total = (int64_t)(s_base + tile_total);
