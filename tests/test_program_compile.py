@@ -52,3 +52,49 @@ def test_replay_books_the_recorded_ranks():
     assert trace[0] == [1, 1] and trace[-1] == rows[-1]
     assert len(trace) == plan.partition.k + plan.partition.k_prime + 1     # reference tests/test_engine.py:77
     assert all(row is not None for row in trace)
+
+
+class _FakeStore:
+    """Counts what reaches the 'real' store behind a one-launch prefix."""
+
+    mark = None
+
+    def __init__(self, n_gen):
+        self.n_gen, self.calls = n_gen, []
+
+    def apply_clifford(self, program):
+        self.calls.append(("clifford", len(program)))
+
+    def order_for_operator(self, counts, by_key=True):
+        self.calls.append(("order",))
+
+    def apply_operator_run(self, counts, axes, weights, program, eps, term_limit=0):
+        self.calls.append(("oprun", len(program)))
+        return 7, [5] * self.n_gen
+
+    def sort(self):
+        self.calls.append(("sort",))
+
+
+def test_prefix_store_hands_out_recorded_ranks_then_forwards():
+    # three branching operators; the first two were one launch, the third goes to the real store
+    gates = [qx.Instruction("H", (0,)), qx.Instruction("RZ", (0,), 0.3), qx.Instruction("CX", (0, 1)),
+             qx.Instruction("RX", (1,), 0.7), qx.Instruction("CX", (1, 0)), qx.Instruction("RY", (0,), 1.1),
+             qx.Instruction("CX", (0, 1))]
+    n = 2
+    plan, steps = _steps(gates, n, "v3")
+    kinds = [s[0] for s in steps]
+    assert kinds.count("oprun") == 3
+    done = kinds.index("oprun", kinds.index("oprun") + 1) + 1          # everything up to the second operator step
+    rows = [[2, 1], [3, 2]]
+    fake = _FakeStore(n)
+    store = engine._PrefixStore(rows, done, fake)
+    w = engine._Walker(store, n, range(n), 1e-12, {"partition": 0.0, "lut": 0.0, "sub_flatten": 0.0, "cx": 0.0})
+    trace = [list(w.ranks)]
+    engine._walk_events(w, engine._program_events(plan, gates, engine.Mode.V3), engine.Mode.V3, trace,
+                        {"sub_flatten_ops": 0, "cx_applications": 0})
+    assert store.seen == done and store.next == 2
+    # only the third operator (with its source order) reached the real store
+    assert [c[0] for c in fake.calls] == ["order", "oprun"]
+    assert trace[-1] == [5, 5] and [2, 1] in trace and [3, 2] in trace
+    assert w.launch_log["raw_terms"] == 7
