@@ -1017,6 +1017,58 @@ extern "C" int qx_bucket_last(int64_t out[8]) {
   return QX_OK;
 }
 
+// ---- packed form behind the bucketed step (a store that is only downloaded next) ---------------
+// The bucketed step leaves canonical 64-bit keys.  What crosses PCIe for n <= 16 is the packed form
+// of the sort's last pass (merge.cuh): 16-bit low halves + per generator the first position of
+// every value of the high 16 bits.  One pass makes it from the sorted keys: 8 B read, 2 B written
+// per term; a term whose predecessor has another high half opens its bucket (positions are unique:
+// plain stores); the empty buckets are filled by the suffix-minimum kernel of the sort.  The halves
+// and the table go into the store's DEAD key buffer, which then becomes the live one.
+namespace {
+__global__ void __launch_bounds__(256)
+k_pack_keys(const u64* __restrict__ keys, const int64_t* __restrict__ seg, unsigned short* __restrict__ lows,
+            u32* __restrict__ bnd) {
+  const int g = blockIdx.y;
+  const int64_t lo = seg[g], hi = seg[g + 1];
+  u32* row = bnd + (size_t)g * (QX_PACK_BUCKETS + 1);
+  for (int64_t i = lo + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < hi; i += (int64_t)gridDim.x * blockDim.x) {
+    const u64 k = keys[i];
+    lows[i] = (unsigned short)k;
+    const u32 h = (u32)(k >> 16);
+    if (i == lo || (u32)(keys[i - 1] >> 16) != h) row[h] = (u32)(i - lo);
+  }
+}
+
+// *packed = false: the form does not apply (small result, a generator of 2^32 terms, no room)
+int pack_for_download(qx_store* s, int64_t total, int64_t ub_seg, bool* packed) {
+  *packed = false;
+  const int n_seg = s->n_seg;
+  const int64_t bnd_bytes = 4ll * n_seg * (QX_PACK_BUCKETS + 1);
+  const int64_t lo_bytes = (2 * total + 255) / 256 * 256;
+  if (s->n_qubits > 16 || total < 8ll * n_seg * QX_PACK_BUCKETS || ub_seg >= (1ll << 32) - 1 ||
+      lo_bytes + bnd_bytes > 8 * s->cap)
+    return QX_OK;
+  const int live = s->cur, dead = s->cur ^ 1;
+  unsigned short* lows = reinterpret_cast<unsigned short*>(s->keys[dead]);
+  u32* bnd = reinterpret_cast<u32*>(reinterpret_cast<char*>(s->keys[dead]) + lo_bytes);
+  QX_CUDA(cudaMemsetAsync(bnd, 0xff, (size_t)bnd_bytes, s->stream));
+  {
+    QxProfileScope prof(QX_K_DENSE_PREP, s->stream, 10.0 * (double)total, 2);
+    const unsigned gx = (unsigned)std::max<int64_t>(1, std::min<int64_t>((ub_seg + 255) / 256, (int64_t)s->sm_count * 4));
+    k_pack_keys<<<dim3(gx, (unsigned)n_seg), 256, 0, s->stream>>>(s->keys[live], s->seg[live], lows, bnd);
+    QX_CUDA(cudaGetLastError());
+    qxm::k_pack_bounds<<<n_seg, 1024, 0, s->stream>>>(bnd, s->seg[live]);
+    QX_CUDA(cudaGetLastError());
+  }
+  // the key buffers trade places: keys[cur] is the packed block now, next to the coefficients it belongs to
+  std::swap(s->keys[live], s->keys[dead]);
+  s->narrow_keys = true;
+  s->pack_bnd = bnd;
+  *packed = true;
+  return QX_OK;
+}
+}  // namespace
+
 // The large operator step.  On entry the store holds the merged input terms (exact offsets on
 // the host); on exit it holds the canonical result and exact offsets.  `nz` is the operator's
 // non-zero branch table (fill_table in branch.cu).
@@ -1103,7 +1155,7 @@ int qx_dense_operator_step(qx_store* s, const OperatorTable& nz, const uint32_t*
   }
   // slot offsets of the generators + totals -> host (sizes the output); the groups go along for
   // the planner of the bucketed step
-  const bool bucket_ok = bucket_enabled() && eps > 0.0 && s->want_narrow != 2;
+  const bool bucket_ok = bucket_enabled() && eps > 0.0;
   qxb::bucket_stats().cap = 0;
   u64* h_groups = nullptr;
   struct ReleasePinned {
@@ -1137,7 +1189,12 @@ int qx_dense_operator_step(qx_store* s, const OperatorTable& nz, const uint32_t*
     const u64* h_src = h_cw + (qxb::kNgCap + 1);
     const u64* h_slot = h_src + (qxb::kNgCap + 1);
     std::vector<int64_t> h_seg_slot(s->h_pinned, s->h_pinned + n_seg + 1);   // the step reuses h_pinned
-    const bool narrow_out = s->n_qubits <= 16 && s->want_narrow != 0;
+    // a store that is only downloaded next: 32-bit keys (want_narrow 1), or -- large results, form
+    // 2 -- 64-bit keys that are packed to 16-bit halves + bucket tables right behind the step
+    const int64_t bnd_room = 4ll * n_seg * (QX_PACK_BUCKETS + 1) + (2 * total + 255) / 256 * 256;
+    const bool will_pack = s->n_qubits <= 16 && s->want_narrow == 2 && total >= 8ll * n_seg * QX_PACK_BUCKETS &&
+                           ub_seg < (1ll << 32) - 1 && bnd_room <= 8 * s->cap;
+    const bool narrow_out = s->n_qubits <= 16 && s->want_narrow != 0 && !will_pack;
     bool handled = false;
     if (s->n_qubits <= 16) {
       ImageTable<u32> im;
@@ -1158,6 +1215,12 @@ int qx_dense_operator_step(qx_store* s, const OperatorTable& nz, const uint32_t*
       s->narrow_keys = narrow_out;
       s->pack_bnd = nullptr;
       QX_TRY(qx_store_refresh(s));                  // kept counts: exact offsets for the caller
+      if (will_pack) {
+        bool packed = false;
+        int64_t kept_max = 0;
+        for (int g = 0; g < n_seg; ++g) kept_max = std::max(kept_max, s->h_seg[g + 1] - s->h_seg[g]);
+        QX_TRY(pack_for_download(s, s->h_seg[n_seg], kept_max, &packed));
+      }
       return QX_OK;
     }
   }
