@@ -241,6 +241,11 @@ int qx_operator_classes(int32_t n_qubits, const int32_t* counts, const int32_t* 
  * bucket, slots, low key bits ranked inside a bucket, bucket capacity (0: the step did not
  * qualify and the grouped step + sort ran), CTAs per SM. */
 int qx_bucket_last(int64_t out[8]);
+/* Host-only: what the last grouped operator step of this process did (csrc/dense.cu).  out[0] =
+ * groups (-1: the group list was not brought to the host), out[1] = groups whose sums were formed
+ * mode by mode ahead of the slot kernel (k_group_kron: many sources on at most 8 digits),
+ * out[2] = slots of those groups, out[3] = their sources. */
+int qx_dense_last(int64_t out[4]);
 /* Host-only: switch the bucketed step on or off for this process (tests and A/B runs compare it
  * with the grouped step + sort; results are bit-identical).  Returns the previous setting (1/0).
  * QX_NO_BUCKET in the environment starts the process with it off. */

@@ -76,6 +76,7 @@ SIGNATURES = {
     "qx_operator_classes": (C.c_int, [_i32, _p, _p, _p, _p, _p, _p, _p]),
     "qx_bucket_last": (C.c_int, [_P(_i64)]),
     "qx_bucket_enable": (C.c_int, [_i32]),
+    "qx_dense_last": (C.c_int, [_P(_i64)]),
     "qx_program_create": (C.c_int, [C.c_int, _i32, _i32, _p, _p, _p, _p, _p, _p, _p, _P(_p)]),
     "qx_program_destroy": (C.c_int, [_p]),
     "qx_program_rows": (C.c_int, [_p, _P(_i32)]),
@@ -267,6 +268,13 @@ def launch_count() -> int:
 def bucket_enable(on: bool) -> bool:
     """Switch the bucketed operator step (csrc/bucket.cuh) on/off; returns the previous setting."""
     return bool(lib().qx_bucket_enable(1 if on else 0))
+
+
+def dense_last() -> dict:
+    """What the last grouped operator step did: groups, and how many had their sums formed mode by mode."""
+    out = (_i64 * 4)()
+    check(lib().qx_dense_last(out))
+    return dict(zip(("groups", "kron_groups", "kron_slots", "kron_sources"), (int(v) for v in out)))
 
 
 def bucket_last() -> dict:

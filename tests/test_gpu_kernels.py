@@ -9,7 +9,7 @@ pytestmark = pytest.mark.gpu
 
 from gpu_util import DeviceStore, merge_on_device, oracle, qx, random_terms  # noqa: E402
 
-from paper_2505_03307_b200 import lut  # noqa: E402
+from paper_2505_03307_b200 import _native, lut  # noqa: E402
 from paper_2505_03307_b200.stabilizer import SimpleGenerator, keys_to_indices  # noqa: E402
 
 TOL = 1e-10
@@ -255,6 +255,52 @@ def test_operator_run_equals_three_steps(n, terms, rot_qubits, n_ops, mix):
             assert np.max(np.abs(gl - wl)) < 1e-12
         else:
             assert np.array_equal(gl, wl)      # sign flips are exact, summation order unchanged
+
+
+@pytest.mark.parametrize("n,qubits,count,bucket", [
+    (8, list(range(8)), 4000, True), (8, list(range(8)), 4000, False),     # 32-bit keys, all digits
+    (9, [0, 2, 3, 5, 6, 7, 8], 2000, True),                              # seven digits, the rest identity or idle
+    (22, [1, 4, 5, 9, 13, 14, 20, 21], 5000, True),                      # 64-bit keys, digits spread over the word
+    (22, [1, 4, 5, 9, 13, 14, 20, 21], 5000, False),
+])
+def test_groups_summed_mode_by_mode(n, qubits, count, bucket):
+    """Groups with many sources on at most 8 digits have their sums formed one qubit at a time
+    ahead of the slot kernel (dense.cu k_group_kron): the same products as stabilizer.py:300-337,
+    associated per qubit instead of per source, so keys are the reference's and coefficients agree
+    to rounding (|sum| <= sum of |lambda| ~ 1e3 here, 1e-16 relative per operation)."""
+    rng = np.random.default_rng(n * 77 + count)
+    shift = np.uint64(2) * (np.uint64(n - 1) - np.array(qubits, dtype=np.uint64))
+    gens = []
+    for c, lowest in ((count, 1), (count // 3, 0), (3, 1)):       # lowest = 0: identities mixed in -> several groups
+        digits = rng.integers(lowest, 4, size=(c * 2, len(qubits))).astype(np.uint64)
+        keys = np.unique((digits << shift).sum(axis=1, dtype=np.uint64))[:c]
+        gens.append((rng.uniform(0.2, 1.0, size=len(keys)) * rng.choice([-1.0, 1.0], size=len(keys)), keys))
+    gates = [qx.Instruction(g, (int(j),), float(rng.uniform(0.3, 5.9))) for j in qubits for g in ("RX", "RY", "RZ")]
+    counts, axes, weights = lut.operator_tables(oracle.lut_blocks(oracle.partition(gates, n), n)[0])
+    prog = [lut.perm_op(n, int(qubits[0]), lut.FIXED_PERMS["H"]), lut.cx_op(n, int(qubits[0]), int(qubits[1]))]
+    with DeviceStore(n, len(gens), 0) as st:
+        st.upload(gens)
+        st.apply_operator(counts, axes, weights)
+        st.apply_clifford(prog)
+        want_ranks = st.merge(1e-12)
+        want = [(l.copy(), k.copy()) for l, k in st.segments()]
+    before = _native.bucket_enable(bucket)
+    try:
+        with DeviceStore(n, len(gens), 0) as st:
+            st.upload(gens)
+            _, ranks = st.apply_operator_run(counts, axes, weights, prog, 1e-12)
+            info, cap = _native.dense_last(), _native.bucket_last()["cap"]
+            got = [(l.copy(), k.copy()) for l, k in st.segments()]
+    finally:
+        _native.bucket_enable(before)
+    if bucket and cap > 0:
+        assert info["kron_groups"] == 0           # the bucketed step took it: its sums stay in source order
+    else:
+        assert info["kron_groups"] >= 1 and info["kron_sources"] >= count // 2, info
+    assert ranks == want_ranks
+    for (gl, gk), (wl, wk) in zip(got, want):
+        assert np.array_equal(gk, wk)
+        assert np.max(np.abs(gl - wl)) < 1e-11
 
 
 def test_operator_run_with_corrupted_cx_table_is_table_driven():
