@@ -954,6 +954,114 @@ k_group_kron(const u64* __restrict__ cw, const u64* __restrict__ skey, const dou
   }
 }
 
+// ---- the same contraction for groups on 9..12 digits: the tensor (3^w doubles, <= 4.3 MB) lives
+// in global memory (L2 resident), one launch per mode over all such groups (blockIdx.y = group).
+constexpr int kKronWideDigits = 12;
+
+template <typename K>
+__global__ void __launch_bounds__(256)
+k_kron_scatter(const u64* __restrict__ cw, const u64* __restrict__ skey, const double* __restrict__ slam,
+               const u64* __restrict__ gsrc, const int* __restrict__ flagged, const int64_t* __restrict__ toff,
+               double* __restrict__ tensor) {
+  const int g = flagged[blockIdx.y];
+  const int64_t s0 = (int64_t)gsrc[g], s1 = (int64_t)gsrc[g + 1];
+  const K cwg = (K)cw[s0];
+  int pos[kKronWideDigits];
+  int w = 0;
+  for (K m = KeyOps<K>::support(cwg); m; m &= m - 1) pos[w++] = KeyOps<K>::lowest(m);
+  double* t = tensor + toff[blockIdx.y];
+  for (int64_t sidx = s0 + (int64_t)blockIdx.x * 256 + threadIdx.x; sidx < s1; sidx += (int64_t)gridDim.x * 256) {
+    const K key = (K)skey[sidx];
+    int idx = 0, mul = 1;
+    for (int j = 0; j < w; ++j) {
+      idx += ((int)((key >> pos[j]) & 3u) - 1) * mul;
+      mul *= 3;
+    }
+    t[idx] = slam[sidx];
+  }
+}
+
+// mode `m` counted from the highest digit (qubit 0 side) of each group; groups with fewer digits copy
+template <typename K>
+__global__ void __launch_bounds__(256)
+k_kron_mode(const u64* __restrict__ cw, const u64* __restrict__ gsrc, const int* __restrict__ flagged,
+            const int64_t* __restrict__ toff, const double* __restrict__ src, double* __restrict__ dst, int m,
+            const __grid_constant__ OperatorTable tb) {
+  const int g = flagged[blockIdx.y];
+  const K cwg = (K)cw[gsrc[g]];
+  const K sup = KeyOps<K>::support(cwg);
+  const int w = (int)Plane<K>::popc(sup);
+  int size = 1;
+  for (int j = 0; j < w; ++j) size *= 3;
+  const int i = blockIdx.x * 256 + threadIdx.x;
+  if (i >= size) return;
+  const double* a = src + toff[blockIdx.y];
+  double* b = dst + toff[blockIdx.y];
+  if (m >= w) {
+    b[i] = a[i];
+    return;
+  }
+  const int j = w - 1 - m;
+  K rest = sup;
+  int stride = 1;
+  for (int q = 0; q < j; ++q) {
+    rest &= rest - 1;
+    stride *= 3;
+  }
+  const int bit = KeyOps<K>::lowest(rest);
+  const int p = bit >> 1;
+  const int radix = tb.cnt[p][(u32)((cwg >> bit) & 3u) - 1u];
+  const int t = (i / stride) % 3;
+  const int base = i - t * stride;
+  double v = 0.0;
+  if (t < radix)
+    v = __dadd_rn(__dadd_rn(__dmul_rn(a[base], tb.w[p][0][t]), __dmul_rn(a[base + stride], tb.w[p][1][t])),
+                  __dmul_rn(a[base + 2 * stride], tb.w[p][2][t]));
+  b[i] = v;
+}
+
+template <typename K>
+__global__ void __launch_bounds__(256)
+k_kron_pick(const u64* __restrict__ cw, const u64* __restrict__ gsrc, const int* __restrict__ flagged,
+            const int64_t* __restrict__ toff, const double* __restrict__ tensor, const int64_t* __restrict__ pre_off,
+            double* __restrict__ pre, const __grid_constant__ OperatorTable tb) {
+  const int g = flagged[blockIdx.y];
+  const K cwg = (K)cw[gsrc[g]];
+  int rest = blockIdx.x * 256 + threadIdx.x, slot = 0, mul = 1;
+  const int i = rest;
+  bool ok = true;
+  for (K m = KeyOps<K>::support(cwg); m; m &= m - 1) {
+    const int bit = KeyOps<K>::lowest(m);
+    const int radix = tb.cnt[bit >> 1][(u32)((cwg >> bit) & 3u) - 1u];
+    const int t = rest % 3;
+    rest /= 3;
+    ok = ok && t < radix;
+    slot += t * mul;
+    mul *= radix;
+  }
+  if (ok && rest == 0) pre[pre_off[g] + slot] = tensor[toff[blockIdx.y] + i];
+}
+
+template <typename K>
+int launch_kron_wide(qx_store* s, const u64* cw, const u64* skey, const double* slam, const u64* gsrc,
+                     const int* d_flag, const int64_t* d_toff, int n_big, int w_max, int64_t max_src, double* ta,
+                     double* tb2, int64_t tensor_total, const int64_t* pre_off, double* pre, const OperatorTable& ct) {
+  int size = 1;
+  for (int j = 0; j < w_max; ++j) size *= 3;
+  const dim3 grid((unsigned)((size + 255) / 256), (unsigned)n_big);
+  QX_CUDA(cudaMemsetAsync(ta, 0, sizeof(double) * (size_t)tensor_total, s->stream));
+  const dim3 sgrid((unsigned)std::max<int64_t>(1, std::min<int64_t>((max_src + 255) / 256, 1024)), (unsigned)n_big);
+  k_kron_scatter<K><<<sgrid, 256, 0, s->stream>>>(cw, skey, slam, gsrc, d_flag, d_toff, ta);
+  for (int m = 0; m < w_max; ++m) {
+    k_kron_mode<K><<<grid, 256, 0, s->stream>>>(cw, gsrc, d_flag, d_toff, ta, tb2, m, ct);
+    std::swap(ta, tb2);
+  }
+  k_kron_pick<K><<<grid, 256, 0, s->stream>>>(cw, gsrc, d_flag, d_toff, ta, pre_off, pre, ct);
+  qx_count_launches(w_max + 2);
+  QX_CUDA(cudaGetLastError());
+  return QX_OK;
+}
+
 template <typename K, typename KO, bool FUSED>
 int launch_group_emit(qx_store* s, int64_t tiles, const u64* cw, const u64* skey, const double* slam,
                       const u64* gsrc, const u64* gslot, const u64* totals, const int2* tile_info,
@@ -1368,52 +1476,84 @@ int qx_dense_operator_step(qx_store* s, const OperatorTable& nz, const uint32_t*
     const u64* h_cw = h_groups + 2;
     const u64* h_src = h_cw + (qxb::kNgCap + 1);
     const u64* h_slot = h_src + (qxb::kNgCap + 1);
-    std::vector<int64_t> off((size_t)ng, -1);
-    std::vector<int> flagged;
-    int64_t pre_total = 0;
+    std::vector<int64_t> off((size_t)ng, -1), toff;
+    std::vector<int> flagged, big;               // tensor in shared memory (<= 8 digits) / in global memory
+    int64_t pre_total = 0, tensor_total = 0, max_src = 0;
+    int w_max = 0;
+    constexpr int64_t kTensorCap = 1ll << 26;    // doubles per ping-pong buffer (512 MB)
     for (int g = 0; g < ng; ++g) {
       const double n_src = (double)(h_src[g + 1] - h_src[g]), slots = (double)(h_slot[g + 1] - h_slot[g]);
       const u64 sup = (h_cw[g] | (h_cw[g] >> 1)) & 0x5555555555555555ull;
       const int w = __builtin_popcountll(sup);
-      if (n_src < kBlockedMin || w < 1 || w > kKronDigits || slots < 1) continue;
-      double tensor = 1.0;
-      for (int j = 0; j < w; ++j) tensor *= 3.0;
+      if (n_src < kBlockedMin || w < 1 || w > kKronWideDigits || slots < 1) continue;
+      int64_t tensor = 1;
+      for (int j = 0; j < w; ++j) tensor *= 3;
       // worth it when the factored sum's (source block, slot) pairs outnumber the contraction's terms
-      if (n_src * slots / 16.0 < 2.0 * (3.0 * w * tensor + n_src)) continue;
+      static const double factor = getenv("QX_KRON_FACTOR") ? atof(getenv("QX_KRON_FACTOR")) : 0.25;
+      if (n_src * slots / 16.0 < factor * (3.0 * w * (double)tensor + n_src)) continue;
+      if (w > kKronDigits) {
+        if (tensor_total + tensor > kTensorCap) continue;
+        toff.push_back(tensor_total);
+        tensor_total += tensor;
+        big.push_back(g);
+        w_max = std::max(w_max, w);
+        max_src = std::max<int64_t>(max_src, (int64_t)n_src);
+      } else {
+        flagged.push_back(g);
+      }
       off[(size_t)g] = pre_total;
       pre_total += (int64_t)slots;
-      flagged.push_back(g);
     }
-    if (!flagged.empty()) {
-      const int64_t bytes3 = padded(8ll * ng) + padded(4ll * (int64_t)flagged.size()) + padded(8 * pre_total);
+    if (!flagged.empty() || !big.empty()) {
+      const int64_t n_small = (int64_t)flagged.size(), n_big = (int64_t)big.size();
+      const int64_t bytes3 = padded(8ll * ng) + padded(4 * (n_small + 1)) + padded(4 * (n_big + 1)) +
+                             padded(8 * (n_big + 1)) + padded(8 * pre_total) + 2 * padded(8 * tensor_total);
       QX_TRY(qx_dev_alloc(&block3, bytes3, s->stream, s->device));
       rel3.p = block3;
       char* c3 = reinterpret_cast<char*>(block3);
       int64_t* d_off = carve<int64_t>(c3, ng);
-      int* d_flag = carve<int>(c3, (int64_t)flagged.size());
+      int* d_flag = carve<int>(c3, n_small + 1);
+      int* d_big = carve<int>(c3, n_big + 1);
+      int64_t* d_toff = carve<int64_t>(c3, n_big + 1);
       double* pre = carve<double>(c3, pre_total);
+      double* ta = carve<double>(c3, tensor_total);
+      double* tb2 = carve<double>(c3, tensor_total);
       QX_CUDA(cudaMemcpyAsync(d_off, off.data(), 8 * (size_t)ng, cudaMemcpyHostToDevice, s->stream));
-      QX_CUDA(cudaMemcpyAsync(d_flag, flagged.data(), 4 * flagged.size(), cudaMemcpyHostToDevice, s->stream));
-      const size_t kron_smem = 2 * (size_t)kKronSize * sizeof(double);
       QxProfileScope prof(QX_K_DENSE_PREP, s->stream, 16.0 * (double)n + 8.0 * (double)pre_total);
-      if (small_keys) {
-        static bool attr32 = false;
-        if (!attr32) {
-          QX_CUDA(cudaFuncSetAttribute(k_group_kron<u32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kron_smem));
-          attr32 = true;
+      if (n_small > 0) {
+        QX_CUDA(cudaMemcpyAsync(d_flag, flagged.data(), 4 * (size_t)n_small, cudaMemcpyHostToDevice, s->stream));
+        const size_t kron_smem = 2 * (size_t)kKronSize * sizeof(double);
+        if (small_keys) {
+          static bool attr32 = false;
+          if (!attr32) {
+            QX_CUDA(cudaFuncSetAttribute(k_group_kron<u32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kron_smem));
+            attr32 = true;
+          }
+          k_group_kron<u32><<<(unsigned)n_small, 256, kron_smem, s->stream>>>(cwb[sorted], skey, slam, gsrc, d_flag,
+                                                                            d_off, pre, ct);
+        } else {
+          static bool attr64 = false;
+          if (!attr64) {
+            QX_CUDA(cudaFuncSetAttribute(k_group_kron<u64>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kron_smem));
+            attr64 = true;
+          }
+          k_group_kron<u64><<<(unsigned)n_small, 256, kron_smem, s->stream>>>(cwb[sorted], skey, slam, gsrc, d_flag,
+                                                                            d_off, pre, ct);
         }
-        k_group_kron<u32><<<(unsigned)flagged.size(), 256, kron_smem, s->stream>>>(cwb[sorted], skey, slam, gsrc, d_flag,
-                                                                                 d_off, pre, ct);
-      } else {
-        static bool attr64 = false;
-        if (!attr64) {
-          QX_CUDA(cudaFuncSetAttribute(k_group_kron<u64>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kron_smem));
-          attr64 = true;
-        }
-        k_group_kron<u64><<<(unsigned)flagged.size(), 256, kron_smem, s->stream>>>(cwb[sorted], skey, slam, gsrc, d_flag,
-                                                                                 d_off, pre, ct);
+        qx_count_launches(1);
+        QX_CUDA(cudaGetLastError());
       }
-      QX_CUDA(cudaGetLastError());
+      if (n_big > 0) {
+        QX_CUDA(cudaMemcpyAsync(d_big, big.data(), 4 * (size_t)n_big, cudaMemcpyHostToDevice, s->stream));
+        QX_CUDA(cudaMemcpyAsync(d_toff, toff.data(), 8 * (size_t)n_big, cudaMemcpyHostToDevice, s->stream));
+        if (small_keys)
+          QX_TRY(launch_kron_wide<u32>(s, cwb[sorted], skey, slam, gsrc, d_big, d_toff, (int)n_big, w_max, max_src, ta,
+                                       tb2, tensor_total, d_off, pre, ct));
+        else
+          QX_TRY(launch_kron_wide<u64>(s, cwb[sorted], skey, slam, gsrc, d_big, d_toff, (int)n_big, w_max, max_src, ta,
+                                       tb2, tensor_total, d_off, pre, ct));
+        flagged.insert(flagged.end(), big.begin(), big.end());
+      }
       d_pre_off = d_off;
       d_pre = pre;
       g_dense_last[1] = (int64_t)flagged.size();

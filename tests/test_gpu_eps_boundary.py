@@ -9,7 +9,8 @@ output term from a first run and run again with eps = |v|.  The reference keeps 
   so they must keep/drop EXACTLY the same terms for every such eps (checked on terms sitting on
   the boundary and on their nearest neighbours in value).
 * The factored sum of the grouped step (groups of >= 64 sources, dense.cu: sources that share
-  their high digits share the high product) associates the products differently: its
+  their high digits share the high product; or, where that is cheaper, the whole group contracted
+  one qubit at a time, k_group_kron / k_kron_mode) associates the products differently: its
   coefficients are within rounding of the reference's, not bitwise, and a term whose reference
   value IS eps can come out one ulp below and be dropped.  The test below documents exactly
   that: every difference between the two term sets is a term whose two values straddle eps and

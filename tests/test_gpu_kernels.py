@@ -262,10 +262,13 @@ def test_operator_run_equals_three_steps(n, terms, rot_qubits, n_ops, mix):
     (9, [0, 2, 3, 5, 6, 7, 8], 2000, True),                              # seven digits, the rest identity or idle
     (22, [1, 4, 5, 9, 13, 14, 20, 21], 5000, True),                      # 64-bit keys, digits spread over the word
     (22, [1, 4, 5, 9, 13, 14, 20, 21], 5000, False),
+    (10, list(range(10)), 1200, False),                                  # ten digits: the tensor in global memory
+    (24, [0, 1, 4, 5, 9, 13, 14, 20, 21, 22, 23], 1300, False),          # eleven digits, 64-bit keys
+    (12, list(range(12)), 1400, False),                                  # twelve digits next to smaller groups
 ])
 def test_groups_summed_mode_by_mode(n, qubits, count, bucket):
     """Groups with many sources on at most 8 digits have their sums formed one qubit at a time
-    ahead of the slot kernel (dense.cu k_group_kron): the same products as stabilizer.py:300-337,
+    ahead of the slot kernel (dense.cu k_group_kron; k_kron_mode above 8 digits): the same products as stabilizer.py:300-337,
     associated per qubit instead of per source, so keys are the reference's and coefficients agree
     to rounding (|sum| <= sum of |lambda| ~ 1e3 here, 1e-16 relative per operation)."""
     rng = np.random.default_rng(n * 77 + count)
