@@ -150,7 +150,7 @@ k_tile_desc(const BGroup<K>* __restrict__ groups, int ng, u64 n_tiles, const u64
 // every thread reads; the rest is for the threads that build the tile's tables.
 template <typename K>
 struct __align__(16) TileFat {
-  u32 Lw, n_mid, n_src, T;   // low branches, mid entries, sources, slots
+  u32 shape, group, n_src, T;   // Lw | n_mid << 8 | (tables reusable across the group's tiles) << 16; group; sources; slots
   K word;              // image of the high picks
   K cw;                // class word of the group
   K l_mask;            // its tile-local digits
@@ -185,8 +185,15 @@ __device__ __forceinline__ void make_tile_fat(const BGroup<K>* __restrict__ grou
   f.pad2 = 0;
   f.n_src = g.n_src;
   f.T = g.T;
-  f.Lw = g.Lw;
-  f.n_mid = g.n_mid;
+  {
+    K mid_mask = g.l_mask;                       // tile-local digits above the three lowest
+    mid_mask &= mid_mask - 1;
+    mid_mask &= mid_mask - 1;
+    mid_mask &= mid_mask - 1;
+    const u32 reusable = g.n_src <= 2 && Plane<K>::popc(mid_mask) <= 3 ? 1u : 0u;
+    f.shape = g.Lw | (g.n_mid << 8) | (reusable << 16);
+  }
+  f.group = d.group;
   f.phi_at = g.phi0 + (tile - g.tile0) * g.n_src;
   f.key01[0] = (K)skey[g.src0];
   f.phi01[0] = phi[f.phi_at];
@@ -252,8 +259,12 @@ k_unit_scan(const u64* __restrict__ sort_key, const double* __restrict__ sort_va
 }
 
 struct UnitHdr;
+// A bucket's record: UnitHdr followed by a copy of its first tile's TileFat (fat16 = the tile
+// records as 16-byte words, fat_words of them per tile), so that one round trip behind the bucket
+// id brings everything the first tile needs.
 __global__ void k_unit_sizes(const u32* __restrict__ unit_tile0, const u64* __restrict__ sort_key,
-                             const double* __restrict__ sort_val, uint4* __restrict__ hdr, u64* __restrict__ info) {
+                             const double* __restrict__ sort_val, uint4* __restrict__ hdr, u64* __restrict__ info,
+                             const uint4* __restrict__ fat16, int fat_words) {
   const u64 nu = info[0];
   u32 worst = 0;
   for (u64 u = (u64)blockIdx.x * blockDim.x + threadIdx.x; u < nu; u += (u64)gridDim.x * blockDim.x) {
@@ -263,7 +274,9 @@ __global__ void k_unit_sizes(const u32* __restrict__ unit_tile0, const u64* __re
     worst = max(worst, slots);
     const u32 first = unit_tile0[u];
     const u64 key = sort_key[first];
-    hdr[u] = make_uint4(first, unit_tile0[u + 1] - first, (u32)key, (u32)(key >> 32));   // UnitHdr
+    uint4* rec = hdr + u * (u64)(1 + fat_words);
+    rec[0] = make_uint4(first, unit_tile0[u + 1] - first, (u32)key, (u32)(key >> 32));   // UnitHdr
+    for (int i = 0; i < fat_words; ++i) rec[1 + i] = fat16[(u64)first * fat_words + i];
   }
   worst = __reduce_max_sync(QX_FULL_MASK, worst);
   if (lane_id() == 0 && worst) atomicMax(reinterpret_cast<unsigned long long*>(info + 1), (unsigned long long)worst);
@@ -295,9 +308,11 @@ template <typename K>
 struct BSmem {
   OperatorTable tb;                  // class-expanded (dense.cu build_class_table)
   ImageTable<K> im;
-  BLow<K> low[2][27];                // tables of the tile in flight, double-buffered by tile parity
+  BLow<K> low[2][27];                // low-digit tables, double-buffered: rebuilt when the group changes
+  BLow<K> gmid[2][27];               // mid digits of the group alone (image word, picks), same buffering
+  double gmid_w[2][2][27][4];        // [buffer][source][mid entry][mid digit]: weights, 1.0 where absent
   BMid<K> mid[2][kMaxMid];
-  double low_w[2][2][27][4];         // [parity][source of the round][low branch][low digit]
+  double low_w[2][2][27][4];         // [buffer][source of the round][low branch][low digit]
   double p_mid[2][2][kMaxMid];       // [parity][source of the round][mid entry]: lambda * high * mid weights
   __align__(16) u32 warp_tot[kBWarps + 4];
   u64 base;
@@ -316,7 +331,10 @@ __device__ __forceinline__ void bucket_publish(u64* status, u32 idx, u64 kept) {
 // all 32 lanes of one warp: exclusive prefix of bucket idx (its own count is published already)
 __device__ __noinline__ u64 bucket_resolve(u64* status, u32 idx, u64 kept) {
   if (idx == 0) return 0;
-  constexpr int R = 8;
+#ifndef QX_BUCKET_LB_R
+#define QX_BUCKET_LB_R 2
+#endif
+  constexpr int R = QX_BUCKET_LB_R;
   u64 excl = 0;
   int base = (int)idx - 1;
   bool done = false;
@@ -359,7 +377,7 @@ __device__ __noinline__ u64 bucket_resolve(u64* status, u32 idx, u64 kept) {
 template <typename K, typename KO>
 __global__ void __launch_bounds__(kBThreads, QX_BUCKET_MINB)
 k_bucket_emit(const TileFat<K>* __restrict__ fat, const double* __restrict__ phi,
-              const UnitHdr* __restrict__ units, u32 u_lo, u32 u_hi, const u64* __restrict__ skey,
+              const uint4* __restrict__ units, u32 u_lo, u32 u_hi, const u64* __restrict__ skey,
               KO* __restrict__ keys_out, double* __restrict__ lam_out, u64* __restrict__ status,
               u32* __restrict__ ticket, int ell, int top_bits, int cap, double eps,
               const __grid_constant__ OperatorTable tb, const __grid_constant__ ImageTable<K> im) {
@@ -388,6 +406,10 @@ k_bucket_emit(const TileFat<K>* __restrict__ fat, const double* __restrict__ phi
   // my column of a tile: low branch my_bl, first mid entry my_m0; row k adds bpr mid entries.
   // Depends on the tile's Lw only, which rarely changes from one tile to the next.
   u32 geo_Lw = 0, bpr = 0, A = 0, my_m0 = 0, my_bl = 0;
+  // tables of the low digits (and, where the group allows, of its mid digits) stay in shared memory
+  // from tile to tile of one group; lpar = the buffer in use
+  u32 cur_group = 0xffffffffu;
+  int lpar = 0;
 
   // the previous bucket: first output position, then out (coalesced, final order, store format)
   auto flush_pending = [&]() {
@@ -419,10 +441,13 @@ k_bucket_emit(const TileFat<K>* __restrict__ fat, const double* __restrict__ phi
     __syncthreads();                              // ranks of the previous bucket taken; tables copied; id visible
     const u32 unit = sm.unit;
     if (unit >= u_hi) break;
-    const UnitHdr hdr = units[unit];
-    const u32 t_begin = hdr.tile0, t_end = hdr.tile0 + hdr.n_tiles;
-    const u32 n_tiles_unit = hdr.n_tiles;
-    const u64 unit_top = hdr.top;
+    constexpr u32 kRecWords = 1u + (u32)(sizeof(TileFat<K>) / 16);
+    const uint4* rec = units + (size_t)unit * kRecWords;        // UnitHdr + its first tile (k_unit_sizes)
+    const uint4 hdr = rec[0];
+    const TileFat<K>* first_tile = reinterpret_cast<const TileFat<K>*>(rec + 1);
+    const u32 t_begin = hdr.x, t_end = hdr.x + hdr.y;
+    const u32 n_tiles_unit = hdr.y;
+    const u64 unit_top = (u64)hdr.z | ((u64)hdr.w << 32);
     const bool slow = n_tiles_unit > (u32)kTrip;  // more tiles than the registers hold: park them
     for (int i = tid; i < words; i += kBThreads) bitmap[i] = 0u;
     if (n_tiles_unit > 1) {                       // descriptors of the later tiles: on their way to L1
@@ -447,9 +472,15 @@ k_bucket_emit(const TileFat<K>* __restrict__ fat, const double* __restrict__ phi
 #pragma unroll
       for (int t = 0; t < kTrip; ++t) {
         if (t0 + t >= t_end) continue;            // uniform
-        const TileFat<K>* tfp = fat + (t0 + t);
+        const TileFat<K>* tfp = (t == 0 && t0 == t_begin) ? first_tile : fat + (t0 + t);
         const uint4 geo = *reinterpret_cast<const uint4*>(tfp);
-        const u32 Lw = geo.x, n_mid = geo.y, n_src = geo.z;
+        const u32 Lw = geo.x & 0xffu, n_mid = (geo.x >> 8) & 0xffu, n_src = geo.z;
+        const bool reusable = (geo.x >> 16) != 0u;
+        const bool fresh = !reusable || geo.y != cur_group;   // uniform: the tables have to be built
+        if (fresh) {
+          lpar ^= 1;
+          cur_group = reusable ? geo.y : 0xffffffffu;
+        }
         const u32 ns2 = min(n_src, 2u);
         if (Lw != geo_Lw) {                       // uniform
           geo_Lw = Lw;
@@ -460,7 +491,77 @@ k_bucket_emit(const TileFat<K>* __restrict__ fat, const double* __restrict__ phi
           my_bl = (u32)tid - my_m0 * Lw;
         }
         // ---- tables of the tile: mid entries by the first threads, low branches by warp 4
-        if ((u32)tid < n_mid) {
+        if ((u32)tid < n_mid && reusable) {
+          // the group's mid digits on their own (once per group), then per tile: image of the high
+          // picks x that word, high product x the three weights (qubit 0 first; 1.0 is exact)
+          if (fresh) {
+            const K cwg = tfp->cw;
+            const K key0 = tfp->key01[0], key1 = tfp->key01[1];
+            K mm = tfp->l_mask;
+            mm &= mm - 1;
+            mm &= mm - 1;
+            mm &= mm - 1;
+            u32 b = (u32)tid, picks = 0;
+            K w = 0;
+            u32 ex = 0;
+            int mbit[3];
+            u32 pick[3];
+#pragma unroll
+            for (int j = 0; j < 3; ++j) {
+              mbit[j] = -1;
+              pick[j] = 0;
+              if (mm) {
+                mbit[j] = KeyOps<K>::lowest(mm);
+                mm &= mm - 1;
+                u32 q;
+                divmod_small<u32>(b, sm.tb.cnt[mbit[j] >> 1][(u32)((cwg >> mbit[j]) & 3u) - 1u], q, pick[j]);
+                b = q;
+                picks |= pick[j] << (2 * j);
+              }
+            }
+#pragma unroll
+            for (int j = 2; j >= 0; --j) {
+              double w0 = 1.0, w1 = 1.0;
+              if (mbit[j] >= 0) {
+                const int p = mbit[j] >> 1;
+                const u32 ax = sm.tb.axis[p][(u32)((cwg >> mbit[j]) & 3u) - 1u][pick[j]];
+                compose<K>(w, ex, sm.im.img[p][ax - 1], sm.im.imx[p][ax - 1], sm.im.e[p][ax - 1]);
+                w0 = sm.tb.w[p][(u32)((key0 >> mbit[j]) & 3u) - 1u][pick[j]];
+                if (ns2 > 1) w1 = sm.tb.w[p][(u32)((key1 >> mbit[j]) & 3u) - 1u][pick[j]];
+              }
+              sm.gmid_w[lpar][0][tid][j] = w0;
+              sm.gmid_w[lpar][1][tid][j] = w1;
+            }
+            BLow<K> ge;
+            ge.word = w;
+            ge.imx = (w ^ (w >> 1)) & Plane<K>::lo;
+            ge.e = ex & 3u;
+            ge.picks = picks;
+            sm.gmid[lpar][tid] = ge;                // read back by this thread only
+          }
+          const BLow<K> ge = sm.gmid[lpar][tid];
+          K w = tfp->word;
+          u32 ex = tfp->e;
+          compose<K>(w, ex, ge.word, ge.imx, ge.e);
+          const double2 a01 = *reinterpret_cast<const double2*>(&sm.gmid_w[lpar][0][tid][0]);
+          double v0 = __dmul_rn(tfp->phi01[0], sm.gmid_w[lpar][0][tid][2]);
+          v0 = __dmul_rn(v0, a01.y);
+          v0 = __dmul_rn(v0, a01.x);
+          double v1 = 0.0;
+          if (ns2 > 1) {
+            const double2 b01 = *reinterpret_cast<const double2*>(&sm.gmid_w[lpar][1][tid][0]);
+            v1 = __dmul_rn(tfp->phi01[1], sm.gmid_w[lpar][1][tid][2]);
+            v1 = __dmul_rn(v1, b01.y);
+            v1 = __dmul_rn(v1, b01.x);
+          }
+          BMid<K> me;
+          me.word = w;
+          me.e = ex & 3u;
+          me.picks = ge.picks;
+          sm.mid[par][tid] = me;
+          sm.p_mid[par][0][tid] = v0;
+          sm.p_mid[par][1][tid] = v1;
+        } else if ((u32)tid < n_mid) {
           const K cwg = tfp->cw;
           K mid_mask = tfp->l_mask;
           mid_mask &= mid_mask - 1;               // without the three lowest digits
@@ -498,7 +599,7 @@ k_bucket_emit(const TileFat<K>* __restrict__ fat, const double* __restrict__ phi
           sm.mid[par][tid] = me;
           sm.p_mid[par][0][tid] = v0;
           sm.p_mid[par][1][tid] = v1;
-        } else if (tid >= 128 && (u32)(tid - 128) < Lw) {
+        } else if (fresh && tid >= 128 && (u32)(tid - 128) < Lw) {
           const int l = tid - 128;
           const K cwg = tfp->cw;
           const K key0 = tfp->key01[0], key1 = tfp->key01[1];
@@ -531,15 +632,15 @@ k_bucket_emit(const TileFat<K>* __restrict__ fat, const double* __restrict__ phi
               w0 = sm.tb.w[p][(u32)((key0 >> lbit[j]) & 3u) - 1u][pick[j]];
               if (ns2 > 1) w1 = sm.tb.w[p][(u32)((key1 >> lbit[j]) & 3u) - 1u][pick[j]];
             }
-            sm.low_w[par][0][l][j] = w0;
-            sm.low_w[par][1][l][j] = w1;
+            sm.low_w[lpar][0][l][j] = w0;
+            sm.low_w[lpar][1][l][j] = w1;
           }
           BLow<K> le;
           le.word = w;
           le.imx = (w ^ (w >> 1)) & Plane<K>::lo;
           le.e = ex & 3u;
           le.picks = picks;
-          sm.low[par][l] = le;
+          sm.low[lpar][l] = le;
         }
         __syncthreads();
         u32 live = 0;
@@ -554,8 +655,8 @@ k_bucket_emit(const TileFat<K>* __restrict__ fat, const double* __restrict__ phi
         if (live) {
           // ((p * w2) * w1) * w0 with explicit roundings: no fused multiply-add into the sum
           {
-            const double2 w01 = *reinterpret_cast<const double2*>(&sm.low_w[par][0][my_bl][0]);
-            const double w2 = sm.low_w[par][0][my_bl][2];
+            const double2 w01 = *reinterpret_cast<const double2*>(&sm.low_w[lpar][0][my_bl][0]);
+            const double w2 = sm.low_w[lpar][0][my_bl][2];
             const double* pm = &sm.p_mid[par][0][my_m0];
 #pragma unroll
             for (int k = 0; k < kBRows; ++k) {
@@ -567,8 +668,8 @@ k_bucket_emit(const TileFat<K>* __restrict__ fat, const double* __restrict__ phi
             }
           }
           if (ns2 > 1) {
-            const double2 w01 = *reinterpret_cast<const double2*>(&sm.low_w[par][1][my_bl][0]);
-            const double w2 = sm.low_w[par][1][my_bl][2];
+            const double2 w01 = *reinterpret_cast<const double2*>(&sm.low_w[lpar][1][my_bl][0]);
+            const double w2 = sm.low_w[lpar][1][my_bl][2];
             const double* pm = &sm.p_mid[par][1][my_m0];
 #pragma unroll
             for (int k = 0; k < kBRows; ++k) {
@@ -619,20 +720,20 @@ k_bucket_emit(const TileFat<K>* __restrict__ fat, const double* __restrict__ phi
             for (u32 w = (u32)tid; w < nc * Lw; w += kBThreads) {
               const u32 c = w >= Lw ? 1u : 0u, l = w - c * Lw;
               const K key = (K)skey[src0 + c0 + c];
-              const u32 picks = sm.low[par][l].picks;
+              const u32 picks = sm.low[lpar][l].picks;
 #pragma unroll
               for (int j = 0; j < 3; ++j) {
                 double wt = 1.0;
                 if (lbit[j] >= 0)
                   wt = sm.tb.w[lbit[j] >> 1][(u32)((key >> lbit[j]) & 3u) - 1u][(picks >> (2 * j)) & 3u];
-                sm.low_w[par][c][l][j] = wt;
+                sm.low_w[lpar][c][l][j] = wt;
               }
             }
             __syncthreads();
             if (live) {
               for (u32 c = 0; c < nc; ++c) {
-                const double2 w01 = *reinterpret_cast<const double2*>(&sm.low_w[par][c][my_bl][0]);
-                const double w2 = sm.low_w[par][c][my_bl][2];
+                const double2 w01 = *reinterpret_cast<const double2*>(&sm.low_w[lpar][c][my_bl][0]);
+                const double w2 = sm.low_w[lpar][c][my_bl][2];
                 const double* pm = &sm.p_mid[par][c][my_m0];
 #pragma unroll
                 for (int k = 0; k < kBRows; ++k) {
@@ -650,7 +751,7 @@ k_bucket_emit(const TileFat<K>* __restrict__ fat, const double* __restrict__ phi
         }
         // words, signs, drop rule; a kept slot marks the bitmap and stays in registers
         if (live) {
-          const BLow<K> le = sm.low[par][my_bl];
+          const BLow<K> le = sm.low[lpar][my_bl];
 #pragma unroll
           for (int k = 0; k < kBRows; ++k) {
             if (live & (1u << k)) {
@@ -680,7 +781,7 @@ k_bucket_emit(const TileFat<K>* __restrict__ fat, const double* __restrict__ phi
         for (int t = 0; t < kTrip; ++t) {
           if (t0 + t >= t_end) continue;          // uniform
           const uint4 geo = *reinterpret_cast<const uint4*>(fat + (t0 + t));
-          const u32 Lw = geo.x, n_mid = geo.y;
+          const u32 Lw = geo.x & 0xffu, n_mid = (geo.x >> 8) & 0xffu;
           const u32 magic = 65536u / Lw + 1u;
           const u32 pb = ((u32)kBThreads * magic) >> 16;
           const u32 pm0 = ((u32)tid * magic) >> 16;
@@ -928,7 +1029,8 @@ int bucket_step(qx_store* s, const OperatorTable& ct, const ImageTable<K>& im, i
                         bpadded(8 * (int64_t)n_phi) + 4 * bpadded(8 * (int64_t)n_tiles) + 2 * 256 +
                         bpadded(4 * ((int64_t)n_tiles + 1)) + bpadded(4 * (int64_t)n_seg) +
                         bpadded(8 * (scan_tiles + 1)) + 256 + bpadded(8 * ((int64_t)n_tiles + 1)) + 256 +
-                        bpadded((int64_t)sizeof(TileFat<K>) * (int64_t)n_tiles) + bpadded(16 * ((int64_t)n_tiles + 1));
+                        bpadded((int64_t)sizeof(TileFat<K>) * (int64_t)n_tiles) +
+                        bpadded((16 + (int64_t)sizeof(TileFat<K>)) * ((int64_t)n_tiles + 1));
   void* block = nullptr;
   QX_TRY(qx_dev_alloc(&block, bytes, s->stream, s->device));
   struct Release {
@@ -950,7 +1052,9 @@ int bucket_step(qx_store* s, const OperatorTable& ct, const ImageTable<K>& im, i
   u64* unit_status = bcarve<u64>(cur, (int64_t)n_tiles + 1);
   u32* ticket = bcarve<u32>(cur, 2);
   TileFat<K>* d_fat = bcarve<TileFat<K>>(cur, (int64_t)n_tiles);
-  UnitHdr* d_units = bcarve<UnitHdr>(cur, (int64_t)n_tiles + 1);
+  static_assert(sizeof(TileFat<K>) % 16 == 0, "tile records are copied as 16-byte words");
+  constexpr int kFatWords = (int)(sizeof(TileFat<K>) / 16);
+  uint4* d_units = bcarve<uint4>(cur, (1 + kFatWords) * ((int64_t)n_tiles + 1));
 
   // groups and the offsets of the one-segment tile sort: host -> device through pinned staging
   const int64_t stage_bytes = (int64_t)sizeof(BGroup<K>) * (ng + 1) + 16;
@@ -999,7 +1103,7 @@ int bucket_step(qx_store* s, const OperatorTable& ct, const ImageTable<K>& im, i
                                                                d_groups, d_desc, d_phi, skey, d_fat);
     QX_CUDA(cudaGetLastError());
     k_unit_sizes<<<(unsigned)std::max<int64_t>(1, std::min<int64_t>(((int64_t)n_tiles + 255) / 256, 1024)), 256, 0, s->stream>>>(
-        unit_tile0, skeys[sorted], svals[sorted], reinterpret_cast<uint4*>(d_units), info);
+        unit_tile0, skeys[sorted], svals[sorted], d_units, info, reinterpret_cast<const uint4*>(d_fat), kFatWords);
     QX_CUDA(cudaGetLastError());
   }
   QX_TRY(qx_readback(s->stream, s->h_pinned, reinterpret_cast<const int64_t*>(info), 2));
