@@ -52,6 +52,15 @@ constexpr int kBWarps = kBThreads / 32;
 constexpr int kBRows = 3;                    // slots per thread per tile: tile <= kBRows * A
 constexpr int kNgCap = 4096;                 // groups the host plans
 constexpr int kMaxMid = 128;                 // mid entries per tile
+#ifndef QX_BUCKET_ELL
+#define QX_BUCKET_ELL 14
+#endif
+#ifndef QX_FLUSH_UNROLL
+#define QX_FLUSH_UNROLL 1
+#endif
+constexpr int kFlushUnroll = QX_FLUSH_UNROLL;
+constexpr int kEll = QX_BUCKET_ELL;          // low key bits ranked inside a bucket (7 digits)
+static_assert(kEll >= 13 && kEll <= 16, "bitmap words per thread and 16-bit staged keys");
 constexpr int kSrcChunk = 4;                 // sources folded per round
 constexpr int kPerThread = 12;               // parked slots per thread
 constexpr int kCapMax = kBThreads * kPerThread;   // slots per bucket (3072)
@@ -383,11 +392,15 @@ k_bucket_emit(const TileFat<K>* __restrict__ fat, const double* __restrict__ phi
               const __grid_constant__ OperatorTable tb, const __grid_constant__ ImageTable<K> im) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   BSmem<K>& sm = *reinterpret_cast<BSmem<K>*>(smem_raw);
-  const int words = 1 << (ell - 5);
-  double* st_lam = reinterpret_cast<double*>(smem_raw + ((sizeof(BSmem<K>) + 15) & ~(size_t)15));
-  u32* bitmap = reinterpret_cast<u32*>(st_lam + cap);
+  // the low key bits ranked inside a bucket are fixed at compile time (kEll): bitmap, prefix and
+  // the coefficients of the staging area sit at constant offsets, the scan has one shape
+  (void)ell;
+  constexpr int ell_c = kEll;
+  constexpr int words = 1 << (kEll - 5);
+  u32* bitmap = reinterpret_cast<u32*>(smem_raw + ((sizeof(BSmem<K>) + 15) & ~(size_t)15));
   unsigned short* prefix = reinterpret_cast<unsigned short*>(bitmap + words);
-  unsigned short* st_key = prefix + words;
+  double* st_lam = reinterpret_cast<double*>(prefix + words);
+  unsigned short* st_key = reinterpret_cast<unsigned short*>(st_lam + cap);
   const int tid = threadIdx.x, warp = tid >> 5, lane = lane_id();
   {
     const u32* src = reinterpret_cast<const u32*>(&tb);
@@ -397,7 +410,7 @@ k_bucket_emit(const TileFat<K>* __restrict__ fat, const double* __restrict__ phi
     u32* idst = reinterpret_cast<u32*>(&sm.im);
     for (int i = tid; i < (int)(sizeof(ImageTable<K>) / 4); i += kBThreads) idst[i] = isrc[i];
   }
-  const K low_bits = (K)(((u64)1 << ell) - 1);
+  constexpr K low_bits = (K)(((u64)1 << ell_c) - 1);
   const u64 top_mask = ((u64)1 << top_bits) - 1;
   int par = 0;
   bool pending = false;                          // a ranked bucket sits in st_key / st_lam
@@ -423,7 +436,7 @@ k_bucket_emit(const TileFat<K>* __restrict__ fat, const double* __restrict__ phi
     __syncthreads();
     KO* kp = keys_out + (int64_t)sm.base + tid;
     double* lp = lam_out + (int64_t)sm.base + tid;
-#pragma unroll 1
+#pragma unroll kFlushUnroll
     for (u32 r = (u32)tid; r < pend_kept; r += kBThreads, kp += kBThreads, lp += kBThreads) {
       st_stream(kp, (KO)(pend_top | (u64)st_key[r]));
       st_stream(lp, st_lam[r]);
@@ -805,7 +818,7 @@ k_bucket_emit(const TileFat<K>* __restrict__ fat, const double* __restrict__ phi
     u32 kept_total;
     {
       u32 cnt, c0 = 0;
-      const int per = words / kBThreads;          // words is a power of two
+      constexpr int per = words / kBThreads;      // words is a power of two
       const int w0 = tid * per;
       if (per == 2) {
         const uint2 b = *reinterpret_cast<const uint2*>(bitmap + w0);
@@ -900,7 +913,7 @@ k_bucket_emit(const TileFat<K>* __restrict__ fat, const double* __restrict__ phi
     pending = true;
     pend_idx = unit - u_lo;
     pend_kept = kept_total;
-    pend_top = (unit_top & top_mask) << ell;
+    pend_top = (unit_top & top_mask) << ell_c;
   }
   if (pending) {
     __syncthreads();
@@ -1009,9 +1022,8 @@ int bucket_step(qx_store* s, const OperatorTable& ct, const ImageTable<K>& im, i
                 const u64* skey, const double* slam, int64_t n_sources, int out, bool narrow_out, double eps,
                 int part, int parts, bool* handled) {
   *handled = false;
-  static const int env_ell = getenv("QX_BUCKET_ELL") ? atoi(getenv("QX_BUCKET_ELL")) : 14;
   const int n_seg = s->n_seg;
-  const int ell = std::min(std::max(env_ell, 5), 16);
+  const int ell = kEll;
   const int top_bits = 2 * s->n_qubits - ell;
   if (top_bits <= 0 || ng <= 0 || ng > kNgCap || total <= 0) return QX_OK;
   int seg_bits = 1;
