@@ -418,7 +418,7 @@ k_bucket_emit(const TileFat<K>* __restrict__ fat, const double* __restrict__ phi
   u64 pend_top = 0;
   // my column of a tile: low branch my_bl, first mid entry my_m0; row k adds bpr mid entries.
   // Depends on the tile's Lw only, which rarely changes from one tile to the next.
-  u32 geo_Lw = 0, bpr = 0, A = 0, my_m0 = 0, my_bl = 0;
+  u32 geo_Lw = 0, bpr = 0, A = 0, my_m0 = 0, my_bl = 0, geo_live = 0;   // geo_Lw: Lw | n_mid << 8
   // tables of the low digits (and, where the group allows, of its mid digits) stay in shared memory
   // from tile to tile of one group; lpar = the buffer in use
   u32 cur_group = 0xffffffffu;
@@ -495,13 +495,19 @@ k_bucket_emit(const TileFat<K>* __restrict__ fat, const double* __restrict__ phi
           cur_group = reusable ? geo.y : 0xffffffffu;
         }
         const u32 ns2 = min(n_src, 2u);
-        if (Lw != geo_Lw) {                       // uniform
-          geo_Lw = Lw;
+        if ((geo.x & 0xffffu) != geo_Lw) {        // uniform
+          geo_Lw = geo.x & 0xffffu;
           const u32 magic = 65536u / Lw + 1u;     // t / Lw == (t * magic) >> 16 for t < 2^16 / Lw
           bpr = ((u32)kBThreads * magic) >> 16;   // mid entries per row
           A = bpr * Lw;                           // slots per row
           my_m0 = ((u32)tid * magic) >> 16;
           my_bl = (u32)tid - my_m0 * Lw;
+          geo_live = 0;
+          if ((u32)tid < A) {
+#pragma unroll
+            for (int k = 0; k < kBRows; ++k)
+              if (my_m0 + (u32)k * bpr < n_mid) geo_live |= 1u << k;
+          }
         }
         // ---- tables of the tile: mid entries by the first threads, low branches by warp 4
         if ((u32)tid < n_mid && reusable) {
@@ -656,12 +662,7 @@ k_bucket_emit(const TileFat<K>* __restrict__ fat, const double* __restrict__ phi
           sm.low[lpar][l] = le;
         }
         __syncthreads();
-        u32 live = 0;
-        if ((u32)tid < A) {
-#pragma unroll
-          for (int k = 0; k < kBRows; ++k)
-            if (my_m0 + (u32)k * bpr < n_mid) live |= 1u << k;
-        }
+        const u32 live = geo_live;
         double acc[kBRows];
 #pragma unroll
         for (int k = 0; k < kBRows; ++k) acc[k] = 0.0;
