@@ -318,7 +318,8 @@ int qx_merge(qx_store* s, double eps, int64_t* ranks);
  * unique inside each segment (with duplicates, use qx_merge). */
 int qx_sort(qx_store* s);
 
-/* ---- north-star kernel (4): per segment, sum of lambda over Z/I-only words. */
+/* ---- north-star kernel (4): per segment, sum of lambda over Z/I-only words (any key width:
+ * one-word stores and the multi-word stores above 32 qubits). */
 int qx_store_zi_sums(qx_store* s, double* sums);
 /* Per segment sum of lambda^2 (the P^2 = I self-check). */
 int qx_store_norms(qx_store* s, double* sum_sq);

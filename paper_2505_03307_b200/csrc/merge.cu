@@ -64,10 +64,12 @@ namespace {
 constexpr int kRedThreads = 256;
 constexpr int kChunks = 64;          // fixed split of every segment: the sum order never changes
 
+// hi / n_words / cap: the upper key words of a multi-word store (n > 32), plane-major (csrc/wide.cu)
 template <int MODE>                  // 0: sum over Z/I-only words, 1: sum of squares
 __global__ void __launch_bounds__(kRedThreads)
-k_segment_partial(const u64* __restrict__ keys, const double* __restrict__ lam,
-                  const int64_t* __restrict__ seg, double* __restrict__ partial) {
+k_segment_partial(const u64* __restrict__ keys, const u64* __restrict__ hi, int n_words, int64_t cap,
+                  const double* __restrict__ lam, const int64_t* __restrict__ seg,
+                  double* __restrict__ partial) {
   __shared__ double s_warp[kRedThreads / 32];
   const int g = blockIdx.y, c = blockIdx.x;
   const int64_t lo = seg[g], n = seg[g + 1] - lo;
@@ -77,7 +79,9 @@ k_segment_partial(const u64* __restrict__ keys, const double* __restrict__ lam,
   for (int64_t i = a + threadIdx.x; i < b; i += kRedThreads) {
     const double v = lam[i];
     if (MODE == 0) {
-      if (zi_only(keys[i])) acc += v;
+      bool zi = zi_only(keys[i]);
+      for (int w = 1; w < n_words; ++w) zi = zi && zi_only(hi[(size_t)(w - 1) * (size_t)cap + i]);
+      if (zi) acc += v;
     } else {
       acc += v * v;
     }
@@ -112,8 +116,9 @@ int segment_reduce(qx_store* s, double* host_out) {
   {
     QxProfileScope prof(QX_K_READOUT_REDUCE, s->stream, 16.0 * (double)s->ub_total, 2);
     dim3 grid(kChunks, s->n_seg);
-    k_segment_partial<MODE><<<grid, kRedThreads, 0, s->stream>>>(s->keys[s->cur], s->lam[s->cur],
-                                                                 s->seg[s->cur], partial);
+    k_segment_partial<MODE><<<grid, kRedThreads, 0, s->stream>>>(
+        s->keys[s->cur], s->n_words > 1 ? s->hi[s->cur] : nullptr, s->n_words, (int64_t)s->cap,
+        s->lam[s->cur], s->seg[s->cur], partial);
     QX_CUDA(cudaGetLastError());
     k_segment_final<<<(s->n_seg + 127) / 128, 128, 0, s->stream>>>(partial, out, s->n_seg);
     QX_CUDA(cudaGetLastError());
@@ -144,7 +149,6 @@ extern "C" int qx_sort(qx_store* s) {
 
 extern "C" int qx_store_zi_sums(qx_store* s, double* sums) {
   QX_REQUIRE(s != nullptr, "store is NULL");
-  QX_NARROW_ONLY(s, "qx_store_zi_sums");
-  return segment_reduce<0>(s, sums);
+  return segment_reduce<0>(s, sums);     // any key width: the upper words are tested plane by plane
 }
 extern "C" int qx_store_norms(qx_store* s, double* sum_sq) { return segment_reduce<1>(s, sum_sq); }

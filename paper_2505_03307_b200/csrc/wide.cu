@@ -18,7 +18,9 @@
 //                           a permutation sorted word by word with the one-word onesweep passes
 //                           (stable LSD over the W words), then one reduce + compaction pass.
 // Branching operators of v2/v3 are applied gate by gate with these kernels (engine.py); the
-// grouped operator step, read-out and partitioning stay one-word (QX_ERR_UNSUPPORTED).
+// grouped operator step (run on the generators' support: qx_store_compact / qx_store_expand), the
+// density-expansion read-out and partitioning stay one-word (QX_ERR_UNSUPPORTED); the Heisenberg
+// read-out (qx_store_zi_sums, merge.cu) takes any width.
 #include <stdlib.h>
 #include <string.h>
 

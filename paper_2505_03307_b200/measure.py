@@ -126,7 +126,7 @@ def expectation(gs: GeneratorSet, word: int, expansion: PauliExpansion = None) -
 
 
 # ------------------------------------------------------------------------------
-# Heisenberg read-out: polynomial in rank, works at any n <= 32
+# Heisenberg read-out: polynomial in rank, any n the store holds (multi-word keys above 32 qubits)
 # ------------------------------------------------------------------------------
 def inverse_circuit(instructions) -> list:
     """Gates reversed and inverted: S^-1 = S^3, SX^-1 = SX^3, R(t)^-1 = R(-t); H, X, CX self-inverse."""
@@ -157,7 +157,10 @@ def expectation_heisenberg(instructions, n: int, words, mode="v1", eps: float = 
             raise ValueError(f"word index {w} out of range [0, 4**{n})")
     if not words:
         return np.zeros(0)
-    initial = [(np.ones(1), np.array([w], dtype=np.uint64)) for w in words]
+    if n > 32:      # multi-word keys: Python ints, as the reference's big-int indices (stabilizer.py:40-59)
+        initial = [(np.ones(1), np.array([w], dtype=object)) for w in words]
+    else:
+        initial = [(np.ones(1), np.array([w], dtype=np.uint64)) for w in words]
     report = run(inverse_circuit(instructions), n, mode, eps, device=device, initial=initial,
                  download=False)
     store = report.device["store"]

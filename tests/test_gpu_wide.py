@@ -174,8 +174,40 @@ def test_limits_above_32_qubits():
     assert ghz.max_rank == 1 and int(ghz.final.generators[0].indices[0]) == (4 ** 400 - 1) // 3
     with DeviceStore(n, 1, 0) as st:
         st.init_z([0])
+        assert st.zi_sums().tolist() == [1.0]                     # Z_0: no X/Y digit in any key word
         with pytest.raises(qx.NativeError, match="one-word keys"):
-            st.zi_sums()
+            st.partition_by_owner(2)
+
+
+@pytest.mark.parametrize("n,mode", [(40, "v1"), (70, "v1"), (70, "v3")])
+def test_heisenberg_read_out_above_32_qubits(n, mode):
+    """<0|U^dag W U|0> with multi-word keys (north star kernel 4 at any width): a near-Clifford
+    circuit on the first m of n qubits and observables supported there must give the one-word
+    read-out's values; words reaching into the idle qubits are 1 on Z/I digits there and 0 on X/Y."""
+    m = 8
+    gates = qx.gen_random(m, 80, 11)
+    rng = np.random.default_rng(5)
+    small = [int(v) for v in rng.integers(0, 4 ** m, size=24)] + [0, 4 ** m - 1]
+    want = qx.expectation_heisenberg(gates, m, small, mode)
+    shift = 4 ** (n - m)
+    got = qx.expectation_heisenberg(gates, n, [w * shift for w in small], mode)
+    assert np.max(np.abs(got - want)) < 1e-12
+    assert np.max(np.abs(want)) > 1e-3                            # the comparison is not 0 == 0
+    z_tail = sum(3 * 4 ** (n - 1 - j) for j in (m, n // 2, n - 1))          # Z on three idle qubits
+    x_tail = 1 * 4 ** (n - 1 - (n - 2))                                     # X on one idle qubit
+    got = qx.expectation_heisenberg(gates, n, [w * shift + z_tail for w in small] + [small[0] * shift + x_tail], mode)
+    assert np.max(np.abs(got[:-1] - want)) < 1e-12 and got[-1] == 0.0
+
+
+def test_heisenberg_read_out_of_a_wide_clifford_state():
+    """GHZ on 100 qubits: stabilizers Z_i Z_j and X...X have expectation exactly 1, single Z exactly 0."""
+    n = 100
+    gates = qx.gen_ghz(n)
+    digit = lambda a, j: a * 4 ** (n - 1 - j)
+    words = [digit(3, 0) + digit(3, 99), digit(3, 17) + digit(3, 64), (4 ** n - 1) // 3, digit(3, 5),
+             digit(1, 0), 0]
+    got = qx.expectation_heisenberg(gates, n, words, "v1")
+    assert got.tolist() == [1.0, 1.0, 1.0, 0.0, 0.0, 1.0]
 
 
 
