@@ -55,6 +55,14 @@ while time.time() < t_end:
     for wv, h in zip(words, hz):
         if abs(h - oracle.expectation(want_final, n, wv, wex)) > 1e-10 or abs(qx.expectation(final, wv, ex) - h) > 1e-10:
             note("expectation", (case - 1, n, wv))
+    # the same observables above 32 qubits (multi-word keys): the circuit on the first n of nw qubits,
+    # Z or I on the idle ones (expectation 1 there)
+    if case % 4 == 0:
+        nw = n + int(rng.integers(33, 90))
+        tail = sum(3 * 4 ** (nw - 1 - j) for j in range(n, nw) if rng.random() < 0.2)
+        hw = qx.expectation_heisenberg(gates, nw, [wv * 4 ** (nw - n) + tail for wv in words], mode="v1")
+        if np.max(np.abs(hw - hz)) > 1e-10:
+            note("wide heisenberg", (case - 1, n, nw))
     # ---- kernel-level: random generator with duplicates through apply_1q / apply_cx / canonicalize
     terms = int(rng.integers(1, 40))
     idx = rng.integers(0, 4 ** n, size=terms)
