@@ -341,7 +341,7 @@ __device__ __forceinline__ void bucket_publish(u64* status, u32 idx, u64 kept) {
 __device__ __noinline__ u64 bucket_resolve(u64* status, u32 idx, u64 kept) {
   if (idx == 0) return 0;
 #ifndef QX_BUCKET_LB_R
-#define QX_BUCKET_LB_R 2
+#define QX_BUCKET_LB_R 1         // status words per lane and round trip (windows of 32: 1.082 ms; 64: 1.091; 96: 1.105)
 #endif
   constexpr int R = QX_BUCKET_LB_R;
   u64 excl = 0;
