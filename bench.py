@@ -77,9 +77,47 @@ class ClockSampler:
               "clocks_event_reasons.sw_power_cap")
 
     def __init__(self, device):
-        self.device, self.rows, self.proc = device, [], None
+        self.device, self.rows, self.proc, self.nvml_thread = device, [], None, None
+
+    def _nvml_start(self):
+        """NVML in a thread, one reading every 4 ms: the device-timed region is ~30 ms long, which
+        nvidia-smi's own loop (>= 100 ms per reading) samples once at best."""
+        import pynvml as nv
+        nv.nvmlInit()
+        ids = os.environ.get("CUDA_VISIBLE_DEVICES", "")
+        index = self.device
+        if ids and all(tok.strip().isdigit() for tok in ids.split(",")) and self.device < len(ids.split(",")):
+            index = int(ids.split(",")[self.device])
+        h = nv.nvmlDeviceGetHandleByIndex(index)
+        mx = float(nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM))
+        bits = ((nv.nvmlClocksEventReasonHwSlowdown, 3), (nv.nvmlClocksEventReasonHwThermalSlowdown, 4),
+                (nv.nvmlClocksEventReasonSwThermalSlowdown, 5), (nv.nvmlClocksEventReasonSwPowerCap, 6))
+        nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)            # fail here, not in the thread
+        nv.nvmlDeviceGetCurrentClocksEventReasons(h)
+        self.stop = threading.Event()
+
+        def poll():
+            while not self.stop.is_set():
+                try:
+                    row = [str(nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)), str(mx), "", "", "", "", ""]
+                    mask = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
+                    for bit, col in bits:
+                        row[col] = "Active" if mask & bit else "Not Active"
+                    self.rows.append(row)
+                except Exception:
+                    return
+                self.stop.wait(0.004)
+
+        self.nvml_thread = threading.Thread(target=poll, daemon=True)
+        self.nvml_thread.start()
 
     def __enter__(self):
+        self.nvml_thread = None
+        try:
+            self._nvml_start()
+            return self
+        except Exception:
+            self.nvml_thread = None
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}",
@@ -96,6 +134,9 @@ class ClockSampler:
             self.rows.append([c.strip() for c in line.split(",")])
 
     def __exit__(self, *exc):
+        if self.nvml_thread is not None:
+            self.stop.set()
+            self.nvml_thread.join(timeout=2)
         if self.proc:
             time.sleep(0.15)
             self.proc.terminate()
@@ -114,7 +155,8 @@ class ClockSampler:
                 if flag.lower().startswith("active"):
                     reasons.add(name)
         return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx or None,
-                "reasons": sorted(reasons), "samples": len(sm)}
+                "reasons": sorted(reasons), "samples": len(sm),
+                "source": "nvml, 4 ms period" if self.nvml_thread is not None else "nvidia-smi -lms 100"}
 
 
 def job_config(name, mode, n, n_gates, total_updates, final_terms, world, strong):
