@@ -291,16 +291,29 @@ __global__ void k_unit_sizes(const u32* __restrict__ unit_tile0, const u64* __re
   if (lane_id() == 0 && worst) atomicMax(reinterpret_cast<unsigned long long*>(info + 1), (unsigned long long)worst);
 }
 
-// generator offsets of the compact output from the inclusive prefixes the buckets left behind
+// generator offsets of the compact output from the inclusive prefixes the buckets left behind.
+// One warp: a generator without slots takes the first bucket of the next one that has some (a fill
+// from the right, 32 generators per round), then one status word per generator, all loads in
+// flight at once (one thread walking the 2 x n_seg dependent loads took 9 us of the step).
 __global__ void k_bucket_offsets(const u64* __restrict__ status, u32* __restrict__ seg_first, int n_seg,
                                  u32 u_lo, u32 u_hi, u32 n_units, int64_t* __restrict__ seg_out) {
-  if (blockIdx.x != 0 || threadIdx.x != 0) return;
-  u32 next = n_units;
-  for (int g = n_seg - 1; g >= 0; --g) {
-    if (seg_first[g] == 0xffffffffu) seg_first[g] = next;
-    else next = seg_first[g];
+  if (blockIdx.x != 0 || threadIdx.x >= 32) return;
+  const int lane = (int)threadIdx.x;
+  u32 carry = n_units;
+  for (int hi = n_seg; hi > 0; hi -= 32) {          // lane l <-> generator hi - 1 - l
+    const int g = hi - 1 - lane;
+    u32 v = g >= 0 ? seg_first[g] : 0u;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const u32 o = __shfl_up_sync(QX_FULL_MASK, v, d);
+      if (v == 0xffffffffu && lane >= d) v = o;
+    }
+    if (v == 0xffffffffu) v = carry;
+    if (g >= 0) seg_first[g] = v;
+    carry = __shfl_sync(QX_FULL_MASK, v, min(31, hi - 1));
   }
-  for (int g = 0; g <= n_seg; ++g) {
+  __syncwarp();
+  for (int g = lane; g <= n_seg; g += 32) {
     u32 u = g < n_seg ? seg_first[g] : n_units;
     u = min(max(u, u_lo), u_hi);
     seg_out[g] = u == u_lo ? 0 : (int64_t)(status[u - 1 - u_lo] & QX_LB_VAL);
