@@ -434,9 +434,12 @@ def run_ours(args):
     barrier()
     t0 = time.perf_counter()
     last = None
+    e2e_each = []
     for _ in range(args.steps):
         last = None                      # drop the previous result first: its pinned block is reused
+        t1 = time.perf_counter()
         last = step_e2e()
+        e2e_each.append(time.perf_counter() - t1)
     barrier()
     e2e_s = (time.perf_counter() - t0) / args.steps
     t = torch.tensor([e2e_s], device=red_dev, dtype=torch.float64)
@@ -518,6 +521,7 @@ def run_ours(args):
         "config": job_config(args.workload, args.mode, n, len(gates), total_updates, int(sum(final_ranks)), world,
                              strong),
         "e2e": {"value": total_updates / e2e_s, "unit": "updates/s", "ms_per_step": e2e_s * 1e3,
+                "ms_per_step_min": min(e2e_each) * 1e3, "ms_per_step_median": statistics.median(e2e_each) * 1e3,
                 "h2d_bytes_per_step": table_bytes(n, gates), "d2h_bytes_per_step": d2h},
         "gpu_launches": launches,
         "ranks": {"world": world, "backend": backend if world > 1 else None},
