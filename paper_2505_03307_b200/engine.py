@@ -365,7 +365,8 @@ def run(instructions: Sequence[Instruction], n: int, mode, eps: float = DEFAULT_
         if initial is not None:
             store.upload(initial)
             walker_ranks = [len(l) for l, _ in initial]
-            min_abs = min((float(np.min(np.abs(l))) for l, _ in initial if len(l)), default=1.0)
+            lams = [np.asarray(l, dtype=np.float64).ravel() for l, _ in initial if len(l)]
+            min_abs = float(np.min(np.abs(np.concatenate(lams)))) if lams else 1.0   # one pass, not one per segment
         else:
             walker_ranks = [1] * len(ids)
             min_abs = 1.0
@@ -378,7 +379,7 @@ def run(instructions: Sequence[Instruction], n: int, mode, eps: float = DEFAULT_
         eager = eps > min_abs
         if initial is not None:
             # caller-supplied generators may hold duplicate or sub-eps terms: canonicalize first
-            eager = eager or any(len(np.unique(k)) != len(k) for _, k in initial)
+            eager = eager or any(len(k) > 1 and len(np.unique(k)) != len(k) for _, k in initial)
         w.eager = eager
         trace = [list(w.ranks)]
 
